@@ -1,0 +1,478 @@
+"""Benchmark of the hot path: forward + backward IIR filtering (BASELINE.json metric
+"fwd+bwd filtered samples/sec (B x T / s) and HBM GB/s vs peak").
+
+    python bench.py [--gpus N --steps K --warmup W] [--workload c2|c1|c4|c5|c3] [--impl ours|reference]
+
+One step = iir_forward + iir_backward (all of SURVEY §8(a)'s rows a1-a8) over one
+batch of synthetic input already resident in HBM, plus (N > 1) the NCCL
+all-reduce of the shared-coefficient gradients.  Weak scaling: every rank
+filters the workload's per-GPU batch.  Inputs rotate over several buffer sets
+whose total size exceeds 2x L2, so no step reads data left in L2 by the
+previous one.  The timed region is K steps captured in one CUDA graph (eager
+with --no-graph), bracketed by barrier + synchronize, timed with CUDA events on
+the launching stream, max over ranks.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2511_14390_b200 import inputs  # noqa: E402
+
+METRIC = "fwd+bwd filtered samples/sec (B x T / s)"
+WORKLOADS = {
+    "c1": dict(desc="config 1: order-2 TDF biquad, batch 1 x 4096, fixed coefficients, fp64", **inputs.CONFIGS["c1"]),
+    "c2": dict(desc="config 2: order-2 TDF fixed coefficients, batch 64 x 2^16, fp32 (audio EQ training shape)",
+               **inputs.CONFIGS["c2"]),
+    "c4": dict(desc="config 4: order-4 TDF, batch 1 x 2^24, fp32 (time-parallel scan stress)", **inputs.CONFIGS["c4"]),
+    "c5": dict(desc="config 5 per-GPU shard: order-8 TDF shared coefficients, batch 256 x 2^16 per GPU, fp32, "
+                    "coefficient-gradient all-reduce", **dict(inputs.CONFIGS["c5"], batch=256)),
+    "c3": dict(desc="config 3: all-pole LPC order 24, per-sample coefficients, batch 32 x 2^18, fp32",
+               **inputs.CONFIGS["c3"]),
+}
+
+
+def algorithmic_bytes(w):
+    """Bytes per sample the method must move, per kernel."""
+    s = 8 if w["dtype"] == "f64" else 4
+    if w["coef"] == "per_sample":
+        M = w["order"]
+        return {"tv_fwd": (2 + M) * s, "tv_bwd": (4 + 2 * M) * s}
+    if w["form"] == "tdf":
+        return {"lti_fwd": 2 * s, "lti_bwd": 4 * s}
+    return {"lti_fwd": 3 * s, "lti_bwd": 3 * s}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML every ~2 ms in a thread."""
+
+    def __init__(self, dev_index):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    _NAMES = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+              0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self._NAMES.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ ours ---
+class Problem:
+    """Device-resident buffers of one workload for the C-ABI calls."""
+
+    def __init__(self, w, dev, seed, nsets):
+        from paper_2511_14390_b200 import _binding as B
+        self.B = B
+        self.w = w
+        td = inputs.torch_dtype(w["dtype"])
+        Bsz, T, M = w["batch"], w["length"], w["order"]
+        rng = np.random.default_rng(seed)
+        self.td = td
+        g = torch.Generator(device=dev).manual_seed(seed)
+        self.sets = []
+        if w["coef"] == "per_sample":
+            p = inputs.tv_allpole_problem(seed, batch=Bsz, length=T, order=M, dtype=w["dtype"], device=dev)
+            self.a = p["a"].to(td).contiguous()
+            self.b = None
+            self.zi = p["zi"].to(td).contiguous()
+            mode = B.IIR_COEF_PER_SAMPLE
+        else:
+            b, a = inputs.stable_coefs(rng, M, w["dtype"], angles=w["angles"])
+            self.b = torch.tensor(b, dtype=td, device=dev)
+            self.a = torch.tensor(a, dtype=td, device=dev)
+            self.zi = (0.1 * torch.randn(Bsz, M, generator=g, device=dev, dtype=torch.float64)).to(td)
+            mode = B.IIR_COEF_SHARED
+        self.gzf = torch.randn(Bsz, M, generator=g, device=dev, dtype=torch.float64).to(td)
+        for _ in range(nsets):
+            x = torch.randn(Bsz, T, generator=g, device=dev, dtype=td)
+            gy = torch.randn(Bsz, T, generator=g, device=dev, dtype=td)
+            self.sets.append(dict(x=x, gy=gy, y=torch.empty_like(x), gx=torch.empty_like(x)))
+        self.zf = torch.empty(Bsz, M, dtype=td, device=dev)
+        self.gzi = torch.empty(Bsz, M, dtype=td, device=dev)
+        self.gb = None if self.b is None else torch.empty_like(self.b)
+        self.ga = torch.empty_like(self.a)
+        self.desc = B.make_desc(Bsz, T, M, w["form"], td, mode)
+        self.tb = B.iir_tape_bytes(self.desc)
+        self.wb = B.iir_workspace_bytes(self.desc)
+        self.tape = torch.empty(self.tb, dtype=torch.uint8, device=dev)
+        self.ws = torch.empty(self.wb, dtype=torch.uint8, device=dev)
+        self.grad_buf = None if self.b is None else torch.empty(2 * (M + 1), dtype=td, device=dev)
+
+    def set_bytes(self):
+        s = self.sets[0]
+        return sum(t.numel() * t.element_size() for t in s.values())
+
+    def step(self, i, stream, pg=None):
+        B = self.B
+        s = self.sets[i % len(self.sets)]
+        B.iir_forward(self.desc, self.b, self.a, s["x"], self.zi, s["y"], self.zf, self.tape, self.tb,
+                      self.ws, self.wb, stream)
+        B.iir_backward(self.desc, s["gy"], self.gzf, self.b, self.a, s["x"], s["y"], self.zi, self.tape, self.tb,
+                       s["gx"], self.gb, self.ga, self.gzi, self.ws, self.wb, stream)
+        if pg is not None and self.b is not None:
+            # the one real exchange of the path: all-reduce of the shared-coefficient gradients (§8(e))
+            torch.cat([self.gb, self.ga], out=self.grad_buf)
+            torch.distributed.all_reduce(self.grad_buf, group=pg)
+
+
+def run_ours(args, w, rank, world, dev, pg):
+    from paper_2511_14390_b200 import _binding as B
+    torch.cuda.set_device(dev)
+    L2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    samples = w["batch"] * w["length"]
+    bytes_per_set = 4 * samples * (8 if w["dtype"] == "f64" else 4)
+    nsets = max(2, int(np.ceil(3 * L2 / bytes_per_set)) + 1)
+    nsets = min(nsets, 64)
+    prob = Problem(w, dev, 1000 + rank, nsets)
+    stream = torch.cuda.Stream(device=dev)
+    use_graph = not args.no_graph
+
+    def run_steps(i0, n):
+        for i in range(i0, i0 + n):
+            prob.step(i, stream, pg)
+
+    with torch.cuda.stream(stream):
+        run_steps(0, max(args.warmup, 1))           # warm-up (also sets kernel attributes)
+    torch.cuda.synchronize(dev)
+
+    graph = None
+    if use_graph:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                run_steps(args.warmup, args.steps)
+            torch.cuda.synchronize(dev)
+            stream.wait_stream(torch.cuda.current_stream(dev))
+            for _ in range(max(args.warmup, 3)):   # warm replays
+                with torch.cuda.stream(stream):
+                    graph.replay()
+            torch.cuda.synchronize(dev)
+        except Exception as e:  # pragma: no cover - fall back to eager on capture failure
+            print(f"[bench] graph capture failed ({e}); timing eager launches", file=sys.stderr)
+            graph = None
+            use_graph = False
+
+    # ---- timed region ----
+    sampler = ClockSampler(dev if isinstance(dev, int) else torch.cuda.current_device())
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = B.iir_launch_count()
+    with sampler:
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            if graph is not None:
+                graph.replay()
+            else:
+                run_steps(args.warmup, args.steps)
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    ms = e0.elapsed_time(e1)
+    # kernels per step are counted at capture/eager time
+    per_step_launches = None
+    if graph is None:
+        gpu_launches = B.iir_launch_count() - launches0
+    else:
+        n0 = B.iir_launch_count()
+        with torch.cuda.stream(stream):
+            prob.step(0, stream, None)
+        torch.cuda.synchronize(dev)
+        per_step_launches = B.iir_launch_count() - n0
+        gpu_launches = per_step_launches * args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+
+    # ---- per-kernel device times: the same K steps, each launch bracketed by
+    #      CUDA events on its stream (library instrumentation), eager ----
+    B.iir_profile_reset()
+    B.iir_profile_enable(True)
+    with torch.cuda.stream(stream):
+        run_steps(args.warmup, args.steps)
+    torch.cuda.synchronize(dev)
+    B.iir_profile_enable(False)
+    names = B.kernel_names()
+    ktimes = {}
+    for k, nm in enumerate(names):
+        tot, n = B.iir_profile_query(k)
+        if n:
+            ktimes[nm] = (tot, n)
+    B.iir_profile_reset()
+
+    # ---- e2e: through the public API with HOST buffers (pinned), copies inside the timed region ----
+    e2e = run_e2e(args, prob, stream, dev, world)
+
+    return dict(ms=ms, ktimes=ktimes, gpu_launches=gpu_launches, per_step_launches=per_step_launches,
+                clocks=sampler.summary(), nsets=nsets, set_bytes=prob.set_bytes(), L2=L2, graph=use_graph,
+                e2e=e2e)
+
+
+def run_e2e(args, prob, stream, dev, world):
+    s0 = prob.sets[0]
+    hx = torch.empty_like(s0["x"], device="cpu").pin_memory()
+    hgy = torch.empty_like(s0["gy"], device="cpu").pin_memory()
+    hx.copy_(s0["x"])
+    hgy.copy_(s0["gy"])
+    hy = torch.empty_like(hx).pin_memory()
+    hgx = torch.empty_like(hx).pin_memory()
+    outs_small = [t for t in (prob.gb, prob.ga, prob.zf, prob.gzi) if t is not None]
+    hsmall = [torch.empty_like(t, device="cpu").pin_memory() for t in outs_small]
+    steps = max(3, min(args.steps, 20))
+
+    def one():
+        s = prob.sets[0]
+        s["x"].copy_(hx, non_blocking=True)
+        s["gy"].copy_(hgy, non_blocking=True)
+        prob.step(0, stream, None)
+        hy.copy_(s["y"], non_blocking=True)
+        hgx.copy_(s["gx"], non_blocking=True)
+        for h, t in zip(hsmall, outs_small):
+            h.copy_(t, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        one()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(steps):
+            one()
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    h2d = hx.numel() * hx.element_size() + hgy.numel() * hgy.element_size()
+    d2h = 2 * hy.numel() * hy.element_size() + sum(h.numel() * h.element_size() for h in hsmall)
+    return dict(ms_per_step=ms, h2d=h2d, d2h=d2h, steps=steps)
+
+
+def cpu_baseline(w, budget_s=10.0):
+    """The fp64 oracle as it stands, on the host cores, on a bounded sample."""
+    import oracle
+    oracle.build()
+    rng = np.random.default_rng(7)
+    T = w["length"]
+    nseq = min(w["batch"], 64)
+    if w["coef"] == "per_sample":
+        T = min(T, 1 << 16)
+        p = inputs.tv_allpole_problem(7, batch=min(nseq, 8), length=T, order=w["order"], dtype=w["dtype"])
+        args = (p["a"].numpy(), p["x"].numpy(), p["zi"].numpy(), p["gy"].numpy(), p["gzf"].numpy())
+        fn = lambda: oracle.tv_allpole(*args)
+        nseq = args[1].shape[0]
+    else:
+        T = min(T, 1 << 20)
+        nseq = max(1, min(nseq, (1 << 22) // T))
+        p = inputs.lti_problem(7, form=w["form"], order=w["order"], batch=nseq, length=T, dtype=w["dtype"],
+                               angles=w["angles"])
+        form = 1 if w["form"] == "tdf" else 0
+        fn = lambda: oracle.lti(form, p["b"], p["a"], p["x"], p["zi"], p["gy"], p["gzf"])
+    cores = min(os.cpu_count() or 1, nseq)
+    reps = 0
+    t0 = time.perf_counter()
+    while True:
+        fn()
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or (reps >= 1 and el * (reps + 1) / reps > 3 * budget_s):
+            break
+    value = reps * nseq * T / el
+    return dict(value=value, unit="samples/s", cores=cores, kind="oracle",
+                sample=f"{reps} x ({nseq} sequences x {T} samples) of the workload, fp64 C oracle "
+                       f"(dense state space), {cores} host threads, {el:.1f} s wall")
+
+
+# -------------------------------------------------------------- reference ---
+def run_reference(args, w, rank, world):
+    """--impl reference: the oracle (the reference arm of this tier) timed as
+    the main loop, each step a bounded sample of the workload."""
+    import oracle
+    oracle.build()
+    if rank != 0:
+        return
+    T = w["length"]
+    if w["coef"] == "per_sample":
+        T = min(T, 1 << 15)
+        nseq = min(w["batch"], 8)
+        p = inputs.tv_allpole_problem(7, batch=nseq, length=T, order=w["order"], dtype=w["dtype"])
+        a_ = (p["a"].numpy(), p["x"].numpy(), p["zi"].numpy(), p["gy"].numpy(), p["gzf"].numpy())
+        fn = lambda: oracle.tv_allpole(*a_)
+    else:
+        T = min(T, 1 << 20)
+        nseq = max(1, min(w["batch"], 8, (1 << 21) // T))
+        p = inputs.lti_problem(7, form=w["form"], order=w["order"], batch=nseq, length=T, dtype=w["dtype"],
+                               angles=w["angles"])
+        form = 1 if w["form"] == "tdf" else 0
+        fn = lambda: oracle.lti(form, p["b"], p["a"], p["x"], p["zi"], p["gy"], p["gzf"])
+    for _ in range(args.warmup):
+        fn()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fn()
+    el = time.perf_counter() - t0
+    cores = min(os.cpu_count() or 1, nseq)
+    value = args.steps * nseq * T / el
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": w["desc"], "batch": w["batch"], "length": w["length"], "order": w["order"],
+                       "form": w["form"], "coef": w["coef"]},
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "oracle",
+                             "sample": f"each step: {nseq} sequences x {T} samples of the workload, fp64 C oracle"},
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def load_traffic(w):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return {}
+    try:
+        d = json.load(open(p))
+        return d.get(w["key"], {})
+    except Exception:
+        return {}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    w = dict(WORKLOADS[args.workload], key=args.workload)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, w, rank, world)
+        return
+
+    pg = None
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = torch.distributed.group.WORLD
+    dev = local
+    r = run_ours(args, w, rank, world, dev, pg)
+
+    samples_step = w["batch"] * w["length"] * world
+    value = samples_step * args.steps / (r["ms"] * 1e-3)
+    peak, peak_src = peaks()
+    abytes = algorithmic_bytes(w)
+    roof = None
+    if r["ktimes"]:
+        dom = max(r["ktimes"], key=lambda k: r["ktimes"][k][0])
+        tot, n = r["ktimes"][dom]
+        avg_ms = tot / n
+        per_launch = abytes.get(dom, 0) * w["batch"] * w["length"]
+        achieved = per_launch / (avg_ms * 1e-3) / 1e9
+        tr = load_traffic(w).get(dom)
+        step_kernel_ms = sum(t for t, _ in r["ktimes"].values()) / args.steps
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": tr, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": per_launch, "avg_launch_ms": avg_ms,
+                "kernel_ms": {k: t / n_ for k, (t, n_) in r["ktimes"].items()},
+                "share_of_step": {k: (t / args.steps) / step_kernel_ms for k, (t, _) in r["ktimes"].items()}}
+    step_bytes = sum(abytes.values()) * w["batch"] * w["length"]
+    e2e = r["e2e"]
+    e2e_val = samples_step / (e2e["ms_per_step"] * 1e-3) if e2e else None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(w)
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic (seeded Gaussian signals, random stable filters)",
+        "config": {"workload": w["desc"], "batch_per_gpu": w["batch"], "length": w["length"], "order": w["order"],
+                   "form": w["form"], "coef": w["coef"],
+                   "l2": f"{r['nsets']} rotating input/output buffer sets x {r['set_bytes'] / 2**20:.0f} MiB "
+                         f"(> 2x L2 = {2 * r['L2'] / 2**20:.0f} MiB)",
+                   "timing": "CUDA graph of K steps" if r["graph"] else "eager launches",
+                   "parallelism": f"dp{world} (batch-sharded)"},
+        "hbm_gbs_algorithmic_step": step_bytes / (r["ms"] / args.steps * 1e-3) / 1e9,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": "samples/s", "h2d_bytes_per_step": e2e["h2d"],
+                "d2h_bytes_per_step": e2e["d2h"]} if e2e else None,
+        "gpu_launches": r["gpu_launches"],
+        "clocks": r["clocks"],
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,126 @@
+/*
+ * iirgrad.h -- C ABI of the B200-native differentiable IIR filter library
+ * (libiirgrad.so), the hot path of arXiv 2511.14390.
+ *
+ * What it computes (citations are /root/reference/PAPER.md lines):
+ *   Eq.1 (l.46-51)   H(z) = (b0 + b1 z^-1 + .. + bM z^-M) / (a0 + a1 z^-1 + .. + aM z^-M)
+ *                    (a0 != 0; the library normalises by a0 -- Eq.1 is monic).
+ *   Eq.2-3 (l.53-56) DF-II:  u(n) = x(n) - sum a_i u(n-i),  y(n) = sum b_i u(n-i)
+ *   TDF-II (l.58,67) the transposed form, state space (A^T, C, B, D)
+ *                    == scipy.signal.lfilter(b, a, x, zi).
+ *   Eq.4-5 (l.60-63) state space v(n+1) = A v(n) + B x(n),  y(n) = C^T v(n) + D x(n),
+ *                    companion realisation (l.66).  zi = v(0), zf = v(N).
+ *   Eq.6-9 (l.89-111) closed-form backward: the adjoint recursion (Eq.7) run in
+ *                    reverse time from dz(N-1) = grad_zf, dx (Eq.8), dv(0) = grad_zi
+ *                    (Eq.9, App. A.3 l.277-294), dA/dB/dC/dD sums (Eqs.6,9), chained to
+ *                    grad_b, grad_a (including grad_a[0]).
+ *   l.178            per-sample ("parameter-varying") all-pole DF:
+ *                    y(n) = x(n) - sum_i a_i(n) y(n-i)   (IIR_COEF_PER_SAMPLE).
+ *   l.121-130 (Eq.10) time parallelism by an associative scan over (A, z) tuples:
+ *                    realised as a chunked scan with fp64 carries and single-pass
+ *                    decoupled look-back.
+ *
+ * The loss whose gradient iir_backward returns is
+ *   L = sum_{b,n} grad_y[b,n] * y[b,n] + sum_{b,i} grad_zf[b,i] * zf[b,i].
+ *
+ * Memory / layout / ownership
+ *   - Every data pointer is DEVICE memory owned by the caller.  The library never
+ *     allocates device memory and never synchronises the host: every call only
+ *     enqueues work on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *   - All tensors are C-contiguous and share the descriptor's dtype (fp32 / fp64).
+ *       x, y, grad_x, grad_y : (batch, length)            time is the last axis
+ *       zi, zf, grad_zi, grad_zf : (batch, order)
+ *       b, a, grad_b, grad_a : (order+1,) for IIR_COEF_SHARED,
+ *                              (batch, order+1) for IIR_COEF_PER_SEQ
+ *       a, grad_a           : (batch, length, order) for IIR_COEF_PER_SAMPLE (b = NULL,
+ *                              monic a0 = 1 implied, form must be IIR_DF2)
+ *     The caller zero-pads b / a to equal length ("padding if necessary").
+ *   - zi / zf are the state-space v(0) / v(N) of the chosen form: TDF = scipy's zi;
+ *     DF = [u(-1) .. u(-M)]; per-sample all-pole = [y(-1) .. y(-M)].
+ *   - `tape` (iir_tape_bytes) is written by iir_forward and read by iir_backward; it
+ *     must stay untouched in between.  `ws` (iir_workspace_bytes) is scratch used by
+ *     both calls; one ws must not be used by two calls that may run concurrently.
+ *   - Gradient outputs are OVERWRITTEN, not accumulated.  SHARED-coefficient
+ *     gradients are sums over the local batch (a multi-GPU driver all-reduces them).
+ *   - Optional pointers may be NULL: zi (zeros), zf (not written), grad_y (zeros),
+ *     grad_zf (zeros), grad_x / grad_b / grad_a / grad_zi (not written).
+ *   - Results are deterministic: same inputs and descriptor -> bitwise-identical
+ *     outputs (fixed reduction order, no floating-point atomics).
+ *
+ * Errors
+ *   Descriptor / pointer / size checks run on the host before any launch and return
+ *   IIR_EINVAL / IIR_EUNSUPPORTED / IIR_EWORKSPACE; a failed launch returns
+ *   IIR_ECUDA.  iir_last_error() returns a thread-local message for the last
+ *   failure.  Data-dependent conditions (a0 == 0, unstable filters, NaN inputs) are
+ *   NOT checked (that would need a device->host sync): they propagate as inf / nan.
+ */
+#ifndef IIRGRAD_H
+#define IIRGRAD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IIRGRAD_ABI_VERSION 1
+
+typedef enum { IIR_OK = 0, IIR_EINVAL = 1, IIR_EUNSUPPORTED = 2, IIR_ECUDA = 3, IIR_EWORKSPACE = 4 } iir_status_t;
+typedef enum { IIR_DF2 = 0, IIR_TDF2 = 1 } iir_form_t;          /* PAPER.md:52 footnote: type-II forms */
+typedef enum { IIR_F32 = 0, IIR_F64 = 1 } iir_dtype_t;
+typedef enum {
+    IIR_COEF_SHARED = 0,     /* b, a: (M+1); one filter for the whole batch          */
+    IIR_COEF_PER_SEQ = 1,    /* b, a: (B, M+1); one filter per sequence              */
+    IIR_COEF_PER_SAMPLE = 2  /* all-pole DF only: a: (B, T, M), b = NULL */
+} iir_coef_mode_t;
+
+typedef void *iir_stream_t;  /* a cudaStream_t */
+
+typedef struct {
+    int64_t batch;      /* B >= 1                                                  */
+    int64_t length;     /* T >= 1 samples per sequence                             */
+    int32_t order;      /* M: 1..8 (SHARED / PER_SEQ), 1..32 (PER_SAMPLE)          */
+    int32_t form;       /* iir_form_t                                              */
+    int32_t dtype;      /* iir_dtype_t                                             */
+    int32_t coef_mode;  /* iir_coef_mode_t                                         */
+} iir_desc_t;
+
+/* Bytes of the forward->backward tape / of the scratch workspace (0 on a bad desc). */
+size_t iir_tape_bytes(const iir_desc_t *desc);
+size_t iir_workspace_bytes(const iir_desc_t *desc);
+
+/* Forward: y = filter(b, a, x; zi), zf = final state.  Eqs.1-5. */
+iir_status_t iir_forward(const iir_desc_t *desc, const void *b, const void *a, const void *x,
+                         const void *zi, void *y, void *zf, void *tape, size_t tape_bytes,
+                         void *ws, size_t ws_bytes, iir_stream_t stream);
+
+/* Backward: gradients of L (above) w.r.t. x, b, a, zi.  Eqs.6-9 + App. A.
+ * b, a, x, y, zi must be the forward's inputs / output (unmodified), tape its tape. */
+iir_status_t iir_backward(const iir_desc_t *desc, const void *grad_y, const void *grad_zf,
+                          const void *b, const void *a, const void *x, const void *y,
+                          const void *zi, const void *tape, size_t tape_bytes,
+                          void *grad_x, void *grad_b, void *grad_a, void *grad_zi,
+                          void *ws, size_t ws_bytes, iir_stream_t stream);
+
+/* Thread-local message describing the last non-IIR_OK status of this thread. */
+const char *iir_last_error(void);
+int iir_abi_version(void);
+
+/* ---- instrumentation (host side only; no effect on results) -------------------
+ * Every kernel the library launches is counted.  When profiling is enabled each
+ * launch is additionally bracketed by cudaEventRecord on its own stream, so the
+ * per-kernel device time can be read back after the caller synchronised.        */
+int64_t iir_launch_count(void);                     /* kernels launched since load  */
+int iir_num_kernels(void);                          /* number of kernel kinds       */
+const char *iir_kernel_name(int kind);
+void iir_profile_enable(int on);
+void iir_profile_reset(void);
+/* Accumulated device milliseconds and launch count of kernel kind `kind` over the
+ * profiled launches; syncs on the recorded events (call after a stream sync). */
+int iir_profile_query(int kind, double *total_ms, int64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IIRGRAD_H */

@@ -1,0 +1,77 @@
+"""torch.autograd front end: ``lfilter`` and ``allpole_tv``.
+
+Both are ``torch.autograd.Function``s whose forward calls ``iir_forward`` and
+whose backward calls ``iir_backward`` of libiirgrad.so on the current CUDA
+stream.  Torch only provides device memory (outputs, tape and workspace come
+from its caching allocator) and streams.  CUDA tensors only: a CPU tensor is
+an error, not a fallback.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _binding as B
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("paper_2511_14390_b200 runs on CUDA tensors only (no CPU fallback)")
+
+
+def _c(t):
+    return None if t is None else t.contiguous()
+
+
+class LFilterFunction(torch.autograd.Function):
+    """y, zf = filter(b, a, x, zi) for DF-II / TDF-II, fixed coefficients."""
+
+    @staticmethod
+    def forward(ctx, x, b, a, zi, form):
+        _require_cuda(x, b, a, zi)
+        x, b, a, zi = _c(x), _c(b), _c(a), _c(zi)
+        Bsz, T = x.shape
+        M = b.shape[-1] - 1
+        mode = B.IIR_COEF_SHARED if b.dim() == 1 else B.IIR_COEF_PER_SEQ
+        desc = B.make_desc(Bsz, T, M, form, x.dtype, mode)
+        y = torch.empty_like(x)
+        zf = torch.empty((Bsz, M), dtype=x.dtype, device=x.device)
+        tb = B.iir_tape_bytes(desc)
+        wb = B.iir_workspace_bytes(desc)
+        tape = torch.empty(tb, dtype=torch.uint8, device=x.device)
+        ws = torch.empty(wb, dtype=torch.uint8, device=x.device)
+        B.iir_forward(desc, b, a, x, zi, y, zf, tape, tb, ws, wb)
+        ctx.desc = desc
+        ctx.save_for_backward(x, b, a, zi if zi is not None else torch.empty(0, device=x.device), y, tape)
+        ctx.has_zi = zi is not None
+        return y, zf
+
+    @staticmethod
+    def backward(ctx, gy, gzf):
+        x, b, a, zi, y, tape = ctx.saved_tensors
+        zi = zi if ctx.has_zi else None
+        desc = ctx.desc
+        gy = _c(gy)
+        gzf = _c(gzf)
+        gx = torch.empty_like(x) if ctx.needs_input_grad[0] else None
+        gb = torch.empty_like(b) if ctx.needs_input_grad[1] else None
+        ga = torch.empty_like(a) if ctx.needs_input_grad[2] else None
+        gzi = torch.empty_like(zi) if (zi is not None and ctx.needs_input_grad[3]) else None
+        wb = B.iir_workspace_bytes(desc)
+        ws = torch.empty(wb, dtype=torch.uint8, device=x.device)
+        B.iir_backward(desc, gy, gzf, b, a, x, y, zi, tape, tape.numel(), gx, gb, ga, gzi, ws, wb)
+        return gx, gb, ga, gzi, None
+
+
+def lfilter(x, b, a, zi=None, form="tdf", return_zf=False):
+    """Differentiable IIR filter of each row of x (B, T) by b, a ((M+1,) or
+    (B, M+1)); zi (B, M) is the state-space initial state of the chosen form
+    (TDF: scipy's zi).  Returns y, or (y, zf) when return_zf."""
+    squeeze = x.dim() == 1
+    if squeeze:
+        x = x[None]
+        zi = None if zi is None else zi[None]
+    y, zf = LFilterFunction.apply(x, b, a, zi, form)
+    if squeeze:
+        y, zf = y[0], zf[0]
+    return (y, zf) if return_zf else y

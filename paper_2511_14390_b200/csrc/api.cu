@@ -1,0 +1,268 @@
+// api.cu -- the C ABI of libiirgrad.so (see include/iirgrad.h): host-side
+// validation, workspace / tape layout, kernel dispatch and instrumentation.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/iirgrad.h"
+#include "lti.cuh"
+#include "host.h"
+#include "lti_host.cuh"
+
+using namespace iirg;
+
+// ---------------------------------------------------------------- errors ----
+static thread_local std::string g_err;
+namespace iirg {
+iir_status_t fail(iir_status_t st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+}  // namespace iirg
+
+// ------------------------------------------------------- instrumentation ----
+static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "lti_finalize", "tv_fwd", "tv_bwd", "tv_fix"};
+static std::atomic<int64_t> g_launches{0};
+struct ProfRec { int kind; cudaEvent_t e0, e1; };
+static std::mutex g_pmu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_pending;
+static std::vector<cudaEvent_t> g_pool;
+static double g_ms[K_NUM];
+static int64_t g_cnt[K_NUM];
+
+static cudaEvent_t ev_get() {
+    if (!g_pool.empty()) { cudaEvent_t e = g_pool.back(); g_pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+namespace iirg {
+LaunchGuard::LaunchGuard(int k, cudaStream_t s) : kind(k), st(s) {
+    std::lock_guard<std::mutex> lk(g_pmu);
+    if (g_prof_on) { e0 = ev_get(); e1 = ev_get(); }
+    if (e0) cudaEventRecord(e0, st);
+}
+iir_status_t LaunchGuard::done() {
+    cudaError_t err = cudaGetLastError();
+    if (e0) {
+        cudaEventRecord(e1, st);
+        std::lock_guard<std::mutex> lk(g_pmu);
+        g_pending.push_back({kind, e0, e1});
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (err != cudaSuccess)
+        return fail(IIR_ECUDA, std::string(kKindNames[kind]) + " launch failed: " + cudaGetErrorString(err));
+    return IIR_OK;
+}
+}  // namespace iirg
+
+// ------------------------------------------------------------- layout -------
+static size_t dsize(int dtype) { return dtype == IIR_F64 ? 8 : 4; }
+static int tile_samples(int dtype) { return NT * (dtype == IIR_F64 ? Chunk<double>::L : Chunk<float>::L); }
+
+static int tab_size(int M) {
+    switch (M) {
+        case 1: return Tab<1>::SIZE; case 2: return Tab<2>::SIZE; case 3: return Tab<3>::SIZE;
+        case 4: return Tab<4>::SIZE; case 5: return Tab<5>::SIZE; case 6: return Tab<6>::SIZE;
+        case 7: return Tab<7>::SIZE; case 8: return Tab<8>::SIZE;
+    }
+    return 0;
+}
+
+static iir_status_t check_desc(const iir_desc_t* d) {
+    if (d == nullptr) return fail(IIR_EINVAL, "desc is NULL");
+    if (d->batch < 1) return fail(IIR_EINVAL, "batch must be >= 1");
+    if (d->length < 1) return fail(IIR_EINVAL, "length must be >= 1");
+    if (d->dtype != IIR_F32 && d->dtype != IIR_F64) return fail(IIR_EINVAL, "dtype must be IIR_F32 or IIR_F64");
+    if (d->form != IIR_DF2 && d->form != IIR_TDF2) return fail(IIR_EINVAL, "form must be IIR_DF2 or IIR_TDF2");
+    if (d->coef_mode == IIR_COEF_PER_SAMPLE) {
+        if (d->form != IIR_DF2) return fail(IIR_EUNSUPPORTED, "per-sample coefficients: only the all-pole DF form");
+        if (d->order < 1 || d->order > TV_MAX_M) return fail(IIR_EUNSUPPORTED, "per-sample order must be 1..32");
+        if (!tv_supported(d->order)) return fail(IIR_EUNSUPPORTED, "per-sample order not compiled in");
+        return IIR_OK;
+    }
+    if (d->coef_mode != IIR_COEF_SHARED && d->coef_mode != IIR_COEF_PER_SEQ)
+        return fail(IIR_EINVAL, "coef_mode must be SHARED, PER_SEQ or PER_SAMPLE");
+    if (d->order < 1 || d->order > 8) return fail(IIR_EUNSUPPORTED, "order must be 1..8 for LTI filters");
+    return IIR_OK;
+}
+
+static Layout layout(const iir_desc_t* d) {
+    if (d->coef_mode == IIR_COEF_PER_SAMPLE) return tv_layout(d);
+    Layout L;
+    const int M = d->order;
+    const int64_t TS = tile_samples(d->dtype);
+    L.ntiles = (d->length + TS - 1) / TS;
+    L.ntot = L.ntiles * d->batch;
+    L.ncoef = d->coef_mode == IIR_COEF_SHARED ? 1 : d->batch;
+    size_t o = 0;
+    L.ws_ticket = o; o += 256;
+    L.ws_flags = o; o += al256(L.ntot * 4);
+    L.ws_clear = o;
+    L.ws_agg = o; o += al256(L.ntot * M * 8);
+    L.ws_incl = o; o += al256(L.ntot * M * 8);
+    L.ws_part = o; o += al256(L.ntot * (2 * M + 1) * 8);
+    L.ws_bytes = o;
+    o = 0;
+    L.tp_tab = o; o += al256((size_t)L.ncoef * tab_size(M) * 8);
+    L.tp_u = o;
+    if (d->form == IIR_DF2) o += al256((size_t)d->batch * d->length * dsize(d->dtype));
+    L.tp_bytes = o;
+    return L;
+}
+
+// -------------------------------------------------------------- kernels -----
+// Instantiated in lti_<dtype>_<form>.cu (split for parallel compilation).
+namespace iirg {
+template <typename T, int FORM> iir_status_t run_lti_m(int M, LtiCall& c);
+extern template iir_status_t run_lti_m<float, 0>(int, LtiCall&);
+extern template iir_status_t run_lti_m<float, 1>(int, LtiCall&);
+extern template iir_status_t run_lti_m<double, 0>(int, LtiCall&);
+extern template iir_status_t run_lti_m<double, 1>(int, LtiCall&);
+}  // namespace iirg
+
+static iir_status_t run_lti_any(LtiCall& c) {
+    const iir_desc_t* d = c.d;
+    if (d->dtype == IIR_F32)
+        return d->form == IIR_DF2 ? run_lti_m<float, 0>(d->order, c) : run_lti_m<float, 1>(d->order, c);
+    return d->form == IIR_DF2 ? run_lti_m<double, 0>(d->order, c) : run_lti_m<double, 1>(d->order, c);
+}
+
+static bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ------------------------------------------------------------- C ABI --------
+extern "C" {
+
+int iir_abi_version(void) { return IIRGRAD_ABI_VERSION; }
+const char* iir_last_error(void) { return g_err.c_str(); }
+
+size_t iir_tape_bytes(const iir_desc_t* d) {
+    if (check_desc(d) != IIR_OK) return 0;
+    return layout(d).tp_bytes;
+}
+size_t iir_workspace_bytes(const iir_desc_t* d) {
+    if (check_desc(d) != IIR_OK) return 0;
+    return layout(d).ws_bytes;
+}
+
+iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, const void* x, const void* zi, void* y,
+                         void* zf, void* tape, size_t tape_bytes, void* ws, size_t ws_bytes, iir_stream_t stream) {
+    iir_status_t s = check_desc(d);
+    if (s != IIR_OK) return s;
+    const Layout L = layout(d);
+    if (x == nullptr || y == nullptr) return fail(IIR_EINVAL, "x and y must be non-NULL");
+    if (a == nullptr) return fail(IIR_EINVAL, "a must be non-NULL");
+    if (d->coef_mode == IIR_COEF_PER_SAMPLE) {
+        if (b != nullptr) return fail(IIR_EINVAL, "per-sample coefficients: b must be NULL (all-pole)");
+    } else if (b == nullptr) {
+        return fail(IIR_EINVAL, "b must be non-NULL");
+    }
+    if (tape == nullptr || tape_bytes < L.tp_bytes) return fail(IIR_EWORKSPACE, "tape missing or too small");
+    if (ws == nullptr || ws_bytes < L.ws_bytes) return fail(IIR_EWORKSPACE, "workspace missing or too small");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    char* w = static_cast<char*>(ws);
+    char* t = static_cast<char*>(tape);
+    cudaError_t e = cudaMemsetAsync(w, 0, L.ws_clear, st);
+    if (e != cudaSuccess) return fail(IIR_ECUDA, std::string("memset: ") + cudaGetErrorString(e));
+    const int W = d->dtype == IIR_F64 ? 2 : 4;
+    const bool vec = (d->length % W == 0) && aligned16(x) && aligned16(y) && aligned16(t + L.tp_u);
+    if (d->coef_mode == IIR_COEF_PER_SAMPLE) return tv_forward(d, L, a, x, zi, y, zf, t, w, vec, st);
+
+    LtiCall c{};
+    c.d = d; c.L = &L; c.st = st; c.is_fwd = true; c.b = b; c.a = a;
+    LtiFwdArgs& fa = c.fa;
+    fa.x = x; fa.zi = zi; fa.y = y; fa.zf = zf;
+    fa.u = d->form == IIR_DF2 ? t + L.tp_u : nullptr;
+    fa.tab = reinterpret_cast<const double*>(t + L.tp_tab);
+    fa.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
+    fa.ticket = reinterpret_cast<unsigned*>(w + L.ws_ticket);
+    fa.flags = reinterpret_cast<unsigned*>(w + L.ws_flags);
+    fa.agg = reinterpret_cast<double*>(w + L.ws_agg);
+    fa.incl = reinterpret_cast<double*>(w + L.ws_incl);
+    fa.B = d->batch; fa.Tlen = d->length; fa.ntiles = (int)L.ntiles; fa.vec = vec;
+    return run_lti_any(c);
+}
+
+iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* grad_zf, const void* b, const void* a,
+                          const void* x, const void* y, const void* zi, const void* tape, size_t tape_bytes,
+                          void* grad_x, void* grad_b, void* grad_a, void* grad_zi, void* ws, size_t ws_bytes,
+                          iir_stream_t stream) {
+    iir_status_t s = check_desc(d);
+    if (s != IIR_OK) return s;
+    const Layout L = layout(d);
+    if (tape == nullptr || tape_bytes < L.tp_bytes) return fail(IIR_EWORKSPACE, "tape missing or too small");
+    if (ws == nullptr || ws_bytes < L.ws_bytes) return fail(IIR_EWORKSPACE, "workspace missing or too small");
+    if (d->coef_mode != IIR_COEF_PER_SAMPLE && d->form == IIR_TDF2 && (x == nullptr || y == nullptr))
+        return fail(IIR_EINVAL, "TDF backward needs the forward's x and y");
+    if (d->coef_mode == IIR_COEF_PER_SAMPLE && (a == nullptr || y == nullptr))
+        return fail(IIR_EINVAL, "per-sample backward needs the forward's a and y");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    char* w = static_cast<char*>(ws);
+    const char* t = static_cast<const char*>(tape);
+    cudaError_t e = cudaMemsetAsync(w, 0, L.ws_clear, st);
+    if (e != cudaSuccess) return fail(IIR_ECUDA, std::string("memset: ") + cudaGetErrorString(e));
+    const int W = d->dtype == IIR_F64 ? 2 : 4;
+    const bool vec = (d->length % W == 0) && aligned16(grad_y) && aligned16(x) && aligned16(y) &&
+                     aligned16(grad_x) && aligned16(t + L.tp_u);
+    if (d->coef_mode == IIR_COEF_PER_SAMPLE)
+        return tv_backward(d, L, grad_y, grad_zf, a, y, zi, t, grad_x, grad_a, grad_zi, w, vec, st);
+
+    LtiCall c{};
+    c.d = d; c.L = &L; c.st = st; c.is_fwd = false; c.gb = grad_b; c.ga = grad_a;
+    LtiBwdArgs& ba = c.ba;
+    ba.gy = grad_y; ba.gzf = grad_zf; ba.x = x; ba.y = y;
+    ba.u = d->form == IIR_DF2 ? t + L.tp_u : nullptr;
+    ba.zi = zi; ba.gx = grad_x; ba.gzi = grad_zi;
+    ba.partial = reinterpret_cast<double*>(w + L.ws_part);
+    ba.want_coef = (grad_b != nullptr || grad_a != nullptr);
+    ba.tab = reinterpret_cast<const double*>(t + L.tp_tab);
+    ba.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
+    ba.ticket = reinterpret_cast<unsigned*>(w + L.ws_ticket);
+    ba.flags = reinterpret_cast<unsigned*>(w + L.ws_flags);
+    ba.agg = reinterpret_cast<double*>(w + L.ws_agg);
+    ba.incl = reinterpret_cast<double*>(w + L.ws_incl);
+    ba.B = d->batch; ba.Tlen = d->length; ba.ntiles = (int)L.ntiles; ba.vec = vec;
+    (void)b; (void)a;
+    return run_lti_any(c);
+}
+
+int64_t iir_launch_count(void) { return g_launches.load(); }
+int iir_num_kernels(void) { return K_NUM; }
+const char* iir_kernel_name(int kind) { return (kind >= 0 && kind < K_NUM) ? kKindNames[kind] : ""; }
+
+void iir_profile_enable(int on) {
+    std::lock_guard<std::mutex> lk(g_pmu);
+    g_prof_on = on != 0;
+}
+void iir_profile_reset(void) {
+    std::lock_guard<std::mutex> lk(g_pmu);
+    for (auto& r : g_pending) { g_pool.push_back(r.e0); g_pool.push_back(r.e1); }
+    g_pending.clear();
+    for (int k = 0; k < K_NUM; ++k) { g_ms[k] = 0; g_cnt[k] = 0; }
+}
+int iir_profile_query(int kind, double* total_ms, int64_t* launches) {
+    if (kind < 0 || kind >= K_NUM) return 1;
+    std::lock_guard<std::mutex> lk(g_pmu);
+    for (auto& r : g_pending) {
+        float ms = 0.f;
+        cudaEventSynchronize(r.e1);
+        cudaEventElapsedTime(&ms, r.e0, r.e1);
+        g_ms[r.kind] += ms;
+        g_cnt[r.kind] += 1;
+        g_pool.push_back(r.e0);
+        g_pool.push_back(r.e1);
+    }
+    g_pending.clear();
+    if (total_ms) *total_ms = g_ms[kind];
+    if (launches) *launches = g_cnt[kind];
+    return 0;
+}
+
+}  // extern "C"

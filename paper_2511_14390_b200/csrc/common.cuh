@@ -1,0 +1,112 @@
+// common.cuh -- shared device helpers of the sm_100a IIR kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace iirg {
+
+constexpr int NT = 128;          // threads per CTA (4 warps)
+constexpr int NW = NT / 32;      // warps per CTA
+constexpr int LOG_NW = 2;
+constexpr int KLB = 32;          // depth of the P_tile^k look-back power table
+constexpr int HALO = 8;          // u-history halo of the DF backward tile (>= M)
+
+// Samples per thread chunk (L) by data type; a tile is NT * L samples.
+template <typename T> struct Chunk;
+template <> struct Chunk<float>  { static constexpr int L = 32; };
+template <> struct Chunk<double> { static constexpr int L = 16; };
+
+// Shared-memory tile layout: 16 B of padding after every 128 B row, so that the
+// 128-bit reads of 8 consecutive threads (each owning one or more whole rows)
+// fall into distinct banks.
+template <typename T> __host__ __device__ constexpr int pidx(int e) {
+    return e + (e / (128 / (int)sizeof(T))) * (16 / (int)sizeof(T));
+}
+
+template <typename T> struct Vec;
+template <> struct Vec<float>  { using type = float4;  static constexpr int W = 4; };
+template <> struct Vec<double> { using type = double2; static constexpr int W = 2; };
+
+__device__ __forceinline__ float  vget(const float4& v, int i)  { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+__device__ __forceinline__ double vget(const double2& v, int i) { return i == 0 ? v.x : v.y; }
+__device__ __forceinline__ void vset(float4& v, int i, float s)   { if (i == 0) v.x = s; else if (i == 1) v.y = s; else if (i == 2) v.z = s; else v.w = s; }
+__device__ __forceinline__ void vset(double2& v, int i, double s) { if (i == 0) v.x = s; else v.y = s; }
+
+// Streaming global accesses (no L1 allocation; inputs are read exactly once).
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double2 ldg_stream(const double2* p) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void stg_stream(float4* p, float4 v) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+__device__ __forceinline__ void stg_stream(double2* p, double2 v) {
+    asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// Look-back status words: release / acquire at GPU scope.
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ double shfl_up_d(double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
+__device__ __forceinline__ double shfl_d(double v, int s) { return __shfl_sync(0xffffffffu, v, s); }
+
+// Copy global [p0, p0+n) of a row of length Tlen into a padded smem tile;
+// positions outside [0, Tlen) read as zero.  vec: rows and p0 are 16 B aligned.
+template <typename T, int N>
+__device__ __forceinline__ void tile_load(T* __restrict__ sm, const T* __restrict__ row, int64_t p0,
+                                          int64_t Tlen, bool vec) {
+    using V = typename Vec<T>::type;
+    constexpr int W = Vec<T>::W;
+    if (vec) {
+#pragma unroll 4
+        for (int q = threadIdx.x; q < N / W; q += NT) {
+            const int64_t pos = p0 + (int64_t)q * W;
+            V v;
+            if (pos >= 0 && pos < Tlen) v = ldg_stream(reinterpret_cast<const V*>(row + pos));
+            else { v = V{}; }
+            *reinterpret_cast<V*>(sm + pidx<T>(q * W)) = v;
+        }
+    } else {
+        for (int e = threadIdx.x; e < N; e += NT) {
+            const int64_t pos = p0 + e;
+            sm[pidx<T>(e)] = (pos >= 0 && pos < Tlen) ? row[pos] : T(0);
+        }
+    }
+}
+
+// Store the smem tile [0, N) to global positions [p0, p0+N) clipped to [0, Tlen).
+template <typename T, int N>
+__device__ __forceinline__ void tile_store(T* __restrict__ row, const T* __restrict__ sm, int64_t p0,
+                                           int64_t Tlen, bool vec) {
+    using V = typename Vec<T>::type;
+    constexpr int W = Vec<T>::W;
+    if (vec) {
+#pragma unroll 4
+        for (int q = threadIdx.x; q < N / W; q += NT) {
+            const int64_t pos = p0 + (int64_t)q * W;
+            if (pos >= 0 && pos < Tlen)
+                stg_stream(reinterpret_cast<V*>(row + pos), *reinterpret_cast<const V*>(sm + pidx<T>(q * W)));
+        }
+    } else {
+        for (int e = threadIdx.x; e < N; e += NT) {
+            const int64_t pos = p0 + e;
+            if (pos >= 0 && pos < Tlen) row[pos] = sm[pidx<T>(e)];
+        }
+    }
+}
+
+}  // namespace iirg

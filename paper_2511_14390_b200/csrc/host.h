@@ -1,0 +1,50 @@
+// host.h -- internal host-side helpers shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/iirgrad.h"
+
+namespace iirg {
+
+iir_status_t fail(iir_status_t st, const std::string& msg);
+
+enum Kind { K_LTI_PREP = 0, K_LTI_FWD, K_LTI_BWD, K_LTI_FIN, K_TV_FWD, K_TV_BWD, K_TV_FIX, K_NUM };
+
+// Launch bookkeeping: counts every kernel and (when profiling is on) brackets it
+// with CUDA events on its stream.
+struct LaunchGuard {
+    int kind; cudaStream_t st; cudaEvent_t e0 = nullptr, e1 = nullptr;
+    LaunchGuard(int k, cudaStream_t s);
+    iir_status_t done();
+};
+template <typename F>
+iir_status_t launch(int kind, cudaStream_t st, F&& f) {
+    LaunchGuard g(kind, st);
+    f();
+    return g.done();
+}
+
+inline size_t al256(size_t n) { return (n + 255) / 256 * 256; }
+
+struct Layout {
+    int64_t ntiles = 0, ntot = 0, ncoef = 0;
+    size_t ws_ticket = 0, ws_flags = 0, ws_agg = 0, ws_incl = 0, ws_part = 0, ws_bytes = 0, ws_clear = 0;
+    size_t tp_tab = 0, tp_u = 0, tp_extra = 0, tp_bytes = 0;
+};
+
+// per-sample (time-varying all-pole) path, tv.cu
+constexpr int TV_MAX_M = 32;
+bool tv_supported(int M);
+Layout tv_layout(const iir_desc_t* d);
+iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* a, const void* x, const void* zi, void* y,
+                        void* zf, char* tape, char* ws, bool vec, cudaStream_t st);
+iir_status_t tv_backward(const iir_desc_t* d, const Layout& L, const void* gy, const void* gzf, const void* a,
+                         const void* y, const void* zi, const char* tape, void* gx, void* ga, void* gzi, char* ws,
+                         bool vec, cudaStream_t st);
+
+}  // namespace iirg

@@ -1,0 +1,91 @@
+// lti_host.cuh -- host-side launchers of the LTI kernels (included by the
+// per-(dtype, form) instantiation units and by api.cu for the declarations).
+#pragma once
+#include "host.h"
+#include "lti.cuh"
+
+namespace iirg {
+
+template <typename K>
+inline void set_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <typename T, int M, int FORM>
+struct LtiOps {
+    static constexpr int TS = NT * Chunk<T>::L;
+    static size_t fwd_smem() { return (size_t)pidx<T>(TS) * sizeof(T) * (FORM == 0 ? 2 : 1); }
+    static size_t bwd_smem() {
+        return ((size_t)pidx<T>(TS) + pidx<T>(TS + HALO) + (FORM == 1 ? pidx<T>(TS) : 0)) * sizeof(T);
+    }
+    static iir_status_t prep(const iir_desc_t* d, const Layout& L, const void* b, const void* a, double* tab,
+                             cudaStream_t st) {
+        const int64_t cstride = d->coef_mode == IIR_COEF_SHARED ? 0 : (M + 1);
+        return launch(K_LTI_PREP, st, [&] {
+            lti_prep_kernel<T, M, FORM><<<(unsigned)L.ncoef, 64, 0, st>>>(
+                static_cast<const T*>(b), static_cast<const T*>(a), cstride, tab, Tab<M>::SIZE);
+        });
+    }
+    static iir_status_t fwd(const iir_desc_t* d, const Layout& L, const LtiFwdArgs& args, cudaStream_t st) {
+        static std::once_flag once;
+        std::call_once(once, [] { set_smem(lti_fwd_kernel<T, M, FORM>, fwd_smem()); });
+        return launch(K_LTI_FWD, st, [&] {
+            lti_fwd_kernel<T, M, FORM><<<(unsigned)L.ntot, NT, fwd_smem(), st>>>(args);
+        });
+    }
+    static iir_status_t bwd(const iir_desc_t* d, const Layout& L, const LtiBwdArgs& args, cudaStream_t st) {
+        static std::once_flag once;
+        std::call_once(once, [] { set_smem(lti_bwd_kernel<T, M, FORM>, bwd_smem()); });
+        return launch(K_LTI_BWD, st, [&] {
+            lti_bwd_kernel<T, M, FORM><<<(unsigned)L.ntot, NT, bwd_smem(), st>>>(args);
+        });
+    }
+    static iir_status_t fin(const iir_desc_t* d, const Layout& L, const double* part, const double* tab, void* gb,
+                            void* ga, cudaStream_t st) {
+        const int64_t per_set = d->coef_mode == IIR_COEF_SHARED ? L.ntot : L.ntiles;
+        const int64_t tstride = d->coef_mode == IIR_COEF_SHARED ? 0 : Tab<M>::SIZE;
+        return launch(K_LTI_FIN, st, [&] {
+            lti_finalize_kernel<T, M, FORM><<<(unsigned)L.ncoef, 256, 0, st>>>(
+                part, per_set, tab, tstride, static_cast<T*>(gb), static_cast<T*>(ga));
+        });
+    }
+};
+
+struct LtiCall {
+    const iir_desc_t* d; const Layout* L; cudaStream_t st;
+    // forward
+    const void *b, *a; LtiFwdArgs fa;
+    // backward
+    LtiBwdArgs ba; void *gb, *ga;
+    bool is_fwd;
+};
+
+template <typename T, int M, int FORM>
+inline iir_status_t run_lti(LtiCall& c) {
+    using Ops = LtiOps<T, M, FORM>;
+    if (c.is_fwd) {
+        iir_status_t s = Ops::prep(c.d, *c.L, c.b, c.a, const_cast<double*>(c.fa.tab), c.st);
+        if (s != IIR_OK) return s;
+        return Ops::fwd(c.d, *c.L, c.fa, c.st);
+    }
+    iir_status_t s = Ops::bwd(c.d, *c.L, c.ba, c.st);
+    if (s != IIR_OK || !c.ba.want_coef) return s;
+    return Ops::fin(c.d, *c.L, c.ba.partial, c.ba.tab, c.gb, c.ga, c.st);
+}
+
+template <typename T, int FORM>
+iir_status_t run_lti_m(int M, LtiCall& c) {
+    switch (M) {
+        case 1: return run_lti<T, 1, FORM>(c);
+        case 2: return run_lti<T, 2, FORM>(c);
+        case 3: return run_lti<T, 3, FORM>(c);
+        case 4: return run_lti<T, 4, FORM>(c);
+        case 5: return run_lti<T, 5, FORM>(c);
+        case 6: return run_lti<T, 6, FORM>(c);
+        case 7: return run_lti<T, 7, FORM>(c);
+        case 8: return run_lti<T, 8, FORM>(c);
+    }
+    return fail(IIR_EUNSUPPORTED, "order");
+}
+
+}  // namespace iirg

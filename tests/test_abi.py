@@ -1,0 +1,75 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol that
+include/iirgrad.h declares, sizes workspaces, and rejects bad descriptors before
+any launch (no GPU needed for any of this)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2511_14390_b200 import _binding as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "iirgrad.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(iir_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = B.lib()
+    names = declared_functions()
+    assert "iir_forward" in names and "iir_backward" in names
+    for n in names:
+        assert hasattr(L, n), n
+        assert n in B.EXPORTS, n
+    assert B.iir_abi_version() == 1
+
+
+def test_workspace_and_tape_sizes():
+    d = B.make_desc(64, 1 << 16, 2, "tdf", B.IIR_F32, B.IIR_COEF_SHARED)
+    assert B.iir_tape_bytes(d) > 0
+    assert B.iir_workspace_bytes(d) > 0
+    d_df = B.make_desc(64, 1 << 16, 2, "df", B.IIR_F32, B.IIR_COEF_SHARED)
+    # DF keeps the internal signal u in the tape: B*T*4 bytes more than TDF.
+    assert B.iir_tape_bytes(d_df) - B.iir_tape_bytes(d) >= 64 * (1 << 16) * 4
+    d_seq = B.make_desc(64, 1 << 16, 8, "tdf", B.IIR_F32, B.IIR_COEF_PER_SEQ)
+    assert B.iir_tape_bytes(d_seq) > B.iir_tape_bytes(B.make_desc(64, 1 << 16, 8, "tdf", B.IIR_F32, 0))
+
+
+@pytest.mark.parametrize("field,value,status", [
+    ("batch", 0, B.IIR_EINVAL), ("length", 0, B.IIR_EINVAL), ("order", 0, B.IIR_EUNSUPPORTED),
+    ("order", 9, B.IIR_EUNSUPPORTED), ("form", 7, B.IIR_EINVAL), ("dtype", 5, B.IIR_EINVAL),
+    ("coef_mode", 9, B.IIR_EINVAL)])
+def test_bad_descriptor_rejected_before_launch(field, value, status):
+    d = B.make_desc(2, 100, 2, "tdf", B.IIR_F32, B.IIR_COEF_SHARED)
+    setattr(d, field, value)
+    assert B.iir_tape_bytes(d) == 0
+    L = B.lib()
+    st = L.iir_forward(ctypes.byref(d), 8, 8, 8, None, 8, None, 8, 1 << 30, 8, 1 << 30, None)
+    assert st == status, B.iir_last_error()
+    assert len(B.iir_last_error()) > 0
+
+
+def test_missing_pointers_and_small_workspace_rejected():
+    d = B.make_desc(2, 100, 2, "tdf", B.IIR_F32, B.IIR_COEF_SHARED)
+    L = B.lib()
+    tb, wb = B.iir_tape_bytes(d), B.iir_workspace_bytes(d)
+    assert L.iir_forward(ctypes.byref(d), 8, 8, None, None, 8, None, 8, tb, 8, wb, None) == B.IIR_EINVAL
+    assert L.iir_forward(ctypes.byref(d), 8, 8, 8, None, 8, None, 8, tb - 1, 8, wb, None) == B.IIR_EWORKSPACE
+    assert L.iir_forward(ctypes.byref(d), 8, 8, 8, None, 8, None, 8, tb, 8, wb - 1, None) == B.IIR_EWORKSPACE
+    # per-sample mode is all-pole: b must be NULL
+    dp = B.make_desc(2, 100, 4, "df", B.IIR_F32, B.IIR_COEF_PER_SAMPLE)
+    if B.iir_tape_bytes(dp) > 0:
+        assert L.iir_forward(ctypes.byref(dp), 8, 8, 8, None, 8, None, 8, 1 << 40, 8, 1 << 40, None) == B.IIR_EINVAL
+    # per-sample TDF is a different filter and is not supported
+    dp.form = B.IIR_TDF2
+    assert B.iir_tape_bytes(dp) == 0
+
+
+def test_kernel_names_and_counters():
+    names = B.kernel_names()
+    assert "lti_fwd" in names and "lti_bwd" in names
+    assert B.iir_launch_count() >= 0
