@@ -150,11 +150,13 @@ class Problem:
         self.gzi = torch.empty(Bsz, M, dtype=td, device=dev)
         self.gb = None if self.b is None else torch.empty_like(self.b)
         self.ga = torch.empty_like(self.a)
-        self.desc = B.make_desc(Bsz, T, M, w["form"], td, mode)
+        # the workspace is cleared once; every completed call leaves it cleared
+        self.desc = B.make_desc(Bsz, T, M, w["form"], td, mode, flags=B.IIR_FLAG_WS_READY)
         self.tb = B.iir_tape_bytes(self.desc)
         self.wb = B.iir_workspace_bytes(self.desc)
         self.tape = torch.empty(self.tb, dtype=torch.uint8, device=dev)
         self.ws = torch.empty(self.wb, dtype=torch.uint8, device=dev)
+        B.iir_workspace_init(self.desc, self.ws, self.wb, torch.cuda.current_stream(dev))
         self.grad_buf = None if self.b is None else torch.empty(2 * (M + 1), dtype=td, device=dev)
 
     def set_bytes(self):

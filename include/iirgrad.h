@@ -17,8 +17,8 @@
  *   l.178            per-sample ("parameter-varying") all-pole DF:
  *                    y(n) = x(n) - sum_i a_i(n) y(n-i)   (IIR_COEF_PER_SAMPLE).
  *   l.121-130 (Eq.10) time parallelism by an associative scan over (A, z) tuples:
- *                    realised as a chunked scan with fp64 carries and single-pass
- *                    decoupled look-back.
+ *                    realised as a chunked scan with fp64 carries and a single-pass,
+ *                    deterministic hierarchical look-back across tiles.
  *
  * The loss whose gradient iir_backward returns is
  *   L = sum_{b,n} grad_y[b,n] * y[b,n] + sum_{b,i} grad_zf[b,i] * zf[b,i].
@@ -40,6 +40,7 @@
  *   - `tape` (iir_tape_bytes) is written by iir_forward and read by iir_backward; it
  *     must stay untouched in between.  `ws` (iir_workspace_bytes) is scratch used by
  *     both calls; one ws must not be used by two calls that may run concurrently.
+ *     Every completed call leaves ws in its initialised (zeroed-counter) state.
  *   - Gradient outputs are OVERWRITTEN, not accumulated.  SHARED-coefficient
  *     gradients are sums over the local batch (a multi-GPU driver all-reduces them).
  *   - Optional pointers may be NULL: zi (zeros), zf (not written), grad_y (zeros),
@@ -84,11 +85,23 @@ typedef struct {
     int32_t form;       /* iir_form_t                                              */
     int32_t dtype;      /* iir_dtype_t                                             */
     int32_t coef_mode;  /* iir_coef_mode_t                                         */
+    int32_t flags;      /* bitwise OR of iir_flags_t (0 = defaults)                */
 } iir_desc_t;
+
+typedef enum {
+    /* The workspace is known to be in its initialised state (fresh from
+     * iir_workspace_init, or left by a previous completed call: every call restores
+     * it), so iir_forward / iir_backward skip their cudaMemsetAsync of it.  Without
+     * this flag every call first clears the workspace's counters itself.           */
+    IIR_FLAG_WS_READY = 1
+} iir_flags_t;
 
 /* Bytes of the forward->backward tape / of the scratch workspace (0 on a bad desc). */
 size_t iir_tape_bytes(const iir_desc_t *desc);
 size_t iir_workspace_bytes(const iir_desc_t *desc);
+
+/* Clear a workspace (stream-ordered cudaMemsetAsync of its counter region). */
+iir_status_t iir_workspace_init(const iir_desc_t *desc, void *ws, size_t ws_bytes, iir_stream_t stream);
 
 /* Forward: y = filter(b, a, x; zi), zf = final state.  Eqs.1-5. */
 iir_status_t iir_forward(const iir_desc_t *desc, const void *b, const void *a, const void *x,

@@ -20,22 +20,24 @@ IIR_OK, IIR_EINVAL, IIR_EUNSUPPORTED, IIR_ECUDA, IIR_EWORKSPACE = range(5)
 IIR_DF2, IIR_TDF2 = 0, 1
 IIR_F32, IIR_F64 = 0, 1
 IIR_COEF_SHARED, IIR_COEF_PER_SEQ, IIR_COEF_PER_SAMPLE = 0, 1, 2
+IIR_FLAG_WS_READY = 1
 
 FORMS = {"df": IIR_DF2, "tdf": IIR_TDF2, IIR_DF2: IIR_DF2, IIR_TDF2: IIR_TDF2}
 DTYPES = {torch.float32: IIR_F32, torch.float64: IIR_F64}
 
-EXPORTS = ["iir_tape_bytes", "iir_workspace_bytes", "iir_forward", "iir_backward", "iir_last_error",
+EXPORTS = ["iir_tape_bytes", "iir_workspace_bytes", "iir_workspace_init", "iir_forward", "iir_backward", "iir_last_error",
            "iir_abi_version", "iir_launch_count", "iir_num_kernels", "iir_kernel_name",
            "iir_profile_enable", "iir_profile_reset", "iir_profile_query"]
 
 
 class Desc(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int64), ("length", ctypes.c_int64), ("order", ctypes.c_int32),
-                ("form", ctypes.c_int32), ("dtype", ctypes.c_int32), ("coef_mode", ctypes.c_int32)]
+                ("form", ctypes.c_int32), ("dtype", ctypes.c_int32), ("coef_mode", ctypes.c_int32),
+                ("flags", ctypes.c_int32)]
 
     def __repr__(self):
         return (f"Desc(batch={self.batch}, length={self.length}, order={self.order}, form={self.form}, "
-                f"dtype={self.dtype}, coef_mode={self.coef_mode})")
+                f"dtype={self.dtype}, coef_mode={self.coef_mode}, flags={self.flags})")
 
 
 class IIRError(RuntimeError):
@@ -62,6 +64,8 @@ def lib():
         L.iir_tape_bytes.argtypes = [dp]
         L.iir_workspace_bytes.restype = ctypes.c_size_t
         L.iir_workspace_bytes.argtypes = [dp]
+        L.iir_workspace_init.restype = ctypes.c_int
+        L.iir_workspace_init.argtypes = [dp, _vp, ctypes.c_size_t, _vp]
         L.iir_forward.restype = ctypes.c_int
         L.iir_forward.argtypes = [dp] + [_vp] * 7 + [ctypes.c_size_t, _vp, ctypes.c_size_t, _vp]
         L.iir_backward.restype = ctypes.c_int
@@ -93,9 +97,9 @@ def _check(status, what):
         raise IIRError(f"{what} failed with status {status}: {msg}")
 
 
-def make_desc(batch, length, order, form="tdf", dtype=torch.float32, coef_mode=IIR_COEF_SHARED) -> Desc:
+def make_desc(batch, length, order, form="tdf", dtype=torch.float32, coef_mode=IIR_COEF_SHARED, flags=0) -> Desc:
     return Desc(int(batch), int(length), int(order), FORMS[form],
-                DTYPES[dtype] if isinstance(dtype, torch.dtype) else int(dtype), int(coef_mode))
+                DTYPES[dtype] if isinstance(dtype, torch.dtype) else int(dtype), int(coef_mode), int(flags))
 
 
 def iir_tape_bytes(desc: Desc) -> int:
@@ -104,6 +108,11 @@ def iir_tape_bytes(desc: Desc) -> int:
 
 def iir_workspace_bytes(desc: Desc) -> int:
     return lib().iir_workspace_bytes(ctypes.byref(desc))
+
+
+def iir_workspace_init(desc, ws, ws_bytes, stream=None):
+    _check(lib().iir_workspace_init(ctypes.byref(desc), _ptr(ws), int(ws_bytes), _stream(stream)),
+           "iir_workspace_init")
 
 
 def _stream(stream):

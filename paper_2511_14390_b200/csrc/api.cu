@@ -26,7 +26,7 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
 }  // namespace iirg
 
 // ------------------------------------------------------- instrumentation ----
-static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "lti_finalize", "tv_fwd", "tv_bwd", "tv_fix"};
+static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_fwd", "tv_bwd", "tv_fix"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;
@@ -91,6 +91,11 @@ static iir_status_t check_desc(const iir_desc_t* d) {
     if (d->coef_mode != IIR_COEF_SHARED && d->coef_mode != IIR_COEF_PER_SEQ)
         return fail(IIR_EINVAL, "coef_mode must be SHARED, PER_SEQ or PER_SAMPLE");
     if (d->order < 1 || d->order > 8) return fail(IIR_EUNSUPPORTED, "order must be 1..8 for LTI filters");
+    const int64_t TS = tile_samples(d->dtype);
+    if ((d->length + TS - 1) / TS > (int64_t(1) << (5 * MAX_LEVELS)))
+        return fail(IIR_EUNSUPPORTED, "length exceeds 32^4 tiles per sequence");
+    if (d->batch * ((d->length + TS - 1) / TS) >= (int64_t(1) << 31))
+        return fail(IIR_EUNSUPPORTED, "batch x tiles exceeds 2^31 CTAs");
     return IIR_OK;
 }
 
@@ -102,13 +107,21 @@ static Layout layout(const iir_desc_t* d) {
     L.ntiles = (d->length + TS - 1) / TS;
     L.ntot = L.ntiles * d->batch;
     L.ncoef = d->coef_mode == IIR_COEF_SHARED ? 1 : d->batch;
+    L.nlev = 1;
+    while (L.nlev < MAX_LEVELS && (int64_t(1) << (5 * L.nlev)) < L.ntiles) ++L.nlev;
+    for (int l = 0; l < MAX_LEVELS; ++l) L.nblk[l] = l < L.nlev ? (L.ntiles + (int64_t(1) << (5 * l)) - 1) >> (5 * l) : 0;
+    const int64_t per_set = d->coef_mode == IIR_COEF_SHARED ? L.ntot : L.ntiles;
+    const int64_t ng_set = (per_set + 31) / 32;
+    L.ngroups = ng_set * L.ncoef;
     size_t o = 0;
-    L.ws_ticket = o; o += 256;
-    L.ws_flags = o; o += al256(L.ntot * 4);
+    L.ws_ticket = o; L.ws_done = o + 4; o += 256;
+    L.ws_gcnt = o; o += al256(L.ngroups * 4);
+    L.ws_scnt = o; o += al256(L.ncoef * 4);
+    for (int l = 0; l < L.nlev; ++l) { L.ws_flg[l] = o; o += al256(d->batch * L.nblk[l] * 4); }
     L.ws_clear = o;
-    L.ws_agg = o; o += al256(L.ntot * M * 8);
-    L.ws_incl = o; o += al256(L.ntot * M * 8);
+    for (int l = 0; l < L.nlev; ++l) { L.ws_agg[l] = o; o += al256(d->batch * L.nblk[l] * M * 8); }
     L.ws_part = o; o += al256(L.ntot * (2 * M + 1) * 8);
+    L.ws_part2 = o; o += al256(L.ngroups * (2 * M + 1) * 8);
     L.ws_bytes = o;
     o = 0;
     L.tp_tab = o; o += al256((size_t)L.ncoef * tab_size(M) * 8);
@@ -116,6 +129,19 @@ static Layout layout(const iir_desc_t* d) {
     if (d->form == IIR_DF2) o += al256((size_t)d->batch * d->length * dsize(d->dtype));
     L.tp_bytes = o;
     return L;
+}
+
+static CarryWs carry_ws(const Layout& L, char* w) {
+    CarryWs c{};
+    c.ticket = reinterpret_cast<unsigned*>(w + L.ws_ticket);
+    c.done = reinterpret_cast<unsigned*>(w + L.ws_done);
+    for (int l = 0; l < MAX_LEVELS; ++l) {
+        c.flg[l] = l < L.nlev ? reinterpret_cast<unsigned*>(w + L.ws_flg[l]) : nullptr;
+        c.agg[l] = l < L.nlev ? reinterpret_cast<double*>(w + L.ws_agg[l]) : nullptr;
+        c.nblk[l] = L.nblk[l];
+    }
+    c.nlev = L.nlev;
+    return c;
 }
 
 // -------------------------------------------------------------- kernels -----
@@ -152,6 +178,16 @@ size_t iir_workspace_bytes(const iir_desc_t* d) {
     return layout(d).ws_bytes;
 }
 
+iir_status_t iir_workspace_init(const iir_desc_t* d, void* ws, size_t ws_bytes, iir_stream_t stream) {
+    iir_status_t s = check_desc(d);
+    if (s != IIR_OK) return s;
+    const Layout L = layout(d);
+    if (ws == nullptr || ws_bytes < L.ws_bytes) return fail(IIR_EWORKSPACE, "workspace missing or too small");
+    cudaError_t e = cudaMemsetAsync(ws, 0, L.ws_clear, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return fail(IIR_ECUDA, std::string("memset: ") + cudaGetErrorString(e));
+    return IIR_OK;
+}
+
 iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, const void* x, const void* zi, void* y,
                          void* zf, void* tape, size_t tape_bytes, void* ws, size_t ws_bytes, iir_stream_t stream) {
     iir_status_t s = check_desc(d);
@@ -169,8 +205,10 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     char* w = static_cast<char*>(ws);
     char* t = static_cast<char*>(tape);
-    cudaError_t e = cudaMemsetAsync(w, 0, L.ws_clear, st);
-    if (e != cudaSuccess) return fail(IIR_ECUDA, std::string("memset: ") + cudaGetErrorString(e));
+    if (!(d->flags & IIR_FLAG_WS_READY)) {
+        cudaError_t e = cudaMemsetAsync(w, 0, L.ws_clear, st);
+        if (e != cudaSuccess) return fail(IIR_ECUDA, std::string("memset: ") + cudaGetErrorString(e));
+    }
     const int W = d->dtype == IIR_F64 ? 2 : 4;
     const bool vec = (d->length % W == 0) && aligned16(x) && aligned16(y) && aligned16(t + L.tp_u);
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) return tv_forward(d, L, a, x, zi, y, zf, t, w, vec, st);
@@ -178,14 +216,12 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     LtiCall c{};
     c.d = d; c.L = &L; c.st = st; c.is_fwd = true; c.b = b; c.a = a;
     LtiFwdArgs& fa = c.fa;
+    fa.b = b; fa.a = a; fa.coef_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : d->order + 1;
     fa.x = x; fa.zi = zi; fa.y = y; fa.zf = zf;
     fa.u = d->form == IIR_DF2 ? t + L.tp_u : nullptr;
     fa.tab = reinterpret_cast<const double*>(t + L.tp_tab);
     fa.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
-    fa.ticket = reinterpret_cast<unsigned*>(w + L.ws_ticket);
-    fa.flags = reinterpret_cast<unsigned*>(w + L.ws_flags);
-    fa.agg = reinterpret_cast<double*>(w + L.ws_agg);
-    fa.incl = reinterpret_cast<double*>(w + L.ws_incl);
+    fa.cw = carry_ws(L, w);
     fa.B = d->batch; fa.Tlen = d->length; fa.ntiles = (int)L.ntiles; fa.vec = vec;
     return run_lti_any(c);
 }
@@ -206,8 +242,10 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     char* w = static_cast<char*>(ws);
     const char* t = static_cast<const char*>(tape);
-    cudaError_t e = cudaMemsetAsync(w, 0, L.ws_clear, st);
-    if (e != cudaSuccess) return fail(IIR_ECUDA, std::string("memset: ") + cudaGetErrorString(e));
+    if (!(d->flags & IIR_FLAG_WS_READY)) {
+        cudaError_t e = cudaMemsetAsync(w, 0, L.ws_clear, st);
+        if (e != cudaSuccess) return fail(IIR_ECUDA, std::string("memset: ") + cudaGetErrorString(e));
+    }
     const int W = d->dtype == IIR_F64 ? 2 : 4;
     const bool vec = (d->length % W == 0) && aligned16(grad_y) && aligned16(x) && aligned16(y) &&
                      aligned16(grad_x) && aligned16(t + L.tp_u);
@@ -215,19 +253,21 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
         return tv_backward(d, L, grad_y, grad_zf, a, y, zi, t, grad_x, grad_a, grad_zi, w, vec, st);
 
     LtiCall c{};
-    c.d = d; c.L = &L; c.st = st; c.is_fwd = false; c.gb = grad_b; c.ga = grad_a;
+    c.d = d; c.L = &L; c.st = st; c.is_fwd = false;
     LtiBwdArgs& ba = c.ba;
     ba.gy = grad_y; ba.gzf = grad_zf; ba.x = x; ba.y = y;
     ba.u = d->form == IIR_DF2 ? t + L.tp_u : nullptr;
     ba.zi = zi; ba.gx = grad_x; ba.gzi = grad_zi;
+    ba.gb = grad_b; ba.ga = grad_a;
     ba.partial = reinterpret_cast<double*>(w + L.ws_part);
+    ba.partial2 = reinterpret_cast<double*>(w + L.ws_part2);
+    ba.gcnt = reinterpret_cast<unsigned*>(w + L.ws_gcnt);
+    ba.scnt = reinterpret_cast<unsigned*>(w + L.ws_scnt);
+    ba.ncoef = L.ncoef;
     ba.want_coef = (grad_b != nullptr || grad_a != nullptr);
     ba.tab = reinterpret_cast<const double*>(t + L.tp_tab);
     ba.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
-    ba.ticket = reinterpret_cast<unsigned*>(w + L.ws_ticket);
-    ba.flags = reinterpret_cast<unsigned*>(w + L.ws_flags);
-    ba.agg = reinterpret_cast<double*>(w + L.ws_agg);
-    ba.incl = reinterpret_cast<double*>(w + L.ws_incl);
+    ba.cw = carry_ws(L, w);
     ba.B = d->batch; ba.Tlen = d->length; ba.ntiles = (int)L.ntiles; ba.vec = vec;
     (void)b; (void)a;
     return run_lti_any(c);

@@ -8,7 +8,7 @@ namespace iirg {
 constexpr int NT = 128;          // threads per CTA (4 warps)
 constexpr int NW = NT / 32;      // warps per CTA
 constexpr int LOG_NW = 2;
-constexpr int KLB = 32;          // depth of the P_tile^k look-back power table
+
 constexpr int HALO = 8;          // u-history halo of the DF backward tile (>= M)
 
 // Samples per thread chunk (L) by data type; a tile is NT * L samples.
@@ -105,6 +105,37 @@ __device__ __forceinline__ void tile_store(T* __restrict__ row, const T* __restr
         for (int e = threadIdx.x; e < N; e += NT) {
             const int64_t pos = p0 + e;
             if (pos >= 0 && pos < Tlen) row[pos] = sm[pidx<T>(e)];
+        }
+    }
+}
+
+
+// ---- cp.async (Ampere+ LDGSTS; 16 B, L2 only, zero-fill when src_bytes = 0) ----
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, unsigned src_bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
+// Asynchronous version of tile_load (vector path via cp.async; the scalar path
+// is synchronous).  The caller commits / waits.
+template <typename T, int N>
+__device__ __forceinline__ void tile_load_async(T* __restrict__ sm, const T* __restrict__ row, int64_t p0,
+                                                int64_t Tlen, bool vec) {
+    constexpr int W = Vec<T>::W;
+    if (vec) {
+#pragma unroll 4
+        for (int q = threadIdx.x; q < N / W; q += NT) {
+            const int64_t pos = p0 + (int64_t)q * W;
+            const bool in = pos >= 0 && pos < Tlen;
+            cp_async16(sm + pidx<T>(q * W), in ? (const void*)(row + pos) : (const void*)row, in ? 16u : 0u);
+        }
+    } else {
+        for (int e = threadIdx.x; e < N; e += NT) {
+            const int64_t pos = p0 + e;
+            sm[pidx<T>(e)] = (pos >= 0 && pos < Tlen) ? row[pos] : T(0);
         }
     }
 }

@@ -13,7 +13,7 @@ namespace iirg {
 
 iir_status_t fail(iir_status_t st, const std::string& msg);
 
-enum Kind { K_LTI_PREP = 0, K_LTI_FWD, K_LTI_BWD, K_LTI_FIN, K_TV_FWD, K_TV_BWD, K_TV_FIX, K_NUM };
+enum Kind { K_LTI_PREP = 0, K_LTI_FWD, K_LTI_BWD, K_TV_FWD, K_TV_BWD, K_TV_FIX, K_NUM };
 
 // Launch bookkeeping: counts every kernel and (when profiling is on) brackets it
 // with CUDA events on its stream.
@@ -31,9 +31,14 @@ iir_status_t launch(int kind, cudaStream_t st, F&& f) {
 
 inline size_t al256(size_t n) { return (n + 255) / 256 * 256; }
 
+constexpr int MAX_LEVELS = 4;
 struct Layout {
-    int64_t ntiles = 0, ntot = 0, ncoef = 0;
-    size_t ws_ticket = 0, ws_flags = 0, ws_agg = 0, ws_incl = 0, ws_part = 0, ws_bytes = 0, ws_clear = 0;
+    int64_t ntiles = 0, ntot = 0, ncoef = 0, ngroups = 0;
+    int nlev = 0;
+    int64_t nblk[MAX_LEVELS] = {0, 0, 0, 0};
+    // workspace: counters + flags (cleared region), then payloads
+    size_t ws_ticket = 0, ws_done = 0, ws_gcnt = 0, ws_scnt = 0, ws_flg[MAX_LEVELS] = {0, 0, 0, 0};
+    size_t ws_clear = 0, ws_agg[MAX_LEVELS] = {0, 0, 0, 0}, ws_part = 0, ws_part2 = 0, ws_bytes = 0;
     size_t tp_tab = 0, tp_u = 0, tp_extra = 0, tp_bytes = 0;
 };
 

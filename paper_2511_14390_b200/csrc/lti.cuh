@@ -2,13 +2,13 @@
 // closed-form backward (arXiv 2511.14390, Eqs.4-9).
 //
 // Time-parallel formulation (Eq.10) as a chunked scan:
-//   * a tile of NT*L samples of one sequence per CTA; each thread owns a
+//   * a tile of TS = NT*L samples of one sequence per CTA; each thread owns a
 //     contiguous chunk of L samples and runs the recursion on it from a zero
 //     state (local pass), giving the chunk aggregate w (the z of Eq.10's tuple);
-//   * carries are combined in fp64 with the constant transition powers
-//     A_f^(L 2^d) (warp Kogge-Stone over shuffles), A_f^(32 L 2^d) (across the
-//     warps, shared memory), and A_f^(TS k) (across tiles: single-pass
-//     decoupled look-back on per-tile status words);
+//   * carries are combined in fp64 with constant transition powers: A_f^(L 2^d)
+//     (warp Kogge-Stone over shuffles), A_f^(32 L 2^d) (across the warps), and
+//     A_f^(k 32^l TS) (across tiles: a deterministic hierarchical look-back in
+//     base 32, see tile_carry);
 //   * each thread then re-runs its chunk from the exact carry-in state and
 //     emits outputs (and, in the backward pass, the gradient partial sums).
 // The backward pass is the same machine run in reverse time on the adjoint
@@ -19,17 +19,20 @@
 
 namespace iirg {
 
+constexpr int LEVELS = 4;          // hierarchical carry levels: ntiles <= 32^4 per sequence
+constexpr int PREP_THREADS = 256;
+
 // ---------------------------------------------------------------------------
-// fp64 power tables of one coefficient set (computed once per call on device).
+// fp64 power tables of one coefficient set (computed on device, once per call).
 template <int M> struct Tab {
     static constexpr int M2 = M * M;
-    static constexpr int PL = 0;                      // A_f^(L 2^d), d = 0..4      [d][i][j]
-    static constexpr int PLT = PL + 5 * M2;           // A_f^(L t),   t = 0..31     [i][j][t]
-    static constexpr int PW = PLT + 32 * M2;          // A_f^(32L 2^d), d < LOG_NW  [d][i][j]
-    static constexpr int PWT = PW + LOG_NW * M2;      // A_f^(32L w), w = 0..NW-1   [i][j][w]
-    static constexpr int PTK = PWT + NW * M2;         // A_f^(TS k), k = 1..KLB     [k-1][i][j]
-    static constexpr int COEF = PTK + KLB * M2;       // b'[0..M], a'[0..M], c[0..M-1]
-    static constexpr int A0 = COEF + 3 * M + 2;       // a0 (un-normalised)
+    static constexpr int PL = 0;                       // A_f^(L 2^d), d = 0..4          [d][i][j]
+    static constexpr int PLT = PL + 5 * M2;            // A_f^(L t),   t = 0..31         [i][j][t]
+    static constexpr int PW = PLT + 32 * M2;           // A_f^(32L 2^d), d < LOG_NW      [d][i][j]
+    static constexpr int PWT = PW + LOG_NW * M2;       // A_f^(32L w), w = 0..NW-1       [i][j][w]
+    static constexpr int PQ = PWT + NW * M2;           // A_f^(k 32^l TS), k = 0..31     [l][i][j][k]
+    static constexpr int COEF = PQ + LEVELS * 32 * M2; // b'[0..M], a'[0..M], c[0..M-1]
+    static constexpr int A0 = COEF + 3 * M + 2;        // a0 (un-normalised)
     static constexpr int SIZE = (A0 + 1 + 31) / 32 * 32;
 };
 
@@ -44,7 +47,7 @@ __device__ __forceinline__ void mv_acc(const double* __restrict__ P, const doubl
         acc[i] = s;
     }
 }
-// Same with a per-lane matrix stored element-major [i][j][stride] (coalesced).
+// Same with one matrix per index t, stored element-major [i][j][stride] (lanes coalesce).
 template <int M, bool TR>
 __device__ __forceinline__ void mv_acc_lane(const double* __restrict__ P, int stride, int t,
                                             const double (&v)[M], double (&acc)[M]) {
@@ -57,77 +60,120 @@ __device__ __forceinline__ void mv_acc_lane(const double* __restrict__ P, int st
     }
 }
 
+// Programmatic dependent launch (PTX griddepcontrol).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // ---------------------------------------------------------------------------
 // a1: coefficient prologue.  Normalise by a0, build A_f (DF: companion(a'),
-// TDF: its transpose) and the fp64 power tables.
+// TDF: its transpose) and every fp64 power table by batched
+// doubling (log depth): about 30 dependent matrix-product steps.
+template <int M> struct PrepSlots {
+    static constexpr int P1 = 0, PLT = 1 /* 33 */, YP = PLT + 33 /* 5 */, Q = YP + 5 /* LEVELS x 33 */;
+    static constexpr int N = Q + LEVELS * 33;
+    static constexpr size_t bytes() { return (size_t)N * M * M * sizeof(double); }
+};
+
 template <typename T, int M, int FORM>
-__global__ void __launch_bounds__(64) lti_prep_kernel(const T* __restrict__ b, const T* __restrict__ a,
-                                                     int64_t coef_stride, double* __restrict__ tab,
-                                                     int64_t tab_stride) {
+__global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restrict__ b, const T* __restrict__ a,
+                                                               int64_t coef_stride, double* __restrict__ tab,
+                                                               int64_t tab_stride, int nlev) {
+    // Let the dependent scan kernel start its prologue (tile loads, local pass);
+    // it waits for this grid's completion (griddepcontrol.wait) before reading tables.
+    pdl_launch_dependents();
     constexpr int L = Chunk<T>::L, M2 = M * M;
     using TB = Tab<M>;
-    __shared__ double Af[M2], X[M2], Y[M2], Z[M2], W[M2], bn[M + 1], an[M + 1];
+    using S = PrepSlots<M>;
+    extern __shared__ __align__(16) unsigned char prep_raw[];
+    double* mat = reinterpret_cast<double*>(prep_raw);
+    __shared__ double bn[M + 1], an[M + 1];
     const int set = blockIdx.x;
     const T* bb = b + set * coef_stride;
     const T* aa = a + set * coef_stride;
     double* tb = tab + set * tab_stride;
-    const int tid = threadIdx.x, i = tid / M, j = tid % M;
-    const bool act = tid < M2;
+    const int tid = threadIdx.x;
     if (tid <= M) {
         const double a0 = (double)aa[0];
         bn[tid] = (double)bb[tid] / a0;
         an[tid] = (double)aa[tid] / a0;
     }
     __syncthreads();
-    if (act) {
-        const double Aij = (i == 0) ? -an[j + 1] : (i == j + 1 ? 1.0 : 0.0);  // companion(a')
+    for (int e = tid; e < M2; e += PREP_THREADS) {
+        const int i = e / M, j = e % M;
+        const double Aij = (i == 0) ? -an[j + 1] : (i == j + 1 ? 1.0 : 0.0);  // companion(a'), row 0 = -a'
         const double Aji = (j == 0) ? -an[i + 1] : (j == i + 1 ? 1.0 : 0.0);
-        Af[tid] = (FORM == 0) ? Aij : Aji;
-        Z[tid] = (i == j) ? 1.0 : 0.0;
+        mat[S::P1 * M2 + e] = (FORM == 0) ? Aij : Aji;
+        const double id = (i == j) ? 1.0 : 0.0;
+        mat[(S::PLT + 0) * M2 + e] = id;
+        mat[(S::YP + 0) * M2 + e] = id;
+        for (int l = 0; l < LEVELS; ++l) mat[(S::Q + l * 33) * M2 + e] = id;
     }
     if (tid <= M) { tb[TB::COEF + tid] = bn[tid]; tb[TB::COEF + M + 1 + tid] = an[tid]; }
     if (tid < M) tb[TB::COEF + 2 * (M + 1) + tid] = bn[tid + 1] - an[tid + 1] * bn[0];
     if (tid == 0) tb[TB::A0] = (double)aa[0];
     __syncthreads();
-    auto mm = [&](double* dst, const double* A, const double* B) {
-        double s = 0.0;
-        if (act)
+    // batched product: for q < n: mat[dst(q)] = mat[lhs(q)] * mat[rhs(q)]
+    auto mm_batch = [&](int n, auto dst, auto lhs, auto rhs) {
+        constexpr int R = (16 * M2 + PREP_THREADS - 1) / PREP_THREADS;
+        double r[R];
 #pragma unroll
-            for (int k = 0; k < M; ++k) s = fma(A[i * M + k], B[k * M + j], s);
+        for (int s = 0; s < R; ++s) {
+            const int w = tid + s * PREP_THREADS;
+            r[s] = 0.0;
+            if (w < n * M2) {
+                const int q = w / M2, e = w % M2, i = e / M, j = e % M;
+                const double* A = mat + lhs(q) * M2;
+                const double* B = mat + rhs(q) * M2;
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < M; ++k) acc = fma(A[i * M + k], B[k * M + j], acc);
+                r[s] = acc;
+            }
+        }
         __syncthreads();
-        if (act) dst[tid] = s;
+#pragma unroll
+        for (int s = 0; s < R; ++s) {
+            const int w = tid + s * PREP_THREADS;
+            if (w < n * M2) mat[dst(w / M2) * M2 + (w % M2)] = r[s];
+        }
         __syncthreads();
     };
-    auto cp = [&](double* dst, const double* src) {
-        if (act) dst[tid] = src[tid];
+    // doubling: slot0 = X^0 and slot0+1 = X^1 known; fill slot0+2 .. slot0+2^nsteps
+    auto powers = [&](int slot0, int nsteps) {
+        for (int st = 0; st < nsteps; ++st) {
+            const int h = 1 << st;  // known X^0..X^h; X^(h+1+q) = X^h X^(1+q), q < h
+            mm_batch(h, [&](int q) { return slot0 + h + 1 + q; }, [&](int) { return slot0 + h; },
+                     [&](int q) { return slot0 + 1 + q; });
+        }
+    };
+    auto copy = [&](int dst, int src) {
+        for (int e = tid; e < M2; e += PREP_THREADS) mat[dst * M2 + e] = mat[src * M2 + e];
         __syncthreads();
     };
-    cp(X, Af);
-    for (int p = 1; p < L; p *= 2) mm(X, X, X);                 // X = A_f^L
-    cp(Y, X);
-    for (int d = 0; d < 5; ++d) {                               // A_f^(L 2^d)
-        if (act) tb[TB::PL + d * M2 + tid] = Y[tid];
-        mm(Y, Y, Y);
-    }                                                           // Y = A_f^(32 L)
-    for (int t = 0; t < 32; ++t) {                              // A_f^(L t)
-        if (act) tb[TB::PLT + tid * 32 + t] = Z[tid];
-        mm(Z, Z, X);
+    for (int p = 1; p < L; p *= 2)                                      // P1 = A_f^L
+        mm_batch(1, [&](int) { return S::P1; }, [&](int) { return S::P1; }, [&](int) { return S::P1; });
+    copy(S::PLT + 1, S::P1);
+    powers(S::PLT, 5);                                                  // A_f^(L t), t = 0..32
+    copy(S::YP + 1, S::PLT + 32);
+    powers(S::YP, LOG_NW);                                              // A_f^(32 L w), w = 0..NW
+    copy(S::Q + 1, S::YP + NW);                                         // A_f^TS
+    for (int l = 0; l < nlev; ++l) {                                    // A_f^(k 32^l TS), k = 0..32
+        powers(S::Q + l * 33, 5);
+        if (l + 1 < LEVELS) copy(S::Q + (l + 1) * 33 + 1, S::Q + l * 33 + 32);
     }
-    cp(W, Y);
-    for (int d = 0; d < LOG_NW; ++d) {                          // A_f^(32 L 2^d)
-        if (act) tb[TB::PW + d * M2 + tid] = W[tid];
-        mm(W, W, W);
-    }                                                           // W = A_f^(TS)
-    if (act) Z[tid] = (i == j) ? 1.0 : 0.0;
-    __syncthreads();
-    for (int w = 0; w < NW; ++w) {                              // A_f^(32 L w)
-        if (act) tb[TB::PWT + tid * NW + w] = Z[tid];
-        mm(Z, Z, Y);
+    // write out in the kernels' layouts
+    for (int e = tid; e < M2; e += PREP_THREADS) {
+        for (int d = 0; d < 5; ++d) tb[TB::PL + d * M2 + e] = mat[(S::PLT + (1 << d)) * M2 + e];
+        for (int d = 0; d < LOG_NW; ++d) tb[TB::PW + d * M2 + e] = mat[(S::YP + (1 << d)) * M2 + e];
+        for (int w = 0; w < NW; ++w) tb[TB::PWT + e * NW + w] = mat[(S::YP + w) * M2 + e];
     }
-    cp(Z, W);
-    for (int k = 1; k <= KLB; ++k) {                            // A_f^(TS k)
-        if (act) tb[TB::PTK + (k - 1) * M2 + tid] = Z[tid];
-        mm(Z, Z, W);
+    for (int w = tid; w < 32 * M2; w += PREP_THREADS) {
+        const int e = w / 32, t = w % 32;
+        tb[TB::PLT + w] = mat[(S::PLT + t) * M2 + e];
+    }
+    for (int w = tid; w < nlev * 32 * M2; w += PREP_THREADS) {
+        const int l = w / (32 * M2), r = w % (32 * M2), e = r / 32, k = r % 32;
+        tb[TB::PQ + w] = mat[(S::Q + l * 33 + k) * M2 + e];
     }
 }
 
@@ -184,21 +230,43 @@ __device__ __forceinline__ T adj_df_step(T (&d)[M], T dy, const T (&bc)[M + 1], 
 }
 
 // ---------------------------------------------------------------------------
+// Grid-level carry bookkeeping (workspace pointers), shared by fwd and bwd.
+struct CarryWs {
+    unsigned* ticket;            // tile ticket counter
+    unsigned* done;              // CTAs finished (the last one cleans the workspace)
+    unsigned* flg[LEVELS];       // readiness of each level-l block aggregate
+    double* agg[LEVELS];         // level-l block aggregates [seq][block][M]
+    int64_t nblk[LEVELS];        // blocks per sequence at level l (ceil(ntiles / 32^l))
+    int nlev;                    // levels in use
+};
+
 struct LtiFwdArgs {
-    const void* x; const void* zi; void* y; void* zf; void* u;   // u: DF tape signal
+    const void* b; const void* a; int64_t coef_stride;           // raw coefficients (local pass)
+    const void* x; const void* zi; void* y; void* zf; void* u;    // u: DF tape signal
     const double* tab; int64_t tab_stride;                        // 0 for SHARED
-    unsigned* ticket; unsigned* flags; double* agg; double* incl;
+    CarryWs cw;
     int64_t B, Tlen; int ntiles; int vec;
 };
 
 struct LtiBwdArgs {
     const void* gy; const void* gzf; const void* x; const void* y; const void* u; const void* zi;
-    void* gx; void* gzi; double* partial; int want_coef;
+    void* gx; void* gzi; void* gb; void* ga; int want_coef;
+    double* partial; double* partial2; unsigned* gcnt; unsigned* scnt;   // fused finalize
+    int64_t ncoef;
     const double* tab; int64_t tab_stride;
-    unsigned* ticket; unsigned* flags; double* agg; double* incl;
+    CarryWs cw;
     int64_t B, Tlen; int ntiles; int vec;
 };
 
+// Normalised coefficients in T, straight from the caller's b, a (the same
+// rounding as the prologue's fp64 b/a0, a/a0 cast to T).
+template <typename T, int M>
+__device__ __forceinline__ void raw_coefs(const T* __restrict__ b, const T* __restrict__ a, T (&bc)[M + 1],
+                                          T (&ac)[M + 1]) {
+    const double a0 = (double)__ldg(a);
+#pragma unroll
+    for (int k = 0; k <= M; ++k) { bc[k] = (T)((double)__ldg(b + k) / a0); ac[k] = (T)((double)__ldg(a + k) / a0); }
+}
 template <typename T, int M>
 __device__ __forceinline__ void load_coefs(const double* __restrict__ tb, T (&bc)[M + 1], T (&ac)[M + 1], T (&cc)[M]) {
     using TB = Tab<M>;
@@ -223,16 +291,40 @@ __device__ __forceinline__ void warp_scan(const double* __restrict__ tb, int lan
     }
 }
 
+template <int M>
+__device__ __forceinline__ void warp_sum(double (&v)[M]) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < M; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+}
+
+template <int M>
+__device__ __forceinline__ void publish(unsigned* flag, double* dst, const double (&v)[M], int lane) {
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) __stcg(dst + i, v[i]);
+        st_release(flag, 1u);
+    }
+}
+
 // Block + grid carry propagation, executed by warp 0 of the CTA.
 //   s_agg[w]: warp-local aggregates (zero-start prefix at the end of warp w).
 //   Produces s_xw[w]: the exact state entering warp w's first chunk.
-//   Decoupled look-back over this sequence's tiles (status 1 = aggregate,
-//   2 = inclusive prefix), tiles ordered by ticket so predecessors are running.
+// Grid level: tile j (scan order within its sequence) has base-32 digits d_l.
+// With AGG^(0) = tile aggregates (tile 0's includes the initial state X0),
+// AGG^(l+1)_blk = sum_{d<32} Q_l^(31-d) AGG^(l)_{32 blk + d}, Q_l = A_f^(32^l TS):
+//   T_l = sum_{d < d_l} Q_l^(d_l - 1 - d) AGG^(l)_{(j >> 5l) - d_l + d}
+//   X_j = T_0 + Q_0^d_0 (T_1 + Q_1^d_1 (T_2 + ...))
+// Each T_l is one lane-parallel round (lane d reads one aggregate) and a fixed
+// butterfly sum, so the result is bitwise deterministic and no tile ever waits
+// on a serial chain of inclusive prefixes.  The last tile of a level-l block
+// publishes AGG^(l+1) = Q_l T_l + AGG^(l)_own.
 template <int M, bool TR>
-__device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int lane,
-                                           double (*s_agg)[M], double (*s_xw)[M],
-                                           int jt, int64_t flat0, const double (&X0)[M],
-                                           unsigned* flags, double* agg, double* incl, bool publish_incl) {
+__device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int lane, double (*s_agg)[M],
+                                           double (*s_xw)[M], int jt, int64_t seq, const double (&X0)[M],
+                                           const CarryWs& cw) {
+    __shared__ double s_T[LEVELS][M];
     using TB = Tab<M>;
     constexpr int M2 = M * M;
     double J[M];
@@ -253,48 +345,71 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
         if (lane == 0) Jex[i] = 0.0;
         G[i] = shfl_d(J[i], NW - 1);           // tile aggregate (all lanes)
     }
-    const int64_t me = flat0 + jt;
-    double X[M];                               // exclusive prefix = state entering this tile
-    if (jt == 0) {
+    double X[M];                               // state entering this tile
 #pragma unroll
-        for (int i = 0; i < M; ++i) X[i] = X0[i];
-    } else {
-        if (lane == 0) {
+    for (int i = 0; i < M; ++i) X[i] = X0[i];
+    if (jt == 0) mv_acc_lane<M, TR>(tb + TB::PQ, 32, 1, X0, G);   // tile 0 carries the initial state
+    publish<M>(cw.flg[0] + seq * cw.nblk[0] + jt, cw.agg[0] + (seq * cw.nblk[0] + jt) * M, G, lane);
+    if (jt > 0) {
+        // T_l (one lane-parallel round per level), kept in shared memory to spare registers
+        int dl[LEVELS];
 #pragma unroll
-            for (int i = 0; i < M; ++i) __stcg(agg + me * M + i, G[i]);
-            st_release(flags + me, 1u);
-        }
+        for (int l = 0; l < LEVELS; ++l) {
+            dl[l] = (jt >> (5 * l)) & 31;
+            double Tv[M];
 #pragma unroll
-        for (int i = 0; i < M; ++i) X[i] = 0.0;
-        int k = 0;                             // multiplier A_f^(TS k) of the next element
-        for (int jj = jt - 1;; --jj, ++k) {
-            unsigned f = 0;
+            for (int i = 0; i < M; ++i) Tv[i] = 0.0;
+            if (l < cw.nlev && dl[l] > 0) {
+                const int64_t base = seq * cw.nblk[l] + (jt >> (5 * l)) - dl[l];
+                if (lane < dl[l]) {
+                    const unsigned* f = cw.flg[l] + base + lane;
+                    while (ld_acquire(f) == 0u) { }
+                    const double* src = cw.agg[l] + (base + lane) * M;
+                    double v[M];
+#pragma unroll
+                    for (int i = 0; i < M; ++i) v[i] = __ldcg(src + i);
+                    mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, dl[l] - 1 - lane, v, Tv);
+                }
+                warp_sum<M>(Tv);
+            }
             if (lane == 0) {
-                const unsigned need = (k >= KLB) ? 2u : 1u;
-                do { f = ld_acquire(flags + flat0 + jj); } while (f < need);
-            }
-            f = __shfl_sync(0xffffffffu, f, 0);
-            const double* src = (f == 2u ? incl : agg) + (flat0 + jj) * M;
-            double val[M];
 #pragma unroll
-            for (int i = 0; i < M; ++i) val[i] = __ldcg(src + i);
-            if (k == 0) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) X[i] += val[i];
-            } else {
-                mv_acc<M, TR>(tb + TB::PTK + (k - 1) * M2, val, X);
+                for (int i = 0; i < M; ++i) s_T[l][i] = Tv[i];
             }
-            if (f == 2u) break;
         }
-    }
-    if (publish_incl && lane == 0) {
-        double I[M];
+        __syncwarp();
+        // X = T_0 + Q_0^d0 (T_1 + Q_1^d1 (T_2 + Q_2^d2 T_3))
+        double R[M];
 #pragma unroll
-        for (int i = 0; i < M; ++i) I[i] = G[i];
-        mv_acc<M, TR>(tb + TB::PTK, X, I);     // I = A_f^TS X + G
+        for (int i = 0; i < M; ++i) R[i] = 0.0;
 #pragma unroll
-        for (int i = 0; i < M; ++i) __stcg(incl + me * M + i, I[i]);
-        st_release(flags + me, 2u);
+        for (int l = LEVELS - 1; l >= 0; --l) {
+            if (l < cw.nlev) {
+                double R2[M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) R2[i] = s_T[l][i];
+                if (l + 1 < cw.nlev) mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, dl[l], R, R2);
+#pragma unroll
+                for (int i = 0; i < M; ++i) R[i] = R2[i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < M; ++i) X[i] = R[i];
+        // publish the completed higher-level blocks this tile closes
+        if (dl[0] == 31) {
+            double Own[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) Own[i] = G[i];
+            for (int l = 0; l + 1 < cw.nlev; ++l) {
+                if (dl[l] != 31) break;
+                double Tv[M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) Tv[i] = s_T[l][i];
+                mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, 1, Tv, Own);   // Own = Q_l T_l + Own
+                const int64_t bi = seq * cw.nblk[l + 1] + (jt >> (5 * (l + 1)));
+                publish<M>(cw.flg[l + 1] + bi, cw.agg[l + 1] + bi * M, Own, lane);
+            }
+        }
     }
     if (lane < NW) {                           // state entering warp `lane`
         double xw[M];
@@ -306,8 +421,26 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
     }
 }
 
+// The last CTA of the grid restores the workspace to its zero state, so the
+// next call on the same (stream-ordered) workspace needs no memset.
+__device__ __forceinline__ void ws_cleanup(const CarryWs& cw, int64_t B, unsigned ntot) {
+    __shared__ unsigned s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = (atomicAdd(cw.done, 1u) == ntot - 1u) ? 1u : 0u;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        for (int l = 0; l < cw.nlev; ++l)
+            for (int64_t i = threadIdx.x; i < B * cw.nblk[l]; i += blockDim.x) cw.flg[l][i] = 0u;
+        if (threadIdx.x == 0) { *cw.ticket = 0u; *cw.done = 0u; }
+    }
+}
+
 // ---------------------------------------------------------------------------
-// Forward: a2-a4.  One CTA per tile (NT*L samples of one sequence).
+// Forward: a2-a4.  One CTA per tile (TS samples of one sequence).
 template <typename T, int M, int FORM>
 __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
     constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
@@ -321,18 +454,20 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
     __shared__ unsigned s_ticket;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_ticket = atomicAdd(p.ticket, 1u);
+    if (tid == 0) s_ticket = atomicAdd(p.cw.ticket, 1u);
     __syncthreads();
     const unsigned tk = s_ticket;
     const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
     const int jt = (int)(tk / (unsigned long long)p.B);
     const int64_t p0 = (int64_t)jt * TS;
     const T* xrow = static_cast<const T*>(p.x) + seq * p.Tlen;
-    const double* tb = p.tab + seq * p.tab_stride;
 
-    tile_load<T, TS>(xs, xrow, p0, p.Tlen, p.vec);
-    T bc[M + 1], ac[M + 1], cc[M];
-    load_coefs<T, M>(tb, bc, ac, cc);
+    tile_load_async<T, TS>(xs, xrow, p0, p.Tlen, p.vec);
+    cp_async_commit();
+    T bc[M + 1], ac[M + 1];
+    raw_coefs<T, M>(static_cast<const T*>(p.b) + seq * p.coef_stride,
+                    static_cast<const T*>(p.a) + seq * p.coef_stride, bc, ac);
+    cp_async_wait<0>();
     __syncthreads();
 
     // a2: local pass from the zero state over this thread's chunk.
@@ -346,7 +481,9 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
 #pragma unroll
         for (int e = 0; e < W; ++e) { T du; fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, du); }
     }
-    // a3: carries in fp64.
+    // a3: carries in fp64 (the power tables come from the prologue: wait for it).
+    pdl_wait();
+    const double* tb = p.tab + seq * p.tab_stride;
     double S[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) S[i] = (double)v[i];
@@ -364,8 +501,7 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
         const T* zi = static_cast<const T*>(p.zi);
 #pragma unroll
         for (int i = 0; i < M; ++i) X0[i] = (zi != nullptr && jt == 0) ? (double)zi[seq * M + i] : 0.0;
-        tile_carry<M, false>(tb, lane, s_agg, s_xw, jt, seq * (int64_t)p.ntiles, X0, p.flags, p.agg, p.incl,
-                             jt + 1 < p.ntiles);
+        tile_carry<M, false>(tb, lane, s_agg, s_xw, jt, seq, X0, p.cw);
     }
     __syncthreads();
     // state entering this thread's chunk: E + A_f^(L lane) x_warp
@@ -414,10 +550,50 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
         T* urow = static_cast<T*>(p.u) + seq * p.Tlen;
         tile_store<T, TS>(urow, us, p0, p.Tlen, p.vec);
     }
+    ws_cleanup(p.cw, p.B, (unsigned)(p.B * p.ntiles));
 }
 
 // ---------------------------------------------------------------------------
-// Backward: a5-a7.  Tiles are aligned to the END of each sequence and processed
+// a8: gradient finalize, fused into the backward kernel.  Fixed-order fp64 sum
+// of the per-tile partials (groups of 32 tiles, then the groups; over the
+// whole local batch for SHARED), then the chain rule from the state-space sums
+// to (b', a') and the a0 un-normalisation:
+//   TDF: G = [Gx(M), Gy(M), Gd]:  gb'_k = Gx[k-1], ga'_k = -Gy[k-1],
+//        gb'_0 = Gd - sum_k a'_k Gx[k-1]            (Eqs.6,9 with C_f = e1)
+//   DF : G = [Gb(0..M), Ga(1..M)]:  gb'_k = Gb[k],  ga'_k = -Ga[k]
+//   gb = gb'/a0;  ga_k = ga'_k/a0 (k>=1);  ga_0 = -(b'.gb' + a'.ga')/a0.
+template <typename T, int M, int FORM>
+__device__ __forceinline__ void chain_rule(const double* __restrict__ G, const double* __restrict__ tb, T* gb, T* ga) {
+    using TB = Tab<M>;
+    const double* bn = tb + TB::COEF;
+    const double* an = tb + TB::COEF + M + 1;
+    const double a0 = tb[TB::A0];
+    double gbn[M + 1], gan[M + 1];
+    gan[0] = 0.0;
+    if constexpr (FORM == 1) {
+        gbn[0] = G[2 * M];
+        for (int k = 1; k <= M; ++k) {
+            gbn[k] = G[k - 1];
+            gan[k] = -G[M + k - 1];
+            gbn[0] -= an[k] * G[k - 1];
+        }
+    } else {
+        for (int k = 0; k <= M; ++k) gbn[k] = G[k];
+        for (int k = 1; k <= M; ++k) gan[k] = -G[M + k];
+    }
+    double s = 0.0;
+    for (int k = 0; k <= M; ++k) s += bn[k] * gbn[k];
+    for (int k = 1; k <= M; ++k) s += an[k] * gan[k];
+    if (gb != nullptr)
+        for (int k = 0; k <= M; ++k) gb[k] = (T)(gbn[k] / a0);
+    if (ga != nullptr) {
+        ga[0] = (T)(-s / a0);
+        for (int k = 1; k <= M; ++k) ga[k] = (T)(gan[k] / a0);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Backward: a5-a8.  Tiles are aligned to the END of each sequence and processed
 // last to first; inside a tile thread t owns chunk NT-1-t, walked backwards.
 // TDF: smem dy | x | y.  DF: smem dy | u (with HALO samples of history).
 template <typename T, int M, int FORM>
@@ -433,10 +609,11 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
     __shared__ double s_agg[NW][M];
     __shared__ double s_xw[NW][M];
     __shared__ double s_red[NW][NG];
-    __shared__ unsigned s_ticket;
+    __shared__ double s_G[NG];
+    __shared__ unsigned s_ticket, s_fin;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_ticket = atomicAdd(p.ticket, 1u);
+    if (tid == 0) s_ticket = atomicAdd(p.cw.ticket, 1u);
     __syncthreads();
     const unsigned tk = s_ticket;
     const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
@@ -446,26 +623,24 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
     const double* tb = p.tab + seq * p.tab_stride;
     const int64_t roff = seq * p.Tlen;
 
-    if (p.gy != nullptr) tile_load<T, TS>(dys, static_cast<const T*>(p.gy) + roff, p0, p.Tlen, p.vec);
+    // group 0: dy;  group 1: x, y (TDF) or u (DF)
+    if (p.gy != nullptr) tile_load_async<T, TS>(dys, static_cast<const T*>(p.gy) + roff, p0, p.Tlen, p.vec);
     else for (int e = tid; e < TS; e += NT) dys[pidx<T>(e)] = T(0);
+    cp_async_commit();
     if constexpr (FORM == 1) {
-        tile_load<T, TS>(s2, static_cast<const T*>(p.x) + roff, p0, p.Tlen, p.vec);
-        tile_load<T, TS>(s3, static_cast<const T*>(p.y) + roff, p0, p.Tlen, p.vec);
-    }
-    T bc[M + 1], ac[M + 1], cc[M];
-    load_coefs<T, M>(tb, bc, ac, cc);
-    __syncthreads();
-    if constexpr (FORM == 0) {
+        tile_load_async<T, TS>(s2, static_cast<const T*>(p.x) + roff, p0, p.Tlen, p.vec);
+        tile_load_async<T, TS>(s3, static_cast<const T*>(p.y) + roff, p0, p.Tlen, p.vec);
+    } else {
+        // u(p0 - HALO .. p0 + TS) -> s2[pidx(e + HALO)]; u(-k) = zi[k-1] (DF state).
         const T* urow = static_cast<const T*>(p.u) + roff;
         const T* zi = static_cast<const T*>(p.zi);
-        // u(p0 - HALO .. p0 + TS) -> s2[pidx(e + HALO)]; u(-k) = zi[k-1] (DF state).
         for (int q = tid; q < (TS + HALO) / W; q += NT) {
             const int e = q * W - HALO;
             const int64_t pos = p0 + e;
-            V val;
             if (p.vec && pos >= 0 && pos + W <= p.Tlen) {
-                val = ldg_stream(reinterpret_cast<const V*>(urow + pos));
+                cp_async16(s2 + pidx<T>(e + HALO), urow + pos, 16u);
             } else {
+                V val;
 #pragma unroll
                 for (int r = 0; r < W; ++r) {
                     const int64_t pr = pos + r;
@@ -474,11 +649,15 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
                     else if (pr < 0 && pr >= -M && zi != nullptr) s = zi[seq * M + (-pr - 1)];
                     vset(val, r, s);
                 }
+                *reinterpret_cast<V*>(s2 + pidx<T>(e + HALO)) = val;
             }
-            *reinterpret_cast<V*>(s2 + pidx<T>(e + HALO)) = val;
         }
-        __syncthreads();
     }
+    cp_async_commit();
+    T bc[M + 1], ac[M + 1], cc[M];
+    load_coefs<T, M>(tb, bc, ac, cc);
+    cp_async_wait<1>();
+    __syncthreads();
 
     const int c = NT - 1 - tid;          // chunk index within the tile (time order)
     const int s0 = c * L;
@@ -513,8 +692,7 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
         const T* gzf = static_cast<const T*>(p.gzf);
 #pragma unroll
         for (int i = 0; i < M; ++i) X0[i] = (gzf != nullptr && jr == 0) ? (double)gzf[seq * M + i] : 0.0;
-        tile_carry<M, true>(tb, lane, s_agg, s_xw, jr, seq * (int64_t)p.ntiles, X0, p.flags, p.agg, p.incl,
-                            jr + 1 < p.ntiles);
+        tile_carry<M, true>(tb, lane, s_agg, s_xw, jr, seq, X0, p.cw);
     }
     __syncthreads();
     {
@@ -523,11 +701,11 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
         for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
         mv_acc_lane<M, true>(tb + TB::PLT, 32, lane, xw, E);
     }
-#pragma unroll
-    for (int i = 0; i < M; ++i) d[i] = (T)E[i];
     T din[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) din[i] = d[i];
+    for (int i = 0; i < M; ++i) { din[i] = (T)E[i]; d[i] = din[i]; }
+    cp_async_wait<0>();
+    __syncthreads();
 
     // grad_zi = dz(-1) (Eq.9, A.3): the thread whose chunk holds n = 0 walks down
     // to it before the emit pass overwrites dy with dx.
@@ -585,7 +763,7 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
         }
         *reinterpret_cast<V*>(dys + pidx<T>(s0 + g * W)) = dv;   // dx in place
     }
-    // block reduction of the partial sums (fp64, fixed order) -> per-tile partial
+    // warp reduction of the partial sums (fp64, fixed order)
     if (p.want_coef) {
 #pragma unroll
         for (int k = 0; k < NG; ++k) {
@@ -596,73 +774,61 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
         }
     }
     __syncthreads();
-    if (p.want_coef && tid < NG) {
-        double s = 0.0;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) s += s_red[w][tid];
-        p.partial[(seq * (int64_t)p.ntiles + jt) * NG + tid] = s;
-    }
     if (p.gx != nullptr) tile_store<T, TS>(static_cast<T*>(p.gx) + roff, dys, p0, p.Tlen, p.vec);
-}
 
-// ---------------------------------------------------------------------------
-// a8: gradient finalize.  One CTA per coefficient set: fixed-order fp64 sum of
-// the per-tile partials (over the whole local batch for SHARED), then the
-// chain rule from the state-space sums to (b', a') and the a0 un-normalisation.
-//   TDF: G = [Gx(M), Gy(M), Gd]:  gb'_k = Gx[k-1], ga'_k = -Gy[k-1],
-//        gb'_0 = Gd - sum_k a'_k Gx[k-1]            (Eqs.6,9 with C_f = e1)
-//   DF : G = [Gb(0..M), Ga(1..M)]:  gb'_k = Gb[k],  ga'_k = -Ga[k]
-//   gb = gb'/a0;  ga_k = ga'_k/a0 (k>=1);  ga_0 = -(b'.gb' + a'.ga')/a0.
-template <typename T, int M, int FORM>
-__global__ void __launch_bounds__(256) lti_finalize_kernel(const double* __restrict__ partial, int64_t tiles_per_set,
-                                                           const double* __restrict__ tab, int64_t tab_stride,
-                                                           T* __restrict__ gb, T* __restrict__ ga) {
-    constexpr int NG = 2 * M + 1;
-    using TB = Tab<M>;
-    __shared__ double red[256];
-    __shared__ double Gs[NG];
-    const int set = blockIdx.x, tid = threadIdx.x;
-    const double* part = partial + (int64_t)set * tiles_per_set * NG;
-    for (int k = 0; k < NG; ++k) {
-        double s = 0.0;
-        for (int64_t t = tid; t < tiles_per_set; t += 256) s += part[t * NG + k];
-        red[tid] = s;
-        __syncthreads();
-        for (int o = 128; o >= 1; o >>= 1) {
-            if (tid < o) red[tid] += red[tid + o];
-            __syncthreads();
+    if (p.want_coef) {
+        // fused a8: group of 32 tiles -> group sum; last group of the set -> chain rule.
+        const bool shared = p.ncoef == 1;
+        const int64_t per_set = shared ? p.B * p.ntiles : p.ntiles;
+        const int64_t set = shared ? 0 : seq;
+        const int64_t li = shared ? seq * p.ntiles + jt : jt;          // index within the set
+        const int64_t gi = li >> 5;
+        const int64_t ngroups = (per_set + 31) >> 5;
+        const int gsize = (int)min((int64_t)32, per_set - (gi << 5));
+        double* part = p.partial + set * per_set * NG;
+        double* part2 = p.partial2 + set * ngroups * NG;
+        if (tid < NG) {
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) s += s_red[w][tid];
+            __stcg(part + li * NG + tid, s);
+            __threadfence();
         }
-        if (tid == 0) Gs[k] = red[0];
         __syncthreads();
-    }
-    if (tid == 0) {
-        const double* tb = tab + set * tab_stride + TB::COEF;
-        const double* bn = tb;
-        const double* an = tb + M + 1;
-        double gbn[M + 1], gan[M + 1];
-        gan[0] = 0.0;
-        if (FORM == 1) {
-            gbn[0] = Gs[2 * M];
-            for (int k = 1; k <= M; ++k) {
-                gbn[k] = Gs[k - 1];
-                gan[k] = -Gs[M + k - 1];
-                gbn[0] -= an[k] * Gs[k - 1];
+        if (tid == 0) s_fin = (atomicAdd(p.gcnt + set * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
+        __syncthreads();
+        if (s_fin) {                                   // last tile of its group
+            __threadfence();
+            if (tid < NG) {
+                double s = 0.0;
+                for (int t = 0; t < gsize; ++t) s += __ldcg(part + ((gi << 5) + t) * NG + tid);
+                __stcg(part2 + gi * NG + tid, s);
+                __threadfence();
             }
-        } else {
-            for (int k = 0; k <= M; ++k) gbn[k] = Gs[k];
-            for (int k = 1; k <= M; ++k) gan[k] = -Gs[M + k];
-        }
-        const double a0 = tab[set * tab_stride + TB::A0];
-        double s = 0.0;
-        for (int k = 0; k <= M; ++k) s += bn[k] * gbn[k];
-        for (int k = 1; k <= M; ++k) s += an[k] * gan[k];
-        if (gb != nullptr)
-            for (int k = 0; k <= M; ++k) gb[set * (M + 1) + k] = (T)(gbn[k] / a0);
-        if (ga != nullptr) {
-            ga[set * (M + 1)] = (T)(-s / a0);
-            for (int k = 1; k <= M; ++k) ga[set * (M + 1) + k] = (T)(gan[k] / a0);
+            __syncthreads();
+            if (tid == 0) {
+                p.gcnt[set * ngroups + gi] = 0u;
+                s_fin = (atomicAdd(p.scnt + set, 1u) == (unsigned)ngroups - 1u) ? 2u : 0u;
+            }
+            __syncthreads();
+            if (s_fin == 2u) {                          // last group of the set
+                __threadfence();
+                if (tid < NG) {
+                    double s = 0.0;
+                    for (int64_t g2 = 0; g2 < ngroups; ++g2) s += __ldcg(part2 + g2 * NG + tid);
+                    s_G[tid] = s;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    chain_rule<T, M, FORM>(s_G, tb,
+                                           p.gb == nullptr ? nullptr : static_cast<T*>(p.gb) + set * (M + 1),
+                                           p.ga == nullptr ? nullptr : static_cast<T*>(p.ga) + set * (M + 1));
+                    p.scnt[set] = 0u;
+                }
+            }
         }
     }
+    ws_cleanup(p.cw, p.B, (unsigned)(p.B * p.ntiles));
 }
 
 }  // namespace iirg

@@ -20,17 +20,32 @@ struct LtiOps {
     }
     static iir_status_t prep(const iir_desc_t* d, const Layout& L, const void* b, const void* a, double* tab,
                              cudaStream_t st) {
+        static std::once_flag once;
+        std::call_once(once, [] { set_smem(lti_prep_kernel<T, M, FORM>, PrepSlots<M>::bytes()); });
         const int64_t cstride = d->coef_mode == IIR_COEF_SHARED ? 0 : (M + 1);
         return launch(K_LTI_PREP, st, [&] {
-            lti_prep_kernel<T, M, FORM><<<(unsigned)L.ncoef, 64, 0, st>>>(
-                static_cast<const T*>(b), static_cast<const T*>(a), cstride, tab, Tab<M>::SIZE);
+            lti_prep_kernel<T, M, FORM><<<(unsigned)L.ncoef, PREP_THREADS, PrepSlots<M>::bytes(), st>>>(
+                static_cast<const T*>(b), static_cast<const T*>(a), cstride, tab, Tab<M>::SIZE, L.nlev);
         });
     }
+    // The scan kernel is launched as a programmatic dependent of the prologue: its
+    // tile loads and local pass overlap the prologue; it waits (griddepcontrol.wait)
+    // before touching the power tables.
     static iir_status_t fwd(const iir_desc_t* d, const Layout& L, const LtiFwdArgs& args, cudaStream_t st) {
         static std::once_flag once;
         std::call_once(once, [] { set_smem(lti_fwd_kernel<T, M, FORM>, fwd_smem()); });
         return launch(K_LTI_FWD, st, [&] {
-            lti_fwd_kernel<T, M, FORM><<<(unsigned)L.ntot, NT, fwd_smem(), st>>>(args);
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((unsigned)L.ntot);
+            cfg.blockDim = dim3(NT);
+            cfg.dynamicSmemBytes = fwd_smem();
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            cudaLaunchKernelEx(&cfg, lti_fwd_kernel<T, M, FORM>, args);
         });
     }
     static iir_status_t bwd(const iir_desc_t* d, const Layout& L, const LtiBwdArgs& args, cudaStream_t st) {
@@ -40,15 +55,6 @@ struct LtiOps {
             lti_bwd_kernel<T, M, FORM><<<(unsigned)L.ntot, NT, bwd_smem(), st>>>(args);
         });
     }
-    static iir_status_t fin(const iir_desc_t* d, const Layout& L, const double* part, const double* tab, void* gb,
-                            void* ga, cudaStream_t st) {
-        const int64_t per_set = d->coef_mode == IIR_COEF_SHARED ? L.ntot : L.ntiles;
-        const int64_t tstride = d->coef_mode == IIR_COEF_SHARED ? 0 : Tab<M>::SIZE;
-        return launch(K_LTI_FIN, st, [&] {
-            lti_finalize_kernel<T, M, FORM><<<(unsigned)L.ncoef, 256, 0, st>>>(
-                part, per_set, tab, tstride, static_cast<T*>(gb), static_cast<T*>(ga));
-        });
-    }
 };
 
 struct LtiCall {
@@ -56,7 +62,7 @@ struct LtiCall {
     // forward
     const void *b, *a; LtiFwdArgs fa;
     // backward
-    LtiBwdArgs ba; void *gb, *ga;
+    LtiBwdArgs ba;
     bool is_fwd;
 };
 
@@ -68,9 +74,7 @@ inline iir_status_t run_lti(LtiCall& c) {
         if (s != IIR_OK) return s;
         return Ops::fwd(c.d, *c.L, c.fa, c.st);
     }
-    iir_status_t s = Ops::bwd(c.d, *c.L, c.ba, c.st);
-    if (s != IIR_OK || !c.ba.want_coef) return s;
-    return Ops::fin(c.d, *c.L, c.ba.partial, c.ba.tab, c.gb, c.ga, c.st);
+    return Ops::bwd(c.d, *c.L, c.ba, c.st);
 }
 
 template <typename T, int FORM>

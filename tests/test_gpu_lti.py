@@ -95,6 +95,38 @@ def test_unnormalised_a0(form, a0):
     check(p)
 
 
+@pytest.mark.parametrize("ntiles", [31, 32, 33, 1023, 1024, 1025])
+def test_hierarchical_carry_levels(ntiles):
+    """Tile counts around the base-32 level boundaries of the grid carry."""
+    p = inputs.lti_problem(7100 + ntiles, form="tdf", order=2, batch=1, length=ntiles * 4096 - 5, dtype="f32",
+                           angles="spread")
+    check(p)
+
+
+def test_workspace_reuse_without_memset():
+    """IIR_FLAG_WS_READY: the workspace is cleared once; every call restores it."""
+    p = inputs.lti_problem(7200, form="df", order=3, batch=5, length=70000, dtype="f32", angles="spread")
+    td = torch.float32
+    dev = lambda a: torch.tensor(a, dtype=td, device="cuda")
+    x, b, a, zi, gy, gzf = map(dev, (p["x"], p["b"], p["a"], p["zi"], p["gy"], p["gzf"]))
+    desc = B.make_desc(5, 70000, 3, "df", td, 0, flags=B.IIR_FLAG_WS_READY)
+    tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
+    tape = torch.empty(tb, dtype=torch.uint8, device="cuda")
+    ws = torch.full((wb,), 0xAB, dtype=torch.uint8, device="cuda")
+    B.iir_workspace_init(desc, ws, wb)
+    o = run_lti_oracle(p)
+    from gpu_util import nrm_err
+    for _ in range(3):
+        y, gx = torch.empty_like(x), torch.empty_like(x)
+        zf, gzi = torch.empty_like(zi), torch.empty_like(zi)
+        gbb, gaa = torch.empty_like(b), torch.empty_like(a)
+        B.iir_forward(desc, b, a, x, zi, y, zf, tape, tb, ws, wb)
+        B.iir_backward(desc, gy, gzf, b, a, x, y, zi, tape, tb, gx, gbb, gaa, gzi, ws, wb)
+        torch.cuda.synchronize()
+        for k, g in (("y", y), ("zf", zf), ("gx", gx), ("gb", gbb), ("ga", gaa), ("gzi", gzi)):
+            assert nrm_err(g.double().cpu().numpy(), o[k]) < 1e-4, k
+
+
 def test_many_tiles_one_sequence_lookback():
     """A long chain of tiles on one sequence exercises deep look-back."""
     p = inputs.lti_problem(7000, form="tdf", order=2, batch=1, length=1 << 22, dtype="f32")
