@@ -132,6 +132,9 @@ void iir_profile_reset(void);
 /* Accumulated device milliseconds and launch count of kernel kind `kind` over the
  * profiled launches; syncs on the recorded events (call after a stream sync). */
 int iir_profile_query(int kind, double *total_ms, int64_t *launches);
+/* Debug: when buf (device, >= 8 u64 per tile) is non-NULL, the scan kernels record
+ * %globaltimer at 8 phase points per tile (indexed by tile ticket).  NULL = off.  */
+void iir_debug_trace(void *buf);
 
 #ifdef __cplusplus
 }

@@ -27,7 +27,7 @@ DTYPES = {torch.float32: IIR_F32, torch.float64: IIR_F64}
 
 EXPORTS = ["iir_tape_bytes", "iir_workspace_bytes", "iir_workspace_init", "iir_forward", "iir_backward", "iir_last_error",
            "iir_abi_version", "iir_launch_count", "iir_num_kernels", "iir_kernel_name",
-           "iir_profile_enable", "iir_profile_reset", "iir_profile_query"]
+           "iir_profile_enable", "iir_profile_reset", "iir_profile_query", "iir_debug_trace"]
 
 
 class Desc(ctypes.Structure):
@@ -77,6 +77,7 @@ def lib():
         L.iir_kernel_name.restype = ctypes.c_char_p
         L.iir_kernel_name.argtypes = [ctypes.c_int]
         L.iir_profile_enable.argtypes = [ctypes.c_int]
+        L.iir_debug_trace.argtypes = [_vp]
         L.iir_profile_query.restype = ctypes.c_int
         L.iir_profile_query.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
         _lib = L
@@ -167,3 +168,7 @@ def iir_profile_query(kind: int):
     n = ctypes.c_int64()
     lib().iir_profile_query(int(kind), ctypes.byref(ms), ctypes.byref(n))
     return ms.value, n.value
+
+
+def iir_debug_trace(buf):
+    lib().iir_debug_trace(_ptr(buf))

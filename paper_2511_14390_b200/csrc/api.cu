@@ -161,6 +161,7 @@ static iir_status_t run_lti_any(LtiCall& c) {
     return d->form == IIR_DF2 ? run_lti_m<double, 0>(d->order, c) : run_lti_m<double, 1>(d->order, c);
 }
 
+static unsigned long long* g_trace = nullptr;
 static bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // ------------------------------------------------------------- C ABI --------
@@ -223,6 +224,7 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     fa.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
     fa.cw = carry_ws(L, w);
     fa.B = d->batch; fa.Tlen = d->length; fa.ntiles = (int)L.ntiles; fa.vec = vec;
+    fa.trace = g_trace;
     return run_lti_any(c);
 }
 
@@ -269,11 +271,13 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     ba.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
     ba.cw = carry_ws(L, w);
     ba.B = d->batch; ba.Tlen = d->length; ba.ntiles = (int)L.ntiles; ba.vec = vec;
+    ba.trace = g_trace;
     (void)b; (void)a;
     return run_lti_any(c);
 }
 
 int64_t iir_launch_count(void) { return g_launches.load(); }
+void iir_debug_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
 int iir_num_kernels(void) { return K_NUM; }
 const char* iir_kernel_name(int kind) { return (kind >= 0 && kind < K_NUM) ? kKindNames[kind] : ""; }
 

@@ -61,6 +61,15 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
+// Debug phase tracing (globaltimer ns); disabled when the pointer is null.
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define IIRG_TRACE(ptr, slot, k) \
+    do { if ((ptr) != nullptr && threadIdx.x == 0) (ptr)[(size_t)(slot) * 8 + (k)] = gtimer(); } while (0)
+
 __device__ __forceinline__ double shfl_up_d(double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
 __device__ __forceinline__ double shfl_d(double v, int s) { return __shfl_sync(0xffffffffu, v, s); }
 

@@ -246,6 +246,7 @@ struct LtiFwdArgs {
     const double* tab; int64_t tab_stride;                        // 0 for SHARED
     CarryWs cw;
     int64_t B, Tlen; int ntiles; int vec;
+    unsigned long long* trace;                                    // debug: per-tile phase times
 };
 
 struct LtiBwdArgs {
@@ -256,6 +257,7 @@ struct LtiBwdArgs {
     const double* tab; int64_t tab_stride;
     CarryWs cw;
     int64_t B, Tlen; int ntiles; int vec;
+    unsigned long long* trace;
 };
 
 // Normalised coefficients in T, straight from the caller's b, a (the same
@@ -351,8 +353,14 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
     if (jt == 0) mv_acc_lane<M, TR>(tb + TB::PQ, 32, 1, X0, G);   // tile 0 carries the initial state
     publish<M>(cw.flg[0] + seq * cw.nblk[0] + jt, cw.agg[0] + (seq * cw.nblk[0] + jt) * M, G, lane);
     if (jt > 0) {
-        // T_l (one lane-parallel round per level), kept in shared memory to spare registers
+        // T_l (one lane-parallel round per level), kept in shared memory to spare
+        // registers.  A tile that closes a level-(l+1) block publishes its aggregate
+        // right after T_l, before waiting on any higher level: no cross-block chain.
         int dl[LEVELS];
+        bool closing = true;                   // all lower digits were 31 so far
+        double Own[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) Own[i] = G[i];
 #pragma unroll
         for (int l = 0; l < LEVELS; ++l) {
             dl[l] = (jt >> (5 * l)) & 31;
@@ -376,6 +384,12 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
 #pragma unroll
                 for (int i = 0; i < M; ++i) s_T[l][i] = Tv[i];
             }
+            closing = closing && dl[l] == 31;
+            if (closing && l + 1 < cw.nlev) {
+                mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, 1, Tv, Own);   // Own = Q_l T_l + Own
+                const int64_t bi = seq * cw.nblk[l + 1] + (jt >> (5 * (l + 1)));
+                publish<M>(cw.flg[l + 1] + bi, cw.agg[l + 1] + bi * M, Own, lane);
+            }
         }
         __syncwarp();
         // X = T_0 + Q_0^d0 (T_1 + Q_1^d1 (T_2 + Q_2^d2 T_3))
@@ -395,21 +409,6 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
         }
 #pragma unroll
         for (int i = 0; i < M; ++i) X[i] = R[i];
-        // publish the completed higher-level blocks this tile closes
-        if (dl[0] == 31) {
-            double Own[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) Own[i] = G[i];
-            for (int l = 0; l + 1 < cw.nlev; ++l) {
-                if (dl[l] != 31) break;
-                double Tv[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) Tv[i] = s_T[l][i];
-                mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, 1, Tv, Own);   // Own = Q_l T_l + Own
-                const int64_t bi = seq * cw.nblk[l + 1] + (jt >> (5 * (l + 1)));
-                publish<M>(cw.flg[l + 1] + bi, cw.agg[l + 1] + bi * M, Own, lane);
-            }
-        }
     }
     if (lane < NW) {                           // state entering warp `lane`
         double xw[M];
@@ -426,13 +425,11 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
 __device__ __forceinline__ void ws_cleanup(const CarryWs& cw, int64_t B, unsigned ntot) {
     __shared__ unsigned s_last;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = (atomicAdd(cw.done, 1u) == ntot - 1u) ? 1u : 0u;
-    }
+    // No fence is needed: this CTA's reads of the status words have completed
+    // (their values were consumed) before its increment.
+    if (threadIdx.x == 0) s_last = (atomicAdd(cw.done, 1u) == ntot - 1u) ? 1u : 0u;
     __syncthreads();
     if (s_last) {
-        __threadfence();
         for (int l = 0; l < cw.nlev; ++l)
             for (int64_t i = threadIdx.x; i < B * cw.nblk[l]; i += blockDim.x) cw.flg[l][i] = 0u;
         if (threadIdx.x == 0) { *cw.ticket = 0u; *cw.done = 0u; }
@@ -461,6 +458,7 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
     const int jt = (int)(tk / (unsigned long long)p.B);
     const int64_t p0 = (int64_t)jt * TS;
     const T* xrow = static_cast<const T*>(p.x) + seq * p.Tlen;
+    IIRG_TRACE(p.trace, tk, 0);
 
     tile_load_async<T, TS>(xs, xrow, p0, p.Tlen, p.vec);
     cp_async_commit();
@@ -481,8 +479,10 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
 #pragma unroll
         for (int e = 0; e < W; ++e) { T du; fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, du); }
     }
+    IIRG_TRACE(p.trace, tk, 1);
     // a3: carries in fp64 (the power tables come from the prologue: wait for it).
     pdl_wait();
+    IIRG_TRACE(p.trace, tk, 2);
     const double* tb = p.tab + seq * p.tab_stride;
     double S[M];
 #pragma unroll
@@ -501,7 +501,9 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
         const T* zi = static_cast<const T*>(p.zi);
 #pragma unroll
         for (int i = 0; i < M; ++i) X0[i] = (zi != nullptr && jt == 0) ? (double)zi[seq * M + i] : 0.0;
+        IIRG_TRACE(p.trace, tk, 3);
         tile_carry<M, false>(tb, lane, s_agg, s_xw, jt, seq, X0, p.cw);
+        IIRG_TRACE(p.trace, tk, 4);
     }
     __syncthreads();
     // state entering this thread's chunk: E + A_f^(L lane) x_warp
@@ -544,13 +546,16 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
         if constexpr (FORM == 0) *reinterpret_cast<V*>(us + pidx<T>(s0 + g * W)) = uv;
     }
     __syncthreads();
+    IIRG_TRACE(p.trace, tk, 5);
     T* yrow = static_cast<T*>(p.y) + seq * p.Tlen;
     tile_store<T, TS>(yrow, xs, p0, p.Tlen, p.vec);
     if constexpr (FORM == 0) {
         T* urow = static_cast<T*>(p.u) + seq * p.Tlen;
         tile_store<T, TS>(urow, us, p0, p.Tlen, p.vec);
     }
+    IIRG_TRACE(p.trace, tk, 6);
     ws_cleanup(p.cw, p.B, (unsigned)(p.B * p.ntiles));
+    IIRG_TRACE(p.trace, tk, 7);
 }
 
 // ---------------------------------------------------------------------------
@@ -622,6 +627,7 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
     const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;          // may be < 0 (first tile)
     const double* tb = p.tab + seq * p.tab_stride;
     const int64_t roff = seq * p.Tlen;
+    IIRG_TRACE(p.trace, tk, 0);
 
     // group 0: dy;  group 1: x, y (TDF) or u (DF)
     if (p.gy != nullptr) tile_load_async<T, TS>(dys, static_cast<const T*>(p.gy) + roff, p0, p.Tlen, p.vec);
@@ -674,6 +680,7 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
             else adj_df_step<T, M>(d, vget(dv, e), bc, ac);
         }
     }
+    IIRG_TRACE(p.trace, tk, 1);
     // a6: carries (transposed powers), tiles last -> first.
     double S[M];
 #pragma unroll
@@ -692,7 +699,9 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
         const T* gzf = static_cast<const T*>(p.gzf);
 #pragma unroll
         for (int i = 0; i < M; ++i) X0[i] = (gzf != nullptr && jr == 0) ? (double)gzf[seq * M + i] : 0.0;
+        IIRG_TRACE(p.trace, tk, 3);
         tile_carry<M, true>(tb, lane, s_agg, s_xw, jr, seq, X0, p.cw);
+        IIRG_TRACE(p.trace, tk, 4);
     }
     __syncthreads();
     {
@@ -774,7 +783,9 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
         }
     }
     __syncthreads();
+    IIRG_TRACE(p.trace, tk, 5);
     if (p.gx != nullptr) tile_store<T, TS>(static_cast<T*>(p.gx) + roff, dys, p0, p.Tlen, p.vec);
+    IIRG_TRACE(p.trace, tk, 6);
 
     if (p.want_coef) {
         // fused a8: group of 32 tiles -> group sum; last group of the set -> chain rule.
@@ -829,6 +840,7 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
         }
     }
     ws_cleanup(p.cw, p.B, (unsigned)(p.B * p.ntiles));
+    IIRG_TRACE(p.trace, tk, 7);
 }
 
 }  // namespace iirg
