@@ -100,7 +100,8 @@ typedef enum {
 size_t iir_tape_bytes(const iir_desc_t *desc);
 size_t iir_workspace_bytes(const iir_desc_t *desc);
 
-/* Clear a workspace (stream-ordered cudaMemsetAsync of its counter region). */
+/* Initialise a workspace (stream-ordered cudaMemsetAsync: counters to 0, look-back
+ * payload slots to the all-ones NaN sentinel). */
 iir_status_t iir_workspace_init(const iir_desc_t *desc, void *ws, size_t ws_bytes, iir_stream_t stream);
 
 /* Forward: y = filter(b, a, x; zi), zf = final state.  Eqs.1-5. */

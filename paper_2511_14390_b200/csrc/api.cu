@@ -117,9 +117,10 @@ static Layout layout(const iir_desc_t* d) {
     L.ws_ticket = o; L.ws_done = o + 4; o += 256;
     L.ws_gcnt = o; o += al256(L.ngroups * 4);
     L.ws_scnt = o; o += al256(L.ncoef * 4);
-    for (int l = 0; l < L.nlev; ++l) { L.ws_flg[l] = o; o += al256(d->batch * L.nblk[l] * 4); }
     L.ws_clear = o;
+    L.ws_sent = o;
     for (int l = 0; l < L.nlev; ++l) { L.ws_agg[l] = o; o += al256(d->batch * L.nblk[l] * M * 8); }
+    L.ws_sent_bytes = o - L.ws_sent;
     L.ws_part = o; o += al256(L.ntot * (2 * M + 1) * 8);
     L.ws_part2 = o; o += al256(L.ngroups * (2 * M + 1) * 8);
     L.ws_bytes = o;
@@ -136,7 +137,6 @@ static CarryWs carry_ws(const Layout& L, char* w) {
     c.ticket = reinterpret_cast<unsigned*>(w + L.ws_ticket);
     c.done = reinterpret_cast<unsigned*>(w + L.ws_done);
     for (int l = 0; l < MAX_LEVELS; ++l) {
-        c.flg[l] = l < L.nlev ? reinterpret_cast<unsigned*>(w + L.ws_flg[l]) : nullptr;
         c.agg[l] = l < L.nlev ? reinterpret_cast<double*>(w + L.ws_agg[l]) : nullptr;
         c.nblk[l] = L.nblk[l];
     }
@@ -162,6 +162,14 @@ static iir_status_t run_lti_any(LtiCall& c) {
 }
 
 static unsigned long long* g_trace = nullptr;
+static iir_status_t ws_reset(const Layout& L, void* ws, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(ws, 0, L.ws_clear, st);
+    if (e == cudaSuccess && L.ws_sent_bytes)
+        e = cudaMemsetAsync(static_cast<char*>(ws) + L.ws_sent, 0xFF, L.ws_sent_bytes, st);
+    if (e != cudaSuccess) return fail(IIR_ECUDA, std::string("workspace memset: ") + cudaGetErrorString(e));
+    return IIR_OK;
+}
+
 static bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // ------------------------------------------------------------- C ABI --------
@@ -184,9 +192,7 @@ iir_status_t iir_workspace_init(const iir_desc_t* d, void* ws, size_t ws_bytes, 
     if (s != IIR_OK) return s;
     const Layout L = layout(d);
     if (ws == nullptr || ws_bytes < L.ws_bytes) return fail(IIR_EWORKSPACE, "workspace missing or too small");
-    cudaError_t e = cudaMemsetAsync(ws, 0, L.ws_clear, static_cast<cudaStream_t>(stream));
-    if (e != cudaSuccess) return fail(IIR_ECUDA, std::string("memset: ") + cudaGetErrorString(e));
-    return IIR_OK;
+    return ws_reset(L, ws, static_cast<cudaStream_t>(stream));
 }
 
 iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, const void* x, const void* zi, void* y,
@@ -207,8 +213,8 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     char* w = static_cast<char*>(ws);
     char* t = static_cast<char*>(tape);
     if (!(d->flags & IIR_FLAG_WS_READY)) {
-        cudaError_t e = cudaMemsetAsync(w, 0, L.ws_clear, st);
-        if (e != cudaSuccess) return fail(IIR_ECUDA, std::string("memset: ") + cudaGetErrorString(e));
+        iir_status_t rs = ws_reset(L, w, st);
+        if (rs != IIR_OK) return rs;
     }
     const int W = d->dtype == IIR_F64 ? 2 : 4;
     const bool vec = (d->length % W == 0) && aligned16(x) && aligned16(y) && aligned16(t + L.tp_u);
@@ -245,8 +251,8 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     char* w = static_cast<char*>(ws);
     const char* t = static_cast<const char*>(tape);
     if (!(d->flags & IIR_FLAG_WS_READY)) {
-        cudaError_t e = cudaMemsetAsync(w, 0, L.ws_clear, st);
-        if (e != cudaSuccess) return fail(IIR_ECUDA, std::string("memset: ") + cudaGetErrorString(e));
+        iir_status_t rs = ws_reset(L, w, st);
+        if (rs != IIR_OK) return rs;
     }
     const int W = d->dtype == IIR_F64 ? 2 : 4;
     const bool vec = (d->length % W == 0) && aligned16(grad_y) && aligned16(x) && aligned16(y) &&

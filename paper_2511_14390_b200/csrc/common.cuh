@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace iirg {
 
@@ -57,6 +58,18 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// Look-back payload slots: every fp64 slot starts as the all-ones NaN sentinel
+// (never produced by arithmetic: NVIDIA GPUs return a canonical NaN), so a
+// reader needs one round trip and no separate flag: it re-reads until no
+// element is the sentinel.  8-byte stores / loads are single-copy atomic.
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+    double v;   // volatile: performed every time (a .cv cache hint alone may be hoisted by ptxas)
+    asm volatile("ld.volatile.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ bool is_sentinel(double v) { return __double_as_longlong(v) == -1LL; }
+__device__ __forceinline__ double sentinel() { return __longlong_as_double(-1LL); }
+
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }

@@ -60,6 +60,29 @@ __device__ __forceinline__ void mv_acc_lane(const double* __restrict__ P, int st
     }
 }
 
+// Shared-memory versions (tables staged once per CTA).
+template <int M, bool TR>
+__device__ __forceinline__ void mv_acc_s(const double* P, const double (&v)[M], double (&acc)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        double s = acc[i];
+#pragma unroll
+        for (int j = 0; j < M; ++j) s = fma(P[TR ? j * M + i : i * M + j], v[j], s);
+        acc[i] = s;
+    }
+}
+template <int M, bool TR>
+__device__ __forceinline__ void mv_acc_lane_s(const double* P, int stride, int t, const double (&v)[M],
+                                              double (&acc)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        double s = acc[i];
+#pragma unroll
+        for (int j = 0; j < M; ++j) s = fma(P[(TR ? j * M + i : i * M + j) * stride + t], v[j], s);
+        acc[i] = s;
+    }
+}
+
 // Programmatic dependent launch (PTX griddepcontrol).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
@@ -234,8 +257,7 @@ __device__ __forceinline__ T adj_df_step(T (&d)[M], T dy, const T (&bc)[M + 1], 
 struct CarryWs {
     unsigned* ticket;            // tile ticket counter
     unsigned* done;              // CTAs finished (the last one cleans the workspace)
-    unsigned* flg[LEVELS];       // readiness of each level-l block aggregate
-    double* agg[LEVELS];         // level-l block aggregates [seq][block][M]
+    double* agg[LEVELS];         // level-l block aggregates [seq][block][M] (sentinel = not ready)
     int64_t nblk[LEVELS];        // blocks per sequence at level l (ceil(ntiles / 32^l))
     int nlev;                    // levels in use
 };
@@ -281,7 +303,7 @@ __device__ __forceinline__ void load_coefs(const double* __restrict__ tb, T (&bc
 // Warp-level inclusive Kogge-Stone scan of chunk aggregates in fp64:
 //   S_t <- P^(2^d) S_{t-2^d} + S_t, P = A_f^L (TR: transposed for the adjoint).
 template <int M, bool TR>
-__device__ __forceinline__ void warp_scan(const double* __restrict__ tb, int lane, double (&S)[M]) {
+__device__ __forceinline__ void warp_scan(const double* st, int lane, double (&S)[M]) {
     using TB = Tab<M>;
 #pragma unroll
     for (int d = 0; d < 5; ++d) {
@@ -289,7 +311,7 @@ __device__ __forceinline__ void warp_scan(const double* __restrict__ tb, int lan
         double O[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) O[i] = shfl_up_d(S[i], off);
-        if (lane >= off) mv_acc<M, TR>(tb + TB::PL + d * M * M, O, S);
+        if (lane >= off) mv_acc_s<M, TR>(st + TB::PL + d * M * M, O, S);
     }
 }
 
@@ -302,11 +324,38 @@ __device__ __forceinline__ void warp_sum(double (&v)[M]) {
 }
 
 template <int M>
-__device__ __forceinline__ void publish(unsigned* flag, double* dst, const double (&v)[M], int lane) {
+__device__ __forceinline__ void publish(double* dst, const double (&v)[M], int lane) {
     if (lane == 0) {
 #pragma unroll
         for (int i = 0; i < M; ++i) __stcg(dst + i, v[i]);
-        st_release(flag, 1u);
+    }
+}
+
+// Wait until a look-back payload slot is published and read it.  One element
+// is polled with exponential back-off (thousands of warps may wait on the same
+// few slots; unthrottled polling floods that L2 slice and delays the very
+// store being waited for), then all M are read and re-checked.
+template <int M>
+__device__ __forceinline__ void wait_slot(const double* src, double (&v)[M]) {
+    unsigned ns = 32;
+    unsigned long long t_spin = 0;
+    for (;;) {
+        if (!is_sentinel(ld_relaxed(src))) {
+            bool ready = true;
+#pragma unroll
+            for (int i = 0; i < M; ++i) { v[i] = ld_relaxed(src + i); ready = ready && !is_sentinel(v[i]); }
+            if (ready) return;
+        }
+        __nanosleep(ns);
+        if (ns < 1024) ns *= 2;
+        else {                                   // a stuck look-back is a bug: report, don't hang
+            const unsigned long long now = gtimer();
+            if (t_spin == 0) t_spin = now;
+            else if (now - t_spin > 4000000000ull) {
+                printf("iirgrad: look-back slot %p never published\n", (const void*)src);
+                __trap();
+            }
+        }
     }
 }
 
@@ -323,7 +372,8 @@ __device__ __forceinline__ void publish(unsigned* flag, double* dst, const doubl
 // on a serial chain of inclusive prefixes.  The last tile of a level-l block
 // publishes AGG^(l+1) = Q_l T_l + AGG^(l)_own.
 template <int M, bool TR>
-__device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int lane, double (*s_agg)[M],
+__device__ __forceinline__ void tile_carry(const double* st, const double* __restrict__ tb, int lane,
+                                           double (*s_agg)[M],
                                            double (*s_xw)[M], int jt, int64_t seq, const double (&X0)[M],
                                            const CarryWs& cw) {
     __shared__ double s_T[LEVELS][M];
@@ -338,7 +388,7 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
         double O[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) O[i] = shfl_up_d(J[i], off);
-        if (lane >= off && lane < NW) mv_acc<M, TR>(tb + TB::PW + d * M2, O, J);
+        if (lane >= off && lane < NW) mv_acc_s<M, TR>(st + TB::PW + d * M2, O, J);
     }
     double Jex[M], G[M];
 #pragma unroll
@@ -351,7 +401,7 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
 #pragma unroll
     for (int i = 0; i < M; ++i) X[i] = X0[i];
     if (jt == 0) mv_acc_lane<M, TR>(tb + TB::PQ, 32, 1, X0, G);   // tile 0 carries the initial state
-    publish<M>(cw.flg[0] + seq * cw.nblk[0] + jt, cw.agg[0] + (seq * cw.nblk[0] + jt) * M, G, lane);
+    publish<M>(cw.agg[0] + (seq * cw.nblk[0] + jt) * M, G, lane);
     if (jt > 0) {
         // T_l (one lane-parallel round per level), kept in shared memory to spare
         // registers.  A tile that closes a level-(l+1) block publishes its aggregate
@@ -370,12 +420,10 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
             if (l < cw.nlev && dl[l] > 0) {
                 const int64_t base = seq * cw.nblk[l] + (jt >> (5 * l)) - dl[l];
                 if (lane < dl[l]) {
-                    const unsigned* f = cw.flg[l] + base + lane;
-                    while (ld_acquire(f) == 0u) { }
                     const double* src = cw.agg[l] + (base + lane) * M;
                     double v[M];
-#pragma unroll
-                    for (int i = 0; i < M; ++i) v[i] = __ldcg(src + i);
+                    wait_slot<M>(src, v);
+                    (void)seq;
                     mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, dl[l] - 1 - lane, v, Tv);
                 }
                 warp_sum<M>(Tv);
@@ -388,7 +436,7 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
             if (closing && l + 1 < cw.nlev) {
                 mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, 1, Tv, Own);   // Own = Q_l T_l + Own
                 const int64_t bi = seq * cw.nblk[l + 1] + (jt >> (5 * (l + 1)));
-                publish<M>(cw.flg[l + 1] + bi, cw.agg[l + 1] + bi * M, Own, lane);
+                publish<M>(cw.agg[l + 1] + bi * M, Own, lane);
             }
         }
         __syncwarp();
@@ -414,148 +462,208 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
         double xw[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) xw[i] = Jex[i];
-        mv_acc_lane<M, TR>(tb + TB::PWT, NW, lane, X, xw);
+        mv_acc_lane_s<M, TR>(st + TB::PWT, NW, lane, X, xw);
 #pragma unroll
         for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
     }
 }
 
-// The last CTA of the grid restores the workspace to its zero state, so the
-// next call on the same (stream-ordered) workspace needs no memset.
-__device__ __forceinline__ void ws_cleanup(const CarryWs& cw, int64_t B, unsigned ntot) {
+// Persistent CTAs exit once the ticket counter runs past the last tile; the last
+// CTA to exit restores the workspace to its zero state, so the next call on the
+// same (stream-ordered) workspace needs no memset.  No fence is needed: every
+// CTA's reads of the status words completed (their values were consumed) and
+// its final ticket grab happened before its exit increment.
+template <int M>
+__device__ __forceinline__ void cta_exit(const CarryWs& cw, int64_t B, unsigned nctas) {
     __shared__ unsigned s_last;
     __syncthreads();
-    // No fence is needed: this CTA's reads of the status words have completed
-    // (their values were consumed) before its increment.
-    if (threadIdx.x == 0) s_last = (atomicAdd(cw.done, 1u) == ntot - 1u) ? 1u : 0u;
+    if (threadIdx.x == 0) s_last = (atomicAdd(cw.done, 1u) == nctas - 1u) ? 1u : 0u;
     __syncthreads();
     if (s_last) {
         for (int l = 0; l < cw.nlev; ++l)
-            for (int64_t i = threadIdx.x; i < B * cw.nblk[l]; i += blockDim.x) cw.flg[l][i] = 0u;
+            for (int64_t i = threadIdx.x; i < B * cw.nblk[l] * M; i += blockDim.x) cw.agg[l][i] = sentinel();
         if (threadIdx.x == 0) { *cw.ticket = 0u; *cw.done = 0u; }
     }
 }
 
+// Stage the per-coefficient-set power tables PL | PLT | PW | PWT (Tab<M>::PQ
+// doubles, identical layout) into shared memory.
+template <int M>
+__device__ __forceinline__ void stage_tables(double* st, const double* __restrict__ tb) {
+    for (int i = threadIdx.x; i < Tab<M>::PQ; i += blockDim.x) st[i] = __ldg(tb + i);
+}
+
+template <typename T, int M>
+struct Smem {
+    static constexpr int TS = NT * Chunk<T>::L;
+    static constexpr int PT = pidx<T>(TS);               // one padded tile
+    static constexpr int PTH = pidx<T>(TS + HALO);       // padded tile with u history
+    static constexpr size_t tab_bytes = ((size_t)Tab<M>::PQ * 8 + 15) / 16 * 16;
+    static constexpr size_t fwd(int form) { return tab_bytes + (size_t)(2 * PT + (form == 0 ? PT : 0)) * sizeof(T); }
+    static constexpr size_t bwd(int form) {
+        return tab_bytes + (size_t)(2 * PT + PTH + (form == 1 ? PT : 0)) * sizeof(T);
+    }
+};
+
 // ---------------------------------------------------------------------------
-// Forward: a2-a4.  One CTA per tile (TS samples of one sequence).
+// Forward: a2-a4.  Persistent CTAs take tiles (TS samples of one sequence) in
+// ticket order and double-buffer them: tile k+1 streams into shared memory
+// (cp.async) while tile k is scanned.  Tickets interleave the sequences (ticket
+// t = tile t / B of sequence t % B), so concurrent tiles rarely wait.
 template <typename T, int M, int FORM>
 __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
     constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
     using V = typename Vec<T>::type;
     using TB = Tab<M>;
+    using SM = Smem<T, M>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* xs = reinterpret_cast<T*>(smem_raw);
-    T* us = xs + pidx<T>(TS);                  // DF: u tile
+    double* st = reinterpret_cast<double*>(smem_raw);
+    T* xb = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);     // 2 stages: x -> y in place
+    T* us = xb + 2 * SM::PT;                                      // DF: u tile
     __shared__ double s_agg[NW][M];
     __shared__ double s_xw[NW][M];
-    __shared__ unsigned s_ticket;
+    __shared__ unsigned s_tk[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_ticket = atomicAdd(p.cw.ticket, 1u);
+    const unsigned ntot = (unsigned)(p.B * p.ntiles);
+    // tickets are taken two tiles ahead so the atomic's latency hides behind a tile
+    if (tid == 0) { s_tk[0] = atomicAdd(p.cw.ticket, 1u); s_tk[1] = atomicAdd(p.cw.ticket, 1u); }
     __syncthreads();
-    const unsigned tk = s_ticket;
-    const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
-    const int jt = (int)(tk / (unsigned long long)p.B);
-    const int64_t p0 = (int64_t)jt * TS;
-    const T* xrow = static_cast<const T*>(p.x) + seq * p.Tlen;
-    IIRG_TRACE(p.trace, tk, 0);
-
-    tile_load_async<T, TS>(xs, xrow, p0, p.Tlen, p.vec);
+    unsigned tk = s_tk[0], tkn = s_tk[1];
+    if (tk < ntot) {
+        const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
+        const int jt = (int)(tk / (unsigned long long)p.B);
+        tile_load_async<T, TS>(xb, static_cast<const T*>(p.x) + seq * p.Tlen, (int64_t)jt * TS, p.Tlen, p.vec);
+    }
     cp_async_commit();
+    int stage = 0;
+    int64_t tab_set = -1, coef_set = -1;
+    bool waited = false;
     T bc[M + 1], ac[M + 1];
-    raw_coefs<T, M>(static_cast<const T*>(p.b) + seq * p.coef_stride,
-                    static_cast<const T*>(p.a) + seq * p.coef_stride, bc, ac);
-    cp_async_wait<0>();
-    __syncthreads();
+    while (tk < ntot) {
+        unsigned tk2 = 0u;
+        if (tid == 0) tk2 = atomicAdd(p.cw.ticket, 1u);          // consumed at the end of the iteration
+        if (tkn < ntot) {
+            const int64_t sq = (int64_t)(tkn % (unsigned long long)p.B);
+            const int jn = (int)(tkn / (unsigned long long)p.B);
+            tile_load_async<T, TS>(xb + (stage ^ 1) * SM::PT, static_cast<const T*>(p.x) + sq * p.Tlen,
+                                   (int64_t)jn * TS, p.Tlen, p.vec);
+        }
+        cp_async_commit();
+        const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
+        const int jt = (int)(tk / (unsigned long long)p.B);
+        const int64_t p0 = (int64_t)jt * TS;
+        T* xs = xb + stage * SM::PT;
+        IIRG_TRACE(p.trace, tk, 0);
+        const int64_t cs = p.coef_stride == 0 ? 0 : seq;
+        if (cs != coef_set) {
+            raw_coefs<T, M>(static_cast<const T*>(p.b) + cs * p.coef_stride,
+                            static_cast<const T*>(p.a) + cs * p.coef_stride, bc, ac);
+            coef_set = cs;
+        }
+        cp_async_wait<1>();
+        __syncthreads();
 
-    // a2: local pass from the zero state over this thread's chunk.
-    const int s0 = tid * L;
-    T v[M];
+        // a2: local pass from the zero state over this thread's chunk.
+        const int s0 = tid * L;
+        T v[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) v[i] = T(0);
+        for (int i = 0; i < M; ++i) v[i] = T(0);
 #pragma unroll
-    for (int g = 0; g < L / W; ++g) {
-        const V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
+        for (int g = 0; g < L / W; ++g) {
+            const V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
 #pragma unroll
-        for (int e = 0; e < W; ++e) { T du; fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, du); }
-    }
-    IIRG_TRACE(p.trace, tk, 1);
-    // a3: carries in fp64 (the power tables come from the prologue: wait for it).
-    pdl_wait();
-    IIRG_TRACE(p.trace, tk, 2);
-    const double* tb = p.tab + seq * p.tab_stride;
-    double S[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) S[i] = (double)v[i];
-    warp_scan<M, false>(tb, lane, S);
-    double E[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
-    if (lane == 31) {
-#pragma unroll
-        for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
-    }
-    __syncthreads();
-    if (warp == 0) {
-        double X0[M];
-        const T* zi = static_cast<const T*>(p.zi);
-#pragma unroll
-        for (int i = 0; i < M; ++i) X0[i] = (zi != nullptr && jt == 0) ? (double)zi[seq * M + i] : 0.0;
-        IIRG_TRACE(p.trace, tk, 3);
-        tile_carry<M, false>(tb, lane, s_agg, s_xw, jt, seq, X0, p.cw);
-        IIRG_TRACE(p.trace, tk, 4);
-    }
-    __syncthreads();
-    // state entering this thread's chunk: E + A_f^(L lane) x_warp
-    {
-        double xw[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
-        mv_acc_lane<M, false>(tb + TB::PLT, 32, lane, xw, E);
-    }
-    T vin[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) { vin[i] = (T)E[i]; v[i] = vin[i]; }
-    // zf = v(T): the thread holding sample T-1 walks its chunk up to it (before
-    // the emit pass overwrites x with y).
-    if (p.zf != nullptr) {
-        const int64_t eL = p.Tlen - 1 - p0;
-        if (eL >= s0 && eL < s0 + L) {
-            T w2[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) w2[i] = vin[i];
-            for (int n = s0; n <= (int)eL; ++n) { T du; fwd_step<T, M, FORM>(w2, xs[pidx<T>(n)], bc, ac, du); }
-            T* zf = static_cast<T*>(p.zf) + seq * M;
-#pragma unroll
-            for (int i = 0; i < M; ++i) zf[i] = w2[i];
+            for (int e = 0; e < W; ++e) { T du; fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, du); }
         }
-    }
-    // a4: re-run from the exact carry-in, emit y (and u for DF) in place.
-#pragma unroll
-    for (int g = 0; g < L / W; ++g) {
-        V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
-        V uv;
-#pragma unroll
-        for (int e = 0; e < W; ++e) {
-            T uu;
-            const T yy = fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, uu);
-            vset(xv, e, yy);
-            vset(uv, e, uu);
+        IIRG_TRACE(p.trace, tk, 1);
+        // a3: carries in fp64; the power tables come from the prologue (PDL wait once).
+        const double* tb = p.tab + seq * p.tab_stride;
+        const int64_t set = p.tab_stride == 0 ? 0 : seq;
+        if (set != tab_set) {
+            if (!waited) { pdl_wait(); waited = true; }
+            stage_tables<M>(st, tb);
+            tab_set = set;
+            __syncthreads();
         }
-        *reinterpret_cast<V*>(xs + pidx<T>(s0 + g * W)) = xv;
-        if constexpr (FORM == 0) *reinterpret_cast<V*>(us + pidx<T>(s0 + g * W)) = uv;
+        IIRG_TRACE(p.trace, tk, 2);
+        double S[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) S[i] = (double)v[i];
+        warp_scan<M, false>(st, lane, S);
+        double E[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
+        if (lane == 31) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double X0[M];
+            const T* zi = static_cast<const T*>(p.zi);
+#pragma unroll
+            for (int i = 0; i < M; ++i) X0[i] = (zi != nullptr && jt == 0) ? (double)zi[seq * M + i] : 0.0;
+            IIRG_TRACE(p.trace, tk, 3);
+            tile_carry<M, false>(st, tb, lane, s_agg, s_xw, jt, seq, X0, p.cw);
+            IIRG_TRACE(p.trace, tk, 4);
+        }
+        __syncthreads();
+        // state entering this thread's chunk: E + A_f^(L lane) x_warp
+        {
+            double xw[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
+            mv_acc_lane_s<M, false>(st + TB::PLT, 32, lane, xw, E);
+        }
+        T vin[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) { vin[i] = (T)E[i]; v[i] = vin[i]; }
+        // zf = v(T): the thread holding sample T-1 walks its chunk up to it (before
+        // the emit pass overwrites x with y).
+        if (p.zf != nullptr) {
+            const int64_t eL = p.Tlen - 1 - p0;
+            if (eL >= s0 && eL < s0 + L) {
+                T w2[M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) w2[i] = vin[i];
+                for (int n = s0; n <= (int)eL; ++n) { T du; fwd_step<T, M, FORM>(w2, xs[pidx<T>(n)], bc, ac, du); }
+                T* zf = static_cast<T*>(p.zf) + seq * M;
+#pragma unroll
+                for (int i = 0; i < M; ++i) zf[i] = w2[i];
+            }
+        }
+        // a4: re-run from the exact carry-in, emit y (and u for DF) in place.
+#pragma unroll
+        for (int g = 0; g < L / W; ++g) {
+            V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
+            V uv;
+#pragma unroll
+            for (int e = 0; e < W; ++e) {
+                T uu;
+                const T yy = fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, uu);
+                vset(xv, e, yy);
+                vset(uv, e, uu);
+            }
+            *reinterpret_cast<V*>(xs + pidx<T>(s0 + g * W)) = xv;
+            if constexpr (FORM == 0) *reinterpret_cast<V*>(us + pidx<T>(s0 + g * W)) = uv;
+        }
+        __syncthreads();
+        IIRG_TRACE(p.trace, tk, 5);
+        T* yrow = static_cast<T*>(p.y) + seq * p.Tlen;
+        tile_store<T, TS>(yrow, xs, p0, p.Tlen, p.vec);
+        if constexpr (FORM == 0) {
+            T* urow = static_cast<T*>(p.u) + seq * p.Tlen;
+            tile_store<T, TS>(urow, us, p0, p.Tlen, p.vec);
+        }
+        IIRG_TRACE(p.trace, tk, 6);
+        if (tid == 0) s_tk[0] = tk2;
+        __syncthreads();                                          // also: stores have read this stage
+        stage ^= 1;
+        tk = tkn;
+        tkn = s_tk[0];
     }
-    __syncthreads();
-    IIRG_TRACE(p.trace, tk, 5);
-    T* yrow = static_cast<T*>(p.y) + seq * p.Tlen;
-    tile_store<T, TS>(yrow, xs, p0, p.Tlen, p.vec);
-    if constexpr (FORM == 0) {
-        T* urow = static_cast<T*>(p.u) + seq * p.Tlen;
-        tile_store<T, TS>(urow, us, p0, p.Tlen, p.vec);
-    }
-    IIRG_TRACE(p.trace, tk, 6);
-    ws_cleanup(p.cw, p.B, (unsigned)(p.B * p.ntiles));
-    IIRG_TRACE(p.trace, tk, 7);
+    if (!waited) pdl_wait();
+    cta_exit<M>(p.cw, p.B, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -598,41 +706,18 @@ __device__ __forceinline__ void chain_rule(const double* __restrict__ G, const d
 }
 
 // ---------------------------------------------------------------------------
-// Backward: a5-a8.  Tiles are aligned to the END of each sequence and processed
+// Backward: a5-a8.  Tiles are aligned to the END of each sequence and taken
 // last to first; inside a tile thread t owns chunk NT-1-t, walked backwards.
-// TDF: smem dy | x | y.  DF: smem dy | u (with HALO samples of history).
+// Persistent CTAs double-buffer dy (the local pass needs only dy); x, y (TDF)
+// or u (DF) of tile k+1 stream in once tile k's emit pass has finished.
 template <typename T, int M, int FORM>
-__global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
-    constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
-    constexpr int NG = 2 * M + 1;                       // gradient partial sums
+__device__ __forceinline__ void bwd_issue_xy(const LtiBwdArgs& p, unsigned tk, T* s2, T* s3) {
+    constexpr int TS = NT * Chunk<T>::L, W = Vec<T>::W;
     using V = typename Vec<T>::type;
-    using TB = Tab<M>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* dys = reinterpret_cast<T*>(smem_raw);
-    T* s2 = dys + pidx<T>(TS);                          // TDF: x        DF: u (+HALO)
-    T* s3 = s2 + pidx<T>(TS + HALO);                    // TDF: y
-    __shared__ double s_agg[NW][M];
-    __shared__ double s_xw[NW][M];
-    __shared__ double s_red[NW][NG];
-    __shared__ double s_G[NG];
-    __shared__ unsigned s_ticket, s_fin;
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_ticket = atomicAdd(p.cw.ticket, 1u);
-    __syncthreads();
-    const unsigned tk = s_ticket;
     const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
-    const int jr = (int)(tk / (unsigned long long)p.B);          // 0 = last tile in time
-    const int jt = p.ntiles - 1 - jr;                            // time index of the tile
-    const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;          // may be < 0 (first tile)
-    const double* tb = p.tab + seq * p.tab_stride;
+    const int jr = (int)(tk / (unsigned long long)p.B);
+    const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;
     const int64_t roff = seq * p.Tlen;
-    IIRG_TRACE(p.trace, tk, 0);
-
-    // group 0: dy;  group 1: x, y (TDF) or u (DF)
-    if (p.gy != nullptr) tile_load_async<T, TS>(dys, static_cast<const T*>(p.gy) + roff, p0, p.Tlen, p.vec);
-    else for (int e = tid; e < TS; e += NT) dys[pidx<T>(e)] = T(0);
-    cp_async_commit();
     if constexpr (FORM == 1) {
         tile_load_async<T, TS>(s2, static_cast<const T*>(p.x) + roff, p0, p.Tlen, p.vec);
         tile_load_async<T, TS>(s3, static_cast<const T*>(p.y) + roff, p0, p.Tlen, p.vec);
@@ -640,7 +725,7 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
         // u(p0 - HALO .. p0 + TS) -> s2[pidx(e + HALO)]; u(-k) = zi[k-1] (DF state).
         const T* urow = static_cast<const T*>(p.u) + roff;
         const T* zi = static_cast<const T*>(p.zi);
-        for (int q = tid; q < (TS + HALO) / W; q += NT) {
+        for (int q = threadIdx.x; q < (TS + HALO) / W; q += NT) {
             const int e = q * W - HALO;
             const int64_t pos = p0 + e;
             if (p.vec && pos >= 0 && pos + W <= p.Tlen) {
@@ -659,188 +744,250 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
             }
         }
     }
+}
+template <typename T>
+__device__ __forceinline__ void bwd_issue_dy(const void* gy, unsigned tk, int64_t B, int64_t Tlen, bool vec, T* dys) {
+    constexpr int TS = NT * Chunk<T>::L;
+    const int64_t seq = (int64_t)(tk % (unsigned long long)B);
+    const int jr = (int)(tk / (unsigned long long)B);
+    const int64_t p0 = Tlen - (int64_t)(jr + 1) * TS;
+    if (gy != nullptr) tile_load_async<T, TS>(dys, static_cast<const T*>(gy) + seq * Tlen, p0, Tlen, vec);
+    else for (int e = threadIdx.x; e < TS; e += NT) dys[pidx<T>(e)] = T(0);
+}
+
+template <typename T, int M, int FORM>
+__global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
+    constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
+    constexpr int NG = 2 * M + 1;                       // gradient partial sums
+    using V = typename Vec<T>::type;
+    using TB = Tab<M>;
+    using SM = Smem<T, M>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* st = reinterpret_cast<double*>(smem_raw);
+    T* dyb = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);   // 2 stages: dy -> dx in place
+    T* s2 = dyb + 2 * SM::PT;                                  // TDF: x        DF: u (+HALO)
+    T* s3 = s2 + SM::PTH;                                      // TDF: y
+    __shared__ double s_agg[NW][M];
+    __shared__ double s_xw[NW][M];
+    __shared__ double s_red[NW][NG];
+    __shared__ double s_G[NG];
+    __shared__ unsigned s_tk[2], s_fin;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned ntot = (unsigned)(p.B * p.ntiles);
+    if (tid == 0) { s_tk[0] = atomicAdd(p.cw.ticket, 1u); s_tk[1] = atomicAdd(p.cw.ticket, 1u); }
+    __syncthreads();
+    unsigned tk = s_tk[0], tkn = s_tk[1];
+    if (tk < ntot) bwd_issue_dy<T>(p.gy, tk, p.B, p.Tlen, p.vec, dyb);
     cp_async_commit();
-    T bc[M + 1], ac[M + 1], cc[M];
-    load_coefs<T, M>(tb, bc, ac, cc);
-    cp_async_wait<1>();
-    __syncthreads();
+    if (tk < ntot) bwd_issue_xy<T, M, FORM>(p, tk, s2, s3);
+    cp_async_commit();
+    int stage = 0;
+    int64_t tab_set = -1;
+    while (tk < ntot) {
+        unsigned tk2 = 0u;
+        if (tid == 0) tk2 = atomicAdd(p.cw.ticket, 1u);          // consumed at the end of the iteration
+        if (tkn < ntot) bwd_issue_dy<T>(p.gy, tkn, p.B, p.Tlen, p.vec, dyb + (stage ^ 1) * SM::PT);
+        cp_async_commit();
+        const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
+        const int jr = (int)(tk / (unsigned long long)p.B);          // 0 = last tile in time
+        const int jt = p.ntiles - 1 - jr;                            // time index of the tile
+        const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;          // may be < 0 (first tile)
+        const double* tb = p.tab + seq * p.tab_stride;
+        const int64_t roff = seq * p.Tlen;
+        T* dys = dyb + stage * SM::PT;
+        IIRG_TRACE(p.trace, tk, 0);
+        const int64_t set = p.tab_stride == 0 ? 0 : seq;
+        if (set != tab_set) { stage_tables<M>(st, tb); tab_set = set; }
+        T bc[M + 1], ac[M + 1], cc[M];
+        load_coefs<T, M>(tb, bc, ac, cc);
+        cp_async_wait<2>();                                          // dy of this tile
+        __syncthreads();
 
-    const int c = NT - 1 - tid;          // chunk index within the tile (time order)
-    const int s0 = c * L;
-    // a5: local adjoint pass from the zero state, walking the chunk backwards.
-    T d[M];
+        const int c = NT - 1 - tid;          // chunk index within the tile (time order)
+        const int s0 = c * L;
+        // a5: local adjoint pass from the zero state, walking the chunk backwards.
+        T d[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) d[i] = T(0);
+        for (int i = 0; i < M; ++i) d[i] = T(0);
 #pragma unroll
-    for (int g = L / W - 1; g >= 0; --g) {
-        const V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
-#pragma unroll
-        for (int e = W - 1; e >= 0; --e) {
-            if constexpr (FORM == 1) adj_tdf_step<T, M>(d, vget(dv, e), ac);
-            else adj_df_step<T, M>(d, vget(dv, e), bc, ac);
-        }
-    }
-    IIRG_TRACE(p.trace, tk, 1);
-    // a6: carries (transposed powers), tiles last -> first.
-    double S[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) S[i] = (double)d[i];
-    warp_scan<M, true>(tb, lane, S);
-    double E[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
-    if (lane == 31) {
-#pragma unroll
-        for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
-    }
-    __syncthreads();
-    if (warp == 0) {
-        double X0[M];
-        const T* gzf = static_cast<const T*>(p.gzf);
-#pragma unroll
-        for (int i = 0; i < M; ++i) X0[i] = (gzf != nullptr && jr == 0) ? (double)gzf[seq * M + i] : 0.0;
-        IIRG_TRACE(p.trace, tk, 3);
-        tile_carry<M, true>(tb, lane, s_agg, s_xw, jr, seq, X0, p.cw);
-        IIRG_TRACE(p.trace, tk, 4);
-    }
-    __syncthreads();
-    {
-        double xw[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
-        mv_acc_lane<M, true>(tb + TB::PLT, 32, lane, xw, E);
-    }
-    T din[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) { din[i] = (T)E[i]; d[i] = din[i]; }
-    cp_async_wait<0>();
-    __syncthreads();
-
-    // grad_zi = dz(-1) (Eq.9, A.3): the thread whose chunk holds n = 0 walks down
-    // to it before the emit pass overwrites dy with dx.
-    if (p.gzi != nullptr && p0 + s0 <= 0 && p0 + s0 + L > 0) {
-        T w2[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) w2[i] = din[i];
-        for (int n = s0 + L - 1; n >= (int)(-p0); --n) {
-            const T dy = dys[pidx<T>(n)];
-            if constexpr (FORM == 1) adj_tdf_step<T, M>(w2, dy, ac);
-            else (void)adj_df_step<T, M>(w2, dy, bc, ac);
-        }
-        T* gzi = static_cast<T*>(p.gzi) + seq * M;
-#pragma unroll
-        for (int i = 0; i < M; ++i) gzi[i] = w2[i];
-    }
-    // a7: re-run with the exact carry, emit dx, accumulate the coefficient sums.
-    T G[NG];
-#pragma unroll
-    for (int k = 0; k < NG; ++k) G[k] = T(0);
-    const bool has_neg = (p0 + s0) < 0;                 // chunk reaches before n = 0
-#pragma unroll
-    for (int g = L / W - 1; g >= 0; --g) {
-        V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
-        if constexpr (FORM == 1) {
-            const V xv = *reinterpret_cast<const V*>(s2 + pidx<T>(s0 + g * W));
-            const V yv = *reinterpret_cast<const V*>(s3 + pidx<T>(s0 + g * W));
+        for (int g = L / W - 1; g >= 0; --g) {
+            const V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
 #pragma unroll
             for (int e = W - 1; e >= 0; --e) {
-                const T dy = vget(dv, e), xx = vget(xv, e), yy = vget(yv, e);
-                T dx = bc[0] * dy;
-#pragma unroll
-                for (int i = 0; i < M; ++i) dx = fma(cc[i], d[i], dx);     // Eq.8: c^T dz + b0 dy
-#pragma unroll
-                for (int i = 0; i < M; ++i) { G[i] = fma(d[i], xx, G[i]); G[M + i] = fma(d[i], yy, G[M + i]); }
-                G[2 * M] = fma(dy, xx, G[2 * M]);
-                vset(dv, e, dx);
-                adj_tdf_step<T, M>(d, dy, ac);
+                if constexpr (FORM == 1) adj_tdf_step<T, M>(d, vget(dv, e), ac);
+                else adj_df_step<T, M>(d, vget(dv, e), bc, ac);
             }
-        } else {
+        }
+        IIRG_TRACE(p.trace, tk, 1);
+        // a6: carries (transposed powers), tiles last -> first.
+        double S[M];
 #pragma unroll
-            for (int e = W - 1; e >= 0; --e) {
-                const int n = s0 + g * W + e;                 // tile-local time index
-                const T dy = vget(dv, e);
-                const T dx = adj_df_step<T, M>(d, dy, bc, ac); // dx(n), then d <- dz(n-1)
-                const T gmask = (!has_neg || p0 + n >= 0) ? dx : T(0);
+        for (int i = 0; i < M; ++i) S[i] = (double)d[i];
+        warp_scan<M, true>(st, lane, S);
+        double E[M];
 #pragma unroll
-                for (int k = 0; k <= M; ++k) {
-                    const T uk = s2[pidx<T>(n - k + HALO)];
-                    G[k] = fma(dy, uk, G[k]);                          // Gb[k] = sum dy u(n-k)
-                    if (k >= 1) G[M + k] = fma(gmask, uk, G[M + k]);  // Ga[k] = sum dx u(n-k)
+        for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
+        if (lane == 31) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
+        }
+        __syncthreads();
+        if (warp == 0) {
+            double X0[M];
+            const T* gzf = static_cast<const T*>(p.gzf);
+#pragma unroll
+            for (int i = 0; i < M; ++i) X0[i] = (gzf != nullptr && jr == 0) ? (double)gzf[seq * M + i] : 0.0;
+            IIRG_TRACE(p.trace, tk, 3);
+            tile_carry<M, true>(st, tb, lane, s_agg, s_xw, jr, seq, X0, p.cw);
+            IIRG_TRACE(p.trace, tk, 4);
+        }
+        __syncthreads();
+        {
+            double xw[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
+            mv_acc_lane_s<M, true>(st + TB::PLT, 32, lane, xw, E);
+        }
+        T din[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) { din[i] = (T)E[i]; d[i] = din[i]; }
+        cp_async_wait<1>();                                          // x, y / u of this tile
+        __syncthreads();
+
+        // grad_zi = dz(-1) (Eq.9, A.3): the thread whose chunk holds n = 0 walks down
+        // to it before the emit pass overwrites dy with dx.
+        if (p.gzi != nullptr && p0 + s0 <= 0 && p0 + s0 + L > 0) {
+            T w2[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) w2[i] = din[i];
+            for (int n = s0 + L - 1; n >= (int)(-p0); --n) {
+                const T dy = dys[pidx<T>(n)];
+                if constexpr (FORM == 1) adj_tdf_step<T, M>(w2, dy, ac);
+                else (void)adj_df_step<T, M>(w2, dy, bc, ac);
+            }
+            T* gzi = static_cast<T*>(p.gzi) + seq * M;
+#pragma unroll
+            for (int i = 0; i < M; ++i) gzi[i] = w2[i];
+        }
+        // a7: re-run with the exact carry, emit dx, accumulate the coefficient sums.
+        T G[NG];
+#pragma unroll
+        for (int k = 0; k < NG; ++k) G[k] = T(0);
+        const bool has_neg = (p0 + s0) < 0;                 // chunk reaches before n = 0
+#pragma unroll
+        for (int g = L / W - 1; g >= 0; --g) {
+            V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
+            if constexpr (FORM == 1) {
+                const V xv = *reinterpret_cast<const V*>(s2 + pidx<T>(s0 + g * W));
+                const V yv = *reinterpret_cast<const V*>(s3 + pidx<T>(s0 + g * W));
+#pragma unroll
+                for (int e = W - 1; e >= 0; --e) {
+                    const T dy = vget(dv, e), xx = vget(xv, e), yy = vget(yv, e);
+                    T dx = bc[0] * dy;
+#pragma unroll
+                    for (int i = 0; i < M; ++i) dx = fma(cc[i], d[i], dx);     // Eq.8: c^T dz + b0 dy
+#pragma unroll
+                    for (int i = 0; i < M; ++i) { G[i] = fma(d[i], xx, G[i]); G[M + i] = fma(d[i], yy, G[M + i]); }
+                    G[2 * M] = fma(dy, xx, G[2 * M]);
+                    vset(dv, e, dx);
+                    adj_tdf_step<T, M>(d, dy, ac);
                 }
-                vset(dv, e, dx);
+            } else {
+#pragma unroll
+                for (int e = W - 1; e >= 0; --e) {
+                    const int n = s0 + g * W + e;                 // tile-local time index
+                    const T dy = vget(dv, e);
+                    const T dx = adj_df_step<T, M>(d, dy, bc, ac); // dx(n), then d <- dz(n-1)
+                    const T gmask = (!has_neg || p0 + n >= 0) ? dx : T(0);
+#pragma unroll
+                    for (int k = 0; k <= M; ++k) {
+                        const T uk = s2[pidx<T>(n - k + HALO)];
+                        G[k] = fma(dy, uk, G[k]);                          // Gb[k] = sum dy u(n-k)
+                        if (k >= 1) G[M + k] = fma(gmask, uk, G[M + k]);  // Ga[k] = sum dx u(n-k)
+                    }
+                    vset(dv, e, dx);
+                }
+            }
+            *reinterpret_cast<V*>(dys + pidx<T>(s0 + g * W)) = dv;   // dx in place
+        }
+        // warp reduction of the partial sums (fp64, fixed order)
+        if (p.want_coef) {
+#pragma unroll
+            for (int k = 0; k < NG; ++k) {
+                double s = (double)G[k];
+#pragma unroll
+                for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                if (lane == 0) s_red[warp][k] = s;
             }
         }
-        *reinterpret_cast<V*>(dys + pidx<T>(s0 + g * W)) = dv;   // dx in place
-    }
-    // warp reduction of the partial sums (fp64, fixed order)
-    if (p.want_coef) {
-#pragma unroll
-        for (int k = 0; k < NG; ++k) {
-            double s = (double)G[k];
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) s_red[warp][k] = s;
-        }
-    }
-    __syncthreads();
-    IIRG_TRACE(p.trace, tk, 5);
-    if (p.gx != nullptr) tile_store<T, TS>(static_cast<T*>(p.gx) + roff, dys, p0, p.Tlen, p.vec);
-    IIRG_TRACE(p.trace, tk, 6);
+        __syncthreads();
+        IIRG_TRACE(p.trace, tk, 5);
+        // x, y / u of the next tile can now stream into s2 / s3
+        if (tkn < ntot) bwd_issue_xy<T, M, FORM>(p, tkn, s2, s3);
+        cp_async_commit();
+        if (p.gx != nullptr) tile_store<T, TS>(static_cast<T*>(p.gx) + roff, dys, p0, p.Tlen, p.vec);
+        IIRG_TRACE(p.trace, tk, 6);
 
-    if (p.want_coef) {
-        // fused a8: group of 32 tiles -> group sum; last group of the set -> chain rule.
-        const bool shared = p.ncoef == 1;
-        const int64_t per_set = shared ? p.B * p.ntiles : p.ntiles;
-        const int64_t set = shared ? 0 : seq;
-        const int64_t li = shared ? seq * p.ntiles + jt : jt;          // index within the set
-        const int64_t gi = li >> 5;
-        const int64_t ngroups = (per_set + 31) >> 5;
-        const int gsize = (int)min((int64_t)32, per_set - (gi << 5));
-        double* part = p.partial + set * per_set * NG;
-        double* part2 = p.partial2 + set * ngroups * NG;
-        if (tid < NG) {
-            double s = 0.0;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) s += s_red[w][tid];
-            __stcg(part + li * NG + tid, s);
-            __threadfence();
-        }
-        __syncthreads();
-        if (tid == 0) s_fin = (atomicAdd(p.gcnt + set * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
-        __syncthreads();
-        if (s_fin) {                                   // last tile of its group
-            __threadfence();
+        if (p.want_coef) {
+            // fused a8: group of 32 tiles -> group sum; last group of the set -> chain rule.
+            const bool shared = p.ncoef == 1;
+            const int64_t per_set = shared ? p.B * p.ntiles : p.ntiles;
+            const int64_t cset = shared ? 0 : seq;
+            const int64_t li = shared ? seq * p.ntiles + jt : jt;          // index within the set
+            const int64_t gi = li >> 5;
+            const int64_t ngroups = (per_set + 31) >> 5;
+            const int gsize = (int)min((int64_t)32, per_set - (gi << 5));
+            double* part = p.partial + cset * per_set * NG;
+            double* part2 = p.partial2 + cset * ngroups * NG;
             if (tid < NG) {
                 double s = 0.0;
-                for (int t = 0; t < gsize; ++t) s += __ldcg(part + ((gi << 5) + t) * NG + tid);
-                __stcg(part2 + gi * NG + tid, s);
+#pragma unroll
+                for (int w = 0; w < NW; ++w) s += s_red[w][tid];
+                __stcg(part + li * NG + tid, s);
                 __threadfence();
             }
             __syncthreads();
-            if (tid == 0) {
-                p.gcnt[set * ngroups + gi] = 0u;
-                s_fin = (atomicAdd(p.scnt + set, 1u) == (unsigned)ngroups - 1u) ? 2u : 0u;
-            }
+            if (tid == 0) s_fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
             __syncthreads();
-            if (s_fin == 2u) {                          // last group of the set
+            if (s_fin) {                                   // last tile of its group
                 __threadfence();
                 if (tid < NG) {
                     double s = 0.0;
-                    for (int64_t g2 = 0; g2 < ngroups; ++g2) s += __ldcg(part2 + g2 * NG + tid);
-                    s_G[tid] = s;
+                    for (int t = 0; t < gsize; ++t) s += __ldcg(part + ((gi << 5) + t) * NG + tid);
+                    __stcg(part2 + gi * NG + tid, s);
+                    __threadfence();
                 }
                 __syncthreads();
                 if (tid == 0) {
-                    chain_rule<T, M, FORM>(s_G, tb,
-                                           p.gb == nullptr ? nullptr : static_cast<T*>(p.gb) + set * (M + 1),
-                                           p.ga == nullptr ? nullptr : static_cast<T*>(p.ga) + set * (M + 1));
-                    p.scnt[set] = 0u;
+                    p.gcnt[cset * ngroups + gi] = 0u;
+                    s_fin = (atomicAdd(p.scnt + cset, 1u) == (unsigned)ngroups - 1u) ? 2u : 0u;
+                }
+                __syncthreads();
+                if (s_fin == 2u) {                          // last group of the set
+                    __threadfence();
+                    if (tid < NG) {
+                        double s = 0.0;
+                        for (int64_t g2 = 0; g2 < ngroups; ++g2) s += __ldcg(part2 + g2 * NG + tid);
+                        s_G[tid] = s;
+                    }
+                    __syncthreads();
+                    if (tid == 0) {
+                        chain_rule<T, M, FORM>(s_G, tb,
+                                               p.gb == nullptr ? nullptr : static_cast<T*>(p.gb) + cset * (M + 1),
+                                               p.ga == nullptr ? nullptr : static_cast<T*>(p.ga) + cset * (M + 1));
+                        p.scnt[cset] = 0u;
+                    }
                 }
             }
         }
+        if (tid == 0) s_tk[0] = tk2;
+        __syncthreads();
+        stage ^= 1;
+        tk = tkn;
+        tkn = s_tk[0];
     }
-    ws_cleanup(p.cw, p.B, (unsigned)(p.B * p.ntiles));
-    IIRG_TRACE(p.trace, tk, 7);
+    cta_exit<M>(p.cw, p.B, gridDim.x);
 }
 
 }  // namespace iirg

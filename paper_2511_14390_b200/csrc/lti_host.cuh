@@ -14,9 +14,23 @@ inline void set_smem(K kernel, size_t bytes) {
 template <typename T, int M, int FORM>
 struct LtiOps {
     static constexpr int TS = NT * Chunk<T>::L;
-    static size_t fwd_smem() { return (size_t)pidx<T>(TS) * sizeof(T) * (FORM == 0 ? 2 : 1); }
-    static size_t bwd_smem() {
-        return ((size_t)pidx<T>(TS) + pidx<T>(TS + HALO) + (FORM == 1 ? pidx<T>(TS) : 0)) * sizeof(T);
+    static size_t fwd_smem() { return Smem<T, M>::fwd(FORM); }
+    static size_t bwd_smem() { return Smem<T, M>::bwd(FORM); }
+    // persistent grid: as many CTAs as fit on the device at once (<= tiles)
+    template <typename K>
+    static unsigned grid_for(K kernel, size_t smem, int64_t ntot) {
+        static int cache[64] = {0};                 // resident CTAs per device
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int g = (dev >= 0 && dev < 64) ? cache[dev] : 0;
+        if (g == 0) {
+            int nsm = 0, per = 0;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, NT, smem);
+            g = nsm * (per > 0 ? per : 1);
+            if (dev >= 0 && dev < 64) cache[dev] = g;
+        }
+        return (unsigned)(ntot < (int64_t)g ? ntot : (int64_t)g);
     }
     static iir_status_t prep(const iir_desc_t* d, const Layout& L, const void* b, const void* a, double* tab,
                              cudaStream_t st) {
@@ -34,9 +48,10 @@ struct LtiOps {
     static iir_status_t fwd(const iir_desc_t* d, const Layout& L, const LtiFwdArgs& args, cudaStream_t st) {
         static std::once_flag once;
         std::call_once(once, [] { set_smem(lti_fwd_kernel<T, M, FORM>, fwd_smem()); });
+        const unsigned grid = grid_for(lti_fwd_kernel<T, M, FORM>, fwd_smem(), L.ntot);
         return launch(K_LTI_FWD, st, [&] {
             cudaLaunchConfig_t cfg{};
-            cfg.gridDim = dim3((unsigned)L.ntot);
+            cfg.gridDim = dim3(grid);
             cfg.blockDim = dim3(NT);
             cfg.dynamicSmemBytes = fwd_smem();
             cfg.stream = st;
@@ -51,8 +66,9 @@ struct LtiOps {
     static iir_status_t bwd(const iir_desc_t* d, const Layout& L, const LtiBwdArgs& args, cudaStream_t st) {
         static std::once_flag once;
         std::call_once(once, [] { set_smem(lti_bwd_kernel<T, M, FORM>, bwd_smem()); });
+        const unsigned grid = grid_for(lti_bwd_kernel<T, M, FORM>, bwd_smem(), L.ntot);
         return launch(K_LTI_BWD, st, [&] {
-            lti_bwd_kernel<T, M, FORM><<<(unsigned)L.ntot, NT, bwd_smem(), st>>>(args);
+            lti_bwd_kernel<T, M, FORM><<<grid, NT, bwd_smem(), st>>>(args);
         });
     }
 };
