@@ -27,10 +27,11 @@ constexpr int PREP_THREADS = 256;
 template <int M> struct Tab {
     static constexpr int M2 = M * M;
     static constexpr int PL = 0;                       // A_f^(L 2^d), d = 0..4          [d][i][j]
-    static constexpr int PLT = PL + 5 * M2;            // A_f^(L t),   t = 0..31         [i][j][t]
-    static constexpr int PW = PLT + 32 * M2;           // A_f^(32L 2^d), d < LOG_NW      [d][i][j]
+    static constexpr int PW = PL + 5 * M2;             // A_f^(32L 2^d), d < LOG_NW      [d][i][j]
     static constexpr int PWT = PW + LOG_NW * M2;       // A_f^(32L w), w = 0..NW-1       [i][j][w]
-    static constexpr int PQ = PWT + NW * M2;           // A_f^(k 32^l TS), k = 0..31     [l][i][j][k]
+    static constexpr int SMALL = PWT + NW * M2;        // [0, SMALL): staged in shared memory per CTA
+    static constexpr int PLT = SMALL;                  // A_f^(L t),   t = 0..31         [i][j][t]
+    static constexpr int PQ = PLT + 32 * M2;           // A_f^(k 32^l TS), k = 0..31     [l][i][j][k]
     static constexpr int COEF = PQ + LEVELS * 32 * M2; // b'[0..M], a'[0..M], c[0..M-1]
     static constexpr int A0 = COEF + 3 * M + 2;        // a0 (un-normalised)
     static constexpr int SIZE = (A0 + 1 + 31) / 32 * 32;
@@ -194,6 +195,7 @@ __global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restr
         const int e = w / 32, t = w % 32;
         tb[TB::PLT + w] = mat[(S::PLT + t) * M2 + e];
     }
+    (void)0;
     for (int w = tid; w < nlev * 32 * M2; w += PREP_THREADS) {
         const int l = w / (32 * M2), r = w % (32 * M2), e = r / 32, k = r % 32;
         tb[TB::PQ + w] = mat[(S::Q + l * 33 + k) * M2 + e];
@@ -253,420 +255,6 @@ __device__ __forceinline__ T adj_df_step(T (&d)[M], T dy, const T (&bc)[M + 1], 
 }
 
 // ---------------------------------------------------------------------------
-// Grid-level carry bookkeeping (workspace pointers), shared by fwd and bwd.
-struct CarryWs {
-    unsigned* ticket;            // tile ticket counter
-    unsigned* done;              // CTAs finished (the last one cleans the workspace)
-    double* agg[LEVELS];         // level-l block aggregates [seq][block][M] (sentinel = not ready)
-    int64_t nblk[LEVELS];        // blocks per sequence at level l (ceil(ntiles / 32^l))
-    int nlev;                    // levels in use
-};
-
-struct LtiFwdArgs {
-    const void* b; const void* a; int64_t coef_stride;           // raw coefficients (local pass)
-    const void* x; const void* zi; void* y; void* zf; void* u;    // u: DF tape signal
-    const double* tab; int64_t tab_stride;                        // 0 for SHARED
-    CarryWs cw;
-    int64_t B, Tlen; int ntiles; int vec;
-    unsigned long long* trace;                                    // debug: per-tile phase times
-};
-
-struct LtiBwdArgs {
-    const void* gy; const void* gzf; const void* x; const void* y; const void* u; const void* zi;
-    void* gx; void* gzi; void* gb; void* ga; int want_coef;
-    double* partial; double* partial2; unsigned* gcnt; unsigned* scnt;   // fused finalize
-    int64_t ncoef;
-    const double* tab; int64_t tab_stride;
-    CarryWs cw;
-    int64_t B, Tlen; int ntiles; int vec;
-    unsigned long long* trace;
-};
-
-// Normalised coefficients in T, straight from the caller's b, a (the same
-// rounding as the prologue's fp64 b/a0, a/a0 cast to T).
-template <typename T, int M>
-__device__ __forceinline__ void raw_coefs(const T* __restrict__ b, const T* __restrict__ a, T (&bc)[M + 1],
-                                          T (&ac)[M + 1]) {
-    const double a0 = (double)__ldg(a);
-#pragma unroll
-    for (int k = 0; k <= M; ++k) { bc[k] = (T)((double)__ldg(b + k) / a0); ac[k] = (T)((double)__ldg(a + k) / a0); }
-}
-template <typename T, int M>
-__device__ __forceinline__ void load_coefs(const double* __restrict__ tb, T (&bc)[M + 1], T (&ac)[M + 1], T (&cc)[M]) {
-    using TB = Tab<M>;
-#pragma unroll
-    for (int k = 0; k <= M; ++k) { bc[k] = (T)__ldg(tb + TB::COEF + k); ac[k] = (T)__ldg(tb + TB::COEF + M + 1 + k); }
-#pragma unroll
-    for (int k = 0; k < M; ++k) cc[k] = (T)__ldg(tb + TB::COEF + 2 * (M + 1) + k);
-}
-
-// Warp-level inclusive Kogge-Stone scan of chunk aggregates in fp64:
-//   S_t <- P^(2^d) S_{t-2^d} + S_t, P = A_f^L (TR: transposed for the adjoint).
-template <int M, bool TR>
-__device__ __forceinline__ void warp_scan(const double* st, int lane, double (&S)[M]) {
-    using TB = Tab<M>;
-#pragma unroll
-    for (int d = 0; d < 5; ++d) {
-        const int off = 1 << d;
-        double O[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) O[i] = shfl_up_d(S[i], off);
-        if (lane >= off) mv_acc_s<M, TR>(st + TB::PL + d * M * M, O, S);
-    }
-}
-
-template <int M>
-__device__ __forceinline__ void warp_sum(double (&v)[M]) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1)
-#pragma unroll
-        for (int i = 0; i < M; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
-}
-
-template <int M>
-__device__ __forceinline__ void publish(double* dst, const double (&v)[M], int lane) {
-    if (lane == 0) {
-#pragma unroll
-        for (int i = 0; i < M; ++i) __stcg(dst + i, v[i]);
-    }
-}
-
-// Wait until a look-back payload slot is published and read it.  One element
-// is polled with exponential back-off (thousands of warps may wait on the same
-// few slots; unthrottled polling floods that L2 slice and delays the very
-// store being waited for), then all M are read and re-checked.
-template <int M>
-__device__ __forceinline__ void wait_slot(const double* src, double (&v)[M]) {
-    unsigned ns = 32;
-    unsigned long long t_spin = 0;
-    for (;;) {
-        if (!is_sentinel(ld_relaxed(src))) {
-            bool ready = true;
-#pragma unroll
-            for (int i = 0; i < M; ++i) { v[i] = ld_relaxed(src + i); ready = ready && !is_sentinel(v[i]); }
-            if (ready) return;
-        }
-        __nanosleep(ns);
-        if (ns < 1024) ns *= 2;
-        else {                                   // a stuck look-back is a bug: report, don't hang
-            const unsigned long long now = gtimer();
-            if (t_spin == 0) t_spin = now;
-            else if (now - t_spin > 4000000000ull) {
-                printf("iirgrad: look-back slot %p never published\n", (const void*)src);
-                __trap();
-            }
-        }
-    }
-}
-
-// Block + grid carry propagation, executed by warp 0 of the CTA.
-//   s_agg[w]: warp-local aggregates (zero-start prefix at the end of warp w).
-//   Produces s_xw[w]: the exact state entering warp w's first chunk.
-// Grid level: tile j (scan order within its sequence) has base-32 digits d_l.
-// With AGG^(0) = tile aggregates (tile 0's includes the initial state X0),
-// AGG^(l+1)_blk = sum_{d<32} Q_l^(31-d) AGG^(l)_{32 blk + d}, Q_l = A_f^(32^l TS):
-//   T_l = sum_{d < d_l} Q_l^(d_l - 1 - d) AGG^(l)_{(j >> 5l) - d_l + d}
-//   X_j = T_0 + Q_0^d_0 (T_1 + Q_1^d_1 (T_2 + ...))
-// Each T_l is one lane-parallel round (lane d reads one aggregate) and a fixed
-// butterfly sum, so the result is bitwise deterministic and no tile ever waits
-// on a serial chain of inclusive prefixes.  The last tile of a level-l block
-// publishes AGG^(l+1) = Q_l T_l + AGG^(l)_own.
-template <int M, bool TR>
-__device__ __forceinline__ void tile_carry(const double* st, const double* __restrict__ tb, int lane,
-                                           double (*s_agg)[M],
-                                           double (*s_xw)[M], int jt, int64_t seq, const double (&X0)[M],
-                                           const CarryWs& cw) {
-    __shared__ double s_T[LEVELS][M];
-    using TB = Tab<M>;
-    constexpr int M2 = M * M;
-    double J[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) J[i] = (lane < NW) ? s_agg[lane][i] : 0.0;
-#pragma unroll
-    for (int d = 0; d < LOG_NW; ++d) {
-        const int off = 1 << d;
-        double O[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) O[i] = shfl_up_d(J[i], off);
-        if (lane >= off && lane < NW) mv_acc_s<M, TR>(st + TB::PW + d * M2, O, J);
-    }
-    double Jex[M], G[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-        Jex[i] = shfl_up_d(J[i], 1);
-        if (lane == 0) Jex[i] = 0.0;
-        G[i] = shfl_d(J[i], NW - 1);           // tile aggregate (all lanes)
-    }
-    double X[M];                               // state entering this tile
-#pragma unroll
-    for (int i = 0; i < M; ++i) X[i] = X0[i];
-    if (jt == 0) mv_acc_lane<M, TR>(tb + TB::PQ, 32, 1, X0, G);   // tile 0 carries the initial state
-    publish<M>(cw.agg[0] + (seq * cw.nblk[0] + jt) * M, G, lane);
-    if (jt > 0) {
-        // T_l (one lane-parallel round per level), kept in shared memory to spare
-        // registers.  A tile that closes a level-(l+1) block publishes its aggregate
-        // right after T_l, before waiting on any higher level: no cross-block chain.
-        int dl[LEVELS];
-        bool closing = true;                   // all lower digits were 31 so far
-        double Own[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) Own[i] = G[i];
-#pragma unroll
-        for (int l = 0; l < LEVELS; ++l) {
-            dl[l] = (jt >> (5 * l)) & 31;
-            double Tv[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) Tv[i] = 0.0;
-            if (l < cw.nlev && dl[l] > 0) {
-                const int64_t base = seq * cw.nblk[l] + (jt >> (5 * l)) - dl[l];
-                if (lane < dl[l]) {
-                    const double* src = cw.agg[l] + (base + lane) * M;
-                    double v[M];
-                    wait_slot<M>(src, v);
-                    (void)seq;
-                    mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, dl[l] - 1 - lane, v, Tv);
-                }
-                warp_sum<M>(Tv);
-            }
-            if (lane == 0) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) s_T[l][i] = Tv[i];
-            }
-            closing = closing && dl[l] == 31;
-            if (closing && l + 1 < cw.nlev) {
-                mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, 1, Tv, Own);   // Own = Q_l T_l + Own
-                const int64_t bi = seq * cw.nblk[l + 1] + (jt >> (5 * (l + 1)));
-                publish<M>(cw.agg[l + 1] + bi * M, Own, lane);
-            }
-        }
-        __syncwarp();
-        // X = T_0 + Q_0^d0 (T_1 + Q_1^d1 (T_2 + Q_2^d2 T_3))
-        double R[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) R[i] = 0.0;
-#pragma unroll
-        for (int l = LEVELS - 1; l >= 0; --l) {
-            if (l < cw.nlev) {
-                double R2[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) R2[i] = s_T[l][i];
-                if (l + 1 < cw.nlev) mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, dl[l], R, R2);
-#pragma unroll
-                for (int i = 0; i < M; ++i) R[i] = R2[i];
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < M; ++i) X[i] = R[i];
-    }
-    if (lane < NW) {                           // state entering warp `lane`
-        double xw[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) xw[i] = Jex[i];
-        mv_acc_lane_s<M, TR>(st + TB::PWT, NW, lane, X, xw);
-#pragma unroll
-        for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
-    }
-}
-
-// Persistent CTAs exit once the ticket counter runs past the last tile; the last
-// CTA to exit restores the workspace to its zero state, so the next call on the
-// same (stream-ordered) workspace needs no memset.  No fence is needed: every
-// CTA's reads of the status words completed (their values were consumed) and
-// its final ticket grab happened before its exit increment.
-template <int M>
-__device__ __forceinline__ void cta_exit(const CarryWs& cw, int64_t B, unsigned nctas) {
-    __shared__ unsigned s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(cw.done, 1u) == nctas - 1u) ? 1u : 0u;
-    __syncthreads();
-    if (s_last) {
-        for (int l = 0; l < cw.nlev; ++l)
-            for (int64_t i = threadIdx.x; i < B * cw.nblk[l] * M; i += blockDim.x) cw.agg[l][i] = sentinel();
-        if (threadIdx.x == 0) { *cw.ticket = 0u; *cw.done = 0u; }
-    }
-}
-
-// Stage the per-coefficient-set power tables PL | PLT | PW | PWT (Tab<M>::PQ
-// doubles, identical layout) into shared memory.
-template <int M>
-__device__ __forceinline__ void stage_tables(double* st, const double* __restrict__ tb) {
-    for (int i = threadIdx.x; i < Tab<M>::PQ; i += blockDim.x) st[i] = __ldg(tb + i);
-}
-
-template <typename T, int M>
-struct Smem {
-    static constexpr int TS = NT * Chunk<T>::L;
-    static constexpr int PT = pidx<T>(TS);               // one padded tile
-    static constexpr int PTH = pidx<T>(TS + HALO);       // padded tile with u history
-    static constexpr size_t tab_bytes = ((size_t)Tab<M>::PQ * 8 + 15) / 16 * 16;
-    static constexpr size_t fwd(int form) { return tab_bytes + (size_t)(2 * PT + (form == 0 ? PT : 0)) * sizeof(T); }
-    static constexpr size_t bwd(int form) {
-        return tab_bytes + (size_t)(2 * PT + PTH + (form == 1 ? PT : 0)) * sizeof(T);
-    }
-};
-
-// ---------------------------------------------------------------------------
-// Forward: a2-a4.  Persistent CTAs take tiles (TS samples of one sequence) in
-// ticket order and double-buffer them: tile k+1 streams into shared memory
-// (cp.async) while tile k is scanned.  Tickets interleave the sequences (ticket
-// t = tile t / B of sequence t % B), so concurrent tiles rarely wait.
-template <typename T, int M, int FORM>
-__global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
-    constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
-    using V = typename Vec<T>::type;
-    using TB = Tab<M>;
-    using SM = Smem<T, M>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* st = reinterpret_cast<double*>(smem_raw);
-    T* xb = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);     // 2 stages: x -> y in place
-    T* us = xb + 2 * SM::PT;                                      // DF: u tile
-    __shared__ double s_agg[NW][M];
-    __shared__ double s_xw[NW][M];
-    __shared__ unsigned s_tk[2];
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned ntot = (unsigned)(p.B * p.ntiles);
-    // tickets are taken two tiles ahead so the atomic's latency hides behind a tile
-    if (tid == 0) { s_tk[0] = atomicAdd(p.cw.ticket, 1u); s_tk[1] = atomicAdd(p.cw.ticket, 1u); }
-    __syncthreads();
-    unsigned tk = s_tk[0], tkn = s_tk[1];
-    if (tk < ntot) {
-        const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
-        const int jt = (int)(tk / (unsigned long long)p.B);
-        tile_load_async<T, TS>(xb, static_cast<const T*>(p.x) + seq * p.Tlen, (int64_t)jt * TS, p.Tlen, p.vec);
-    }
-    cp_async_commit();
-    int stage = 0;
-    int64_t tab_set = -1, coef_set = -1;
-    bool waited = false;
-    T bc[M + 1], ac[M + 1];
-    while (tk < ntot) {
-        unsigned tk2 = 0u;
-        if (tid == 0) tk2 = atomicAdd(p.cw.ticket, 1u);          // consumed at the end of the iteration
-        if (tkn < ntot) {
-            const int64_t sq = (int64_t)(tkn % (unsigned long long)p.B);
-            const int jn = (int)(tkn / (unsigned long long)p.B);
-            tile_load_async<T, TS>(xb + (stage ^ 1) * SM::PT, static_cast<const T*>(p.x) + sq * p.Tlen,
-                                   (int64_t)jn * TS, p.Tlen, p.vec);
-        }
-        cp_async_commit();
-        const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
-        const int jt = (int)(tk / (unsigned long long)p.B);
-        const int64_t p0 = (int64_t)jt * TS;
-        T* xs = xb + stage * SM::PT;
-        IIRG_TRACE(p.trace, tk, 0);
-        const int64_t cs = p.coef_stride == 0 ? 0 : seq;
-        if (cs != coef_set) {
-            raw_coefs<T, M>(static_cast<const T*>(p.b) + cs * p.coef_stride,
-                            static_cast<const T*>(p.a) + cs * p.coef_stride, bc, ac);
-            coef_set = cs;
-        }
-        cp_async_wait<1>();
-        __syncthreads();
-
-        // a2: local pass from the zero state over this thread's chunk.
-        const int s0 = tid * L;
-        T v[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) v[i] = T(0);
-#pragma unroll
-        for (int g = 0; g < L / W; ++g) {
-            const V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
-#pragma unroll
-            for (int e = 0; e < W; ++e) { T du; fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, du); }
-        }
-        IIRG_TRACE(p.trace, tk, 1);
-        // a3: carries in fp64; the power tables come from the prologue (PDL wait once).
-        const double* tb = p.tab + seq * p.tab_stride;
-        const int64_t set = p.tab_stride == 0 ? 0 : seq;
-        if (set != tab_set) {
-            if (!waited) { pdl_wait(); waited = true; }
-            stage_tables<M>(st, tb);
-            tab_set = set;
-            __syncthreads();
-        }
-        IIRG_TRACE(p.trace, tk, 2);
-        double S[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) S[i] = (double)v[i];
-        warp_scan<M, false>(st, lane, S);
-        double E[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
-        if (lane == 31) {
-#pragma unroll
-            for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
-        }
-        __syncthreads();
-        if (warp == 0) {
-            double X0[M];
-            const T* zi = static_cast<const T*>(p.zi);
-#pragma unroll
-            for (int i = 0; i < M; ++i) X0[i] = (zi != nullptr && jt == 0) ? (double)zi[seq * M + i] : 0.0;
-            IIRG_TRACE(p.trace, tk, 3);
-            tile_carry<M, false>(st, tb, lane, s_agg, s_xw, jt, seq, X0, p.cw);
-            IIRG_TRACE(p.trace, tk, 4);
-        }
-        __syncthreads();
-        // state entering this thread's chunk: E + A_f^(L lane) x_warp
-        {
-            double xw[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
-            mv_acc_lane_s<M, false>(st + TB::PLT, 32, lane, xw, E);
-        }
-        T vin[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) { vin[i] = (T)E[i]; v[i] = vin[i]; }
-        // zf = v(T): the thread holding sample T-1 walks its chunk up to it (before
-        // the emit pass overwrites x with y).
-        if (p.zf != nullptr) {
-            const int64_t eL = p.Tlen - 1 - p0;
-            if (eL >= s0 && eL < s0 + L) {
-                T w2[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) w2[i] = vin[i];
-                for (int n = s0; n <= (int)eL; ++n) { T du; fwd_step<T, M, FORM>(w2, xs[pidx<T>(n)], bc, ac, du); }
-                T* zf = static_cast<T*>(p.zf) + seq * M;
-#pragma unroll
-                for (int i = 0; i < M; ++i) zf[i] = w2[i];
-            }
-        }
-        // a4: re-run from the exact carry-in, emit y (and u for DF) in place.
-#pragma unroll
-        for (int g = 0; g < L / W; ++g) {
-            V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
-            V uv;
-#pragma unroll
-            for (int e = 0; e < W; ++e) {
-                T uu;
-                const T yy = fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, uu);
-                vset(xv, e, yy);
-                vset(uv, e, uu);
-            }
-            *reinterpret_cast<V*>(xs + pidx<T>(s0 + g * W)) = xv;
-            if constexpr (FORM == 0) *reinterpret_cast<V*>(us + pidx<T>(s0 + g * W)) = uv;
-        }
-        __syncthreads();
-        IIRG_TRACE(p.trace, tk, 5);
-        T* yrow = static_cast<T*>(p.y) + seq * p.Tlen;
-        tile_store<T, TS>(yrow, xs, p0, p.Tlen, p.vec);
-        if constexpr (FORM == 0) {
-            T* urow = static_cast<T*>(p.u) + seq * p.Tlen;
-            tile_store<T, TS>(urow, us, p0, p.Tlen, p.vec);
-        }
-        IIRG_TRACE(p.trace, tk, 6);
-        if (tid == 0) s_tk[0] = tk2;
-        __syncthreads();                                          // also: stores have read this stage
-        stage ^= 1;
-        tk = tkn;
-        tkn = s_tk[0];
-    }
-    if (!waited) pdl_wait();
-    cta_exit<M>(p.cw, p.B, gridDim.x);
-}
-
-// ---------------------------------------------------------------------------
 // a8: gradient finalize, fused into the backward kernel.  Fixed-order fp64 sum
 // of the per-tile partials (groups of 32 tiles, then the groups; over the
 // whole local batch for SHARED), then the chain rule from the state-space sums
@@ -706,56 +294,448 @@ __device__ __forceinline__ void chain_rule(const double* __restrict__ G, const d
 }
 
 // ---------------------------------------------------------------------------
-// Backward: a5-a8.  Tiles are aligned to the END of each sequence and taken
-// last to first; inside a tile thread t owns chunk NT-1-t, walked backwards.
-// Persistent CTAs double-buffer dy (the local pass needs only dy); x, y (TDF)
-// or u (DF) of tile k+1 stream in once tile k's emit pass has finished.
+// Kernel arguments.  Scan order: forward tiles in time order (tile jt covers
+// [jt TS, (jt+1) TS)), backward tiles in reverse time order (tile jr covers
+// [T - (jr+1) TS, T - jr TS)).  agg / carry are indexed [seq][scan index][M].
+struct LtiFwdArgs {
+    const void* b; const void* a; int64_t coef_stride;           // raw coefficients (local pass)
+    const void* x; const void* zi; void* y; void* zf; void* u;    // u: DF tape signal
+    const double* tab; int64_t tab_stride;                        // 0 for SHARED
+    double* agg;                                                  // tile aggregates (phase 1)
+    const double* carry;                                          // state entering each tile (phase 3)
+    int64_t B, Tlen; int ntiles; int vec;
+    unsigned long long* trace;                                    // debug: per-tile phase times
+};
+
+struct LtiBwdArgs {
+    const void* gy; const void* gzf; const void* x; const void* y; const void* u; const void* zi;
+    void* gx; void* gzi; void* gb; void* ga; int want_coef;
+    double* partial; double* partial2; unsigned* gcnt; unsigned* scnt;   // fused finalize
+    int64_t ncoef;
+    const double* tab; int64_t tab_stride;
+    double* agg; const double* carry;
+    int64_t B, Tlen; int ntiles; int vec;
+    unsigned long long* trace;
+};
+
+struct CarryArgs {
+    const double* agg; double* carry;
+    const void* x0; int x0_f64;                                   // zi (fwd) / grad_zf (bwd), may be NULL
+    const double* tab; int64_t tab_stride;
+    int64_t B; int ntiles;
+};
+
+// Normalised coefficients in T, straight from the caller's b, a (the same
+// rounding as the prologue's fp64 b/a0, a/a0 cast to T).
+template <typename T, int M>
+__device__ __forceinline__ void raw_coefs(const T* __restrict__ b, const T* __restrict__ a, T (&bc)[M + 1],
+                                          T (&ac)[M + 1]) {
+    const double a0 = (double)__ldg(a);
+#pragma unroll
+    for (int k = 0; k <= M; ++k) { bc[k] = (T)((double)__ldg(b + k) / a0); ac[k] = (T)((double)__ldg(a + k) / a0); }
+}
+template <typename T, int M>
+__device__ __forceinline__ void load_coefs(const double* __restrict__ tb, T (&bc)[M + 1], T (&ac)[M + 1], T (&cc)[M]) {
+    using TB = Tab<M>;
+#pragma unroll
+    for (int k = 0; k <= M; ++k) { bc[k] = (T)__ldg(tb + TB::COEF + k); ac[k] = (T)__ldg(tb + TB::COEF + M + 1 + k); }
+#pragma unroll
+    for (int k = 0; k < M; ++k) cc[k] = (T)__ldg(tb + TB::COEF + 2 * (M + 1) + k);
+}
+
+// Stage the small power tables (PL | PW | PWT) of this tile's coefficient set.
+template <int M>
+__device__ __forceinline__ void stage_small(double* st, const double* __restrict__ tb) {
+    for (int i = threadIdx.x; i < Tab<M>::SMALL; i += blockDim.x) st[i] = __ldg(tb + i);
+}
+
+// Warp-level inclusive Kogge-Stone scan of chunk aggregates in fp64:
+//   S_t <- P^(2^d) S_{t-2^d} + S_t, P = A_f^L (TR: transposed for the adjoint).
+template <int M, bool TR>
+__device__ __forceinline__ void warp_scan(const double* st, int lane, double (&S)[M]) {
+    using TB = Tab<M>;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        const int off = 1 << d;
+        double O[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) O[i] = shfl_up_d(S[i], off);
+        if (lane >= off) mv_acc_s<M, TR>(st + TB::PL + d * M * M, O, S);
+    }
+}
+
+// Block level (warp 0): inclusive scan of the NW warp aggregates with
+// A_f^(32 L 2^d); returns the exclusive prefix Jex (lanes < NW) and the tile
+// aggregate G (all lanes).
+template <int M, bool TR>
+__device__ __forceinline__ void block_scan(const double* st, int lane, double (*s_agg)[M], double (&Jex)[M],
+                                           double (&G)[M]) {
+    using TB = Tab<M>;
+    double J[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) J[i] = (lane < NW) ? s_agg[lane][i] : 0.0;
+#pragma unroll
+    for (int d = 0; d < LOG_NW; ++d) {
+        const int off = 1 << d;
+        double O[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) O[i] = shfl_up_d(J[i], off);
+        if (lane >= off && lane < NW) mv_acc_s<M, TR>(st + TB::PW + d * M * M, O, J);
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        Jex[i] = shfl_up_d(J[i], 1);
+        if (lane == 0) Jex[i] = 0.0;
+        G[i] = shfl_d(J[i], NW - 1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Phase 2 (a3/a6 across tiles): per sequence, the exact state entering every
+// tile from the tile aggregates:  X_0 = x0,  X_{j+1} = Q X_j + agg_j, Q = A_f^TS.
+// One CTA per sequence; thread t owns k consecutive tiles: a Horner pass gives
+// its aggregate, a block-wide Kogge-Stone scan with Q^(k 2^d) (fp64) gives its
+// entering state, and a second Horner pass writes X for each of its tiles.
+// Fixed order throughout: bitwise deterministic.
+constexpr int CARRY_THREADS = 256;
+
+template <int M, bool TR>
+__global__ void __launch_bounds__(CARRY_THREADS) lti_carry_kernel(const CarryArgs c) {
+    constexpr int M2 = M * M;
+    using TB = Tab<M>;
+    __shared__ double sQ[M2];                     // Q = A_f^TS (transposed for the adjoint)
+    __shared__ double sR[9][M2];                  // Q^(k 2^d), d = 0..8
+    __shared__ double sW[CARRY_THREADS / 32][M];
+    __shared__ double tmp[2][M2];
+    pdl_launch_dependents();
+    pdl_wait();                                   // aggregates of phase 1
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t seq = blockIdx.x;
+    const double* tb = c.tab + seq * c.tab_stride;
+    const int n = c.ntiles;
+    const int k = (n + CARRY_THREADS - 1) / CARRY_THREADS;
+    // Q from the level-0 power table (k = 1 entry), transposed for TR
+    for (int e = tid; e < M2; e += CARRY_THREADS) {
+        const int i = e / M, j = e % M;
+        sQ[e] = __ldg(tb + TB::PQ + (TR ? j * M + i : e) * 32 + 1);
+    }
+    __syncthreads();
+    // R_0 = Q^k by binary powering (M2 threads), R_{d+1} = R_d^2
+    auto mm = [&](double* dst, const double* A, const double* Bm) {
+        double s = 0.0;
+        const int e = tid, i = e / M, j = e % M;
+        if (e < M2)
+#pragma unroll
+            for (int q = 0; q < M; ++q) s = fma(A[i * M + q], Bm[q * M + j], s);
+        __syncthreads();
+        if (e < M2) dst[e] = s;
+        __syncthreads();
+    };
+    for (int e = tid; e < M2; e += CARRY_THREADS) {
+        sR[0][e] = (e / M == e % M) ? 1.0 : 0.0;
+        tmp[0][e] = sQ[e];
+    }
+    __syncthreads();
+    for (int kk = k; kk > 0; kk >>= 1) {
+        if (kk & 1) mm(sR[0], sR[0], tmp[0]);
+        if (kk > 1) mm(tmp[0], tmp[0], tmp[0]);
+    }
+    for (int d = 1; d < 9; ++d) mm(sR[d], sR[d - 1], sR[d - 1]);
+
+    const double* agg = c.agg + seq * (int64_t)n * M;
+    double* carry = c.carry + seq * (int64_t)n * M;
+    double X0[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        X0[i] = 0.0;
+        if (c.x0 != nullptr)
+            X0[i] = c.x0_f64 ? static_cast<const double*>(c.x0)[seq * M + i]
+                             : (double)static_cast<const float*>(c.x0)[seq * M + i];
+    }
+    const int i0 = tid * k, i1 = min(n, i0 + k);
+    // Horner over this thread's tiles (thread 0 starts from the initial state)
+    double S[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) S[i] = (tid == 0) ? X0[i] : 0.0;
+    for (int t = i0; t < i1; ++t) {
+        double Sn[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) Sn[i] = agg[(int64_t)t * M + i];
+        mv_acc_s<M, false>(sQ, S, Sn);
+#pragma unroll
+        for (int i = 0; i < M; ++i) S[i] = Sn[i];
+    }
+    if (i0 >= n) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) S[i] = 0.0;
+    }
+    // inclusive scan across threads: warp level then across warps
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        const int off = 1 << d;
+        double O[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) O[i] = shfl_up_d(S[i], off);
+        if (lane >= off) mv_acc_s<M, false>(sR[d], O, S);
+    }
+    if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) sW[warp][i] = S[i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        constexpr int NWC = CARRY_THREADS / 32;
+        double Wv[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) Wv[i] = (lane < NWC) ? sW[lane][i] : 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const int off = 1 << d;
+            double O[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) O[i] = shfl_up_d(Wv[i], off);
+            if (lane >= off && lane < NWC) mv_acc_s<M, false>(sR[5 + d], O, Wv);
+        }
+        double We[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) { We[i] = shfl_up_d(Wv[i], 1); if (lane == 0) We[i] = 0.0; }
+        __syncwarp();
+        if (lane < NWC) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) sW[lane][i] = We[i];
+        }
+    }
+    __syncthreads();
+    // entering state of this thread: exclusive lane prefix + Q^(k lane) (warp prefix)
+    double E[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
+    {
+        double Y[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) Y[i] = sW[warp][i];
+        // Y <- Q^(k lane) Y by the binary digits of lane
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+            if ((lane >> d) & 1) {
+                double Z[M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) Z[i] = 0.0;
+                mv_acc_s<M, false>(sR[d], Y, Z);
+#pragma unroll
+                for (int i = 0; i < M; ++i) Y[i] = Z[i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < M; ++i) E[i] += Y[i];
+    }
+    if (tid == 0) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) E[i] = X0[i];
+    }
+    // second Horner pass: state entering each tile
+    for (int t = i0; t < i1; ++t) {
+        double Sn[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) { carry[(int64_t)t * M + i] = E[i]; Sn[i] = agg[(int64_t)t * M + i]; }
+        mv_acc_s<M, false>(sQ, E, Sn);
+#pragma unroll
+        for (int i = 0; i < M; ++i) E[i] = Sn[i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+template <typename T, int M>
+struct Smem {
+    static constexpr int TS = NT * Chunk<T>::L;
+    static constexpr int PT = pidx<T>(TS);               // one padded tile
+    static constexpr int PTH = pidx<T>(TS + HALO);       // padded tile with u history
+    static constexpr size_t tab_bytes = ((size_t)Tab<M>::SMALL * 8 + 15) / 16 * 16;
+    static constexpr size_t fwd(int form, int phase) {
+        return tab_bytes + (size_t)(PT + (form == 0 && phase == 3 ? PT : 0)) * sizeof(T);
+    }
+    static constexpr size_t bwd(int form, int phase) {
+        return tab_bytes + (size_t)(PT + (phase == 3 ? PTH + (form == 1 ? PT : 0) : 0)) * sizeof(T);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Forward, phases 1 and 3 (a2-a4).  One CTA per tile of TS samples.
+//   PHASE 1: local pass, warp + block scans -> tile aggregate (no outputs).
+//   PHASE 3: the same scans again (x now comes from L2), plus the state
+//            entering the tile from phase 2 -> exact per-thread carry-in,
+//            re-run and emit y (and u for DF), zf.
+template <typename T, int M, int FORM, int PHASE>
+__global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
+    constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
+    using V = typename Vec<T>::type;
+    using TB = Tab<M>;
+    using SM = Smem<T, M>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* st = reinterpret_cast<double*>(smem_raw);
+    T* xs = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);     // x -> y in place
+    T* us = xs + SM::PT;                                          // DF: u tile (phase 3)
+    __shared__ double s_agg[NW][M];
+    __shared__ double s_xw[NW][M];
+
+    pdl_launch_dependents();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t tile = blockIdx.x;
+    const int64_t seq = tile / p.ntiles;
+    const int jt = (int)(tile - seq * p.ntiles);
+    const int64_t p0 = (int64_t)jt * TS;
+    const T* xrow = static_cast<const T*>(p.x) + seq * p.Tlen;
+    IIRG_TRACE(p.trace, tile, 0);
+    tile_load_async<T, TS>(xs, xrow, p0, p.Tlen, p.vec);
+    cp_async_commit();
+    T bc[M + 1], ac[M + 1];
+    raw_coefs<T, M>(static_cast<const T*>(p.b) + seq * p.coef_stride,
+                    static_cast<const T*>(p.a) + seq * p.coef_stride, bc, ac);
+    cp_async_wait<0>();
+    __syncthreads();
+
+    // a2: local pass from the zero state over this thread's chunk.
+    const int s0 = tid * L;
+    T v[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) v[i] = T(0);
+#pragma unroll
+    for (int g = 0; g < L / W; ++g) {
+        const V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
+#pragma unroll
+        for (int e = 0; e < W; ++e) { T du; fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, du); }
+    }
+    IIRG_TRACE(p.trace, tile, 1);
+    // previous grid: phase 1 waits for the prologue (tables), phase 3 for phase 2
+    pdl_wait();
+    const double* tb = p.tab + seq * p.tab_stride;
+    stage_small<M>(st, tb);
+    __syncthreads();
+    IIRG_TRACE(p.trace, tile, 2);
+    // a3: carries in fp64
+    double S[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) S[i] = (double)v[i];
+    warp_scan<M, false>(st, lane, S);
+    if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
+    }
+    __syncthreads();
+    if constexpr (PHASE == 1) {
+        if (warp == 0) {
+            double Jex[M], G[M];
+            block_scan<M, false>(st, lane, s_agg, Jex, G);
+            if (lane == 0) {
+#pragma unroll
+                for (int i = 0; i < M; ++i) p.agg[tile * M + i] = G[i];
+            }
+        }
+        IIRG_TRACE(p.trace, tile, 3);
+        return;
+    } else {
+        double E[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
+        if (warp == 0) {
+            double Jex[M], G[M];
+            block_scan<M, false>(st, lane, s_agg, Jex, G);
+            if (lane < NW) {                           // state entering warp `lane`
+                double X[M], xw[M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) { X[i] = p.carry[tile * M + i]; xw[i] = Jex[i]; }
+                mv_acc_lane_s<M, false>(st + TB::PWT, NW, lane, X, xw);
+#pragma unroll
+                for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
+            }
+        }
+        __syncthreads();
+        IIRG_TRACE(p.trace, tile, 3);
+        // state entering this thread's chunk: E + A_f^(L lane) x_warp
+        {
+            double xw[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
+            mv_acc_lane<M, false>(tb + TB::PLT, 32, lane, xw, E);
+        }
+        T vin[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) { vin[i] = (T)E[i]; v[i] = vin[i]; }
+        // zf = v(T): the thread holding sample T-1 walks its chunk up to it.
+        if (p.zf != nullptr) {
+            const int64_t eL = p.Tlen - 1 - p0;
+            if (eL >= s0 && eL < s0 + L) {
+                T w2[M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) w2[i] = vin[i];
+                for (int n = s0; n <= (int)eL; ++n) { T du; fwd_step<T, M, FORM>(w2, xs[pidx<T>(n)], bc, ac, du); }
+                T* zf = static_cast<T*>(p.zf) + seq * M;
+#pragma unroll
+                for (int i = 0; i < M; ++i) zf[i] = w2[i];
+            }
+        }
+        // a4: re-run from the exact carry-in, emit y (and u for DF) in place.
+#pragma unroll
+        for (int g = 0; g < L / W; ++g) {
+            V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
+            V uv;
+#pragma unroll
+            for (int e = 0; e < W; ++e) {
+                T uu;
+                const T yy = fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, uu);
+                vset(xv, e, yy);
+                vset(uv, e, uu);
+            }
+            *reinterpret_cast<V*>(xs + pidx<T>(s0 + g * W)) = xv;
+            if constexpr (FORM == 0) *reinterpret_cast<V*>(us + pidx<T>(s0 + g * W)) = uv;
+        }
+        __syncthreads();
+        IIRG_TRACE(p.trace, tile, 4);
+        T* yrow = static_cast<T*>(p.y) + seq * p.Tlen;
+        tile_store<T, TS>(yrow, xs, p0, p.Tlen, p.vec);
+        if constexpr (FORM == 0) {
+            T* urow = static_cast<T*>(p.u) + seq * p.Tlen;
+            tile_store<T, TS>(urow, us, p0, p.Tlen, p.vec);
+        }
+        IIRG_TRACE(p.trace, tile, 5);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Backward, phases 1 and 3 (a5-a8).  Tiles are aligned to the END of each
+// sequence; scan index jr = 0 is the last tile in time; inside a tile thread t
+// owns chunk NT-1-t, walked backwards.
+//   PHASE 1: local adjoint pass over dy, warp + block scans -> tile aggregate.
+//   PHASE 3: dy again (from L2) plus x, y (TDF) or u (DF): carry-in from phase
+//            2, re-run, emit dx and grad_zi, coefficient partial sums, fused a8.
 template <typename T, int M, int FORM>
-__device__ __forceinline__ void bwd_issue_xy(const LtiBwdArgs& p, unsigned tk, T* s2, T* s3) {
+__device__ __forceinline__ void bwd_load_u(const LtiBwdArgs& p, int64_t seq, int64_t p0, T* s2) {
     constexpr int TS = NT * Chunk<T>::L, W = Vec<T>::W;
     using V = typename Vec<T>::type;
-    const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
-    const int jr = (int)(tk / (unsigned long long)p.B);
-    const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;
-    const int64_t roff = seq * p.Tlen;
-    if constexpr (FORM == 1) {
-        tile_load_async<T, TS>(s2, static_cast<const T*>(p.x) + roff, p0, p.Tlen, p.vec);
-        tile_load_async<T, TS>(s3, static_cast<const T*>(p.y) + roff, p0, p.Tlen, p.vec);
-    } else {
-        // u(p0 - HALO .. p0 + TS) -> s2[pidx(e + HALO)]; u(-k) = zi[k-1] (DF state).
-        const T* urow = static_cast<const T*>(p.u) + roff;
-        const T* zi = static_cast<const T*>(p.zi);
-        for (int q = threadIdx.x; q < (TS + HALO) / W; q += NT) {
-            const int e = q * W - HALO;
-            const int64_t pos = p0 + e;
-            if (p.vec && pos >= 0 && pos + W <= p.Tlen) {
-                cp_async16(s2 + pidx<T>(e + HALO), urow + pos, 16u);
-            } else {
-                V val;
+    // u(p0 - HALO .. p0 + TS) -> s2[pidx(e + HALO)]; u(-k) = zi[k-1] (DF state).
+    const T* urow = static_cast<const T*>(p.u) + seq * p.Tlen;
+    const T* zi = static_cast<const T*>(p.zi);
+    for (int q = threadIdx.x; q < (TS + HALO) / W; q += NT) {
+        const int e = q * W - HALO;
+        const int64_t pos = p0 + e;
+        if (p.vec && pos >= 0 && pos + W <= p.Tlen) {
+            cp_async16(s2 + pidx<T>(e + HALO), urow + pos, 16u);
+        } else {
+            V val;
 #pragma unroll
-                for (int r = 0; r < W; ++r) {
-                    const int64_t pr = pos + r;
-                    T s = T(0);
-                    if (pr >= 0 && pr < p.Tlen) s = urow[pr];
-                    else if (pr < 0 && pr >= -M && zi != nullptr) s = zi[seq * M + (-pr - 1)];
-                    vset(val, r, s);
-                }
-                *reinterpret_cast<V*>(s2 + pidx<T>(e + HALO)) = val;
+            for (int r = 0; r < W; ++r) {
+                const int64_t pr = pos + r;
+                T s = T(0);
+                if (pr >= 0 && pr < p.Tlen) s = urow[pr];
+                else if (pr < 0 && pr >= -M && zi != nullptr) s = zi[seq * M + (-pr - 1)];
+                vset(val, r, s);
             }
+            *reinterpret_cast<V*>(s2 + pidx<T>(e + HALO)) = val;
         }
     }
 }
-template <typename T>
-__device__ __forceinline__ void bwd_issue_dy(const void* gy, unsigned tk, int64_t B, int64_t Tlen, bool vec, T* dys) {
-    constexpr int TS = NT * Chunk<T>::L;
-    const int64_t seq = (int64_t)(tk % (unsigned long long)B);
-    const int jr = (int)(tk / (unsigned long long)B);
-    const int64_t p0 = Tlen - (int64_t)(jr + 1) * TS;
-    if (gy != nullptr) tile_load_async<T, TS>(dys, static_cast<const T*>(gy) + seq * Tlen, p0, Tlen, vec);
-    else for (int e = threadIdx.x; e < TS; e += NT) dys[pidx<T>(e)] = T(0);
-}
 
-template <typename T, int M, int FORM>
+template <typename T, int M, int FORM, int PHASE>
 __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
     constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
     constexpr int NG = 2 * M + 1;                       // gradient partial sums
@@ -764,96 +744,110 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
     using SM = Smem<T, M>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* st = reinterpret_cast<double*>(smem_raw);
-    T* dyb = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);   // 2 stages: dy -> dx in place
-    T* s2 = dyb + 2 * SM::PT;                                  // TDF: x        DF: u (+HALO)
+    T* dys = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);   // dy -> dx in place
+    T* s2 = dys + SM::PT;                                      // TDF: x        DF: u (+HALO)
     T* s3 = s2 + SM::PTH;                                      // TDF: y
     __shared__ double s_agg[NW][M];
     __shared__ double s_xw[NW][M];
     __shared__ double s_red[NW][NG];
     __shared__ double s_G[NG];
-    __shared__ unsigned s_tk[2], s_fin;
+    __shared__ unsigned s_fin;
 
+    pdl_launch_dependents();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned ntot = (unsigned)(p.B * p.ntiles);
-    if (tid == 0) { s_tk[0] = atomicAdd(p.cw.ticket, 1u); s_tk[1] = atomicAdd(p.cw.ticket, 1u); }
-    __syncthreads();
-    unsigned tk = s_tk[0], tkn = s_tk[1];
-    if (tk < ntot) bwd_issue_dy<T>(p.gy, tk, p.B, p.Tlen, p.vec, dyb);
-    cp_async_commit();
-    if (tk < ntot) bwd_issue_xy<T, M, FORM>(p, tk, s2, s3);
-    cp_async_commit();
-    int stage = 0;
-    int64_t tab_set = -1;
-    while (tk < ntot) {
-        unsigned tk2 = 0u;
-        if (tid == 0) tk2 = atomicAdd(p.cw.ticket, 1u);          // consumed at the end of the iteration
-        if (tkn < ntot) bwd_issue_dy<T>(p.gy, tkn, p.B, p.Tlen, p.vec, dyb + (stage ^ 1) * SM::PT);
-        cp_async_commit();
-        const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
-        const int jr = (int)(tk / (unsigned long long)p.B);          // 0 = last tile in time
-        const int jt = p.ntiles - 1 - jr;                            // time index of the tile
-        const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;          // may be < 0 (first tile)
-        const double* tb = p.tab + seq * p.tab_stride;
-        const int64_t roff = seq * p.Tlen;
-        T* dys = dyb + stage * SM::PT;
-        IIRG_TRACE(p.trace, tk, 0);
-        const int64_t set = p.tab_stride == 0 ? 0 : seq;
-        if (set != tab_set) { stage_tables<M>(st, tb); tab_set = set; }
-        T bc[M + 1], ac[M + 1], cc[M];
-        load_coefs<T, M>(tb, bc, ac, cc);
-        cp_async_wait<2>();                                          // dy of this tile
-        __syncthreads();
+    const int64_t tile = blockIdx.x;
+    const int64_t seq = tile / p.ntiles;
+    const int jr = (int)(tile - seq * p.ntiles);                 // 0 = last tile in time
+    const int jt = p.ntiles - 1 - jr;                            // time index of the tile
+    const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;          // may be < 0 (first tile)
+    const double* tb = p.tab + seq * p.tab_stride;
+    const int64_t roff = seq * p.Tlen;
+    IIRG_TRACE(p.trace, tile, 0);
 
-        const int c = NT - 1 - tid;          // chunk index within the tile (time order)
-        const int s0 = c * L;
-        // a5: local adjoint pass from the zero state, walking the chunk backwards.
-        T d[M];
+    if (p.gy != nullptr) tile_load_async<T, TS>(dys, static_cast<const T*>(p.gy) + roff, p0, p.Tlen, p.vec);
+    else for (int e = tid; e < TS; e += NT) dys[pidx<T>(e)] = T(0);
+    cp_async_commit();
+    if constexpr (PHASE == 3) {
+        if constexpr (FORM == 1) {
+            tile_load_async<T, TS>(s2, static_cast<const T*>(p.x) + roff, p0, p.Tlen, p.vec);
+            tile_load_async<T, TS>(s3, static_cast<const T*>(p.y) + roff, p0, p.Tlen, p.vec);
+        } else {
+            bwd_load_u<T, M, FORM>(p, seq, p0, s2);
+        }
+    }
+    cp_async_commit();
+    stage_small<M>(st, tb);                          // tables live in the tape (written by the forward)
+    T bc[M + 1], ac[M + 1], cc[M];
+    load_coefs<T, M>(tb, bc, ac, cc);
+    cp_async_wait<1>();                              // dy
+    __syncthreads();
+
+    const int c = NT - 1 - tid;          // chunk index within the tile (time order)
+    const int s0 = c * L;
+    // a5: local adjoint pass from the zero state, walking the chunk backwards.
+    T d[M];
 #pragma unroll
-        for (int i = 0; i < M; ++i) d[i] = T(0);
+    for (int i = 0; i < M; ++i) d[i] = T(0);
 #pragma unroll
-        for (int g = L / W - 1; g >= 0; --g) {
-            const V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
+    for (int g = L / W - 1; g >= 0; --g) {
+        const V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
 #pragma unroll
-            for (int e = W - 1; e >= 0; --e) {
-                if constexpr (FORM == 1) adj_tdf_step<T, M>(d, vget(dv, e), ac);
-                else adj_df_step<T, M>(d, vget(dv, e), bc, ac);
+        for (int e = W - 1; e >= 0; --e) {
+            if constexpr (FORM == 1) adj_tdf_step<T, M>(d, vget(dv, e), ac);
+            else adj_df_step<T, M>(d, vget(dv, e), bc, ac);
+        }
+    }
+    IIRG_TRACE(p.trace, tile, 1);
+    // a6: carries (transposed powers)
+    double S[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) S[i] = (double)d[i];
+    warp_scan<M, true>(st, lane, S);
+    if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
+    }
+    __syncthreads();
+    if constexpr (PHASE == 1) {
+        if (warp == 0) {
+            double Jex[M], G[M];
+            block_scan<M, true>(st, lane, s_agg, Jex, G);
+            if (lane == 0) {
+#pragma unroll
+                for (int i = 0; i < M; ++i) p.agg[tile * M + i] = G[i];
             }
         }
-        IIRG_TRACE(p.trace, tk, 1);
-        // a6: carries (transposed powers), tiles last -> first.
-        double S[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) S[i] = (double)d[i];
-        warp_scan<M, true>(st, lane, S);
+        IIRG_TRACE(p.trace, tile, 2);
+        return;
+    } else {
         double E[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
-        if (lane == 31) {
+        double Jex[M], G[M];
+        if (warp == 0) block_scan<M, true>(st, lane, s_agg, Jex, G);
+        pdl_wait();                                  // tile carries of phase 2
+        IIRG_TRACE(p.trace, tile, 2);
+        if (warp == 0 && lane < NW) {                // state entering warp `lane`
+            double X[M], xw[M];
 #pragma unroll
-            for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
-        }
-        __syncthreads();
-        if (warp == 0) {
-            double X0[M];
-            const T* gzf = static_cast<const T*>(p.gzf);
+            for (int i = 0; i < M; ++i) { X[i] = p.carry[tile * M + i]; xw[i] = Jex[i]; }
+            mv_acc_lane_s<M, true>(st + TB::PWT, NW, lane, X, xw);
 #pragma unroll
-            for (int i = 0; i < M; ++i) X0[i] = (gzf != nullptr && jr == 0) ? (double)gzf[seq * M + i] : 0.0;
-            IIRG_TRACE(p.trace, tk, 3);
-            tile_carry<M, true>(st, tb, lane, s_agg, s_xw, jr, seq, X0, p.cw);
-            IIRG_TRACE(p.trace, tk, 4);
+            for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
         }
         __syncthreads();
         {
             double xw[M];
 #pragma unroll
             for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
-            mv_acc_lane_s<M, true>(st + TB::PLT, 32, lane, xw, E);
+            mv_acc_lane<M, true>(tb + TB::PLT, 32, lane, xw, E);
         }
         T din[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) { din[i] = (T)E[i]; d[i] = din[i]; }
-        cp_async_wait<1>();                                          // x, y / u of this tile
+        cp_async_wait<0>();                          // x, y / u
         __syncthreads();
+        IIRG_TRACE(p.trace, tile, 3);
 
         // grad_zi = dz(-1) (Eq.9, A.3): the thread whose chunk holds n = 0 walks down
         // to it before the emit pass overwrites dy with dx.
@@ -871,9 +865,9 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
             for (int i = 0; i < M; ++i) gzi[i] = w2[i];
         }
         // a7: re-run with the exact carry, emit dx, accumulate the coefficient sums.
-        T G[NG];
+        T Gs[NG];
 #pragma unroll
-        for (int k = 0; k < NG; ++k) G[k] = T(0);
+        for (int k = 0; k < NG; ++k) Gs[k] = T(0);
         const bool has_neg = (p0 + s0) < 0;                 // chunk reaches before n = 0
 #pragma unroll
         for (int g = L / W - 1; g >= 0; --g) {
@@ -888,8 +882,8 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
 #pragma unroll
                     for (int i = 0; i < M; ++i) dx = fma(cc[i], d[i], dx);     // Eq.8: c^T dz + b0 dy
 #pragma unroll
-                    for (int i = 0; i < M; ++i) { G[i] = fma(d[i], xx, G[i]); G[M + i] = fma(d[i], yy, G[M + i]); }
-                    G[2 * M] = fma(dy, xx, G[2 * M]);
+                    for (int i = 0; i < M; ++i) { Gs[i] = fma(d[i], xx, Gs[i]); Gs[M + i] = fma(d[i], yy, Gs[M + i]); }
+                    Gs[2 * M] = fma(dy, xx, Gs[2 * M]);
                     vset(dv, e, dx);
                     adj_tdf_step<T, M>(d, dy, ac);
                 }
@@ -903,8 +897,8 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
 #pragma unroll
                     for (int k = 0; k <= M; ++k) {
                         const T uk = s2[pidx<T>(n - k + HALO)];
-                        G[k] = fma(dy, uk, G[k]);                          // Gb[k] = sum dy u(n-k)
-                        if (k >= 1) G[M + k] = fma(gmask, uk, G[M + k]);  // Ga[k] = sum dx u(n-k)
+                        Gs[k] = fma(dy, uk, Gs[k]);                          // Gb[k] = sum dy u(n-k)
+                        if (k >= 1) Gs[M + k] = fma(gmask, uk, Gs[M + k]);  // Ga[k] = sum dx u(n-k)
                     }
                     vset(dv, e, dx);
                 }
@@ -915,19 +909,16 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
         if (p.want_coef) {
 #pragma unroll
             for (int k = 0; k < NG; ++k) {
-                double s = (double)G[k];
+                double s = (double)Gs[k];
 #pragma unroll
                 for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
                 if (lane == 0) s_red[warp][k] = s;
             }
         }
         __syncthreads();
-        IIRG_TRACE(p.trace, tk, 5);
-        // x, y / u of the next tile can now stream into s2 / s3
-        if (tkn < ntot) bwd_issue_xy<T, M, FORM>(p, tkn, s2, s3);
-        cp_async_commit();
+        IIRG_TRACE(p.trace, tile, 4);
         if (p.gx != nullptr) tile_store<T, TS>(static_cast<T*>(p.gx) + roff, dys, p0, p.Tlen, p.vec);
-        IIRG_TRACE(p.trace, tk, 6);
+        IIRG_TRACE(p.trace, tile, 5);
 
         if (p.want_coef) {
             // fused a8: group of 32 tiles -> group sum; last group of the set -> chain rule.
@@ -981,13 +972,7 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
                 }
             }
         }
-        if (tid == 0) s_tk[0] = tk2;
-        __syncthreads();
-        stage ^= 1;
-        tk = tkn;
-        tkn = s_tk[0];
     }
-    cta_exit<M>(p.cw, p.B, gridDim.x);
 }
 
 }  // namespace iirg

@@ -15,8 +15,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2511_14390_b200 import _binding as B  # noqa: E402
 
-PH_F = ["start", "local", "pdl", "carry0", "carry1", "emit", "store", "end"]
-PH_B = ["start", "local", "-", "carry0", "carry1", "emit", "store", "end"]
+PH_F = ["start", "local", "wait", "carry", "emit", "store", "-", "-"]
+PH_B = ["start", "local", "wait", "xy", "emit", "store", "-", "-"]
 
 
 def main():
