@@ -19,7 +19,6 @@
 
 namespace iirg {
 
-constexpr int LEVELS = 4;          // hierarchical carry levels: ntiles <= 32^4 per sequence
 constexpr int PREP_THREADS = 256;
 
 // ---------------------------------------------------------------------------
@@ -31,8 +30,9 @@ template <int M> struct Tab {
     static constexpr int PWT = PW + LOG_NW * M2;       // A_f^(32L w), w = 0..NW-1       [i][j][w]
     static constexpr int SMALL = PWT + NW * M2;        // [0, SMALL): staged in shared memory per CTA
     static constexpr int PLT = SMALL;                  // A_f^(L t),   t = 0..31         [i][j][t]
-    static constexpr int PQ = PLT + 32 * M2;           // A_f^(k 32^l TS), k = 0..31     [l][i][j][k]
-    static constexpr int COEF = PQ + LEVELS * 32 * M2; // b'[0..M], a'[0..M], c[0..M-1]
+    static constexpr int PQ = PLT + 32 * M2;           // A_f^(k TS), k = 0..31          [i][j][k]
+    static constexpr int PC = PQ + 32 * M2;            // A_f^(4 TS 2^d), d = 0..8 (carry pass) [d][i][j]
+    static constexpr int COEF = PC + 9 * M2;           // b'[0..M], a'[0..M], c[0..M-1]
     static constexpr int A0 = COEF + 3 * M + 2;        // a0 (un-normalised)
     static constexpr int SIZE = (A0 + 1 + 31) / 32 * 32;
 };
@@ -64,12 +64,39 @@ __device__ __forceinline__ void mv_acc_lane(const double* __restrict__ P, int st
 // Shared-memory versions (tables staged once per CTA).
 template <int M, bool TR>
 __device__ __forceinline__ void mv_acc_s(const double* P, const double (&v)[M], double (&acc)[M]) {
+    if constexpr (M % 2 == 0) {
+        // 128-bit shared loads (two matrix elements each); P is 16-byte aligned
+        const double2* P2 = reinterpret_cast<const double2*>(P);
+        if constexpr (!TR) {
 #pragma unroll
-    for (int i = 0; i < M; ++i) {
-        double s = acc[i];
+            for (int i = 0; i < M; ++i) {
+                double s = acc[i];
 #pragma unroll
-        for (int j = 0; j < M; ++j) s = fma(P[TR ? j * M + i : i * M + j], v[j], s);
-        acc[i] = s;
+                for (int j = 0; j < M; j += 2) {
+                    const double2 q = P2[(i * M + j) / 2];
+                    s = fma(q.x, v[j], s);
+                    s = fma(q.y, v[j + 1], s);
+                }
+                acc[i] = s;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < M; ++j)
+#pragma unroll
+                for (int i = 0; i < M; i += 2) {
+                    const double2 q = P2[(j * M + i) / 2];       // P[j][i], P[j][i+1] = (P^T)[i][j], [i+1][j]
+                    acc[i] = fma(q.x, v[j], acc[i]);
+                    acc[i + 1] = fma(q.y, v[j], acc[i + 1]);
+                }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            double s = acc[i];
+#pragma unroll
+            for (int j = 0; j < M; ++j) s = fma(P[TR ? j * M + i : i * M + j], v[j], s);
+            acc[i] = s;
+        }
     }
 }
 template <int M, bool TR>
@@ -93,8 +120,8 @@ __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepc
 // TDF: its transpose) and every fp64 power table by batched
 // doubling (log depth): about 30 dependent matrix-product steps.
 template <int M> struct PrepSlots {
-    static constexpr int P1 = 0, PLT = 1 /* 33 */, YP = PLT + 33 /* 5 */, Q = YP + 5 /* LEVELS x 33 */;
-    static constexpr int N = Q + LEVELS * 33;
+    static constexpr int P1 = 0, PLT = 1 /* 33 */, YP = PLT + 33 /* 5 */, Q = YP + 5 /* 33 */, C = Q + 33 /* 9 */;
+    static constexpr int N = C + 9;
     static constexpr size_t bytes() { return (size_t)N * M * M * sizeof(double); }
 };
 
@@ -130,7 +157,7 @@ __global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restr
         const double id = (i == j) ? 1.0 : 0.0;
         mat[(S::PLT + 0) * M2 + e] = id;
         mat[(S::YP + 0) * M2 + e] = id;
-        for (int l = 0; l < LEVELS; ++l) mat[(S::Q + l * 33) * M2 + e] = id;
+        mat[S::Q * M2 + e] = id;
     }
     if (tid <= M) { tb[TB::COEF + tid] = bn[tid]; tb[TB::COEF + M + 1 + tid] = an[tid]; }
     if (tid < M) tb[TB::COEF + 2 * (M + 1) + tid] = bn[tid + 1] - an[tid + 1] * bn[0];
@@ -181,10 +208,11 @@ __global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restr
     copy(S::YP + 1, S::PLT + 32);
     powers(S::YP, LOG_NW);                                              // A_f^(32 L w), w = 0..NW
     copy(S::Q + 1, S::YP + NW);                                         // A_f^TS
-    for (int l = 0; l < nlev; ++l) {                                    // A_f^(k 32^l TS), k = 0..32
-        powers(S::Q + l * 33, 5);
-        if (l + 1 < LEVELS) copy(S::Q + (l + 1) * 33 + 1, S::Q + l * 33 + 32);
-    }
+    powers(S::Q, 5);                                                    // A_f^(k TS), k = 0..32
+    copy(S::C, S::Q + 4);                                               // A_f^(4 TS 2^d), d = 0..8
+    for (int d = 1; d < 9; ++d)
+        mm_batch(1, [&](int) { return S::C + d; }, [&](int) { return S::C + d - 1; }, [&](int) { return S::C + d - 1; });
+    (void)nlev;
     // write out in the kernels' layouts
     for (int e = tid; e < M2; e += PREP_THREADS) {
         for (int d = 0; d < 5; ++d) tb[TB::PL + d * M2 + e] = mat[(S::PLT + (1 << d)) * M2 + e];
@@ -196,10 +224,11 @@ __global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restr
         tb[TB::PLT + w] = mat[(S::PLT + t) * M2 + e];
     }
     (void)0;
-    for (int w = tid; w < nlev * 32 * M2; w += PREP_THREADS) {
-        const int l = w / (32 * M2), r = w % (32 * M2), e = r / 32, k = r % 32;
-        tb[TB::PQ + w] = mat[(S::Q + l * 33 + k) * M2 + e];
+    for (int w = tid; w < 32 * M2; w += PREP_THREADS) {
+        const int e = w / 32, k = w % 32;
+        tb[TB::PQ + w] = mat[(S::Q + k) * M2 + e];
     }
+    for (int w = tid; w < 9 * M2; w += PREP_THREADS) tb[TB::PC + w] = mat[(S::C + w / M2) * M2 + (w % M2)];
 }
 
 // ---------------------------------------------------------------------------
@@ -390,157 +419,199 @@ __device__ __forceinline__ void block_scan(const double* st, int lane, double (*
     }
 }
 
+template <int M>
+__device__ __forceinline__ void warp_sum(double (&v)[M]) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < M; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+}
+
+// Phase 1 needs only the tile aggregate, a reduction rather than a scan:
+//   G = sum_t A_f^(L (NT-1-t)) w_t   (t in scan order; TR: transposed powers)
+// lane term with A_f^(L (31-lane)), fixed butterfly sum per warp, then warp 0
+// combines the NW warp sums with A_f^(32 L (NW-1-w)).  Writes G to dst.
+template <int M, bool TR>
+__device__ __forceinline__ void tile_reduce(const double* __restrict__ tb, const double* st, int lane, int warp,
+                                            const double (&w)[M], double (*s_agg)[M], double* dst) {
+    using TB = Tab<M>;
+    double t[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) t[i] = 0.0;
+    mv_acc_lane<M, TR>(tb + TB::PLT, 32, 31 - lane, w, t);
+    warp_sum<M>(t);
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) s_agg[warp][i] = t[i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double v[M], g[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) { v[i] = (lane < NW) ? s_agg[lane][i] : 0.0; g[i] = 0.0; }
+        if (lane < NW) mv_acc_lane_s<M, TR>(st + TB::PWT, NW, NW - 1 - lane, v, g);
+        warp_sum<M>(g);
+        if (lane == 0) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) dst[i] = g[i];
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Phase 2 (a3/a6 across tiles): per sequence, the exact state entering every
 // tile from the tile aggregates:  X_0 = x0,  X_{j+1} = Q X_j + agg_j, Q = A_f^TS.
-// One CTA per sequence; thread t owns k consecutive tiles: a Horner pass gives
-// its aggregate, a block-wide Kogge-Stone scan with Q^(k 2^d) (fp64) gives its
-// entering state, and a second Horner pass writes X for each of its tiles.
+// One CTA per sequence walks the tiles in chunks of CARRY_CHUNK staged in
+// shared memory; thread t owns CARRY_K consecutive tiles of a chunk: a Horner
+// pass gives its aggregate, a block-wide Kogge-Stone scan with Q^(K 2^d)
+// (fp64) gives its entering state, a second Horner pass writes X per tile.
 // Fixed order throughout: bitwise deterministic.
 constexpr int CARRY_THREADS = 256;
+constexpr int CARRY_K = 4;
+constexpr int CARRY_CHUNK = CARRY_THREADS * CARRY_K;
+
+template <int M>
+constexpr size_t carry_smem() { return (size_t)CARRY_CHUNK * M * sizeof(double); }
 
 template <int M, bool TR>
 __global__ void __launch_bounds__(CARRY_THREADS) lti_carry_kernel(const CarryArgs c) {
     constexpr int M2 = M * M;
+    constexpr int NWC = CARRY_THREADS / 32;
     using TB = Tab<M>;
-    __shared__ double sQ[M2];                     // Q = A_f^TS (transposed for the adjoint)
-    __shared__ double sR[9][M2];                  // Q^(k 2^d), d = 0..8
-    __shared__ double sW[CARRY_THREADS / 32][M];
-    __shared__ double tmp[2][M2];
+    extern __shared__ __align__(16) unsigned char carry_raw[];
+    double* sA = reinterpret_cast<double*>(carry_raw);     // [CARRY_CHUNK][M] aggregates of a chunk
+    __shared__ __align__(16) double sQ[M2];                 // Q = A_f^TS (transposed for the adjoint)
+    __shared__ __align__(16) double sR[9][M2];              // Q^(K 2^d), d = 0..8
+    __shared__ double sW[NWC][M];
+    __shared__ double sX[M];
     pdl_launch_dependents();
-    pdl_wait();                                   // aggregates of phase 1
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t seq = blockIdx.x;
     const double* tb = c.tab + seq * c.tab_stride;
     const int n = c.ntiles;
-    const int k = (n + CARRY_THREADS - 1) / CARRY_THREADS;
-    // Q from the level-0 power table (k = 1 entry), transposed for TR
     for (int e = tid; e < M2; e += CARRY_THREADS) {
         const int i = e / M, j = e % M;
-        sQ[e] = __ldg(tb + TB::PQ + (TR ? j * M + i : e) * 32 + 1);
-    }
-    __syncthreads();
-    // R_0 = Q^k by binary powering (M2 threads), R_{d+1} = R_d^2
-    auto mm = [&](double* dst, const double* A, const double* Bm) {
-        double s = 0.0;
-        const int e = tid, i = e / M, j = e % M;
-        if (e < M2)
+        const int src = TR ? j * M + i : e;
+        sQ[e] = __ldg(tb + TB::PQ + src * 32 + 1);                                  // A_f^TS
 #pragma unroll
-            for (int q = 0; q < M; ++q) s = fma(A[i * M + q], Bm[q * M + j], s);
-        __syncthreads();
-        if (e < M2) dst[e] = s;
-        __syncthreads();
-    };
-    for (int e = tid; e < M2; e += CARRY_THREADS) {
-        sR[0][e] = (e / M == e % M) ? 1.0 : 0.0;
-        tmp[0][e] = sQ[e];
+        for (int d = 0; d < 9; ++d) sR[d][e] = __ldg(tb + TB::PC + d * M2 + src); // A_f^(K TS 2^d)
+    }
+    static_assert(CARRY_K == 4, "PC tables hold A_f^(4 TS 2^d)");
+    if (tid < M) {
+        double x0 = 0.0;
+        if (c.x0 != nullptr)
+            x0 = c.x0_f64 ? static_cast<const double*>(c.x0)[seq * M + tid]
+                          : (double)static_cast<const float*>(c.x0)[seq * M + tid];
+        sX[tid] = x0;
     }
     __syncthreads();
-    for (int kk = k; kk > 0; kk >>= 1) {
-        if (kk & 1) mm(sR[0], sR[0], tmp[0]);
-        if (kk > 1) mm(tmp[0], tmp[0], tmp[0]);
-    }
-    for (int d = 1; d < 9; ++d) mm(sR[d], sR[d - 1], sR[d - 1]);
-
+    pdl_wait();                                                                 // phase-1 aggregates
     const double* agg = c.agg + seq * (int64_t)n * M;
     double* carry = c.carry + seq * (int64_t)n * M;
-    double X0[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-        X0[i] = 0.0;
-        if (c.x0 != nullptr)
-            X0[i] = c.x0_f64 ? static_cast<const double*>(c.x0)[seq * M + i]
-                             : (double)static_cast<const float*>(c.x0)[seq * M + i];
-    }
-    const int i0 = tid * k, i1 = min(n, i0 + k);
-    // Horner over this thread's tiles (thread 0 starts from the initial state)
-    double S[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) S[i] = (tid == 0) ? X0[i] : 0.0;
-    for (int t = i0; t < i1; ++t) {
-        double Sn[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) Sn[i] = agg[(int64_t)t * M + i];
-        mv_acc_s<M, false>(sQ, S, Sn);
-#pragma unroll
-        for (int i = 0; i < M; ++i) S[i] = Sn[i];
-    }
-    if (i0 >= n) {
+    for (int cs = 0; cs < n; cs += CARRY_CHUNK) {
+        const int cnt = min(CARRY_CHUNK, n - cs);
+        for (int e = tid; e < CARRY_CHUNK * M; e += CARRY_THREADS)
+            sA[e] = (e < cnt * M) ? __ldcg(agg + (int64_t)cs * M + e) : 0.0;
+        __syncthreads();
+        // Horner over this thread's tiles
+        double S[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) S[i] = 0.0;
-    }
-    // inclusive scan across threads: warp level then across warps
 #pragma unroll
-    for (int d = 0; d < 5; ++d) {
-        const int off = 1 << d;
-        double O[M];
+        for (int q = 0; q < CARRY_K; ++q) {
+            double Sn[M];
 #pragma unroll
-        for (int i = 0; i < M; ++i) O[i] = shfl_up_d(S[i], off);
-        if (lane >= off) mv_acc_s<M, false>(sR[d], O, S);
-    }
-    if (lane == 31) {
+            for (int i = 0; i < M; ++i) Sn[i] = sA[(tid * CARRY_K + q) * M + i];
+            mv_acc_s<M, false>(sQ, S, Sn);
 #pragma unroll
-        for (int i = 0; i < M; ++i) sW[warp][i] = S[i];
-    }
-    __syncthreads();
-    if (warp == 0) {
-        constexpr int NWC = CARRY_THREADS / 32;
-        double Wv[M];
+            for (int i = 0; i < M; ++i) S[i] = Sn[i];
+        }
+        // inclusive scan across threads: warp level then across warps
 #pragma unroll
-        for (int i = 0; i < M; ++i) Wv[i] = (lane < NWC) ? sW[lane][i] : 0.0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
+        for (int d = 0; d < 5; ++d) {
             const int off = 1 << d;
             double O[M];
 #pragma unroll
-            for (int i = 0; i < M; ++i) O[i] = shfl_up_d(Wv[i], off);
-            if (lane >= off && lane < NWC) mv_acc_s<M, false>(sR[5 + d], O, Wv);
+            for (int i = 0; i < M; ++i) O[i] = shfl_up_d(S[i], off);
+            if (lane >= off) mv_acc_s<M, false>(sR[d], O, S);
         }
-        double We[M];
+        if (lane == 31) {
 #pragma unroll
-        for (int i = 0; i < M; ++i) { We[i] = shfl_up_d(Wv[i], 1); if (lane == 0) We[i] = 0.0; }
-        __syncwarp();
-        if (lane < NWC) {
-#pragma unroll
-            for (int i = 0; i < M; ++i) sW[lane][i] = We[i];
+            for (int i = 0; i < M; ++i) sW[warp][i] = S[i];
         }
-    }
-    __syncthreads();
-    // entering state of this thread: exclusive lane prefix + Q^(k lane) (warp prefix)
-    double E[M];
+        __syncthreads();
+        if (warp == 0) {
+            double Wv[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
-    {
-        double Y[M];
+            for (int i = 0; i < M; ++i) Wv[i] = (lane < NWC) ? sW[lane][i] : 0.0;
 #pragma unroll
-        for (int i = 0; i < M; ++i) Y[i] = sW[warp][i];
-        // Y <- Q^(k lane) Y by the binary digits of lane
+            for (int d = 0; d < 3; ++d) {
+                const int off = 1 << d;
+                double O[M];
 #pragma unroll
-        for (int d = 0; d < 5; ++d) {
-            if ((lane >> d) & 1) {
-                double Z[M];
+                for (int i = 0; i < M; ++i) O[i] = shfl_up_d(Wv[i], off);
+                if (lane >= off && lane < NWC) mv_acc_s<M, false>(sR[5 + d], O, Wv);
+            }
+            double We[M];
 #pragma unroll
-                for (int i = 0; i < M; ++i) Z[i] = 0.0;
-                mv_acc_s<M, false>(sR[d], Y, Z);
+            for (int i = 0; i < M; ++i) { We[i] = shfl_up_d(Wv[i], 1); if (lane == 0) We[i] = 0.0; }
+            __syncwarp();
+            if (lane < NWC) {
 #pragma unroll
-                for (int i = 0; i < M; ++i) Y[i] = Z[i];
+                for (int i = 0; i < M; ++i) sW[lane][i] = We[i];
+            }
+        }
+        __syncthreads();
+        // entering state: exclusive lane prefix + Q^(K lane) (warp prefix) + Q^(K tid) X_chunk
+        double E[M], Y[M], Z[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            E[i] = shfl_up_d(S[i], 1);
+            if (lane == 0) E[i] = 0.0;
+            Y[i] = sW[warp][i];
+            Z[i] = sX[i];
+        }
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {                 // Z <- Q^(K tid) X,  Y <- Q^(K lane) Y
+            if ((tid >> d) & 1) {
+                double Zn[M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) Zn[i] = 0.0;
+                mv_acc_s<M, false>(sR[d], Z, Zn);
+#pragma unroll
+                for (int i = 0; i < M; ++i) Z[i] = Zn[i];
+            }
+            if (d < 5 && ((lane >> d) & 1)) {
+                double Yn[M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) Yn[i] = 0.0;
+                mv_acc_s<M, false>(sR[d], Y, Yn);
+#pragma unroll
+                for (int i = 0; i < M; ++i) Y[i] = Yn[i];
             }
         }
 #pragma unroll
-        for (int i = 0; i < M; ++i) E[i] += Y[i];
-    }
-    if (tid == 0) {
+        for (int i = 0; i < M; ++i) E[i] += Y[i] + Z[i];
+        __syncthreads();                                        // everyone has read sX / sW
+        // second Horner pass: state entering each tile
 #pragma unroll
-        for (int i = 0; i < M; ++i) E[i] = X0[i];
-    }
-    // second Horner pass: state entering each tile
-    for (int t = i0; t < i1; ++t) {
-        double Sn[M];
+        for (int q = 0; q < CARRY_K; ++q) {
+            const int t = tid * CARRY_K + q;
+            double Sn[M];
 #pragma unroll
-        for (int i = 0; i < M; ++i) { carry[(int64_t)t * M + i] = E[i]; Sn[i] = agg[(int64_t)t * M + i]; }
-        mv_acc_s<M, false>(sQ, E, Sn);
+            for (int i = 0; i < M; ++i) {
+                if (t < cnt) carry[(int64_t)(cs + t) * M + i] = E[i];
+                Sn[i] = sA[t * M + i];
+            }
+            mv_acc_s<M, false>(sQ, E, Sn);
 #pragma unroll
-        for (int i = 0; i < M; ++i) E[i] = Sn[i];
+            for (int i = 0; i < M; ++i) E[i] = Sn[i];
+        }
+        if (tid == CARRY_THREADS - 1) {                          // state at the end of the chunk
+#pragma unroll
+            for (int i = 0; i < M; ++i) sX[i] = E[i];
+        }
+        __syncthreads();
     }
 }
 
@@ -551,16 +622,27 @@ struct Smem {
     static constexpr int PT = pidx<T>(TS);               // one padded tile
     static constexpr int PTH = pidx<T>(TS + HALO);       // padded tile with u history
     static constexpr size_t tab_bytes = ((size_t)Tab<M>::SMALL * 8 + 15) / 16 * 16;
+    // forward: 2 stages of x (-> y), plus the u tile for DF emits
     static constexpr size_t fwd(int form, int phase) {
-        return tab_bytes + (size_t)(PT + (form == 0 && phase == 3 ? PT : 0)) * sizeof(T);
+        return tab_bytes + (size_t)(2 * PT + (form == 0 && phase == 3 ? PT : 0)) * sizeof(T);
     }
+    // backward: 2 stages of dy (-> dx) [+ one x, y (TDF) or u (DF) tile in phase 3]
+    static constexpr int bwd_xy(int form, int phase) { return phase == 3 ? PTH + (form == 1 ? PT : 0) : 0; }
     static constexpr size_t bwd(int form, int phase) {
-        return tab_bytes + (size_t)(PT + (phase == 3 ? PTH + (form == 1 ? PT : 0) : 0)) * sizeof(T);
+        return tab_bytes + (size_t)(2 * PT + bwd_xy(form, phase)) * sizeof(T);
     }
 };
 
+// Per-CTA coefficient state (tables staged in shared memory, coefficients in registers).
+template <typename T, int M>
+struct CoefRegs {
+    T bc[M + 1], ac[M + 1], cc[M];
+};
+
 // ---------------------------------------------------------------------------
-// Forward, phases 1 and 3 (a2-a4).  One CTA per tile of TS samples.
+// Forward, phases 1 and 3 (a2-a4).  Persistent CTAs stride over the tiles
+// (tile = seq * ntiles + jt, TS samples each) and double-buffer them: tile k+1
+// streams into shared memory (cp.async) while tile k is scanned.
 //   PHASE 1: local pass, warp + block scans -> tile aggregate (no outputs).
 //   PHASE 3: the same scans again (x now comes from L2), plus the state
 //            entering the tile from phase 2 -> exact per-thread carry-in,
@@ -573,138 +655,149 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
     using SM = Smem<T, M>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* st = reinterpret_cast<double*>(smem_raw);
-    T* xs = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);     // x -> y in place
-    T* us = xs + SM::PT;                                          // DF: u tile (phase 3)
+    T* xb = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);     // 2 stages, x -> y in place
+    T* us = xb + 2 * SM::PT;                                      // DF: u tile (phase 3)
     __shared__ double s_agg[NW][M];
     __shared__ double s_xw[NW][M];
 
     pdl_launch_dependents();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tile = blockIdx.x;
-    const int64_t seq = tile / p.ntiles;
-    const int jt = (int)(tile - seq * p.ntiles);
-    const int64_t p0 = (int64_t)jt * TS;
-    const T* xrow = static_cast<const T*>(p.x) + seq * p.Tlen;
-    IIRG_TRACE(p.trace, tile, 0);
-    tile_load_async<T, TS>(xs, xrow, p0, p.Tlen, p.vec);
+    const int64_t ntot = p.B * (int64_t)p.ntiles;
+    int64_t tile = blockIdx.x;
+    if (tile < ntot) {
+        const int64_t sq = tile / p.ntiles;
+        tile_load_async<T, TS>(xb, static_cast<const T*>(p.x) + sq * p.Tlen, (tile - sq * p.ntiles) * TS,
+                               p.Tlen, p.vec);
+    }
     cp_async_commit();
-    T bc[M + 1], ac[M + 1];
-    raw_coefs<T, M>(static_cast<const T*>(p.b) + seq * p.coef_stride,
-                    static_cast<const T*>(p.a) + seq * p.coef_stride, bc, ac);
-    cp_async_wait<0>();
-    __syncthreads();
-
-    // a2: local pass from the zero state over this thread's chunk.
-    const int s0 = tid * L;
-    T v[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) v[i] = T(0);
-#pragma unroll
-    for (int g = 0; g < L / W; ++g) {
-        const V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
-#pragma unroll
-        for (int e = 0; e < W; ++e) { T du; fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, du); }
-    }
-    IIRG_TRACE(p.trace, tile, 1);
-    // previous grid: phase 1 waits for the prologue (tables), phase 3 for phase 2
-    pdl_wait();
-    const double* tb = p.tab + seq * p.tab_stride;
-    stage_small<M>(st, tb);
-    __syncthreads();
-    IIRG_TRACE(p.trace, tile, 2);
-    // a3: carries in fp64
-    double S[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) S[i] = (double)v[i];
-    warp_scan<M, false>(st, lane, S);
-    if (lane == 31) {
-#pragma unroll
-        for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
-    }
-    __syncthreads();
-    if constexpr (PHASE == 1) {
-        if (warp == 0) {
-            double Jex[M], G[M];
-            block_scan<M, false>(st, lane, s_agg, Jex, G);
-            if (lane == 0) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) p.agg[tile * M + i] = G[i];
-            }
+    int64_t staged = -1;
+    bool waited = false;
+    T bc[M + 1], ac[M + 1], cc[M];
+    for (int it = 0; tile < ntot; ++it, tile += gridDim.x) {
+        const int64_t next = tile + gridDim.x;
+        if (next < ntot) {
+            const int64_t sq = next / p.ntiles;
+            tile_load_async<T, TS>(xb + ((it + 1) & 1) * SM::PT, static_cast<const T*>(p.x) + sq * p.Tlen,
+                                   (next - sq * p.ntiles) * TS, p.Tlen, p.vec);
         }
-        IIRG_TRACE(p.trace, tile, 3);
-        return;
-    } else {
-        double E[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
-        if (warp == 0) {
-            double Jex[M], G[M];
-            block_scan<M, false>(st, lane, s_agg, Jex, G);
-            if (lane < NW) {                           // state entering warp `lane`
-                double X[M], xw[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) { X[i] = p.carry[tile * M + i]; xw[i] = Jex[i]; }
-                mv_acc_lane_s<M, false>(st + TB::PWT, NW, lane, X, xw);
-#pragma unroll
-                for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
-            }
+        cp_async_commit();
+        const int64_t seq = tile / p.ntiles;
+        const int jt = (int)(tile - seq * p.ntiles);
+        const int64_t p0 = (int64_t)jt * TS;
+        const double* tb = p.tab + seq * p.tab_stride;
+        T* xs = xb + (it & 1) * SM::PT;
+        const int64_t set = p.tab_stride == 0 ? 0 : seq;
+        if (set != staged) {
+            // previous grid: phase 1 waits for the prologue (tables), phase 3 for phase 2
+            if (!waited) { pdl_wait(); waited = true; }
+            stage_small<M>(st, tb);
+            load_coefs<T, M>(tb, bc, ac, cc);
+            staged = set;
         }
+        IIRG_TRACE(p.trace, tile, 0);
+        cp_async_wait<1>();
         __syncthreads();
-        IIRG_TRACE(p.trace, tile, 3);
-        // state entering this thread's chunk: E + A_f^(L lane) x_warp
-        {
-            double xw[M];
+
+        // a2: local pass from the zero state over this thread's chunk.
+        const int s0 = tid * L;
+        T v[M];
 #pragma unroll
-            for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
-            mv_acc_lane<M, false>(tb + TB::PLT, 32, lane, xw, E);
-        }
-        T vin[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) { vin[i] = (T)E[i]; v[i] = vin[i]; }
-        // zf = v(T): the thread holding sample T-1 walks its chunk up to it.
-        if (p.zf != nullptr) {
-            const int64_t eL = p.Tlen - 1 - p0;
-            if (eL >= s0 && eL < s0 + L) {
-                T w2[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) w2[i] = vin[i];
-                for (int n = s0; n <= (int)eL; ++n) { T du; fwd_step<T, M, FORM>(w2, xs[pidx<T>(n)], bc, ac, du); }
-                T* zf = static_cast<T*>(p.zf) + seq * M;
-#pragma unroll
-                for (int i = 0; i < M; ++i) zf[i] = w2[i];
-            }
-        }
-        // a4: re-run from the exact carry-in, emit y (and u for DF) in place.
+        for (int i = 0; i < M; ++i) v[i] = T(0);
 #pragma unroll
         for (int g = 0; g < L / W; ++g) {
-            V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
-            V uv;
+            const V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
 #pragma unroll
-            for (int e = 0; e < W; ++e) {
-                T uu;
-                const T yy = fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, uu);
-                vset(xv, e, yy);
-                vset(uv, e, uu);
+            for (int e = 0; e < W; ++e) { T du; fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, du); }
+        }
+        IIRG_TRACE(p.trace, tile, 1);
+        // a3: carries in fp64
+        double S[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) S[i] = (double)v[i];
+        if constexpr (PHASE == 1) {
+            tile_reduce<M, false>(tb, st, lane, warp, S, s_agg, p.agg + tile * M);
+            IIRG_TRACE(p.trace, tile, 2);
+        } else {
+            warp_scan<M, false>(st, lane, S);
+            if (lane == 31) {
+#pragma unroll
+                for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
             }
-            *reinterpret_cast<V*>(xs + pidx<T>(s0 + g * W)) = xv;
-            if constexpr (FORM == 0) *reinterpret_cast<V*>(us + pidx<T>(s0 + g * W)) = uv;
+            __syncthreads();
+            double E[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
+            if (warp == 0) {
+                double Jex[M], G[M];
+                block_scan<M, false>(st, lane, s_agg, Jex, G);
+                if (lane < NW) {                           // state entering warp `lane`
+                    double X[M], xw[M];
+#pragma unroll
+                    for (int i = 0; i < M; ++i) { X[i] = p.carry[tile * M + i]; xw[i] = Jex[i]; }
+                    mv_acc_lane_s<M, false>(st + TB::PWT, NW, lane, X, xw);
+#pragma unroll
+                    for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
+                }
+            }
+            __syncthreads();
+            IIRG_TRACE(p.trace, tile, 2);
+            // state entering this thread's chunk: E + A_f^(L lane) x_warp
+            {
+                double xw[M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
+                mv_acc_lane<M, false>(tb + TB::PLT, 32, lane, xw, E);
+            }
+            T vin[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) { vin[i] = (T)E[i]; v[i] = vin[i]; }
+            // zf = v(T): the thread holding sample T-1 walks its chunk up to it.
+            if (p.zf != nullptr) {
+                const int64_t eL = p.Tlen - 1 - p0;
+                if (eL >= s0 && eL < s0 + L) {
+                    T w2[M];
+#pragma unroll
+                    for (int i = 0; i < M; ++i) w2[i] = vin[i];
+                    for (int n = s0; n <= (int)eL; ++n) { T du; fwd_step<T, M, FORM>(w2, xs[pidx<T>(n)], bc, ac, du); }
+                    T* zf = static_cast<T*>(p.zf) + seq * M;
+#pragma unroll
+                    for (int i = 0; i < M; ++i) zf[i] = w2[i];
+                }
+            }
+            // a4: re-run from the exact carry-in, emit y (and u for DF) in place.
+#pragma unroll
+            for (int g = 0; g < L / W; ++g) {
+                V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
+                V uv;
+#pragma unroll
+                for (int e = 0; e < W; ++e) {
+                    T uu;
+                    const T yy = fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, uu);
+                    vset(xv, e, yy);
+                    vset(uv, e, uu);
+                }
+                *reinterpret_cast<V*>(xs + pidx<T>(s0 + g * W)) = xv;
+                if constexpr (FORM == 0) *reinterpret_cast<V*>(us + pidx<T>(s0 + g * W)) = uv;
+            }
+            __syncthreads();
+            IIRG_TRACE(p.trace, tile, 3);
+            T* yrow = static_cast<T*>(p.y) + seq * p.Tlen;
+            tile_store<T, TS>(yrow, xs, p0, p.Tlen, p.vec);
+            if constexpr (FORM == 0) {
+                T* urow = static_cast<T*>(p.u) + seq * p.Tlen;
+                tile_store<T, TS>(urow, us, p0, p.Tlen, p.vec);
+            }
         }
-        __syncthreads();
-        IIRG_TRACE(p.trace, tile, 4);
-        T* yrow = static_cast<T*>(p.y) + seq * p.Tlen;
-        tile_store<T, TS>(yrow, xs, p0, p.Tlen, p.vec);
-        if constexpr (FORM == 0) {
-            T* urow = static_cast<T*>(p.u) + seq * p.Tlen;
-            tile_store<T, TS>(urow, us, p0, p.Tlen, p.vec);
-        }
-        IIRG_TRACE(p.trace, tile, 5);
+        __syncthreads();                                  // this stage may be refilled
     }
+    if (!waited) pdl_wait();
 }
 
 // ---------------------------------------------------------------------------
 // Backward, phases 1 and 3 (a5-a8).  Tiles are aligned to the END of each
 // sequence; scan index jr = 0 is the last tile in time; inside a tile thread t
-// owns chunk NT-1-t, walked backwards.
+// owns chunk NT-1-t, walked backwards.  Persistent, double-buffered like the
+// forward kernel.
 //   PHASE 1: local adjoint pass over dy, warp + block scans -> tile aggregate.
 //   PHASE 3: dy again (from L2) plus x, y (TDF) or u (DF): carry-in from phase
 //            2, re-run, emit dx and grad_zi, coefficient partial sums, fused a8.
@@ -735,6 +828,30 @@ __device__ __forceinline__ void bwd_load_u(const LtiBwdArgs& p, int64_t seq, int
     }
 }
 
+template <typename T>
+__device__ __forceinline__ void bwd_issue_dy(const LtiBwdArgs& p, int64_t tile, T* dys) {
+    constexpr int TS = NT * Chunk<T>::L;
+    const int64_t seq = tile / p.ntiles;
+    const int jr = (int)(tile - seq * p.ntiles);
+    const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;
+    if (p.gy != nullptr) tile_load_async<T, TS>(dys, static_cast<const T*>(p.gy) + seq * p.Tlen, p0, p.Tlen, p.vec);
+    else for (int e = threadIdx.x; e < TS; e += NT) dys[pidx<T>(e)] = T(0);
+}
+template <typename T, int M, int FORM>
+__device__ __forceinline__ void bwd_issue_xy(const LtiBwdArgs& p, int64_t tile, T* s2, T* s3) {
+    constexpr int TS = NT * Chunk<T>::L;
+    const int64_t seq = tile / p.ntiles;
+    const int jr = (int)(tile - seq * p.ntiles);
+    const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;
+    const int64_t roff = seq * p.Tlen;
+    if constexpr (FORM == 1) {
+        tile_load_async<T, TS>(s2, static_cast<const T*>(p.x) + roff, p0, p.Tlen, p.vec);
+        tile_load_async<T, TS>(s3, static_cast<const T*>(p.y) + roff, p0, p.Tlen, p.vec);
+    } else {
+        bwd_load_u<T, M, FORM>(p, seq, p0, s2);
+    }
+}
+
 template <typename T, int M, int FORM, int PHASE>
 __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
     constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
@@ -744,8 +861,8 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
     using SM = Smem<T, M>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* st = reinterpret_cast<double*>(smem_raw);
-    T* dys = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);   // dy -> dx in place
-    T* s2 = dys + SM::PT;                                      // TDF: x        DF: u (+HALO)
+    T* sb = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);    // 2 stages of dy -> dx
+    T* s2 = sb + 2 * SM::PT;                                   // TDF: x        DF: u (+HALO)
     T* s3 = s2 + SM::PTH;                                      // TDF: y
     __shared__ double s_agg[NW][M];
     __shared__ double s_xw[NW][M];
@@ -755,224 +872,223 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
 
     pdl_launch_dependents();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tile = blockIdx.x;
-    const int64_t seq = tile / p.ntiles;
-    const int jr = (int)(tile - seq * p.ntiles);                 // 0 = last tile in time
-    const int jt = p.ntiles - 1 - jr;                            // time index of the tile
-    const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;          // may be < 0 (first tile)
-    const double* tb = p.tab + seq * p.tab_stride;
-    const int64_t roff = seq * p.Tlen;
-    IIRG_TRACE(p.trace, tile, 0);
-
-    if (p.gy != nullptr) tile_load_async<T, TS>(dys, static_cast<const T*>(p.gy) + roff, p0, p.Tlen, p.vec);
-    else for (int e = tid; e < TS; e += NT) dys[pidx<T>(e)] = T(0);
+    const int64_t ntot = p.B * (int64_t)p.ntiles;
+    int64_t tile = blockIdx.x;
+    if (tile < ntot) bwd_issue_dy<T>(p, tile, sb);
     cp_async_commit();
-    if constexpr (PHASE == 3) {
-        if constexpr (FORM == 1) {
-            tile_load_async<T, TS>(s2, static_cast<const T*>(p.x) + roff, p0, p.Tlen, p.vec);
-            tile_load_async<T, TS>(s3, static_cast<const T*>(p.y) + roff, p0, p.Tlen, p.vec);
-        } else {
-            bwd_load_u<T, M, FORM>(p, seq, p0, s2);
-        }
-    }
-    cp_async_commit();
-    stage_small<M>(st, tb);                          // tables live in the tape (written by the forward)
+    int64_t staged = -1;
+    bool waited = false;
     T bc[M + 1], ac[M + 1], cc[M];
-    load_coefs<T, M>(tb, bc, ac, cc);
-    cp_async_wait<1>();                              // dy
-    __syncthreads();
-
-    const int c = NT - 1 - tid;          // chunk index within the tile (time order)
-    const int s0 = c * L;
-    // a5: local adjoint pass from the zero state, walking the chunk backwards.
-    T d[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) d[i] = T(0);
-#pragma unroll
-    for (int g = L / W - 1; g >= 0; --g) {
-        const V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
-#pragma unroll
-        for (int e = W - 1; e >= 0; --e) {
-            if constexpr (FORM == 1) adj_tdf_step<T, M>(d, vget(dv, e), ac);
-            else adj_df_step<T, M>(d, vget(dv, e), bc, ac);
+    for (int it = 0; tile < ntot; ++it, tile += gridDim.x) {
+        const int64_t next = tile + gridDim.x;
+        // groups in flight: dy(this) [earlier], x/y(this), dy(next)
+        if constexpr (PHASE == 3) bwd_issue_xy<T, M, FORM>(p, tile, s2, s3);
+        cp_async_commit();
+        if (next < ntot) bwd_issue_dy<T>(p, next, sb + ((it + 1) & 1) * SM::PT);
+        cp_async_commit();
+        const int64_t seq = tile / p.ntiles;
+        const int jr = (int)(tile - seq * p.ntiles);                 // 0 = last tile in time
+        const int jt = p.ntiles - 1 - jr;                            // time index of the tile
+        const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;          // may be < 0 (first tile)
+        const double* tb = p.tab + seq * p.tab_stride;
+        const int64_t roff = seq * p.Tlen;
+        T* dys = sb + (it & 1) * SM::PT;
+        const int64_t set = p.tab_stride == 0 ? 0 : seq;
+        if (set != staged) {                   // tables live in the tape (written by the forward)
+            stage_small<M>(st, tb);
+            load_coefs<T, M>(tb, bc, ac, cc);
+            staged = set;
         }
-    }
-    IIRG_TRACE(p.trace, tile, 1);
-    // a6: carries (transposed powers)
-    double S[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) S[i] = (double)d[i];
-    warp_scan<M, true>(st, lane, S);
-    if (lane == 31) {
-#pragma unroll
-        for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
-    }
-    __syncthreads();
-    if constexpr (PHASE == 1) {
-        if (warp == 0) {
-            double Jex[M], G[M];
-            block_scan<M, true>(st, lane, s_agg, Jex, G);
-            if (lane == 0) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) p.agg[tile * M + i] = G[i];
-            }
-        }
-        IIRG_TRACE(p.trace, tile, 2);
-        return;
-    } else {
-        double E[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
-        double Jex[M], G[M];
-        if (warp == 0) block_scan<M, true>(st, lane, s_agg, Jex, G);
-        pdl_wait();                                  // tile carries of phase 2
-        IIRG_TRACE(p.trace, tile, 2);
-        if (warp == 0 && lane < NW) {                // state entering warp `lane`
-            double X[M], xw[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) { X[i] = p.carry[tile * M + i]; xw[i] = Jex[i]; }
-            mv_acc_lane_s<M, true>(st + TB::PWT, NW, lane, X, xw);
-#pragma unroll
-            for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
-        }
+        IIRG_TRACE(p.trace, tile, 0);
+        cp_async_wait<2>();                                          // dy of this tile
         __syncthreads();
-        {
-            double xw[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
-            mv_acc_lane<M, true>(tb + TB::PLT, 32, lane, xw, E);
-        }
-        T din[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) { din[i] = (T)E[i]; d[i] = din[i]; }
-        cp_async_wait<0>();                          // x, y / u
-        __syncthreads();
-        IIRG_TRACE(p.trace, tile, 3);
 
-        // grad_zi = dz(-1) (Eq.9, A.3): the thread whose chunk holds n = 0 walks down
-        // to it before the emit pass overwrites dy with dx.
-        if (p.gzi != nullptr && p0 + s0 <= 0 && p0 + s0 + L > 0) {
-            T w2[M];
+        const int c = NT - 1 - tid;          // chunk index within the tile (time order)
+        const int s0 = c * L;
+        // a5: local adjoint pass from the zero state, walking the chunk backwards.
+        T d[M];
 #pragma unroll
-            for (int i = 0; i < M; ++i) w2[i] = din[i];
-            for (int n = s0 + L - 1; n >= (int)(-p0); --n) {
-                const T dy = dys[pidx<T>(n)];
-                if constexpr (FORM == 1) adj_tdf_step<T, M>(w2, dy, ac);
-                else (void)adj_df_step<T, M>(w2, dy, bc, ac);
-            }
-            T* gzi = static_cast<T*>(p.gzi) + seq * M;
-#pragma unroll
-            for (int i = 0; i < M; ++i) gzi[i] = w2[i];
-        }
-        // a7: re-run with the exact carry, emit dx, accumulate the coefficient sums.
-        T Gs[NG];
-#pragma unroll
-        for (int k = 0; k < NG; ++k) Gs[k] = T(0);
-        const bool has_neg = (p0 + s0) < 0;                 // chunk reaches before n = 0
+        for (int i = 0; i < M; ++i) d[i] = T(0);
 #pragma unroll
         for (int g = L / W - 1; g >= 0; --g) {
-            V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
-            if constexpr (FORM == 1) {
-                const V xv = *reinterpret_cast<const V*>(s2 + pidx<T>(s0 + g * W));
-                const V yv = *reinterpret_cast<const V*>(s3 + pidx<T>(s0 + g * W));
+            const V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
 #pragma unroll
-                for (int e = W - 1; e >= 0; --e) {
-                    const T dy = vget(dv, e), xx = vget(xv, e), yy = vget(yv, e);
-                    T dx = bc[0] * dy;
-#pragma unroll
-                    for (int i = 0; i < M; ++i) dx = fma(cc[i], d[i], dx);     // Eq.8: c^T dz + b0 dy
-#pragma unroll
-                    for (int i = 0; i < M; ++i) { Gs[i] = fma(d[i], xx, Gs[i]); Gs[M + i] = fma(d[i], yy, Gs[M + i]); }
-                    Gs[2 * M] = fma(dy, xx, Gs[2 * M]);
-                    vset(dv, e, dx);
-                    adj_tdf_step<T, M>(d, dy, ac);
-                }
-            } else {
-#pragma unroll
-                for (int e = W - 1; e >= 0; --e) {
-                    const int n = s0 + g * W + e;                 // tile-local time index
-                    const T dy = vget(dv, e);
-                    const T dx = adj_df_step<T, M>(d, dy, bc, ac); // dx(n), then d <- dz(n-1)
-                    const T gmask = (!has_neg || p0 + n >= 0) ? dx : T(0);
-#pragma unroll
-                    for (int k = 0; k <= M; ++k) {
-                        const T uk = s2[pidx<T>(n - k + HALO)];
-                        Gs[k] = fma(dy, uk, Gs[k]);                          // Gb[k] = sum dy u(n-k)
-                        if (k >= 1) Gs[M + k] = fma(gmask, uk, Gs[M + k]);  // Ga[k] = sum dx u(n-k)
-                    }
-                    vset(dv, e, dx);
-                }
-            }
-            *reinterpret_cast<V*>(dys + pidx<T>(s0 + g * W)) = dv;   // dx in place
-        }
-        // warp reduction of the partial sums (fp64, fixed order)
-        if (p.want_coef) {
-#pragma unroll
-            for (int k = 0; k < NG; ++k) {
-                double s = (double)Gs[k];
-#pragma unroll
-                for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-                if (lane == 0) s_red[warp][k] = s;
+            for (int e = W - 1; e >= 0; --e) {
+                if constexpr (FORM == 1) adj_tdf_step<T, M>(d, vget(dv, e), ac);
+                else adj_df_step<T, M>(d, vget(dv, e), bc, ac);
             }
         }
-        __syncthreads();
-        IIRG_TRACE(p.trace, tile, 4);
-        if (p.gx != nullptr) tile_store<T, TS>(static_cast<T*>(p.gx) + roff, dys, p0, p.Tlen, p.vec);
-        IIRG_TRACE(p.trace, tile, 5);
+        IIRG_TRACE(p.trace, tile, 1);
+        // a6: carries (transposed powers)
+        double S[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) S[i] = (double)d[i];
+        if constexpr (PHASE == 1) {
+            tile_reduce<M, true>(tb, st, lane, warp, S, s_agg, p.agg + tile * M);
+            IIRG_TRACE(p.trace, tile, 2);
+        } else {
+            warp_scan<M, true>(st, lane, S);
+            if (lane == 31) {
+#pragma unroll
+                for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
+            }
+            __syncthreads();
+            double E[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
+            if (!waited) { pdl_wait(); waited = true; }          // tile carries of phase 2
+            if (warp == 0) {
+                double Jex[M], G[M];
+                block_scan<M, true>(st, lane, s_agg, Jex, G);
+                if (lane < NW) {                                 // state entering warp `lane`
+                    double X[M], xw[M];
+#pragma unroll
+                    for (int i = 0; i < M; ++i) { X[i] = p.carry[tile * M + i]; xw[i] = Jex[i]; }
+                    mv_acc_lane_s<M, true>(st + TB::PWT, NW, lane, X, xw);
+#pragma unroll
+                    for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
+                }
+            }
+            __syncthreads();
+            IIRG_TRACE(p.trace, tile, 2);
+            {
+                double xw[M];
+#pragma unroll
+                for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
+                mv_acc_lane<M, true>(tb + TB::PLT, 32, lane, xw, E);
+            }
+            T din[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) { din[i] = (T)E[i]; d[i] = din[i]; }
+            cp_async_wait<1>();                                      // x, y / u of this tile
+            __syncthreads();
 
-        if (p.want_coef) {
-            // fused a8: group of 32 tiles -> group sum; last group of the set -> chain rule.
-            const bool shared = p.ncoef == 1;
-            const int64_t per_set = shared ? p.B * p.ntiles : p.ntiles;
-            const int64_t cset = shared ? 0 : seq;
-            const int64_t li = shared ? seq * p.ntiles + jt : jt;          // index within the set
-            const int64_t gi = li >> 5;
-            const int64_t ngroups = (per_set + 31) >> 5;
-            const int gsize = (int)min((int64_t)32, per_set - (gi << 5));
-            double* part = p.partial + cset * per_set * NG;
-            double* part2 = p.partial2 + cset * ngroups * NG;
-            if (tid < NG) {
-                double s = 0.0;
+            // grad_zi = dz(-1) (Eq.9, A.3): the thread whose chunk holds n = 0 walks down
+            // to it before the emit pass overwrites dy with dx.
+            if (p.gzi != nullptr && p0 + s0 <= 0 && p0 + s0 + L > 0) {
+                T w2[M];
 #pragma unroll
-                for (int w = 0; w < NW; ++w) s += s_red[w][tid];
-                __stcg(part + li * NG + tid, s);
-                __threadfence();
+                for (int i = 0; i < M; ++i) w2[i] = din[i];
+                for (int n = s0 + L - 1; n >= (int)(-p0); --n) {
+                    const T dy = dys[pidx<T>(n)];
+                    if constexpr (FORM == 1) adj_tdf_step<T, M>(w2, dy, ac);
+                    else (void)adj_df_step<T, M>(w2, dy, bc, ac);
+                }
+                T* gzi = static_cast<T*>(p.gzi) + seq * M;
+#pragma unroll
+                for (int i = 0; i < M; ++i) gzi[i] = w2[i];
+            }
+            // a7: re-run with the exact carry, emit dx, accumulate the coefficient sums.
+            T Gs[NG];
+#pragma unroll
+            for (int k = 0; k < NG; ++k) Gs[k] = T(0);
+            const bool has_neg = (p0 + s0) < 0;                 // chunk reaches before n = 0
+#pragma unroll
+            for (int g = L / W - 1; g >= 0; --g) {
+                V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
+                if constexpr (FORM == 1) {
+                    const V xv = *reinterpret_cast<const V*>(s2 + pidx<T>(s0 + g * W));
+                    const V yv = *reinterpret_cast<const V*>(s3 + pidx<T>(s0 + g * W));
+#pragma unroll
+                    for (int e = W - 1; e >= 0; --e) {
+                        const T dy = vget(dv, e), xx = vget(xv, e), yy = vget(yv, e);
+                        T dx = bc[0] * dy;
+#pragma unroll
+                        for (int i = 0; i < M; ++i) dx = fma(cc[i], d[i], dx);     // Eq.8: c^T dz + b0 dy
+#pragma unroll
+                        for (int i = 0; i < M; ++i) { Gs[i] = fma(d[i], xx, Gs[i]); Gs[M + i] = fma(d[i], yy, Gs[M + i]); }
+                        Gs[2 * M] = fma(dy, xx, Gs[2 * M]);
+                        vset(dv, e, dx);
+                        adj_tdf_step<T, M>(d, dy, ac);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = W - 1; e >= 0; --e) {
+                        const int n = s0 + g * W + e;                 // tile-local time index
+                        const T dy = vget(dv, e);
+                        const T dx = adj_df_step<T, M>(d, dy, bc, ac); // dx(n), then d <- dz(n-1)
+                        const T gmask = (!has_neg || p0 + n >= 0) ? dx : T(0);
+#pragma unroll
+                        for (int k = 0; k <= M; ++k) {
+                            const T uk = s2[pidx<T>(n - k + HALO)];
+                            Gs[k] = fma(dy, uk, Gs[k]);                          // Gb[k] = sum dy u(n-k)
+                            if (k >= 1) Gs[M + k] = fma(gmask, uk, Gs[M + k]);  // Ga[k] = sum dx u(n-k)
+                        }
+                        vset(dv, e, dx);
+                    }
+                }
+                *reinterpret_cast<V*>(dys + pidx<T>(s0 + g * W)) = dv;   // dx in place
+            }
+            // warp reduction of the partial sums (fp64, fixed order)
+            if (p.want_coef) {
+#pragma unroll
+                for (int k = 0; k < NG; ++k) {
+                    double s = (double)Gs[k];
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                    if (lane == 0) s_red[warp][k] = s;
+                }
             }
             __syncthreads();
-            if (tid == 0) s_fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
-            __syncthreads();
-            if (s_fin) {                                   // last tile of its group
-                __threadfence();
+            IIRG_TRACE(p.trace, tile, 3);
+            if (p.gx != nullptr) tile_store<T, TS>(static_cast<T*>(p.gx) + roff, dys, p0, p.Tlen, p.vec);
+
+            if (p.want_coef) {
+                // fused a8: group of 32 tiles -> group sum; last group of the set -> chain rule.
+                const bool shared = p.ncoef == 1;
+                const int64_t per_set = shared ? p.B * p.ntiles : p.ntiles;
+                const int64_t cset = shared ? 0 : seq;
+                const int64_t li = shared ? seq * p.ntiles + jt : jt;          // index within the set
+                const int64_t gi = li >> 5;
+                const int64_t ngroups = (per_set + 31) >> 5;
+                const int gsize = (int)min((int64_t)32, per_set - (gi << 5));
+                double* part = p.partial + cset * per_set * NG;
+                double* part2 = p.partial2 + cset * ngroups * NG;
                 if (tid < NG) {
                     double s = 0.0;
-                    for (int t = 0; t < gsize; ++t) s += __ldcg(part + ((gi << 5) + t) * NG + tid);
-                    __stcg(part2 + gi * NG + tid, s);
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) s += s_red[w][tid];
+                    __stcg(part + li * NG + tid, s);
                     __threadfence();
                 }
                 __syncthreads();
-                if (tid == 0) {
-                    p.gcnt[cset * ngroups + gi] = 0u;
-                    s_fin = (atomicAdd(p.scnt + cset, 1u) == (unsigned)ngroups - 1u) ? 2u : 0u;
-                }
+                if (tid == 0) s_fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
                 __syncthreads();
-                if (s_fin == 2u) {                          // last group of the set
+                if (s_fin) {                                   // last tile of its group
                     __threadfence();
                     if (tid < NG) {
                         double s = 0.0;
-                        for (int64_t g2 = 0; g2 < ngroups; ++g2) s += __ldcg(part2 + g2 * NG + tid);
-                        s_G[tid] = s;
+                        for (int t = 0; t < gsize; ++t) s += __ldcg(part + ((gi << 5) + t) * NG + tid);
+                        __stcg(part2 + gi * NG + tid, s);
+                        __threadfence();
                     }
                     __syncthreads();
                     if (tid == 0) {
-                        chain_rule<T, M, FORM>(s_G, tb,
-                                               p.gb == nullptr ? nullptr : static_cast<T*>(p.gb) + cset * (M + 1),
-                                               p.ga == nullptr ? nullptr : static_cast<T*>(p.ga) + cset * (M + 1));
-                        p.scnt[cset] = 0u;
+                        p.gcnt[cset * ngroups + gi] = 0u;
+                        s_fin = (atomicAdd(p.scnt + cset, 1u) == (unsigned)ngroups - 1u) ? 2u : 0u;
+                    }
+                    __syncthreads();
+                    if (s_fin == 2u) {                          // last group of the set
+                        __threadfence();
+                        if (tid < NG) {
+                            double s = 0.0;
+                            for (int64_t g2 = 0; g2 < ngroups; ++g2) s += __ldcg(part2 + g2 * NG + tid);
+                            s_G[tid] = s;
+                        }
+                        __syncthreads();
+                        if (tid == 0) {
+                            chain_rule<T, M, FORM>(s_G, tb,
+                                                   p.gb == nullptr ? nullptr : static_cast<T*>(p.gb) + cset * (M + 1),
+                                                   p.ga == nullptr ? nullptr : static_cast<T*>(p.ga) + cset * (M + 1));
+                            p.scnt[cset] = 0u;
+                        }
                     }
                 }
             }
         }
+        __syncthreads();                                  // this stage may be refilled
     }
+    if (!waited) pdl_wait();
 }
 
 }  // namespace iirg
