@@ -49,11 +49,11 @@ def algorithmic_bytes(w):
     if w["coef"] == "per_sample":
         M = w["order"]
         return {"tv_fwd": (2 + M) * s, "tv_bwd": (4 + 2 * M) * s}
-    # first-touch HBM bytes per kernel: phase 1 reads x / dy, phase 3 re-reads them
-    # from L2 and moves the rest; the sum is the method's 24 B/sample (fp32)
+    # HBM bytes per kernel the method must move: fwd reads x, writes y (+u for DF);
+    # bwd reads dy, x, y (TDF) or dy, u (DF) and writes dx: 24 B/sample in fp32
     if w["form"] == "tdf":
-        return {"lti_fwd_agg": s, "lti_fwd_emit": s, "lti_bwd_agg": s, "lti_bwd_emit": 3 * s}
-    return {"lti_fwd_agg": s, "lti_fwd_emit": 2 * s, "lti_bwd_agg": s, "lti_bwd_emit": 2 * s}
+        return {"lti_fwd": 2 * s, "lti_bwd": 4 * s}
+    return {"lti_fwd": 3 * s, "lti_bwd": 3 * s}
 
 
 def peaks():

@@ -26,8 +26,7 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
 }  // namespace iirg
 
 // ------------------------------------------------------- instrumentation ----
-static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd_agg", "lti_carry", "lti_fwd_emit", "lti_bwd_agg",
-                                        "lti_bwd_emit", "tv_fwd", "tv_bwd", "tv_fix"};
+static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_fwd", "tv_bwd", "tv_fix"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;
@@ -93,6 +92,8 @@ static iir_status_t check_desc(const iir_desc_t* d) {
         return fail(IIR_EINVAL, "coef_mode must be SHARED, PER_SEQ or PER_SAMPLE");
     if (d->order < 1 || d->order > 8) return fail(IIR_EUNSUPPORTED, "order must be 1..8 for LTI filters");
     const int64_t TS = tile_samples(d->dtype);
+    if ((d->length + TS - 1) / TS > (int64_t(1) << (5 * MAX_LEVELS)))
+        return fail(IIR_EUNSUPPORTED, "length exceeds 32^4 tiles per sequence");
     if (d->batch * ((d->length + TS - 1) / TS) >= (int64_t(1) << 31))
         return fail(IIR_EUNSUPPORTED, "batch x tiles exceeds 2^31 CTAs");
     return IIR_OK;
@@ -106,16 +107,21 @@ static Layout layout(const iir_desc_t* d) {
     L.ntiles = (d->length + TS - 1) / TS;
     L.ntot = L.ntiles * d->batch;
     L.ncoef = d->coef_mode == IIR_COEF_SHARED ? 1 : d->batch;
-    L.nlev = 1;                                   // the carry pass needs A_f^(k TS), k < 32, only
+    L.nlev = 1;
+    while (L.nlev < MAX_LEVELS && (int64_t(1) << (5 * L.nlev)) < L.ntiles) ++L.nlev;
+    for (int l = 0; l < MAX_LEVELS; ++l)
+        L.nblk[l] = l < L.nlev ? (L.ntiles + (int64_t(1) << (5 * l)) - 1) >> (5 * l) : 0;
     const int64_t per_set = d->coef_mode == IIR_COEF_SHARED ? L.ntot : L.ntiles;
     const int64_t ng_set = (per_set + 31) / 32;
     L.ngroups = ng_set * L.ncoef;
     size_t o = 0;
+    L.ws_ticket = o; L.ws_done = o + 4; o += 256;
     L.ws_gcnt = o; o += al256(L.ngroups * 4);
     L.ws_scnt = o; o += al256(L.ncoef * 4);
     L.ws_clear = o;
-    L.ws_agg = o; o += al256(L.ntot * M * 8);
-    L.ws_carry = o; o += al256(L.ntot * M * 8);
+    L.ws_sent = o;
+    for (int l = 0; l < L.nlev; ++l) { L.ws_agg[l] = o; o += al256(d->batch * L.nblk[l] * M * 8); }
+    L.ws_sent_bytes = o - L.ws_sent;
     L.ws_part = o; o += al256(L.ntot * (2 * M + 1) * 8);
     L.ws_part2 = o; o += al256(L.ngroups * (2 * M + 1) * 8);
     L.ws_bytes = o;
@@ -145,8 +151,22 @@ static iir_status_t run_lti_any(LtiCall& c) {
 }
 
 static unsigned long long* g_trace = nullptr;
+static CarryWs carry_ws(const Layout& L, char* w) {
+    CarryWs c{};
+    c.ticket = reinterpret_cast<unsigned*>(w + L.ws_ticket);
+    c.done = reinterpret_cast<unsigned*>(w + L.ws_done);
+    for (int l = 0; l < MAX_LEVELS; ++l) {
+        c.agg[l] = l < L.nlev ? reinterpret_cast<double*>(w + L.ws_agg[l]) : nullptr;
+        c.nblk[l] = L.nblk[l];
+    }
+    c.nlev = L.nlev;
+    return c;
+}
+
 static iir_status_t ws_reset(const Layout& L, void* ws, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(ws, 0, L.ws_clear, st);
+    if (e == cudaSuccess && L.ws_sent_bytes)
+        e = cudaMemsetAsync(static_cast<char*>(ws) + L.ws_sent, 0xFF, L.ws_sent_bytes, st);
     if (e != cudaSuccess) return fail(IIR_ECUDA, std::string("workspace memset: ") + cudaGetErrorString(e));
     return IIR_OK;
 }
@@ -209,12 +229,9 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     fa.u = d->form == IIR_DF2 ? t + L.tp_u : nullptr;
     fa.tab = reinterpret_cast<const double*>(t + L.tp_tab);
     fa.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
-    fa.agg = reinterpret_cast<double*>(w + L.ws_agg);
-    fa.carry = reinterpret_cast<const double*>(w + L.ws_carry);
+    fa.cw = carry_ws(L, w);
     fa.B = d->batch; fa.Tlen = d->length; fa.ntiles = (int)L.ntiles; fa.vec = vec;
     fa.trace = g_trace;
-    c.ca = CarryArgs{fa.agg, reinterpret_cast<double*>(w + L.ws_carry), zi, d->dtype == IIR_F64,
-                     fa.tab, fa.tab_stride, d->batch, (int)L.ntiles};
     return run_lti_any(c);
 }
 
@@ -259,12 +276,9 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     ba.want_coef = (grad_b != nullptr || grad_a != nullptr);
     ba.tab = reinterpret_cast<const double*>(t + L.tp_tab);
     ba.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
-    ba.agg = reinterpret_cast<double*>(w + L.ws_agg);
-    ba.carry = reinterpret_cast<const double*>(w + L.ws_carry);
+    ba.cw = carry_ws(L, w);
     ba.B = d->batch; ba.Tlen = d->length; ba.ntiles = (int)L.ntiles; ba.vec = vec;
     ba.trace = g_trace;
-    c.ca = CarryArgs{ba.agg, reinterpret_cast<double*>(w + L.ws_carry), grad_zf, d->dtype == IIR_F64,
-                     ba.tab, ba.tab_stride, d->batch, (int)L.ntiles};
     (void)b; (void)a;
     return run_lti_any(c);
 }

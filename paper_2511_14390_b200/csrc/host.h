@@ -13,8 +13,7 @@ namespace iirg {
 
 iir_status_t fail(iir_status_t st, const std::string& msg);
 
-enum Kind { K_LTI_PREP = 0, K_LTI_FWD1, K_LTI_CARRY, K_LTI_FWD3, K_LTI_BWD1, K_LTI_BWD3, K_TV_FWD, K_TV_BWD, K_TV_FIX,
-            K_NUM };
+enum Kind { K_LTI_PREP = 0, K_LTI_FWD, K_LTI_BWD, K_TV_FWD, K_TV_BWD, K_TV_FIX, K_NUM };
 
 // Launch bookkeeping: counts every kernel and (when profiling is on) brackets it
 // with CUDA events on its stream.
@@ -38,9 +37,10 @@ struct Layout {
     int nlev = 0;
     int64_t nblk[MAX_LEVELS] = {0, 0, 0, 0};
     // workspace: counters + flags (cleared region), then payloads
-    size_t ws_gcnt = 0, ws_scnt = 0;
+    size_t ws_ticket = 0, ws_done = 0, ws_gcnt = 0, ws_scnt = 0;
     size_t ws_clear = 0;                                   // [0, ws_clear): counters, initialised to 0
-    size_t ws_agg = 0, ws_carry = 0, ws_part = 0, ws_part2 = 0, ws_bytes = 0;
+    size_t ws_sent = 0, ws_sent_bytes = 0;                 // look-back slots, initialised to all-ones (NaN)
+    size_t ws_agg[MAX_LEVELS] = {0, 0, 0, 0}, ws_part = 0, ws_part2 = 0, ws_bytes = 0;
     size_t tp_tab = 0, tp_u = 0, tp_extra = 0, tp_bytes = 0;
 };
 

@@ -19,6 +19,7 @@
 
 namespace iirg {
 
+constexpr int LEVELS = 4;          // hierarchical carry levels: ntiles <= 32^4 per sequence
 constexpr int PREP_THREADS = 256;
 
 // ---------------------------------------------------------------------------
@@ -30,9 +31,8 @@ template <int M> struct Tab {
     static constexpr int PWT = PW + LOG_NW * M2;       // A_f^(32L w), w = 0..NW-1       [i][j][w]
     static constexpr int SMALL = PWT + NW * M2;        // [0, SMALL): staged in shared memory per CTA
     static constexpr int PLT = SMALL;                  // A_f^(L t),   t = 0..31         [i][j][t]
-    static constexpr int PQ = PLT + 32 * M2;           // A_f^(k TS), k = 0..31          [i][j][k]
-    static constexpr int PC = PQ + 32 * M2;            // A_f^(4 TS 2^d), d = 0..8 (carry pass) [d][i][j]
-    static constexpr int COEF = PC + 9 * M2;           // b'[0..M], a'[0..M], c[0..M-1]
+    static constexpr int PQ = PLT + 32 * M2;           // A_f^(k 32^l TS), k = 0..31     [l][i][j][k]
+    static constexpr int COEF = PQ + LEVELS * 32 * M2; // b'[0..M], a'[0..M], c[0..M-1]
     static constexpr int A0 = COEF + 3 * M + 2;        // a0 (un-normalised)
     static constexpr int SIZE = (A0 + 1 + 31) / 32 * 32;
 };
@@ -120,8 +120,8 @@ __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepc
 // TDF: its transpose) and every fp64 power table by batched
 // doubling (log depth): about 30 dependent matrix-product steps.
 template <int M> struct PrepSlots {
-    static constexpr int P1 = 0, PLT = 1 /* 33 */, YP = PLT + 33 /* 5 */, Q = YP + 5 /* 33 */, C = Q + 33 /* 9 */;
-    static constexpr int N = C + 9;
+    static constexpr int P1 = 0, PLT = 1 /* 33 */, YP = PLT + 33 /* 5 */, Q = YP + 5 /* LEVELS x 33 */;
+    static constexpr int N = Q + LEVELS * 33;
     static constexpr size_t bytes() { return (size_t)N * M * M * sizeof(double); }
 };
 
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restr
         const double id = (i == j) ? 1.0 : 0.0;
         mat[(S::PLT + 0) * M2 + e] = id;
         mat[(S::YP + 0) * M2 + e] = id;
-        mat[S::Q * M2 + e] = id;
+        for (int l = 0; l < LEVELS; ++l) mat[(S::Q + l * 33) * M2 + e] = id;
     }
     if (tid <= M) { tb[TB::COEF + tid] = bn[tid]; tb[TB::COEF + M + 1 + tid] = an[tid]; }
     if (tid < M) tb[TB::COEF + 2 * (M + 1) + tid] = bn[tid + 1] - an[tid + 1] * bn[0];
@@ -208,11 +208,10 @@ __global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restr
     copy(S::YP + 1, S::PLT + 32);
     powers(S::YP, LOG_NW);                                              // A_f^(32 L w), w = 0..NW
     copy(S::Q + 1, S::YP + NW);                                         // A_f^TS
-    powers(S::Q, 5);                                                    // A_f^(k TS), k = 0..32
-    copy(S::C, S::Q + 4);                                               // A_f^(4 TS 2^d), d = 0..8
-    for (int d = 1; d < 9; ++d)
-        mm_batch(1, [&](int) { return S::C + d; }, [&](int) { return S::C + d - 1; }, [&](int) { return S::C + d - 1; });
-    (void)nlev;
+    for (int l = 0; l < nlev; ++l) {                                    // A_f^(k 32^l TS), k = 0..32
+        powers(S::Q + l * 33, 5);
+        if (l + 1 < LEVELS) copy(S::Q + (l + 1) * 33 + 1, S::Q + l * 33 + 32);
+    }
     // write out in the kernels' layouts
     for (int e = tid; e < M2; e += PREP_THREADS) {
         for (int d = 0; d < 5; ++d) tb[TB::PL + d * M2 + e] = mat[(S::PLT + (1 << d)) * M2 + e];
@@ -224,11 +223,10 @@ __global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restr
         tb[TB::PLT + w] = mat[(S::PLT + t) * M2 + e];
     }
     (void)0;
-    for (int w = tid; w < 32 * M2; w += PREP_THREADS) {
-        const int e = w / 32, k = w % 32;
-        tb[TB::PQ + w] = mat[(S::Q + k) * M2 + e];
+    for (int w = tid; w < nlev * 32 * M2; w += PREP_THREADS) {
+        const int l = w / (32 * M2), r = w % (32 * M2), e = r / 32, k = r % 32;
+        tb[TB::PQ + w] = mat[(S::Q + l * 33 + k) * M2 + e];
     }
-    for (int w = tid; w < 9 * M2; w += PREP_THREADS) tb[TB::PC + w] = mat[(S::C + w / M2) * M2 + (w % M2)];
 }
 
 // ---------------------------------------------------------------------------
@@ -323,15 +321,20 @@ __device__ __forceinline__ void chain_rule(const double* __restrict__ G, const d
 }
 
 // ---------------------------------------------------------------------------
-// Kernel arguments.  Scan order: forward tiles in time order (tile jt covers
-// [jt TS, (jt+1) TS)), backward tiles in reverse time order (tile jr covers
-// [T - (jr+1) TS, T - jr TS)).  agg / carry are indexed [seq][scan index][M].
+// Grid-level carry bookkeeping (workspace pointers), shared by fwd and bwd.
+struct CarryWs {
+    unsigned* ticket;            // tile ticket counter (tiles are scanned in ticket order)
+    unsigned* done;              // CTAs finished (the last one restores the workspace)
+    double* agg[LEVELS];         // level-l block aggregates [seq][block][M]; all-ones NaN = not published
+    int64_t nblk[LEVELS];        // blocks per sequence at level l (ceil(ntiles / 32^l))
+    int nlev;                    // levels in use
+};
+
 struct LtiFwdArgs {
     const void* b; const void* a; int64_t coef_stride;           // raw coefficients (local pass)
     const void* x; const void* zi; void* y; void* zf; void* u;    // u: DF tape signal
     const double* tab; int64_t tab_stride;                        // 0 for SHARED
-    double* agg;                                                  // tile aggregates (phase 1)
-    const double* carry;                                          // state entering each tile (phase 3)
+    CarryWs cw;
     int64_t B, Tlen; int ntiles; int vec;
     unsigned long long* trace;                                    // debug: per-tile phase times
 };
@@ -342,20 +345,14 @@ struct LtiBwdArgs {
     double* partial; double* partial2; unsigned* gcnt; unsigned* scnt;   // fused finalize
     int64_t ncoef;
     const double* tab; int64_t tab_stride;
-    double* agg; const double* carry;
+    CarryWs cw;
     int64_t B, Tlen; int ntiles; int vec;
     unsigned long long* trace;
 };
 
-struct CarryArgs {
-    const double* agg; double* carry;
-    const void* x0; int x0_f64;                                   // zi (fwd) / grad_zf (bwd), may be NULL
-    const double* tab; int64_t tab_stride;
-    int64_t B; int ntiles;
-};
-
 // Normalised coefficients in T, straight from the caller's b, a (the same
-// rounding as the prologue's fp64 b/a0, a/a0 cast to T).
+// rounding as the prologue's fp64 b/a0, a/a0 cast to T): the forward local pass
+// runs before the prologue's tables are ready.
 template <typename T, int M>
 __device__ __forceinline__ void raw_coefs(const T* __restrict__ b, const T* __restrict__ a, T (&bc)[M + 1],
                                           T (&ac)[M + 1]) {
@@ -427,227 +424,148 @@ __device__ __forceinline__ void warp_sum(double (&v)[M]) {
         for (int i = 0; i < M; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
 }
 
-// Phase 1 needs only the tile aggregate, a reduction rather than a scan:
-//   G = sum_t A_f^(L (NT-1-t)) w_t   (t in scan order; TR: transposed powers)
-// lane term with A_f^(L (31-lane)), fixed butterfly sum per warp, then warp 0
-// combines the NW warp sums with A_f^(32 L (NW-1-w)).  Writes G to dst.
-template <int M, bool TR>
-__device__ __forceinline__ void tile_reduce(const double* __restrict__ tb, const double* st, int lane, int warp,
-                                            const double (&w)[M], double (*s_agg)[M], double* dst) {
-    using TB = Tab<M>;
-    double t[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) t[i] = 0.0;
-    mv_acc_lane<M, TR>(tb + TB::PLT, 32, 31 - lane, w, t);
-    warp_sum<M>(t);
+template <int M>
+__device__ __forceinline__ void publish(double* dst, const double (&v)[M], int lane) {
     if (lane == 0) {
 #pragma unroll
-        for (int i = 0; i < M; ++i) s_agg[warp][i] = t[i];
+        for (int i = 0; i < M; ++i) __stcg(dst + i, v[i]);
     }
-    __syncthreads();
-    if (warp == 0) {
-        double v[M], g[M];
+}
+
+// Wait until a look-back payload slot is published and read it: one element is
+// polled (volatile loads: never hoisted, never served from a stale L1 line)
+// with exponential back-off, then all M are read and re-checked.  A slot that
+// is never published is a bug: report and trap instead of hanging the GPU.
+template <int M>
+__device__ __forceinline__ void wait_slot(const double* src, double (&v)[M]) {
+    unsigned ns = 32;
+    unsigned long long t0 = 0;
+    for (;;) {
+        if (!is_sentinel(ld_relaxed(src))) {
+            bool ready = true;
 #pragma unroll
-        for (int i = 0; i < M; ++i) { v[i] = (lane < NW) ? s_agg[lane][i] : 0.0; g[i] = 0.0; }
-        if (lane < NW) mv_acc_lane_s<M, TR>(st + TB::PWT, NW, NW - 1 - lane, v, g);
-        warp_sum<M>(g);
+            for (int i = 0; i < M; ++i) { v[i] = ld_relaxed(src + i); ready = ready && !is_sentinel(v[i]); }
+            if (ready) return;
+        }
+        __nanosleep(ns);
+        if (ns < 512) ns *= 2;
+        else {
+            const unsigned long long now = gtimer();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 4000000000ull) {
+                printf("iirgrad: look-back slot %p never published\n", (const void*)src);
+                __trap();
+            }
+        }
+    }
+}
+
+// Grid-level carry (warp 0).  Tile j (scan order within its sequence) has
+// base-32 digits d_l.  With AGG^(0) = tile aggregates (tile 0's includes the
+// initial state X0) and AGG^(l+1)_b = sum_{d<32} Q_l^(31-d) AGG^(l)_{32b+d},
+// Q_l = A_f^(32^l TS):
+//   T_l = sum_{d < d_l} Q_l^(d_l - 1 - d) AGG^(l)_{(j >> 5l) - d_l + d}
+//   X_j = T_0 + Q_0^d_0 (T_1 + Q_1^d_1 (T_2 + ...))     (state entering tile j)
+// Each T_l is one lane-parallel round (lane d waits for one aggregate) and a
+// fixed butterfly sum: bitwise deterministic, and no tile waits on a serial
+// chain.  A tile that closes a level-(l+1) block publishes AGG^(l+1) =
+// Q_l T_l + AGG^(l)_own right after T_l, before any higher-level wait.
+template <int M, bool TR>
+__device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int lane, int jt, int64_t seq,
+                                           const double (&X0)[M], double (&G)[M], const CarryWs& cw,
+                                           double (&X)[M]) {
+    using TB = Tab<M>;
+    constexpr int M2 = M * M;
+    __shared__ double s_T[LEVELS][M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) X[i] = X0[i];
+    if (jt == 0) mv_acc_lane<M, TR>(tb + TB::PQ, 32, 1, X0, G);   // tile 0 carries the initial state
+    publish<M>(cw.agg[0] + (seq * cw.nblk[0] + jt) * M, G, lane);
+    if (jt == 0) return;
+    int dl[LEVELS];
+    bool closing = true;                   // all lower digits were 31 so far
+    double Own[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) Own[i] = G[i];
+#pragma unroll
+    for (int l = 0; l < LEVELS; ++l) {
+        dl[l] = (jt >> (5 * l)) & 31;
+        double Tv[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) Tv[i] = 0.0;
+        if (l < cw.nlev && dl[l] > 0) {
+            const int64_t base = seq * cw.nblk[l] + (jt >> (5 * l)) - dl[l];
+            if (lane < dl[l]) {
+                double v[M];
+                wait_slot<M>(cw.agg[l] + (base + lane) * M, v);
+                mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, dl[l] - 1 - lane, v, Tv);
+            }
+            warp_sum<M>(Tv);
+        }
         if (lane == 0) {
 #pragma unroll
-            for (int i = 0; i < M; ++i) dst[i] = g[i];
+            for (int i = 0; i < M; ++i) s_T[l][i] = Tv[i];
+        }
+        closing = closing && dl[l] == 31;
+        if (closing && l + 1 < cw.nlev) {
+            mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, 1, Tv, Own);   // Own = Q_l T_l + Own
+            const int64_t bi = seq * cw.nblk[l + 1] + (jt >> (5 * (l + 1)));
+            publish<M>(cw.agg[l + 1] + bi * M, Own, lane);
         }
     }
+    __syncwarp();
+    double R[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) R[i] = 0.0;
+#pragma unroll
+    for (int l = LEVELS - 1; l >= 0; --l) {
+        if (l < cw.nlev) {
+            double R2[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) R2[i] = s_T[l][i];
+            if (l + 1 < cw.nlev) mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, dl[l], R, R2);
+#pragma unroll
+            for (int i = 0; i < M; ++i) R[i] = R2[i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i) X[i] = R[i];
 }
 
-// ---------------------------------------------------------------------------
-// Phase 2 (a3/a6 across tiles): per sequence, the exact state entering every
-// tile from the tile aggregates:  X_0 = x0,  X_{j+1} = Q X_j + agg_j, Q = A_f^TS.
-// One CTA per sequence walks the tiles in chunks of CARRY_CHUNK staged in
-// shared memory; thread t owns CARRY_K consecutive tiles of a chunk: a Horner
-// pass gives its aggregate, a block-wide Kogge-Stone scan with Q^(K 2^d)
-// (fp64) gives its entering state, a second Horner pass writes X per tile.
-// Fixed order throughout: bitwise deterministic.
-constexpr int CARRY_THREADS = 256;
-constexpr int CARRY_K = 4;
-constexpr int CARRY_CHUNK = CARRY_THREADS * CARRY_K;
-
+// The last CTA to finish restores the workspace (tickets, look-back slots), so
+// the next call on the same stream-ordered workspace needs no memset.  No fence:
+// every CTA's slot reads completed (their values were consumed) before its
+// increment.
 template <int M>
-constexpr size_t carry_smem() { return (size_t)CARRY_CHUNK * M * sizeof(double); }
-
-template <int M, bool TR>
-__global__ void __launch_bounds__(CARRY_THREADS) lti_carry_kernel(const CarryArgs c) {
-    constexpr int M2 = M * M;
-    constexpr int NWC = CARRY_THREADS / 32;
-    using TB = Tab<M>;
-    extern __shared__ __align__(16) unsigned char carry_raw[];
-    double* sA = reinterpret_cast<double*>(carry_raw);     // [CARRY_CHUNK][M] aggregates of a chunk
-    __shared__ __align__(16) double sQ[M2];                 // Q = A_f^TS (transposed for the adjoint)
-    __shared__ __align__(16) double sR[9][M2];              // Q^(K 2^d), d = 0..8
-    __shared__ double sW[NWC][M];
-    __shared__ double sX[M];
-    pdl_launch_dependents();
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t seq = blockIdx.x;
-    const double* tb = c.tab + seq * c.tab_stride;
-    const int n = c.ntiles;
-    for (int e = tid; e < M2; e += CARRY_THREADS) {
-        const int i = e / M, j = e % M;
-        const int src = TR ? j * M + i : e;
-        sQ[e] = __ldg(tb + TB::PQ + src * 32 + 1);                                  // A_f^TS
-#pragma unroll
-        for (int d = 0; d < 9; ++d) sR[d][e] = __ldg(tb + TB::PC + d * M2 + src); // A_f^(K TS 2^d)
-    }
-    static_assert(CARRY_K == 4, "PC tables hold A_f^(4 TS 2^d)");
-    if (tid < M) {
-        double x0 = 0.0;
-        if (c.x0 != nullptr)
-            x0 = c.x0_f64 ? static_cast<const double*>(c.x0)[seq * M + tid]
-                          : (double)static_cast<const float*>(c.x0)[seq * M + tid];
-        sX[tid] = x0;
-    }
+__device__ __forceinline__ void cta_exit(const CarryWs& cw, int64_t B, unsigned nctas) {
+    __shared__ unsigned s_last;
     __syncthreads();
-    pdl_wait();                                                                 // phase-1 aggregates
-    const double* agg = c.agg + seq * (int64_t)n * M;
-    double* carry = c.carry + seq * (int64_t)n * M;
-    for (int cs = 0; cs < n; cs += CARRY_CHUNK) {
-        const int cnt = min(CARRY_CHUNK, n - cs);
-        for (int e = tid; e < CARRY_CHUNK * M; e += CARRY_THREADS)
-            sA[e] = (e < cnt * M) ? __ldcg(agg + (int64_t)cs * M + e) : 0.0;
-        __syncthreads();
-        // Horner over this thread's tiles
-        double S[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) S[i] = 0.0;
-#pragma unroll
-        for (int q = 0; q < CARRY_K; ++q) {
-            double Sn[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) Sn[i] = sA[(tid * CARRY_K + q) * M + i];
-            mv_acc_s<M, false>(sQ, S, Sn);
-#pragma unroll
-            for (int i = 0; i < M; ++i) S[i] = Sn[i];
-        }
-        // inclusive scan across threads: warp level then across warps
-#pragma unroll
-        for (int d = 0; d < 5; ++d) {
-            const int off = 1 << d;
-            double O[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) O[i] = shfl_up_d(S[i], off);
-            if (lane >= off) mv_acc_s<M, false>(sR[d], O, S);
-        }
-        if (lane == 31) {
-#pragma unroll
-            for (int i = 0; i < M; ++i) sW[warp][i] = S[i];
-        }
-        __syncthreads();
-        if (warp == 0) {
-            double Wv[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) Wv[i] = (lane < NWC) ? sW[lane][i] : 0.0;
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                const int off = 1 << d;
-                double O[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) O[i] = shfl_up_d(Wv[i], off);
-                if (lane >= off && lane < NWC) mv_acc_s<M, false>(sR[5 + d], O, Wv);
-            }
-            double We[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) { We[i] = shfl_up_d(Wv[i], 1); if (lane == 0) We[i] = 0.0; }
-            __syncwarp();
-            if (lane < NWC) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) sW[lane][i] = We[i];
-            }
-        }
-        __syncthreads();
-        // entering state: exclusive lane prefix + Q^(K lane) (warp prefix) + Q^(K tid) X_chunk
-        double E[M], Y[M], Z[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) {
-            E[i] = shfl_up_d(S[i], 1);
-            if (lane == 0) E[i] = 0.0;
-            Y[i] = sW[warp][i];
-            Z[i] = sX[i];
-        }
-#pragma unroll
-        for (int d = 0; d < 8; ++d) {                 // Z <- Q^(K tid) X,  Y <- Q^(K lane) Y
-            if ((tid >> d) & 1) {
-                double Zn[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) Zn[i] = 0.0;
-                mv_acc_s<M, false>(sR[d], Z, Zn);
-#pragma unroll
-                for (int i = 0; i < M; ++i) Z[i] = Zn[i];
-            }
-            if (d < 5 && ((lane >> d) & 1)) {
-                double Yn[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) Yn[i] = 0.0;
-                mv_acc_s<M, false>(sR[d], Y, Yn);
-#pragma unroll
-                for (int i = 0; i < M; ++i) Y[i] = Yn[i];
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < M; ++i) E[i] += Y[i] + Z[i];
-        __syncthreads();                                        // everyone has read sX / sW
-        // second Horner pass: state entering each tile
-#pragma unroll
-        for (int q = 0; q < CARRY_K; ++q) {
-            const int t = tid * CARRY_K + q;
-            double Sn[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) {
-                if (t < cnt) carry[(int64_t)(cs + t) * M + i] = E[i];
-                Sn[i] = sA[t * M + i];
-            }
-            mv_acc_s<M, false>(sQ, E, Sn);
-#pragma unroll
-            for (int i = 0; i < M; ++i) E[i] = Sn[i];
-        }
-        if (tid == CARRY_THREADS - 1) {                          // state at the end of the chunk
-#pragma unroll
-            for (int i = 0; i < M; ++i) sX[i] = E[i];
-        }
-        __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(cw.done, 1u) == nctas - 1u) ? 1u : 0u;
+    __syncthreads();
+    if (s_last) {
+        for (int l = 0; l < cw.nlev; ++l)
+            for (int64_t i = threadIdx.x; i < B * cw.nblk[l] * M; i += blockDim.x) cw.agg[l][i] = sentinel();
+        if (threadIdx.x == 0) { *cw.ticket = 0u; *cw.done = 0u; }
     }
 }
 
-// ---------------------------------------------------------------------------
 template <typename T, int M>
 struct Smem {
     static constexpr int TS = NT * Chunk<T>::L;
     static constexpr int PT = pidx<T>(TS);               // one padded tile
     static constexpr int PTH = pidx<T>(TS + HALO);       // padded tile with u history
     static constexpr size_t tab_bytes = ((size_t)Tab<M>::SMALL * 8 + 15) / 16 * 16;
-    // forward: 2 stages of x (-> y), plus the u tile for DF emits
-    static constexpr size_t fwd(int form, int phase) {
-        return tab_bytes + (size_t)(2 * PT + (form == 0 && phase == 3 ? PT : 0)) * sizeof(T);
+    static constexpr size_t fwd(int form) { return tab_bytes + (size_t)(PT + (form == 0 ? PT : 0)) * sizeof(T); }
+    static constexpr size_t bwd(int form) {
+        return tab_bytes + (size_t)(PT + PTH + (form == 1 ? PT : 0)) * sizeof(T);
     }
-    // backward: 2 stages of dy (-> dx) [+ one x, y (TDF) or u (DF) tile in phase 3]
-    static constexpr int bwd_xy(int form, int phase) { return phase == 3 ? PTH + (form == 1 ? PT : 0) : 0; }
-    static constexpr size_t bwd(int form, int phase) {
-        return tab_bytes + (size_t)(2 * PT + bwd_xy(form, phase)) * sizeof(T);
-    }
-};
-
-// Per-CTA coefficient state (tables staged in shared memory, coefficients in registers).
-template <typename T, int M>
-struct CoefRegs {
-    T bc[M + 1], ac[M + 1], cc[M];
 };
 
 // ---------------------------------------------------------------------------
-// Forward, phases 1 and 3 (a2-a4).  Persistent CTAs stride over the tiles
-// (tile = seq * ntiles + jt, TS samples each) and double-buffer them: tile k+1
-// streams into shared memory (cp.async) while tile k is scanned.
-//   PHASE 1: local pass, warp + block scans -> tile aggregate (no outputs).
-//   PHASE 3: the same scans again (x now comes from L2), plus the state
-//            entering the tile from phase 2 -> exact per-thread carry-in,
-//            re-run and emit y (and u for DF), zf.
-template <typename T, int M, int FORM, int PHASE>
+// Forward: a2-a4.  One CTA per tile of TS samples; tiles are taken in ticket
+// order (ticket t = tile t / B of sequence t % B), so every tile a CTA waits
+// for belongs to a CTA that is already running.
+template <typename T, int M, int FORM>
 __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
     constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
     using V = typename Vec<T>::type;
@@ -655,152 +573,128 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
     using SM = Smem<T, M>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* st = reinterpret_cast<double*>(smem_raw);
-    T* xb = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);     // 2 stages, x -> y in place
-    T* us = xb + 2 * SM::PT;                                      // DF: u tile (phase 3)
+    T* xs = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);     // x -> y in place
+    T* us = xs + SM::PT;                                          // DF: u tile
     __shared__ double s_agg[NW][M];
     __shared__ double s_xw[NW][M];
+    __shared__ unsigned s_ticket;
 
-    pdl_launch_dependents();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t ntot = p.B * (int64_t)p.ntiles;
-    int64_t tile = blockIdx.x;
-    if (tile < ntot) {
-        const int64_t sq = tile / p.ntiles;
-        tile_load_async<T, TS>(xb, static_cast<const T*>(p.x) + sq * p.Tlen, (tile - sq * p.ntiles) * TS,
-                               p.Tlen, p.vec);
-    }
+    if (tid == 0) s_ticket = atomicAdd(p.cw.ticket, 1u);
+    __syncthreads();
+    const unsigned tk = s_ticket;
+    const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
+    const int jt = (int)(tk / (unsigned long long)p.B);
+    const int64_t p0 = (int64_t)jt * TS;
+    const T* xrow = static_cast<const T*>(p.x) + seq * p.Tlen;
+    IIRG_TRACE(p.trace, tk, 0);
+    tile_load_async<T, TS>(xs, xrow, p0, p.Tlen, p.vec);
     cp_async_commit();
-    int64_t staged = -1;
-    bool waited = false;
-    T bc[M + 1], ac[M + 1], cc[M];
-    for (int it = 0; tile < ntot; ++it, tile += gridDim.x) {
-        const int64_t next = tile + gridDim.x;
-        if (next < ntot) {
-            const int64_t sq = next / p.ntiles;
-            tile_load_async<T, TS>(xb + ((it + 1) & 1) * SM::PT, static_cast<const T*>(p.x) + sq * p.Tlen,
-                                   (next - sq * p.ntiles) * TS, p.Tlen, p.vec);
-        }
-        cp_async_commit();
-        const int64_t seq = tile / p.ntiles;
-        const int jt = (int)(tile - seq * p.ntiles);
-        const int64_t p0 = (int64_t)jt * TS;
-        const double* tb = p.tab + seq * p.tab_stride;
-        T* xs = xb + (it & 1) * SM::PT;
-        const int64_t set = p.tab_stride == 0 ? 0 : seq;
-        if (set != staged) {
-            // previous grid: phase 1 waits for the prologue (tables), phase 3 for phase 2
-            if (!waited) { pdl_wait(); waited = true; }
-            stage_small<M>(st, tb);
-            load_coefs<T, M>(tb, bc, ac, cc);
-            staged = set;
-        }
-        IIRG_TRACE(p.trace, tile, 0);
-        cp_async_wait<1>();
-        __syncthreads();
+    T bc[M + 1], ac[M + 1];
+    raw_coefs<T, M>(static_cast<const T*>(p.b) + seq * p.coef_stride,
+                    static_cast<const T*>(p.a) + seq * p.coef_stride, bc, ac);
+    cp_async_wait<0>();
+    __syncthreads();
 
-        // a2: local pass from the zero state over this thread's chunk.
-        const int s0 = tid * L;
-        T v[M];
+    // a2: local pass from the zero state over this thread's chunk.
+    const int s0 = tid * L;
+    T v[M];
 #pragma unroll
-        for (int i = 0; i < M; ++i) v[i] = T(0);
+    for (int i = 0; i < M; ++i) v[i] = T(0);
 #pragma unroll
-        for (int g = 0; g < L / W; ++g) {
-            const V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
+    for (int g = 0; g < L / W; ++g) {
+        const V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
 #pragma unroll
-            for (int e = 0; e < W; ++e) { T du; fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, du); }
-        }
-        IIRG_TRACE(p.trace, tile, 1);
-        // a3: carries in fp64
-        double S[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) S[i] = (double)v[i];
-        if constexpr (PHASE == 1) {
-            tile_reduce<M, false>(tb, st, lane, warp, S, s_agg, p.agg + tile * M);
-            IIRG_TRACE(p.trace, tile, 2);
-        } else {
-            warp_scan<M, false>(st, lane, S);
-            if (lane == 31) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
-            }
-            __syncthreads();
-            double E[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
-            if (warp == 0) {
-                double Jex[M], G[M];
-                block_scan<M, false>(st, lane, s_agg, Jex, G);
-                if (lane < NW) {                           // state entering warp `lane`
-                    double X[M], xw[M];
-#pragma unroll
-                    for (int i = 0; i < M; ++i) { X[i] = p.carry[tile * M + i]; xw[i] = Jex[i]; }
-                    mv_acc_lane_s<M, false>(st + TB::PWT, NW, lane, X, xw);
-#pragma unroll
-                    for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
-                }
-            }
-            __syncthreads();
-            IIRG_TRACE(p.trace, tile, 2);
-            // state entering this thread's chunk: E + A_f^(L lane) x_warp
-            {
-                double xw[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
-                mv_acc_lane<M, false>(tb + TB::PLT, 32, lane, xw, E);
-            }
-            T vin[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) { vin[i] = (T)E[i]; v[i] = vin[i]; }
-            // zf = v(T): the thread holding sample T-1 walks its chunk up to it.
-            if (p.zf != nullptr) {
-                const int64_t eL = p.Tlen - 1 - p0;
-                if (eL >= s0 && eL < s0 + L) {
-                    T w2[M];
-#pragma unroll
-                    for (int i = 0; i < M; ++i) w2[i] = vin[i];
-                    for (int n = s0; n <= (int)eL; ++n) { T du; fwd_step<T, M, FORM>(w2, xs[pidx<T>(n)], bc, ac, du); }
-                    T* zf = static_cast<T*>(p.zf) + seq * M;
-#pragma unroll
-                    for (int i = 0; i < M; ++i) zf[i] = w2[i];
-                }
-            }
-            // a4: re-run from the exact carry-in, emit y (and u for DF) in place.
-#pragma unroll
-            for (int g = 0; g < L / W; ++g) {
-                V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
-                V uv;
-#pragma unroll
-                for (int e = 0; e < W; ++e) {
-                    T uu;
-                    const T yy = fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, uu);
-                    vset(xv, e, yy);
-                    vset(uv, e, uu);
-                }
-                *reinterpret_cast<V*>(xs + pidx<T>(s0 + g * W)) = xv;
-                if constexpr (FORM == 0) *reinterpret_cast<V*>(us + pidx<T>(s0 + g * W)) = uv;
-            }
-            __syncthreads();
-            IIRG_TRACE(p.trace, tile, 3);
-            T* yrow = static_cast<T*>(p.y) + seq * p.Tlen;
-            tile_store<T, TS>(yrow, xs, p0, p.Tlen, p.vec);
-            if constexpr (FORM == 0) {
-                T* urow = static_cast<T*>(p.u) + seq * p.Tlen;
-                tile_store<T, TS>(urow, us, p0, p.Tlen, p.vec);
-            }
-        }
-        __syncthreads();                                  // this stage may be refilled
+        for (int e = 0; e < W; ++e) { T du; fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, du); }
     }
-    if (!waited) pdl_wait();
+    IIRG_TRACE(p.trace, tk, 1);
+    // a3: carries in fp64; the power tables come from the prologue (PDL).
+    pdl_wait();
+    const double* tb = p.tab + seq * p.tab_stride;
+    stage_small<M>(st, tb);
+    __syncthreads();
+    double S[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) S[i] = (double)v[i];
+    warp_scan<M, false>(st, lane, S);
+    double E[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
+    if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double Jex[M], G[M], X0[M], X[M];
+        block_scan<M, false>(st, lane, s_agg, Jex, G);
+        const T* zi = static_cast<const T*>(p.zi);
+#pragma unroll
+        for (int i = 0; i < M; ++i) X0[i] = (zi != nullptr && jt == 0) ? (double)zi[seq * M + i] : 0.0;
+        IIRG_TRACE(p.trace, tk, 2);
+        tile_carry<M, false>(tb, lane, jt, seq, X0, G, p.cw, X);
+        IIRG_TRACE(p.trace, tk, 3);
+        if (lane < NW) {                           // state entering warp `lane`
+            double xw[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) xw[i] = Jex[i];
+            mv_acc_lane_s<M, false>(st + TB::PWT, NW, lane, X, xw);
+#pragma unroll
+            for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
+        }
+    }
+    __syncthreads();
+    // state entering this thread's chunk: E + A_f^(L lane) x_warp
+    {
+        double xw[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
+        mv_acc_lane<M, false>(tb + TB::PLT, 32, lane, xw, E);
+    }
+    T vin[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) { vin[i] = (T)E[i]; v[i] = vin[i]; }
+    // zf = v(T): the thread holding sample T-1 walks its chunk up to it (before
+    // the emit pass overwrites x with y).
+    if (p.zf != nullptr) {
+        const int64_t eL = p.Tlen - 1 - p0;
+        if (eL >= s0 && eL < s0 + L) {
+            T w2[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) w2[i] = vin[i];
+            for (int n = s0; n <= (int)eL; ++n) { T du; fwd_step<T, M, FORM>(w2, xs[pidx<T>(n)], bc, ac, du); }
+            T* zf = static_cast<T*>(p.zf) + seq * M;
+#pragma unroll
+            for (int i = 0; i < M; ++i) zf[i] = w2[i];
+        }
+    }
+    // a4: re-run from the exact carry-in, emit y (and u for DF) in place.
+#pragma unroll
+    for (int g = 0; g < L / W; ++g) {
+        V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
+        V uv;
+#pragma unroll
+        for (int e = 0; e < W; ++e) {
+            T uu;
+            const T yy = fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, uu);
+            vset(xv, e, yy);
+            vset(uv, e, uu);
+        }
+        *reinterpret_cast<V*>(xs + pidx<T>(s0 + g * W)) = xv;
+        if constexpr (FORM == 0) *reinterpret_cast<V*>(us + pidx<T>(s0 + g * W)) = uv;
+    }
+    __syncthreads();
+    IIRG_TRACE(p.trace, tk, 4);
+    T* yrow = static_cast<T*>(p.y) + seq * p.Tlen;
+    tile_store<T, TS>(yrow, xs, p0, p.Tlen, p.vec);
+    if constexpr (FORM == 0) {
+        T* urow = static_cast<T*>(p.u) + seq * p.Tlen;
+        tile_store<T, TS>(urow, us, p0, p.Tlen, p.vec);
+    }
+    IIRG_TRACE(p.trace, tk, 5);
+    cta_exit<M>(p.cw, p.B, gridDim.x);
 }
 
-// ---------------------------------------------------------------------------
-// Backward, phases 1 and 3 (a5-a8).  Tiles are aligned to the END of each
-// sequence; scan index jr = 0 is the last tile in time; inside a tile thread t
-// owns chunk NT-1-t, walked backwards.  Persistent, double-buffered like the
-// forward kernel.
-//   PHASE 1: local adjoint pass over dy, warp + block scans -> tile aggregate.
-//   PHASE 3: dy again (from L2) plus x, y (TDF) or u (DF): carry-in from phase
-//            2, re-run, emit dx and grad_zi, coefficient partial sums, fused a8.
 template <typename T, int M, int FORM>
 __device__ __forceinline__ void bwd_load_u(const LtiBwdArgs& p, int64_t seq, int64_t p0, T* s2) {
     constexpr int TS = NT * Chunk<T>::L, W = Vec<T>::W;
@@ -828,31 +722,11 @@ __device__ __forceinline__ void bwd_load_u(const LtiBwdArgs& p, int64_t seq, int
     }
 }
 
-template <typename T>
-__device__ __forceinline__ void bwd_issue_dy(const LtiBwdArgs& p, int64_t tile, T* dys) {
-    constexpr int TS = NT * Chunk<T>::L;
-    const int64_t seq = tile / p.ntiles;
-    const int jr = (int)(tile - seq * p.ntiles);
-    const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;
-    if (p.gy != nullptr) tile_load_async<T, TS>(dys, static_cast<const T*>(p.gy) + seq * p.Tlen, p0, p.Tlen, p.vec);
-    else for (int e = threadIdx.x; e < TS; e += NT) dys[pidx<T>(e)] = T(0);
-}
+// ---------------------------------------------------------------------------
+// Backward: a5-a8.  Tiles are aligned to the END of each sequence and taken in
+// ticket order last to first; inside a tile thread t owns chunk NT-1-t, walked
+// backwards.  TDF: smem dy | x | y.  DF: smem dy | u (with HALO samples of history).
 template <typename T, int M, int FORM>
-__device__ __forceinline__ void bwd_issue_xy(const LtiBwdArgs& p, int64_t tile, T* s2, T* s3) {
-    constexpr int TS = NT * Chunk<T>::L;
-    const int64_t seq = tile / p.ntiles;
-    const int jr = (int)(tile - seq * p.ntiles);
-    const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;
-    const int64_t roff = seq * p.Tlen;
-    if constexpr (FORM == 1) {
-        tile_load_async<T, TS>(s2, static_cast<const T*>(p.x) + roff, p0, p.Tlen, p.vec);
-        tile_load_async<T, TS>(s3, static_cast<const T*>(p.y) + roff, p0, p.Tlen, p.vec);
-    } else {
-        bwd_load_u<T, M, FORM>(p, seq, p0, s2);
-    }
-}
-
-template <typename T, int M, int FORM, int PHASE>
 __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
     constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
     constexpr int NG = 2 * M + 1;                       // gradient partial sums
@@ -861,234 +735,228 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
     using SM = Smem<T, M>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* st = reinterpret_cast<double*>(smem_raw);
-    T* sb = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);    // 2 stages of dy -> dx
-    T* s2 = sb + 2 * SM::PT;                                   // TDF: x        DF: u (+HALO)
+    T* dys = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);   // dy -> dx in place
+    T* s2 = dys + SM::PT;                                      // TDF: x        DF: u (+HALO)
     T* s3 = s2 + SM::PTH;                                      // TDF: y
     __shared__ double s_agg[NW][M];
     __shared__ double s_xw[NW][M];
     __shared__ double s_red[NW][NG];
     __shared__ double s_G[NG];
-    __shared__ unsigned s_fin;
+    __shared__ unsigned s_ticket, s_fin;
 
-    pdl_launch_dependents();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t ntot = p.B * (int64_t)p.ntiles;
-    int64_t tile = blockIdx.x;
-    if (tile < ntot) bwd_issue_dy<T>(p, tile, sb);
-    cp_async_commit();
-    int64_t staged = -1;
-    bool waited = false;
-    T bc[M + 1], ac[M + 1], cc[M];
-    for (int it = 0; tile < ntot; ++it, tile += gridDim.x) {
-        const int64_t next = tile + gridDim.x;
-        // groups in flight: dy(this) [earlier], x/y(this), dy(next)
-        if constexpr (PHASE == 3) bwd_issue_xy<T, M, FORM>(p, tile, s2, s3);
-        cp_async_commit();
-        if (next < ntot) bwd_issue_dy<T>(p, next, sb + ((it + 1) & 1) * SM::PT);
-        cp_async_commit();
-        const int64_t seq = tile / p.ntiles;
-        const int jr = (int)(tile - seq * p.ntiles);                 // 0 = last tile in time
-        const int jt = p.ntiles - 1 - jr;                            // time index of the tile
-        const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;          // may be < 0 (first tile)
-        const double* tb = p.tab + seq * p.tab_stride;
-        const int64_t roff = seq * p.Tlen;
-        T* dys = sb + (it & 1) * SM::PT;
-        const int64_t set = p.tab_stride == 0 ? 0 : seq;
-        if (set != staged) {                   // tables live in the tape (written by the forward)
-            stage_small<M>(st, tb);
-            load_coefs<T, M>(tb, bc, ac, cc);
-            staged = set;
-        }
-        IIRG_TRACE(p.trace, tile, 0);
-        cp_async_wait<2>();                                          // dy of this tile
-        __syncthreads();
+    if (tid == 0) s_ticket = atomicAdd(p.cw.ticket, 1u);
+    __syncthreads();
+    const unsigned tk = s_ticket;
+    const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
+    const int jr = (int)(tk / (unsigned long long)p.B);          // 0 = last tile in time
+    const int jt = p.ntiles - 1 - jr;                            // time index of the tile
+    const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;          // may be < 0 (first tile)
+    const double* tb = p.tab + seq * p.tab_stride;
+    const int64_t roff = seq * p.Tlen;
+    IIRG_TRACE(p.trace, tk, 0);
 
-        const int c = NT - 1 - tid;          // chunk index within the tile (time order)
-        const int s0 = c * L;
-        // a5: local adjoint pass from the zero state, walking the chunk backwards.
-        T d[M];
+    // group 0: dy;  group 1: x, y (TDF) or u (DF)
+    if (p.gy != nullptr) tile_load_async<T, TS>(dys, static_cast<const T*>(p.gy) + roff, p0, p.Tlen, p.vec);
+    else for (int e = tid; e < TS; e += NT) dys[pidx<T>(e)] = T(0);
+    cp_async_commit();
+    if constexpr (FORM == 1) {
+        tile_load_async<T, TS>(s2, static_cast<const T*>(p.x) + roff, p0, p.Tlen, p.vec);
+        tile_load_async<T, TS>(s3, static_cast<const T*>(p.y) + roff, p0, p.Tlen, p.vec);
+    } else {
+        bwd_load_u<T, M, FORM>(p, seq, p0, s2);
+    }
+    cp_async_commit();
+    stage_small<M>(st, tb);                          // tables live in the tape (written by the forward)
+    T bc[M + 1], ac[M + 1], cc[M];
+    load_coefs<T, M>(tb, bc, ac, cc);
+    cp_async_wait<1>();                              // dy
+    __syncthreads();
+
+    const int c = NT - 1 - tid;          // chunk index within the tile (time order)
+    const int s0 = c * L;
+    // a5: local adjoint pass from the zero state, walking the chunk backwards.
+    T d[M];
 #pragma unroll
-        for (int i = 0; i < M; ++i) d[i] = T(0);
+    for (int i = 0; i < M; ++i) d[i] = T(0);
 #pragma unroll
-        for (int g = L / W - 1; g >= 0; --g) {
-            const V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
+    for (int g = L / W - 1; g >= 0; --g) {
+        const V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
+#pragma unroll
+        for (int e = W - 1; e >= 0; --e) {
+            if constexpr (FORM == 1) adj_tdf_step<T, M>(d, vget(dv, e), ac);
+            else adj_df_step<T, M>(d, vget(dv, e), bc, ac);
+        }
+    }
+    IIRG_TRACE(p.trace, tk, 1);
+    // a6: carries (transposed powers), tiles last -> first.
+    double S[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) S[i] = (double)d[i];
+    warp_scan<M, true>(st, lane, S);
+    double E[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
+    if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double Jex[M], G[M], X0[M], X[M];
+        block_scan<M, true>(st, lane, s_agg, Jex, G);
+        const T* gzf = static_cast<const T*>(p.gzf);
+#pragma unroll
+        for (int i = 0; i < M; ++i) X0[i] = (gzf != nullptr && jr == 0) ? (double)gzf[seq * M + i] : 0.0;
+        IIRG_TRACE(p.trace, tk, 2);
+        tile_carry<M, true>(tb, lane, jr, seq, X0, G, p.cw, X);
+        IIRG_TRACE(p.trace, tk, 3);
+        if (lane < NW) {
+            double xw[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) xw[i] = Jex[i];
+            mv_acc_lane_s<M, true>(st + TB::PWT, NW, lane, X, xw);
+#pragma unroll
+            for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
+        }
+    }
+    __syncthreads();
+    {
+        double xw[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
+        mv_acc_lane<M, true>(tb + TB::PLT, 32, lane, xw, E);
+    }
+    T din[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) { din[i] = (T)E[i]; d[i] = din[i]; }
+    cp_async_wait<0>();                              // x, y / u
+    __syncthreads();
+
+    // grad_zi = dz(-1) (Eq.9, A.3): the thread whose chunk holds n = 0 walks down
+    // to it before the emit pass overwrites dy with dx.
+    if (p.gzi != nullptr && p0 + s0 <= 0 && p0 + s0 + L > 0) {
+        T w2[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) w2[i] = din[i];
+        for (int n = s0 + L - 1; n >= (int)(-p0); --n) {
+            const T dy = dys[pidx<T>(n)];
+            if constexpr (FORM == 1) adj_tdf_step<T, M>(w2, dy, ac);
+            else (void)adj_df_step<T, M>(w2, dy, bc, ac);
+        }
+        T* gzi = static_cast<T*>(p.gzi) + seq * M;
+#pragma unroll
+        for (int i = 0; i < M; ++i) gzi[i] = w2[i];
+    }
+    // a7: re-run with the exact carry, emit dx, accumulate the coefficient sums.
+    T Gs[NG];
+#pragma unroll
+    for (int k = 0; k < NG; ++k) Gs[k] = T(0);
+    const bool has_neg = (p0 + s0) < 0;                 // chunk reaches before n = 0
+#pragma unroll
+    for (int g = L / W - 1; g >= 0; --g) {
+        V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
+        if constexpr (FORM == 1) {
+            const V xv = *reinterpret_cast<const V*>(s2 + pidx<T>(s0 + g * W));
+            const V yv = *reinterpret_cast<const V*>(s3 + pidx<T>(s0 + g * W));
 #pragma unroll
             for (int e = W - 1; e >= 0; --e) {
-                if constexpr (FORM == 1) adj_tdf_step<T, M>(d, vget(dv, e), ac);
-                else adj_df_step<T, M>(d, vget(dv, e), bc, ac);
+                const T dy = vget(dv, e), xx = vget(xv, e), yy = vget(yv, e);
+                T dx = bc[0] * dy;
+#pragma unroll
+                for (int i = 0; i < M; ++i) dx = fma(cc[i], d[i], dx);     // Eq.8: c^T dz + b0 dy
+#pragma unroll
+                for (int i = 0; i < M; ++i) { Gs[i] = fma(d[i], xx, Gs[i]); Gs[M + i] = fma(d[i], yy, Gs[M + i]); }
+                Gs[2 * M] = fma(dy, xx, Gs[2 * M]);
+                vset(dv, e, dx);
+                adj_tdf_step<T, M>(d, dy, ac);
+            }
+        } else {
+#pragma unroll
+            for (int e = W - 1; e >= 0; --e) {
+                const int n = s0 + g * W + e;                 // tile-local time index
+                const T dy = vget(dv, e);
+                const T dx = adj_df_step<T, M>(d, dy, bc, ac); // dx(n), then d <- dz(n-1)
+                const T gmask = (!has_neg || p0 + n >= 0) ? dx : T(0);
+#pragma unroll
+                for (int k = 0; k <= M; ++k) {
+                    const T uk = s2[pidx<T>(n - k + HALO)];
+                    Gs[k] = fma(dy, uk, Gs[k]);                          // Gb[k] = sum dy u(n-k)
+                    if (k >= 1) Gs[M + k] = fma(gmask, uk, Gs[M + k]);  // Ga[k] = sum dx u(n-k)
+                }
+                vset(dv, e, dx);
             }
         }
-        IIRG_TRACE(p.trace, tile, 1);
-        // a6: carries (transposed powers)
-        double S[M];
+        *reinterpret_cast<V*>(dys + pidx<T>(s0 + g * W)) = dv;   // dx in place
+    }
+    // warp reduction of the partial sums (fp64, fixed order)
+    if (p.want_coef) {
 #pragma unroll
-        for (int i = 0; i < M; ++i) S[i] = (double)d[i];
-        if constexpr (PHASE == 1) {
-            tile_reduce<M, true>(tb, st, lane, warp, S, s_agg, p.agg + tile * M);
-            IIRG_TRACE(p.trace, tile, 2);
-        } else {
-            warp_scan<M, true>(st, lane, S);
-            if (lane == 31) {
+        for (int k = 0; k < NG; ++k) {
+            double s = (double)Gs[k];
 #pragma unroll
-                for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
-            }
-            __syncthreads();
-            double E[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
-            if (!waited) { pdl_wait(); waited = true; }          // tile carries of phase 2
-            if (warp == 0) {
-                double Jex[M], G[M];
-                block_scan<M, true>(st, lane, s_agg, Jex, G);
-                if (lane < NW) {                                 // state entering warp `lane`
-                    double X[M], xw[M];
-#pragma unroll
-                    for (int i = 0; i < M; ++i) { X[i] = p.carry[tile * M + i]; xw[i] = Jex[i]; }
-                    mv_acc_lane_s<M, true>(st + TB::PWT, NW, lane, X, xw);
-#pragma unroll
-                    for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
-                }
-            }
-            __syncthreads();
-            IIRG_TRACE(p.trace, tile, 2);
-            {
-                double xw[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
-                mv_acc_lane<M, true>(tb + TB::PLT, 32, lane, xw, E);
-            }
-            T din[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) { din[i] = (T)E[i]; d[i] = din[i]; }
-            cp_async_wait<1>();                                      // x, y / u of this tile
-            __syncthreads();
+            for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) s_red[warp][k] = s;
+        }
+    }
+    __syncthreads();
+    IIRG_TRACE(p.trace, tk, 4);
+    if (p.gx != nullptr) tile_store<T, TS>(static_cast<T*>(p.gx) + roff, dys, p0, p.Tlen, p.vec);
+    IIRG_TRACE(p.trace, tk, 5);
 
-            // grad_zi = dz(-1) (Eq.9, A.3): the thread whose chunk holds n = 0 walks down
-            // to it before the emit pass overwrites dy with dx.
-            if (p.gzi != nullptr && p0 + s0 <= 0 && p0 + s0 + L > 0) {
-                T w2[M];
+    if (p.want_coef) {
+        // fused a8: group of 32 tiles -> group sum; last group of the set -> chain rule.
+        const bool shared = p.ncoef == 1;
+        const int64_t per_set = shared ? p.B * p.ntiles : p.ntiles;
+        const int64_t cset = shared ? 0 : seq;
+        const int64_t li = shared ? seq * p.ntiles + jt : jt;          // index within the set
+        const int64_t gi = li >> 5;
+        const int64_t ngroups = (per_set + 31) >> 5;
+        const int gsize = (int)min((int64_t)32, per_set - (gi << 5));
+        double* part = p.partial + cset * per_set * NG;
+        double* part2 = p.partial2 + cset * ngroups * NG;
+        if (tid < NG) {
+            double s = 0.0;
 #pragma unroll
-                for (int i = 0; i < M; ++i) w2[i] = din[i];
-                for (int n = s0 + L - 1; n >= (int)(-p0); --n) {
-                    const T dy = dys[pidx<T>(n)];
-                    if constexpr (FORM == 1) adj_tdf_step<T, M>(w2, dy, ac);
-                    else (void)adj_df_step<T, M>(w2, dy, bc, ac);
-                }
-                T* gzi = static_cast<T*>(p.gzi) + seq * M;
-#pragma unroll
-                for (int i = 0; i < M; ++i) gzi[i] = w2[i];
-            }
-            // a7: re-run with the exact carry, emit dx, accumulate the coefficient sums.
-            T Gs[NG];
-#pragma unroll
-            for (int k = 0; k < NG; ++k) Gs[k] = T(0);
-            const bool has_neg = (p0 + s0) < 0;                 // chunk reaches before n = 0
-#pragma unroll
-            for (int g = L / W - 1; g >= 0; --g) {
-                V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
-                if constexpr (FORM == 1) {
-                    const V xv = *reinterpret_cast<const V*>(s2 + pidx<T>(s0 + g * W));
-                    const V yv = *reinterpret_cast<const V*>(s3 + pidx<T>(s0 + g * W));
-#pragma unroll
-                    for (int e = W - 1; e >= 0; --e) {
-                        const T dy = vget(dv, e), xx = vget(xv, e), yy = vget(yv, e);
-                        T dx = bc[0] * dy;
-#pragma unroll
-                        for (int i = 0; i < M; ++i) dx = fma(cc[i], d[i], dx);     // Eq.8: c^T dz + b0 dy
-#pragma unroll
-                        for (int i = 0; i < M; ++i) { Gs[i] = fma(d[i], xx, Gs[i]); Gs[M + i] = fma(d[i], yy, Gs[M + i]); }
-                        Gs[2 * M] = fma(dy, xx, Gs[2 * M]);
-                        vset(dv, e, dx);
-                        adj_tdf_step<T, M>(d, dy, ac);
-                    }
-                } else {
-#pragma unroll
-                    for (int e = W - 1; e >= 0; --e) {
-                        const int n = s0 + g * W + e;                 // tile-local time index
-                        const T dy = vget(dv, e);
-                        const T dx = adj_df_step<T, M>(d, dy, bc, ac); // dx(n), then d <- dz(n-1)
-                        const T gmask = (!has_neg || p0 + n >= 0) ? dx : T(0);
-#pragma unroll
-                        for (int k = 0; k <= M; ++k) {
-                            const T uk = s2[pidx<T>(n - k + HALO)];
-                            Gs[k] = fma(dy, uk, Gs[k]);                          // Gb[k] = sum dy u(n-k)
-                            if (k >= 1) Gs[M + k] = fma(gmask, uk, Gs[M + k]);  // Ga[k] = sum dx u(n-k)
-                        }
-                        vset(dv, e, dx);
-                    }
-                }
-                *reinterpret_cast<V*>(dys + pidx<T>(s0 + g * W)) = dv;   // dx in place
-            }
-            // warp reduction of the partial sums (fp64, fixed order)
-            if (p.want_coef) {
-#pragma unroll
-                for (int k = 0; k < NG; ++k) {
-                    double s = (double)Gs[k];
-#pragma unroll
-                    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-                    if (lane == 0) s_red[warp][k] = s;
-                }
+            for (int w = 0; w < NW; ++w) s += s_red[w][tid];
+            __stcg(part + li * NG + tid, s);
+            __threadfence();
+        }
+        __syncthreads();
+        if (tid == 0) s_fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
+        __syncthreads();
+        if (s_fin) {                                   // last tile of its group
+            __threadfence();
+            if (tid < NG) {
+                double s = 0.0;
+                for (int t = 0; t < gsize; ++t) s += __ldcg(part + ((gi << 5) + t) * NG + tid);
+                __stcg(part2 + gi * NG + tid, s);
+                __threadfence();
             }
             __syncthreads();
-            IIRG_TRACE(p.trace, tile, 3);
-            if (p.gx != nullptr) tile_store<T, TS>(static_cast<T*>(p.gx) + roff, dys, p0, p.Tlen, p.vec);
-
-            if (p.want_coef) {
-                // fused a8: group of 32 tiles -> group sum; last group of the set -> chain rule.
-                const bool shared = p.ncoef == 1;
-                const int64_t per_set = shared ? p.B * p.ntiles : p.ntiles;
-                const int64_t cset = shared ? 0 : seq;
-                const int64_t li = shared ? seq * p.ntiles + jt : jt;          // index within the set
-                const int64_t gi = li >> 5;
-                const int64_t ngroups = (per_set + 31) >> 5;
-                const int gsize = (int)min((int64_t)32, per_set - (gi << 5));
-                double* part = p.partial + cset * per_set * NG;
-                double* part2 = p.partial2 + cset * ngroups * NG;
+            if (tid == 0) {
+                p.gcnt[cset * ngroups + gi] = 0u;
+                s_fin = (atomicAdd(p.scnt + cset, 1u) == (unsigned)ngroups - 1u) ? 2u : 0u;
+            }
+            __syncthreads();
+            if (s_fin == 2u) {                          // last group of the set
+                __threadfence();
                 if (tid < NG) {
                     double s = 0.0;
-#pragma unroll
-                    for (int w = 0; w < NW; ++w) s += s_red[w][tid];
-                    __stcg(part + li * NG + tid, s);
-                    __threadfence();
+                    for (int64_t g2 = 0; g2 < ngroups; ++g2) s += __ldcg(part2 + g2 * NG + tid);
+                    s_G[tid] = s;
                 }
                 __syncthreads();
-                if (tid == 0) s_fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
-                __syncthreads();
-                if (s_fin) {                                   // last tile of its group
-                    __threadfence();
-                    if (tid < NG) {
-                        double s = 0.0;
-                        for (int t = 0; t < gsize; ++t) s += __ldcg(part + ((gi << 5) + t) * NG + tid);
-                        __stcg(part2 + gi * NG + tid, s);
-                        __threadfence();
-                    }
-                    __syncthreads();
-                    if (tid == 0) {
-                        p.gcnt[cset * ngroups + gi] = 0u;
-                        s_fin = (atomicAdd(p.scnt + cset, 1u) == (unsigned)ngroups - 1u) ? 2u : 0u;
-                    }
-                    __syncthreads();
-                    if (s_fin == 2u) {                          // last group of the set
-                        __threadfence();
-                        if (tid < NG) {
-                            double s = 0.0;
-                            for (int64_t g2 = 0; g2 < ngroups; ++g2) s += __ldcg(part2 + g2 * NG + tid);
-                            s_G[tid] = s;
-                        }
-                        __syncthreads();
-                        if (tid == 0) {
-                            chain_rule<T, M, FORM>(s_G, tb,
-                                                   p.gb == nullptr ? nullptr : static_cast<T*>(p.gb) + cset * (M + 1),
-                                                   p.ga == nullptr ? nullptr : static_cast<T*>(p.ga) + cset * (M + 1));
-                            p.scnt[cset] = 0u;
-                        }
-                    }
+                if (tid == 0) {
+                    chain_rule<T, M, FORM>(s_G, tb,
+                                           p.gb == nullptr ? nullptr : static_cast<T*>(p.gb) + cset * (M + 1),
+                                           p.ga == nullptr ? nullptr : static_cast<T*>(p.ga) + cset * (M + 1));
+                    p.scnt[cset] = 0u;
                 }
             }
         }
-        __syncthreads();                                  // this stage may be refilled
     }
-    if (!waited) pdl_wait();
+    cta_exit<M>(p.cw, p.B, gridDim.x);
 }
 
 }  // namespace iirg

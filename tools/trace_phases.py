@@ -15,8 +15,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2511_14390_b200 import _binding as B  # noqa: E402
 
-PH_F = ["start", "local", "wait", "carry", "emit", "store", "-", "-"]
-PH_B = ["start", "local", "wait", "xy", "emit", "store", "-", "-"]
+PH_F = ["start", "local", "scan", "carry", "emit", "store", "-", "-"]
+PH_B = ["start", "local", "scan", "carry", "emit", "store", "-", "-"]
 
 
 def main():
@@ -51,13 +51,11 @@ def main():
         torch.cuda.synchronize()
         B.iir_debug_trace(None)
         t = buf.view(ntot, 8).cpu().numpy().astype(np.float64)
-        if kern == 'bwd':
-            t[:, 2] = t[:, 1]
         t0 = t[:, 0].min()
         rel = (t - t0) / 1e3
         names = PH_F if kern == "fwd" else PH_B
         print(f"== {kern} ({ntot} tiles), us relative to first tile start; columns p0 p10 p50 p90 p100")
-        for k, nm in enumerate(names):
+        for k, nm in enumerate(names[:6]):
             col = rel[:, k]
             col = col[t[:, k] > 0]
             if nm == "-" or col.size == 0:
@@ -66,7 +64,7 @@ def main():
             print(f"   {nm:8s} " + " ".join(f"{v:8.2f}" for v in q))
         d = np.diff(rel, axis=1)
         print("   phase durations (median us): " + ", ".join(
-            f"{names[k]}->{names[k + 1]} {np.median(d[:, k]):.2f}" for k in range(7)))
+            f"{names[k]}->{names[k + 1]} {np.median(d[:, k]):.2f}" for k in range(5)))
 
 
 if __name__ == "__main__":
