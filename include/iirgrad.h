@@ -81,7 +81,7 @@ typedef void *iir_stream_t;  /* a cudaStream_t */
 typedef struct {
     int64_t batch;      /* B >= 1                                                  */
     int64_t length;     /* T >= 1 samples per sequence                             */
-    int32_t order;      /* M: 1..8 (SHARED / PER_SEQ), 1..32 (PER_SAMPLE)          */
+    int32_t order;      /* M: 1..8 (SHARED / PER_SEQ); PER_SAMPLE: 1-8,10,12,16,20,24,28,31 */
     int32_t form;       /* iir_form_t                                              */
     int32_t dtype;      /* iir_dtype_t                                             */
     int32_t coef_mode;  /* iir_coef_mode_t                                         */

@@ -9,7 +9,7 @@ __all__ = ["lfilter", "iir_forward", "iir_backward"]
 
 
 def __getattr__(name):
-    if name in ("lfilter", "LFilterFunction", "allpole_tv"):
+    if name in ("lfilter", "LFilterFunction", "allpole_tv", "AllPoleTVFunction"):
         from . import autograd
         return getattr(autograd, name)
     if name in ("iir_forward", "iir_backward", "Desc", "lib"):

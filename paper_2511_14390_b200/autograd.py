@@ -75,3 +75,46 @@ def lfilter(x, b, a, zi=None, form="tdf", return_zf=False):
     if squeeze:
         y, zf = y[0], zf[0]
     return (y, zf) if return_zf else y
+
+
+class AllPoleTVFunction(torch.autograd.Function):
+    """y, zf = per-sample all-pole DF filter:
+    y(n) = x(n) - sum_i a[.., n, i-1] y(n-i);  zi = [y(-1) .. y(-M)]."""
+
+    @staticmethod
+    def forward(ctx, x, a, zi):
+        _require_cuda(x, a, zi)
+        x, a, zi = _c(x), _c(a), _c(zi)
+        Bsz, T = x.shape
+        M = a.shape[-1]
+        desc = B.make_desc(Bsz, T, M, "df", x.dtype, B.IIR_COEF_PER_SAMPLE)
+        y = torch.empty_like(x)
+        zf = torch.empty((Bsz, M), dtype=x.dtype, device=x.device)
+        tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
+        tape = torch.empty(tb, dtype=torch.uint8, device=x.device)
+        ws = torch.empty(wb, dtype=torch.uint8, device=x.device)
+        B.iir_forward(desc, None, a, x, zi, y, zf, tape, tb, ws, wb)
+        ctx.desc = desc
+        ctx.has_zi = zi is not None
+        ctx.save_for_backward(a, zi if zi is not None else torch.empty(0, device=x.device), y, tape)
+        return y, zf
+
+    @staticmethod
+    def backward(ctx, gy, gzf):
+        a, zi, y, tape = ctx.saved_tensors
+        zi = zi if ctx.has_zi else None
+        desc = ctx.desc
+        gx = torch.empty_like(y) if ctx.needs_input_grad[0] else None
+        ga = torch.empty_like(a) if ctx.needs_input_grad[1] else None
+        gzi = torch.empty_like(zi) if (zi is not None and ctx.needs_input_grad[2]) else None
+        wb = B.iir_workspace_bytes(desc)
+        ws = torch.empty(wb, dtype=torch.uint8, device=y.device)
+        B.iir_backward(desc, _c(gy), _c(gzf), None, a, None, y, zi, tape, tape.numel(), gx, None, ga, gzi, ws, wb)
+        return gx, ga, gzi
+
+
+def allpole_tv(x, a, zi=None, return_zf=False):
+    """Differentiable per-sample all-pole filter: x (B, T), a (B, T, M) with
+    a[b, n, i-1] = a_i(n) (monic, a_0 = 1 implied), zi (B, M) = past outputs."""
+    y, zf = AllPoleTVFunction.apply(x, a, zi)
+    return (y, zf) if return_zf else y

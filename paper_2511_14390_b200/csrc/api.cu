@@ -26,7 +26,8 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
 }  // namespace iirg
 
 // ------------------------------------------------------- instrumentation ----
-static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_fwd", "tv_bwd", "tv_fix"};
+static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_phi", "tv_chain", "tv_fwd",
+                                        "tv_bwd_agg", "tv_bwd"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;
@@ -84,7 +85,7 @@ static iir_status_t check_desc(const iir_desc_t* d) {
     if (d->form != IIR_DF2 && d->form != IIR_TDF2) return fail(IIR_EINVAL, "form must be IIR_DF2 or IIR_TDF2");
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) {
         if (d->form != IIR_DF2) return fail(IIR_EUNSUPPORTED, "per-sample coefficients: only the all-pole DF form");
-        if (d->order < 1 || d->order > TV_MAX_M) return fail(IIR_EUNSUPPORTED, "per-sample order must be 1..32");
+        if (d->order < 1 || d->order > TV_MAX_M) return fail(IIR_EUNSUPPORTED, "per-sample order must be 1..31");
         if (!tv_supported(d->order)) return fail(IIR_EUNSUPPORTED, "per-sample order not compiled in");
         return IIR_OK;
     }

@@ -13,7 +13,7 @@ namespace iirg {
 
 iir_status_t fail(iir_status_t st, const std::string& msg);
 
-enum Kind { K_LTI_PREP = 0, K_LTI_FWD, K_LTI_BWD, K_TV_FWD, K_TV_BWD, K_TV_FIX, K_NUM };
+enum Kind { K_LTI_PREP = 0, K_LTI_FWD, K_LTI_BWD, K_TV_PHI, K_TV_CHAIN, K_TV_FWD, K_TV_BWD_AGG, K_TV_BWD, K_NUM };
 
 // Launch bookkeeping: counts every kernel and (when profiling is on) brackets it
 // with CUDA events on its stream.
@@ -45,7 +45,7 @@ struct Layout {
 };
 
 // per-sample (time-varying all-pole) path, tv.cu
-constexpr int TV_MAX_M = 32;
+constexpr int TV_MAX_M = 31;
 bool tv_supported(int M);
 Layout tv_layout(const iir_desc_t* d);
 iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* a, const void* x, const void* zi, void* y,

@@ -1,16 +1,101 @@
-// tv.cu -- per-sample (time-varying) all-pole DF path.  Stub
-// until the kernels land: reports IIR_EUNSUPPORTED.
+// tv.cu -- host side of the per-sample (time-varying) all-pole DF path
+// (IIR_COEF_PER_SAMPLE): layout, dispatch, instantiations.
 #include "host.h"
+#include "tv.cuh"
 
 namespace iirg {
-bool tv_supported(int) { return false; }
-Layout tv_layout(const iir_desc_t*) { return Layout{}; }
-iir_status_t tv_forward(const iir_desc_t*, const Layout&, const void*, const void*, const void*, void*, void*, char*,
-                        char*, bool, cudaStream_t) {
-    return fail(IIR_EUNSUPPORTED, "per-sample path not built");
+
+#define IIRG_TV_ORDERS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(10) X(12) X(16) X(20) X(24) X(28) X(31)
+
+bool tv_supported(int M) {
+    switch (M) {
+#define IIRG_CASE(m) case m: return true;
+        IIRG_TV_ORDERS(IIRG_CASE)
+#undef IIRG_CASE
+    }
+    return false;
 }
-iir_status_t tv_backward(const iir_desc_t*, const Layout&, const void*, const void*, const void*, const void*,
-                         const void*, const char*, void*, void*, void*, char*, bool, cudaStream_t) {
-    return fail(IIR_EUNSUPPORTED, "per-sample path not built");
+
+Layout tv_layout(const iir_desc_t* d) {
+    Layout L;
+    const int M = d->order;
+    const size_t ts = d->dtype == IIR_F64 ? 8 : 4;
+    L.ntiles = (d->length + TV_SEG - 1) / TV_SEG;          // segments per sequence
+    L.ntot = L.ntiles * d->batch;
+    L.ncoef = d->batch;
+    size_t o = 0;
+    L.ws_clear = 0;                                        // no counters: nothing to initialise
+    L.ws_part = o; o += al256((size_t)L.ntot * M * 8);     // w: segment aggregates
+    L.ws_part2 = o; o += al256((size_t)L.ntot * M * 8);    // carry: entering states
+    L.ws_bytes = o;
+    L.tp_tab = 0;
+    L.tp_bytes = al256((size_t)L.ntot * M * M * ts);       // Phi_k per segment (reused by the backward)
+    L.tp_u = L.tp_bytes;
+    return L;
 }
+
+template <typename T, int M>
+static iir_status_t tv_fwd_m(const Layout& L, TvArgs& a, cudaStream_t st) {
+    const unsigned nseg_tot = (unsigned)L.ntot;
+    iir_status_t s = launch(K_TV_PHI, st, [&] {
+        tv_phi_kernel<T, M><<<(nseg_tot + TV_PHI_WARPS - 1) / TV_PHI_WARPS, 32 * TV_PHI_WARPS, 0, st>>>(a);
+    });
+    if (s != IIR_OK) return s;
+    s = launch(K_TV_CHAIN, st, [&] { tv_chain_kernel<T, M, false><<<(unsigned)a.B, 32, 0, st>>>(a); });
+    if (s != IIR_OK) return s;
+    return launch(K_TV_FWD, st, [&] {
+        tv_emit_kernel<T, M><<<(nseg_tot + TV_THREADS - 1) / TV_THREADS, TV_THREADS, 0, st>>>(a);
+    });
+}
+
+template <typename T, int M>
+static iir_status_t tv_bwd_m(const Layout& L, TvArgs& a, cudaStream_t st) {
+    const unsigned nseg_tot = (unsigned)L.ntot;
+    iir_status_t s = launch(K_TV_BWD_AGG, st, [&] {
+        tv_bwd_agg_kernel<T, M><<<(nseg_tot + TV_THREADS - 1) / TV_THREADS, TV_THREADS, 0, st>>>(a);
+    });
+    if (s != IIR_OK) return s;
+    s = launch(K_TV_CHAIN, st, [&] { tv_chain_kernel<T, M, true><<<(unsigned)a.B, 32, 0, st>>>(a); });
+    if (s != IIR_OK) return s;
+    return launch(K_TV_BWD, st, [&] {
+        tv_bwd_emit_kernel<T, M><<<(nseg_tot + TV_THREADS - 1) / TV_THREADS, TV_THREADS, 0, st>>>(a);
+    });
+}
+
+template <typename T>
+static iir_status_t tv_dispatch(bool fwd, int M, const Layout& L, TvArgs& a, cudaStream_t st) {
+    switch (M) {
+#define IIRG_CASE(m) case m: return fwd ? tv_fwd_m<T, m>(L, a, st) : tv_bwd_m<T, m>(L, a, st);
+        IIRG_TV_ORDERS(IIRG_CASE)
+#undef IIRG_CASE
+    }
+    return fail(IIR_EUNSUPPORTED, "per-sample order not compiled in");
+}
+
+iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* a, const void* x, const void* zi, void* y,
+                        void* zf, char* tape, char* ws, bool, cudaStream_t st) {
+    TvArgs ta{};
+    ta.a = a; ta.x = x; ta.zi = zi; ta.y = y; ta.zf = zf;
+    ta.phi = tape;
+    ta.w = reinterpret_cast<double*>(ws + L.ws_part);
+    ta.carry = reinterpret_cast<double*>(ws + L.ws_part2);
+    ta.B = d->batch; ta.T = d->length; ta.nseg = (int)L.ntiles;
+    return d->dtype == IIR_F64 ? tv_dispatch<double>(true, d->order, L, ta, st)
+                               : tv_dispatch<float>(true, d->order, L, ta, st);
+}
+
+iir_status_t tv_backward(const iir_desc_t* d, const Layout& L, const void* gy, const void* gzf, const void* a,
+                         const void* y, const void* zi, const char* tape, void* gx, void* ga, void* gzi, char* ws,
+                         bool, cudaStream_t st) {
+    TvArgs ta{};
+    ta.a = a; ta.zi = zi; ta.gy = gy; ta.gzf = gzf; ta.yin = y;
+    ta.gx = gx; ta.ga = ga; ta.gzi = gzi;
+    ta.phi = const_cast<char*>(tape);
+    ta.w = reinterpret_cast<double*>(ws + L.ws_part);
+    ta.carry = reinterpret_cast<double*>(ws + L.ws_part2);
+    ta.B = d->batch; ta.T = d->length; ta.nseg = (int)L.ntiles;
+    return d->dtype == IIR_F64 ? tv_dispatch<double>(false, d->order, L, ta, st)
+                               : tv_dispatch<float>(false, d->order, L, ta, st);
+}
+
 }  // namespace iirg
