@@ -3,6 +3,8 @@
 #include "host.h"
 #include "tv.cuh"
 
+#include <mutex>
+
 namespace iirg {
 
 #define IIRG_TV_ORDERS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(10) X(12) X(16) X(20) X(24) X(28) X(31)
@@ -34,6 +36,17 @@ Layout tv_layout(const iir_desc_t* d) {
     return L;
 }
 
+template <typename T, int M, int MODE>
+static void tv_seq_launch(unsigned nseg_tot, const TvArgs& a, cudaStream_t st) {
+    const size_t smem = TvStage<T, M>::bytes(MODE);
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        cudaFuncSetAttribute(tv_seq_kernel<T, M, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    const unsigned per = 32 * TV_SEQ_WARPS;
+    tv_seq_kernel<T, M, MODE><<<(nseg_tot + per - 1) / per, per, smem, st>>>(a);
+}
+
 template <typename T, int M>
 static iir_status_t tv_fwd_m(const Layout& L, TvArgs& a, cudaStream_t st) {
     const unsigned nseg_tot = (unsigned)L.ntot;
@@ -43,23 +56,17 @@ static iir_status_t tv_fwd_m(const Layout& L, TvArgs& a, cudaStream_t st) {
     if (s != IIR_OK) return s;
     s = launch(K_TV_CHAIN, st, [&] { tv_chain_kernel<T, M, false><<<(unsigned)a.B, 32, 0, st>>>(a); });
     if (s != IIR_OK) return s;
-    return launch(K_TV_FWD, st, [&] {
-        tv_emit_kernel<T, M><<<(nseg_tot + TV_THREADS - 1) / TV_THREADS, TV_THREADS, 0, st>>>(a);
-    });
+    return launch(K_TV_FWD, st, [&] { tv_seq_launch<T, M, TV_FWD_EMIT>(nseg_tot, a, st); });
 }
 
 template <typename T, int M>
 static iir_status_t tv_bwd_m(const Layout& L, TvArgs& a, cudaStream_t st) {
     const unsigned nseg_tot = (unsigned)L.ntot;
-    iir_status_t s = launch(K_TV_BWD_AGG, st, [&] {
-        tv_bwd_agg_kernel<T, M><<<(nseg_tot + TV_THREADS - 1) / TV_THREADS, TV_THREADS, 0, st>>>(a);
-    });
+    iir_status_t s = launch(K_TV_BWD_AGG, st, [&] { tv_seq_launch<T, M, TV_BWD_AGG>(nseg_tot, a, st); });
     if (s != IIR_OK) return s;
     s = launch(K_TV_CHAIN, st, [&] { tv_chain_kernel<T, M, true><<<(unsigned)a.B, 32, 0, st>>>(a); });
     if (s != IIR_OK) return s;
-    return launch(K_TV_BWD, st, [&] {
-        tv_bwd_emit_kernel<T, M><<<(nseg_tot + TV_THREADS - 1) / TV_THREADS, TV_THREADS, 0, st>>>(a);
-    });
+    return launch(K_TV_BWD, st, [&] { tv_seq_launch<T, M, TV_BWD_EMIT>(nseg_tot, a, st); });
 }
 
 template <typename T>
@@ -72,6 +79,13 @@ static iir_status_t tv_dispatch(bool fwd, int M, const Layout& L, TvArgs& a, cud
     return fail(IIR_EUNSUPPORTED, "per-sample order not compiled in");
 }
 
+// 16 B staging copies of coefficient rows need aligned rows and pieces that
+// never straddle two samples.
+static int tv_vec(const iir_desc_t* d, const void* a) {
+    const size_t ts = d->dtype == IIR_F64 ? 8 : 4;
+    return (((size_t)d->order * ts) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15u) == 0);
+}
+
 iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* a, const void* x, const void* zi, void* y,
                         void* zf, char* tape, char* ws, bool, cudaStream_t st) {
     TvArgs ta{};
@@ -80,6 +94,7 @@ iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* a, con
     ta.w = reinterpret_cast<double*>(ws + L.ws_part);
     ta.carry = reinterpret_cast<double*>(ws + L.ws_part2);
     ta.B = d->batch; ta.T = d->length; ta.nseg = (int)L.ntiles;
+    ta.vec = tv_vec(d, a);
     return d->dtype == IIR_F64 ? tv_dispatch<double>(true, d->order, L, ta, st)
                                : tv_dispatch<float>(true, d->order, L, ta, st);
 }
@@ -94,6 +109,7 @@ iir_status_t tv_backward(const iir_desc_t* d, const Layout& L, const void* gy, c
     ta.w = reinterpret_cast<double*>(ws + L.ws_part);
     ta.carry = reinterpret_cast<double*>(ws + L.ws_part2);
     ta.B = d->batch; ta.T = d->length; ta.nseg = (int)L.ntiles;
+    ta.vec = tv_vec(d, a) && (reinterpret_cast<uintptr_t>(ga) & 15u) == 0;
     return d->dtype == IIR_F64 ? tv_dispatch<double>(false, d->order, L, ta, st)
                                : tv_dispatch<float>(false, d->order, L, ta, st);
 }

@@ -22,7 +22,7 @@ namespace iirg {
 constexpr int TV_SEG = 512;          // samples per segment
 constexpr int TV_THREADS = 128;      // thread-per-segment kernels
 constexpr int TV_PHI_WARPS = 4;      // warps (segments) per CTA of the Phi kernel
-constexpr int TV_CH = 32;            // samples per staged coefficient chunk (Phi kernel)
+template <typename T> constexpr int tv_ch() { return sizeof(T) == 4 ? 32 : 16; }   // staged chunk (Phi kernel)
 constexpr int TV_U = 8;              // unroll of the sequential recursions
 
 struct TvArgs {
@@ -34,6 +34,7 @@ struct TvArgs {
     double* w;                                        // ws: [B][nseg][M] segment aggregates
     double* carry;                                    // ws: [B][nseg][M] entering states
     int64_t B, T; int nseg;
+    int vec;                                          // rows 16 B aligned and M % (16 / sizeof(T)) == 0
 };
 
 // ---------------------------------------------------------------------------
@@ -43,8 +44,9 @@ struct TvArgs {
 template <typename T, int M>
 __global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs p) {
     static_assert(M + 1 <= 32, "one lane per basis state plus one for the input");
-    __shared__ __align__(16) T sa[TV_PHI_WARPS][TV_CH * M];
-    __shared__ T sx[TV_PHI_WARPS][TV_CH];
+    constexpr int TV_CH = tv_ch<T>();
+    __shared__ __align__(16) T sa[TV_PHI_WARPS][2][TV_CH * M];
+    __shared__ __align__(16) T sx[TV_PHI_WARPS][2][TV_CH];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t seg = (int64_t)blockIdx.x * TV_PHI_WARPS + warp;
     if (seg >= p.B * p.nseg) return;
@@ -53,44 +55,70 @@ __global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs 
     const int64_t n0 = (int64_t)k * TV_SEG, n1 = min(n0 + TV_SEG, p.T);
     const T* arow = static_cast<const T*>(p.a) + seq * p.T * M;
     const T* xrow = static_cast<const T*>(p.x) + seq * p.T;
+    constexpr int E = 16 / (int)sizeof(T);
+    const bool vec = p.vec != 0 && (TV_CH * M) % E == 0;
+    // stage chunk [c, c + TV_CH) into buffer b (zero beyond n1)
+    auto stage = [&](int64_t c, int b) {
+        const int cnt = (int)min((int64_t)TV_CH, n1 - c);
+        if (vec && cnt == TV_CH) {
+            for (int e = lane * E; e < TV_CH * M; e += 32 * E) cp_async16(&sa[warp][b][e], arow + c * M + e, 16u);
+        } else {
+            for (int e = lane; e < TV_CH * M; e += 32) sa[warp][b][e] = (e < cnt * M) ? arow[c * M + e] : T(0);
+        }
+        if (lane < TV_CH) sx[warp][b][lane] = (lane < cnt) ? xrow[c + lane] : T(0);
+    };
     T v[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) v[i] = (lane == i) ? T(1) : T(0);
-    for (int64_t c = n0; c < n1; c += TV_CH) {
+    stage(n0, 0);
+    cp_async_commit();
+    int b = 0;
+    for (int64_t c = n0; c < n1; c += TV_CH, b ^= 1) {
         const int cnt = (int)min((int64_t)TV_CH, n1 - c);
         __syncwarp();
-        for (int e = lane; e < TV_CH * M; e += 32) sa[warp][e] = (e < cnt * M) ? arow[c * M + e] : T(0);
-        sx[warp][lane] = (lane < cnt) ? xrow[c + lane] : T(0);
+        if (c + TV_CH < n1) stage(c + TV_CH, b ^ 1);
+        cp_async_commit();
+        cp_async_wait<1>();
         __syncwarp();
         if (cnt == TV_CH) {
 #pragma unroll
             for (int s2 = 0; s2 < TV_CH; ++s2) {
-                T yn = (lane == M) ? sx[warp][s2] : T(0);
+                T yn = (lane == M) ? sx[warp][b][s2] : T(0);
+                T cf[M];
+                if constexpr ((M * sizeof(T)) % 16 == 0) {
 #pragma unroll
-                for (int i = M - 1; i >= 0; --i) yn = fma(-sa[warp][s2 * M + i], v[i], yn);   // newest term last
+                    for (int q = 0; q < M * (int)sizeof(T) / 16; ++q) {
+                        const uint4 t4 = reinterpret_cast<const uint4*>(&sa[warp][b][s2 * M])[q];
+                        memcpy(&cf[q * (16 / sizeof(T))], &t4, 16);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < M; ++i) cf[i] = sa[warp][b][s2 * M + i];
+                }
+#pragma unroll
+                for (int i = M - 1; i >= 0; --i) yn = fma(-cf[i], v[i], yn);   // newest term last
 #pragma unroll
                 for (int i = M - 1; i >= 1; --i) v[i] = v[i - 1];
                 v[0] = yn;
             }
         } else {                                   // ragged last chunk: exactly cnt samples
             for (int s2 = 0; s2 < cnt; ++s2) {
-                T yn = (lane == M) ? sx[warp][s2] : T(0);
+                T yn = (lane == M) ? sx[warp][b][s2] : T(0);
 #pragma unroll
-                for (int i = M - 1; i >= 0; --i) yn = fma(-sa[warp][s2 * M + i], v[i], yn);
+                for (int i = M - 1; i >= 0; --i) yn = fma(-sa[warp][b][s2 * M + i], v[i], yn);
 #pragma unroll
                 for (int i = M - 1; i >= 1; --i) v[i] = v[i - 1];
                 v[0] = yn;
             }
         }
     }
-    const T (&vf)[M] = v;
     if (lane < M) {
         T* ph = static_cast<T*>(p.phi) + seg * M * M;
 #pragma unroll
-        for (int i = 0; i < M; ++i) ph[i * M + lane] = vf[i];              // column `lane`
+        for (int i = 0; i < M; ++i) ph[i * M + lane] = v[i];               // column `lane`
     } else if (lane == M) {
 #pragma unroll
-        for (int i = 0; i < M; ++i) p.w[seg * M + i] = (double)vf[i];
+        for (int i = 0; i < M; ++i) p.w[seg * M + i] = (double)v[i];
     }
 }
 
@@ -98,29 +126,69 @@ __global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs 
 // Phase 2: per-sequence fp64 chain over the segments (one warp per sequence,
 // lane i = row i).  FWD: s_0 = zi, s_{k+1} = Phi_k s_k + w_k.
 // BWD: d_{nseg-1} = grad_zf, d_{k-1} = Phi_k^T d_k + w_k.  carry[k] = entering state.
+// Phi matrices in flight in the chain kernel (<= ~40 KB of static shared memory)
+template <typename T, int M> constexpr int tv_ring() {
+    return (int)(40960 / (M * M * sizeof(T))) < 2 ? 2 : ((int)(40960 / (M * M * sizeof(T))) > 8 ? 8 : (int)(40960 / (M * M * sizeof(T))));
+}
+
 template <typename T, int M, bool BWD>
 __global__ void __launch_bounds__(32) tv_chain_kernel(const TvArgs p) {
+    constexpr int TV_RING = tv_ring<T, M>();
+    constexpr int MM = M * M;
+    constexpr unsigned PB = (unsigned)(MM * sizeof(T));
+    constexpr int PS = (int)((PB + 15) / 16 * 16 / sizeof(T));        // ring slot stride (elements)
+    __shared__ __align__(128) T ring[TV_RING][PS];
+    __shared__ __align__(8) unsigned long long bar[TV_RING];
     __shared__ double ss[M];
     const int lane = threadIdx.x;
     const int64_t seq = blockIdx.x;
     const T* x0 = static_cast<const T*>(BWD ? p.gzf : p.zi);
     double s = (lane < M && x0 != nullptr) ? (double)x0[seq * M + lane] : 0.0;
-    const T* phi = static_cast<const T*>(p.phi) + seq * p.nseg * M * M;
+    const T* phi = static_cast<const T*>(p.phi) + seq * p.nseg * MM;
+    const double* wv = p.w + seq * p.nseg * M;
+    const bool bulk = (PB % 16 == 0) && ((reinterpret_cast<uintptr_t>(p.phi) & 15u) == 0);
+    if (lane == 0)
+        for (int r = 0; r < TV_RING; ++r) mbar_init(&bar[r], 1);
+    mbar_fence_init();
+    __syncwarp();
+    auto issue = [&](int q) {                    // hop q -> ring slot q % TV_RING
+        if (q >= p.nseg) return;
+        const int k = BWD ? p.nseg - 1 - q : q;
+        const int r = q % TV_RING;
+        if (bulk) {
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&bar[r], PB);
+                bulk_g2s(ring[r], phi + (int64_t)k * MM, PB, &bar[r]);
+            }
+        } else {
+            for (int e = lane; e < MM; e += 32) ring[r][e] = phi[(int64_t)k * MM + e];
+        }
+    };
+    for (int q = 0; q < TV_RING - 1; ++q) issue(q);
     for (int q = 0; q < p.nseg; ++q) {
         const int k = BWD ? p.nseg - 1 - q : q;
+        const int r = q % TV_RING;
+        const double wk = (lane < M) ? wv[(int64_t)k * M + lane] : 0.0;
+        __syncwarp();                            // everyone finished with the slot being refilled
+        issue(q + TV_RING - 1);
+        if (bulk) mbar_wait(&bar[r], (unsigned)((q / TV_RING) & 1));
         if (lane < M) {
             p.carry[(seq * p.nseg + k) * M + lane] = s;
             ss[lane] = s;
         }
         __syncwarp();
-        double acc = (lane < M) ? p.w[(seq * p.nseg + k) * M + lane] : 0.0;
+        double acc0 = wk, acc1 = 0.0;
         if (lane < M) {
-            const T* ph = phi + (int64_t)k * M * M;
+            const T* ph = ring[r];
 #pragma unroll
-            for (int j = 0; j < M; ++j) acc = fma((double)(BWD ? ph[j * M + lane] : ph[lane * M + j]), ss[j], acc);
+            for (int j = 0; j < M; j += 2) {
+                acc0 = fma((double)(BWD ? ph[j * M + lane] : ph[lane * M + j]), ss[j], acc0);
+                if (j + 1 < M)
+                    acc1 = fma((double)(BWD ? ph[(j + 1) * M + lane] : ph[lane * M + j + 1]), ss[j + 1], acc1);
+            }
         }
         __syncwarp();
-        s = acc;
+        s = acc0 + acc1;
     }
 }
 
@@ -146,129 +214,210 @@ __device__ __forceinline__ void load_row(const T* __restrict__ ar, T (&c)[M]) {
 }
 
 // ---------------------------------------------------------------------------
-// Forward phase 3: one thread per segment re-runs the recursion from its
-// entering state and writes y (and zf from the segment holding sample T-1).
-// The thread-per-segment recursions accumulate in fp64 (R = double) with T I/O:
-// they are bound by the 4M bytes of coefficients per sample, and fp64 removes the
-// O(TV_SEG) fp32 rounding growth of a 24-tap feedback loop ("TV precision").
+// Thread-per-segment recursions (forward emit, backward aggregate, backward
+// emit).  Lane l of a warp owns segment 32 w + l, so every lane streams its own
+// contiguous 4M bytes/sample of coefficient rows.  Each lane moves its segment's
+// chunk of C samples with ONE TMA bulk copy (cp.async.bulk, global -> shared,
+// completion counted on a per-buffer mbarrier; double-buffered), and grad_a
+// leaves the same way (shared -> global bulk copy), so the 96 B/sample streams
+// cost O(1) instructions per chunk instead of one uncoalesced access per 16 B.
+// Rows are padded by 16 B in shared memory: the lanes' 128-bit reads of their
+// own rows are bank-conflict free.  The short per-sample scalars (x, y, dy, dx)
+// are accessed per lane; each 128 B line then serves 32 samples from L1.
+// The recursions accumulate in fp64 (R) with T I/O: these kernels are bound by
+// the coefficient bytes, and fp64 removes the O(TV_SEG) fp32 rounding growth of
+// a long feedback loop ("TV precision").
+constexpr int TV_SEQ_WARPS = 2;           // warps per CTA (x 32 segments)
+template <typename T> constexpr int tv_chunk() { return 4; }   // samples per staged chunk
+template <typename T>
+__device__ __forceinline__ int64_t chunk_start_of(int64_t n0, int c, bool bwd) {
+    constexpr int C = tv_chunk<T>();
+    return bwd ? n0 + (int64_t)(TV_SEG / C - 1 - c) * C : n0 + (int64_t)c * C;
+}
+
+enum TvMode { TV_FWD_EMIT = 0, TV_BWD_AGG = 1, TV_BWD_EMIT = 2 };
+
 template <typename T, int M>
-__global__ void __launch_bounds__(TV_THREADS) tv_emit_kernel(const TvArgs p) {
+struct TvStage {
+    static constexpr int PAD = 16 / (int)sizeof(T);
+    static constexpr int C = tv_chunk<T>();
+    static constexpr int ROW = C * M;                   // elements of one segment's chunk
+    static constexpr int STRIDE = ROW + PAD;            // smem row stride (elements), 16 B multiple
+    static constexpr int NBUF(int mode) { return 2 + (mode == TV_BWD_EMIT ? 1 : 0); }
+    static constexpr size_t bytes(int mode) {           // per CTA (plus static mbarriers)
+        return (size_t)TV_SEQ_WARPS * NBUF(mode) * 32 * STRIDE * sizeof(T);
+    }
+};
+
+template <typename T, int M, int MODE>
+__global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs p) {
     using R = double;
-    const int64_t seg = (int64_t)blockIdx.x * TV_THREADS + threadIdx.x;
-    if (seg >= p.B * p.nseg) return;
-    const int64_t seq = seg / p.nseg;
-    const int k = (int)(seg - seq * p.nseg);
-    const int64_t n0 = (int64_t)k * TV_SEG, n1 = min(n0 + TV_SEG, p.T);
-    const T* arow = static_cast<const T*>(p.a) + seq * p.T * M;
-    const T* xrow = static_cast<const T*>(p.x) + seq * p.T;
-    T* yrow = static_cast<T*>(p.y) + seq * p.T;
-    R v[M];
+    using ST = TvStage<T, M>;
+    constexpr bool BWD = MODE != TV_FWD_EMIT;
+    constexpr int C = ST::C;
+    constexpr int NCH = TV_SEG / C;
+    constexpr int RB = M * (int)sizeof(T);                  // bytes of one coefficient row
+    extern __shared__ __align__(128) unsigned char tv_raw[];
+    __shared__ __align__(8) unsigned long long s_bar[TV_SEQ_WARPS][2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T* sA = reinterpret_cast<T*>(tv_raw) + (size_t)warp * ST::NBUF(MODE) * 32 * ST::STRIDE;   // 2 buffers
+    T* sG = sA + 2 * 32 * ST::STRIDE;                                                            // grad_a staging
+    unsigned long long* bar = s_bar[warp];
+    const bool bulk = p.vec != 0;                            // rows 16 B multiples, aligned bases
+    const int64_t nsegtot = p.B * p.nseg;
+    const int64_t seg = ((int64_t)blockIdx.x * TV_SEQ_WARPS + warp) * 32 + lane;
+    const bool valid = seg < nsegtot;
+    const int64_t seq = valid ? seg / p.nseg : 0;
+    const int k = valid ? (int)(seg - seq * p.nseg) : 0;
+    const int64_t n0 = (int64_t)k * TV_SEG, n1 = valid ? min(n0 + TV_SEG, p.T) : n0;
+    const T* a = static_cast<const T*>(p.a);
+    T* myA[2] = {sA + lane * ST::STRIDE, sA + 32 * ST::STRIDE + lane * ST::STRIDE};
+    T* myG = sG + lane * ST::STRIDE;
+    if (lane == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); }
+    mbar_fence_init();
+    __syncwarp();
+    unsigned phase[2] = {0u, 0u};
+
+    // stage chunk c of every lane's segment into buffer b
+    auto stage = [&](int c, int b) {
+        const int64_t cs = chunk_start_of<T>(n0, c, BWD);
+        const int64_t vs = max(cs, n0), ve = min(cs + C, n1);
+        const int nv = valid && ve > vs ? (int)(ve - vs) : 0;
+        T* dst = myA[b];
+        // rows outside the valid range read as zero (ragged last segment only)
+        if (nv < C)
+            for (int e = 0; e < C * M; ++e) {
+                const int64_t n = cs + e / M;
+                if (!(n >= vs && n < ve)) dst[e] = T(0);
+            }
+        if (bulk) {
+            fence_proxy_async();                             // generic reads / writes of this buffer done
+            const unsigned bytes = (unsigned)(nv * RB);
+            const unsigned total = __reduce_add_sync(0xffffffffu, bytes);
+            if (lane == 0) mbar_arrive_expect_tx(&bar[b], total);
+            __syncwarp();
+            if (bytes) bulk_g2s(dst + (vs - cs) * M, a + (seq * p.T + vs) * M, bytes, &bar[b]);
+        } else {
+            for (int64_t n = vs; n < ve; ++n)
 #pragma unroll
-    for (int i = 0; i < M; ++i) v[i] = p.carry[seg * M + i];
-    int64_t n = n0;
-    for (; n + TV_U <= n1; n += TV_U) {
-#pragma unroll
-        for (int u = 0; u < TV_U; ++u) {
-            T c[M];
-            load_row<T, M>(arow + (n + u) * M, c);
-            R yn = (R)__ldg(xrow + n + u);
-#pragma unroll
-            for (int i = M - 1; i >= 0; --i) yn = fma(-(R)c[i], v[i], yn);
-#pragma unroll
-            for (int i = M - 1; i >= 1; --i) v[i] = v[i - 1];
-            v[0] = yn;
-            yrow[n + u] = (T)yn;
+                for (int i = 0; i < M; ++i) dst[(n - cs) * M + i] = __ldg(a + (seq * p.T + n) * M + i);
         }
-    }
-    for (; n < n1; ++n) {
-        T c[M];
-        load_row<T, M>(arow + n * M, c);
-        R yn = (R)__ldg(xrow + n);
-#pragma unroll
-        for (int i = M - 1; i >= 0; --i) yn = fma(-(R)c[i], v[i], yn);
-#pragma unroll
-        for (int i = M - 1; i >= 1; --i) v[i] = v[i - 1];
-        v[0] = yn;
-        yrow[n] = (T)yn;
-    }
-    if (p.zf != nullptr && n1 == p.T) {
-        T* zf = static_cast<T*>(p.zf) + seq * M;
-#pragma unroll
-        for (int i = 0; i < M; ++i) zf[i] = (T)v[i];
-    }
-}
+    };
 
-// ---------------------------------------------------------------------------
-// Backward phase 1: one thread per segment, adjoint from the zero state at the
-// segment's end, walking back: w_k = dz(n0-1) given dz(n1-1) = 0.
-template <typename T, int M>
-__global__ void __launch_bounds__(TV_THREADS) tv_bwd_agg_kernel(const TvArgs p) {
-    using R = double;
-    const int64_t seg = (int64_t)blockIdx.x * TV_THREADS + threadIdx.x;
-    if (seg >= p.B * p.nseg) return;
-    const int64_t seq = seg / p.nseg;
-    const int k = (int)(seg - seq * p.nseg);
-    const int64_t n0 = (int64_t)k * TV_SEG, n1 = min(n0 + TV_SEG, p.T);
-    const T* arow = static_cast<const T*>(p.a) + seq * p.T * M;
-    const T* gyrow = p.gy == nullptr ? nullptr : static_cast<const T*>(p.gy) + seq * p.T;
-    R d[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) d[i] = 0.0;
-    for (int64_t n = n1 - 1; n >= n0; --n) {
-        T c[M];
-        load_row<T, M>(arow + n * M, c);
-        const R g = d[0] + (gyrow ? (R)__ldg(gyrow + n) : 0.0);
-#pragma unroll
-        for (int i = 0; i < M - 1; ++i) d[i] = fma(-(R)c[i], g, d[i + 1]);
-        d[M - 1] = -(R)c[M - 1] * g;
-    }
-#pragma unroll
-    for (int i = 0; i < M; ++i) p.w[seg * M + i] = (double)d[i];
-}
-
-// Backward phase 3: one thread per segment from its entering adjoint state:
-// grad_x, grad_a (M per sample), and grad_zi from the first segment.
-template <typename T, int M>
-__global__ void __launch_bounds__(TV_THREADS) tv_bwd_emit_kernel(const TvArgs p) {
-    using R = double;
-    const int64_t seg = (int64_t)blockIdx.x * TV_THREADS + threadIdx.x;
-    if (seg >= p.B * p.nseg) return;
-    const int64_t seq = seg / p.nseg;
-    const int k = (int)(seg - seq * p.nseg);
-    const int64_t n0 = (int64_t)k * TV_SEG, n1 = min(n0 + TV_SEG, p.T);
-    const T* arow = static_cast<const T*>(p.a) + seq * p.T * M;
+    R v[M];                                      // FWD: v = [y(n-1)..y(n-M)];  BWD: d = dz(n)
+    R yw[M];                                     // BWD_EMIT: yw[i] = y(n-1-i)
+    const T* xrow = static_cast<const T*>(p.x) + seq * p.T;
     const T* gyrow = p.gy == nullptr ? nullptr : static_cast<const T*>(p.gy) + seq * p.T;
     const T* yrow = static_cast<const T*>(p.yin) + seq * p.T;
+    T* youtrow = MODE == TV_FWD_EMIT ? static_cast<T*>(p.y) + seq * p.T : nullptr;
+    T* gxrow = (MODE == TV_BWD_EMIT && p.gx != nullptr) ? static_cast<T*>(p.gx) + seq * p.T : nullptr;
+    T* garow = (MODE == TV_BWD_EMIT && p.ga != nullptr) ? static_cast<T*>(p.ga) + seq * p.T * M : nullptr;
     const T* zi = p.zi == nullptr ? nullptr : static_cast<const T*>(p.zi) + seq * M;
-    T* gxrow = p.gx == nullptr ? nullptr : static_cast<T*>(p.gx) + seq * p.T;
-    T* garow = p.ga == nullptr ? nullptr : static_cast<T*>(p.ga) + seq * p.T * M;
-    auto yat = [&](int64_t m) -> R {                 // y(m), m >= -M; y(-k) = zi[k-1]
+    auto yat = [&](int64_t m) -> R {             // y(m), m >= -M; y(-k) = zi[k-1]
         if (m >= 0) return (R)__ldg(yrow + m);
         return zi != nullptr ? (R)zi[-m - 1] : 0.0;
     };
-    R d[M], yw[M];                                   // yw[i] = y(n-1-i)
 #pragma unroll
-    for (int i = 0; i < M; ++i) { d[i] = p.carry[seg * M + i]; yw[i] = yat(n1 - 2 - i); }
-    for (int64_t n = n1 - 1; n >= n0; --n) {
-        T c[M];
-        load_row<T, M>(arow + n * M, c);
-        const R g = d[0] + (gyrow ? (R)__ldg(gyrow + n) : 0.0);
-        if (gxrow) gxrow[n] = (T)g;
-        if (garow) {
-#pragma unroll
-            for (int i = 0; i < M; ++i) garow[n * M + i] = (T)(-g * yw[i]);
+    for (int i = 0; i < M; ++i) {
+        v[i] = (MODE == TV_BWD_AGG || !valid) ? 0.0 : p.carry[seg * M + i];
+        yw[i] = (MODE == TV_BWD_EMIT && valid) ? yat(n1 - 2 - i) : 0.0;
+    }
+    stage(0, 0);
+    for (int c = 0; c < NCH; ++c) {
+        const int b = c & 1;
+        __syncwarp();
+        if (c + 1 < NCH) stage(c + 1, b ^ 1);
+        if (bulk) { mbar_wait(&bar[b], phase[b]); phase[b] ^= 1u; }
+        __syncwarp();
+        const T* my = myA[b];
+        const int64_t cs = chunk_start_of<T>(n0, c, BWD);
+        if constexpr (MODE == TV_BWD_EMIT) {
+            if (bulk) bulk_wait_read0();                 // previous grad_a chunk has left smem
+            __syncwarp();
         }
 #pragma unroll
-        for (int i = 0; i < M - 1; ++i) d[i] = fma(-(R)c[i], g, d[i + 1]);
-        d[M - 1] = -(R)c[M - 1] * g;
+        for (int u = 0; u < C; ++u) {
+            const int s2 = BWD ? C - 1 - u : u;          // position in the chunk
+            const int64_t n = cs + s2;
+            const bool in = valid && n >= n0 && n < n1;
+            T cf[M];
+            if constexpr (RB % 16 == 0) {
 #pragma unroll
-        for (int i = 0; i < M - 1; ++i) yw[i] = yw[i + 1];
-        yw[M - 1] = yat(n - 2 - (M - 1));
+                for (int q = 0; q < M * (int)sizeof(T) / 16; ++q) {
+                    const uint4 t4 = reinterpret_cast<const uint4*>(my + s2 * M)[q];
+                    memcpy(&cf[q * (16 / sizeof(T))], &t4, 16);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < M; ++i) cf[i] = my[s2 * M + i];
+            }
+            if constexpr (MODE == TV_FWD_EMIT) {
+                if (in) {
+                    // four independent partial sums of the older terms; only the
+                    // newest term (a_1 y(n-1)) waits on the previous sample
+                    R acc[4] = {(R)__ldg(xrow + n), 0.0, 0.0, 0.0};
+#pragma unroll
+                    for (int i = M - 1; i >= 1; --i) acc[i & 3] = fma(-(R)cf[i], v[i], acc[i & 3]);
+                    const R rest = (acc[1] + acc[2]) + (acc[3] + acc[0]);
+                    const R yn = fma(-(R)cf[0], v[0], rest);
+#pragma unroll
+                    for (int i = M - 1; i >= 1; --i) v[i] = v[i - 1];
+                    v[0] = yn;
+                    youtrow[n] = (T)yn;
+                }
+            } else {
+                if (in) {
+                    const R g = v[0] + (gyrow ? (R)__ldg(gyrow + n) : 0.0);
+                    if constexpr (MODE == TV_BWD_EMIT) {
+                        if (gxrow) gxrow[n] = (T)g;
+#pragma unroll
+                        for (int i = 0; i < M; ++i) myG[s2 * M + i] = (T)(-g * yw[i]);
+#pragma unroll
+                        for (int i = 0; i < M - 1; ++i) yw[i] = yw[i + 1];
+                        yw[M - 1] = yat(n - 1 - M);
+                    }
+#pragma unroll
+                    for (int i = 0; i < M - 1; ++i) v[i] = fma(-(R)cf[i], g, v[i + 1]);
+                    v[M - 1] = -(R)cf[M - 1] * g;
+                }
+            }
+        }
+        if constexpr (MODE == TV_BWD_EMIT) {
+            if (garow != nullptr) {
+                const int64_t vs = max(cs, n0), ve = min(cs + C, n1);
+                if (valid && ve > vs) {
+                    if (bulk) {
+                        fence_proxy_async();                 // make the generic smem writes visible to TMA
+                        bulk_s2g(garow + vs * M, myG + (vs - cs) * M, (unsigned)((ve - vs) * RB));
+                        bulk_commit();
+                    } else {
+                        for (int64_t n = vs; n < ve; ++n)
+#pragma unroll
+                            for (int i = 0; i < M; ++i) garow[n * M + i] = myG[(n - cs) * M + i];
+                    }
+                }
+            }
+        }
     }
-    if (p.gzi != nullptr && k == 0) {
-        T* gzi = static_cast<T*>(p.gzi) + seq * M;
+    if constexpr (MODE == TV_BWD_EMIT) {
+        if (bulk) bulk_wait0();
+    }
+    if (!valid) return;
+    if constexpr (MODE == TV_FWD_EMIT) {
+        if (p.zf != nullptr && n1 == p.T) {
+            T* zf = static_cast<T*>(p.zf) + seq * M;
 #pragma unroll
-        for (int i = 0; i < M; ++i) gzi[i] = (T)d[i];
+            for (int i = 0; i < M; ++i) zf[i] = (T)v[i];
+        }
+    } else if constexpr (MODE == TV_BWD_AGG) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) p.w[seg * M + i] = v[i];
+    } else {
+        if (p.gzi != nullptr && k == 0) {
+            T* gzi = static_cast<T*>(p.gzi) + seq * M;
+#pragma unroll
+            for (int i = 0; i < M; ++i) gzi[i] = (T)v[i];
+        }
     }
 }
 
