@@ -116,12 +116,14 @@ static Layout layout(const iir_desc_t* d) {
     const int64_t ng_set = (per_set + 31) / 32;
     L.ngroups = ng_set * L.ncoef;
     size_t o = 0;
-    L.ws_ticket = o; L.ws_done = o + 4; o += 256;
+    L.ws_ticket = o; L.ws_done = o + 4; L.ws_epoch = o + 8; o += 256;
     L.ws_gcnt = o; o += al256(L.ngroups * 4);
     L.ws_scnt = o; o += al256(L.ncoef * 4);
     L.ws_clear = o;
     L.ws_sent = o;
     for (int l = 0; l < L.nlev; ++l) { L.ws_agg[l] = o; o += al256(d->batch * L.nblk[l] * M * 8); }
+    L.ws_bank = o - L.ws_sent;                           // two banks of look-back slots (epoch parity)
+    o += L.ws_bank;
     L.ws_sent_bytes = o - L.ws_sent;
     L.ws_part = o; o += al256(L.ntot * (2 * M + 1) * 8);
     L.ws_part2 = o; o += al256(L.ngroups * (2 * M + 1) * 8);
@@ -156,6 +158,8 @@ static CarryWs carry_ws(const Layout& L, char* w) {
     CarryWs c{};
     c.ticket = reinterpret_cast<unsigned*>(w + L.ws_ticket);
     c.done = reinterpret_cast<unsigned*>(w + L.ws_done);
+    c.epoch = reinterpret_cast<unsigned*>(w + L.ws_epoch);
+    c.bank = (int64_t)(L.ws_bank / 8);
     for (int l = 0; l < MAX_LEVELS; ++l) {
         c.agg[l] = l < L.nlev ? reinterpret_cast<double*>(w + L.ws_agg[l]) : nullptr;
         c.nblk[l] = L.nblk[l];
@@ -233,6 +237,7 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     fa.cw = carry_ws(L, w);
     fa.B = d->batch; fa.Tlen = d->length; fa.ntiles = (int)L.ntiles; fa.vec = vec;
     fa.trace = g_trace;
+    fa.span = g_trace == nullptr ? nullptr : g_trace + L.ntot * 16 + 2;   // [prep][fwd][bwd]
     return run_lti_any(c);
 }
 
@@ -280,6 +285,7 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     ba.cw = carry_ws(L, w);
     ba.B = d->batch; ba.Tlen = d->length; ba.ntiles = (int)L.ntiles; ba.vec = vec;
     ba.trace = g_trace;
+    ba.span = g_trace == nullptr ? nullptr : g_trace + L.ntot * 16 + 4;
     (void)b; (void)a;
     return run_lti_any(c);
 }

@@ -80,8 +80,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+// Kernel spans (debug): slots [base + 2 kind] = first CTA entry, [+1] = last CTA exit.
+__device__ __forceinline__ void span_enter(unsigned long long* sp) {
+    if (sp != nullptr && threadIdx.x == 0) atomicMin(sp, gtimer());
+}
+__device__ __forceinline__ void span_exit(unsigned long long* sp) {
+    if (sp != nullptr && threadIdx.x == 0) atomicMax(sp + 1, gtimer());
+}
 #define IIRG_TRACE(ptr, slot, k) \
-    do { if ((ptr) != nullptr && threadIdx.x == 0) (ptr)[(size_t)(slot) * 8 + (k)] = gtimer(); } while (0)
+    do { if ((ptr) != nullptr && threadIdx.x == 0) (ptr)[(size_t)(slot) * 16 + (k)] = gtimer(); } while (0)
 
 __device__ __forceinline__ double shfl_up_d(double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); }
 __device__ __forceinline__ double shfl_d(double v, int s) { return __shfl_sync(0xffffffffu, v, s); }
@@ -136,6 +143,10 @@ __device__ __forceinline__ void tile_store(T* __restrict__ row, const T* __restr
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, unsigned src_bytes) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>

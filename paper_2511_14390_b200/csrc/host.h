@@ -37,7 +37,7 @@ struct Layout {
     int nlev = 0;
     int64_t nblk[MAX_LEVELS] = {0, 0, 0, 0};
     // workspace: counters + flags (cleared region), then payloads
-    size_t ws_ticket = 0, ws_done = 0, ws_gcnt = 0, ws_scnt = 0;
+    size_t ws_ticket = 0, ws_done = 0, ws_epoch = 0, ws_gcnt = 0, ws_scnt = 0, ws_bank = 0;
     size_t ws_clear = 0;                                   // [0, ws_clear): counters, initialised to 0
     size_t ws_sent = 0, ws_sent_bytes = 0;                 // look-back slots, initialised to all-ones (NaN)
     size_t ws_agg[MAX_LEVELS] = {0, 0, 0, 0}, ws_part = 0, ws_part2 = 0, ws_bytes = 0;

@@ -128,10 +128,12 @@ template <int M> struct PrepSlots {
 template <typename T, int M, int FORM>
 __global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restrict__ b, const T* __restrict__ a,
                                                                int64_t coef_stride, double* __restrict__ tab,
-                                                               int64_t tab_stride, int nlev) {
+                                                               int64_t tab_stride, int nlev,
+                                                               unsigned long long* span = nullptr) {
     // Let the dependent scan kernel start its prologue (tile loads, local pass);
     // it waits for this grid's completion (griddepcontrol.wait) before reading tables.
     pdl_launch_dependents();
+    span_enter(span);
     constexpr int L = Chunk<T>::L, M2 = M * M;
     using TB = Tab<M>;
     using S = PrepSlots<M>;
@@ -227,6 +229,8 @@ __global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restr
         const int l = w / (32 * M2), r = w % (32 * M2), e = r / 32, k = r % 32;
         tb[TB::PQ + w] = mat[(S::Q + l * 33 + k) * M2 + e];
     }
+    __syncthreads();
+    span_exit(span);
 }
 
 // ---------------------------------------------------------------------------
@@ -293,39 +297,50 @@ __device__ __forceinline__ T adj_df_step(T (&d)[M], T dy, const T (&bc)[M + 1], 
 template <typename T, int M, int FORM>
 __device__ __forceinline__ void chain_rule(const double* __restrict__ G, const double* __restrict__ tb, T* gb, T* ga) {
     using TB = Tab<M>;
-    const double* bn = tb + TB::COEF;
-    const double* an = tb + TB::COEF + M + 1;
-    const double a0 = tb[TB::A0];
+    double bn[M + 1], an[M + 1];                 // every load issued up front (one round trip)
+#pragma unroll
+    for (int k = 0; k <= M; ++k) { bn[k] = __ldg(tb + TB::COEF + k); an[k] = __ldg(tb + TB::COEF + M + 1 + k); }
+    const double inv_a0 = 1.0 / __ldg(tb + TB::A0);
     double gbn[M + 1], gan[M + 1];
     gan[0] = 0.0;
     if constexpr (FORM == 1) {
         gbn[0] = G[2 * M];
+#pragma unroll
         for (int k = 1; k <= M; ++k) {
             gbn[k] = G[k - 1];
             gan[k] = -G[M + k - 1];
             gbn[0] -= an[k] * G[k - 1];
         }
     } else {
+#pragma unroll
         for (int k = 0; k <= M; ++k) gbn[k] = G[k];
+#pragma unroll
         for (int k = 1; k <= M; ++k) gan[k] = -G[M + k];
     }
     double s = 0.0;
+#pragma unroll
     for (int k = 0; k <= M; ++k) s += bn[k] * gbn[k];
+#pragma unroll
     for (int k = 1; k <= M; ++k) s += an[k] * gan[k];
-    if (gb != nullptr)
-        for (int k = 0; k <= M; ++k) gb[k] = (T)(gbn[k] / a0);
+    if (gb != nullptr) {
+#pragma unroll
+        for (int k = 0; k <= M; ++k) gb[k] = (T)(gbn[k] * inv_a0);
+    }
     if (ga != nullptr) {
-        ga[0] = (T)(-s / a0);
-        for (int k = 1; k <= M; ++k) ga[k] = (T)(gan[k] / a0);
+        ga[0] = (T)(-s * inv_a0);
+#pragma unroll
+        for (int k = 1; k <= M; ++k) ga[k] = (T)(gan[k] * inv_a0);
     }
 }
 
 // ---------------------------------------------------------------------------
 // Grid-level carry bookkeeping (workspace pointers), shared by fwd and bwd.
 struct CarryWs {
-    unsigned* ticket;            // tile ticket counter (tiles are scanned in ticket order)
-    unsigned* done;              // CTAs finished (the last one restores the workspace)
-    double* agg[LEVELS];         // level-l block aggregates [seq][block][M]; all-ones NaN = not published
+    unsigned* ticket;            // tile ticket counter (IIRG_TICKETS only)
+    unsigned* done;              // CTAs finished (the last one advances the epoch)
+    unsigned* epoch;             // call counter: slot bank = epoch & 1
+    int64_t bank;                // elements between the two slot banks
+    double* agg[LEVELS];         // bank 0 level-l block aggregates [seq][block][M]; all-ones NaN = not published
     int64_t nblk[LEVELS];        // blocks per sequence at level l (ceil(ntiles / 32^l))
     int nlev;                    // levels in use
 };
@@ -337,6 +352,7 @@ struct LtiFwdArgs {
     CarryWs cw;
     int64_t B, Tlen; int ntiles; int vec;
     unsigned long long* trace;                                    // debug: per-tile phase times
+    unsigned long long* span;                                     // debug: kernel span
 };
 
 struct LtiBwdArgs {
@@ -348,6 +364,7 @@ struct LtiBwdArgs {
     CarryWs cw;
     int64_t B, Tlen; int ntiles; int vec;
     unsigned long long* trace;
+    unsigned long long* span;
 };
 
 // Normalised coefficients in T, straight from the caller's b, a (the same
@@ -369,6 +386,10 @@ __device__ __forceinline__ void load_coefs(const double* __restrict__ tb, T (&bc
     for (int k = 0; k < M; ++k) cc[k] = (T)__ldg(tb + TB::COEF + 2 * (M + 1) + k);
 }
 
+template <int M>
+__device__ __forceinline__ void stage_small_async(double* st, const double* __restrict__ tb) {
+    for (int i = threadIdx.x; i < Tab<M>::SMALL; i += blockDim.x) cp_async8(st + i, tb + i);
+}
 // Stage the small power tables (PL | PW | PWT) of this tile's coefficient set.
 template <int M>
 __device__ __forceinline__ void stage_small(double* st, const double* __restrict__ tb) {
@@ -416,6 +437,42 @@ __device__ __forceinline__ void block_scan(const double* st, int lane, double (*
     }
 }
 
+// dst[k] = sum_r src[r NG + k] (r < nrows) in a fixed order: warp w owns the
+// columns k = w (mod NW); lane l sums rows l, l+32, ... and a xor butterfly
+// combines the lanes.  All loads of a row sweep are independent (one round trip
+// for up to 32 rows), and the result is bitwise reproducible.
+template <int NG>
+__device__ __forceinline__ void reduce_rows(const double* src, int64_t nrows, double* dst, int lane, int warp) {
+    constexpr int KQ = (NG + NW - 1) / NW;
+    constexpr int RB = 2;                        // rows per lane loaded together
+    double acc[KQ];
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) acc[q] = 0.0;
+    for (int64_t r0 = lane; r0 < nrows; r0 += 32 * RB) {
+        double v[RB][KQ];
+#pragma unroll
+        for (int b = 0; b < RB; ++b)
+#pragma unroll
+            for (int q = 0; q < KQ; ++q) {
+                const int k = warp + q * NW;
+                const int64_t r = r0 + 32 * b;
+                v[b][q] = (k < NG && r < nrows) ? __ldcg(src + r * NG + k) : 0.0;
+            }
+#pragma unroll
+        for (int b = 0; b < RB; ++b)
+#pragma unroll
+            for (int q = 0; q < KQ; ++q) acc[q] += v[b][q];
+    }
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+        double v = acc[q];
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const int k = warp + q * NW;
+        if (lane == 0 && k < NG) dst[k] = v;
+    }
+}
+
 template <int M>
 __device__ __forceinline__ void warp_sum(double (&v)[M]) {
 #pragma unroll
@@ -432,23 +489,32 @@ __device__ __forceinline__ void publish(double* dst, const double (&v)[M], int l
     }
 }
 
-// Wait until a look-back payload slot is published and read it: one element is
-// polled (volatile loads: never hoisted, never served from a stale L1 line)
-// with exponential back-off, then all M are read and re-checked.  A slot that
-// is never published is a bug: report and trap instead of hanging the GPU.
+// Look-back payload slots.  A read is one round trip: all M elements are
+// loaded at once (volatile: never hoisted, never served from a stale L1 line)
+// and the slot is ready when none is the sentinel.
+template <int M>
+__device__ __forceinline__ void load_slot(const double* src, double (&v)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) v[i] = ld_relaxed(src + i);
+}
+template <int M>
+__device__ __forceinline__ bool slot_ready(const double (&v)[M]) {
+    bool r = true;
+#pragma unroll
+    for (int i = 0; i < M; ++i) r = r && !is_sentinel(v[i]);
+    return r;
+}
+// Re-poll a slot whose first read was not ready, with exponential back-off.  A
+// slot that is never published is a bug: report and trap instead of hanging.
 template <int M>
 __device__ __forceinline__ void wait_slot(const double* src, double (&v)[M]) {
     unsigned ns = 32;
     unsigned long long t0 = 0;
     for (;;) {
-        if (!is_sentinel(ld_relaxed(src))) {
-            bool ready = true;
-#pragma unroll
-            for (int i = 0; i < M; ++i) { v[i] = ld_relaxed(src + i); ready = ready && !is_sentinel(v[i]); }
-            if (ready) return;
-        }
         __nanosleep(ns);
-        if (ns < 512) ns *= 2;
+        load_slot<M>(src, v);
+        if (slot_ready<M>(v)) return;
+        if (ns < 256) ns *= 2;
         else {
             const unsigned long long now = gtimer();
             if (t0 == 0) t0 = now;
@@ -466,14 +532,16 @@ __device__ __forceinline__ void wait_slot(const double* src, double (&v)[M]) {
 // Q_l = A_f^(32^l TS):
 //   T_l = sum_{d < d_l} Q_l^(d_l - 1 - d) AGG^(l)_{(j >> 5l) - d_l + d}
 //   X_j = T_0 + Q_0^d_0 (T_1 + Q_1^d_1 (T_2 + ...))     (state entering tile j)
-// Each T_l is one lane-parallel round (lane d waits for one aggregate) and a
-// fixed butterfly sum: bitwise deterministic, and no tile waits on a serial
-// chain.  A tile that closes a level-(l+1) block publishes AGG^(l+1) =
-// Q_l T_l + AGG^(l)_own right after T_l, before any higher-level wait.
+// Lane d reads slot d of EVERY level at once, so a tile whose inputs are all
+// published pays one round trip for the whole look-back (the levels are not
+// waited for one after the other).  Each T_l is then a fixed butterfly sum:
+// bitwise deterministic.  A tile that closes a level-(l+1) block publishes
+// AGG^(l+1) = Q_l T_l + AGG^(l)_own as soon as T_l is known.
 template <int M, bool TR>
 __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int lane, int jt, int64_t seq,
                                            const double (&X0)[M], double (&G)[M], const CarryWs& cw,
-                                           double (&X)[M]) {
+                                           double (&X)[M], unsigned long long* trace = nullptr,
+                                           unsigned tk = 0) {
     using TB = Tab<M>;
     constexpr int M2 = M * M;
     __shared__ double s_T[LEVELS][M];
@@ -482,26 +550,36 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
     if (jt == 0) mv_acc_lane<M, TR>(tb + TB::PQ, 32, 1, X0, G);   // tile 0 carries the initial state
     publish<M>(cw.agg[0] + (seq * cw.nblk[0] + jt) * M, G, lane);
     if (jt == 0) return;
+    // levels 0 and 1 are read up front (one round trip); deeper levels, used only
+    // by sequences of more than 32^2 tiles, when they are reached
+    constexpr int PF = LEVELS < 2 ? LEVELS : 2;
     int dl[LEVELS];
+    double V[LEVELS][M];
+#pragma unroll
+    for (int l = 0; l < LEVELS; ++l) {
+        dl[l] = l < cw.nlev ? (jt >> (5 * l)) & 31 : 0;
+        if (l < PF && lane < dl[l])
+            load_slot<M>(cw.agg[l] + (seq * cw.nblk[l] + (jt >> (5 * l)) - dl[l] + lane) * M, V[l]);
+    }
     bool closing = true;                   // all lower digits were 31 so far
     double Own[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) Own[i] = G[i];
 #pragma unroll
     for (int l = 0; l < LEVELS; ++l) {
-        dl[l] = (jt >> (5 * l)) & 31;
         double Tv[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) Tv[i] = 0.0;
-        if (l < cw.nlev && dl[l] > 0) {
-            const int64_t base = seq * cw.nblk[l] + (jt >> (5 * l)) - dl[l];
+        if (dl[l] > 0) {
             if (lane < dl[l]) {
-                double v[M];
-                wait_slot<M>(cw.agg[l] + (base + lane) * M, v);
-                mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, dl[l] - 1 - lane, v, Tv);
+                if (l >= PF) load_slot<M>(cw.agg[l] + (seq * cw.nblk[l] + (jt >> (5 * l)) - dl[l] + lane) * M, V[l]);
+                if (!slot_ready<M>(V[l]))
+                    wait_slot<M>(cw.agg[l] + (seq * cw.nblk[l] + (jt >> (5 * l)) - dl[l] + lane) * M, V[l]);
+                mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, dl[l] - 1 - lane, V[l], Tv);
             }
             warp_sum<M>(Tv);
         }
+        if (l < 2 && trace != nullptr && lane == 0) trace[(size_t)tk * 16 + 6 + l] = gtimer();
         if (lane == 0) {
 #pragma unroll
             for (int i = 0; i < M; ++i) s_T[l][i] = Tv[i];
@@ -532,21 +610,51 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
     for (int i = 0; i < M; ++i) X[i] = R[i];
 }
 
-// The last CTA to finish restores the workspace (tickets, look-back slots), so
-// the next call on the same stream-ordered workspace needs no memset.  No fence:
-// every CTA's slot reads completed (their values were consumed) before its
-// increment.
-template <int M>
-__device__ __forceinline__ void cta_exit(const CarryWs& cw, int64_t B, unsigned nctas) {
+// Scan order of this CTA's tile.  Tiles are scanned in CTA launch order: the
+// hardware dispatches the CTAs of a 1-D grid in increasing blockIdx, so every
+// tile a CTA waits for belongs to a CTA that is already resident (the single-
+// pass look-back of CUB-style scans relies on the same order).  IIRG_TICKETS=1
+// takes an atomic ticket instead (one more round trip before the tile load).
+#ifndef IIRG_TICKETS
+#define IIRG_TICKETS 0
+#endif
+__device__ __forceinline__ unsigned tile_order(unsigned* ticket) {
+#if IIRG_TICKETS
+    __shared__ unsigned s_ticket;
+    if (threadIdx.x == 0) s_ticket = atomicAdd(ticket, 1u);
+    __syncthreads();
+    return s_ticket;
+#else
+    (void)ticket;
+    return blockIdx.x;
+#endif
+}
+
+// Look-back slots live in two banks used by alternate calls (epoch parity).
+// Every CTA re-arms its share of the OTHER bank (last used by the previous
+// call on this workspace, which has completed) with sentinels, and the last
+// CTA to finish advances the epoch, so a call leaves the workspace ready for
+// the next one without a serial clean-up tail.
+__device__ __forceinline__ unsigned carry_bank(CarryWs& cw) {
+    const unsigned ep = __ldcg(cw.epoch);
+    if (ep & 1u)
+        for (int l = 0; l < LEVELS; ++l)
+            if (cw.agg[l] != nullptr) cw.agg[l] += cw.bank;
+    return ep;
+}
+__device__ __forceinline__ void rearm_other_bank(const CarryWs& cw, unsigned ep, unsigned cta, unsigned nctas) {
+    // the other bank is one contiguous range starting at agg[0] -/+ bank
+    double* other = cw.agg[0] + ((ep & 1u) ? -cw.bank : cw.bank);
+    const int64_t per = (cw.bank + nctas - 1) / nctas;
+    const int64_t e0 = (int64_t)cta * per, e1 = min(e0 + per, cw.bank);
+    for (int64_t i = e0 + threadIdx.x; i < e1; i += blockDim.x) __stcg(other + i, sentinel());
+}
+__device__ __forceinline__ void cta_exit(const CarryWs& cw, unsigned ep, unsigned nctas) {
     __shared__ unsigned s_last;
     __syncthreads();
     if (threadIdx.x == 0) s_last = (atomicAdd(cw.done, 1u) == nctas - 1u) ? 1u : 0u;
     __syncthreads();
-    if (s_last) {
-        for (int l = 0; l < cw.nlev; ++l)
-            for (int64_t i = threadIdx.x; i < B * cw.nblk[l] * M; i += blockDim.x) cw.agg[l][i] = sentinel();
-        if (threadIdx.x == 0) { *cw.ticket = 0u; *cw.done = 0u; }
-    }
+    if (s_last && threadIdx.x == 0) { *cw.ticket = 0u; *cw.done = 0u; *cw.epoch = ep + 1u; }
 }
 
 template <typename T, int M>
@@ -565,8 +673,13 @@ struct Smem {
 // Forward: a2-a4.  One CTA per tile of TS samples; tiles are taken in ticket
 // order (ticket t = tile t / B of sequence t % B), so every tile a CTA waits
 // for belongs to a CTA that is already running.
+// Minimum resident CTAs per SM requested from ptxas (caps the registers of the
+// high-order instantiations, whose occupancy is otherwise register-bound).
+template <int M> constexpr int fwd_min_blocks() { return M <= 2 ? 8 : (M <= 4 ? 6 : 4); }
+template <int M> constexpr int bwd_min_blocks() { return M <= 4 ? 4 : 3; }
+
 template <typename T, int M, int FORM>
-__global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
+__global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const LtiFwdArgs p) {
     constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
     using V = typename Vec<T>::type;
     using TB = Tab<M>;
@@ -577,12 +690,11 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
     T* us = xs + SM::PT;                                          // DF: u tile
     __shared__ double s_agg[NW][M];
     __shared__ double s_xw[NW][M];
-    __shared__ unsigned s_ticket;
-
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_ticket = atomicAdd(p.cw.ticket, 1u);
-    __syncthreads();
-    const unsigned tk = s_ticket;
+    const unsigned tk = tile_order(p.cw.ticket);
+    span_enter(p.span);
+    CarryWs cw = p.cw;
+    const unsigned ep = carry_bank(cw);
     const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
     const int jt = (int)(tk / (unsigned long long)p.B);
     const int64_t p0 = (int64_t)jt * TS;
@@ -590,10 +702,17 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
     IIRG_TRACE(p.trace, tk, 0);
     tile_load_async<T, TS>(xs, xrow, p0, p.Tlen, p.vec);
     cp_async_commit();
+    // the power tables come from the prologue kernel (PDL): wait, then stage them
+    // asynchronously so that their load overlaps the tile's and the local pass
+    pdl_wait();
+    const double* tb = p.tab + seq * p.tab_stride;
+    stage_small_async<M>(st, tb);
+    cp_async_commit();
+    rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
     T bc[M + 1], ac[M + 1];
     raw_coefs<T, M>(static_cast<const T*>(p.b) + seq * p.coef_stride,
                     static_cast<const T*>(p.a) + seq * p.coef_stride, bc, ac);
-    cp_async_wait<0>();
+    cp_async_wait<1>();                                // x tile
     __syncthreads();
 
     // a2: local pass from the zero state over this thread's chunk.
@@ -608,10 +727,8 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
         for (int e = 0; e < W; ++e) { T du; fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, du); }
     }
     IIRG_TRACE(p.trace, tk, 1);
-    // a3: carries in fp64; the power tables come from the prologue (PDL).
-    pdl_wait();
-    const double* tb = p.tab + seq * p.tab_stride;
-    stage_small<M>(st, tb);
+    // a3: carries in fp64
+    cp_async_wait<0>();                                // power tables
     __syncthreads();
     double S[M];
 #pragma unroll
@@ -632,7 +749,7 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
 #pragma unroll
         for (int i = 0; i < M; ++i) X0[i] = (zi != nullptr && jt == 0) ? (double)zi[seq * M + i] : 0.0;
         IIRG_TRACE(p.trace, tk, 2);
-        tile_carry<M, false>(tb, lane, jt, seq, X0, G, p.cw, X);
+        tile_carry<M, false>(tb, lane, jt, seq, X0, G, cw, X, p.trace, tk);
         IIRG_TRACE(p.trace, tk, 3);
         if (lane < NW) {                           // state entering warp `lane`
             double xw[M];
@@ -692,7 +809,8 @@ __global__ void __launch_bounds__(NT) lti_fwd_kernel(const LtiFwdArgs p) {
         tile_store<T, TS>(urow, us, p0, p.Tlen, p.vec);
     }
     IIRG_TRACE(p.trace, tk, 5);
-    cta_exit<M>(p.cw, p.B, gridDim.x);
+    cta_exit(cw, ep, gridDim.x);
+    span_exit(p.span);
 }
 
 template <typename T, int M, int FORM>
@@ -727,7 +845,7 @@ __device__ __forceinline__ void bwd_load_u(const LtiBwdArgs& p, int64_t seq, int
 // ticket order last to first; inside a tile thread t owns chunk NT-1-t, walked
 // backwards.  TDF: smem dy | x | y.  DF: smem dy | u (with HALO samples of history).
 template <typename T, int M, int FORM>
-__global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
+__global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const LtiBwdArgs p) {
     constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
     constexpr int NG = 2 * M + 1;                       // gradient partial sums
     using V = typename Vec<T>::type;
@@ -742,12 +860,13 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
     __shared__ double s_xw[NW][M];
     __shared__ double s_red[NW][NG];
     __shared__ double s_G[NG];
-    __shared__ unsigned s_ticket, s_fin;
+    __shared__ unsigned s_fin;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_ticket = atomicAdd(p.cw.ticket, 1u);
-    __syncthreads();
-    const unsigned tk = s_ticket;
+    const unsigned tk = tile_order(p.cw.ticket);
+    span_enter(p.span);
+    CarryWs cw = p.cw;
+    const unsigned ep = carry_bank(cw);
     const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
     const int jr = (int)(tk / (unsigned long long)p.B);          // 0 = last tile in time
     const int jt = p.ntiles - 1 - jr;                            // time index of the tile
@@ -767,6 +886,7 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
         bwd_load_u<T, M, FORM>(p, seq, p0, s2);
     }
     cp_async_commit();
+    rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
     stage_small<M>(st, tb);                          // tables live in the tape (written by the forward)
     T bc[M + 1], ac[M + 1], cc[M];
     load_coefs<T, M>(tb, bc, ac, cc);
@@ -809,7 +929,7 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
 #pragma unroll
         for (int i = 0; i < M; ++i) X0[i] = (gzf != nullptr && jr == 0) ? (double)gzf[seq * M + i] : 0.0;
         IIRG_TRACE(p.trace, tk, 2);
-        tile_carry<M, true>(tb, lane, jr, seq, X0, G, p.cw, X);
+        tile_carry<M, true>(tb, lane, jr, seq, X0, G, cw, X, p.trace, tk);
         IIRG_TRACE(p.trace, tk, 3);
         if (lane < NW) {
             double xw[M];
@@ -906,10 +1026,12 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
 
     if (p.want_coef) {
         // fused a8: group of 32 tiles -> group sum; last group of the set -> chain rule.
+        // SHARED groups are consecutive tiles in scan order (they complete, and are
+        // reduced, while the kernel runs); PER_SEQ groups are a sequence's tiles.
         const bool shared = p.ncoef == 1;
         const int64_t per_set = shared ? p.B * p.ntiles : p.ntiles;
         const int64_t cset = shared ? 0 : seq;
-        const int64_t li = shared ? seq * p.ntiles + jt : jt;          // index within the set
+        const int64_t li = shared ? (int64_t)tk : jt;                  // index within the set
         const int64_t gi = li >> 5;
         const int64_t ngroups = (per_set + 31) >> 5;
         const int gsize = (int)min((int64_t)32, per_set - (gi << 5));
@@ -923,17 +1045,15 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
             __threadfence();
         }
         __syncthreads();
+        IIRG_TRACE(p.trace, tk, 8);
         if (tid == 0) s_fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
         __syncthreads();
         if (s_fin) {                                   // last tile of its group
             __threadfence();
-            if (tid < NG) {
-                double s = 0.0;
-                for (int t = 0; t < gsize; ++t) s += __ldcg(part + ((gi << 5) + t) * NG + tid);
-                __stcg(part2 + gi * NG + tid, s);
-                __threadfence();
-            }
+            reduce_rows<NG>(part + (gi << 5) * NG, gsize, part2 + gi * NG, lane, warp);
+            __threadfence();
             __syncthreads();
+            IIRG_TRACE(p.trace, tk, 9);
             if (tid == 0) {
                 p.gcnt[cset * ngroups + gi] = 0u;
                 s_fin = (atomicAdd(p.scnt + cset, 1u) == (unsigned)ngroups - 1u) ? 2u : 0u;
@@ -941,22 +1061,24 @@ __global__ void __launch_bounds__(NT) lti_bwd_kernel(const LtiBwdArgs p) {
             __syncthreads();
             if (s_fin == 2u) {                          // last group of the set
                 __threadfence();
-                if (tid < NG) {
-                    double s = 0.0;
-                    for (int64_t g2 = 0; g2 < ngroups; ++g2) s += __ldcg(part2 + g2 * NG + tid);
-                    s_G[tid] = s;
-                }
+                IIRG_TRACE(p.trace, tk, 12);
+                reduce_rows<NG>(part2, ngroups, s_G, lane, warp);
                 __syncthreads();
+                IIRG_TRACE(p.trace, tk, 13);
                 if (tid == 0) {
                     chain_rule<T, M, FORM>(s_G, tb,
                                            p.gb == nullptr ? nullptr : static_cast<T*>(p.gb) + cset * (M + 1),
                                            p.ga == nullptr ? nullptr : static_cast<T*>(p.ga) + cset * (M + 1));
                     p.scnt[cset] = 0u;
+                    IIRG_TRACE(p.trace, tk, 14);
                 }
             }
         }
     }
-    cta_exit<M>(p.cw, p.B, gridDim.x);
+    IIRG_TRACE(p.trace, tk, 10);
+    cta_exit(cw, ep, gridDim.x);
+    IIRG_TRACE(p.trace, tk, 11);
+    span_exit(p.span);
 }
 
 }  // namespace iirg

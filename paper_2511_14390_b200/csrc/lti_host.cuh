@@ -48,7 +48,7 @@ struct LtiOps {
         iir_status_t s = launch(K_LTI_PREP, st, [&] {
             lti_prep_kernel<T, M, FORM><<<(unsigned)L.ncoef, PREP_THREADS, PrepSlots<M>::bytes(), st>>>(
                 static_cast<const T*>(b), static_cast<const T*>(a), cstride, const_cast<double*>(fa.tab),
-                Tab<M>::SIZE, L.nlev);
+                Tab<M>::SIZE, L.nlev, fa.span == nullptr ? nullptr : fa.span - 2);
         });
         if (s != IIR_OK) return s;
         return launch(K_LTI_FWD, st, [&] {

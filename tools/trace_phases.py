@@ -15,8 +15,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2511_14390_b200 import _binding as B  # noqa: E402
 
-PH_F = ["start", "local", "scan", "carry", "emit", "store", "-", "-"]
-PH_B = ["start", "local", "scan", "carry", "emit", "store", "-", "-"]
+PH_F = ["start", "local", "scan", "carry", "emit", "store", "lvl0", "lvl1"]
+PH_B = ["start", "local", "scan", "carry", "emit", "store", "lvl0", "lvl1"]
 
 
 def main():
@@ -28,13 +28,49 @@ def main():
     prob = bench.Problem(w, 0, 1, 2)
     s = torch.cuda.Stream()
     ntot = w["batch"] * ((w["length"] + 4095) // 4096)
-    buf = torch.zeros(ntot * 8, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(ntot * 16 + 8, dtype=torch.int64, device="cuda")
+    buf2 = torch.zeros(ntot * 16 + 8, dtype=torch.int64, device="cuda")
+
+    def reset(b):
+        b.zero_()
+        b[ntot * 16::2] = (1 << 63) - 1          # span entry slots (atomicMin)
     for rep in range(a.reps):
         with torch.cuda.stream(s):
             prob.step(0, s)
         torch.cuda.synchronize()
+    # one whole step (prep, fwd, bwd back to back on one stream): kernel spans
+    st = prob.sets[0]
+    for rep in range(3):
+        reset(buf)
+        reset(buf2)
+        with torch.cuda.stream(s):
+            B.iir_debug_trace(buf)
+            B.iir_forward(prob.desc, prob.b, prob.a, st["x"], prob.zi, st["y"], prob.zf, prob.tape, prob.tb,
+                          prob.ws, prob.wb, s)
+            B.iir_debug_trace(buf2)
+            B.iir_backward(prob.desc, st["gy"], prob.gzf, prob.b, prob.a, st["x"], st["y"], prob.zi, prob.tape,
+                           prob.tb, st["gx"], prob.gb, prob.ga, prob.gzi, prob.ws, prob.wb, s)
+            B.iir_debug_trace(None)
+        torch.cuda.synchronize()
+    a1 = buf[ntot * 16:].cpu().numpy().astype(np.float64)
+    a2 = buf2[ntot * 16:].cpu().numpy().astype(np.float64)
+    t0 = a1[0]
+    spans = {"prep": (a1[0], a1[1]), "fwd": (a1[2], a1[3]), "bwd": (a2[4], a2[5])}
+    print("== one step, kernel spans (us from prep entry): " + ", ".join(
+        f"{k} [{(v[0] - t0) / 1e3:.2f}, {(v[1] - t0) / 1e3:.2f}]" for k, v in spans.items()))
+    tf = buf[:ntot * 16].view(ntot, 16).cpu().numpy().astype(np.float64)
+    tb_ = buf2[:ntot * 16].view(ntot, 16).cpu().numpy().astype(np.float64)
+    for k, nm in ((8, "partial"), (9, "group"), (12, "set-start"), (13, "set-sum"), (14, "chain"), (10, "pre-exit"),
+                  (11, "exit")):
+        col = tb_[:, k]
+        col = col[col > 0]
+        if col.size:
+            print(f"   bwd {nm:9s} max {(col.max() - t0) / 1e3:.2f}  n={col.size}")
+    print("   fwd tiles: first start %.2f last store %.2f | bwd tiles: first start %.2f last store %.2f" % (
+        (tf[:, 0].min() - t0) / 1e3, (tf[:, 5].max() - t0) / 1e3, (tb_[:, 0].min() - t0) / 1e3,
+        (tb_[:, 5].max() - t0) / 1e3))
     for kern in ("fwd", "bwd"):
-        buf.zero_()
+        reset(buf)
         B.iir_debug_trace(buf)
         st = prob.sets[0]
         with torch.cuda.stream(s):
@@ -50,12 +86,12 @@ def main():
                                prob.tb, st["gx"], prob.gb, prob.ga, prob.gzi, prob.ws, prob.wb, s)
         torch.cuda.synchronize()
         B.iir_debug_trace(None)
-        t = buf.view(ntot, 8).cpu().numpy().astype(np.float64)
+        t = buf[:ntot * 16].view(ntot, 16).cpu().numpy().astype(np.float64)
         t0 = t[:, 0].min()
         rel = (t - t0) / 1e3
         names = PH_F if kern == "fwd" else PH_B
         print(f"== {kern} ({ntot} tiles), us relative to first tile start; columns p0 p10 p50 p90 p100")
-        for k, nm in enumerate(names[:6]):
+        for k, nm in enumerate(names):
             col = rel[:, k]
             col = col[t[:, k] > 0]
             if nm == "-" or col.size == 0:
@@ -65,6 +101,16 @@ def main():
         d = np.diff(rel, axis=1)
         print("   phase durations (median us): " + ", ".join(
             f"{names[k]}->{names[k + 1]} {np.median(d[:, k]):.2f}" for k in range(5)))
+        ok = (t[:, 6] > 0) & (t[:, 2] > 0)
+        if ok.any():
+            w0 = (t[ok, 6] - t[ok, 2]) / 1e3
+            print("   scan->lvl0 wait p50 %.2f p90 %.2f" % tuple(np.percentile(w0, [50, 90])))
+        ok = (t[:, 7] > 0) & (t[:, 6] > 0)
+        if ok.any():
+            w1 = (t[ok, 7] - t[ok, 6]) / 1e3
+            w2 = (t[ok, 3] - t[ok, 7]) / 1e3
+            print("   lvl0->lvl1 p50 %.2f p90 %.2f ; lvl1->carry p50 %.2f p90 %.2f" % (
+                tuple(np.percentile(w1, [50, 90])) + tuple(np.percentile(w2, [50, 90]))))
 
 
 if __name__ == "__main__":
