@@ -122,8 +122,8 @@ static Layout layout(const iir_desc_t* d) {
     L.ws_clear = o;
     L.ws_sent = o;
     for (int l = 0; l < L.nlev; ++l) { L.ws_agg[l] = o; o += al256(d->batch * L.nblk[l] * M * 8); }
-    L.ws_bank = o - L.ws_sent;                           // two banks of look-back slots (epoch parity)
-    o += L.ws_bank;
+    L.ws_bank = o - L.ws_sent;                           // two banks of look-back slots (epoch parity),
+    o += 3 * L.ws_bank;                                  // for the forward and for the backward
     L.ws_sent_bytes = o - L.ws_sent;
     L.ws_part = o; o += al256(L.ntot * (2 * M + 1) * 8);
     L.ws_part2 = o; o += al256(L.ngroups * (2 * M + 1) * 8);
@@ -154,14 +154,17 @@ static iir_status_t run_lti_any(LtiCall& c) {
 }
 
 static unsigned long long* g_trace = nullptr;
-static CarryWs carry_ws(const Layout& L, char* w) {
+// The forward and the backward have separate counters and slot banks, so a
+// backward launched with PDL may run its dy-only phases while the forward ends.
+static CarryWs carry_ws(const Layout& L, char* w, bool bwd) {
     CarryWs c{};
-    c.ticket = reinterpret_cast<unsigned*>(w + L.ws_ticket);
-    c.done = reinterpret_cast<unsigned*>(w + L.ws_done);
-    c.epoch = reinterpret_cast<unsigned*>(w + L.ws_epoch);
+    const size_t co = bwd ? 16 : 0, bo = bwd ? 2 * L.ws_bank : 0;
+    c.ticket = reinterpret_cast<unsigned*>(w + L.ws_ticket + co);
+    c.done = reinterpret_cast<unsigned*>(w + L.ws_done + co);
+    c.epoch = reinterpret_cast<unsigned*>(w + L.ws_epoch + co);
     c.bank = (int64_t)(L.ws_bank / 8);
     for (int l = 0; l < MAX_LEVELS; ++l) {
-        c.agg[l] = l < L.nlev ? reinterpret_cast<double*>(w + L.ws_agg[l]) : nullptr;
+        c.agg[l] = l < L.nlev ? reinterpret_cast<double*>(w + L.ws_agg[l] + bo) : nullptr;
         c.nblk[l] = L.nblk[l];
     }
     c.nlev = L.nlev;
@@ -234,7 +237,7 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     fa.u = d->form == IIR_DF2 ? t + L.tp_u : nullptr;
     fa.tab = reinterpret_cast<const double*>(t + L.tp_tab);
     fa.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
-    fa.cw = carry_ws(L, w);
+    fa.cw = carry_ws(L, w, false);
     fa.B = d->batch; fa.Tlen = d->length; fa.ntiles = (int)L.ntiles; fa.vec = vec;
     fa.trace = g_trace;
     fa.span = g_trace == nullptr ? nullptr : g_trace + L.ntot * 16 + 2;   // [prep][fwd][bwd]
@@ -282,7 +285,7 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     ba.want_coef = (grad_b != nullptr || grad_a != nullptr);
     ba.tab = reinterpret_cast<const double*>(t + L.tp_tab);
     ba.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
-    ba.cw = carry_ws(L, w);
+    ba.cw = carry_ws(L, w, true);
     ba.B = d->batch; ba.Tlen = d->length; ba.ntiles = (int)L.ntiles; ba.vec = vec;
     ba.trace = g_trace;
     ba.span = g_trace == nullptr ? nullptr : g_trace + L.ntot * 16 + 4;

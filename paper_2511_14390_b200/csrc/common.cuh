@@ -52,6 +52,22 @@ __device__ __forceinline__ void stg_stream(double2* p, double2 v) {
     asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" :: "l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
+// Loads of data another pass just pulled into L2 (no L1 allocation).
+__device__ __forceinline__ float4 ldg_l2(const float4* p) {
+    float4 r;
+    asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double2 ldg_l2(const double2* p) {
+    double2 r;
+    asm volatile("ld.global.cg.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+// Bulk prefetch of [p, p + bytes) into L2 (16 B aligned, bytes a multiple of 16).
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
+
 // Look-back status words: release / acquire at GPU scope.
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     unsigned v;

@@ -664,6 +664,7 @@ struct Smem {
     static constexpr int PTH = pidx<T>(TS + HALO);       // padded tile with u history
     static constexpr size_t tab_bytes = ((size_t)Tab<M>::SMALL * 8 + 15) / 16 * 16;
     static constexpr size_t fwd(int form) { return tab_bytes + (size_t)(PT + (form == 0 ? PT : 0)) * sizeof(T); }
+    static constexpr size_t bwd_tdf() { return tab_bytes + (size_t)PT * sizeof(T); }
     static constexpr size_t bwd(int form) {
         return tab_bytes + (size_t)(PT + PTH + (form == 1 ? PT : 0)) * sizeof(T);
     }
@@ -677,6 +678,7 @@ struct Smem {
 // high-order instantiations, whose occupancy is otherwise register-bound).
 template <int M> constexpr int fwd_min_blocks() { return M <= 2 ? 8 : (M <= 4 ? 6 : 4); }
 template <int M> constexpr int bwd_min_blocks() { return M <= 4 ? 4 : 3; }
+template <int M> constexpr int bwd_tdf_min_blocks() { return M <= 2 ? 8 : (M <= 4 ? 6 : 4); }
 
 template <typename T, int M, int FORM>
 __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const LtiFwdArgs p) {
@@ -705,6 +707,9 @@ __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const 
     // the power tables come from the prologue kernel (PDL): wait, then stage them
     // asynchronously so that their load overlaps the tile's and the local pass
     pdl_wait();
+    // the prologue has completed: a dependent backward may start (it reads the
+    // tables, never this kernel's outputs, before its own griddepcontrol.wait)
+    pdl_launch_dependents();
     const double* tb = p.tab + seq * p.tab_stride;
     stage_small_async<M>(st, tb);
     cp_async_commit();
@@ -840,6 +845,68 @@ __device__ __forceinline__ void bwd_load_u(const LtiBwdArgs& p, int64_t seq, int
     }
 }
 
+// a8 (fused): the CTA's fp64 partial sums (s_red, per warp) -> per-tile row ->
+// group of 32 tiles -> set -> chain rule.  SHARED groups are consecutive tiles
+// in scan order (they complete, and are reduced, while the kernel runs);
+// PER_SEQ groups are a sequence's tiles.  Fixed reduction order throughout.
+template <typename T, int M, int FORM>
+__device__ __forceinline__ void bwd_finalize(const LtiBwdArgs& p, unsigned tk, int64_t seq, int jt,
+                                             const double* __restrict__ tb, const double (*s_red)[2 * M + 1]) {
+    constexpr int NG = 2 * M + 1;
+    __shared__ double s_G[NG];
+    __shared__ unsigned s_fin;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // fused a8: group of 32 tiles -> group sum; last group of the set -> chain rule.
+    // SHARED groups are consecutive tiles in scan order (they complete, and are
+    // reduced, while the kernel runs); PER_SEQ groups are a sequence's tiles.
+    const bool shared = p.ncoef == 1;
+    const int64_t per_set = shared ? p.B * p.ntiles : p.ntiles;
+    const int64_t cset = shared ? 0 : seq;
+    const int64_t li = shared ? (int64_t)tk : jt;                  // index within the set
+    const int64_t gi = li >> 5;
+    const int64_t ngroups = (per_set + 31) >> 5;
+    const int gsize = (int)min((int64_t)32, per_set - (gi << 5));
+    double* part = p.partial + cset * per_set * NG;
+    double* part2 = p.partial2 + cset * ngroups * NG;
+    if (tid < NG) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) s += s_red[w][tid];
+        __stcg(part + li * NG + tid, s);
+        __threadfence();
+    }
+    __syncthreads();
+    IIRG_TRACE(p.trace, tk, 8);
+    if (tid == 0) s_fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
+    __syncthreads();
+    if (s_fin) {                                   // last tile of its group
+        __threadfence();
+        reduce_rows<NG>(part + (gi << 5) * NG, gsize, part2 + gi * NG, lane, warp);
+        __threadfence();
+        __syncthreads();
+        IIRG_TRACE(p.trace, tk, 9);
+        if (tid == 0) {
+            p.gcnt[cset * ngroups + gi] = 0u;
+            s_fin = (atomicAdd(p.scnt + cset, 1u) == (unsigned)ngroups - 1u) ? 2u : 0u;
+        }
+        __syncthreads();
+        if (s_fin == 2u) {                          // last group of the set
+            __threadfence();
+            IIRG_TRACE(p.trace, tk, 12);
+            reduce_rows<NG>(part2, ngroups, s_G, lane, warp);
+            __syncthreads();
+            IIRG_TRACE(p.trace, tk, 13);
+            if (tid == 0) {
+                chain_rule<T, M, FORM>(s_G, tb,
+                                       p.gb == nullptr ? nullptr : static_cast<T*>(p.gb) + cset * (M + 1),
+                                       p.ga == nullptr ? nullptr : static_cast<T*>(p.ga) + cset * (M + 1));
+                p.scnt[cset] = 0u;
+                IIRG_TRACE(p.trace, tk, 14);
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Backward: a5-a8.  Tiles are aligned to the END of each sequence and taken in
 // ticket order last to first; inside a tile thread t owns chunk NT-1-t, walked
@@ -859,8 +926,6 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
     __shared__ double s_agg[NW][M];
     __shared__ double s_xw[NW][M];
     __shared__ double s_red[NW][NG];
-    __shared__ double s_G[NG];
-    __shared__ unsigned s_fin;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned tk = tile_order(p.cw.ticket);
@@ -1024,57 +1089,210 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
     if (p.gx != nullptr) tile_store<T, TS>(static_cast<T*>(p.gx) + roff, dys, p0, p.Tlen, p.vec);
     IIRG_TRACE(p.trace, tk, 5);
 
-    if (p.want_coef) {
-        // fused a8: group of 32 tiles -> group sum; last group of the set -> chain rule.
-        // SHARED groups are consecutive tiles in scan order (they complete, and are
-        // reduced, while the kernel runs); PER_SEQ groups are a sequence's tiles.
-        const bool shared = p.ncoef == 1;
-        const int64_t per_set = shared ? p.B * p.ntiles : p.ntiles;
-        const int64_t cset = shared ? 0 : seq;
-        const int64_t li = shared ? (int64_t)tk : jt;                  // index within the set
-        const int64_t gi = li >> 5;
-        const int64_t ngroups = (per_set + 31) >> 5;
-        const int gsize = (int)min((int64_t)32, per_set - (gi << 5));
-        double* part = p.partial + cset * per_set * NG;
-        double* part2 = p.partial2 + cset * ngroups * NG;
-        if (tid < NG) {
-            double s = 0.0;
+    if (p.want_coef) bwd_finalize<T, M, FORM>(p, tk, seq, jt, tb, s_red);
+    IIRG_TRACE(p.trace, tk, 10);
+    cta_exit(cw, ep, gridDim.x);
+    IIRG_TRACE(p.trace, tk, 11);
+    span_exit(p.span);
+}
+
+// ---------------------------------------------------------------------------
+// TDF backward (a5-a8) with a single shared-memory tile.  The TDF adjoint state
+// is a shift register: dz(n)[i] = g(n+i) with g(n) = dz(n)[0] (Eq.7 with
+// A_f^T = A, C_f = e1), so after the carry the emit pass only has to produce
+// g(n) (written in place of dy), and a second, coalesced pass forms
+//   dx(n) = b0 dy(n) + sum_i c_i g(n+i)                       (Eq.8)
+//   Gx[i] = sum_n g(n+i) x(n),  Gy[i] = sum_n g(n+i) y(n),  Gd = sum dy x   (Eqs.6, 9)
+// reading dy, x, y straight from global memory (x, y are prefetched into L2 at
+// tile start) and storing dx straight to global memory.  The tile's shared
+// footprint drops from three tiles to one, so about twice as many tiles are in
+// flight.  g beyond the tile end comes from the carry: g(p0+TS+j) = X[j+1].
+template <typename T, int M>
+__global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kernel(const LtiBwdArgs p) {
+    constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
+    constexpr int NG = 2 * M + 1;
+    using V = typename Vec<T>::type;
+    using TB = Tab<M>;
+    using SM = Smem<T, M>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* st = reinterpret_cast<double*>(smem_raw);
+    T* gs = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);    // dy -> g in place
+    __shared__ double s_agg[NW][M];
+    __shared__ double s_xw[NW][M];
+    __shared__ double s_red[NW][NG];
+    __shared__ T s_halo[8];                                     // g(p0 + TS + j), j < M - 1
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned tk = tile_order(p.cw.ticket);
+    span_enter(p.span);
+    CarryWs cw = p.cw;
+    const unsigned ep = carry_bank(cw);
+    const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
+    const int jr = (int)(tk / (unsigned long long)p.B);          // 0 = last tile in time
+    const int jt = p.ntiles - 1 - jr;
+    const int64_t p0 = p.Tlen - (int64_t)(jr + 1) * TS;          // may be < 0 (first tile)
+    const double* tb = p.tab + seq * p.tab_stride;
+    const int64_t roff = seq * p.Tlen;
+    const T* gyrow = static_cast<const T*>(p.gy) + roff;
+    const T* xrow = static_cast<const T*>(p.x) + roff;
+    const T* yrow = static_cast<const T*>(p.y) + roff;
+    IIRG_TRACE(p.trace, tk, 0);
+
+    if (p.gy != nullptr) tile_load_async<T, TS>(gs, gyrow, p0, p.Tlen, p.vec);
+    else for (int e = tid; e < TS; e += NT) gs[pidx<T>(e)] = T(0);
+    cp_async_commit();
+    const int64_t pa = p0 < 0 ? 0 : p0;              // x, y are read after the carry: pull them into L2
+    const unsigned pbytes = (unsigned)((p0 + TS - pa) * (int64_t)sizeof(T));
+    if (tid == 0 && p.vec) prefetch_l2_bulk(xrow + pa, pbytes);
+    stage_small_async<M>(st, tb);                    // tables live in the tape (written by the forward)
+    cp_async_commit();
+    rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
+    T bc[M + 1], ac[M + 1], cc[M];
+    load_coefs<T, M>(tb, bc, ac, cc);
+    cp_async_wait<0>();
+    __syncthreads();
+
+    const int c = NT - 1 - tid;          // chunk index within the tile (time order)
+    const int s0 = c * L;
+    // a5: local adjoint pass from the zero state, walking the chunk backwards.
+    T d[M];
 #pragma unroll
-            for (int w = 0; w < NW; ++w) s += s_red[w][tid];
-            __stcg(part + li * NG + tid, s);
-            __threadfence();
+    for (int i = 0; i < M; ++i) d[i] = T(0);
+#pragma unroll
+    for (int g = L / W - 1; g >= 0; --g) {
+        const V dv = *reinterpret_cast<const V*>(gs + pidx<T>(s0 + g * W));
+#pragma unroll
+        for (int e = W - 1; e >= 0; --e) adj_tdf_step<T, M>(d, vget(dv, e), ac);
+    }
+    IIRG_TRACE(p.trace, tk, 1);
+    // a6: carries (transposed powers), tiles last -> first.
+    double S[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) S[i] = (double)d[i];
+    warp_scan<M, true>(st, lane, S);
+    double E[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) { E[i] = shfl_up_d(S[i], 1); if (lane == 0) E[i] = 0.0; }
+    if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double Jex[M], G[M], X0[M], X[M];
+        block_scan<M, true>(st, lane, s_agg, Jex, G);
+        const T* gzf = static_cast<const T*>(p.gzf);
+#pragma unroll
+        for (int i = 0; i < M; ++i) X0[i] = (gzf != nullptr && jr == 0) ? (double)gzf[seq * M + i] : 0.0;
+        IIRG_TRACE(p.trace, tk, 2);
+        tile_carry<M, true>(tb, lane, jr, seq, X0, G, cw, X, p.trace, tk);
+        IIRG_TRACE(p.trace, tk, 3);
+        if (lane < NW) {
+            double xw[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) xw[i] = Jex[i];
+            mv_acc_lane_s<M, true>(st + TB::PWT, NW, lane, X, xw);
+#pragma unroll
+            for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
         }
-        __syncthreads();
-        IIRG_TRACE(p.trace, tk, 8);
-        if (tid == 0) s_fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
-        __syncthreads();
-        if (s_fin) {                                   // last tile of its group
-            __threadfence();
-            reduce_rows<NG>(part + (gi << 5) * NG, gsize, part2 + gi * NG, lane, warp);
-            __threadfence();
-            __syncthreads();
-            IIRG_TRACE(p.trace, tk, 9);
-            if (tid == 0) {
-                p.gcnt[cset * ngroups + gi] = 0u;
-                s_fin = (atomicAdd(p.scnt + cset, 1u) == (unsigned)ngroups - 1u) ? 2u : 0u;
-            }
-            __syncthreads();
-            if (s_fin == 2u) {                          // last group of the set
-                __threadfence();
-                IIRG_TRACE(p.trace, tk, 12);
-                reduce_rows<NG>(part2, ngroups, s_G, lane, warp);
-                __syncthreads();
-                IIRG_TRACE(p.trace, tk, 13);
-                if (tid == 0) {
-                    chain_rule<T, M, FORM>(s_G, tb,
-                                           p.gb == nullptr ? nullptr : static_cast<T*>(p.gb) + cset * (M + 1),
-                                           p.ga == nullptr ? nullptr : static_cast<T*>(p.ga) + cset * (M + 1));
-                    p.scnt[cset] = 0u;
-                    IIRG_TRACE(p.trace, tk, 14);
-                }
-            }
+        if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j + 1 < M; ++j) s_halo[j] = (T)X[j + 1];
         }
     }
+    __syncthreads();
+    {
+        double xw[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
+        mv_acc_lane<M, true>(tb + TB::PLT, 32, lane, xw, E);
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i) d[i] = (T)E[i];
+    // a7, pass A: re-run with the exact carry, write g(n) = dz(n)[0] over dy(n).
+    // The chunk holding n = 0 also yields grad_zi = dz(-1) (Eq.9, A.3).
+    const bool has_zero = p.gzi != nullptr && p0 + s0 <= 0 && p0 + s0 + L > 0;
+#pragma unroll
+    for (int g = L / W - 1; g >= 0; --g) {
+        V dv = *reinterpret_cast<const V*>(gs + pidx<T>(s0 + g * W));
+#pragma unroll
+        for (int e = W - 1; e >= 0; --e) {
+            const T dy = vget(dv, e);
+            vset(dv, e, d[0]);
+            adj_tdf_step<T, M>(d, dy, ac);           // d <- dz(n-1)
+            if (has_zero && p0 + s0 + g * W + e == 0) {
+                T* gzi = static_cast<T*>(p.gzi) + seq * M;
+#pragma unroll
+                for (int i = 0; i < M; ++i) gzi[i] = d[i];
+            }
+        }
+        *reinterpret_cast<V*>(gs + pidx<T>(s0 + g * W)) = dv;
+    }
+    // y is the forward's output: with PDL this kernel may have started while the
+    // forward was still running (its dy-only phases above overlap it)
+    pdl_wait();
+    if (tid == 0 && p.vec) prefetch_l2_bulk(yrow + pa, pbytes);
+    __syncthreads();
+    IIRG_TRACE(p.trace, tk, 4);
+    // a7, pass B: coalesced.  Thread t owns the W-sample groups q = t + NT k.
+    auto gat = [&](int m) -> T { return m < TS ? gs[pidx<T>(m)] : s_halo[m - TS]; };
+    T Gs[NG];
+#pragma unroll
+    for (int k = 0; k < NG; ++k) Gs[k] = T(0);
+    T* gxrow = p.gx == nullptr ? nullptr : static_cast<T*>(p.gx) + roff;
+#pragma unroll 2
+    for (int k = 0; k < L / W; ++k) {
+        const int n0 = (tid + NT * k) * W;             // tile-local
+        const int64_t pos = p0 + n0;
+        V xv, yv, dyv;
+        if (p.vec && pos >= 0) {
+            xv = ldg_l2(reinterpret_cast<const V*>(xrow + pos));
+            yv = ldg_l2(reinterpret_cast<const V*>(yrow + pos));
+            dyv = p.gy != nullptr ? ldg_l2(reinterpret_cast<const V*>(gyrow + pos)) : V{};
+        } else {
+#pragma unroll
+            for (int e = 0; e < W; ++e) {
+                const bool in = pos + e >= 0;
+                vset(xv, e, in ? xrow[pos + e] : T(0));
+                vset(yv, e, in ? yrow[pos + e] : T(0));
+                vset(dyv, e, (in && p.gy != nullptr) ? gyrow[pos + e] : T(0));
+            }
+        }
+        T gw[W + M - 1];
+#pragma unroll
+        for (int j = 0; j < W + M - 1; ++j) gw[j] = gat(n0 + j);
+        V dxv;
+#pragma unroll
+        for (int e = 0; e < W; ++e) {
+            const T dy = vget(dyv, e), xx = vget(xv, e), yy = vget(yv, e);
+            T dx = bc[0] * dy;
+#pragma unroll
+            for (int i = 0; i < M; ++i) dx = fma(cc[i], gw[e + i], dx);
+#pragma unroll
+            for (int i = 0; i < M; ++i) { Gs[i] = fma(gw[e + i], xx, Gs[i]); Gs[M + i] = fma(gw[e + i], yy, Gs[M + i]); }
+            Gs[2 * M] = fma(dy, xx, Gs[2 * M]);
+            vset(dxv, e, dx);
+        }
+        if (gxrow != nullptr) {
+            if (p.vec && pos >= 0) stg_stream(reinterpret_cast<V*>(gxrow + pos), dxv);
+            else
+#pragma unroll
+                for (int e = 0; e < W; ++e)
+                    if (pos + e >= 0) gxrow[pos + e] = vget(dxv, e);
+        }
+    }
+    if (p.want_coef) {
+#pragma unroll
+        for (int k = 0; k < NG; ++k) {
+            double s = (double)Gs[k];
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) s_red[warp][k] = s;
+        }
+    }
+    __syncthreads();
+    IIRG_TRACE(p.trace, tk, 5);
+    if (p.want_coef) bwd_finalize<T, M, 1>(p, tk, seq, jt, tb, s_red);
     IIRG_TRACE(p.trace, tk, 10);
     cta_exit(cw, ep, gridDim.x);
     IIRG_TRACE(p.trace, tk, 11);

@@ -37,6 +37,7 @@ struct LtiOps {
             set_smem(lti_prep_kernel<T, M, FORM>, PrepSlots<M>::bytes());
             set_smem(lti_fwd_kernel<T, M, FORM>, SM::fwd(FORM));
             set_smem(lti_bwd_kernel<T, M, FORM>, SM::bwd(FORM));
+            if constexpr (FORM == 1) set_smem(lti_bwd_tdf_kernel<T, M>, SM::bwd_tdf());
         });
     }
     // a1 prologue, then the single-pass scan (PDL: its loads and local pass
@@ -58,7 +59,8 @@ struct LtiOps {
     static iir_status_t backward(const iir_desc_t* d, const Layout& L, const LtiBwdArgs& ba, cudaStream_t st) {
         attrs();
         return launch(K_LTI_BWD, st, [&] {
-            lti_bwd_kernel<T, M, FORM><<<(unsigned)L.ntot, NT, SM::bwd(FORM), st>>>(ba);
+            if constexpr (FORM == 1) launch_pdl(lti_bwd_tdf_kernel<T, M>, (unsigned)L.ntot, NT, SM::bwd_tdf(), st, ba);
+            else lti_bwd_kernel<T, M, FORM><<<(unsigned)L.ntot, NT, SM::bwd(FORM), st>>>(ba);
         });
     }
 };
