@@ -1,3 +1,4 @@
+#include <type_traits>
 // tv.cu -- host side of the per-sample (time-varying) all-pole DF path
 // (IIR_COEF_PER_SAMPLE): layout, dispatch, instantiations.
 #include "host.h"
@@ -38,7 +39,7 @@ Layout tv_layout(const iir_desc_t* d) {
 
 template <typename T, int M, int MODE>
 static void tv_seq_launch(unsigned nseg_tot, const TvArgs& a, cudaStream_t st) {
-    const size_t smem = TvStage<T, M>::bytes(MODE);
+    const size_t smem = TvStage<T, M, MODE>::bytes(MODE);
     static std::once_flag once;
     std::call_once(once, [&] {
         cudaFuncSetAttribute(tv_seq_kernel<T, M, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -51,7 +52,12 @@ template <typename T, int M>
 static iir_status_t tv_fwd_m(const Layout& L, TvArgs& a, cudaStream_t st) {
     const unsigned nseg_tot = (unsigned)L.ntot;
     iir_status_t s = launch(K_TV_PHI, st, [&] {
-        tv_phi_kernel<T, M><<<(nseg_tot + TV_PHI_WARPS - 1) / TV_PHI_WARPS, 32 * TV_PHI_WARPS, 0, st>>>(a);
+        if constexpr (std::is_same<T, float>::value) {
+            const unsigned per = 2 * TV_PHI2_WARPS;          // segments per CTA
+            tv_phi2_kernel<M><<<(nseg_tot + per - 1) / per, 32 * TV_PHI2_WARPS, 0, st>>>(a);
+        } else {
+            tv_phi_kernel<T, M><<<(nseg_tot + TV_PHI_WARPS - 1) / TV_PHI_WARPS, 32 * TV_PHI_WARPS, 0, st>>>(a);
+        }
     });
     if (s != IIR_OK) return s;
     s = launch(K_TV_CHAIN, st, [&] { tv_chain_kernel<T, M, false><<<(unsigned)a.B, 32, 0, st>>>(a); });

@@ -122,6 +122,113 @@ __global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs 
     }
 }
 
+// fp32 variant with paired FMAs (Blackwell FFMA2): each lane carries TWO basis
+// columns as one f32x2 state, the coefficient a_i(n) is a scalar broadcast
+// operand, so one instruction advances two columns; a warp therefore builds two
+// segments at once (half-warp each, (M + 2) / 2 lanes per segment).  Same
+// arithmetic, same order as tv_phi_kernel (bit-identical Phi_k and w_k).
+constexpr int TV_PHI2_WARPS = 2;
+__device__ __forceinline__ unsigned long long pk2(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ float lo2(unsigned long long v) { return __uint_as_float((unsigned)(v & 0xffffffffull)); }
+__device__ __forceinline__ float hi2(unsigned long long v) { return __uint_as_float((unsigned)(v >> 32)); }
+
+template <int M>
+__global__ void __launch_bounds__(32 * TV_PHI2_WARPS) tv_phi2_kernel(const TvArgs p) {
+    static_assert(M + 1 <= 32, "two columns per lane, sixteen lanes per segment");
+    constexpr int CH = 32;                                 // samples per staged chunk
+    constexpr int P = (M + 2) / 2;                         // lanes per segment
+    __shared__ __align__(16) float sa[TV_PHI2_WARPS][2][2][CH * M];
+    __shared__ __align__(16) float sx[TV_PHI2_WARPS][2][2][CH];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int half = lane >> 4, hl = lane & 15;
+    const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+    const int64_t seg = ((int64_t)blockIdx.x * TV_PHI2_WARPS + warp) * 2 + half;
+    if (seg >= p.B * p.nseg) return;                       // whole half-warps only
+    const int64_t seq = seg / p.nseg;
+    const int k = (int)(seg - seq * p.nseg);
+    const int64_t n0 = (int64_t)k * TV_SEG, n1 = min(n0 + TV_SEG, p.T);
+    const float* arow = static_cast<const float*>(p.a) + seq * p.T * M;
+    const float* xrow = static_cast<const float*>(p.x) + seq * p.T;
+    const bool vec = p.vec != 0 && (CH * M) % 4 == 0;
+    float* SA[2] = {sa[warp][half][0], sa[warp][half][1]};
+    float* SX[2] = {sx[warp][half][0], sx[warp][half][1]};
+    auto stage = [&](int64_t c, int b) {
+        const int cnt = (int)min((int64_t)CH, n1 - c);
+        if (vec && cnt == CH) {
+            for (int e = hl * 4; e < CH * M; e += 64) cp_async16(SA[b] + e, arow + c * M + e, 16u);
+        } else {
+            for (int e = hl; e < CH * M; e += 16) SA[b][e] = (e < cnt * M) ? arow[c * M + e] : 0.f;
+        }
+        for (int e = hl; e < CH; e += 16) SX[b][e] = (e < cnt) ? xrow[c + e] : 0.f;
+    };
+    const int j0 = 2 * hl, j1 = 2 * hl + 1;                // this lane's columns (M = the input column)
+    unsigned long long v[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) v[i] = pk2(j0 == i ? 1.f : 0.f, j1 == i ? 1.f : 0.f);
+    stage(n0, 0);
+    cp_async_commit();
+    int b = 0;
+    for (int64_t c = n0; c < n1; c += CH, b ^= 1) {
+        const int cnt = (int)min((int64_t)CH, n1 - c);
+        __syncwarp(hmask);
+        if (c + CH < n1) stage(c + CH, b ^ 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp(hmask);
+        const float* A = SA[b];
+        if (cnt == CH) {
+#pragma unroll 4
+            for (int s2 = 0; s2 < CH; ++s2) {
+                const float xv = SX[b][s2];
+                unsigned long long acc = pk2(j0 == M ? xv : 0.f, j1 == M ? xv : 0.f);
+                float cf[M];
+#pragma unroll
+                for (int q = 0; q < M / 4; ++q) {
+                    const float4 t4 = reinterpret_cast<const float4*>(A + s2 * M)[q];
+                    cf[4 * q] = t4.x; cf[4 * q + 1] = t4.y; cf[4 * q + 2] = t4.z; cf[4 * q + 3] = t4.w;
+                }
+#pragma unroll
+                for (int i = 4 * (M / 4); i < M; ++i) cf[i] = A[s2 * M + i];
+#pragma unroll
+                for (int i = M - 1; i >= 0; --i) acc = ffma2(pk2(-cf[i], -cf[i]), v[i], acc);   // newest term last
+#pragma unroll
+                for (int i = M - 1; i >= 1; --i) v[i] = v[i - 1];
+                v[0] = acc;
+            }
+        } else {                                           // ragged last chunk: exactly cnt samples
+            for (int s2 = 0; s2 < cnt; ++s2) {
+                const float xv = SX[b][s2];
+                unsigned long long acc = pk2(j0 == M ? xv : 0.f, j1 == M ? xv : 0.f);
+#pragma unroll
+                for (int i = M - 1; i >= 0; --i) acc = ffma2(pk2(-A[s2 * M + i], -A[s2 * M + i]), v[i], acc);
+#pragma unroll
+                for (int i = M - 1; i >= 1; --i) v[i] = v[i - 1];
+                v[0] = acc;
+            }
+        }
+    }
+    if (hl < P) {
+        float* ph = static_cast<float*>(p.phi) + seg * M * M;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const float a0 = lo2(v[i]), a1 = hi2(v[i]);
+            if (j0 < M) ph[i * M + j0] = a0;
+            else p.w[seg * M + i] = (double)a0;           // j0 == M: the input column
+            if (j1 < M) ph[i * M + j1] = a1;
+            else if (j1 == M) p.w[seg * M + i] = (double)a1;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Phase 2: per-sequence fp64 chain over the segments (one warp per sequence,
 // lane i = row i).  FWD: s_0 = zi, s_{k+1} = Phi_k s_k + w_k.
@@ -228,19 +335,25 @@ __device__ __forceinline__ void load_row(const T* __restrict__ ar, T (&c)[M]) {
 // the coefficient bytes, and fp64 removes the O(TV_SEG) fp32 rounding growth of
 // a long feedback loop ("TV precision").
 constexpr int TV_SEQ_WARPS = 2;           // warps per CTA (x 32 segments)
-template <typename T> constexpr int tv_chunk() { return 4; }   // samples per staged chunk
-template <typename T>
+enum TvMode { TV_FWD_EMIT = 0, TV_BWD_AGG = 1, TV_BWD_EMIT = 2 };
+// Samples per staged chunk: the coefficient stream is latency-bound (one
+// thread per segment, few warps per SM), so the bytes in flight per lane are
+// what sets the bandwidth; the emit-backward also stages grad_a (its TMA
+// store beats per-lane row stores), so it keeps smaller chunks to stay at the
+// same occupancy.
+template <typename T, int M, int MODE> constexpr int tv_chunk() {
+    return (MODE != TV_BWD_EMIT && M * (int)sizeof(T) <= 128) ? 8 : 4;
+}
+template <typename T, int M, int MODE>
 __device__ __forceinline__ int64_t chunk_start_of(int64_t n0, int c, bool bwd) {
-    constexpr int C = tv_chunk<T>();
+    constexpr int C = tv_chunk<T, M, MODE>();
     return bwd ? n0 + (int64_t)(TV_SEG / C - 1 - c) * C : n0 + (int64_t)c * C;
 }
 
-enum TvMode { TV_FWD_EMIT = 0, TV_BWD_AGG = 1, TV_BWD_EMIT = 2 };
-
-template <typename T, int M>
+template <typename T, int M, int MODE>
 struct TvStage {
     static constexpr int PAD = 16 / (int)sizeof(T);
-    static constexpr int C = tv_chunk<T>();
+    static constexpr int C = tv_chunk<T, M, MODE>();
     static constexpr int ROW = C * M;                   // elements of one segment's chunk
     static constexpr int STRIDE = ROW + PAD;            // smem row stride (elements), 16 B multiple
     static constexpr int NBUF(int mode) { return 2 + (mode == TV_BWD_EMIT ? 1 : 0); }
@@ -252,7 +365,7 @@ struct TvStage {
 template <typename T, int M, int MODE>
 __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs p) {
     using R = double;
-    using ST = TvStage<T, M>;
+    using ST = TvStage<T, M, MODE>;
     constexpr bool BWD = MODE != TV_FWD_EMIT;
     constexpr int C = ST::C;
     constexpr int NCH = TV_SEG / C;
@@ -280,7 +393,7 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
 
     // stage chunk c of every lane's segment into buffer b
     auto stage = [&](int c, int b) {
-        const int64_t cs = chunk_start_of<T>(n0, c, BWD);
+        const int64_t cs = chunk_start_of<T, M, MODE>(n0, c, BWD);
         const int64_t vs = max(cs, n0), ve = min(cs + C, n1);
         const int nv = valid && ve > vs ? (int)(ve - vs) : 0;
         T* dst = myA[b];
@@ -330,7 +443,7 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
         if (bulk) { mbar_wait(&bar[b], phase[b]); phase[b] ^= 1u; }
         __syncwarp();
         const T* my = myA[b];
-        const int64_t cs = chunk_start_of<T>(n0, c, BWD);
+        const int64_t cs = chunk_start_of<T, M, MODE>(n0, c, BWD);
         if constexpr (MODE == TV_BWD_EMIT) {
             if (bulk) bulk_wait_read0();                 // previous grad_a chunk has left smem
             __syncwarp();

@@ -1,0 +1,86 @@
+"""Summarise ncu launch lists (gpu__time_duration + dram bytes per launch) into
+profiles/traffic.json and a per-kernel text table.
+
+    python tools/make_traffic.py gpurun_out/r01b profiles/r01_launches.txt
+
+traffic.json maps workload -> library kernel kind -> mean DRAM bytes per launch
+(read + write), the `roofline.traffic` bench.py reports.  ncu replays every
+launch cold and serialised, so its durations are for the kernel's SHARE of the
+step, not absolute timings."""
+import csv
+import json
+import os
+import re
+import sys
+from collections import OrderedDict, defaultdict
+
+KIND = [(r"lti_prep_kernel", "lti_prep"), (r"lti_fwd_kernel", "lti_fwd"), (r"lti_bwd", "lti_bwd"),
+        (r"tv_phi_kernel", "tv_phi"), (r"tv_chain_kernel", "tv_chain"), (r"tv_seq_kernel<[^,]+, *\d+, *0>", "tv_fwd"),
+        (r"tv_seq_kernel<[^,]+, *\d+, *1>", "tv_bwd_agg"), (r"tv_seq_kernel<[^,]+, *\d+, *2>", "tv_bwd")]
+
+
+def kind_of(name):
+    for pat, k in KIND:
+        if re.search(pat, name):
+            return k
+    return None
+
+
+def parse(path):
+    lines = open(path).read().splitlines()
+    i = next(k for k, l in enumerate(lines) if l.startswith('"ID"'))
+    rows = list(csv.reader(lines[i:]))
+    hdr = rows[0]
+    per = OrderedDict()
+    for r in rows[1:]:
+        x = dict(zip(hdr, r))
+        key = (x["ID"], x["Kernel Name"])
+        v = float(x["Metric Value"].replace(",", ""))
+        unit = x["Metric Unit"]
+        if unit == "usecond":
+            v *= 1e3
+        elif unit == "msecond":
+            v *= 1e6
+        elif unit == "Kbyte":
+            v *= 1e3
+        elif unit == "Mbyte":
+            v *= 1e6
+        elif unit == "Gbyte":
+            v *= 1e9
+        per.setdefault(key, {})[x["Metric Name"]] = v
+    return per
+
+
+def main():
+    src, out_txt = sys.argv[1], sys.argv[2]
+    traffic, lines = {}, []
+    for f in sorted(os.listdir(src)):
+        m = re.match(r"launches_(\w+)\.csv$", f)
+        if not m:
+            continue
+        w = m.group(1)
+        agg = defaultdict(lambda: [0, 0.0, 0.0, 0.0])
+        for (_, name), d in parse(os.path.join(src, f)).items():
+            k = kind_of(name)
+            if k is None:
+                continue
+            a = agg[k]
+            a[0] += 1
+            a[1] += d.get("gpu__time_duration.sum", 0.0)
+            a[2] += d.get("dram__bytes_read.sum", 0.0)
+            a[3] += d.get("dram__bytes_write.sum", 0.0)
+        traffic[w] = {k: (a[2] + a[3]) / a[0] for k, a in agg.items()}
+        tot = sum(a[1] / a[0] for a in agg.values())
+        lines.append(f"== {w}: per launch (mean over {min(a[0] for a in agg.values())}+ launches), ncu cold-cache replay")
+        for k, a in agg.items():
+            n = a[0]
+            lines.append(f"   {k:11s} n={n:3d}  {a[1] / n / 1e3:9.2f} us  share {a[1] / n / tot:6.1%}  "
+                         f"dram read {a[2] / n / 1e6:9.2f} MB  write {a[3] / n / 1e6:9.2f} MB")
+    os.makedirs("profiles", exist_ok=True)
+    json.dump(traffic, open("profiles/traffic.json", "w"), indent=1)
+    open(out_txt, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
