@@ -41,6 +41,7 @@ struct Layout {
     size_t ws_clear = 0;                                   // [0, ws_clear): counters, initialised to 0
     size_t ws_sent = 0, ws_sent_bytes = 0;                 // look-back slots, initialised to all-ones (NaN)
     size_t ws_agg[MAX_LEVELS] = {0, 0, 0, 0}, ws_part = 0, ws_part2 = 0, ws_bytes = 0;
+    size_t ws_psi = 0, ws_omega = 0, ws_sgrp = 0;          // TV two-level chain
     size_t tp_tab = 0, tp_u = 0, tp_extra = 0, tp_bytes = 0;
 };
 

@@ -30,6 +30,11 @@ Layout tv_layout(const iir_desc_t* d) {
     L.ws_clear = 0;                                        // no counters: nothing to initialise
     L.ws_part = o; o += al256((size_t)L.ntot * M * 8);     // w: segment aggregates
     L.ws_part2 = o; o += al256((size_t)L.ntot * M * 8);    // carry: entering states
+    const int64_t ngrp = (L.ntiles + TV_GS - 1) / TV_GS;
+    L.ngroups = ngrp;
+    L.ws_psi = o; o += al256((size_t)d->batch * ngrp * M * M * 8);
+    L.ws_omega = o; o += al256((size_t)d->batch * ngrp * M * 8);
+    L.ws_sgrp = o; o += al256((size_t)d->batch * ngrp * M * 8);
     L.ws_bytes = o;
     L.tp_tab = 0;
     L.tp_bytes = al256((size_t)L.ntot * M * M * ts);       // Phi_k per segment (reused by the backward)
@@ -48,6 +53,22 @@ static void tv_seq_launch(unsigned nseg_tot, const TvArgs& a, cudaStream_t st) {
     tv_seq_kernel<T, M, MODE><<<(nseg_tot + per - 1) / per, per, smem, st>>>(a);
 }
 
+// phase 2 (both directions): group maps, chain over the groups, expansion
+template <typename T, int M, bool BWD>
+static iir_status_t tv_chain2(const TvArgs& a, const void* x0, cudaStream_t st) {
+    const unsigned ng = (unsigned)(a.B * a.ngrp);
+    const unsigned blocks = (ng + TV_GRP_WARPS - 1) / TV_GRP_WARPS;
+    iir_status_t s = launch(K_TV_CHAIN, st, [&] {
+        tv_group_kernel<T, M, BWD><<<blocks, 32 * TV_GRP_WARPS, 0, st>>>(a);
+    });
+    if (s != IIR_OK) return s;
+    s = launch(K_TV_CHAIN, st, [&] {
+        tv_groupchain_kernel<M, BWD><<<(unsigned)a.B, 32, 0, st>>>(a, x0, (int)sizeof(T));
+    });
+    if (s != IIR_OK) return s;
+    return launch(K_TV_CHAIN, st, [&] { tv_expand_kernel<T, M, BWD><<<blocks, 32 * TV_GRP_WARPS, 0, st>>>(a); });
+}
+
 template <typename T, int M>
 static iir_status_t tv_fwd_m(const Layout& L, TvArgs& a, cudaStream_t st) {
     const unsigned nseg_tot = (unsigned)L.ntot;
@@ -60,7 +81,7 @@ static iir_status_t tv_fwd_m(const Layout& L, TvArgs& a, cudaStream_t st) {
         }
     });
     if (s != IIR_OK) return s;
-    s = launch(K_TV_CHAIN, st, [&] { tv_chain_kernel<T, M, false><<<(unsigned)a.B, 32, 0, st>>>(a); });
+    s = tv_chain2<T, M, false>(a, a.zi, st);
     if (s != IIR_OK) return s;
     return launch(K_TV_FWD, st, [&] { tv_seq_launch<T, M, TV_FWD_EMIT>(nseg_tot, a, st); });
 }
@@ -70,7 +91,7 @@ static iir_status_t tv_bwd_m(const Layout& L, TvArgs& a, cudaStream_t st) {
     const unsigned nseg_tot = (unsigned)L.ntot;
     iir_status_t s = launch(K_TV_BWD_AGG, st, [&] { tv_seq_launch<T, M, TV_BWD_AGG>(nseg_tot, a, st); });
     if (s != IIR_OK) return s;
-    s = launch(K_TV_CHAIN, st, [&] { tv_chain_kernel<T, M, true><<<(unsigned)a.B, 32, 0, st>>>(a); });
+    s = tv_chain2<T, M, true>(a, a.gzf, st);
     if (s != IIR_OK) return s;
     return launch(K_TV_BWD, st, [&] { tv_seq_launch<T, M, TV_BWD_EMIT>(nseg_tot, a, st); });
 }
@@ -101,6 +122,10 @@ iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* a, con
     ta.carry = reinterpret_cast<double*>(ws + L.ws_part2);
     ta.B = d->batch; ta.T = d->length; ta.nseg = (int)L.ntiles;
     ta.vec = tv_vec(d, a);
+    ta.psi = reinterpret_cast<double*>(ws + L.ws_psi);
+    ta.omega = reinterpret_cast<double*>(ws + L.ws_omega);
+    ta.sgrp = reinterpret_cast<double*>(ws + L.ws_sgrp);
+    ta.ngrp = (int)L.ngroups;
     return d->dtype == IIR_F64 ? tv_dispatch<double>(true, d->order, L, ta, st)
                                : tv_dispatch<float>(true, d->order, L, ta, st);
 }
@@ -116,6 +141,10 @@ iir_status_t tv_backward(const iir_desc_t* d, const Layout& L, const void* gy, c
     ta.carry = reinterpret_cast<double*>(ws + L.ws_part2);
     ta.B = d->batch; ta.T = d->length; ta.nseg = (int)L.ntiles;
     ta.vec = tv_vec(d, a) && (reinterpret_cast<uintptr_t>(ga) & 15u) == 0;
+    ta.psi = reinterpret_cast<double*>(ws + L.ws_psi);
+    ta.omega = reinterpret_cast<double*>(ws + L.ws_omega);
+    ta.sgrp = reinterpret_cast<double*>(ws + L.ws_sgrp);
+    ta.ngrp = (int)L.ngroups;
     return d->dtype == IIR_F64 ? tv_dispatch<double>(false, d->order, L, ta, st)
                                : tv_dispatch<float>(false, d->order, L, ta, st);
 }

@@ -11,7 +11,8 @@
 // and zero-state response w_k are built by one warp, lane j propagating the
 // basis state e_j (lane M propagates x from the zero state): M^2 FMA per sample,
 // the price of a matrix-valued scan element.  A per-sequence fp64
-// chain s_{k+1} = Phi_k s_k + w_k gives every segment's entering state, and one
+// chain s_{k+1} = Phi_k s_k + w_k (two-level: groups of TV_GS segments) gives
+// every segment's entering state, and one
 // thread per segment re-runs the plain recursion from it.  The backward reuses
 // Phi_k^T from the tape (the adjoint segment map is exactly Phi_k^T).
 #pragma once
@@ -25,6 +26,9 @@ constexpr int TV_PHI_WARPS = 4;      // warps (segments) per CTA of the Phi kern
 template <typename T> constexpr int tv_ch() { return sizeof(T) == 4 ? 32 : 16; }   // staged chunk (Phi kernel)
 constexpr int TV_U = 8;              // unroll of the sequential recursions
 
+constexpr int TV_GS = 16;            // segments per group of the two-level chain
+constexpr int TV_GRP_WARPS = 2;      // warps (groups) per CTA of the group / expansion kernels
+
 struct TvArgs {
     const void* a; const void* x; const void* zi;     // a: (B, T, M)
     void* y; void* zf;                                // forward outputs
@@ -35,6 +39,10 @@ struct TvArgs {
     double* carry;                                    // ws: [B][nseg][M] entering states
     int64_t B, T; int nseg;
     int vec;                                          // rows 16 B aligned and M % (16 / sizeof(T)) == 0
+    double* psi;                                      // ws: [B][ngrp][M][M] group transitions
+    double* omega;                                    // ws: [B][ngrp][M] group zero-state responses
+    double* sgrp;                                     // ws: [B][ngrp][M] states entering each group
+    int ngrp;
 };
 
 // ---------------------------------------------------------------------------
@@ -230,72 +238,172 @@ __global__ void __launch_bounds__(32 * TV_PHI2_WARPS) tv_phi2_kernel(const TvArg
 }
 
 // ---------------------------------------------------------------------------
-// Phase 2: per-sequence fp64 chain over the segments (one warp per sequence,
-// lane i = row i).  FWD: s_0 = zi, s_{k+1} = Phi_k s_k + w_k.
-// BWD: d_{nseg-1} = grad_zf, d_{k-1} = Phi_k^T d_k + w_k.  carry[k] = entering state.
-// Phi matrices in flight in the chain kernel (<= ~40 KB of static shared memory)
-template <typename T, int M> constexpr int tv_ring() {
-    return (int)(40960 / (M * M * sizeof(T))) < 2 ? 2 : ((int)(40960 / (M * M * sizeof(T))) > 8 ? 8 : (int)(40960 / (M * M * sizeof(T))));
+// Two-level chain (replaces the serial per-sequence chain over all segments).
+// Segments are grouped by TV_GS in chain order (FWD: increasing k, BWD:
+// decreasing k).  (1) tv_group_kernel, one warp per group: the group map
+// Psi_g = Phi_last .. Phi_first (BWD: transposes) and zero-state response
+// omega_g, fp64;  (2) tv_groupchain_kernel, one warp per sequence:
+// S_{g+1} = Psi_g S_g + omega_g over the groups;  (3) tv_expand_kernel, one
+// warp per group: carry[k] for the group's segments from S_g.  The serial
+// depth drops from nseg hops to nseg / TV_GS + TV_GS hops.
+template <typename T, int M>
+struct TvPhiBuf {                                       // per-warp double buffer of one Phi_k (T, M x M)
+    static constexpr int MM = M * M;
+    static constexpr int E = 16 / (int)sizeof(T);
+    static constexpr int SLOT = (MM + E - 1) / E * E;   // elements, 16 B multiple
+};
+template <typename T, int M>
+__device__ __forceinline__ void tv_load_phi(T* dst, const T* src, int lane, bool vec) {
+    using PB = TvPhiBuf<T, M>;
+    if (vec && (PB::MM % PB::E) == 0) {
+        for (int e = lane * PB::E; e < PB::MM; e += 32 * PB::E) cp_async16(dst + e, src + e, 16u);
+    } else {
+        for (int e = lane; e < PB::MM; e += 32) dst[e] = src[e];
+    }
 }
 
 template <typename T, int M, bool BWD>
-__global__ void __launch_bounds__(32) tv_chain_kernel(const TvArgs p) {
-    constexpr int TV_RING = tv_ring<T, M>();
+__global__ void __launch_bounds__(32 * TV_GRP_WARPS) tv_group_kernel(const TvArgs p) {
+    using PB = TvPhiBuf<T, M>;
+    __shared__ __align__(16) T sphi[TV_GRP_WARPS][2][PB::SLOT];
+    __shared__ double som[TV_GRP_WARPS][M];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gid = (int64_t)blockIdx.x * TV_GRP_WARPS + warp;
+    if (gid >= p.B * p.ngrp) return;
+    const int64_t seq = gid / p.ngrp;
+    const int g = (int)(gid - seq * p.ngrp);
+    const int k0 = g * TV_GS, k1 = min(k0 + TV_GS, p.nseg), nk = k1 - k0;
+    const T* phi = static_cast<const T*>(p.phi) + seq * p.nseg * PB::MM;
+    const double* wv = p.w + seq * p.nseg * M;
+    const bool vec = (reinterpret_cast<uintptr_t>(p.phi) & 15u) == 0;
+    auto kof = [&](int q) { return BWD ? k1 - 1 - q : k0 + q; };
+    double col[M];                                       // lane j: column j of Psi
+#pragma unroll
+    for (int i = 0; i < M; ++i) col[i] = (i == lane) ? 1.0 : 0.0;
+    double om = 0.0;                                     // lane i: omega_i
+    tv_load_phi<T, M>(sphi[warp][0], phi + (int64_t)kof(0) * PB::MM, lane, vec);
+    cp_async_commit();
+    for (int q = 0; q < nk; ++q) {
+        const int k = kof(q), b = q & 1;
+        if (q + 1 < nk) tv_load_phi<T, M>(sphi[warp][b ^ 1], phi + (int64_t)kof(q + 1) * PB::MM, lane, vec);
+        cp_async_commit();
+        const double wk = lane < M ? wv[(int64_t)k * M + lane] : 0.0;
+        if (lane < M) som[warp][lane] = om;
+        cp_async_wait<1>();
+        __syncwarp();
+        const T* P = sphi[warp][b];
+        if (lane < M) {
+            double nc[M];
+#pragma unroll
+            for (int i = 0; i < M; ++i) {                // Psi <- Phi Psi  (BWD: Phi^T Psi)
+                double acc = 0.0;
+#pragma unroll
+                for (int l = 0; l < M; ++l) acc = fma((double)(BWD ? P[l * M + i] : P[i * M + l]), col[l], acc);
+                nc[i] = acc;
+            }
+#pragma unroll
+            for (int i = 0; i < M; ++i) col[i] = nc[i];
+            double a = wk;                               // omega <- Phi omega + w_k
+#pragma unroll
+            for (int l = 0; l < M; ++l) a = fma((double)(BWD ? P[l * M + lane] : P[lane * M + l]), som[warp][l], a);
+            om = a;
+        }
+        __syncwarp();
+    }
+    if (lane < M) {
+        double* ps = p.psi + gid * PB::MM;
+#pragma unroll
+        for (int i = 0; i < M; ++i) ps[i * M + lane] = col[i];
+        p.omega[gid * M + lane] = om;
+    }
+}
+
+// one warp per sequence: S_{g+1} = Psi_g S_g + omega_g (chain order), S_0 = zi / grad_zf
+template <int M, bool BWD>
+__global__ void __launch_bounds__(32) tv_groupchain_kernel(const TvArgs p, const void* x0v, int dsz) {
     constexpr int MM = M * M;
-    constexpr unsigned PB = (unsigned)(MM * sizeof(T));
-    constexpr int PS = (int)((PB + 15) / 16 * 16 / sizeof(T));        // ring slot stride (elements)
-    __shared__ __align__(128) T ring[TV_RING][PS];
-    __shared__ __align__(8) unsigned long long bar[TV_RING];
+    constexpr int RING = 4;
+    __shared__ __align__(16) double ring[RING][MM + (MM & 1)];
     __shared__ double ss[M];
     const int lane = threadIdx.x;
     const int64_t seq = blockIdx.x;
-    const T* x0 = static_cast<const T*>(BWD ? p.gzf : p.zi);
-    double s = (lane < M && x0 != nullptr) ? (double)x0[seq * M + lane] : 0.0;
-    const T* phi = static_cast<const T*>(p.phi) + seq * p.nseg * MM;
-    const double* wv = p.w + seq * p.nseg * M;
-    const bool bulk = (PB % 16 == 0) && ((reinterpret_cast<uintptr_t>(p.phi) & 15u) == 0);
-    if (lane == 0)
-        for (int r = 0; r < TV_RING; ++r) mbar_init(&bar[r], 1);
-    mbar_fence_init();
-    __syncwarp();
-    auto issue = [&](int q) {                    // hop q -> ring slot q % TV_RING
-        if (q >= p.nseg) return;
-        const int k = BWD ? p.nseg - 1 - q : q;
-        const int r = q % TV_RING;
-        if (bulk) {
-            if (lane == 0) {
-                mbar_arrive_expect_tx(&bar[r], PB);
-                bulk_g2s(ring[r], phi + (int64_t)k * MM, PB, &bar[r]);
+    double s = 0.0;
+    if (x0v != nullptr && lane < M)
+        s = dsz == 8 ? static_cast<const double*>(x0v)[seq * M + lane]
+                     : (double)static_cast<const float*>(x0v)[seq * M + lane];
+    const double* psi = p.psi + seq * p.ngrp * MM;
+    auto gof = [&](int q) { return BWD ? p.ngrp - 1 - q : q; };
+    auto issue = [&](int q) {
+        if (q < p.ngrp) {
+            const double* src = psi + (int64_t)gof(q) * MM;
+            if constexpr (MM % 2 == 0) {                 // 16 B pieces stay aligned
+                for (int e = lane * 2; e < MM; e += 64) cp_async16(&ring[q % RING][e], src + e, 16u);
+            } else {
+                for (int e = lane; e < MM; e += 32) ring[q % RING][e] = src[e];
             }
-        } else {
-            for (int e = lane; e < MM; e += 32) ring[r][e] = phi[(int64_t)k * MM + e];
         }
+        cp_async_commit();
     };
-    for (int q = 0; q < TV_RING - 1; ++q) issue(q);
-    for (int q = 0; q < p.nseg; ++q) {
-        const int k = BWD ? p.nseg - 1 - q : q;
-        const int r = q % TV_RING;
-        const double wk = (lane < M) ? wv[(int64_t)k * M + lane] : 0.0;
-        __syncwarp();                            // everyone finished with the slot being refilled
-        issue(q + TV_RING - 1);
-        if (bulk) mbar_wait(&bar[r], (unsigned)((q / TV_RING) & 1));
-        if (lane < M) {
-            p.carry[(seq * p.nseg + k) * M + lane] = s;
-            ss[lane] = s;
-        }
+    for (int q = 0; q < RING - 1; ++q) issue(q);
+    for (int q = 0; q < p.ngrp; ++q) {
+        const int g = gof(q);
         __syncwarp();
-        double acc0 = wk, acc1 = 0.0;
+        issue(q + RING - 1);
+        const double og = lane < M ? p.omega[(seq * p.ngrp + g) * M + lane] : 0.0;
+        if (lane < M) { p.sgrp[(seq * p.ngrp + g) * M + lane] = s; ss[lane] = s; }
+        cp_async_wait<RING - 1>();
+        __syncwarp();
+        double a0 = og, a1 = 0.0;
         if (lane < M) {
-            const T* ph = ring[r];
+            const double* P = ring[q % RING];
 #pragma unroll
             for (int j = 0; j < M; j += 2) {
-                acc0 = fma((double)(BWD ? ph[j * M + lane] : ph[lane * M + j]), ss[j], acc0);
-                if (j + 1 < M)
-                    acc1 = fma((double)(BWD ? ph[(j + 1) * M + lane] : ph[lane * M + j + 1]), ss[j + 1], acc1);
+                a0 = fma(P[lane * M + j], ss[j], a0);
+                if (j + 1 < M) a1 = fma(P[lane * M + j + 1], ss[j + 1], a1);
+            }
+        }
+        s = a0 + a1;
+    }
+}
+
+// one warp per group: carry[k] = state entering segment k, from S_g
+template <typename T, int M, bool BWD>
+__global__ void __launch_bounds__(32 * TV_GRP_WARPS) tv_expand_kernel(const TvArgs p) {
+    using PB = TvPhiBuf<T, M>;
+    __shared__ __align__(16) T sphi[TV_GRP_WARPS][2][PB::SLOT];
+    __shared__ double ss[TV_GRP_WARPS][M];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gid = (int64_t)blockIdx.x * TV_GRP_WARPS + warp;
+    if (gid >= p.B * p.ngrp) return;
+    const int64_t seq = gid / p.ngrp;
+    const int g = (int)(gid - seq * p.ngrp);
+    const int k0 = g * TV_GS, k1 = min(k0 + TV_GS, p.nseg), nk = k1 - k0;
+    const T* phi = static_cast<const T*>(p.phi) + seq * p.nseg * PB::MM;
+    const double* wv = p.w + seq * p.nseg * M;
+    const bool vec = (reinterpret_cast<uintptr_t>(p.phi) & 15u) == 0;
+    auto kof = [&](int q) { return BWD ? k1 - 1 - q : k0 + q; };
+    double s = lane < M ? p.sgrp[gid * M + lane] : 0.0;
+    tv_load_phi<T, M>(sphi[warp][0], phi + (int64_t)kof(0) * PB::MM, lane, vec);
+    cp_async_commit();
+    for (int q = 0; q < nk; ++q) {
+        const int k = kof(q), b = q & 1;
+        if (q + 1 < nk) tv_load_phi<T, M>(sphi[warp][b ^ 1], phi + (int64_t)kof(q + 1) * PB::MM, lane, vec);
+        cp_async_commit();
+        const double wk = lane < M ? wv[(int64_t)k * M + lane] : 0.0;
+        if (lane < M) { p.carry[(seq * p.nseg + k) * M + lane] = s; ss[warp][lane] = s; }
+        cp_async_wait<1>();
+        __syncwarp();
+        double a0 = wk, a1 = 0.0;
+        if (lane < M) {
+            const T* P = sphi[warp][b];
+#pragma unroll
+            for (int j = 0; j < M; j += 2) {
+                a0 = fma((double)(BWD ? P[j * M + lane] : P[lane * M + j]), ss[warp][j], a0);
+                if (j + 1 < M) a1 = fma((double)(BWD ? P[(j + 1) * M + lane] : P[lane * M + j + 1]), ss[warp][j + 1], a1);
             }
         }
         __syncwarp();
-        s = acc0 + acc1;
+        s = a0 + a1;
     }
 }
 
