@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
     };
 
     R v[M];                                      // FWD: v = [y(n-1)..y(n-M)];  BWD: d = dz(n)
-    R yw[M];                                     // BWD_EMIT: yw[i] = y(n-1-i)
+    T yw[M];                                     // BWD_EMIT: yw[i] = y(n-1-i) (data type: grad_a = -g y is one product)
     const T* xrow = static_cast<const T*>(p.x) + seq * p.T;
     const T* gyrow = p.gy == nullptr ? nullptr : static_cast<const T*>(p.gy) + seq * p.T;
     const T* yrow = static_cast<const T*>(p.yin) + seq * p.T;
@@ -534,14 +534,14 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
     T* gxrow = (MODE == TV_BWD_EMIT && p.gx != nullptr) ? static_cast<T*>(p.gx) + seq * p.T : nullptr;
     T* garow = (MODE == TV_BWD_EMIT && p.ga != nullptr) ? static_cast<T*>(p.ga) + seq * p.T * M : nullptr;
     const T* zi = p.zi == nullptr ? nullptr : static_cast<const T*>(p.zi) + seq * M;
-    auto yat = [&](int64_t m) -> R {             // y(m), m >= -M; y(-k) = zi[k-1]
-        if (m >= 0) return (R)__ldg(yrow + m);
-        return zi != nullptr ? (R)zi[-m - 1] : 0.0;
+    auto yat = [&](int64_t m) -> T {             // y(m), m >= -M; y(-k) = zi[k-1]
+        if (m >= 0) return __ldg(yrow + m);
+        return zi != nullptr ? zi[-m - 1] : T(0);
     };
 #pragma unroll
     for (int i = 0; i < M; ++i) {
         v[i] = (MODE == TV_BWD_AGG || !valid) ? 0.0 : p.carry[seg * M + i];
-        yw[i] = (MODE == TV_BWD_EMIT && valid) ? yat(n1 - 2 - i) : 0.0;
+        yw[i] = (MODE == TV_BWD_EMIT && valid) ? yat(n1 - 2 - i) : T(0);
     }
     stage(0, 0);
     for (int c = 0; c < NCH; ++c) {
@@ -590,9 +590,10 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
                 if (in) {
                     const R g = v[0] + (gyrow ? (R)__ldg(gyrow + n) : 0.0);
                     if constexpr (MODE == TV_BWD_EMIT) {
-                        if (gxrow) gxrow[n] = (T)g;
+                        const T gT = (T)g;
+                        if (gxrow) gxrow[n] = gT;
 #pragma unroll
-                        for (int i = 0; i < M; ++i) myG[s2 * M + i] = (T)(-g * yw[i]);
+                        for (int i = 0; i < M; ++i) myG[s2 * M + i] = -gT * yw[i];
 #pragma unroll
                         for (int i = 0; i < M - 1; ++i) yw[i] = yw[i + 1];
                         yw[M - 1] = yat(n - 1 - M);
