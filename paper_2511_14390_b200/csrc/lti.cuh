@@ -1258,9 +1258,20 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
                 vset(dyv, e, (in && p.gy != nullptr) ? gyrow[pos + e] : T(0));
             }
         }
-        T gw[W + M - 1];
+        constexpr int NQ = (2 * W + M - 2) / W;       // W-vectors covering g(n0 .. n0 + W + M - 2)
+        T gw[NQ * W];
 #pragma unroll
-        for (int j = 0; j < W + M - 1; ++j) gw[j] = gat(n0 + j);
+        for (int q = 0; q < NQ; ++q) {                 // 128-bit shared loads: conflict free
+            const int m = n0 + q * W;
+            if (m + W <= TS) {
+                const V t = *reinterpret_cast<const V*>(gs + pidx<T>(m));
+#pragma unroll
+                for (int e = 0; e < W; ++e) gw[q * W + e] = vget(t, e);
+            } else {
+#pragma unroll
+                for (int e = 0; e < W; ++e) gw[q * W + e] = gat(m + e);
+            }
+        }
         V dxv;
 #pragma unroll
         for (int e = 0; e < W; ++e) {

@@ -15,8 +15,9 @@ import sys
 from collections import OrderedDict, defaultdict
 
 KIND = [(r"lti_prep_kernel", "lti_prep"), (r"lti_fwd_kernel", "lti_fwd"), (r"lti_bwd", "lti_bwd"),
-        (r"tv_phi_kernel", "tv_phi"), (r"tv_chain_kernel", "tv_chain"), (r"tv_seq_kernel<[^,]+, *\d+, *0>", "tv_fwd"),
-        (r"tv_seq_kernel<[^,]+, *\d+, *1>", "tv_bwd_agg"), (r"tv_seq_kernel<[^,]+, *\d+, *2>", "tv_bwd")]
+        (r"tv_phi2?_kernel", "tv_phi"), (r"tv_(group|groupchain|expand|chain)_kernel", "tv_chain"), (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?0>", "tv_fwd"),
+        (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?1>", "tv_bwd_agg"),
+        (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?2>", "tv_bwd")]
 
 
 def kind_of(name):
@@ -70,12 +71,14 @@ def main():
             a[2] += d.get("dram__bytes_read.sum", 0.0)
             a[3] += d.get("dram__bytes_write.sum", 0.0)
         traffic[w] = {k: (a[2] + a[3]) / a[0] for k, a in agg.items()}
-        tot = sum(a[1] / a[0] for a in agg.values())
-        lines.append(f"== {w}: per launch (mean over {min(a[0] for a in agg.values())}+ launches), ncu cold-cache replay")
+        steps = agg["tv_fwd"][0] if "tv_fwd" in agg else agg["lti_fwd"][0]
+        tot = sum(a[1] for a in agg.values()) / steps
+        lines.append(f"== {w}: {steps} steps, ncu cold-cache serialised replay; per launch and share of the step")
         for k, a in agg.items():
             n = a[0]
-            lines.append(f"   {k:11s} n={n:3d}  {a[1] / n / 1e3:9.2f} us  share {a[1] / n / tot:6.1%}  "
-                         f"dram read {a[2] / n / 1e6:9.2f} MB  write {a[3] / n / 1e6:9.2f} MB")
+            lines.append(f"   {k:11s} launches/step {n / steps:4.1f}  {a[1] / n / 1e3:9.2f} us/launch  "
+                         f"share {a[1] / steps / tot:6.1%}  dram read {a[2] / n / 1e6:9.2f} MB  "
+                         f"write {a[3] / n / 1e6:9.2f} MB per launch")
     os.makedirs("profiles", exist_ok=True)
     json.dump(traffic, open("profiles/traffic.json", "w"), indent=1)
     open(out_txt, "w").write("\n".join(lines) + "\n")

@@ -32,7 +32,7 @@ if [[ " $WLS " == *" c2 "* ]]; then
   echo "full c2 rc=$?"
 fi
 if [[ " $WLS " == *" c3 "* ]]; then
-  timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k "regex:tv_seq_kernel<float, 24, 2>" -s 1 -c 1 \
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:tv_seq_kernel -s 2 -c 1 \
     -o "$OUT/full_c3_tv_bwd" python bench.py --workload c3 --steps 2 --warmup 3 --no-graph --no-cpu-baseline \
     > "$OUT/full_c3.log" 2>&1
   echo "full c3 rc=$?"
