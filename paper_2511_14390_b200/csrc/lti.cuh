@@ -1240,7 +1240,7 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
 #pragma unroll
     for (int k = 0; k < NG; ++k) Gs[k] = T(0);
     T* gxrow = p.gx == nullptr ? nullptr : static_cast<T*>(p.gx) + roff;
-#pragma unroll 2
+#pragma unroll 4
     for (int k = 0; k < L / W; ++k) {
         const int n0 = (tid + NT * k) * W;             // tile-local
         const int64_t pos = p0 + n0;
