@@ -66,7 +66,11 @@ iir_status_t LaunchGuard::done() {
 
 // ------------------------------------------------------------- layout -------
 static size_t dsize(int dtype) { return dtype == IIR_F64 ? 8 : 4; }
-static int tile_samples(int dtype) { return NT * (dtype == IIR_F64 ? Chunk<double>::L : Chunk<float>::L); }
+static int tile_samples(int dtype, int M) {
+    const int L = dtype == IIR_F64 ? (M > 4 ? Chunk<double, 8>::L : Chunk<double, 1>::L)
+                                   : (M > 4 ? Chunk<float, 8>::L : Chunk<float, 1>::L);
+    return NT * L;
+}
 
 static int tab_size(int M) {
     switch (M) {
@@ -92,7 +96,7 @@ static iir_status_t check_desc(const iir_desc_t* d) {
     if (d->coef_mode != IIR_COEF_SHARED && d->coef_mode != IIR_COEF_PER_SEQ)
         return fail(IIR_EINVAL, "coef_mode must be SHARED, PER_SEQ or PER_SAMPLE");
     if (d->order < 1 || d->order > 8) return fail(IIR_EUNSUPPORTED, "order must be 1..8 for LTI filters");
-    const int64_t TS = tile_samples(d->dtype);
+    const int64_t TS = tile_samples(d->dtype, d->order);
     if ((d->length + TS - 1) / TS > (int64_t(1) << (5 * MAX_LEVELS)))
         return fail(IIR_EUNSUPPORTED, "length exceeds 32^4 tiles per sequence");
     if (d->batch * ((d->length + TS - 1) / TS) >= (int64_t(1) << 31))
@@ -104,7 +108,7 @@ static Layout layout(const iir_desc_t* d) {
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) return tv_layout(d);
     Layout L;
     const int M = d->order;
-    const int64_t TS = tile_samples(d->dtype);
+    const int64_t TS = tile_samples(d->dtype, d->order);
     L.ntiles = (d->length + TS - 1) / TS;
     L.ntot = L.ntiles * d->batch;
     L.ncoef = d->coef_mode == IIR_COEF_SHARED ? 1 : d->batch;

@@ -13,9 +13,12 @@ constexpr int LOG_NW = 2;
 constexpr int HALO = 8;          // u-history halo of the DF backward tile (>= M)
 
 // Samples per thread chunk (L) by data type; a tile is NT * L samples.
-template <typename T> struct Chunk;
-template <> struct Chunk<float>  { static constexpr int L = 32; };
-template <> struct Chunk<double> { static constexpr int L = 16; };
+// High orders use twice the chunk length: the fp64 carry scans cost M^2 per
+// chunk, so longer chunks halve that work per sample (the per-thread recursion
+// they lengthen is cheap in comparison).
+template <typename T, int M> struct Chunk {
+    static constexpr int L = (sizeof(T) == 4 ? 32 : 16) * (M > 4 ? 2 : 1);
+};
 
 // Shared-memory tile layout: 16 B of padding after every 128 B row, so that the
 // 128-bit reads of 8 consecutive threads (each owning one or more whole rows)

@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restr
     // it waits for this grid's completion (griddepcontrol.wait) before reading tables.
     pdl_launch_dependents();
     span_enter(span);
-    constexpr int L = Chunk<T>::L, M2 = M * M;
+    constexpr int L = Chunk<T, M>::L, M2 = M * M;
     using TB = Tab<M>;
     using S = PrepSlots<M>;
     extern __shared__ __align__(16) unsigned char prep_raw[];
@@ -659,7 +659,7 @@ __device__ __forceinline__ void cta_exit(const CarryWs& cw, unsigned ep, unsigne
 
 template <typename T, int M>
 struct Smem {
-    static constexpr int TS = NT * Chunk<T>::L;
+    static constexpr int TS = NT * Chunk<T, M>::L;
     static constexpr int PT = pidx<T>(TS);               // one padded tile
     static constexpr int PTH = pidx<T>(TS + HALO);       // padded tile with u history
     static constexpr size_t tab_bytes = ((size_t)Tab<M>::SMALL * 8 + 15) / 16 * 16;
@@ -682,7 +682,7 @@ template <int M> constexpr int bwd_tdf_min_blocks() { return M <= 2 ? 8 : (M <= 
 
 template <typename T, int M, int FORM>
 __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const LtiFwdArgs p) {
-    constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
+    constexpr int L = Chunk<T, M>::L, TS = NT * L, W = Vec<T>::W;
     using V = typename Vec<T>::type;
     using TB = Tab<M>;
     using SM = Smem<T, M>;
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const 
 
 template <typename T, int M, int FORM>
 __device__ __forceinline__ void bwd_load_u(const LtiBwdArgs& p, int64_t seq, int64_t p0, T* s2) {
-    constexpr int TS = NT * Chunk<T>::L, W = Vec<T>::W;
+    constexpr int TS = NT * Chunk<T, M>::L, W = Vec<T>::W;
     using V = typename Vec<T>::type;
     // u(p0 - HALO .. p0 + TS) -> s2[pidx(e + HALO)]; u(-k) = zi[k-1] (DF state).
     const T* urow = static_cast<const T*>(p.u) + seq * p.Tlen;
@@ -913,7 +913,7 @@ __device__ __forceinline__ void bwd_finalize(const LtiBwdArgs& p, unsigned tk, i
 // backwards.  TDF: smem dy | x | y.  DF: smem dy | u (with HALO samples of history).
 template <typename T, int M, int FORM>
 __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const LtiBwdArgs p) {
-    constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
+    constexpr int L = Chunk<T, M>::L, TS = NT * L, W = Vec<T>::W;
     constexpr int NG = 2 * M + 1;                       // gradient partial sums
     using V = typename Vec<T>::type;
     using TB = Tab<M>;
@@ -1109,7 +1109,7 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
 // flight.  g beyond the tile end comes from the carry: g(p0+TS+j) = X[j+1].
 template <typename T, int M>
 __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kernel(const LtiBwdArgs p) {
-    constexpr int L = Chunk<T>::L, TS = NT * L, W = Vec<T>::W;
+    constexpr int L = Chunk<T, M>::L, TS = NT * L, W = Vec<T>::W;
     constexpr int NG = 2 * M + 1;
     using V = typename Vec<T>::type;
     using TB = Tab<M>;

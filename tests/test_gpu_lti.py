@@ -13,7 +13,12 @@ from gpu_util import TOL, compare, run_lti_gpu, run_lti_oracle
 
 pytestmark = pytest.mark.gpu
 
-TS = {"f32": 4096, "f64": 2048}     # samples per tile (NT * L)
+TS = {"f32": 4096, "f64": 2048}     # samples per tile (NT * L) for M <= 4
+
+
+def tile(dtype, M):
+    """Samples per tile: orders above 4 use chunks twice as long (lti.cuh Chunk)."""
+    return TS[dtype] * (2 if M > 4 else 1)
 
 
 def check(p, tol=None, seqs=None, **kw):
@@ -56,7 +61,7 @@ def test_config5_shard_order8_fp32():
 @pytest.mark.parametrize("form", ["tdf", "df"])
 @pytest.mark.parametrize("M", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_orders_forms_dtypes(dtype, form, M):
-    p = inputs.lti_problem(2000 + M, form=form, order=M, batch=3, length=3 * TS[dtype] + 77, dtype=dtype,
+    p = inputs.lti_problem(2000 + M, form=form, order=M, batch=3, length=3 * tile(dtype, M) + 77, dtype=dtype,
                            angles="spread")
     check(p)
 
