@@ -67,8 +67,8 @@ iir_status_t LaunchGuard::done() {
 // ------------------------------------------------------------- layout -------
 static size_t dsize(int dtype) { return dtype == IIR_F64 ? 8 : 4; }
 static int tile_samples(int dtype, int M) {
-    const int L = dtype == IIR_F64 ? (M > 4 ? Chunk<double, 8>::L : Chunk<double, 1>::L)
-                                   : (M > 4 ? Chunk<float, 8>::L : Chunk<float, 1>::L);
+    const int L = dtype == IIR_F64 ? (M >= IIRG_LONG_CHUNK_M ? Chunk<double, 8>::L : Chunk<double, 1>::L)
+                                   : (M >= IIRG_LONG_CHUNK_M ? Chunk<float, 8>::L : Chunk<float, 1>::L);
     return NT * L;
 }
 

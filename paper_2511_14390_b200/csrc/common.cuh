@@ -16,8 +16,11 @@ constexpr int HALO = 8;          // u-history halo of the DF backward tile (>= M
 // High orders use twice the chunk length: the fp64 carry scans cost M^2 per
 // chunk, so longer chunks halve that work per sample (the per-thread recursion
 // they lengthen is cheap in comparison).
+#ifndef IIRG_LONG_CHUNK_M
+#define IIRG_LONG_CHUNK_M 4
+#endif
 template <typename T, int M> struct Chunk {
-    static constexpr int L = (sizeof(T) == 4 ? 32 : 16) * (M > 4 ? 2 : 1);
+    static constexpr int L = (sizeof(T) == 4 ? 32 : 16) * (M >= IIRG_LONG_CHUNK_M ? 2 : 1);
 };
 
 // Shared-memory tile layout: 16 B of padding after every 128 B row, so that the

@@ -13,12 +13,12 @@ from gpu_util import TOL, compare, run_lti_gpu, run_lti_oracle
 
 pytestmark = pytest.mark.gpu
 
-TS = {"f32": 4096, "f64": 2048}     # samples per tile (NT * L) for M <= 4
+TS = {"f32": 4096, "f64": 2048}     # samples per tile (NT * L) for M < 4
 
 
 def tile(dtype, M):
-    """Samples per tile: orders above 4 use chunks twice as long (lti.cuh Chunk)."""
-    return TS[dtype] * (2 if M > 4 else 1)
+    """Samples per tile: orders from 4 up use chunks twice as long (common.cuh Chunk)."""
+    return TS[dtype] * (2 if M >= 4 else 1)
 
 
 def check(p, tol=None, seqs=None, **kw):

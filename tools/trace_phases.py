@@ -27,7 +27,7 @@ def main():
     w = dict(bench.WORKLOADS[a.workload], key=a.workload)
     prob = bench.Problem(w, 0, 1, 2)
     s = torch.cuda.Stream()
-    ts = 128 * (32 if w["dtype"] == "f32" else 16) * (2 if w["order"] > 4 else 1)   # tile samples (lti.cuh Chunk)
+    ts = 128 * (32 if w["dtype"] == "f32" else 16) * (2 if w["order"] >= 4 else 1)   # tile samples (lti.cuh Chunk)
     ntot = w["batch"] * ((w["length"] + ts - 1) // ts)
     buf = torch.zeros(ntot * 16 + 8, dtype=torch.int64, device="cuda")
     buf2 = torch.zeros(ntot * 16 + 8, dtype=torch.int64, device="cuda")
