@@ -40,12 +40,16 @@ WORKLOADS = {
                     "coefficient-gradient all-reduce", **dict(inputs.CONFIGS["c5"], batch=256)),
     "c3": dict(desc="config 3: all-pole LPC order 24, per-sample coefficients, batch 32 x 2^18, fp32",
                **inputs.CONFIGS["c3"]),
+    "f1": dict(desc="SURVEY 8(f) f1: bare recurrence v(n+1) = A v(n) + z(n) of Listing 1, M = 2, batch 16 x 2^20, "
+                    "fp32 (the paper's benchmarked operator at its longest N)", **dict(inputs.CONFIGS["f1"], batch=16)),
 }
 
 
 def algorithmic_bytes(w):
     """Bytes per sample the method must move, per kernel."""
     s = 8 if w["dtype"] == "f64" else 4
+    if w["form"] == "ss":                       # rec_fwd reads z, writes v; rec_bwd reads gv, v, writes gz
+        return {"rec_fwd": 2 * w["order"] * s, "rec_bwd": 3 * w["order"] * s}
     if w["coef"] == "per_sample":
         # tv_phi reads a, x; tv_fwd reads a, x and writes y; tv_bwd_agg reads a, dy;
         # tv_bwd reads a, dy, y and writes dx, grad_a.  tv_chain moves only the
@@ -65,6 +69,8 @@ def step_min_bytes(w):
     LTI TDF x, y, dy, dx (+x, y re-read by the backward); TV all-pole x, y, dy, dx,
     a read by each direction and grad_a written: (3M + 5) elements."""
     s = 8 if w["dtype"] == "f64" else 4
+    if w["form"] == "ss":
+        return 5 * w["order"] * s
     if w["coef"] == "per_sample":
         return (3 * w["order"] + 5) * s
     return 6 * s
@@ -145,27 +151,34 @@ class Problem:
         self.td = td
         g = torch.Generator(device=dev).manual_seed(seed)
         self.sets = []
+        ss = w["form"] == "ss"
+        shape = (Bsz, T, M) if ss else (Bsz, T)
         if w["coef"] == "per_sample":
             p = inputs.tv_allpole_problem(seed, batch=Bsz, length=T, order=M, dtype=w["dtype"], device=dev)
             self.a = p["a"].to(td).contiguous()
             self.b = None
             self.zi = p["zi"].to(td).contiguous()
             mode = B.IIR_COEF_PER_SAMPLE
+        elif ss:
+            self.a = torch.tensor(inputs.stable_matrix(rng, M), dtype=td, device=dev)
+            self.b = None
+            self.zi = (0.1 * torch.randn(Bsz, M, generator=g, device=dev, dtype=torch.float64)).to(td)
+            mode = B.IIR_COEF_SHARED
         else:
             b, a = inputs.stable_coefs(rng, M, w["dtype"], angles=w["angles"])
             self.b = torch.tensor(b, dtype=td, device=dev)
             self.a = torch.tensor(a, dtype=td, device=dev)
             self.zi = (0.1 * torch.randn(Bsz, M, generator=g, device=dev, dtype=torch.float64)).to(td)
             mode = B.IIR_COEF_SHARED
-        self.gzf = torch.randn(Bsz, M, generator=g, device=dev, dtype=torch.float64).to(td)
+        self.gzf = None if ss else torch.randn(Bsz, M, generator=g, device=dev, dtype=torch.float64).to(td)
         for _ in range(nsets):
-            x = torch.randn(Bsz, T, generator=g, device=dev, dtype=td)
-            gy = torch.randn(Bsz, T, generator=g, device=dev, dtype=td)
+            x = torch.randn(*shape, generator=g, device=dev, dtype=td)
+            gy = torch.randn(*shape, generator=g, device=dev, dtype=td)
             st = dict(x=x, gy=gy, y=torch.empty_like(x), gx=torch.empty_like(x))
             if w["coef"] == "per_sample":
                 st["ga"] = torch.empty_like(self.a)          # (B, T, M): one per set, like y and dx
             self.sets.append(st)
-        self.zf = torch.empty(Bsz, M, dtype=td, device=dev)
+        self.zf = None if ss else torch.empty(Bsz, M, dtype=td, device=dev)
         self.gzi = torch.empty(Bsz, M, dtype=td, device=dev)
         self.gb = None if self.b is None else torch.empty_like(self.b)
         self.ga = None if w["coef"] == "per_sample" else torch.empty_like(self.a)
@@ -177,6 +190,7 @@ class Problem:
         self.ws = torch.empty(self.wb, dtype=torch.uint8, device=dev)
         B.iir_workspace_init(self.desc, self.ws, self.wb, torch.cuda.current_stream(dev))
         self.grad_buf = None if self.b is None else torch.empty(2 * (M + 1), dtype=td, device=dev)
+        self.ss = ss
 
     def set_bytes(self):
         s = self.sets[0]
@@ -193,6 +207,8 @@ class Problem:
             # the one real exchange of the path: all-reduce of the shared-coefficient gradients (§8(e))
             torch.cat([self.gb, self.ga], out=self.grad_buf)
             torch.distributed.all_reduce(self.grad_buf, group=pg)
+        elif pg is not None and self.ss:
+            torch.distributed.all_reduce(self.ga, group=pg)      # shared A of the bare recurrence
 
 
 def run_ours(args, w, rank, world, dev, pg):
@@ -200,7 +216,7 @@ def run_ours(args, w, rank, world, dev, pg):
     torch.cuda.set_device(dev)
     L2 = torch.cuda.get_device_properties(dev).L2_cache_size
     samples = w["batch"] * w["length"]
-    bytes_per_set = 4 * samples * (8 if w["dtype"] == "f64" else 4)
+    bytes_per_set = 4 * samples * (8 if w["dtype"] == "f64" else 4) * (w["order"] if w["form"] == "ss" else 1)
     nsets = max(2, int(np.ceil(3 * L2 / bytes_per_set)) + 1)
     nsets = min(nsets, 64)
     prob = Problem(w, dev, 1000 + rank, nsets)
@@ -369,7 +385,12 @@ def cpu_baseline(w, budget_s=10.0):
     rng = np.random.default_rng(7)
     T = w["length"]
     nseq = min(w["batch"], 64)
-    if w["coef"] == "per_sample":
+    if w["form"] == "ss":
+        T = min(T, 1 << 20)
+        nseq = 2
+        p = inputs.rec_problem(7, batch=nseq, length=T, order=w["order"], dtype=w["dtype"])
+        fn = lambda: [oracle.recurrence(p["A"], p["v0"][i], p["z"][i], p["gv"][i]) for i in range(nseq)]
+    elif w["coef"] == "per_sample":
         T = min(T, 1 << 16)
         p = inputs.tv_allpole_problem(7, batch=min(nseq, 8), length=T, order=w["order"], dtype=w["dtype"])
         args = (p["a"].numpy(), p["x"].numpy(), p["zi"].numpy(), p["gy"].numpy(), p["gzf"].numpy())
@@ -382,7 +403,7 @@ def cpu_baseline(w, budget_s=10.0):
                                angles=w["angles"])
         form = 1 if w["form"] == "tdf" else 0
         fn = lambda: oracle.lti(form, p["b"], p["a"], p["x"], p["zi"], p["gy"], p["gzf"])
-    cores = min(os.cpu_count() or 1, nseq)
+    cores = 1 if w["form"] == "ss" else min(os.cpu_count() or 1, nseq)
     reps = 0
     t0 = time.perf_counter()
     while True:
@@ -406,7 +427,12 @@ def run_reference(args, w, rank, world):
     if rank != 0:
         return
     T = w["length"]
-    if w["coef"] == "per_sample":
+    if w["form"] == "ss":
+        T = min(T, 1 << 19)
+        nseq = 1
+        p = inputs.rec_problem(7, batch=nseq, length=T, order=w["order"], dtype=w["dtype"])
+        fn = lambda: oracle.recurrence(p["A"], p["v0"][0], p["z"][0], p["gv"][0])
+    elif w["coef"] == "per_sample":
         T = min(T, 1 << 15)
         nseq = min(w["batch"], 8)
         p = inputs.tv_allpole_problem(7, batch=nseq, length=T, order=w["order"], dtype=w["dtype"])
@@ -425,7 +451,7 @@ def run_reference(args, w, rank, world):
     for _ in range(args.steps):
         fn()
     el = time.perf_counter() - t0
-    cores = min(os.cpu_count() or 1, nseq)
+    cores = 1 if w["form"] == "ss" else min(os.cpu_count() or 1, nseq)
     value = args.steps * nseq * T / el
     line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,

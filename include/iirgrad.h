@@ -68,7 +68,18 @@ extern "C" {
 #define IIRGRAD_ABI_VERSION 1
 
 typedef enum { IIR_OK = 0, IIR_EINVAL = 1, IIR_EUNSUPPORTED = 2, IIR_ECUDA = 3, IIR_EWORKSPACE = 4 } iir_status_t;
-typedef enum { IIR_DF2 = 0, IIR_TDF2 = 1 } iir_form_t;          /* PAPER.md:52 footnote: type-II forms */
+typedef enum {
+    IIR_DF2 = 0,   /* direct form II (Eqs.2-3)                        PAPER.md:52 footnote: type-II forms */
+    IIR_TDF2 = 1,  /* transposed direct form II (= scipy lfilter)                                          */
+    IIR_SS = 2     /* bare state-space recurrence of Listing 1 (the paper's benchmark op):
+                    *   v(n+1) = A v(n) + z(n), dense A (order M = 1..4), SHARED (M, M) or PER_SEQ (B, M, M),
+                    *   row-major.  Argument mapping: a = A, b = NULL, x = z (B, T, M), zi = v0 (B, M) or NULL,
+                    *   y = v(1..T) (B, T, M), zf unused (NULL).  Backward: grad_y = dL/dv(1..T) (B, T, M),
+                    *   grad_zf = NULL, y = the forward's v, zi = v0; grad_x = dL/dz (B, T, M),
+                    *   grad_a = dL/dA (shape of A; SHARED: summed over the batch), grad_zi = dL/dv0,
+                    *   grad_b = NULL.  Listing 1's VJP: g(n) = gv(n) + A^T g(n+1),
+                    *   dL/dv0 = A^T g(0), dL/dA = sum_n g(n) v(n)^T.                                       */
+} iir_form_t;
 typedef enum { IIR_F32 = 0, IIR_F64 = 1 } iir_dtype_t;
 typedef enum {
     IIR_COEF_SHARED = 0,     /* b, a: (M+1); one filter for the whole batch          */

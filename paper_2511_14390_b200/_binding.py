@@ -17,12 +17,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libiirgrad.so")
 
 IIR_OK, IIR_EINVAL, IIR_EUNSUPPORTED, IIR_ECUDA, IIR_EWORKSPACE = range(5)
-IIR_DF2, IIR_TDF2 = 0, 1
+IIR_DF2, IIR_TDF2, IIR_SS = 0, 1, 2
 IIR_F32, IIR_F64 = 0, 1
 IIR_COEF_SHARED, IIR_COEF_PER_SEQ, IIR_COEF_PER_SAMPLE = 0, 1, 2
 IIR_FLAG_WS_READY = 1
 
-FORMS = {"df": IIR_DF2, "tdf": IIR_TDF2, IIR_DF2: IIR_DF2, IIR_TDF2: IIR_TDF2}
+FORMS = {"df": IIR_DF2, "tdf": IIR_TDF2, "ss": IIR_SS, IIR_DF2: IIR_DF2, IIR_TDF2: IIR_TDF2, IIR_SS: IIR_SS}
 DTYPES = {torch.float32: IIR_F32, torch.float64: IIR_F64}
 
 EXPORTS = ["iir_tape_bytes", "iir_workspace_bytes", "iir_workspace_init", "iir_forward", "iir_backward", "iir_last_error",

@@ -118,3 +118,43 @@ def allpole_tv(x, a, zi=None, return_zf=False):
     a[b, n, i-1] = a_i(n) (monic, a_0 = 1 implied), zi (B, M) = past outputs."""
     y, zf = AllPoleTVFunction.apply(x, a, zi)
     return (y, zf) if return_zf else y
+
+
+class LTIMatrixRecurrenceFunction(torch.autograd.Function):
+    """v(1..N) = recurrence(A, v0, z): v(n+1) = A v(n) + z(n) (PAPER.md:296-343,
+    Listing 1), batched: z (B, N, M), v0 (B, M), A (M, M) shared or (B, M, M)."""
+
+    @staticmethod
+    def forward(ctx, A, v0, z):
+        _require_cuda(A, v0, z)
+        A, v0, z = _c(A), _c(v0), _c(z)
+        Bsz, N, M = z.shape
+        mode = B.IIR_COEF_SHARED if A.dim() == 2 else B.IIR_COEF_PER_SEQ
+        desc = B.make_desc(Bsz, N, M, "ss", z.dtype, mode)
+        v = torch.empty_like(z)
+        tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
+        tape = torch.empty(tb, dtype=torch.uint8, device=z.device)
+        ws = torch.empty(wb, dtype=torch.uint8, device=z.device)
+        B.iir_forward(desc, None, A, z, v0, v, None, tape, tb, ws, wb)
+        ctx.desc = desc
+        ctx.has_v0 = v0 is not None
+        ctx.save_for_backward(A, v0 if v0 is not None else torch.empty(0, device=z.device), v, tape)
+        return v
+
+    @staticmethod
+    def backward(ctx, gv):
+        A, v0, v, tape = ctx.saved_tensors
+        v0 = v0 if ctx.has_v0 else None
+        desc = ctx.desc
+        gA = torch.empty_like(A) if ctx.needs_input_grad[0] else None
+        gv0 = torch.empty_like(v0) if (v0 is not None and ctx.needs_input_grad[1]) else None
+        gz = torch.empty_like(v) if ctx.needs_input_grad[2] else None
+        wb = B.iir_workspace_bytes(desc)
+        ws = torch.empty(wb, dtype=torch.uint8, device=v.device)
+        B.iir_backward(desc, _c(gv), None, None, A, None, v, v0, tape, tape.numel(), gz, None, gA, gv0, ws, wb)
+        return gA, gv0, gz
+
+
+def matrix_recurrence(A, v0, z):
+    """Differentiable batched v(n+1) = A v(n) + z(n); returns v(1..N) (B, N, M)."""
+    return LTIMatrixRecurrenceFunction.apply(A, v0, z)

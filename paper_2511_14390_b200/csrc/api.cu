@@ -27,7 +27,7 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
 
 // ------------------------------------------------------- instrumentation ----
 static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_phi", "tv_chain", "tv_fwd",
-                                        "tv_bwd_agg", "tv_bwd"};
+                                        "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;
@@ -81,12 +81,28 @@ static int tab_size(int M) {
     return 0;
 }
 
+namespace iirg {
+int rec_tile_samples(int dtype, int M);
+iir_status_t rec_run(bool fwd, int dtype, int M, const Layout& L, const LtiFwdArgs& fa, const LtiBwdArgs& ba,
+                     cudaStream_t st);
+}  // namespace iirg
+
+static int scan_tile_samples(const iir_desc_t* d) {
+    return d->form == IIR_SS ? rec_tile_samples(d->dtype, d->order) : tile_samples(d->dtype, d->order);
+}
+
 static iir_status_t check_desc(const iir_desc_t* d) {
     if (d == nullptr) return fail(IIR_EINVAL, "desc is NULL");
     if (d->batch < 1) return fail(IIR_EINVAL, "batch must be >= 1");
     if (d->length < 1) return fail(IIR_EINVAL, "length must be >= 1");
     if (d->dtype != IIR_F32 && d->dtype != IIR_F64) return fail(IIR_EINVAL, "dtype must be IIR_F32 or IIR_F64");
-    if (d->form != IIR_DF2 && d->form != IIR_TDF2) return fail(IIR_EINVAL, "form must be IIR_DF2 or IIR_TDF2");
+    if (d->form != IIR_DF2 && d->form != IIR_TDF2 && d->form != IIR_SS)
+        return fail(IIR_EINVAL, "form must be IIR_DF2, IIR_TDF2 or IIR_SS");
+    if (d->form == IIR_SS) {
+        if (d->coef_mode != IIR_COEF_SHARED && d->coef_mode != IIR_COEF_PER_SEQ)
+            return fail(IIR_EUNSUPPORTED, "bare recurrence: A is SHARED or PER_SEQ");
+        if (d->order < 1 || d->order > 4) return fail(IIR_EUNSUPPORTED, "bare recurrence: order must be 1..4");
+    }
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) {
         if (d->form != IIR_DF2) return fail(IIR_EUNSUPPORTED, "per-sample coefficients: only the all-pole DF form");
         if (d->order < 1 || d->order > TV_MAX_M) return fail(IIR_EUNSUPPORTED, "per-sample order must be 1..31");
@@ -96,7 +112,7 @@ static iir_status_t check_desc(const iir_desc_t* d) {
     if (d->coef_mode != IIR_COEF_SHARED && d->coef_mode != IIR_COEF_PER_SEQ)
         return fail(IIR_EINVAL, "coef_mode must be SHARED, PER_SEQ or PER_SAMPLE");
     if (d->order < 1 || d->order > 8) return fail(IIR_EUNSUPPORTED, "order must be 1..8 for LTI filters");
-    const int64_t TS = tile_samples(d->dtype, d->order);
+    const int64_t TS = scan_tile_samples(d);
     if ((d->length + TS - 1) / TS > (int64_t(1) << (5 * MAX_LEVELS)))
         return fail(IIR_EUNSUPPORTED, "length exceeds 32^4 tiles per sequence");
     if (d->batch * ((d->length + TS - 1) / TS) >= (int64_t(1) << 31))
@@ -108,7 +124,8 @@ static Layout layout(const iir_desc_t* d) {
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) return tv_layout(d);
     Layout L;
     const int M = d->order;
-    const int64_t TS = tile_samples(d->dtype, d->order);
+    const int64_t TS = scan_tile_samples(d);
+    const int NGP = d->form == IIR_SS ? M * M : 2 * M + 1;   // coefficient partial sums per tile
     L.ntiles = (d->length + TS - 1) / TS;
     L.ntot = L.ntiles * d->batch;
     L.ncoef = d->coef_mode == IIR_COEF_SHARED ? 1 : d->batch;
@@ -129,8 +146,8 @@ static Layout layout(const iir_desc_t* d) {
     L.ws_bank = o - L.ws_sent;                           // two banks of look-back slots (epoch parity),
     o += 3 * L.ws_bank;                                  // for the forward and for the backward
     L.ws_sent_bytes = o - L.ws_sent;
-    L.ws_part = o; o += al256(L.ntot * (2 * M + 1) * 8);
-    L.ws_part2 = o; o += al256(L.ngroups * (2 * M + 1) * 8);
+    L.ws_part = o; o += al256(L.ntot * NGP * 8);
+    L.ws_part2 = o; o += al256(L.ngroups * NGP * 8);
     L.ws_bytes = o;
     o = 0;
     L.tp_tab = o; o += al256((size_t)L.ncoef * tab_size(M) * 8);
@@ -215,8 +232,8 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     const Layout L = layout(d);
     if (x == nullptr || y == nullptr) return fail(IIR_EINVAL, "x and y must be non-NULL");
     if (a == nullptr) return fail(IIR_EINVAL, "a must be non-NULL");
-    if (d->coef_mode == IIR_COEF_PER_SAMPLE) {
-        if (b != nullptr) return fail(IIR_EINVAL, "per-sample coefficients: b must be NULL (all-pole)");
+    if (d->coef_mode == IIR_COEF_PER_SAMPLE || d->form == IIR_SS) {
+        if (b != nullptr) return fail(IIR_EINVAL, "per-sample all-pole / bare recurrence: b must be NULL");
     } else if (b == nullptr) {
         return fail(IIR_EINVAL, "b must be non-NULL");
     }
@@ -230,7 +247,8 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
         if (rs != IIR_OK) return rs;
     }
     const int W = d->dtype == IIR_F64 ? 2 : 4;
-    const bool vec = (d->length % W == 0) && aligned16(x) && aligned16(y) && aligned16(t + L.tp_u);
+    const int64_t rowlen = d->length * (d->form == IIR_SS ? d->order : 1);
+    const bool vec = (rowlen % W == 0) && aligned16(x) && aligned16(y) && aligned16(t + L.tp_u);
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) return tv_forward(d, L, a, x, zi, y, zf, t, w, vec, st);
 
     LtiCall c{};
@@ -245,6 +263,10 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     fa.B = d->batch; fa.Tlen = d->length; fa.ntiles = (int)L.ntiles; fa.vec = vec;
     fa.trace = g_trace;
     fa.span = g_trace == nullptr ? nullptr : g_trace + L.ntot * 16 + 2;   // [prep][fwd][bwd]
+    if (d->form == IIR_SS) {
+        fa.coef_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : (int64_t)d->order * d->order;
+        return rec_run(true, d->dtype, d->order, L, fa, LtiBwdArgs{}, st);
+    }
     return run_lti_any(c);
 }
 
@@ -259,6 +281,9 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     if (ws == nullptr || ws_bytes < L.ws_bytes) return fail(IIR_EWORKSPACE, "workspace missing or too small");
     if (d->coef_mode != IIR_COEF_PER_SAMPLE && d->form == IIR_TDF2 && (x == nullptr || y == nullptr))
         return fail(IIR_EINVAL, "TDF backward needs the forward's x and y");
+    if (d->form == IIR_SS && (a == nullptr || y == nullptr))
+        return fail(IIR_EINVAL, "bare-recurrence backward needs A and the forward's v");
+    if (d->form == IIR_SS && grad_b != nullptr) return fail(IIR_EINVAL, "bare recurrence: grad_b must be NULL");
     if (d->coef_mode == IIR_COEF_PER_SAMPLE && (a == nullptr || y == nullptr))
         return fail(IIR_EINVAL, "per-sample backward needs the forward's a and y");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -269,7 +294,8 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
         if (rs != IIR_OK) return rs;
     }
     const int W = d->dtype == IIR_F64 ? 2 : 4;
-    const bool vec = (d->length % W == 0) && aligned16(grad_y) && aligned16(x) && aligned16(y) &&
+    const int64_t rowlen = d->length * (d->form == IIR_SS ? d->order : 1);
+    const bool vec = (rowlen % W == 0) && aligned16(grad_y) && aligned16(x) && aligned16(y) &&
                      aligned16(grad_x) && aligned16(t + L.tp_u);
     if (d->coef_mode == IIR_COEF_PER_SAMPLE)
         return tv_backward(d, L, grad_y, grad_zf, a, y, zi, t, grad_x, grad_a, grad_zi, w, vec, st);
@@ -293,7 +319,12 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     ba.B = d->batch; ba.Tlen = d->length; ba.ntiles = (int)L.ntiles; ba.vec = vec;
     ba.trace = g_trace;
     ba.span = g_trace == nullptr ? nullptr : g_trace + L.ntot * 16 + 4;
-    (void)b; (void)a;
+    (void)b;
+    if (d->form == IIR_SS) {
+        ba.a = a;
+        ba.coef_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : (int64_t)d->order * d->order;
+        return rec_run(false, d->dtype, d->order, L, LtiFwdArgs{}, ba, st);
+    }
     return run_lti_any(c);
 }
 

@@ -125,7 +125,10 @@ template <int M> struct PrepSlots {
     static constexpr size_t bytes() { return (size_t)N * M * M * sizeof(double); }
 };
 
-template <typename T, int M, int FORM>
+// FORM 0 / 1: companion(a') (DF) or its transpose (TDF) from (b, a); FORM 2: the
+// dense A itself (the bare recurrence, rec.cuh), given row-major in `a`.  LC is
+// the chunk length of the consuming scan kernel.
+template <typename T, int M, int FORM, int LC = Chunk<T, M>::L>
 __global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restrict__ b, const T* __restrict__ a,
                                                                int64_t coef_stride, double* __restrict__ tab,
                                                                int64_t tab_stride, int nlev,
@@ -134,18 +137,18 @@ __global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restr
     // it waits for this grid's completion (griddepcontrol.wait) before reading tables.
     pdl_launch_dependents();
     span_enter(span);
-    constexpr int L = Chunk<T, M>::L, M2 = M * M;
+    constexpr int L = LC, M2 = M * M;
     using TB = Tab<M>;
     using S = PrepSlots<M>;
     extern __shared__ __align__(16) unsigned char prep_raw[];
     double* mat = reinterpret_cast<double*>(prep_raw);
     __shared__ double bn[M + 1], an[M + 1];
     const int set = blockIdx.x;
-    const T* bb = b + set * coef_stride;
+    const T* bb = FORM == 2 ? nullptr : b + set * coef_stride;
     const T* aa = a + set * coef_stride;
     double* tb = tab + set * tab_stride;
     const int tid = threadIdx.x;
-    if (tid <= M) {
+    if (FORM != 2 && tid <= M) {
         const double a0 = (double)aa[0];
         bn[tid] = (double)bb[tid] / a0;
         an[tid] = (double)aa[tid] / a0;
@@ -153,17 +156,23 @@ __global__ void __launch_bounds__(PREP_THREADS) lti_prep_kernel(const T* __restr
     __syncthreads();
     for (int e = tid; e < M2; e += PREP_THREADS) {
         const int i = e / M, j = e % M;
-        const double Aij = (i == 0) ? -an[j + 1] : (i == j + 1 ? 1.0 : 0.0);  // companion(a'), row 0 = -a'
-        const double Aji = (j == 0) ? -an[i + 1] : (j == i + 1 ? 1.0 : 0.0);
-        mat[S::P1 * M2 + e] = (FORM == 0) ? Aij : Aji;
+        if constexpr (FORM == 2) {
+            mat[S::P1 * M2 + e] = (double)aa[e];
+        } else {
+            const double Aij = (i == 0) ? -an[j + 1] : (i == j + 1 ? 1.0 : 0.0);  // companion(a'), row 0 = -a'
+            const double Aji = (j == 0) ? -an[i + 1] : (j == i + 1 ? 1.0 : 0.0);
+            mat[S::P1 * M2 + e] = (FORM == 0) ? Aij : Aji;
+        }
         const double id = (i == j) ? 1.0 : 0.0;
         mat[(S::PLT + 0) * M2 + e] = id;
         mat[(S::YP + 0) * M2 + e] = id;
         for (int l = 0; l < LEVELS; ++l) mat[(S::Q + l * 33) * M2 + e] = id;
     }
-    if (tid <= M) { tb[TB::COEF + tid] = bn[tid]; tb[TB::COEF + M + 1 + tid] = an[tid]; }
-    if (tid < M) tb[TB::COEF + 2 * (M + 1) + tid] = bn[tid + 1] - an[tid + 1] * bn[0];
-    if (tid == 0) tb[TB::A0] = (double)aa[0];
+    if constexpr (FORM != 2) {
+        if (tid <= M) { tb[TB::COEF + tid] = bn[tid]; tb[TB::COEF + M + 1 + tid] = an[tid]; }
+        if (tid < M) tb[TB::COEF + 2 * (M + 1) + tid] = bn[tid + 1] - an[tid + 1] * bn[0];
+        if (tid == 0) tb[TB::A0] = (double)aa[0];
+    }
     __syncthreads();
     // batched product: for q < n: mat[dst(q)] = mat[lhs(q)] * mat[rhs(q)]
     auto mm_batch = [&](int n, auto dst, auto lhs, auto rhs) {
@@ -357,6 +366,7 @@ struct LtiFwdArgs {
 
 struct LtiBwdArgs {
     const void* gy; const void* gzf; const void* x; const void* y; const void* u; const void* zi;
+    const void* a; int64_t coef_stride;                           // bare recurrence (rec.cuh): A
     void* gx; void* gzi; void* gb; void* ga; int want_coef;
     double* partial; double* partial2; unsigned* gcnt; unsigned* scnt;   // fused finalize
     int64_t ncoef;
@@ -849,10 +859,13 @@ __device__ __forceinline__ void bwd_load_u(const LtiBwdArgs& p, int64_t seq, int
 // group of 32 tiles -> set -> chain rule.  SHARED groups are consecutive tiles
 // in scan order (they complete, and are reduced, while the kernel runs);
 // PER_SEQ groups are a sequence's tiles.  Fixed reduction order throughout.
+template <int M, int FORM> constexpr int n_partials() { return FORM == 2 ? M * M : 2 * M + 1; }
+
 template <typename T, int M, int FORM>
 __device__ __forceinline__ void bwd_finalize(const LtiBwdArgs& p, unsigned tk, int64_t seq, int jt,
-                                             const double* __restrict__ tb, const double (*s_red)[2 * M + 1]) {
-    constexpr int NG = 2 * M + 1;
+                                             const double* __restrict__ tb,
+                                             const double (*s_red)[n_partials<M, FORM>()]) {
+    constexpr int NG = n_partials<M, FORM>();
     __shared__ double s_G[NG];
     __shared__ unsigned s_fin;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -897,9 +910,14 @@ __device__ __forceinline__ void bwd_finalize(const LtiBwdArgs& p, unsigned tk, i
             __syncthreads();
             IIRG_TRACE(p.trace, tk, 13);
             if (tid == 0) {
-                chain_rule<T, M, FORM>(s_G, tb,
+                if constexpr (FORM == 2) {                   // bare recurrence: grad_A is the sum itself
+                    if (p.ga != nullptr)
+                        for (int e = 0; e < NG; ++e) static_cast<T*>(p.ga)[cset * NG + e] = (T)s_G[e];
+                } else {
+                    chain_rule<T, M, FORM>(s_G, tb,
                                        p.gb == nullptr ? nullptr : static_cast<T*>(p.gb) + cset * (M + 1),
                                        p.ga == nullptr ? nullptr : static_cast<T*>(p.ga) + cset * (M + 1));
+                }
                 p.scnt[cset] = 0u;
                 IIRG_TRACE(p.trace, tk, 14);
             }

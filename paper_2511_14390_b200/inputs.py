@@ -30,6 +30,8 @@ CONFIGS = {
     "c3": dict(form="df", order=24, batch=32, length=1 << 18, dtype="f32", coef="per_sample", angles="spread"),
     "c4": dict(form="tdf", order=4, batch=1, length=1 << 24, dtype="f32", coef="shared", angles="spread"),
     "c5": dict(form="tdf", order=8, batch=2048, length=1 << 16, dtype="f32", coef="shared", angles="spread"),
+    # the bare recurrence the paper benchmarks (M = 2, N = 2^14 .. 2^20)
+    "f1": dict(form="ss", order=2, batch=64, length=1 << 20, dtype="f32", coef="shared", angles="random"),
 }
 
 
@@ -142,3 +144,36 @@ def tv_allpole_problem(seed, batch=32, length=1 << 18, order=24, hop=256, dtype=
     return dict(a=a, x=rnd(batch, length), gy=rnd(batch, length),
                 zi=(0.1 * rnd(batch, order)).to(td).to(torch.float64) if zi else None,
                 gzf=rnd(batch, order) if gzf else None, dtype=dtype)
+
+
+def stable_matrix(rng, order, r_lo=0.5, r_hi=0.99):
+    """Dense stable A (order x order): rotation-scaling blocks r R(theta) (and one
+    real eigenvalue for odd orders) conjugated by a random orthogonal matrix, so
+    A is normal (well-conditioned eigenvectors) with spectral radius <= r_hi."""
+    A = np.zeros((order, order))
+    i = 0
+    while i + 1 < order:
+        r = rng.uniform(r_lo, r_hi)
+        th = rng.uniform(0.02 * np.pi, 0.98 * np.pi)
+        A[i:i + 2, i:i + 2] = r * np.array([[np.cos(th), -np.sin(th)], [np.sin(th), np.cos(th)]])
+        i += 2
+    if i < order:
+        A[i, i] = rng.uniform(r_lo, r_hi) * rng.choice([-1.0, 1.0])
+    Q, _ = np.linalg.qr(rng.standard_normal((order, order)))
+    return Q @ A @ Q.T
+
+
+def rec_problem(seed, batch=2, length=4096, order=2, dtype="f32", coef="shared", v0=True, r_hi=0.99):
+    """Inputs of the bare recurrence v(n+1) = A v(n) + z(n) (Listing 1), float64
+    numpy rounded to dtype: A (M, M) or (B, M, M), v0 (B, M), z, gv (B, N, M)."""
+    rng = np.random.default_rng(seed)
+    t = np_dtype(dtype)
+    r = lambda a: np.asarray(a).astype(t).astype(np.float64)
+    if coef == "shared":
+        A = r(stable_matrix(rng, order, r_hi=r_hi))
+    else:
+        A = r(np.stack([stable_matrix(rng, order, r_hi=r_hi) for _ in range(batch)]))
+    z = r(rng.standard_normal((batch, length, order)))
+    gv = r(rng.standard_normal((batch, length, order)))
+    return dict(form="ss", A=A, z=z, gv=gv, v0=r(0.1 * rng.standard_normal((batch, order))) if v0 else None,
+                dtype=dtype)

@@ -293,3 +293,41 @@ def test_batched_shared_is_sum_of_sequences(orc):
     tot = sum(orc.lti(1, p["b"], p["a"], p["x"][i], p["zi"][i], p["gy"][i], p["gzf"][i])["gb"]
               for i in range(5))
     assert rel(o["gb"], tot) < 1e-14
+
+
+@pytest.mark.parametrize("M,N", [(1, 1), (2, 7), (2, 64), (3, 40), (4, 33)])
+def test_recurrence_equals_autograd_of_listing1_loop(orc, M, N):
+    """Bare recurrence: oracle.recurrence against torch autograd
+    through the plain loop of Listing 1's forward (restated):
+    v(n+1) = A v(n) + z(n), loss = sum gv * v(1..N)."""
+    import torch
+    from paper_2511_14390_b200 import inputs
+    rng = np.random.default_rng(700 + 10 * M + N)
+    A = inputs.stable_matrix(rng, M)
+    v0, z, gv = rng.standard_normal(M), rng.standard_normal((N, M)), rng.standard_normal((N, M))
+    At = torch.tensor(A, requires_grad=True)
+    v0t = torch.tensor(v0, requires_grad=True)
+    zt = torch.tensor(z, requires_grad=True)
+    vn, outs = v0t, []
+    for n in range(N):
+        vn = At @ vn + zt[n]
+        outs.append(vn)
+    v = torch.stack(outs)
+    (v * torch.tensor(gv)).sum().backward()
+    o = orc.recurrence(A, v0, z, gv)
+    np.testing.assert_allclose(o["v"], v.detach().numpy(), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(o["gz"], zt.grad.numpy(), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(o["gv0"], v0t.grad.numpy(), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(o["gA"], At.grad.numpy(), rtol=0, atol=1e-12)
+
+
+def test_recurrence_closed_form_impulse():
+    """v(n) = A^n v0 for z = 0 (Eq.11's unrolled form)."""
+    import oracle
+    from paper_2511_14390_b200 import inputs
+    rng = np.random.default_rng(777)
+    A = inputs.stable_matrix(rng, 3)
+    v0 = rng.standard_normal(3)
+    o = oracle.recurrence(A, v0, np.zeros((20, 3)))
+    for n in range(1, 21):
+        np.testing.assert_allclose(o["v"][n - 1], np.linalg.matrix_power(A, n) @ v0, rtol=0, atol=1e-12)

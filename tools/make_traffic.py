@@ -14,7 +14,7 @@ import re
 import sys
 from collections import OrderedDict, defaultdict
 
-KIND = [(r"lti_prep_kernel", "lti_prep"), (r"lti_fwd_kernel", "lti_fwd"), (r"lti_bwd", "lti_bwd"),
+KIND = [(r"rec_fwd_kernel", "rec_fwd"), (r"rec_bwd_kernel", "rec_bwd"), (r"lti_prep_kernel", "lti_prep"), (r"lti_fwd_kernel", "lti_fwd"), (r"lti_bwd", "lti_bwd"),
         (r"tv_phi2?_kernel", "tv_phi"), (r"tv_(group|groupchain|expand|chain)_kernel", "tv_chain"), (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?0>", "tv_fwd"),
         (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?1>", "tv_bwd_agg"),
         (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?2>", "tv_bwd")]
@@ -71,7 +71,8 @@ def main():
             a[2] += d.get("dram__bytes_read.sum", 0.0)
             a[3] += d.get("dram__bytes_write.sum", 0.0)
         traffic[w] = {k: (a[2] + a[3]) / a[0] for k, a in agg.items()}
-        steps = agg["tv_fwd"][0] if "tv_fwd" in agg else agg["lti_fwd"][0]
+        fk = next(k for k in ("tv_fwd", "rec_fwd", "lti_fwd") if k in agg)
+        steps = agg[fk][0]
         tot = sum(a[1] for a in agg.values()) / steps
         lines.append(f"== {w}: {steps} steps, ncu cold-cache serialised replay; per launch and share of the step")
         for k, a in agg.items():

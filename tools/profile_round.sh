@@ -7,7 +7,7 @@
 set -u
 TAG=${1:-r01}
 shift || true
-WLS=${*:-"c2 c1 c4 c5 c3"}
+WLS=${*:-"c2 c1 c4 c5 c3 f1"}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > "$OUT/gpu.txt" 2>&1
