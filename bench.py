@@ -327,6 +327,8 @@ def run_e2e(args, prob, stream, dev, world):
     steps = max(3, min(args.steps, 20))
     s_h2d = torch.cuda.Stream(device=dev)
     s_d2h = torch.cuda.Stream(device=dev)
+    s_h2d2 = torch.cuda.Stream(device=dev)       # second copy of each direction runs concurrently
+    s_d2h2 = torch.cuda.Stream(device=dev)
     ev = lambda: torch.cuda.Event()
     h2d_done = [ev() for _ in range(nbuf)]
     comp_done = [ev() for _ in range(nbuf)]
@@ -339,8 +341,11 @@ def run_e2e(args, prob, stream, dev, world):
         with torch.cuda.stream(s_h2d):
             if used[k]:
                 s_h2d.wait_event(comp_done[k])          # the kernels of step i-2 have read set k
+            s_h2d2.wait_stream(s_h2d)
             s["x"].copy_(hx[k], non_blocking=True)
-            s["gy"].copy_(hgy[k], non_blocking=True)
+            with torch.cuda.stream(s_h2d2):
+                s["gy"].copy_(hgy[k], non_blocking=True)
+            s_h2d.wait_stream(s_h2d2)
             h2d_done[k].record(s_h2d)
         stream.wait_event(h2d_done[k])
         if used[k]:
@@ -352,10 +357,13 @@ def run_e2e(args, prob, stream, dev, world):
             comp_done[k].record(stream)
         with torch.cuda.stream(s_d2h):
             s_d2h.wait_event(comp_done[k])
-            for name in big:
-                hbig[k][name].copy_(s[name], non_blocking=True)
+            s_d2h2.wait_stream(s_d2h)
+            for j, name in enumerate(big):
+                with torch.cuda.stream(s_d2h2 if j % 2 else s_d2h):
+                    hbig[k][name].copy_(s[name], non_blocking=True)
             for h, d in zip(hsmall[k], small_dev[k]):
                 h.copy_(d, non_blocking=True)
+            s_d2h.wait_stream(s_d2h2)
             d2h_done[k].record(s_d2h)
         used[k] = True
 
