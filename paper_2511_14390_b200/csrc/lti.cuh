@@ -1107,10 +1107,12 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
     if (p.gx != nullptr) tile_store<T, TS>(static_cast<T*>(p.gx) + roff, dys, p0, p.Tlen, p.vec);
     IIRG_TRACE(p.trace, tk, 5);
 
-    if (p.want_coef) bwd_finalize<T, M, FORM>(p, tk, seq, jt, tb, s_red);
+    // the look-back slots are no longer needed: count this CTA out first, so the
+    // gradient finalize of the last CTAs is the kernel's only tail
     IIRG_TRACE(p.trace, tk, 10);
     cta_exit(cw, ep, gridDim.x);
     IIRG_TRACE(p.trace, tk, 11);
+    if (p.want_coef) bwd_finalize<T, M, FORM>(p, tk, seq, jt, tb, s_red);
     span_exit(p.span);
 }
 
@@ -1321,10 +1323,10 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
     }
     __syncthreads();
     IIRG_TRACE(p.trace, tk, 5);
-    if (p.want_coef) bwd_finalize<T, M, 1>(p, tk, seq, jt, tb, s_red);
     IIRG_TRACE(p.trace, tk, 10);
     cta_exit(cw, ep, gridDim.x);
     IIRG_TRACE(p.trace, tk, 11);
+    if (p.want_coef) bwd_finalize<T, M, 1>(p, tk, seq, jt, tb, s_red);
     span_exit(p.span);
 }
 

@@ -370,8 +370,8 @@ __global__ void __launch_bounds__(NT) rec_bwd_kernel(const LtiBwdArgs p) {
     IIRG_TRACE(p.trace, tk, 4);
     if (p.gx != nullptr) tile_store<T, TE>(static_cast<T*>(p.gx) + roff, gs, p0 * M, rowlen, p.vec);
     IIRG_TRACE(p.trace, tk, 5);
-    if (p.want_coef) bwd_finalize<T, M, 2>(p, tk, seq, jt, tb, s_red);
     cta_exit(cw, ep, gridDim.x);
+    if (p.want_coef) bwd_finalize<T, M, 2>(p, tk, seq, jt, tb, s_red);
     span_exit(p.span);
 }
 

@@ -53,6 +53,39 @@ def main():
                            prob.tb, st["gx"], prob.gb, prob.ga, prob.gzi, prob.ws, prob.wb, s)
             B.iir_debug_trace(None)
         torch.cuda.synchronize()
+    # the same step captured in a CUDA graph (the bench's timed mode: PDL overlaps the launches)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=s):
+        B.iir_debug_trace(buf)
+        B.iir_forward(prob.desc, prob.b, prob.a, st["x"], prob.zi, st["y"], prob.zf, prob.tape, prob.tb,
+                      prob.ws, prob.wb, s)
+        B.iir_debug_trace(buf2)
+        B.iir_backward(prob.desc, st["gy"], prob.gzf, prob.b, prob.a, st["x"], st["y"], prob.zi, prob.tape,
+                       prob.tb, st["gx"], prob.gb, prob.ga, prob.gzi, prob.ws, prob.wb, s)
+        B.iir_debug_trace(None)
+    torch.cuda.synchronize()
+    for rep in range(3):
+        reset(buf)
+        reset(buf2)
+        gr.replay()
+        torch.cuda.synchronize()
+    g1 = buf[ntot * 16:].cpu().numpy().astype(np.float64)
+    g2 = buf2[ntot * 16:].cpu().numpy().astype(np.float64)
+    gt0 = g1[0]
+    print("== one step in a CUDA graph, kernel spans (us from prep entry): " + ", ".join(
+        f"{k} [{(v[0] - gt0) / 1e3:.2f}, {(v[1] - gt0) / 1e3:.2f}]" for k, v in
+        {"prep": (g1[0], g1[1]), "fwd": (g1[2], g1[3]), "bwd": (g2[4], g2[5])}.items()))
+    reset(buf)
+    reset(buf2)
+    with torch.cuda.stream(s):
+        B.iir_debug_trace(buf)
+        B.iir_forward(prob.desc, prob.b, prob.a, st["x"], prob.zi, st["y"], prob.zf, prob.tape, prob.tb,
+                      prob.ws, prob.wb, s)
+        B.iir_debug_trace(buf2)
+        B.iir_backward(prob.desc, st["gy"], prob.gzf, prob.b, prob.a, st["x"], st["y"], prob.zi, prob.tape,
+                       prob.tb, st["gx"], prob.gb, prob.ga, prob.gzi, prob.ws, prob.wb, s)
+        B.iir_debug_trace(None)
+    torch.cuda.synchronize()
     a1 = buf[ntot * 16:].cpu().numpy().astype(np.float64)
     a2 = buf2[ntot * 16:].cpu().numpy().astype(np.float64)
     t0 = a1[0]
