@@ -521,7 +521,8 @@ def main():
         dom = max(r["ktimes"], key=lambda k: r["ktimes"][k][0])
         tot, n = r["ktimes"][dom]
         avg_ms = tot / n
-        per_launch = abytes.get(dom, 0) * w["batch"] * w["length"]
+        # a kind launched k times per step (three-phase mode) moves its bytes over k launches
+        per_launch = abytes.get(dom, 0) * w["batch"] * w["length"] / max(1.0, n / args.steps)
         achieved = per_launch / (avg_ms * 1e-3) / 1e9
         tr = load_traffic(w).get(dom)
         step_kernel_ms = sum(t for t, _ in r["ktimes"].values()) / args.steps
