@@ -59,9 +59,13 @@ def algorithmic_bytes(w):
                 "tv_bwd": (2 * M + 3) * s}
     # HBM bytes per kernel the method must move: fwd reads x, writes y (+u for DF);
     # bwd reads dy, x, y (TDF) or dy, u (DF) and writes dx: 24 B/sample in fp32
+    # three-phase schedule: lti_red_fwd reads x, lti_red_bwd reads dy (the emit
+    # kernels then re-read them, counted in their own bytes: from L2 when the
+    # working set fits); lti_cscan moves M fp64 per tile only
+    red = {"lti_red_fwd": s, "lti_red_bwd": s, "lti_cscan": 0}
     if w["form"] == "tdf":
-        return {"lti_fwd": 2 * s, "lti_bwd": 4 * s}
-    return {"lti_fwd": 3 * s, "lti_bwd": 3 * s}
+        return dict(red, lti_fwd=2 * s, lti_bwd=4 * s)
+    return dict(red, lti_fwd=3 * s, lti_bwd=3 * s)
 
 
 def step_min_bytes(w):
@@ -183,7 +187,8 @@ class Problem:
         self.gb = None if self.b is None else torch.empty_like(self.b)
         self.ga = None if w["coef"] == "per_sample" else torch.empty_like(self.a)
         # the workspace is cleared once; every completed call leaves it cleared
-        self.desc = B.make_desc(Bsz, T, M, w["form"], td, mode, flags=B.IIR_FLAG_WS_READY)
+        sched = {"auto": 0, "1p": B.IIR_FLAG_SINGLE_PASS, "3p": B.IIR_FLAG_THREE_PHASE}[w.get("scan", "auto")]
+        self.desc = B.make_desc(Bsz, T, M, w["form"], td, mode, flags=B.IIR_FLAG_WS_READY | sched)
         self.tb = B.iir_tape_bytes(self.desc)
         self.wb = B.iir_workspace_bytes(self.desc)
         self.tape = torch.empty(self.tb, dtype=torch.uint8, device=dev)
@@ -493,8 +498,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scan", default="auto", choices=["auto", "1p", "3p"],
+                    help="LTI scan schedule: auto (by tile count), single-pass or three-phase")
     args = ap.parse_args()
-    w = dict(WORKLOADS[args.workload], key=args.workload)
+    w = dict(WORKLOADS[args.workload], key=args.workload, scan=args.scan)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -542,7 +549,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic (seeded Gaussian signals, random stable filters)",
         "config": {"workload": w["desc"], "batch_per_gpu": w["batch"], "length": w["length"], "order": w["order"],
-                   "form": w["form"], "coef": w["coef"],
+                   "form": w["form"], "coef": w["coef"], "scan_schedule": w["scan"],
                    "l2": f"{r['nsets']} rotating input/output buffer sets x {r['set_bytes'] / 2**20:.0f} MiB "
                          f"(> 2x L2 = {2 * r['L2'] / 2**20:.0f} MiB)",
                    "timing": "CUDA graph of K steps" if r["graph"] else "eager launches",

@@ -14,13 +14,15 @@ import threading
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libiirgrad.so")
+LIB_PATH = os.environ.get("IIRG_LIB") or os.path.join(HERE, "lib", "libiirgrad.so")   # IIRG_LIB: build variants
 
 IIR_OK, IIR_EINVAL, IIR_EUNSUPPORTED, IIR_ECUDA, IIR_EWORKSPACE = range(5)
 IIR_DF2, IIR_TDF2, IIR_SS = 0, 1, 2
 IIR_F32, IIR_F64 = 0, 1
 IIR_COEF_SHARED, IIR_COEF_PER_SEQ, IIR_COEF_PER_SAMPLE = 0, 1, 2
 IIR_FLAG_WS_READY = 1
+IIR_FLAG_SINGLE_PASS = 2
+IIR_FLAG_THREE_PHASE = 4
 
 FORMS = {"df": IIR_DF2, "tdf": IIR_TDF2, "ss": IIR_SS, IIR_DF2: IIR_DF2, IIR_TDF2: IIR_TDF2, IIR_SS: IIR_SS}
 DTYPES = {torch.float32: IIR_F32, torch.float64: IIR_F64}

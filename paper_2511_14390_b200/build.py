@@ -18,9 +18,13 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "build")
+# Experiment variants (never the default build): IIRG_VARIANT=name IIRG_DEFS="-DX=1 ..."
+# builds build_<name>/ and lib/libiirgrad_<name>.so; load one with IIRG_LIB=<path>.
+VARIANT = os.environ.get("IIRG_VARIANT", "")
+DEFS = os.environ.get("IIRG_DEFS", "").split() if VARIANT else []
+BUILD = os.path.join(HERE, "build" + (f"_{VARIANT}" if VARIANT else ""))
 LIBDIR = os.path.join(HERE, "lib")
-LIB = os.path.join(LIBDIR, "libiirgrad.so")
+LIB = os.path.join(LIBDIR, "libiirgrad" + (f"_{VARIANT}" if VARIANT else "") + ".so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -56,7 +60,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
 
     def compile_one(so):
         s, o = so
-        cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", s, "-o", o + ".tmp"]
+        cmd = [NVCC] + FLAGS + DEFS + (["-Xptxas", "-v"] if verbose else []) + ["-c", s, "-o", o + ".tmp"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {s}:\n{r.stdout}\n{r.stderr}")

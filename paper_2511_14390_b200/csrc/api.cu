@@ -27,7 +27,8 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
 
 // ------------------------------------------------------- instrumentation ----
 static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_phi", "tv_chain", "tv_fwd",
-                                        "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd"};
+                                        "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd", "lti_red_fwd",
+                                        "lti_red_bwd", "lti_cscan"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;
@@ -148,6 +149,8 @@ static Layout layout(const iir_desc_t* d) {
     L.ws_sent_bytes = o - L.ws_sent;
     L.ws_part = o; o += al256(L.ntot * NGP * 8);
     L.ws_part2 = o; o += al256(L.ngroups * NGP * 8);
+    L.ws_car = o; o += al256(L.ntot * M * 8);
+    L.ws_carb = o; o += al256(L.ntot * M * 8);
     L.ws_bytes = o;
     o = 0;
     L.tp_tab = o; o += al256((size_t)L.ncoef * tab_size(M) * 8);
@@ -260,6 +263,7 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     fa.tab = reinterpret_cast<const double*>(t + L.tp_tab);
     fa.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
     fa.cw = carry_ws(L, w, false);
+    fa.car = reinterpret_cast<double*>(w + L.ws_car);
     fa.B = d->batch; fa.Tlen = d->length; fa.ntiles = (int)L.ntiles; fa.vec = vec;
     fa.trace = g_trace;
     fa.span = g_trace == nullptr ? nullptr : g_trace + L.ntot * 16 + 2;   // [prep][fwd][bwd]
@@ -316,6 +320,7 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     ba.tab = reinterpret_cast<const double*>(t + L.tp_tab);
     ba.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
     ba.cw = carry_ws(L, w, true);
+    ba.car = reinterpret_cast<double*>(w + L.ws_carb);
     ba.B = d->batch; ba.Tlen = d->length; ba.ntiles = (int)L.ntiles; ba.vec = vec;
     ba.trace = g_trace;
     ba.span = g_trace == nullptr ? nullptr : g_trace + L.ntot * 16 + 4;

@@ -26,8 +26,11 @@ def to_dev(a, dtype):
     return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float64).to(dtype).cuda()
 
 
-def run_lti_gpu(p, coef_mode=None, want=("y", "zf", "gx", "gb", "ga", "gzi"), repeat=1, stream=None):
-    """Forward + backward through iir_forward / iir_backward.  Returns numpy fp64."""
+def run_lti_gpu(p, coef_mode=None, want=("y", "zf", "gx", "gb", "ga", "gzi"), repeat=1, stream=None, flags=0,
+                flags_bwd=None):
+    """Forward + backward through iir_forward / iir_backward.  Returns numpy fp64.
+    `flags` (iir_flags_t, e.g. the scan schedule) for the forward; the backward
+    uses `flags_bwd` when given, else the same."""
     td = torch.float32 if p["dtype"] == "f32" else torch.float64
     x = to_dev(p["x"], td)
     b = to_dev(p["b"], td)
@@ -39,7 +42,8 @@ def run_lti_gpu(p, coef_mode=None, want=("y", "zf", "gx", "gb", "ga", "gzi"), re
     M = b.shape[-1] - 1
     if coef_mode is None:
         coef_mode = B.IIR_COEF_SHARED if b.dim() == 1 else B.IIR_COEF_PER_SEQ
-    desc = B.make_desc(Bsz, T, M, p["form"], td, coef_mode)
+    desc = B.make_desc(Bsz, T, M, p["form"], td, coef_mode, flags=flags)
+    desc_b = B.make_desc(Bsz, T, M, p["form"], td, coef_mode, flags=flags if flags_bwd is None else flags_bwd)
     tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
     tape = torch.empty(tb, dtype=torch.uint8, device="cuda")
     ws = torch.empty(wb, dtype=torch.uint8, device="cuda")
@@ -51,7 +55,7 @@ def run_lti_gpu(p, coef_mode=None, want=("y", "zf", "gx", "gb", "ga", "gzi"), re
     gzi = torch.full((Bsz, M), float("nan"), dtype=td, device="cuda") if "gzi" in want else None
     for _ in range(repeat):
         B.iir_forward(desc, b, a, x, zi, y, zf, tape, tb, ws, wb, stream)
-        B.iir_backward(desc, gy, gzf, b, a, x, y, zi, tape, tb, gx, gb, ga, gzi, ws, wb, stream)
+        B.iir_backward(desc_b, gy, gzf, b, a, x, y, zi, tape, tb, gx, gb, ga, gzi, ws, wb, stream)
     torch.cuda.synchronize()
     out = {"y": y, "zf": zf, "gx": gx, "gb": gb, "ga": ga, "gzi": gzi}
     return {k: (None if v is None else v.double().cpu().numpy()) for k, v in out.items()}
