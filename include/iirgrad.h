@@ -105,13 +105,13 @@ typedef enum {
      * it), so iir_forward / iir_backward skip their cudaMemsetAsync of it.  Without
      * this flag every call first clears the workspace's counters itself.           */
     IIR_FLAG_WS_READY = 1,
-    /* LTI scan schedule (default: chosen per call from the
-     * tile count).  SINGLE_PASS: one kernel per direction, carries by decoupled
-     * look-back across resident tiles (best while every tile of the call is
-     * resident at once).  THREE_PHASE: tile aggregates (streaming), a per-sequence
-     * fp64 carry scan, then emission from the precomputed carries (best once the
-     * call spans several waves of tiles).  Both give the same result up to fp64
-     * rounding of the carries; the bare recurrence (IIR_SS) is always single-pass. */
+    /* LTI scan schedule (default: SINGLE_PASS).
+     * SINGLE_PASS: one kernel per direction, carries by decoupled look-back across
+     * resident tiles.  THREE_PHASE: tile aggregates (streaming), a per-sequence
+     * fp64 carry scan, then emission from the precomputed carries (no inter-CTA
+     * waits, one more pass over the data; slower on the BASELINE shapes, see
+     * DESIGN.md).  Both give the same result up to fp64 rounding of the carries;
+     * the bare recurrence (IIR_SS) is always single-pass. */
     IIR_FLAG_SINGLE_PASS = 2,
     IIR_FLAG_THREE_PHASE = 4
 } iir_flags_t;

@@ -35,7 +35,21 @@ template <int M> struct Tab {
     static constexpr int COEF = PQ + LEVELS * 32 * M2; // b'[0..M], a'[0..M], c[0..M-1]
     static constexpr int A0 = COEF + 3 * M + 2;        // a0 (un-normalised)
     static constexpr int SIZE = (A0 + 1 + 31) / 32 * 32;
+    // [0, STAGE) is staged in shared memory: the small tables always, the
+    // per-lane carry-in powers A_f^(L t) for M <= 4 and the look-back powers of
+    // levels 0, 1 for M <= 2 (smaller orders: the round trips they save sit on
+    // every tile's critical path; larger orders: they would cost occupancy)
+    static constexpr int STAGE = M <= 2 ? PQ + 2 * 32 * M2 : (M <= 4 ? PQ : SMALL);
 };
+
+// acc += P v with P = A_f^(L t) (the carry into lane t's chunk), staged or global.
+template <int M, bool TR>
+__device__ __forceinline__ void mv_plt(const double* st, const double* __restrict__ tb, int t, const double (&v)[M],
+                                       double (&acc)[M]);
+// acc += P v with P = A_f^(k 32^l TS) (look-back level l), staged or global.
+template <int M, bool TR>
+__device__ __forceinline__ void mv_pq(const double* st, const double* __restrict__ tb, int l, int k,
+                                      const double (&v)[M], double (&acc)[M]);
 
 // acc += P v (TR = false) or P^T v (TR = true); P row-major M x M (fp64).
 template <int M, bool TR>
@@ -109,6 +123,20 @@ __device__ __forceinline__ void mv_acc_lane_s(const double* P, int stride, int t
         for (int j = 0; j < M; ++j) s = fma(P[(TR ? j * M + i : i * M + j) * stride + t], v[j], s);
         acc[i] = s;
     }
+}
+
+template <int M, bool TR>
+__device__ __forceinline__ void mv_plt(const double* st, const double* __restrict__ tb, int t, const double (&v)[M],
+                                       double (&acc)[M]) {
+    if constexpr (Tab<M>::STAGE > Tab<M>::PLT) mv_acc_lane_s<M, TR>(st + Tab<M>::PLT, 32, t, v, acc);
+    else mv_acc_lane<M, TR>(tb + Tab<M>::PLT, 32, t, v, acc);
+}
+template <int M, bool TR>
+__device__ __forceinline__ void mv_pq(const double* st, const double* __restrict__ tb, int l, int k,
+                                      const double (&v)[M], double (&acc)[M]) {
+    constexpr int M2 = M * M;
+    if (Tab<M>::STAGE >= Tab<M>::PQ + (l + 1) * 32 * M2) mv_acc_lane_s<M, TR>(st + Tab<M>::PQ + l * 32 * M2, 32, k, v, acc);
+    else mv_acc_lane<M, TR>(tb + Tab<M>::PQ + l * 32 * M2, 32, k, v, acc);
 }
 
 // Programmatic dependent launch (PTX griddepcontrol).
@@ -400,12 +428,12 @@ __device__ __forceinline__ void load_coefs(const double* __restrict__ tb, T (&bc
 
 template <int M>
 __device__ __forceinline__ void stage_small_async(double* st, const double* __restrict__ tb) {
-    for (int i = threadIdx.x; i < Tab<M>::SMALL; i += blockDim.x) cp_async8(st + i, tb + i);
+    for (int i = threadIdx.x; i < Tab<M>::STAGE; i += blockDim.x) cp_async8(st + i, tb + i);
 }
 // Stage the small power tables (PL | PW | PWT) of this tile's coefficient set.
 template <int M>
 __device__ __forceinline__ void stage_small(double* st, const double* __restrict__ tb) {
-    for (int i = threadIdx.x; i < Tab<M>::SMALL; i += blockDim.x) st[i] = __ldg(tb + i);
+    for (int i = threadIdx.x; i < Tab<M>::STAGE; i += blockDim.x) st[i] = __ldg(tb + i);
 }
 
 // Warp-level inclusive Kogge-Stone scan of chunk aggregates in fp64:
@@ -550,7 +578,7 @@ __device__ __forceinline__ void wait_slot(const double* src, double (&v)[M]) {
 // bitwise deterministic.  A tile that closes a level-(l+1) block publishes
 // AGG^(l+1) = Q_l T_l + AGG^(l)_own as soon as T_l is known.
 template <int M, bool TR>
-__device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int lane, int jt, int64_t seq,
+__device__ __forceinline__ void tile_carry(const double* st, const double* __restrict__ tb, int lane, int jt, int64_t seq,
                                            const double (&X0)[M], double (&G)[M], const CarryWs& cw,
                                            double (&X)[M], unsigned long long* trace = nullptr,
                                            unsigned tk = 0) {
@@ -559,7 +587,7 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
     __shared__ double s_T[LEVELS][M];
 #pragma unroll
     for (int i = 0; i < M; ++i) X[i] = X0[i];
-    if (jt == 0) mv_acc_lane<M, TR>(tb + TB::PQ, 32, 1, X0, G);   // tile 0 carries the initial state
+    if (jt == 0) mv_pq<M, TR>(st, tb, 0, 1, X0, G);               // tile 0 carries the initial state
     publish<M>(cw.agg[0] + (seq * cw.nblk[0] + jt) * M, G, lane);
     if (jt == 0) return;
     // levels 0 and 1 are read up front (one round trip); deeper levels, used only
@@ -587,7 +615,7 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
                 if (l >= PF) load_slot<M>(cw.agg[l] + (seq * cw.nblk[l] + (jt >> (5 * l)) - dl[l] + lane) * M, V[l]);
                 if (!slot_ready<M>(V[l]))
                     wait_slot<M>(cw.agg[l] + (seq * cw.nblk[l] + (jt >> (5 * l)) - dl[l] + lane) * M, V[l]);
-                mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, dl[l] - 1 - lane, V[l], Tv);
+                mv_pq<M, TR>(st, tb, l, dl[l] - 1 - lane, V[l], Tv);
             }
             warp_sum<M>(Tv);
         }
@@ -598,7 +626,7 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
         }
         closing = closing && dl[l] == 31;
         if (closing && l + 1 < cw.nlev) {
-            mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, 1, Tv, Own);   // Own = Q_l T_l + Own
+            mv_pq<M, TR>(st, tb, l, 1, Tv, Own);                          // Own = Q_l T_l + Own
             const int64_t bi = seq * cw.nblk[l + 1] + (jt >> (5 * (l + 1)));
             publish<M>(cw.agg[l + 1] + bi * M, Own, lane);
         }
@@ -613,7 +641,7 @@ __device__ __forceinline__ void tile_carry(const double* __restrict__ tb, int la
             double R2[M];
 #pragma unroll
             for (int i = 0; i < M; ++i) R2[i] = s_T[l][i];
-            if (l + 1 < cw.nlev) mv_acc_lane<M, TR>(tb + TB::PQ + l * 32 * M2, 32, dl[l], R, R2);
+            if (l + 1 < cw.nlev) mv_pq<M, TR>(st, tb, l, dl[l], R, R2);
 #pragma unroll
             for (int i = 0; i < M; ++i) R[i] = R2[i];
         }
@@ -665,9 +693,8 @@ __device__ __forceinline__ unsigned carry_bank(CarryWs& cw) {
 __device__ __forceinline__ void rearm_other_bank(const CarryWs& cw, unsigned ep, unsigned cta, unsigned nctas) {
     // the other bank is one contiguous range starting at agg[0] -/+ bank
     double* other = cw.agg[0] + ((ep & 1u) ? -cw.bank : cw.bank);
-    const int64_t per = (cw.bank + nctas - 1) / nctas;
-    const int64_t e0 = (int64_t)cta * per, e1 = min(e0 + per, cw.bank);
-    for (int64_t i = e0 + threadIdx.x; i < e1; i += blockDim.x) __stcg(other + i, sentinel());
+    for (int64_t i = (int64_t)cta * blockDim.x + threadIdx.x; i < cw.bank; i += (int64_t)nctas * blockDim.x)
+        __stcg(other + i, sentinel());
 }
 __device__ __forceinline__ void cta_exit(const CarryWs& cw, unsigned ep, unsigned nctas) {
     __shared__ unsigned s_last;
@@ -682,7 +709,7 @@ struct Smem {
     static constexpr int TS = NT * Chunk<T, M>::L;
     static constexpr int PT = pidx<T>(TS);               // one padded tile
     static constexpr int PTH = pidx<T>(TS + HALO);       // padded tile with u history
-    static constexpr size_t tab_bytes = ((size_t)Tab<M>::SMALL * 8 + 15) / 16 * 16;
+    static constexpr size_t tab_bytes = ((size_t)Tab<M>::STAGE * 8 + 15) / 16 * 16;
     static constexpr size_t fwd(int form) { return tab_bytes + (size_t)(PT + (form == 0 ? PT : 0)) * sizeof(T); }
     static constexpr size_t bwd_tdf() { return tab_bytes + (size_t)PT * sizeof(T); }
     static constexpr size_t bwd(int form) {
@@ -777,7 +804,7 @@ __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const 
         for (int i = 0; i < M; ++i) X0[i] = (zi != nullptr && jt == 0) ? (double)zi[seq * M + i] : 0.0;
         IIRG_TRACE(p.trace, tk, 2);
         if constexpr (PRE) load_carry<M>(p.car, seq * p.ntiles + jt, X);
-        else tile_carry<M, false>(tb, lane, jt, seq, X0, G, cw, X, p.trace, tk);
+        else tile_carry<M, false>(st, tb, lane, jt, seq, X0, G, cw, X, p.trace, tk);
         IIRG_TRACE(p.trace, tk, 3);
         if (lane < NW) {                           // state entering warp `lane`
             double xw[M];
@@ -794,7 +821,7 @@ __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const 
         double xw[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
-        mv_acc_lane<M, false>(tb + TB::PLT, 32, lane, xw, E);
+        mv_plt<M, false>(st, tb, lane, xw, E);
     }
     T vin[M];
 #pragma unroll
@@ -875,12 +902,15 @@ __device__ __forceinline__ void bwd_load_u(const LtiBwdArgs& p, int64_t seq, int
 template <int M, int FORM> constexpr int n_partials() { return FORM == 2 ? M * M : 2 * M + 1; }
 
 template <typename T, int M, int FORM>
-__device__ __forceinline__ void bwd_finalize(const LtiBwdArgs& p, unsigned tk, int64_t seq, int jt,
-                                             const double* __restrict__ tb,
+// Also counts the CTA out of the look-back (cw != NULL): its atomic and the
+// partial-sum publication run concurrently (warps 0 and 1).
+__device__ __forceinline__ void bwd_finalize(const LtiBwdArgs& p, const CarryWs* cw, unsigned ep, unsigned tk,
+                                             int64_t seq, int jt, const double* __restrict__ tb,
                                              const double (*s_red)[n_partials<M, FORM>()]) {
     constexpr int NG = n_partials<M, FORM>();
+    static_assert(NG <= 32, "one lane of warp 1 per partial sum");
     __shared__ double s_G[NG];
-    __shared__ unsigned s_fin;
+    __shared__ unsigned s_fin, s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // fused a8: group of 32 tiles -> group sum; last group of the set -> chain rule.
     // SHARED groups are consecutive tiles in scan order (they complete, and are
@@ -894,18 +924,23 @@ __device__ __forceinline__ void bwd_finalize(const LtiBwdArgs& p, unsigned tk, i
     const int gsize = (int)min((int64_t)32, per_set - (gi << 5));
     double* part = p.partial + cset * per_set * NG;
     double* part2 = p.partial2 + cset * ngroups * NG;
-    if (tid < NG) {
-        double s = 0.0;
+    __syncthreads();                               // s_red complete; the look-back slots are no longer read
+    if (p.want_coef && warp == 1) {
+        if (lane < NG) {
+            double s = 0.0;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) s += s_red[w][tid];
-        __stcg(part + li * NG + tid, s);
-        __threadfence();
+            for (int w = 0; w < NW; ++w) s += s_red[w][lane];
+            __stcg(part + li * NG + lane, s);
+            __threadfence();
+        }
+        __syncwarp();
+        if (lane == 0) s_fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
     }
+    if (cw != nullptr && tid == 0) s_last = (atomicAdd(cw->done, 1u) == gridDim.x - 1u) ? 1u : 0u;
     __syncthreads();
     IIRG_TRACE(p.trace, tk, 8);
-    if (tid == 0) s_fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
-    __syncthreads();
-    if (s_fin) {                                   // last tile of its group
+    if (cw != nullptr && s_last && tid == 0) { *cw->ticket = 0u; *cw->done = 0u; *cw->epoch = ep + 1u; }
+    if (p.want_coef && s_fin) {                    // last tile of its group
         __threadfence();
         reduce_rows<NG>(part + (gi << 5) * NG, gsize, part2 + gi * NG, lane, warp);
         __threadfence();
@@ -1027,7 +1062,7 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
         for (int i = 0; i < M; ++i) X0[i] = (gzf != nullptr && jr == 0) ? (double)gzf[seq * M + i] : 0.0;
         IIRG_TRACE(p.trace, tk, 2);
         if constexpr (PRE) { pdl_wait(); load_carry<M>(p.car, seq * p.ntiles + jr, X); }   // lti_cscan_kernel's carries
-        else tile_carry<M, true>(tb, lane, jr, seq, X0, G, cw, X, p.trace, tk);
+        else tile_carry<M, true>(st, tb, lane, jr, seq, X0, G, cw, X, p.trace, tk);
         IIRG_TRACE(p.trace, tk, 3);
         if (lane < NW) {
             double xw[M];
@@ -1043,7 +1078,7 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
         double xw[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
-        mv_acc_lane<M, true>(tb + TB::PLT, 32, lane, xw, E);
+        mv_plt<M, true>(st, tb, lane, xw, E);
     }
     T din[M];
 #pragma unroll
@@ -1125,9 +1160,8 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
     // the look-back slots are no longer needed: count this CTA out first, so the
     // gradient finalize of the last CTAs is the kernel's only tail
     IIRG_TRACE(p.trace, tk, 10);
-    if (!PRE) cta_exit(cw, ep, gridDim.x);
+    bwd_finalize<T, M, FORM>(p, PRE ? nullptr : &cw, ep, tk, seq, jt, tb, s_red);
     IIRG_TRACE(p.trace, tk, 11);
-    if (p.want_coef) bwd_finalize<T, M, FORM>(p, tk, seq, jt, tb, s_red);
     span_exit(p.span);
 }
 
@@ -1221,7 +1255,7 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
         for (int i = 0; i < M; ++i) X0[i] = (gzf != nullptr && jr == 0) ? (double)gzf[seq * M + i] : 0.0;
         IIRG_TRACE(p.trace, tk, 2);
         if constexpr (PRE) { pdl_wait(); load_carry<M>(p.car, seq * p.ntiles + jr, X); }   // lti_cscan_kernel's carries
-        else tile_carry<M, true>(tb, lane, jr, seq, X0, G, cw, X, p.trace, tk);
+        else tile_carry<M, true>(st, tb, lane, jr, seq, X0, G, cw, X, p.trace, tk);
         IIRG_TRACE(p.trace, tk, 3);
         if (lane < NW) {
             double xw[M];
@@ -1241,13 +1275,21 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
         double xw[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
-        mv_acc_lane<M, true>(tb + TB::PLT, 32, lane, xw, E);
+        mv_plt<M, true>(st, tb, lane, xw, E);
     }
 #pragma unroll
     for (int i = 0; i < M; ++i) d[i] = (T)E[i];
     // a7, pass A: re-run with the exact carry, write g(n) = dz(n)[0] over dy(n).
     // The chunk holding n = 0 also yields grad_zi = dz(-1) (Eq.9, A.3).
-    const bool has_zero = p.gzi != nullptr && p0 + s0 <= 0 && p0 + s0 + L > 0;
+    if (p.gzi != nullptr && p0 + s0 <= 0 && p0 + s0 + L > 0) {   // this chunk holds n = 0: walk down to it
+        T w2[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) w2[i] = d[i];
+        for (int n = s0 + L - 1; n >= (int)(-p0); --n) adj_tdf_step<T, M>(w2, gs[pidx<T>(n)], ac);
+        T* gzi = static_cast<T*>(p.gzi) + seq * M;
+#pragma unroll
+        for (int i = 0; i < M; ++i) gzi[i] = w2[i];
+    }
 #pragma unroll
     for (int g = L / W - 1; g >= 0; --g) {
         V dv = *reinterpret_cast<const V*>(gs + pidx<T>(s0 + g * W));
@@ -1256,11 +1298,6 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
             const T dy = vget(dv, e);
             vset(dv, e, d[0]);
             adj_tdf_step<T, M>(d, dy, ac);           // d <- dz(n-1)
-            if (has_zero && p0 + s0 + g * W + e == 0) {
-                T* gzi = static_cast<T*>(p.gzi) + seq * M;
-#pragma unroll
-                for (int i = 0; i < M; ++i) gzi[i] = d[i];
-            }
         }
         *reinterpret_cast<V*>(gs + pidx<T>(s0 + g * W)) = dv;
     }
@@ -1276,12 +1313,17 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
 #pragma unroll
     for (int k = 0; k < NG; ++k) Gs[k] = T(0);
     T* gxrow = p.gx == nullptr ? nullptr : static_cast<T*>(p.gx) + roff;
+    const bool fast = p.vec && p0 >= 0 && p.gy != nullptr;   // interior tile: no clipping, no NULL dy
 #pragma unroll 4
     for (int k = 0; k < L / W; ++k) {
         const int n0 = (tid + NT * k) * W;             // tile-local
         const int64_t pos = p0 + n0;
         V xv, yv, dyv;
-        if (p.vec && pos >= 0) {
+        if (fast) {
+            xv = ldg_l2(reinterpret_cast<const V*>(xrow + pos));
+            yv = ldg_l2(reinterpret_cast<const V*>(yrow + pos));
+            dyv = ldg_l2(reinterpret_cast<const V*>(gyrow + pos));
+        } else if (p.vec && pos >= 0) {
             xv = ldg_l2(reinterpret_cast<const V*>(xrow + pos));
             yv = ldg_l2(reinterpret_cast<const V*>(yrow + pos));
             dyv = p.gy != nullptr ? ldg_l2(reinterpret_cast<const V*>(gyrow + pos)) : V{};
@@ -1321,7 +1363,7 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
             vset(dxv, e, dx);
         }
         if (gxrow != nullptr) {
-            if (p.vec && pos >= 0) stg_stream(reinterpret_cast<V*>(gxrow + pos), dxv);
+            if (fast || (p.vec && pos >= 0)) stg_stream(reinterpret_cast<V*>(gxrow + pos), dxv);
             else
 #pragma unroll
                 for (int e = 0; e < W; ++e)
@@ -1340,9 +1382,8 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
     __syncthreads();
     IIRG_TRACE(p.trace, tk, 5);
     IIRG_TRACE(p.trace, tk, 10);
-    if (!PRE) cta_exit(cw, ep, gridDim.x);
+    bwd_finalize<T, M, 1>(p, PRE ? nullptr : &cw, ep, tk, seq, jt, tb, s_red);
     IIRG_TRACE(p.trace, tk, 11);
-    if (p.want_coef) bwd_finalize<T, M, 1>(p, tk, seq, jt, tb, s_red);
     span_exit(p.span);
 }
 

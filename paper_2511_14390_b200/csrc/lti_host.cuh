@@ -47,19 +47,6 @@ struct LtiOps {
             }
         });
     }
-    // Tiles the single-pass forward kernel keeps resident at once on this device.
-    static int64_t resident_tiles() {
-        static int64_t cap = 0;
-        static std::once_flag once;
-        std::call_once(once, [] {
-            int dev = 0, sms = 0, per = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, lti_fwd_kernel<T, M, FORM>, NT, SM::fwd(FORM));
-            cap = (int64_t)sms * per;
-        });
-        return cap;
-    }
     // Persistent grid of the reduce kernel: every resident slot, at most one CTA per tile.
     static unsigned red_grid(int64_t ntot) {
         static int64_t cap = 0;
@@ -74,12 +61,13 @@ struct LtiOps {
         });
         return (unsigned)(ntot < cap ? ntot : cap);
     }
-    // Schedule (iir_flags_t): single pass while the whole call fits in one wave of
-    // resident tiles, three-phase beyond.  The same rule for both directions.
-    static bool three_phase(const iir_desc_t* d, const Layout& L) {
+    // Schedule (iir_flags_t).  Default: single pass.  Measured on B200 (DESIGN.md
+    // §6), three-phase lost at every BASELINE shape: its extra pass over the data
+    // costs more issue slots than the look-back waits it removes (C2 44.6 vs 35.5,
+    // C4 181.6 vs 186.2, C5 252 vs 231 us/step), so it is opt-in only.
+    static bool three_phase(const iir_desc_t* d, const Layout&) {
         if (d->flags & IIR_FLAG_SINGLE_PASS) return false;
-        if (d->flags & IIR_FLAG_THREE_PHASE) return true;
-        return L.ntot > resident_tiles();
+        return (d->flags & IIR_FLAG_THREE_PHASE) != 0;
     }
     // a1 prologue, then the scan (PDL throughout: each kernel's loads and local
     // pass overlap its predecessor; it waits before reading the predecessor's output)

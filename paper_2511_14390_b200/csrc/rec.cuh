@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(NT) rec_fwd_kernel(const LtiFwdArgs p) {
 #pragma unroll
         for (int i = 0; i < M; ++i) X0[i] = (v0 != nullptr && jt == 0) ? (double)v0[seq * M + i] : 0.0;
         IIRG_TRACE(p.trace, tk, 2);
-        tile_carry<M, false>(tb, lane, jt, seq, X0, G, cw, X, p.trace, tk);
+        tile_carry<M, false>(st, tb, lane, jt, seq, X0, G, cw, X, p.trace, tk);
         IIRG_TRACE(p.trace, tk, 3);
         if (lane < NW) {
             double xw[M];
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(NT) rec_fwd_kernel(const LtiFwdArgs p) {
         double xw[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
-        mv_acc_lane<M, false>(tb + TB::PLT, 32, lane, xw, E);
+        mv_plt<M, false>(st, tb, lane, xw, E);
     }
 #pragma unroll
     for (int i = 0; i < M; ++i) v[i] = (T)E[i];
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(NT) rec_bwd_kernel(const LtiBwdArgs p) {
 #pragma unroll
         for (int i = 0; i < M; ++i) X0[i] = 0.0;                 // g(N) = 0
         IIRG_TRACE(p.trace, tk, 2);
-        tile_carry<M, true>(tb, lane, jr, seq, X0, G, cw, X, p.trace, tk);
+        tile_carry<M, true>(st, tb, lane, jr, seq, X0, G, cw, X, p.trace, tk);
         IIRG_TRACE(p.trace, tk, 3);
         if (lane < NW) {
             double xw[M];
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(NT) rec_bwd_kernel(const LtiBwdArgs p) {
         double xw[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) xw[i] = s_xw[warp][i];
-        mv_acc_lane<M, true>(tb + TB::PLT, 32, lane, xw, E);
+        mv_plt<M, true>(st, tb, lane, xw, E);
     }
 #pragma unroll
     for (int i = 0; i < M; ++i) s[i] = (T)E[i];
@@ -370,8 +370,7 @@ __global__ void __launch_bounds__(NT) rec_bwd_kernel(const LtiBwdArgs p) {
     IIRG_TRACE(p.trace, tk, 4);
     if (p.gx != nullptr) tile_store<T, TE>(static_cast<T*>(p.gx) + roff, gs, p0 * M, rowlen, p.vec);
     IIRG_TRACE(p.trace, tk, 5);
-    cta_exit(cw, ep, gridDim.x);
-    if (p.want_coef) bwd_finalize<T, M, 2>(p, tk, seq, jt, tb, s_red);
+    bwd_finalize<T, M, 2>(p, &cw, ep, tk, seq, jt, tb, s_red);
     span_exit(p.span);
 }
 
