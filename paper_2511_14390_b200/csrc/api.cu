@@ -46,15 +46,22 @@ static cudaEvent_t ev_get() {
 }
 
 namespace iirg {
+// Under stream capture a plain cudaEventRecord is only a dependency edge: the
+// profiling events must be external record nodes to be timestamped at replay.
+static unsigned rec_flags(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    return cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+}
 LaunchGuard::LaunchGuard(int k, cudaStream_t s) : kind(k), st(s) {
     std::lock_guard<std::mutex> lk(g_pmu);
     if (g_prof_on) { e0 = ev_get(); e1 = ev_get(); }
-    if (e0) cudaEventRecord(e0, st);
+    if (e0) cudaEventRecordWithFlags(e0, st, rec_flags(st));
 }
 iir_status_t LaunchGuard::done() {
     cudaError_t err = cudaGetLastError();
     if (e0) {
-        cudaEventRecord(e1, st);
+        cudaEventRecordWithFlags(e1, st, rec_flags(st));
         std::lock_guard<std::mutex> lk(g_pmu);
         g_pending.push_back({kind, e0, e1});
     }
@@ -354,7 +361,7 @@ int iir_profile_query(int kind, double* total_ms, int64_t* launches) {
     for (auto& r : g_pending) {
         float ms = 0.f;
         cudaEventSynchronize(r.e1);
-        cudaEventElapsedTime(&ms, r.e0, r.e1);
+        if (cudaEventElapsedTime(&ms, r.e0, r.e1) != cudaSuccess) { ms = 0.f; (void)cudaGetLastError(); }
         g_ms[r.kind] += ms;
         g_cnt[r.kind] += 1;
         g_pool.push_back(r.e0);

@@ -6,9 +6,12 @@
 
 namespace iirg {
 
-constexpr int NT = 128;          // threads per CTA (4 warps)
+#ifndef IIRG_NT
+#define IIRG_NT 128
+#endif
+constexpr int NT = IIRG_NT;      // threads per CTA (4 warps)
 constexpr int NW = NT / 32;      // warps per CTA
-constexpr int LOG_NW = 2;
+constexpr int LOG_NW = NW == 2 ? 1 : NW == 4 ? 2 : NW == 8 ? 3 : NW == 16 ? 4 : 5;
 
 constexpr int HALO = 8;          // u-history halo of the DF backward tile (>= M)
 

@@ -723,9 +723,13 @@ struct Smem {
 // for belongs to a CTA that is already running.
 // Minimum resident CTAs per SM requested from ptxas (caps the registers of the
 // high-order instantiations, whose occupancy is otherwise register-bound).
-template <int M> constexpr int fwd_min_blocks() { return M <= 2 ? 8 : (M <= 4 ? 6 : 4); }
-template <int M> constexpr int bwd_min_blocks() { return M <= 4 ? 4 : 3; }
-template <int M> constexpr int bwd_tdf_min_blocks() { return M <= 2 ? 8 : (M <= 4 ? 6 : 4); }
+// (counts for 128-thread CTAs, scaled to NT)
+#ifndef IIRG_MINB2
+#define IIRG_MINB2 8
+#endif
+template <int M> constexpr int fwd_min_blocks() { return (M <= 2 ? IIRG_MINB2 : (M <= 4 ? 6 : 4)) * 128 / NT; }
+template <int M> constexpr int bwd_min_blocks() { return (M <= 4 ? 4 : 3) * 128 / NT > 0 ? (M <= 4 ? 4 : 3) * 128 / NT : 1; }
+template <int M> constexpr int bwd_tdf_min_blocks() { return (M <= 2 ? IIRG_MINB2 : (M <= 4 ? 6 : 4)) * 128 / NT; }
 
 // PRE = true (three-phase mode): the carry entering the tile was computed by
 // lti_red_kernel + lti_cscan_kernel; the tile only emits (no look-back).
