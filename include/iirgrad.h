@@ -137,6 +137,26 @@ iir_status_t iir_backward(const iir_desc_t *desc, const void *grad_y, const void
                           void *grad_x, void *grad_b, void *grad_a, void *grad_zi,
                           void *ws, size_t ws_bytes, iir_stream_t stream);
 
+/* Time-sharded sequences (Eq.10, with the
+ * segment as the chunk).  One sequence is split into `nseg` consecutive segments
+ * of `seg_len` samples (the last may be shorter), one per rank.  Each segment is
+ * first filtered with a zero carry: its forward gives the final state w_j (zf;
+ * segment 0 uses the true zi), its backward the adjoint state at its start
+ * (grad_zi; the last segment uses the true grad_zf).  With P = A_f^seg_len
+ * (A_f = companion(a / a0) for DF, its transpose for TDF):
+ *   reverse = 0:  out = sum_{j < rank} P^(rank-1-j) w_j       (zi of segment rank)
+ *   reverse = 1:  out = sum_{j > rank} (P^T)^(j-rank-1) w_j   (grad_zf of segment rank)
+ * i.e. the exact carry into the segment, after which the segment's forward /
+ * backward with that zi / grad_zf equals the unsharded computation on it.
+ *   desc: the per-segment descriptor (batch B, order M, form DF2 / TDF2, dtype,
+ *         coef_mode SHARED or PER_SEQ); a: (M+1) or (B, M+1), device;
+ *   w:    (nseg, B, M) device, the gathered aggregates; out: (B, M) device
+ *         (zeros for rank 0 forward / rank nseg-1 reverse).
+ * fp64 arithmetic (binary powering of A_f, Horner over the segments), one
+ * launch, no host sync.  IIR_EINVAL on a bad rank / nseg / seg_len / NULL. */
+iir_status_t iir_state_carry(const iir_desc_t *desc, const void *a, const void *w, int32_t nseg, int32_t rank,
+                             int64_t seg_len, int32_t reverse, void *out, iir_stream_t stream);
+
 /* Thread-local message describing the last non-IIR_OK status of this thread. */
 const char *iir_last_error(void);
 int iir_abi_version(void);

@@ -29,7 +29,7 @@ DTYPES = {torch.float32: IIR_F32, torch.float64: IIR_F64}
 
 EXPORTS = ["iir_tape_bytes", "iir_workspace_bytes", "iir_workspace_init", "iir_forward", "iir_backward", "iir_last_error",
            "iir_abi_version", "iir_launch_count", "iir_num_kernels", "iir_kernel_name",
-           "iir_profile_enable", "iir_profile_reset", "iir_profile_query", "iir_debug_trace"]
+           "iir_profile_enable", "iir_profile_reset", "iir_profile_query", "iir_debug_trace", "iir_state_carry"]
 
 
 class Desc(ctypes.Structure):
@@ -72,6 +72,9 @@ def lib():
         L.iir_forward.argtypes = [dp] + [_vp] * 7 + [ctypes.c_size_t, _vp, ctypes.c_size_t, _vp]
         L.iir_backward.restype = ctypes.c_int
         L.iir_backward.argtypes = [dp] + [_vp] * 8 + [ctypes.c_size_t] + [_vp] * 5 + [ctypes.c_size_t, _vp]
+        L.iir_state_carry.restype = ctypes.c_int
+        L.iir_state_carry.argtypes = [dp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
+                                      _vp, _vp]
         L.iir_last_error.restype = ctypes.c_char_p
         L.iir_abi_version.restype = ctypes.c_int
         L.iir_launch_count.restype = ctypes.c_int64
@@ -138,6 +141,12 @@ def iir_backward(desc, grad_y, grad_zf, b, a, x, y, zi, tape, tape_bytes, grad_x
                             _ptr(zi), _ptr(tape), int(tape_bytes), _ptr(grad_x), _ptr(grad_b), _ptr(grad_a),
                             _ptr(grad_zi), _ptr(ws), int(ws_bytes), _stream(stream))
     _check(st, "iir_backward")
+
+
+def iir_state_carry(desc, a, w, nseg, rank, seg_len, reverse, out, stream=None):
+    st = lib().iir_state_carry(ctypes.byref(desc), _ptr(a), _ptr(w), int(nseg), int(rank), int(seg_len),
+                               1 if reverse else 0, _ptr(out), _stream(stream))
+    _check(st, "iir_state_carry")
 
 
 def iir_last_error() -> str:

@@ -28,7 +28,7 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
 // ------------------------------------------------------- instrumentation ----
 static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_phi", "tv_chain", "tv_fwd",
                                         "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd", "lti_red_fwd",
-                                        "lti_red_bwd", "lti_cscan"};
+                                        "lti_red_bwd", "lti_cscan", "state_carry"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;

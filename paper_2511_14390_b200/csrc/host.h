@@ -14,7 +14,7 @@ namespace iirg {
 iir_status_t fail(iir_status_t st, const std::string& msg);
 
 enum Kind { K_LTI_PREP = 0, K_LTI_FWD, K_LTI_BWD, K_TV_PHI, K_TV_CHAIN, K_TV_FWD, K_TV_BWD_AGG, K_TV_BWD, K_REC_FWD,
-            K_REC_BWD, K_LTI_RED_F, K_LTI_RED_B, K_LTI_CSCAN, K_NUM };
+            K_REC_BWD, K_LTI_RED_F, K_LTI_RED_B, K_LTI_CSCAN, K_STATE_CARRY, K_NUM };
 
 // Launch bookkeeping: counts every kernel and (when profiling is on) brackets it
 // with CUDA events on its stream.
