@@ -20,7 +20,10 @@
 
 namespace iirg {
 
-constexpr int TV_SEG = 512;          // samples per segment
+#ifndef IIRG_TV_SEG
+#define IIRG_TV_SEG 512
+#endif
+constexpr int TV_SEG = IIRG_TV_SEG;  // samples per segment
 constexpr int TV_THREADS = 128;      // thread-per-segment kernels
 constexpr int TV_PHI_WARPS = 4;      // warps (segments) per CTA of the Phi kernel
 template <typename T> constexpr int tv_ch() { return sizeof(T) == 4 ? 32 : 16; }   // staged chunk (Phi kernel)

@@ -73,3 +73,18 @@ def test_kernel_names_and_counters():
     names = B.kernel_names()
     assert "lti_fwd" in names and "lti_bwd" in names
     assert B.iir_launch_count() >= 0
+
+
+def test_state_carry_rejects_bad_arguments_before_launch():
+    """iir_state_carry: argument checks return IIR_EINVAL / IIR_EUNSUPPORTED, no launch."""
+    d = B.make_desc(2, 100, 2, "tdf", B.IIR_F32, B.IIR_COEF_SHARED)
+    L = B.lib()
+    fake = 16                                  # never dereferenced: the checks fail first
+    n0 = B.iir_launch_count()
+    assert L.iir_state_carry(ctypes.byref(d), fake, fake, 4, 4, 10, 0, fake, None) == B.IIR_EINVAL   # rank >= nseg
+    assert L.iir_state_carry(ctypes.byref(d), fake, fake, 0, 0, 10, 0, fake, None) == B.IIR_EINVAL   # nseg < 1
+    assert L.iir_state_carry(ctypes.byref(d), fake, fake, 2, 0, -1, 0, fake, None) == B.IIR_EINVAL   # seg_len < 0
+    assert L.iir_state_carry(ctypes.byref(d), None, fake, 2, 0, 10, 0, fake, None) == B.IIR_EINVAL   # a NULL
+    d_ss = B.make_desc(2, 100, 2, "ss", B.IIR_F32, B.IIR_COEF_SHARED)
+    assert L.iir_state_carry(ctypes.byref(d_ss), fake, fake, 2, 0, 10, 0, fake, None) == B.IIR_EUNSUPPORTED
+    assert B.iir_launch_count() == n0

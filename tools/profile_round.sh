@@ -1,9 +1,9 @@
 #!/usr/bin/env bash
 # One gpurun call's worth of round evidence (run from the repo root on the GPU box):
 #   bench lines for every workload, the reference (oracle) arm, per-launch ncu
-#   lists (duration + DRAM bytes) and one `--set full` capture of each
-#   workload family's dominant kernel.  Output: gpurun_out/$TAG/.
-#   usage: tools/profile_round.sh TAG [workloads...]
+#   lists (duration + DRAM bytes) and `--set full` captures of the dominant
+#   kernels (C2 lti_fwd / lti_bwd, C5 lti_fwd / lti_bwd, C3 tv_bwd).
+#   Output: gpurun_out/$TAG/.   usage: tools/profile_round.sh TAG [workloads...]
 set -u
 TAG=${1:-r01}
 shift || true
@@ -22,18 +22,22 @@ for w in $WLS; do
     python bench.py --workload "$w" --steps 2 --warmup 3 --no-graph --no-cpu-baseline > /dev/null 2>&1
   echo "launches $w rc=$?"
 done
-if [[ " $WLS " == *" c2 "* ]]; then
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:lti_bwd -s 4 -c 1 \
-    -o "$OUT/full_c2_lti_bwd" python bench.py --workload c2 --steps 2 --warmup 3 --no-graph --no-cpu-baseline \
-    > "$OUT/full_c2.log" 2>&1
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:lti_fwd -s 4 -c 1 \
-    -o "$OUT/full_c2_lti_fwd" python bench.py --workload c2 --steps 2 --warmup 3 --no-graph --no-cpu-baseline \
-    > "$OUT/full_c2f.log" 2>&1
-  echo "full c2 rc=$?"
-fi
-if [[ " $WLS " == *" c3 "* ]]; then
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:tv_seq_kernel -s 2 -c 1 \
-    -o "$OUT/full_c3_tv_bwd" python bench.py --workload c3 --steps 2 --warmup 3 --no-graph --no-cpu-baseline \
-    > "$OUT/full_c3.log" 2>&1
-  echo "full c3 rc=$?"
-fi
+full() {   # workload kernel-regex skip name
+  timeout 900 ncu --set full --import-source on --clock-control none -k "regex:$2" -s "$3" -c 1 \
+    -o "$OUT/full_$4" python bench.py --workload "$1" --steps 2 --warmup 3 --no-graph --no-cpu-baseline \
+    > "$OUT/full_$4.log" 2>&1
+  echo "full $4 rc=$?"
+}
+[[ " $WLS " == *" c2 "* ]] && { full c2 lti_bwd 4 c2_lti_bwd; full c2 lti_fwd 4 c2_lti_fwd; }
+[[ " $WLS " == *" c5 "* ]] && { full c5 lti_bwd 4 c5_lti_bwd; full c5 lti_fwd 4 c5_lti_fwd; }
+[[ " $WLS " == *" c3 "* ]] && full c3 "tv_seq_kernel" 2 c3_tv_bwd
+# summarise the captures here (gpurun copies back <= 64 MiB): text only, reports dropped
+for r in "$OUT"/full_*.ncu-rep; do
+  [ -e "$r" ] || continue
+  n=$(basename "$r" .ncu-rep)
+  python profiles/ncu_summary.py "$r" "$OUT/${n}_summary.txt" > /dev/null 2>&1
+  python tools/ncu_lines.py "$r" "." 40 > "$OUT/${n}_lines.txt" 2>&1
+  ncu -i "$r" --page raw --csv > "$OUT/${n}_raw.csv" 2>/dev/null
+  rm -f "$r"
+done
+exit 0
