@@ -42,6 +42,22 @@ __device__ __forceinline__ double vget(const double2& v, int i) { return i == 0 
 __device__ __forceinline__ void vset(float4& v, int i, float s)   { if (i == 0) v.x = s; else if (i == 1) v.y = s; else if (i == 2) v.z = s; else v.w = s; }
 __device__ __forceinline__ void vset(double2& v, int i, double s) { if (i == 0) v.x = s; else v.y = s; }
 
+// Blackwell paired fp32 FMA (fma.rn.f32x2 -> FFMA2): two lanes of a 64-bit
+// register pair per instruction; a pair built from one scalar (pk2(s, s)) is
+// folded by ptxas into the instruction's scalar-broadcast operand form.
+__device__ __forceinline__ unsigned long long pk2(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ float lo2(unsigned long long v) { return __uint_as_float((unsigned)(v & 0xffffffffull)); }
+__device__ __forceinline__ float hi2(unsigned long long v) { return __uint_as_float((unsigned)(v >> 32)); }
+
 // Streaming global accesses (no L1 allocation; inputs are read exactly once).
 __device__ __forceinline__ float4 ldg_stream(const float4* p) {
     float4 r;

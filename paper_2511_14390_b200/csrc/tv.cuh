@@ -139,18 +139,6 @@ __global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs 
 // segments at once (half-warp each, (M + 2) / 2 lanes per segment).  Same
 // arithmetic, same order as tv_phi_kernel (bit-identical Phi_k and w_k).
 constexpr int TV_PHI2_WARPS = 2;
-__device__ __forceinline__ unsigned long long pk2(float lo, float hi) {
-    unsigned long long r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-    return r;
-}
-__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
-    unsigned long long r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-__device__ __forceinline__ float lo2(unsigned long long v) { return __uint_as_float((unsigned)(v & 0xffffffffull)); }
-__device__ __forceinline__ float hi2(unsigned long long v) { return __uint_as_float((unsigned)(v >> 32)); }
 
 template <int M>
 __global__ void __launch_bounds__(32 * TV_PHI2_WARPS) tv_phi2_kernel(const TvArgs p) {
