@@ -987,6 +987,8 @@ __device__ __forceinline__ void bwd_load_u(const LtiBwdArgs& p, int64_t seq, int
 // in scan order (they complete, and are reduced, while the kernel runs);
 // PER_SEQ groups are a sequence's tiles.  Fixed reduction order throughout.
 template <int M, int FORM> constexpr int n_partials() { return FORM == 2 ? M * M : 2 * M + 1; }
+constexpr int64_t FLAT_MAX = 8192;   // partial values of a set reduced flat (one round trip) by its last CTA
+
 
 template <typename T, int M, int FORM>
 // Also counts the CTA out of the look-back (cw != NULL): its atomic and the
@@ -1011,6 +1013,9 @@ __device__ __forceinline__ void bwd_finalize(const LtiBwdArgs& p, const CarryWs*
     const int gsize = (int)min((int64_t)32, per_set - (gi << 5));
     double* part = p.partial + cset * per_set * NG;
     double* part2 = p.partial2 + cset * ngroups * NG;
+    // small sets: one counter per set and a flat fixed-order reduction of every
+    // per-tile row by the set's last CTA (one load round trip; no group level)
+    const bool flat = per_set * NG <= FLAT_MAX;
     __syncthreads();                               // s_red complete; the look-back slots are no longer read
     if (p.want_coef && warp == 1) {
         if (lane < NG) {
@@ -1021,13 +1026,63 @@ __device__ __forceinline__ void bwd_finalize(const LtiBwdArgs& p, const CarryWs*
             __threadfence();
         }
         __syncwarp();
-        if (lane == 0) s_fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
+        if (lane == 0) {
+            if (flat) s_fin = (atomicAdd(p.scnt + cset, 1u) == (unsigned)per_set - 1u) ? 3u : 0u;
+            else s_fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
+        }
     }
     if (cw != nullptr && tid == 0) s_last = (atomicAdd(cw->done, 1u) == gridDim.x - 1u) ? 1u : 0u;
     __syncthreads();
     IIRG_TRACE(p.trace, tk, 8);
     if (cw != nullptr && s_last && tid == 0) { *cw->ticket = 0u; *cw->done = 0u; *cw->epoch = ep + 1u; }
-    if (p.want_coef && s_fin) {                    // last tile of its group
+    if (p.want_coef && s_fin == 3u) {              // flat: last tile of the set
+        constexpr int FLAT_RB = (24 / NG) > 0 ? 24 / NG : 1;   // rows per thread per load round trip
+        __threadfence();
+        double acc[NG];
+#pragma unroll
+        for (int k = 0; k < NG; ++k) acc[k] = 0.0;
+        for (int64_t r0 = 0; r0 < per_set; r0 += (int64_t)NT * FLAT_RB) {   // rows tid, tid + NT, ... in order
+            double v[FLAT_RB][NG];
+#pragma unroll
+            for (int b = 0; b < FLAT_RB; ++b) {
+                const int64_t r = r0 + (int64_t)b * NT + tid;
+#pragma unroll
+                for (int k = 0; k < NG; ++k) v[b][k] = r < per_set ? __ldcg(part + r * NG + k) : 0.0;
+            }
+#pragma unroll
+            for (int b = 0; b < FLAT_RB; ++b)
+#pragma unroll
+                for (int k = 0; k < NG; ++k) acc[k] += v[b][k];
+        }
+        __shared__ double s_w[NW][NG];
+#pragma unroll
+        for (int k = 0; k < NG; ++k) {
+            double v = acc[k];
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) s_w[warp][k] = v;
+        }
+        __syncthreads();
+        if (tid < NG) {
+            double v = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) v += s_w[w][tid];
+            s_G[tid] = v;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if constexpr (FORM == 2) {
+                if (p.ga != nullptr)
+                    for (int e = 0; e < NG; ++e) static_cast<T*>(p.ga)[cset * NG + e] = (T)s_G[e];
+            } else {
+                chain_rule<T, M, FORM>(s_G, tb, p.gb == nullptr ? nullptr : static_cast<T*>(p.gb) + cset * (M + 1),
+                                       p.ga == nullptr ? nullptr : static_cast<T*>(p.ga) + cset * (M + 1));
+            }
+            p.scnt[cset] = 0u;
+        }
+        return;
+    }
+    if (p.want_coef && s_fin == 1u) {              // last tile of its group
         __threadfence();
         reduce_rows<NG>(part + (gi << 5) * NG, gsize, part2 + gi * NG, lane, warp);
         __threadfence();
