@@ -440,6 +440,7 @@ enum TvMode { TV_FWD_EMIT = 0, TV_BWD_AGG = 1, TV_BWD_EMIT = 2 };
 // what sets the bandwidth; the emit-backward also stages grad_a (its TMA
 // store beats per-lane row stores), so it keeps smaller chunks to stay at the
 // same occupancy.
+constexpr int TV_PF = 3;                  // chunks of scalar-stream prefetch in tv_seq_kernel (ring of 4)
 template <typename T, int M, int MODE> constexpr int tv_chunk() {
     return (MODE != TV_BWD_EMIT && M * (int)sizeof(T) <= 128) ? 8 : 4;
 }
@@ -534,11 +535,35 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
         v[i] = (MODE == TV_BWD_AGG || !valid) ? 0.0 : p.carry[seg * M + i];
         yw[i] = (MODE == TV_BWD_EMIT && valid) ? yat(n1 - 2 - i) : T(0);
     }
+    // The per-sample scalar streams (x forward; dy and the y window backward) are
+    // loaded TV_PF chunks ahead into a register ring: a load issued at the sample
+    // that needs it puts one full memory latency on the serial recursion per sample.
+    constexpr int NR = TV_PF + 1;
+    T ps[NR][C], py[NR][C];
+    auto prefetch = [&](int c, int slot) {
+        const int64_t cs = chunk_start_of<T, M, MODE>(n0, c, BWD);
+#pragma unroll
+        for (int u = 0; u < C; ++u) {
+            const int s2 = BWD ? C - 1 - u : u;
+            const int64_t n = cs + s2;
+            const bool in = valid && n >= n0 && n < n1;
+            if constexpr (MODE == TV_FWD_EMIT) ps[slot][u] = in ? __ldg(xrow + n) : T(0);
+            else ps[slot][u] = (in && gyrow != nullptr) ? __ldg(gyrow + n) : T(0);
+            if constexpr (MODE == TV_BWD_EMIT) py[slot][u] = in ? yat(n - 1 - M) : T(0);
+        }
+    };
+#pragma unroll
+    for (int c = 0; c < TV_PF; ++c)
+        if (c < NCH) prefetch(c, c);
     stage(0, 0);
+    static_assert(NCH % NR == 0, "the ring slot must be a compile-time constant in the unrolled loop");
+#pragma unroll NR
     for (int c = 0; c < NCH; ++c) {
         const int b = c & 1;
         __syncwarp();
         if (c + 1 < NCH) stage(c + 1, b ^ 1);
+        if (c + TV_PF < NCH) prefetch(c + TV_PF, (c + TV_PF) % NR);
+        const int slot = c % NR;
         if (bulk) { mbar_wait(&bar[b], phase[b]); phase[b] ^= 1u; }
         __syncwarp();
         const T* my = myA[b];
@@ -567,7 +592,7 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
                 if (in) {
                     // four independent partial sums of the older terms; only the
                     // newest term (a_1 y(n-1)) waits on the previous sample
-                    R acc[4] = {(R)__ldg(xrow + n), 0.0, 0.0, 0.0};
+                    R acc[4] = {(R)ps[slot][u], 0.0, 0.0, 0.0};
 #pragma unroll
                     for (int i = M - 1; i >= 1; --i) acc[i & 3] = fma(-(R)cf[i], v[i], acc[i & 3]);
                     const R rest = (acc[1] + acc[2]) + (acc[3] + acc[0]);
@@ -579,7 +604,7 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
                 }
             } else {
                 if (in) {
-                    const R g = v[0] + (gyrow ? (R)__ldg(gyrow + n) : 0.0);
+                    const R g = v[0] + (R)ps[slot][u];
                     if constexpr (MODE == TV_BWD_EMIT) {
                         const T gT = (T)g;
                         if (gxrow) gxrow[n] = gT;
@@ -587,7 +612,7 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
                         for (int i = 0; i < M; ++i) myG[s2 * M + i] = -gT * yw[i];
 #pragma unroll
                         for (int i = 0; i < M - 1; ++i) yw[i] = yw[i + 1];
-                        yw[M - 1] = yat(n - 1 - M);
+                        yw[M - 1] = py[slot][u];
                     }
 #pragma unroll
                     for (int i = 0; i < M - 1; ++i) v[i] = fma(-(R)cf[i], g, v[i + 1]);
