@@ -36,6 +36,8 @@
  *   R10 time-varying all-pole DF: row n of a applies at output time n,
  *      y(n) = x(n) - sum_i a_i(n) y(n-i)  ("easily extended").
  *   R11 its adjoint is Eq.7 with the time-varying A(n+1), C(n+1).
+ *   R19 general time-varying DF (b(n) and a(n)): both rows apply at output
+ *      time n; a(n) monic (orc_tv_df).
  */
 #include <stdlib.h>
 #include <string.h>
@@ -279,6 +281,101 @@ int orc_tv_allpole(int M, long N, const double *a, const double *x,
             }
         }
 #undef BUILD_AC
+    free(v); free(dz); free(A); free(C);
+    return 0;
+}
+
+/*
+ * orc_tv_df: one sequence of the general time-varying DF-II filter (SURVEY
+ * 8(f) f2): per-sample numerator b(n) (M+1) and monic denominator a(n) (M),
+ * row n applied at output time n (reading R10 extended to b):
+ *     u(n) = x(n) - sum_{i=1..M} a_i(n) u(n-i),   y(n) = sum_{k=0..M} b_k(n) u(n-k),
+ * u(-k) = zi[k-1], zf[k-1] = u(N-k).  Coded as the per-sample state space of
+ * Eqs.4-5 with the DF realisation of PAPER.md:66 at every n:
+ * A(n) = companion(a(n)), B = e1, C(n) = b(n)[1..M] - a(n) b_0(n), D(n) = b_0(n),
+ * v(n) = [u(n-1) .. u(n-M)].  Backward: Eq.7 with A(n+1), C(n+1) (R11),
+ * Eq.8 with D(n), and per sample dA(n) = dz(n) v(n)^T, dC(n) = dy(n) v(n),
+ * dD(n) = dy(n) x(n) (Eqs.6, 9 before the sum over n), mapped to (b(n), a(n))
+ * as in the LTI DF chain rule: gb_k(n) = dC(n)[k-1] (k >= 1),
+ * gb_0(n) = dD(n) - sum_k a_k(n) dC(n)[k-1],
+ * ga_k(n) = -dA(n)[0][k-1] - b_0(n) dC(n)[k-1].
+ * b: N x (M+1), a: N x M, gb: N x (M+1), ga: N x M (row-major, per sample).
+ */
+int orc_tv_df(int M, long N, const double *b, const double *a, const double *x,
+              const double *zi, const double *gy, const double *gzf,
+              double *y, double *zf, double *gx, double *gb, double *ga, double *gzi)
+{
+    if (M < 1 || N < 1) return 1;
+    double *v = (double *)malloc((size_t)(N + 1) * M * sizeof(double));
+    double *dz = (double *)malloc((size_t)N * M * sizeof(double));
+    double *A = (double *)malloc((size_t)M * M * sizeof(double));
+    double *C = (double *)malloc((size_t)M * sizeof(double));
+    if (!v || !dz || !A || !C) return 2;
+    const int K = M + 1;
+
+#define BUILD_ACD(n)                                                       \
+    do {                                                                   \
+        memset(A, 0, (size_t)M * M * sizeof(double));                     \
+        for (int k = 1; k <= M; ++k) {                                     \
+            A[IDX(0, k - 1, M)] = -a[(n) * M + (k - 1)];                   \
+            C[k - 1] = b[(n) * K + k] - a[(n) * M + (k - 1)] * b[(n) * K]; \
+        }                                                                  \
+        for (int i = 1; i < M; ++i) A[IDX(i, i - 1, M)] = 1.0;             \
+    } while (0)
+
+    for (int i = 0; i < M; ++i) v[i] = zi ? zi[i] : 0.0;
+    for (long n = 0; n < N; ++n) {                  /* Eqs.4-5 with A(n), C(n), D(n) */
+        BUILD_ACD(n);
+        const double D = b[n * K];
+        const double *vn = v + n * M;
+        double *vn1 = v + (n + 1) * M;
+        double yn = D * x[n];
+        for (int i = 0; i < M; ++i) yn += C[i] * vn[i];
+        if (y) y[n] = yn;
+        for (int i = 0; i < M; ++i) {
+            double s = (i == 0 ? 1.0 : 0.0) * x[n];
+            for (int j = 0; j < M; ++j) s += A[IDX(i, j, M)] * vn[j];
+            vn1[i] = s;
+        }
+    }
+    if (zf) for (int i = 0; i < M; ++i) zf[i] = v[N * M + i];
+
+    for (int i = 0; i < M; ++i) dz[(N - 1) * M + i] = gzf ? gzf[i] : 0.0;   /* R4 */
+    for (long n = N - 2; n >= 0; --n) {             /* Eq.7 */
+        BUILD_ACD(n + 1);
+        const double *d1 = dz + (n + 1) * M;
+        const double dy1 = gy ? gy[n + 1] : 0.0;
+        for (int i = 0; i < M; ++i) {
+            double s = C[i] * dy1;
+            for (int j = 0; j < M; ++j) s += A[IDX(j, i, M)] * d1[j];
+            dz[n * M + i] = s;
+        }
+    }
+    if (gx)                                         /* Eq.8: B^T dz(n) + D(n) dy(n) */
+        for (long n = 0; n < N; ++n) gx[n] = dz[n * M] + b[n * K] * (gy ? gy[n] : 0.0);
+    if (gzi) {                                      /* A.3 with A(0), C(0) */
+        BUILD_ACD(0);
+        const double dy0 = gy ? gy[0] : 0.0;
+        for (int i = 0; i < M; ++i) {
+            double s = C[i] * dy0;
+            for (int j = 0; j < M; ++j) s += A[IDX(j, i, M)] * dz[j];
+            gzi[i] = s;
+        }
+    }
+    for (long n = 0; n < N; ++n) {                  /* per-sample Eqs.6, 9 -> (b(n), a(n)) */
+        const double dyn = gy ? gy[n] : 0.0;
+        const double dD = dyn * x[n];
+        double gb0 = dD;
+        for (int k = 1; k <= M; ++k) {
+            const double dCk = dyn * v[n * M + (k - 1)];
+            const double dA0k = dz[n * M + 0] * v[n * M + (k - 1)];
+            if (gb) gb[n * K + k] = dCk;
+            if (ga) ga[n * M + (k - 1)] = -dA0k - b[n * K] * dCk;
+            gb0 -= a[n * M + (k - 1)] * dCk;
+        }
+        if (gb) gb[n * K] = gb0;
+    }
+#undef BUILD_ACD
     free(v); free(dz); free(A); free(C);
     return 0;
 }
