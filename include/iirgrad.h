@@ -113,7 +113,14 @@ typedef enum {
      * DESIGN.md).  Both give the same result up to fp64 rounding of the carries;
      * the bare recurrence (IIR_SS) is always single-pass. */
     IIR_FLAG_SINGLE_PASS = 2,
-    IIR_FLAG_THREE_PHASE = 4
+    IIR_FLAG_THREE_PHASE = 4,
+    /* IIR_COEF_PER_SAMPLE with a per-sample numerator: the general
+     * time-varying DF-II filter u(n) = x(n) - sum_i a_i(n) u(n-i),
+     * y(n) = sum_k b_k(n) u(n-k), both rows applied at output time n (R19);
+     * b (B, T, M+1) and grad_b (B, T, M+1) are then required / returned; zi, zf are
+     * the internal signal history [u(-1)..u(-M)].  Without it, PER_SAMPLE is the
+     * all-pole filter (b must be NULL). */
+    IIR_FLAG_PER_SAMPLE_B = 8
 } iir_flags_t;
 
 /* Bytes of the forward->backward tape / of the scratch workspace (0 on a bad desc). */

@@ -28,7 +28,7 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
 // ------------------------------------------------------- instrumentation ----
 static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_phi", "tv_chain", "tv_fwd",
                                         "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd", "lti_red_fwd",
-                                        "lti_red_bwd", "lti_cscan", "state_carry"};
+                                        "lti_red_bwd", "lti_cscan", "state_carry", "tv_fir"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;
@@ -111,8 +111,10 @@ static iir_status_t check_desc(const iir_desc_t* d) {
             return fail(IIR_EUNSUPPORTED, "bare recurrence: A is SHARED or PER_SEQ");
         if (d->order < 1 || d->order > 4) return fail(IIR_EUNSUPPORTED, "bare recurrence: order must be 1..4");
     }
+    if ((d->flags & IIR_FLAG_PER_SAMPLE_B) && d->coef_mode != IIR_COEF_PER_SAMPLE)
+        return fail(IIR_EINVAL, "IIR_FLAG_PER_SAMPLE_B needs IIR_COEF_PER_SAMPLE");
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) {
-        if (d->form != IIR_DF2) return fail(IIR_EUNSUPPORTED, "per-sample coefficients: only the all-pole DF form");
+        if (d->form != IIR_DF2) return fail(IIR_EUNSUPPORTED, "per-sample coefficients: only the DF form");
         if (d->order < 1 || d->order > TV_MAX_M) return fail(IIR_EUNSUPPORTED, "per-sample order must be 1..31");
         if (!tv_supported(d->order)) return fail(IIR_EUNSUPPORTED, "per-sample order not compiled in");
         return IIR_OK;
@@ -242,7 +244,9 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     const Layout L = layout(d);
     if (x == nullptr || y == nullptr) return fail(IIR_EINVAL, "x and y must be non-NULL");
     if (a == nullptr) return fail(IIR_EINVAL, "a must be non-NULL");
-    if (d->coef_mode == IIR_COEF_PER_SAMPLE || d->form == IIR_SS) {
+    if (d->coef_mode == IIR_COEF_PER_SAMPLE && (d->flags & IIR_FLAG_PER_SAMPLE_B)) {
+        if (b == nullptr) return fail(IIR_EINVAL, "IIR_FLAG_PER_SAMPLE_B: b (B, T, M+1) must be non-NULL");
+    } else if (d->coef_mode == IIR_COEF_PER_SAMPLE || d->form == IIR_SS) {
         if (b != nullptr) return fail(IIR_EINVAL, "per-sample all-pole / bare recurrence: b must be NULL");
     } else if (b == nullptr) {
         return fail(IIR_EINVAL, "b must be non-NULL");
@@ -259,7 +263,7 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     const int W = d->dtype == IIR_F64 ? 2 : 4;
     const int64_t rowlen = d->length * (d->form == IIR_SS ? d->order : 1);
     const bool vec = (rowlen % W == 0) && aligned16(x) && aligned16(y) && aligned16(t + L.tp_u);
-    if (d->coef_mode == IIR_COEF_PER_SAMPLE) return tv_forward(d, L, a, x, zi, y, zf, t, w, vec, st);
+    if (d->coef_mode == IIR_COEF_PER_SAMPLE) return tv_forward(d, L, b, a, x, zi, y, zf, t, w, vec, st);
 
     LtiCall c{};
     c.d = d; c.L = &L; c.st = st; c.is_fwd = true; c.b = b; c.a = a;
@@ -295,6 +299,10 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     if (d->form == IIR_SS && (a == nullptr || y == nullptr))
         return fail(IIR_EINVAL, "bare-recurrence backward needs A and the forward's v");
     if (d->form == IIR_SS && grad_b != nullptr) return fail(IIR_EINVAL, "bare recurrence: grad_b must be NULL");
+    if (d->coef_mode == IIR_COEF_PER_SAMPLE && (d->flags & IIR_FLAG_PER_SAMPLE_B) && b == nullptr)
+        return fail(IIR_EINVAL, "IIR_FLAG_PER_SAMPLE_B backward needs the forward's b");
+    if (d->coef_mode == IIR_COEF_PER_SAMPLE && !(d->flags & IIR_FLAG_PER_SAMPLE_B) && grad_b != nullptr)
+        return fail(IIR_EINVAL, "per-sample all-pole: grad_b must be NULL");
     if (d->coef_mode == IIR_COEF_PER_SAMPLE && (a == nullptr || y == nullptr))
         return fail(IIR_EINVAL, "per-sample backward needs the forward's a and y");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -309,7 +317,7 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     const bool vec = (rowlen % W == 0) && aligned16(grad_y) && aligned16(x) && aligned16(y) &&
                      aligned16(grad_x) && aligned16(t + L.tp_u);
     if (d->coef_mode == IIR_COEF_PER_SAMPLE)
-        return tv_backward(d, L, grad_y, grad_zf, a, y, zi, t, grad_x, grad_a, grad_zi, w, vec, st);
+        return tv_backward(d, L, grad_y, grad_zf, b, a, y, zi, t, grad_x, grad_b, grad_a, grad_zi, w, vec, st);
 
     LtiCall c{};
     c.d = d; c.L = &L; c.st = st; c.is_fwd = false;

@@ -14,7 +14,7 @@ namespace iirg {
 iir_status_t fail(iir_status_t st, const std::string& msg);
 
 enum Kind { K_LTI_PREP = 0, K_LTI_FWD, K_LTI_BWD, K_TV_PHI, K_TV_CHAIN, K_TV_FWD, K_TV_BWD_AGG, K_TV_BWD, K_REC_FWD,
-            K_REC_BWD, K_LTI_RED_F, K_LTI_RED_B, K_LTI_CSCAN, K_STATE_CARRY, K_NUM };
+            K_REC_BWD, K_LTI_RED_F, K_LTI_RED_B, K_LTI_CSCAN, K_STATE_CARRY, K_TV_FIR, K_NUM };
 
 // Launch bookkeeping: counts every kernel and (when profiling is on) brackets it
 // with CUDA events on its stream.
@@ -43,6 +43,7 @@ struct Layout {
     size_t ws_sent = 0, ws_sent_bytes = 0;                 // look-back slots, initialised to all-ones (NaN)
     size_t ws_agg[MAX_LEVELS] = {0, 0, 0, 0}, ws_part = 0, ws_part2 = 0, ws_bytes = 0;
     size_t ws_car = 0, ws_carb = 0;                        // three-phase carries [B][ntiles][M] fp64 (fwd, bwd)
+    size_t ws_du = 0, ws_duneg = 0;                        // general TV DF: FIR-stage adjoint of u
     size_t ws_psi = 0, ws_omega = 0, ws_sgrp = 0;          // TV two-level chain
     size_t tp_tab = 0, tp_u = 0, tp_extra = 0, tp_bytes = 0;
 };
@@ -51,10 +52,10 @@ struct Layout {
 constexpr int TV_MAX_M = 31;
 bool tv_supported(int M);
 Layout tv_layout(const iir_desc_t* d);
-iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* a, const void* x, const void* zi, void* y,
-                        void* zf, char* tape, char* ws, bool vec, cudaStream_t st);
-iir_status_t tv_backward(const iir_desc_t* d, const Layout& L, const void* gy, const void* gzf, const void* a,
-                         const void* y, const void* zi, const char* tape, void* gx, void* ga, void* gzi, char* ws,
-                         bool vec, cudaStream_t st);
+iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* b, const void* a, const void* x,
+                        const void* zi, void* y, void* zf, char* tape, char* ws, bool vec, cudaStream_t st);
+iir_status_t tv_backward(const iir_desc_t* d, const Layout& L, const void* gy, const void* gzf, const void* b,
+                         const void* a, const void* y, const void* zi, const char* tape, void* gx, void* gb,
+                         void* ga, void* gzi, char* ws, bool vec, cudaStream_t st);
 
 }  // namespace iirg

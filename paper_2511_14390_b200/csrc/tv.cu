@@ -39,7 +39,72 @@ Layout tv_layout(const iir_desc_t* d) {
     L.tp_tab = 0;
     L.tp_bytes = al256((size_t)L.ntot * M * M * ts);       // Phi_k per segment (reused by the backward)
     L.tp_u = L.tp_bytes;
+    if (d->flags & IIR_FLAG_PER_SAMPLE_B) {               // general DF: the all-pole output u (B, T)
+        L.tp_bytes += al256((size_t)d->batch * d->length * ts);
+        L.ws_du = o; o += al256((size_t)d->batch * d->length * ts);   // FIR-stage adjoint of u(0..T-1)
+        L.ws_duneg = o; o += al256((size_t)d->batch * M * ts);        //   ... and of u(-1..-M)
+        L.ws_bytes = o;
+    }
     return L;
+}
+
+// ---- general time-varying DF (IIR_FLAG_PER_SAMPLE_B) ---------
+// The filter factors into the all-pole recursion on the internal signal u
+// (tv_* kernels above, whose "y" is u) and a per-sample FIR stage
+// y(n) = sum_k b_k(n) u(n-k), u(-k) = zi[k-1] (Eqs.2-3 with b(n), a(n)).  The
+// FIR stage's adjoint is  du(m) = sum_k b_k(m+k) dy(m+k)  (m >= -M; m < 0 are
+// the zi entries) and  grad_b_k(n) = dy(n) u(n-k);  the all-pole backward then
+// runs with grad_y = du, and grad_zi gains the FIR's direct terms du(-1..-M).
+template <typename T>
+__global__ void __launch_bounds__(256) tv_fir_fwd_kernel(const T* __restrict__ b, const T* __restrict__ u,
+                                                         const T* __restrict__ zi, T* __restrict__ y, int M,
+                                                         int64_t Tlen, int64_t total) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const int64_t seq = i / Tlen, n = i - seq * Tlen;
+    const T* br = b + i * (M + 1);
+    double acc = 0.0;
+    for (int k = 0; k <= M; ++k) {
+        const int64_t m = n - k;
+        const T um = m >= 0 ? u[seq * Tlen + m] : (zi != nullptr ? zi[seq * M + (-m - 1)] : T(0));
+        acc = fma((double)br[k], (double)um, acc);
+    }
+    y[i] = (T)acc;
+}
+template <typename T>
+__global__ void __launch_bounds__(256) tv_fir_bwd_kernel(const T* __restrict__ b, const T* __restrict__ u,
+                                                         const T* __restrict__ zi, const T* __restrict__ gy,
+                                                         T* __restrict__ du, T* __restrict__ duneg,
+                                                         T* __restrict__ gb, int M, int64_t Tlen, int64_t B) {
+    const int64_t span = Tlen + M;                         // m = -M .. T-1
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B * span) return;
+    const int64_t seq = i / span, m = i - seq * span - M;
+    double acc = 0.0;
+    if (gy != nullptr)
+        for (int k = 0; k <= M; ++k) {
+            const int64_t n = m + k;
+            if (n >= 0 && n < Tlen)
+                acc = fma((double)b[(seq * Tlen + n) * (M + 1) + k], (double)gy[seq * Tlen + n], acc);
+        }
+    if (m >= 0) {
+        du[seq * Tlen + m] = (T)acc;
+        if (gb != nullptr) {
+            const double dyn = gy != nullptr ? (double)gy[seq * Tlen + m] : 0.0;
+            for (int k = 0; k <= M; ++k) {
+                const int64_t q = m - k;
+                const T uq = q >= 0 ? u[seq * Tlen + q] : (zi != nullptr ? zi[seq * M + (-q - 1)] : T(0));
+                gb[(seq * Tlen + m) * (M + 1) + k] = (T)(dyn * (double)uq);
+            }
+        }
+    } else {
+        duneg[seq * M + (-m - 1)] = (T)acc;
+    }
+}
+template <typename T>
+__global__ void tv_add_kernel(T* __restrict__ dst, const T* __restrict__ src, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = dst[i] + src[i];
 }
 
 template <typename T, int M, int MODE>
@@ -113,10 +178,12 @@ static int tv_vec(const iir_desc_t* d, const void* a) {
     return (((size_t)d->order * ts) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15u) == 0);
 }
 
-iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* a, const void* x, const void* zi, void* y,
-                        void* zf, char* tape, char* ws, bool, cudaStream_t st) {
+iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* b, const void* a, const void* x,
+                        const void* zi, void* y, void* zf, char* tape, char* ws, bool, cudaStream_t st) {
+    const bool fir = (d->flags & IIR_FLAG_PER_SAMPLE_B) != 0;
+    void* u = fir ? static_cast<void*>(tape + L.tp_u) : y;   // general DF: the recursion's output is u
     TvArgs ta{};
-    ta.a = a; ta.x = x; ta.zi = zi; ta.y = y; ta.zf = zf;
+    ta.a = a; ta.x = x; ta.zi = zi; ta.y = u; ta.zf = zf;
     ta.phi = tape;
     ta.w = reinterpret_cast<double*>(ws + L.ws_part);
     ta.carry = reinterpret_cast<double*>(ws + L.ws_part2);
@@ -126,15 +193,47 @@ iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* a, con
     ta.omega = reinterpret_cast<double*>(ws + L.ws_omega);
     ta.sgrp = reinterpret_cast<double*>(ws + L.ws_sgrp);
     ta.ngrp = (int)L.ngroups;
-    return d->dtype == IIR_F64 ? tv_dispatch<double>(true, d->order, L, ta, st)
-                               : tv_dispatch<float>(true, d->order, L, ta, st);
+    iir_status_t s = d->dtype == IIR_F64 ? tv_dispatch<double>(true, d->order, L, ta, st)
+                                         : tv_dispatch<float>(true, d->order, L, ta, st);
+    if (s != IIR_OK || !fir) return s;
+    const int64_t total = d->batch * d->length;
+    const unsigned grid = (unsigned)((total + 255) / 256);
+    return launch(K_TV_FIR, st, [&] {
+        if (d->dtype == IIR_F64)
+            tv_fir_fwd_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(b), static_cast<const double*>(u),
+                static_cast<const double*>(zi), static_cast<double*>(y), d->order, d->length, total);
+        else
+            tv_fir_fwd_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(b), static_cast<const float*>(u),
+                static_cast<const float*>(zi), static_cast<float*>(y), d->order, d->length, total);
+    });
 }
 
-iir_status_t tv_backward(const iir_desc_t* d, const Layout& L, const void* gy, const void* gzf, const void* a,
-                         const void* y, const void* zi, const char* tape, void* gx, void* ga, void* gzi, char* ws,
-                         bool, cudaStream_t st) {
+iir_status_t tv_backward(const iir_desc_t* d, const Layout& L, const void* gy, const void* gzf, const void* b,
+                         const void* a, const void* y, const void* zi, const char* tape, void* gx, void* gb,
+                         void* ga, void* gzi, char* ws, bool, cudaStream_t st) {
+    const bool fir = (d->flags & IIR_FLAG_PER_SAMPLE_B) != 0;
+    const void* u = fir ? static_cast<const void*>(tape + L.tp_u) : y;
+    void* du = fir ? static_cast<void*>(ws + L.ws_du) : nullptr;
+    void* duneg = fir ? static_cast<void*>(ws + L.ws_duneg) : nullptr;
+    if (fir) {                                             // FIR stage adjoint first: du, grad_b
+        const int64_t n = d->batch * (d->length + d->order);
+        const unsigned grid = (unsigned)((n + 255) / 256);
+        iir_status_t s = launch(K_TV_FIR, st, [&] {
+            if (d->dtype == IIR_F64)
+                tv_fir_bwd_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(b),
+                    static_cast<const double*>(u), static_cast<const double*>(zi), static_cast<const double*>(gy),
+                    static_cast<double*>(du), static_cast<double*>(duneg), static_cast<double*>(gb), d->order,
+                    d->length, d->batch);
+            else
+                tv_fir_bwd_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(b),
+                    static_cast<const float*>(u), static_cast<const float*>(zi), static_cast<const float*>(gy),
+                    static_cast<float*>(du), static_cast<float*>(duneg), static_cast<float*>(gb), d->order,
+                    d->length, d->batch);
+        });
+        if (s != IIR_OK) return s;
+    }
     TvArgs ta{};
-    ta.a = a; ta.zi = zi; ta.gy = gy; ta.gzf = gzf; ta.yin = y;
+    ta.a = a; ta.zi = zi; ta.gy = fir ? du : gy; ta.gzf = gzf; ta.yin = u;
     ta.gx = gx; ta.ga = ga; ta.gzi = gzi;
     ta.phi = const_cast<char*>(tape);
     ta.w = reinterpret_cast<double*>(ws + L.ws_part);
@@ -145,8 +244,18 @@ iir_status_t tv_backward(const iir_desc_t* d, const Layout& L, const void* gy, c
     ta.omega = reinterpret_cast<double*>(ws + L.ws_omega);
     ta.sgrp = reinterpret_cast<double*>(ws + L.ws_sgrp);
     ta.ngrp = (int)L.ngroups;
-    return d->dtype == IIR_F64 ? tv_dispatch<double>(false, d->order, L, ta, st)
-                               : tv_dispatch<float>(false, d->order, L, ta, st);
+    iir_status_t s = d->dtype == IIR_F64 ? tv_dispatch<double>(false, d->order, L, ta, st)
+                                         : tv_dispatch<float>(false, d->order, L, ta, st);
+    if (s != IIR_OK || !fir || gzi == nullptr) return s;
+    const int64_t n = d->batch * d->order;                 // grad_zi += the FIR stage's direct terms
+    return launch(K_TV_FIR, st, [&] {
+        if (d->dtype == IIR_F64)
+            tv_add_kernel<double><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(static_cast<double*>(gzi),
+                static_cast<const double*>(duneg), n);
+        else
+            tv_add_kernel<float><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(static_cast<float*>(gzi),
+                static_cast<const float*>(duneg), n);
+    });
 }
 
 }  // namespace iirg

@@ -1,0 +1,83 @@
+"""GPU parity of the general time-varying DF path (IIR_FLAG_PER_SAMPLE_B, SURVEY
+§8(f) f2: per-sample b and a, reading R19) against the fp64 oracle orc_tv_df on
+the same dtype-rounded inputs; gate: fp32 1e-4, fp64 1e-10 of max|err| / rms,
+per output tensor (y, zf, grad_x, grad_b, grad_a, grad_zi)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2511_14390_b200 import _binding as B
+from paper_2511_14390_b200 import inputs
+
+from gpu_util import TOL, nrm_err
+
+pytestmark = pytest.mark.gpu
+
+
+def run(q, dtype, want=("y", "zf", "gx", "gb", "ga", "gzi")):
+    td = torch.float32 if dtype == "f32" else torch.float64
+    dev = lambda t: None if t is None else torch.as_tensor(np.asarray(t), dtype=torch.float64).to(td).cuda()
+    b, a, x, zi, gy, gzf = map(dev, (q["b"], q["a"], q["x"], q["zi"], q["gy"], q["gzf"]))
+    Bsz, T = x.shape
+    M = a.shape[-1]
+    desc = B.make_desc(Bsz, T, M, "df", td, B.IIR_COEF_PER_SAMPLE, flags=B.IIR_FLAG_PER_SAMPLE_B)
+    tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
+    tape = torch.empty(tb, dtype=torch.uint8, device="cuda")
+    ws = torch.empty(wb, dtype=torch.uint8, device="cuda")
+    nan = lambda *s: torch.full(s, float("nan"), dtype=td, device="cuda")
+    y = nan(Bsz, T)
+    out = dict(zf=nan(Bsz, M), gx=nan(Bsz, T), gb=nan(Bsz, T, M + 1), ga=nan(Bsz, T, M), gzi=nan(Bsz, M))
+    out = {k: (v if k in want else None) for k, v in out.items()}
+    B.iir_forward(desc, b, a, x, zi, y, out["zf"], tape, tb, ws, wb)
+    B.iir_backward(desc, gy, gzf, b, a, None, y, zi, tape, tb, out["gx"], out["gb"], out["ga"], out["gzi"], ws, wb)
+    torch.cuda.synchronize()
+    f = lambda t: None if t is None else t.double().cpu().numpy()
+    return dict(y=f(y), **{k: f(v) for k, v in out.items()})
+
+
+def rounded(p, dtype):
+    t = np.float32 if dtype == "f32" else np.float64
+    c = lambda v: None if v is None else np.asarray(v.numpy() if torch.is_tensor(v) else v).astype(t).astype(np.float64)
+    return {k: c(p[k]) for k in ("b", "a", "x", "zi", "gy", "gzf")}
+
+
+def check(p, dtype, tol=None, want=("y", "zf", "gx", "gb", "ga", "gzi")):
+    tol = TOL[dtype] if tol is None else tol
+    q = rounded(p, dtype)
+    g = run(q, dtype, want)
+    o = oracle.tv_df(q["b"], q["a"], q["x"], q["zi"], q["gy"], q["gzf"])
+    errs = {k: nrm_err(g[k], o[k]) for k in want}
+    bad = {k: v for k, v in errs.items() if not v <= tol}
+    assert not bad, f"errors {errs} exceed {tol}"
+    return errs
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("M", [1, 2, 4, 8, 24])
+def test_orders_dtypes(dtype, M):
+    p = inputs.tv_df_problem(31000 + M, batch=3, length=3 * 512 + 37, order=M, dtype=dtype, hop=128)
+    check(p, dtype)
+
+
+@pytest.mark.parametrize("T", [1, 2, 5, 23, 24, 25, 511, 512, 513, 1500])
+def test_edge_lengths(T):
+    p = inputs.tv_df_problem(32000 + T, batch=2, length=T, order=24, dtype="f64", hop=64)
+    check(p, "f64")
+
+
+@pytest.mark.parametrize("zi,gzf", [(False, False), (True, False), (False, True)])
+def test_initial_condition_paths(zi, gzf):
+    p = inputs.tv_df_problem(33000, batch=2, length=3000, order=8, dtype="f32", zi=zi, gzf=gzf)
+    check(p, "f32")
+
+
+def test_null_optional_outputs():
+    p = inputs.tv_df_problem(33100, batch=2, length=2000, order=4, dtype="f32")
+    check(p, "f32", want=("y", "gx"))
+
+
+def test_config3_shape_with_numerator_fp32():
+    """Config-3 shape (order 24, per-sample coefficients, 2^18 samples) with a per-sample numerator, 2 sequences."""
+    p = inputs.tv_df_problem(1003, batch=2, length=1 << 18, order=24, dtype="f32")
+    check(p, "f32")
