@@ -40,6 +40,8 @@ WORKLOADS = {
                     "coefficient-gradient all-reduce", **dict(inputs.CONFIGS["c5"], batch=256)),
     "c3": dict(desc="config 3: all-pole LPC order 24, per-sample coefficients, batch 32 x 2^18, fp32",
                **inputs.CONFIGS["c3"]),
+    "f2": dict(desc="SURVEY 8(f) f2: general time-varying DF (per-sample b and a), config-3 shape: order 24, "
+                    "batch 32 x 2^18, fp32", fir=True, **inputs.CONFIGS["c3"]),
     "f1": dict(desc="SURVEY 8(f) f1: bare recurrence v(n+1) = A v(n) + z(n) of Listing 1, M = 2, batch 16 x 2^20, "
                     "fp32 (the paper's benchmarked operator at its longest N)", **dict(inputs.CONFIGS["f1"], batch=16)),
 }
@@ -55,8 +57,11 @@ def algorithmic_bytes(w):
         # tv_bwd reads a, dy, y and writes dx, grad_a.  tv_chain moves only the
         # per-segment tape (M^2 per 512 samples): design overhead, no per-sample bytes.
         M = w["order"]
-        return {"tv_phi": (M + 1) * s, "tv_chain": 0, "tv_fwd": (M + 2) * s, "tv_bwd_agg": (M + 1) * s,
-                "tv_bwd": (2 * M + 3) * s}
+        d = {"tv_phi": (M + 1) * s, "tv_chain": 0, "tv_fwd": (M + 2) * s, "tv_bwd_agg": (M + 1) * s,
+             "tv_bwd": (2 * M + 3) * s}
+        if w.get("fir"):       # FIR stage, 3 launches per step: fwd b, u -> y; bwd b, dy, u -> du, grad_b; zi add
+            d["tv_fir"] = ((M + 3) + (2 * M + 5)) * s / 3
+        return d
     # HBM bytes per kernel the method must move: fwd reads x, writes y (+u for DF);
     # bwd reads dy, x, y (TDF) or dy, u (DF) and writes dx: 24 B/sample in fp32
     # three-phase schedule: lti_red_fwd reads x, lti_red_bwd reads dy (the emit
@@ -76,7 +81,8 @@ def step_min_bytes(w):
     if w["form"] == "ss":
         return 5 * w["order"] * s
     if w["coef"] == "per_sample":
-        return (3 * w["order"] + 5) * s
+        # + per-sample b read by each direction and grad_b written (general DF)
+        return (3 * w["order"] + 5 + (3 * (w["order"] + 1) if w.get("fir") else 0)) * s
     return 6 * s
 
 
@@ -158,9 +164,12 @@ class Problem:
         ss = w["form"] == "ss"
         shape = (Bsz, T, M) if ss else (Bsz, T)
         if w["coef"] == "per_sample":
-            p = inputs.tv_allpole_problem(seed, batch=Bsz, length=T, order=M, dtype=w["dtype"], device=dev)
+            if w.get("fir"):
+                p = inputs.tv_df_problem(seed, batch=Bsz, length=T, order=M, dtype=w["dtype"], device=dev)
+            else:
+                p = inputs.tv_allpole_problem(seed, batch=Bsz, length=T, order=M, dtype=w["dtype"], device=dev)
             self.a = p["a"].to(td).contiguous()
-            self.b = None
+            self.b = p["b"].to(td).contiguous() if w.get("fir") else None
             self.zi = p["zi"].to(td).contiguous()
             mode = B.IIR_COEF_PER_SAMPLE
         elif ss:
@@ -188,6 +197,8 @@ class Problem:
         self.ga = None if w["coef"] == "per_sample" else torch.empty_like(self.a)
         # the workspace is cleared once; every completed call leaves it cleared
         sched = {"auto": 0, "1p": B.IIR_FLAG_SINGLE_PASS, "3p": B.IIR_FLAG_THREE_PHASE}[w.get("scan", "auto")]
+        if w.get("fir"):
+            sched |= B.IIR_FLAG_PER_SAMPLE_B
         self.desc = B.make_desc(Bsz, T, M, w["form"], td, mode, flags=B.IIR_FLAG_WS_READY | sched)
         self.tb = B.iir_tape_bytes(self.desc)
         self.wb = B.iir_workspace_bytes(self.desc)
@@ -208,7 +219,7 @@ class Problem:
                       self.ws, self.wb, stream)
         B.iir_backward(self.desc, s["gy"], self.gzf, self.b, self.a, s["x"], s["y"], self.zi, self.tape, self.tb,
                        s["gx"], self.gb, s.get("ga", self.ga), self.gzi, self.ws, self.wb, stream)
-        if pg is not None and self.b is not None:
+        if pg is not None and self.b is not None and self.w["coef"] == "shared":
             # the one real exchange of the path: all-reduce of the shared-coefficient gradients (§8(e))
             torch.cat([self.gb, self.ga], out=self.grad_buf)
             torch.distributed.all_reduce(self.grad_buf, group=pg)
@@ -418,10 +429,15 @@ def cpu_baseline(w, budget_s=10.0):
         fn = lambda: [oracle.recurrence(p["A"], p["v0"][i], p["z"][i], p["gv"][i]) for i in range(nseq)]
     elif w["coef"] == "per_sample":
         T = min(T, 1 << 16)
-        p = inputs.tv_allpole_problem(7, batch=min(nseq, 8), length=T, order=w["order"], dtype=w["dtype"])
-        args = (p["a"].numpy(), p["x"].numpy(), p["zi"].numpy(), p["gy"].numpy(), p["gzf"].numpy())
-        fn = lambda: oracle.tv_allpole(*args)
-        nseq = args[1].shape[0]
+        if w.get("fir"):
+            p = inputs.tv_df_problem(7, batch=min(nseq, 8), length=T, order=w["order"], dtype=w["dtype"])
+            args = tuple(p[k].numpy() for k in ("b", "a", "x", "zi", "gy", "gzf"))
+            fn = lambda: oracle.tv_df(*args)
+        else:
+            p = inputs.tv_allpole_problem(7, batch=min(nseq, 8), length=T, order=w["order"], dtype=w["dtype"])
+            args = (p["a"].numpy(), p["x"].numpy(), p["zi"].numpy(), p["gy"].numpy(), p["gzf"].numpy())
+            fn = lambda: oracle.tv_allpole(*args)
+        nseq = p["x"].shape[0]
     else:
         T = min(T, 1 << 20)
         nseq = max(1, min(nseq, (1 << 22) // T))
@@ -461,9 +477,14 @@ def run_reference(args, w, rank, world):
     elif w["coef"] == "per_sample":
         T = min(T, 1 << 15)
         nseq = min(w["batch"], 8)
-        p = inputs.tv_allpole_problem(7, batch=nseq, length=T, order=w["order"], dtype=w["dtype"])
-        a_ = (p["a"].numpy(), p["x"].numpy(), p["zi"].numpy(), p["gy"].numpy(), p["gzf"].numpy())
-        fn = lambda: oracle.tv_allpole(*a_)
+        if w.get("fir"):
+            p = inputs.tv_df_problem(7, batch=nseq, length=T, order=w["order"], dtype=w["dtype"])
+            a_ = tuple(p[k].numpy() for k in ("b", "a", "x", "zi", "gy", "gzf"))
+            fn = lambda: oracle.tv_df(*a_)
+        else:
+            p = inputs.tv_allpole_problem(7, batch=nseq, length=T, order=w["order"], dtype=w["dtype"])
+            a_ = (p["a"].numpy(), p["x"].numpy(), p["zi"].numpy(), p["gy"].numpy(), p["gzf"].numpy())
+            fn = lambda: oracle.tv_allpole(*a_)
     else:
         T = min(T, 1 << 20)
         nseq = max(1, min(w["batch"], 8, (1 << 21) // T))

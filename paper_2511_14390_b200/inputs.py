@@ -146,15 +146,16 @@ def tv_allpole_problem(seed, batch=32, length=1 << 18, order=24, hop=256, dtype=
                 gzf=rnd(batch, order) if gzf else None, dtype=dtype)
 
 
-def tv_df_problem(seed, batch=4, length=1 << 14, order=8, hop=256, dtype="f32", zi=True, gzf=True):
+def tv_df_problem(seed, batch=4, length=1 << 14, order=8, hop=256, dtype="f32", zi=True, gzf=True, device="cpu"):
     """General time-varying DF inputs: the config-3 all-pole recipe
     for a(n) plus a per-sample numerator b(n) (B, T, M+1): per frame b ~ N(0, 1/(M+1)),
     linearly interpolated per sample (the frame-interpolated synthesis shape)."""
-    p = tv_allpole_problem(seed, batch=batch, length=length, order=order, hop=hop, dtype=dtype, zi=zi, gzf=gzf)
+    p = tv_allpole_problem(seed, batch=batch, length=length, order=order, hop=hop, dtype=dtype, zi=zi, gzf=gzf,
+                           device=device)
     rng = np.random.default_rng(seed + 7)
     nf = (length + hop - 1) // hop + 1
-    bf = torch.from_numpy(rng.standard_normal((batch, nf, order + 1)) / np.sqrt(order + 1))
-    n = torch.arange(length, dtype=torch.float64)
+    bf = torch.from_numpy(rng.standard_normal((batch, nf, order + 1)) / np.sqrt(order + 1)).to(device)
+    n = torch.arange(length, dtype=torch.float64, device=device)
     f0 = torch.div(n, hop, rounding_mode="floor").long()
     w = ((n - f0 * hop) / hop)[None, :, None]
     b = bf[:, f0] * (1 - w) + bf[:, f0 + 1] * w
