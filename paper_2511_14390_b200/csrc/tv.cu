@@ -55,52 +55,134 @@ Layout tv_layout(const iir_desc_t* d) {
 // FIR stage's adjoint is  du(m) = sum_k b_k(m+k) dy(m+k)  (m >= -M; m < 0 are
 // the zi entries) and  grad_b_k(n) = dy(n) u(n-k);  the all-pole backward then
 // runs with grad_y = du, and grad_zi gains the FIR's direct terms du(-1..-M).
-template <typename T>
-__global__ void __launch_bounds__(256) tv_fir_fwd_kernel(const T* __restrict__ b, const T* __restrict__ u,
-                                                         const T* __restrict__ zi, T* __restrict__ y, int M,
-                                                         int64_t Tlen, int64_t total) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= total) return;
-    const int64_t seq = i / Tlen, n = i - seq * Tlen;
-    const T* br = b + i * (M + 1);
-    double acc = 0.0;
-    for (int k = 0; k <= M; ++k) {
-        const int64_t m = n - k;
-        const T um = m >= 0 ? u[seq * Tlen + m] : (zi != nullptr ? zi[seq * M + (-m - 1)] : T(0));
-        acc = fma((double)br[k], (double)um, acc);
-    }
-    y[i] = (T)acc;
-}
-template <typename T>
-__global__ void __launch_bounds__(256) tv_fir_bwd_kernel(const T* __restrict__ b, const T* __restrict__ u,
-                                                         const T* __restrict__ zi, const T* __restrict__ gy,
-                                                         T* __restrict__ du, T* __restrict__ duneg,
-                                                         T* __restrict__ gb, int M, int64_t Tlen, int64_t B) {
-    const int64_t span = Tlen + M;                         // m = -M .. T-1
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= B * span) return;
-    const int64_t seq = i / span, m = i - seq * span - M;
-    double acc = 0.0;
-    if (gy != nullptr)
-        for (int k = 0; k <= M; ++k) {
-            const int64_t n = m + k;
-            if (n >= 0 && n < Tlen)
-                acc = fma((double)b[(seq * Tlen + n) * (M + 1) + k], (double)gy[seq * Tlen + n], acc);
-        }
-    if (m >= 0) {
-        du[seq * Tlen + m] = (T)acc;
-        if (gb != nullptr) {
-            const double dyn = gy != nullptr ? (double)gy[seq * Tlen + m] : 0.0;
-            for (int k = 0; k <= M; ++k) {
-                const int64_t q = m - k;
-                const T uq = q >= 0 ? u[seq * Tlen + q] : (zi != nullptr ? zi[seq * M + (-q - 1)] : T(0));
-                gb[(seq * Tlen + m) * (M + 1) + k] = (T)(dyn * (double)uq);
-            }
-        }
-    } else {
-        duneg[seq * M + (-m - 1)] = (T)acc;
+// One CTA per tile of FIR_TS consecutive samples of one sequence (compile-time
+// order: every loop unrolled, no runtime division): the tile's b rows
+// (contiguous in global memory) and the u / dy windows are staged in shared
+// memory by coalesced loads (row stride padded to an odd count: the per-thread
+// row reads are conflict free); grad_b rows leave through shared memory by
+// coalesced stores.
+constexpr int FIR_TS = 256;
+template <int M> struct Fir {
+    static constexpr int K = M + 1, RS = K | 1;
+};
+template <typename T, int M>
+__device__ __forceinline__ void fir_stage_rows(T* sb, const T* __restrict__ b, int64_t seq, int64_t Tlen, int64_t r0,
+                                               int nr) {
+    constexpr int K = Fir<M>::K, RS = Fir<M>::RS;
+    const int nv = (int)max((int64_t)0, min((int64_t)nr, Tlen - r0));   // rows inside the sequence
+    const T* src = b + (seq * Tlen + r0) * K;
+    for (int e = threadIdx.x; e < nr * K; e += FIR_TS) {
+        const int r = e / K, k = e - r * K;
+        sb[r * RS + k] = r < nv ? src[e] : T(0);
     }
 }
+template <typename T, int M>
+__device__ __forceinline__ T u_at(const T* __restrict__ u, const T* __restrict__ zi, int64_t seq, int64_t Tlen,
+                                  int64_t m) {
+    if (m >= 0) return m < Tlen ? u[seq * Tlen + m] : T(0);
+    return zi != nullptr ? zi[seq * M + (-m - 1)] : T(0);
+}
+template <typename T, int M>
+constexpr size_t fir_fwd_smem() { return ((size_t)FIR_TS * Fir<M>::RS + FIR_TS + M) * sizeof(T); }
+template <typename T, int M>
+constexpr size_t fir_bwd_smem() {
+    return ((size_t)(FIR_TS + M) * Fir<M>::RS + (size_t)FIR_TS * Fir<M>::K + 2 * (FIR_TS + M)) * sizeof(T);
+}
+
+template <typename T, int M>
+__global__ void __launch_bounds__(FIR_TS) tv_fir_fwd_kernel(const T* __restrict__ b, const T* __restrict__ u,
+                                                            const T* __restrict__ zi, T* __restrict__ y,
+                                                            int64_t Tlen, int64_t ntile) {
+    constexpr int RS = Fir<M>::RS;
+    extern __shared__ __align__(16) unsigned char fir_raw[];
+    T* sb = reinterpret_cast<T*>(fir_raw);
+    T* su = sb + FIR_TS * RS;                       // u(n0 - M .. n0 + FIR_TS - 1)
+    const int64_t seq = blockIdx.x / ntile, n0 = (blockIdx.x - seq * ntile) * (int64_t)FIR_TS;
+    const int t = threadIdx.x;
+    fir_stage_rows<T, M>(sb, b, seq, Tlen, n0, FIR_TS);
+    for (int e = t; e < FIR_TS + M; e += FIR_TS) su[e] = u_at<T, M>(u, zi, seq, Tlen, n0 - M + e);
+    __syncthreads();
+    if (n0 + t >= Tlen) return;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k <= M; ++k) acc = fma((double)sb[t * RS + k], (double)su[M + t - k], acc);
+    y[seq * Tlen + n0 + t] = (T)acc;
+}
+
+template <typename T, int M>
+__global__ void __launch_bounds__(FIR_TS) tv_fir_bwd_kernel(const T* __restrict__ b, const T* __restrict__ u,
+                                                            const T* __restrict__ zi, const T* __restrict__ gy,
+                                                            T* __restrict__ du, T* __restrict__ duneg,
+                                                            T* __restrict__ gb, int64_t Tlen, int64_t ntile) {
+    constexpr int K = Fir<M>::K, RS = Fir<M>::RS;
+    extern __shared__ __align__(16) unsigned char fir_raw[];
+    T* sb = reinterpret_cast<T*>(fir_raw);         // b rows n0 .. n0 + FIR_TS + M - 1
+    T* sg = sb + (FIR_TS + M) * RS;                // grad_b rows of the tile, contiguous (stride K)
+    T* sdy = sg + FIR_TS * K;                      // dy(n0 .. n0 + FIR_TS + M - 1)
+    T* su = sdy + FIR_TS + M;                      // u(n0 - M .. n0 + FIR_TS - 1)
+    const int64_t seq = blockIdx.x / ntile, n0 = (blockIdx.x - seq * ntile) * (int64_t)FIR_TS;
+    const int t = threadIdx.x;
+    fir_stage_rows<T, M>(sb, b, seq, Tlen, n0, FIR_TS + M);
+    for (int e = t; e < FIR_TS + M; e += FIR_TS) {
+        const int64_t n = n0 + e;
+        sdy[e] = (gy != nullptr && n < Tlen) ? gy[seq * Tlen + n] : T(0);
+        su[e] = u_at<T, M>(u, zi, seq, Tlen, n0 - M + e);
+    }
+    __syncthreads();
+    if (n0 + t < Tlen) {                            // du(m) = sum_k b_k(m+k) dy(m+k)
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k <= M; ++k) acc = fma((double)sb[(t + k) * RS + k], (double)sdy[t + k], acc);
+        du[seq * Tlen + n0 + t] = (T)acc;
+        const double dyn = (double)sdy[t];          // grad_b_k(m) = dy(m) u(m-k)
+#pragma unroll
+        for (int k = 0; k <= M; ++k) sg[t * K + k] = (T)(dyn * (double)su[M + t - k]);
+    }
+    if (n0 == 0 && t < M) {                         // du(-1-t) (the zi entries): sum_{k > t} b_k(k-1-t) dy(k-1-t)
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 1; k <= M; ++k)
+            if (k > t) acc = fma((double)sb[(k - 1 - t) * RS + k], (double)sdy[k - 1 - t], acc);
+        duneg[seq * M + t] = (T)acc;
+    }
+    if (gb == nullptr) return;
+    __syncthreads();
+    const int nv = (int)min((int64_t)FIR_TS, Tlen - n0);
+    T* gbt = gb + (seq * Tlen + n0) * K;            // the tile's grad_b rows are contiguous
+    for (int e = t; e < nv * K; e += FIR_TS) gbt[e] = sg[e];
+}
+
+template <typename T, int M>
+static iir_status_t fir_run(bool fwd, const iir_desc_t* d, const void* b, const void* u, const void* zi,
+                            const void* gy, void* y, void* du, void* duneg, void* gb, cudaStream_t st) {
+    const int64_t ntile = (d->length + FIR_TS - 1) / FIR_TS;
+    const unsigned grid = (unsigned)(d->batch * ntile);
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(tv_fir_fwd_kernel<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fir_fwd_smem<T, M>());
+        cudaFuncSetAttribute(tv_fir_bwd_kernel<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fir_bwd_smem<T, M>());
+    });
+    return launch(K_TV_FIR, st, [&] {
+        if (fwd)
+            tv_fir_fwd_kernel<T, M><<<grid, FIR_TS, fir_fwd_smem<T, M>(), st>>>(static_cast<const T*>(b),
+                static_cast<const T*>(u), static_cast<const T*>(zi), static_cast<T*>(y), d->length, ntile);
+        else
+            tv_fir_bwd_kernel<T, M><<<grid, FIR_TS, fir_bwd_smem<T, M>(), st>>>(static_cast<const T*>(b),
+                static_cast<const T*>(u), static_cast<const T*>(zi), static_cast<const T*>(gy), static_cast<T*>(du),
+                static_cast<T*>(duneg), static_cast<T*>(gb), d->length, ntile);
+    });
+}
+template <typename T>
+static iir_status_t fir_dispatch(bool fwd, const iir_desc_t* d, const void* b, const void* u, const void* zi,
+                                 const void* gy, void* y, void* du, void* duneg, void* gb, cudaStream_t st) {
+    switch (d->order) {
+#define IIRG_CASE(m) case m: return fir_run<T, m>(fwd, d, b, u, zi, gy, y, du, duneg, gb, st);
+        IIRG_TV_ORDERS(IIRG_CASE)
+#undef IIRG_CASE
+    }
+    return fail(IIR_EUNSUPPORTED, "per-sample order not compiled in");
+}
+
 template <typename T>
 __global__ void tv_add_kernel(T* __restrict__ dst, const T* __restrict__ src, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -196,16 +278,8 @@ iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* b, con
     iir_status_t s = d->dtype == IIR_F64 ? tv_dispatch<double>(true, d->order, L, ta, st)
                                          : tv_dispatch<float>(true, d->order, L, ta, st);
     if (s != IIR_OK || !fir) return s;
-    const int64_t total = d->batch * d->length;
-    const unsigned grid = (unsigned)((total + 255) / 256);
-    return launch(K_TV_FIR, st, [&] {
-        if (d->dtype == IIR_F64)
-            tv_fir_fwd_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(b), static_cast<const double*>(u),
-                static_cast<const double*>(zi), static_cast<double*>(y), d->order, d->length, total);
-        else
-            tv_fir_fwd_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(b), static_cast<const float*>(u),
-                static_cast<const float*>(zi), static_cast<float*>(y), d->order, d->length, total);
-    });
+    return d->dtype == IIR_F64 ? fir_dispatch<double>(true, d, b, u, zi, nullptr, y, nullptr, nullptr, nullptr, st)
+                               : fir_dispatch<float>(true, d, b, u, zi, nullptr, y, nullptr, nullptr, nullptr, st);
 }
 
 iir_status_t tv_backward(const iir_desc_t* d, const Layout& L, const void* gy, const void* gzf, const void* b,
@@ -216,20 +290,9 @@ iir_status_t tv_backward(const iir_desc_t* d, const Layout& L, const void* gy, c
     void* du = fir ? static_cast<void*>(ws + L.ws_du) : nullptr;
     void* duneg = fir ? static_cast<void*>(ws + L.ws_duneg) : nullptr;
     if (fir) {                                             // FIR stage adjoint first: du, grad_b
-        const int64_t n = d->batch * (d->length + d->order);
-        const unsigned grid = (unsigned)((n + 255) / 256);
-        iir_status_t s = launch(K_TV_FIR, st, [&] {
-            if (d->dtype == IIR_F64)
-                tv_fir_bwd_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(b),
-                    static_cast<const double*>(u), static_cast<const double*>(zi), static_cast<const double*>(gy),
-                    static_cast<double*>(du), static_cast<double*>(duneg), static_cast<double*>(gb), d->order,
-                    d->length, d->batch);
-            else
-                tv_fir_bwd_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(b),
-                    static_cast<const float*>(u), static_cast<const float*>(zi), static_cast<const float*>(gy),
-                    static_cast<float*>(du), static_cast<float*>(duneg), static_cast<float*>(gb), d->order,
-                    d->length, d->batch);
-        });
+        iir_status_t s = d->dtype == IIR_F64
+            ? fir_dispatch<double>(false, d, b, u, zi, gy, nullptr, du, duneg, gb, st)
+            : fir_dispatch<float>(false, d, b, u, zi, gy, nullptr, du, duneg, gb, st);
         if (s != IIR_OK) return s;
     }
     TvArgs ta{};
