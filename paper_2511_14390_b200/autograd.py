@@ -120,6 +120,50 @@ def allpole_tv(x, a, zi=None, return_zf=False):
     return (y, zf) if return_zf else y
 
 
+class TVDFFunction(torch.autograd.Function):
+    """y, zf = general per-sample DF-II filter (R19):
+    u(n) = x(n) - sum_i a[.., n, i-1] u(n-i),  y(n) = sum_k b[.., n, k] u(n-k);  zi = [u(-1) .. u(-M)]."""
+
+    @staticmethod
+    def forward(ctx, x, b, a, zi):
+        _require_cuda(x, b, a, zi)
+        x, b, a, zi = _c(x), _c(b), _c(a), _c(zi)
+        Bsz, T = x.shape
+        M = a.shape[-1]
+        desc = B.make_desc(Bsz, T, M, "df", x.dtype, B.IIR_COEF_PER_SAMPLE, flags=B.IIR_FLAG_PER_SAMPLE_B)
+        y = torch.empty_like(x)
+        zf = torch.empty((Bsz, M), dtype=x.dtype, device=x.device)
+        tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
+        tape = torch.empty(tb, dtype=torch.uint8, device=x.device)
+        ws = torch.empty(wb, dtype=torch.uint8, device=x.device)
+        B.iir_forward(desc, b, a, x, zi, y, zf, tape, tb, ws, wb)
+        ctx.desc = desc
+        ctx.has_zi = zi is not None
+        ctx.save_for_backward(b, a, zi if zi is not None else torch.empty(0, device=x.device), y, tape)
+        return y, zf
+
+    @staticmethod
+    def backward(ctx, gy, gzf):
+        b, a, zi, y, tape = ctx.saved_tensors
+        zi = zi if ctx.has_zi else None
+        desc = ctx.desc
+        gx = torch.empty_like(y) if ctx.needs_input_grad[0] else None
+        gb = torch.empty_like(b) if ctx.needs_input_grad[1] else None
+        ga = torch.empty_like(a) if ctx.needs_input_grad[2] else None
+        gzi = torch.empty_like(zi) if (zi is not None and ctx.needs_input_grad[3]) else None
+        wb = B.iir_workspace_bytes(desc)
+        ws = torch.empty(wb, dtype=torch.uint8, device=y.device)
+        B.iir_backward(desc, _c(gy), _c(gzf), b, a, None, y, zi, tape, tape.numel(), gx, gb, ga, gzi, ws, wb)
+        return gx, gb, ga, gzi
+
+
+def lfilter_tv(x, b, a, zi=None, return_zf=False):
+    """Differentiable general per-sample DF filter: x (B, T), b (B, T, M+1), a (B, T, M)
+    (a[.., n, i-1] = a_i(n), monic), zi (B, M) = past internal signal u."""
+    y, zf = TVDFFunction.apply(x, b, a, zi)
+    return (y, zf) if return_zf else y
+
+
 class LTIMatrixRecurrenceFunction(torch.autograd.Function):
     """v(1..N) = recurrence(A, v0, z): v(n+1) = A v(n) + z(n) (PAPER.md:296-343,
     Listing 1), batched: z (B, N, M), v0 (B, M), A (M, M) shared or (B, M, M)."""

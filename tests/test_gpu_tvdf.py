@@ -81,3 +81,28 @@ def test_config3_shape_with_numerator_fp32():
     """Config-3 shape (order 24, per-sample coefficients, 2^18 samples) with a per-sample numerator, 2 sequences."""
     p = inputs.tv_df_problem(1003, batch=2, length=1 << 18, order=24, dtype="f32")
     check(p, "f32")
+
+
+def test_autograd_function_matches_oracle():
+    from paper_2511_14390_b200 import lfilter_tv
+    p = inputs.tv_df_problem(34000, batch=2, length=3000, order=6, dtype="f32")
+    q = rounded(p, "f32")
+    dev = lambda v: torch.tensor(v, dtype=torch.float32, device="cuda", requires_grad=True)
+    x, b, a, zi = dev(q["x"]), dev(q["b"]), dev(q["a"]), dev(q["zi"])
+    y, zf = lfilter_tv(x, b, a, zi=zi, return_zf=True)
+    L = (y * torch.tensor(q["gy"], dtype=torch.float32, device="cuda")).sum() + \
+        (zf * torch.tensor(q["gzf"], dtype=torch.float32, device="cuda")).sum()
+    L.backward()
+    o = oracle.tv_df(q["b"], q["a"], q["x"], q["zi"], q["gy"], q["gzf"])
+    for k, t in (("y", y.detach()), ("zf", zf.detach()), ("gx", x.grad), ("gb", b.grad), ("ga", a.grad),
+                 ("gzi", zi.grad)):
+        assert nrm_err(t.double().cpu().numpy(), o[k]) < 1e-4, k
+
+
+def test_gradcheck_fp64_tiny():
+    from paper_2511_14390_b200 import lfilter_tv
+    torch.manual_seed(0)
+    mk = lambda *s: (0.2 * torch.randn(*s, dtype=torch.float64, device="cuda")).requires_grad_(True)
+    x, b, a, zi = mk(2, 19), mk(2, 19, 4), mk(2, 19, 3), mk(2, 3)
+    f = lambda x, b, a, zi: lfilter_tv(x, b, a, zi=zi, return_zf=True)
+    assert torch.autograd.gradcheck(f, (x, b, a, zi), eps=1e-6, atol=1e-8, rtol=1e-6)
