@@ -309,7 +309,7 @@ def run_ours(args, w, rank, world, dev, pg):
     # replayed once.  Eager launching (--no-graph) records them directly.
     B.iir_profile_reset()
     B.iir_profile_enable(True)
-    if use_graph:
+    if use_graph and world == 1:        # multi-rank runs profile eagerly (no second NCCL capture)
         pg_graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(pg_graph, stream=stream):
             run_steps(args.warmup, args.steps)
@@ -572,7 +572,8 @@ def main():
                 "algorithmic_bytes_per_launch": per_launch, "avg_launch_ms": avg_ms,
                 "launch_timing": "CUDA events around every library launch on its stream, the K steps captured "
                                  "with the events in a CUDA graph and replayed (event nodes serialise the "
-                                 "launches: no PDL overlap counted)" if r["graph"] else "CUDA events, eager launches",
+                                 "launches: no PDL overlap counted)" if (r["graph"] and world == 1)
+                                else "CUDA events, eager launches",
                 "kernel_ms": {k: t / n_ for k, (t, n_) in r["ktimes"].items()},
                 "share_of_step": {k: (t / args.steps) / step_kernel_ms for k, (t, _) in r["ktimes"].items()}}
     step_bytes = step_min_bytes(w) * w["batch"] * w["length"]
