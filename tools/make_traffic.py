@@ -17,7 +17,7 @@ from collections import OrderedDict, defaultdict
 KIND = [(r"rec_fwd_kernel", "rec_fwd"), (r"rec_bwd_kernel", "rec_bwd"), (r"lti_prep_kernel", "lti_prep"),
         (r"lti_red_kernel<[^>]*, *(\(bool\))?(0|false)>", "lti_red_fwd"),
         (r"lti_red_kernel<[^>]*, *(\(bool\))?(1|true)>", "lti_red_bwd"), (r"lti_cscan_kernel", "lti_cscan"),
-        (r"state_carry_kernel", "state_carry"), (r"lti_fwd_kernel", "lti_fwd"), (r"lti_bwd", "lti_bwd"),
+        (r"state_carry_kernel", "state_carry"), (r"tv_fir_|tv_add_kernel", "tv_fir"), (r"lti_fwd_kernel", "lti_fwd"), (r"lti_bwd", "lti_bwd"),
         (r"tv_phi2?_kernel", "tv_phi"), (r"tv_(group|groupchain|expand|chain)_kernel", "tv_chain"), (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?0>", "tv_fwd"),
         (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?1>", "tv_bwd_agg"),
         (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?2>", "tv_bwd")]
