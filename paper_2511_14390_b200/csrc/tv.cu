@@ -68,13 +68,26 @@ template <int M> struct Fir {
 template <typename T, int M>
 __device__ __forceinline__ void fir_stage_rows(T* sb, const T* __restrict__ b, int64_t seq, int64_t Tlen, int64_t r0,
                                                int nr) {
-    constexpr int K = Fir<M>::K, RS = Fir<M>::RS;
+    constexpr int K = Fir<M>::K, RS = Fir<M>::RS, W = 16 / (int)sizeof(T);
     const int nv = (int)max((int64_t)0, min((int64_t)nr, Tlen - r0));   // rows inside the sequence
     const T* src = b + (seq * Tlen + r0) * K;
-    for (int e = threadIdx.x; e < nr * K; e += FIR_TS) {
-        const int r = e / K, k = e - r * K;
-        sb[r * RS + k] = r < nv ? src[e] : T(0);
+    // asynchronous copies (no register round trip: every load of the tile is in
+    // flight at once); rows past the sequence end are zero-filled
+    if (RS == K && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {     // same layout: 16 B chunks
+        const int nvalid = nv * K;
+        for (int e = threadIdx.x * W; e < nr * K; e += FIR_TS * W) {
+            const int left = nvalid - e;
+            const unsigned bytes = left <= 0 ? 0u : (unsigned)(min(left, W) * (int)sizeof(T));
+            cp_async16(sb + e, bytes ? (const void*)(src + e) : (const void*)src, bytes);
+        }
+    } else {
+        for (int e = threadIdx.x; e < nr * K; e += FIR_TS) {
+            const int r = e / K, k = e - r * K;
+            if (r < nv) cp_async_elem(sb + r * RS + k, src + e);
+            else sb[r * RS + k] = T(0);
+        }
     }
+    cp_async_commit();
 }
 template <typename T, int M>
 __device__ __forceinline__ T u_at(const T* __restrict__ u, const T* __restrict__ zi, int64_t seq, int64_t Tlen,
@@ -101,6 +114,7 @@ __global__ void __launch_bounds__(FIR_TS) tv_fir_fwd_kernel(const T* __restrict_
     const int t = threadIdx.x;
     fir_stage_rows<T, M>(sb, b, seq, Tlen, n0, FIR_TS);
     for (int e = t; e < FIR_TS + M; e += FIR_TS) su[e] = u_at<T, M>(u, zi, seq, Tlen, n0 - M + e);
+    cp_async_wait<0>();
     __syncthreads();
     if (n0 + t >= Tlen) return;
     double acc = 0.0;
@@ -128,6 +142,7 @@ __global__ void __launch_bounds__(FIR_TS) tv_fir_bwd_kernel(const T* __restrict_
         sdy[e] = (gy != nullptr && n < Tlen) ? gy[seq * Tlen + n] : T(0);
         su[e] = u_at<T, M>(u, zi, seq, Tlen, n0 - M + e);
     }
+    cp_async_wait<0>();
     __syncthreads();
     if (n0 + t < Tlen) {                            // du(m) = sum_k b_k(m+k) dy(m+k)
         double acc = 0.0;
