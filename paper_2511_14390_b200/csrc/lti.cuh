@@ -1148,9 +1148,12 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
     const int64_t roff = seq * p.Tlen;
     IIRG_TRACE(p.trace, tk, 0);
 
-    // group 0: dy;  group 1: x, y (TDF) or u (DF)
+    // group 0: dy;  group 1: the power tables (in the tape, written by the forward's
+    // prologue);  group 2: x, y (TDF) or u (DF).  All in flight at once.
     if (p.gy != nullptr) tile_load_async<T, TS>(dys, static_cast<const T*>(p.gy) + roff, p0, p.Tlen, p.vec);
     else for (int e = tid; e < TS; e += NT) dys[pidx<T>(e)] = T(0);
+    cp_async_commit();
+    stage_small_async<M>(st, tb);
     cp_async_commit();
     if constexpr (FORM == 1) {
         tile_load_async<T, TS>(s2, static_cast<const T*>(p.x) + roff, p0, p.Tlen, p.vec);
@@ -1161,10 +1164,9 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
     cp_async_commit();
     if (!PRE) rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
     if (PRE) pdl_wait();                             // carries (lti_cscan_kernel) and, transitively, y / u
-    stage_small<M>(st, tb);                          // tables live in the tape (written by the forward)
     T bc[M + 1], ac[M + 1], cc[M];
     load_coefs<T, M>(tb, bc, ac, cc);
-    cp_async_wait<1>();                              // dy
+    cp_async_wait<2>();                              // dy
     __syncthreads();
 
     const int c = NT - 1 - tid;          // chunk index within the tile (time order)
@@ -1184,6 +1186,8 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
     }
     IIRG_TRACE(p.trace, tk, 1);
     // a6: carries (transposed powers), tiles last -> first.
+    cp_async_wait<1>();                              // power tables
+    __syncthreads();
     double S[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) S[i] = (double)d[i];
