@@ -164,7 +164,12 @@ __device__ __forceinline__ void tile_store(T* __restrict__ row, const T* __restr
                                            int64_t Tlen, bool vec) {
     using V = typename Vec<T>::type;
     constexpr int W = Vec<T>::W;
-    if (vec) {
+    if (vec && p0 >= 0 && p0 + N <= Tlen) {        // interior tile: no clipping
+        T* dst = row + p0;
+#pragma unroll
+        for (int q = threadIdx.x; q < N / W; q += NT)
+            stg_stream(reinterpret_cast<V*>(dst + q * W), *reinterpret_cast<const V*>(sm + pidx<T>(q * W)));
+    } else if (vec) {
 #pragma unroll 4
         for (int q = threadIdx.x; q < N / W; q += NT) {
             const int64_t pos = p0 + (int64_t)q * W;
@@ -184,6 +189,11 @@ __device__ __forceinline__ void tile_store(T* __restrict__ row, const T* __restr
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, unsigned src_bytes) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
+// 16 B through L1 (.ca): data every CTA of an SM reads (the power tables)
+__device__ __forceinline__ void cp_async16_ca(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" :: "r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -208,7 +218,11 @@ template <typename T, int N>
 __device__ __forceinline__ void tile_load_async(T* __restrict__ sm, const T* __restrict__ row, int64_t p0,
                                                 int64_t Tlen, bool vec) {
     constexpr int W = Vec<T>::W;
-    if (vec) {
+    if (vec && p0 >= 0 && p0 + N <= Tlen) {        // interior tile: no clipping
+        const T* src = row + p0;
+#pragma unroll
+        for (int q = threadIdx.x; q < N / W; q += NT) cp_async16(sm + pidx<T>(q * W), src + q * W, 16u);
+    } else if (vec) {
 #pragma unroll 4
         for (int q = threadIdx.x; q < N / W; q += NT) {
             const int64_t pos = p0 + (int64_t)q * W;

@@ -467,9 +467,12 @@ struct LtiBwdArgs {
 template <typename T, int M>
 __device__ __forceinline__ void raw_coefs(const T* __restrict__ b, const T* __restrict__ a, T (&bc)[M + 1],
                                           T (&ac)[M + 1]) {
-    const double a0 = (double)__ldg(a);
+    double bb[M + 1], aa[M + 1];                 // every load issued before the one division
 #pragma unroll
-    for (int k = 0; k <= M; ++k) { bc[k] = (T)((double)__ldg(b + k) / a0); ac[k] = (T)((double)__ldg(a + k) / a0); }
+    for (int k = 0; k <= M; ++k) { bb[k] = (double)__ldg(b + k); aa[k] = (double)__ldg(a + k); }
+    const double inv_a0 = 1.0 / aa[0];
+#pragma unroll
+    for (int k = 0; k <= M; ++k) { bc[k] = (T)(bb[k] * inv_a0); ac[k] = (T)(aa[k] * inv_a0); }
 }
 template <typename T, int M>
 __device__ __forceinline__ void load_coefs(const double* __restrict__ tb, T (&bc)[M + 1], T (&ac)[M + 1], T (&cc)[M]) {
@@ -482,7 +485,13 @@ __device__ __forceinline__ void load_coefs(const double* __restrict__ tb, T (&bc
 
 template <int M>
 __device__ __forceinline__ void stage_small_async(double* st, const double* __restrict__ tb) {
-    for (int i = threadIdx.x; i < Tab<M>::STAGE; i += blockDim.x) cp_async8(st + i, tb + i);
+    // 16 B copies through L1 (every CTA of the SM reads the same tables; st and tb
+    // are 16 B aligned: tables start on 256 B boundaries)
+    constexpr int N2 = Tab<M>::STAGE / 2;
+    for (int i = threadIdx.x; i < N2; i += blockDim.x) cp_async16_ca(st + 2 * i, tb + 2 * i);
+    if constexpr (Tab<M>::STAGE % 2 != 0) {
+        if (threadIdx.x == 0) cp_async8(st + Tab<M>::STAGE - 1, tb + Tab<M>::STAGE - 1);
+    }
 }
 // Stage the small power tables (PL | PW | PWT) of this tile's coefficient set.
 template <int M>
