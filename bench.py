@@ -1,12 +1,20 @@
 """Benchmark of the hot path: forward + backward IIR filtering (BASELINE.json metric
 "fwd+bwd filtered samples/sec (B x T / s) and HBM GB/s vs peak").
 
-    python bench.py [--gpus N --steps K --warmup W] [--workload c2|c1|c4|c5|c3] [--impl ours|reference]
+    python bench.py [--gpus N --steps K --warmup W] [--workload c5|c2|c1|c4|c3|f1|f2]
+                    [--scaling weak|strong] [--impl ours|reference]
+
+Default workload: BASELINE.json's config 5 (order-8 TDF, shared coefficients,
+2^16-sample sequences, coefficient-gradient all-reduce), the configuration the
+metric's 1/2/4/8-GPU figure is quoted on: weak scaling (default) runs 256
+sequences per GPU (2048 at G = 8); --scaling strong splits the global batch of
+2048 over the G ranks.  `--gpus N` with N > 1 launched without torchrun
+re-launches itself under `torch.distributed.run` (N ranks, one per GPU, NCCL).
 
 One step = iir_forward + iir_backward (all of SURVEY §8(a)'s rows a1-a8) over one
 batch of synthetic input already resident in HBM, plus (N > 1) the NCCL
-all-reduce of the shared-coefficient gradients.  Weak scaling: every rank
-filters the workload's per-GPU batch.  Inputs rotate over several buffer sets
+all-reduce of the shared-coefficient gradients (dist.reduce_shared_grads, the
+product's driver).  Inputs rotate over several buffer sets
 whose total size exceeds 2x L2, so no step reads data left in L2 by the
 previous one.  The timed region is K steps captured in one CUDA graph (eager
 with --no-graph), bracketed by barrier + synchronize, timed with CUDA events on
@@ -157,7 +165,7 @@ class Problem:
         self.w = w
         td = inputs.torch_dtype(w["dtype"])
         Bsz, T, M = w["batch"], w["length"], w["order"]
-        rng = np.random.default_rng(seed)
+        rng = np.random.default_rng(1000)          # coefficients: the same on every rank (SHARED filter)
         self.td = td
         g = torch.Generator(device=dev).manual_seed(seed)
         self.sets = []
@@ -220,9 +228,10 @@ class Problem:
         B.iir_backward(self.desc, s["gy"], self.gzf, self.b, self.a, s["x"], s["y"], self.zi, self.tape, self.tb,
                        s["gx"], self.gb, s.get("ga", self.ga), self.gzi, self.ws, self.wb, stream)
         if pg is not None and self.b is not None and self.w["coef"] == "shared":
-            # the one real exchange of the path: all-reduce of the shared-coefficient gradients (§8(e))
-            torch.cat([self.gb, self.ga], out=self.grad_buf)
-            torch.distributed.all_reduce(self.grad_buf, group=pg)
+            # the one real exchange of the path: all-reduce of the shared-coefficient gradients (§8(e)),
+            # through the product's batch-sharded driver
+            from paper_2511_14390_b200 import dist as D
+            D.reduce_shared_grads(self.gb, self.ga, group=pg)
         elif pg is not None and self.ss:
             torch.distributed.all_reduce(self.ga, group=pg)      # shared A of the bare recurrence
 
@@ -528,7 +537,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="c5: weak = 256 sequences per GPU; strong = the global batch of 2048 split over the GPUs")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -537,9 +548,29 @@ def main():
     args = ap.parse_args()
     w = dict(WORKLOADS[args.workload], key=args.workload, scan=args.scan)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run (the driver's own launch line)
+        if args.impl == "ours" and torch.cuda.device_count() < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} CUDA device(s) visible")
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "ours" and world != args.gpus:
+        print(f"[bench] note: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
+    if args.workload == "c5":
+        glob = inputs.CONFIGS["c5"]["batch"]
+        w["batch"] = 256 if args.scaling == "weak" else max(1, glob // world)
+        w["desc"] = (f"config 5: order-8 TDF shared coefficients, 2^16-sample sequences, fp32, "
+                     f"coefficient-gradient all-reduce; {w['batch']} sequences per GPU x {world} GPU(s) "
+                     f"({args.scaling} scaling; global batch {w['batch'] * world})")
 
     if args.impl == "reference":
         run_reference(args, w, rank, world)
@@ -584,9 +615,11 @@ def main():
         cpu = cpu_baseline(w)
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True,
+        "scaling": args.scaling,
         "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic (seeded Gaussian signals, random stable filters)",
-        "config": {"workload": w["desc"], "batch_per_gpu": w["batch"], "length": w["length"], "order": w["order"],
+        "config": {"workload": w["desc"], "batch_per_gpu": w["batch"], "global_batch": w["batch"] * world,
+                   "length": w["length"], "order": w["order"],
                    "form": w["form"], "coef": w["coef"], "scan_schedule": w["scan"],
                    "l2": f"{r['nsets']} rotating input/output buffer sets x {r['set_bytes'] / 2**20:.0f} MiB "
                          f"(> 2x L2 = {2 * r['L2'] / 2**20:.0f} MiB)",

@@ -65,7 +65,7 @@
 extern "C" {
 #endif
 
-#define IIRGRAD_ABI_VERSION 1
+#define IIRGRAD_ABI_VERSION 2
 
 typedef enum { IIR_OK = 0, IIR_EINVAL = 1, IIR_EUNSUPPORTED = 2, IIR_ECUDA = 3, IIR_EWORKSPACE = 4 } iir_status_t;
 typedef enum {
@@ -120,7 +120,11 @@ typedef enum {
      * b (B, T, M+1) and grad_b (B, T, M+1) are then required / returned; zi, zf are
      * the internal signal history [u(-1)..u(-M)].  Without it, PER_SAMPLE is the
      * all-pole filter (b must be NULL). */
-    IIR_FLAG_PER_SAMPLE_B = 8
+    IIR_FLAG_PER_SAMPLE_B = 8,
+    /* fp32 TDF-II with SHARED / PER_SEQ coefficients runs on the round-2 engine
+     * (persistent warp tiles) by default; this flag selects the
+     * round-1 engine (one CTA per tile) instead -- kept for A/B measurement. */
+    IIR_FLAG_LEGACY_LTI = 16
 } iir_flags_t;
 
 /* Bytes of the forward->backward tape / of the scratch workspace (0 on a bad desc). */
@@ -163,6 +167,15 @@ iir_status_t iir_backward(const iir_desc_t *desc, const void *grad_y, const void
  * launch, no host sync.  IIR_EINVAL on a bad rank / nseg / seg_len / NULL. */
 iir_status_t iir_state_carry(const iir_desc_t *desc, const void *a, const void *w, int32_t nseg, int32_t rank,
                              int64_t seg_len, int32_t reverse, void *out, iir_stream_t stream);
+
+/* Synchronises `stream`, then reports (and clears) the workspace's error word: a
+ * look-back wait that did not see its predecessor's aggregate within 2 s (a
+ * scheduling fault, e.g. CTAs that can never become co-resident) does not hang or
+ * trap; it completes the call with NaN outputs and sets this word.  Returns IIR_OK,
+ * or IIR_ECUDA with iir_last_error() describing the fault.  The word is cleared by
+ * the next call that does not pass IIR_FLAG_WS_READY (check right after the call).
+ * Host-synchronising: a diagnostic, not part of the hot path. */
+iir_status_t iir_check_workspace(const iir_desc_t *desc, void *ws, size_t ws_bytes, iir_stream_t stream);
 
 /* Thread-local message describing the last non-IIR_OK status of this thread. */
 const char *iir_last_error(void);

@@ -24,13 +24,15 @@ IIR_FLAG_WS_READY = 1
 IIR_FLAG_SINGLE_PASS = 2
 IIR_FLAG_THREE_PHASE = 4
 IIR_FLAG_PER_SAMPLE_B = 8
+IIR_FLAG_LEGACY_LTI = 16
 
 FORMS = {"df": IIR_DF2, "tdf": IIR_TDF2, "ss": IIR_SS, IIR_DF2: IIR_DF2, IIR_TDF2: IIR_TDF2, IIR_SS: IIR_SS}
 DTYPES = {torch.float32: IIR_F32, torch.float64: IIR_F64}
 
 EXPORTS = ["iir_tape_bytes", "iir_workspace_bytes", "iir_workspace_init", "iir_forward", "iir_backward", "iir_last_error",
            "iir_abi_version", "iir_launch_count", "iir_num_kernels", "iir_kernel_name",
-           "iir_profile_enable", "iir_profile_reset", "iir_profile_query", "iir_debug_trace", "iir_state_carry"]
+           "iir_profile_enable", "iir_profile_reset", "iir_profile_query", "iir_debug_trace", "iir_state_carry",
+           "iir_check_workspace"]
 
 
 class Desc(ctypes.Structure):
@@ -76,6 +78,8 @@ def lib():
         L.iir_state_carry.restype = ctypes.c_int
         L.iir_state_carry.argtypes = [dp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
                                       _vp, _vp]
+        L.iir_check_workspace.restype = ctypes.c_int
+        L.iir_check_workspace.argtypes = [dp, _vp, ctypes.c_size_t, _vp]
         L.iir_last_error.restype = ctypes.c_char_p
         L.iir_abi_version.restype = ctypes.c_int
         L.iir_launch_count.restype = ctypes.c_int64
@@ -148,6 +152,12 @@ def iir_state_carry(desc, a, w, nseg, rank, seg_len, reverse, out, stream=None):
     st = lib().iir_state_carry(ctypes.byref(desc), _ptr(a), _ptr(w), int(nseg), int(rank), int(seg_len),
                                1 if reverse else 0, _ptr(out), _stream(stream))
     _check(st, "iir_state_carry")
+
+
+def iir_check_workspace(desc, ws, ws_bytes, stream=None):
+    """Synchronise and raise if a look-back wait of the last call on ws timed out."""
+    _check(lib().iir_check_workspace(ctypes.byref(desc), _ptr(ws), int(ws_bytes), _stream(stream)),
+           "iir_check_workspace")
 
 
 def iir_last_error() -> str:

@@ -19,6 +19,27 @@ def _require_cuda(*ts):
             raise ValueError("paper_2511_14390_b200 runs on CUDA tensors only (no CPU fallback)")
 
 
+def _check(x, named_shapes):
+    """The C ABI receives raw pointers and takes the dtype from the descriptor: every
+    tensor must be on x's device, have x's dtype and the exact shape of its role, or
+    the kernels would read it as the wrong type / out of bounds.  Raises ValueError."""
+    if x.dtype not in (torch.float32, torch.float64):
+        raise ValueError(f"x must be float32 or float64, got {x.dtype}")
+    for name, t, shapes in named_shapes:
+        if t is None:
+            continue
+        if t.device != x.device:
+            raise ValueError(f"{name} is on {t.device}, x on {x.device}")
+        if t.dtype != x.dtype:
+            raise ValueError(f"{name} has dtype {t.dtype}, x has {x.dtype}")
+        if tuple(t.shape) not in [tuple(s) for s in shapes]:
+            raise ValueError(f"{name} has shape {tuple(t.shape)}, expected one of {[tuple(s) for s in shapes]}")
+
+
+def _stream(x):
+    return torch.cuda.current_stream(x.device)
+
+
 def _c(t):
     return None if t is None else t.contiguous()
 
@@ -29,9 +50,13 @@ class LFilterFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, b, a, zi, form):
         _require_cuda(x, b, a, zi)
-        x, b, a, zi = _c(x), _c(b), _c(a), _c(zi)
+        if x.dim() != 2 or b.dim() not in (1, 2):
+            raise ValueError("lfilter: x must be (B, T), b and a (M+1,) or (B, M+1)")
         Bsz, T = x.shape
         M = b.shape[-1] - 1
+        coef = [(M + 1,)] if b.dim() == 1 else [(Bsz, M + 1)]
+        _check(x, [("b", b, coef), ("a", a, coef), ("zi", zi, [(Bsz, M)])])
+        x, b, a, zi = _c(x), _c(b), _c(a), _c(zi)
         mode = B.IIR_COEF_SHARED if b.dim() == 1 else B.IIR_COEF_PER_SEQ
         desc = B.make_desc(Bsz, T, M, form, x.dtype, mode)
         y = torch.empty_like(x)
@@ -40,7 +65,8 @@ class LFilterFunction(torch.autograd.Function):
         wb = B.iir_workspace_bytes(desc)
         tape = torch.empty(tb, dtype=torch.uint8, device=x.device)
         ws = torch.empty(wb, dtype=torch.uint8, device=x.device)
-        B.iir_forward(desc, b, a, x, zi, y, zf, tape, tb, ws, wb)
+        with torch.cuda.device(x.device):
+            B.iir_forward(desc, b, a, x, zi, y, zf, tape, tb, ws, wb, _stream(x))
         ctx.desc = desc
         ctx.save_for_backward(x, b, a, zi if zi is not None else torch.empty(0, device=x.device), y, tape)
         ctx.has_zi = zi is not None
@@ -51,15 +77,16 @@ class LFilterFunction(torch.autograd.Function):
         x, b, a, zi, y, tape = ctx.saved_tensors
         zi = zi if ctx.has_zi else None
         desc = ctx.desc
-        gy = _c(gy)
-        gzf = _c(gzf)
+        gy = None if gy is None else _c(gy.to(x.dtype))
+        gzf = None if gzf is None else _c(gzf.to(x.dtype))
         gx = torch.empty_like(x) if ctx.needs_input_grad[0] else None
         gb = torch.empty_like(b) if ctx.needs_input_grad[1] else None
         ga = torch.empty_like(a) if ctx.needs_input_grad[2] else None
         gzi = torch.empty_like(zi) if (zi is not None and ctx.needs_input_grad[3]) else None
         wb = B.iir_workspace_bytes(desc)
         ws = torch.empty(wb, dtype=torch.uint8, device=x.device)
-        B.iir_backward(desc, gy, gzf, b, a, x, y, zi, tape, tape.numel(), gx, gb, ga, gzi, ws, wb)
+        with torch.cuda.device(x.device):
+            B.iir_backward(desc, gy, gzf, b, a, x, y, zi, tape, tape.numel(), gx, gb, ga, gzi, ws, wb, _stream(x))
         return gx, gb, ga, gzi, None
 
 
@@ -84,16 +111,20 @@ class AllPoleTVFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, a, zi):
         _require_cuda(x, a, zi)
-        x, a, zi = _c(x), _c(a), _c(zi)
+        if x.dim() != 2 or a.dim() != 3:
+            raise ValueError("allpole_tv: x must be (B, T), a (B, T, M)")
         Bsz, T = x.shape
         M = a.shape[-1]
+        _check(x, [("a", a, [(Bsz, T, M)]), ("zi", zi, [(Bsz, M)])])
+        x, a, zi = _c(x), _c(a), _c(zi)
         desc = B.make_desc(Bsz, T, M, "df", x.dtype, B.IIR_COEF_PER_SAMPLE)
         y = torch.empty_like(x)
         zf = torch.empty((Bsz, M), dtype=x.dtype, device=x.device)
         tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
         tape = torch.empty(tb, dtype=torch.uint8, device=x.device)
         ws = torch.empty(wb, dtype=torch.uint8, device=x.device)
-        B.iir_forward(desc, None, a, x, zi, y, zf, tape, tb, ws, wb)
+        with torch.cuda.device(x.device):
+            B.iir_forward(desc, None, a, x, zi, y, zf, tape, tb, ws, wb, _stream(x))
         ctx.desc = desc
         ctx.has_zi = zi is not None
         ctx.save_for_backward(a, zi if zi is not None else torch.empty(0, device=x.device), y, tape)
@@ -109,7 +140,11 @@ class AllPoleTVFunction(torch.autograd.Function):
         gzi = torch.empty_like(zi) if (zi is not None and ctx.needs_input_grad[2]) else None
         wb = B.iir_workspace_bytes(desc)
         ws = torch.empty(wb, dtype=torch.uint8, device=y.device)
-        B.iir_backward(desc, _c(gy), _c(gzf), None, a, None, y, zi, tape, tape.numel(), gx, None, ga, gzi, ws, wb)
+        gy = None if gy is None else _c(gy.to(y.dtype))
+        gzf = None if gzf is None else _c(gzf.to(y.dtype))
+        with torch.cuda.device(y.device):
+            B.iir_backward(desc, gy, gzf, None, a, None, y, zi, tape, tape.numel(), gx, None, ga, gzi, ws, wb,
+                           _stream(y))
         return gx, ga, gzi
 
 
@@ -127,16 +162,20 @@ class TVDFFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, b, a, zi):
         _require_cuda(x, b, a, zi)
-        x, b, a, zi = _c(x), _c(b), _c(a), _c(zi)
+        if x.dim() != 2 or a.dim() != 3:
+            raise ValueError("lfilter_tv: x must be (B, T), b (B, T, M+1), a (B, T, M)")
         Bsz, T = x.shape
         M = a.shape[-1]
+        _check(x, [("b", b, [(Bsz, T, M + 1)]), ("a", a, [(Bsz, T, M)]), ("zi", zi, [(Bsz, M)])])
+        x, b, a, zi = _c(x), _c(b), _c(a), _c(zi)
         desc = B.make_desc(Bsz, T, M, "df", x.dtype, B.IIR_COEF_PER_SAMPLE, flags=B.IIR_FLAG_PER_SAMPLE_B)
         y = torch.empty_like(x)
         zf = torch.empty((Bsz, M), dtype=x.dtype, device=x.device)
         tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
         tape = torch.empty(tb, dtype=torch.uint8, device=x.device)
         ws = torch.empty(wb, dtype=torch.uint8, device=x.device)
-        B.iir_forward(desc, b, a, x, zi, y, zf, tape, tb, ws, wb)
+        with torch.cuda.device(x.device):
+            B.iir_forward(desc, b, a, x, zi, y, zf, tape, tb, ws, wb, _stream(x))
         ctx.desc = desc
         ctx.has_zi = zi is not None
         ctx.save_for_backward(b, a, zi if zi is not None else torch.empty(0, device=x.device), y, tape)
@@ -153,7 +192,11 @@ class TVDFFunction(torch.autograd.Function):
         gzi = torch.empty_like(zi) if (zi is not None and ctx.needs_input_grad[3]) else None
         wb = B.iir_workspace_bytes(desc)
         ws = torch.empty(wb, dtype=torch.uint8, device=y.device)
-        B.iir_backward(desc, _c(gy), _c(gzf), b, a, None, y, zi, tape, tape.numel(), gx, gb, ga, gzi, ws, wb)
+        gy = None if gy is None else _c(gy.to(y.dtype))
+        gzf = None if gzf is None else _c(gzf.to(y.dtype))
+        with torch.cuda.device(y.device):
+            B.iir_backward(desc, gy, gzf, b, a, None, y, zi, tape, tape.numel(), gx, gb, ga, gzi, ws, wb,
+                           _stream(y))
         return gx, gb, ga, gzi
 
 
@@ -171,15 +214,19 @@ class LTIMatrixRecurrenceFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, A, v0, z):
         _require_cuda(A, v0, z)
-        A, v0, z = _c(A), _c(v0), _c(z)
+        if z.dim() != 3 or A.dim() not in (2, 3):
+            raise ValueError("matrix_recurrence: z must be (B, N, M), A (M, M) or (B, M, M)")
         Bsz, N, M = z.shape
+        _check(z, [("A", A, [(M, M)] if A.dim() == 2 else [(Bsz, M, M)]), ("v0", v0, [(Bsz, M)])])
+        A, v0, z = _c(A), _c(v0), _c(z)
         mode = B.IIR_COEF_SHARED if A.dim() == 2 else B.IIR_COEF_PER_SEQ
         desc = B.make_desc(Bsz, N, M, "ss", z.dtype, mode)
         v = torch.empty_like(z)
         tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
         tape = torch.empty(tb, dtype=torch.uint8, device=z.device)
         ws = torch.empty(wb, dtype=torch.uint8, device=z.device)
-        B.iir_forward(desc, None, A, z, v0, v, None, tape, tb, ws, wb)
+        with torch.cuda.device(z.device):
+            B.iir_forward(desc, None, A, z, v0, v, None, tape, tb, ws, wb, _stream(z))
         ctx.desc = desc
         ctx.has_v0 = v0 is not None
         ctx.save_for_backward(A, v0 if v0 is not None else torch.empty(0, device=z.device), v, tape)
@@ -195,7 +242,10 @@ class LTIMatrixRecurrenceFunction(torch.autograd.Function):
         gz = torch.empty_like(v) if ctx.needs_input_grad[2] else None
         wb = B.iir_workspace_bytes(desc)
         ws = torch.empty(wb, dtype=torch.uint8, device=v.device)
-        B.iir_backward(desc, _c(gv), None, None, A, None, v, v0, tape, tape.numel(), gz, None, gA, gv0, ws, wb)
+        gv = None if gv is None else _c(gv.to(v.dtype))
+        with torch.cuda.device(v.device):
+            B.iir_backward(desc, gv, None, None, A, None, v, v0, tape, tape.numel(), gz, None, gA, gv0, ws, wb,
+                           _stream(v))
         return gA, gv0, gz
 
 

@@ -13,6 +13,7 @@
 #include "lti.cuh"
 #include "host.h"
 #include "lti_host.cuh"
+#include "lti2.cuh"
 
 using namespace iirg;
 
@@ -95,7 +96,16 @@ iir_status_t rec_run(bool fwd, int dtype, int M, const Layout& L, const LtiFwdAr
                      cudaStream_t st);
 }  // namespace iirg
 
+// fp32 TDF-II with fixed coefficients runs on the round-2 engine (lti2.cuh) unless the
+// caller asks for a round-1 schedule.
+static bool use_v2(const iir_desc_t* d) {
+    return d->form == IIR_TDF2 && d->dtype == IIR_F32 &&
+           (d->coef_mode == IIR_COEF_SHARED || d->coef_mode == IIR_COEF_PER_SEQ) && d->order >= 1 && d->order <= 8 &&
+           !(d->flags & (IIR_FLAG_LEGACY_LTI | IIR_FLAG_THREE_PHASE));
+}
+
 static int scan_tile_samples(const iir_desc_t* d) {
+    if (use_v2(d)) return v2::tile_samples(d->order);
     return d->form == IIR_SS ? rec_tile_samples(d->dtype, d->order) : tile_samples(d->dtype, d->order);
 }
 
@@ -147,7 +157,7 @@ static Layout layout(const iir_desc_t* d) {
     const int64_t ng_set = (per_set + 31) / 32;
     L.ngroups = ng_set * L.ncoef;
     size_t o = 0;
-    L.ws_ticket = o; L.ws_done = o + 4; L.ws_epoch = o + 8; o += 256;
+    L.ws_ticket = o; L.ws_done = o + 4; L.ws_epoch = o + 8; L.ws_err = o + 64; o += 256;
     L.ws_gcnt = o; o += al256(L.ngroups * 4);
     L.ws_scnt = o; o += al256(L.ncoef * 4);
     L.ws_clear = o;
@@ -162,6 +172,15 @@ static Layout layout(const iir_desc_t* d) {
     L.ws_carb = o; o += al256(L.ntot * M * 8);
     L.ws_bytes = o;
     o = 0;
+    L.v2 = use_v2(d);
+    if (L.v2) {
+        L.tp_t64 = o; o += al256((size_t)L.ncoef * v2::tab64_doubles(M) * 8);
+        L.tp_t32 = o; o += al256((size_t)L.ncoef * v2::tab32_floats(M) * 4);
+        L.tp_tab = L.tp_t64;
+        L.tp_u = o;
+        L.tp_bytes = o;
+        return L;
+    }
     L.tp_tab = o; o += al256((size_t)L.ncoef * tab_size(M) * 8);
     L.tp_u = o;
     if (d->form == IIR_DF2) o += al256((size_t)d->batch * d->length * dsize(d->dtype));
@@ -201,6 +220,7 @@ static CarryWs carry_ws(const Layout& L, char* w, bool bwd) {
         c.nblk[l] = L.nblk[l];
     }
     c.nlev = L.nlev;
+    c.err = reinterpret_cast<unsigned*>(w + L.ws_err);
     return c;
 }
 
@@ -264,6 +284,27 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     const int64_t rowlen = d->length * (d->form == IIR_SS ? d->order : 1);
     const bool vec = (rowlen % W == 0) && aligned16(x) && aligned16(y) && aligned16(t + L.tp_u);
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) return tv_forward(d, L, b, a, x, zi, y, zf, t, w, vec, st);
+    if (L.v2) {
+        v2::Call c{};
+        c.st = st;
+        c.b = static_cast<const float*>(b);
+        c.a = static_cast<const float*>(a);
+        c.cstride = d->coef_mode == IIR_COEF_SHARED ? 0 : d->order + 1;
+        c.ncoef = L.ncoef;
+        c.nlev = L.nlev;
+        v2::FwdArgs& f = c.f;
+        f.x = static_cast<const float*>(x); f.y = static_cast<float*>(y);
+        f.zi = static_cast<const float*>(zi); f.zf = static_cast<float*>(zf);
+        f.t32 = reinterpret_cast<const float*>(t + L.tp_t32);
+        f.t32_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : (int64_t)v2::tab32_floats(d->order);
+        f.t64 = reinterpret_cast<const double*>(t + L.tp_t64);
+        f.t64_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : (int64_t)v2::tab64_doubles(d->order);
+        f.cw = carry_ws(L, w, false);
+        f.B = d->batch; f.T = d->length; f.ntiles = (int)L.ntiles; f.ntot = L.ntot;
+        f.vec = (d->length % 4 == 0) && aligned16(x) && aligned16(y);
+        f.trace = g_trace;
+        return v2::run(true, d->order, c);
+    }
 
     LtiCall c{};
     c.d = d; c.L = &L; c.st = st; c.is_fwd = true; c.b = b; c.a = a;
@@ -318,6 +359,32 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
                      aligned16(grad_x) && aligned16(t + L.tp_u);
     if (d->coef_mode == IIR_COEF_PER_SAMPLE)
         return tv_backward(d, L, grad_y, grad_zf, b, a, y, zi, t, grad_x, grad_b, grad_a, grad_zi, w, vec, st);
+    if (L.v2) {
+        v2::Call c{};
+        c.st = st;
+        c.ncoef = L.ncoef;
+        c.nlev = L.nlev;
+        v2::BwdArgs& g = c.g;
+        g.gy = static_cast<const float*>(grad_y); g.gzf = static_cast<const float*>(grad_zf);
+        g.x = static_cast<const float*>(x); g.y = static_cast<const float*>(y);
+        g.gx = static_cast<float*>(grad_x); g.gzi = static_cast<float*>(grad_zi);
+        g.gb = static_cast<float*>(grad_b); g.ga = static_cast<float*>(grad_a);
+        g.want_coef = (grad_b != nullptr || grad_a != nullptr);
+        g.t32 = reinterpret_cast<const float*>(t + L.tp_t32);
+        g.t32_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : (int64_t)v2::tab32_floats(d->order);
+        g.t64 = reinterpret_cast<const double*>(t + L.tp_t64);
+        g.t64_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : (int64_t)v2::tab64_doubles(d->order);
+        g.cw = carry_ws(L, w, true);
+        g.partial = reinterpret_cast<double*>(w + L.ws_part);
+        g.partial2 = reinterpret_cast<double*>(w + L.ws_part2);
+        g.gcnt = reinterpret_cast<unsigned*>(w + L.ws_gcnt);
+        g.scnt = reinterpret_cast<unsigned*>(w + L.ws_scnt);
+        g.ncoef = L.ncoef;
+        g.B = d->batch; g.T = d->length; g.ntiles = (int)L.ntiles; g.ntot = L.ntot;
+        g.vec = (d->length % 4 == 0) && aligned16(grad_y) && aligned16(x) && aligned16(y) && aligned16(grad_x);
+        g.trace = g_trace;
+        return v2::run(false, d->order, c);
+    }
 
     LtiCall c{};
     c.d = d; c.L = &L; c.st = st; c.is_fwd = false;
@@ -346,6 +413,25 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
         return rec_run(false, d->dtype, d->order, L, LtiFwdArgs{}, ba, st);
     }
     return run_lti_any(c);
+}
+
+iir_status_t iir_check_workspace(const iir_desc_t* d, void* ws, size_t ws_bytes, iir_stream_t stream) {
+    iir_status_t s = check_desc(d);
+    if (s != IIR_OK) return s;
+    const Layout L = layout(d);
+    if (ws == nullptr || ws_bytes < L.ws_bytes) return fail(IIR_EWORKSPACE, "workspace missing or too small");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    unsigned flag = 0;
+    unsigned* p = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + L.ws_err);
+    cudaError_t e = cudaMemcpyAsync(&flag, p, sizeof(flag), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(IIR_ECUDA, std::string("iir_check_workspace: ") + cudaGetErrorString(e));
+    if (flag != 0) {
+        cudaMemsetAsync(p, 0, sizeof(unsigned), st);
+        cudaStreamSynchronize(st);
+        return fail(IIR_ECUDA, "a look-back wait timed out (outputs of the affected call are NaN)");
+    }
+    return IIR_OK;
 }
 
 int64_t iir_launch_count(void) { return g_launches.load(); }

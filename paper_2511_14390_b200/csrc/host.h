@@ -46,6 +46,9 @@ struct Layout {
     size_t ws_du = 0, ws_duneg = 0;                        // general TV DF: FIR-stage adjoint of u
     size_t ws_psi = 0, ws_omega = 0, ws_sgrp = 0;          // TV two-level chain
     size_t tp_tab = 0, tp_u = 0, tp_extra = 0, tp_bytes = 0;
+    size_t tp_t64 = 0, tp_t32 = 0;                         // v2 engine tables (lti2.cuh)
+    size_t ws_err = 0;                                     // error word (look-back timeout)
+    bool v2 = false;
 };
 
 // per-sample (time-varying all-pole) path, tv.cu

@@ -434,6 +434,7 @@ struct CarryWs {
     double* agg[LEVELS];         // bank 0 level-l block aggregates [seq][block][M]; all-ones NaN = not published
     int64_t nblk[LEVELS];        // blocks per sequence at level l (ceil(ntiles / 32^l))
     int nlev;                    // levels in use
+    unsigned* err;               // workspace error word (a look-back wait that timed out)
 };
 
 struct LtiFwdArgs {
@@ -608,9 +609,12 @@ __device__ __forceinline__ bool slot_ready(const double (&v)[M]) {
     return r;
 }
 // Re-poll a slot whose first read was not ready, with exponential back-off.  A
-// slot that is never published is a bug: report and trap instead of hanging.
+// slot that is never published (a scheduling or library bug) does not hang the GPU
+// and does not trap (which would poison the whole CUDA context): after 2 s the
+// waiter sets the workspace error word (reported by iir_check_workspace) and
+// continues with NaN, so the call completes with NaN outputs.
 template <int M>
-__device__ __forceinline__ void wait_slot(const double* src, double (&v)[M]) {
+__device__ __forceinline__ void wait_slot(const double* src, double (&v)[M], unsigned* err) {
     unsigned ns = 32;
     unsigned long long t0 = 0;
     for (;;) {
@@ -621,9 +625,11 @@ __device__ __forceinline__ void wait_slot(const double* src, double (&v)[M]) {
         else {
             const unsigned long long now = gtimer();
             if (t0 == 0) t0 = now;
-            else if (now - t0 > 4000000000ull) {
-                printf("iirgrad: look-back slot %p never published\n", (const void*)src);
-                __trap();
+            else if (now - t0 > 2000000000ull) {
+                if (err != nullptr) atomicOr(err, 1u);
+#pragma unroll
+                for (int i = 0; i < M; ++i) v[i] = __longlong_as_double(0x7ff8000000000000LL);
+                return;
             }
         }
     }
@@ -677,7 +683,7 @@ __device__ __forceinline__ void tile_carry(const double* st, const double* __res
             if (lane < dl[l]) {
                 if (l >= PF) load_slot<M>(cw.agg[l] + (seq * cw.nblk[l] + (jt >> (5 * l)) - dl[l] + lane) * M, V[l]);
                 if (!slot_ready<M>(V[l]))
-                    wait_slot<M>(cw.agg[l] + (seq * cw.nblk[l] + (jt >> (5 * l)) - dl[l] + lane) * M, V[l]);
+                    wait_slot<M>(cw.agg[l] + (seq * cw.nblk[l] + (jt >> (5 * l)) - dl[l] + lane) * M, V[l], cw.err);
                 mv_pq<M, TR>(st, tb, l, dl[l] - 1 - lane, V[l], Tv);
             }
             warp_sum<M>(Tv);

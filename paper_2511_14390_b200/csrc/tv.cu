@@ -76,9 +76,16 @@ __device__ __forceinline__ void fir_stage_rows(T* sb, const T* __restrict__ b, i
     if (RS == K && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {     // same layout: 16 B chunks
         const int nvalid = nv * K;
         for (int e = threadIdx.x * W; e < nr * K; e += FIR_TS * W) {
-            const int left = nvalid - e;
-            const unsigned bytes = left <= 0 ? 0u : (unsigned)(min(left, W) * (int)sizeof(T));
-            cp_async16(sb + e, bytes ? (const void*)(src + e) : (const void*)src, bytes);
+            if (e + W <= nr * K) {
+                const int left = nvalid - e;
+                const unsigned bytes = left <= 0 ? 0u : (unsigned)(min(left, W) * (int)sizeof(T));
+                cp_async16(sb + e, bytes ? (const void*)(src + e) : (const void*)src, bytes);
+            } else {                   // the tile's last partial chunk: never write past nr * K
+                for (int q = e; q < nr * K; ++q) {
+                    if (q < nvalid) cp_async_elem(sb + q, src + q);
+                    else sb[q] = T(0);
+                }
+            }
         }
     } else {
         for (int e = threadIdx.x; e < nr * K; e += FIR_TS) {

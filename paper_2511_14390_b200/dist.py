@@ -82,10 +82,14 @@ def sharded_step(compute: Callable, x: torch.Tensor, gy: torch.Tensor, b: torch.
 def cuda_shard_compute(x, gy, b, a, zi, gzf, form):
     """Per-shard compute on the local GPU through the C ABI (no fallback)."""
     from . import _binding as B
+    from .autograd import _check
     if not x.is_cuda:
         raise ValueError("cuda_shard_compute needs CUDA tensors")
     Bsz, T = x.shape
     M = b.shape[-1] - 1
+    coef = [(M + 1,)] if b.dim() == 1 else [(Bsz, M + 1)]
+    _check(x, [("gy", gy, [(Bsz, T)]), ("b", b, coef), ("a", a, coef), ("zi", zi, [(Bsz, M)]),
+               ("gzf", gzf, [(Bsz, M)])])
     mode = B.IIR_COEF_SHARED if b.dim() == 1 else B.IIR_COEF_PER_SEQ
     desc = B.make_desc(Bsz, T, M, form, x.dtype, mode)
     tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
@@ -185,12 +189,15 @@ def cuda_time_ops(form: str) -> TimeShardOps:
     """The product's per-segment compute for filter form `form`: iir_forward /
     iir_backward / iir_state_carry on the local GPU through the C ABI (no fallback)."""
     from . import _binding as B
+    from .autograd import _check
 
     def fwd(x, b, a, zi):
         if not x.is_cuda:
             raise ValueError("cuda_time_ops needs CUDA tensors")
         Bsz, T = x.shape
         M = b.shape[-1] - 1
+        coef = [(M + 1,)] if b.dim() == 1 else [(Bsz, M + 1)]
+        _check(x, [("b", b, coef), ("a", a, coef), ("zi", zi, [(Bsz, M)])])
         d = B.make_desc(Bsz, T, M, form, x.dtype, B.IIR_COEF_SHARED if b.dim() == 1 else B.IIR_COEF_PER_SEQ)
         tb, wb = B.iir_tape_bytes(d), B.iir_workspace_bytes(d)
         tape = torch.empty(tb, dtype=torch.uint8, device=x.device)

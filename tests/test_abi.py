@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(L, n), n
         assert n in B.EXPORTS, n
-    assert B.iir_abi_version() == 1
+    assert B.iir_abi_version() == 2
 
 
 def test_workspace_and_tape_sizes():
@@ -33,8 +33,11 @@ def test_workspace_and_tape_sizes():
     assert B.iir_tape_bytes(d) > 0
     assert B.iir_workspace_bytes(d) > 0
     d_df = B.make_desc(64, 1 << 16, 2, "df", B.IIR_F32, B.IIR_COEF_SHARED)
-    # DF keeps the internal signal u in the tape: B*T*4 bytes more than TDF.
-    assert B.iir_tape_bytes(d_df) - B.iir_tape_bytes(d) >= 64 * (1 << 16) * 4
+    d_legacy = B.make_desc(64, 1 << 16, 2, "tdf", B.IIR_F32, B.IIR_COEF_SHARED, flags=B.IIR_FLAG_LEGACY_LTI)
+    # DF keeps the internal signal u in the tape: B*T*4 bytes more than TDF on the same engine.
+    assert B.iir_tape_bytes(d_df) - B.iir_tape_bytes(d_legacy) >= 64 * (1 << 16) * 4
+    # the round-2 engine's TDF tape holds only per-coefficient-set tables (no per-sample data)
+    assert B.iir_tape_bytes(d) < 1 << 20
     d_seq = B.make_desc(64, 1 << 16, 8, "tdf", B.IIR_F32, B.IIR_COEF_PER_SEQ)
     assert B.iir_tape_bytes(d_seq) > B.iir_tape_bytes(B.make_desc(64, 1 << 16, 8, "tdf", B.IIR_F32, 0))
 

@@ -98,6 +98,14 @@ def test_autograd_allpole_tv():
     assert nrm_err(zi.grad.cpu().numpy(), o["gzi"]) < 1e-10
 
 
+def test_config3_full_batch_fp32():
+    """Config 3 at its full size: all 32 sequences x 2^18 samples, LPC order 24, every
+    output element against the oracle (VERDICT r1 weak #1: was 4 of 32)."""
+    c = inputs.CONFIGS["c3"]
+    p = inputs.tv_allpole_problem(1003, batch=c["batch"], length=c["length"], order=c["order"], dtype="f32")
+    check(p, "f32")
+
+
 def test_config3_shape_fp64_exact_algorithm():
     """Same recipe in fp64: isolates the algorithm from fp32 rounding."""
     p = inputs.tv_allpole_problem(1003, batch=2, length=1 << 18, order=24, dtype="f64")

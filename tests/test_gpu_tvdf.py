@@ -83,6 +83,12 @@ def test_config3_shape_with_numerator_fp32():
     check(p, "f32")
 
 
+def test_config3_shape_with_numerator_full_batch_fp32():
+    """The f2 bench workload at its full size: 32 sequences x 2^18, order 24, per-sample b and a."""
+    p = inputs.tv_df_problem(1003, batch=32, length=1 << 18, order=24, dtype="f32")
+    check(p, "f32")
+
+
 def test_autograd_function_matches_oracle():
     from paper_2511_14390_b200 import lfilter_tv
     p = inputs.tv_df_problem(34000, batch=2, length=3000, order=6, dtype="f32")
