@@ -16,9 +16,14 @@ constexpr int NWF = IIRG_V2_NWF;   // warps per CTA, forward
 constexpr int NWB = IIRG_V2_NWB;   // warps per CTA, backward
 
 template <int M>
-constexpr size_t smem_bytes(bool gt, int nwp) {
-    return (gt ? 0 : (size_t)Cfg<M>::STAGE * 4) + (size_t)nwp * Cfg<M>::NBUF * Cfg<M>::BUF * 4;
+constexpr size_t smem_bytes(bool gt, int nwp, int nbuf) {
+    return (gt ? 0 : (size_t)Cfg<M>::STAGE * 4) + (size_t)nwp * nbuf * Cfg<M>::BUF * 4;
 }
+// shared buffers per warp: forward x in / y out; backward dy in, x -> dx, y
+template <int M, bool GT>
+constexpr auto fwd_kernel() { return lti2_fwd_kernel<M, NWF, GT>; }
+template <int M>
+constexpr size_t fwd_smem(bool gt) { return smem_bytes<M>(gt, NWF, 2); }
 
 // Per-device launch setup: the max-dynamic-smem attribute is per device, so it is
 // set (and the resident-CTA counts queried) once for every device that calls in.
@@ -40,18 +45,18 @@ struct Ops {
         if (!d.ready) {
             cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
             set_smem(lti2_prep_kernel<M>, Prep2Slots<M>::bytes());
-            set_smem(lti2_fwd_kernel<M, NWF, false>, smem_bytes<M>(false, NWF));
-            set_smem(lti2_fwd_kernel<M, NWF, true>, smem_bytes<M>(true, NWF));
-            set_smem(lti2_bwd_kernel<M, NWB, false>, smem_bytes<M>(false, NWB));
-            set_smem(lti2_bwd_kernel<M, NWB, true>, smem_bytes<M>(true, NWB));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ[0], lti2_fwd_kernel<M, NWF, false>, NWF * 32,
-                                                          smem_bytes<M>(false, NWF));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ[1], lti2_fwd_kernel<M, NWF, true>, NWF * 32,
-                                                          smem_bytes<M>(true, NWF));
+            set_smem(fwd_kernel<M, false>(), fwd_smem<M>(false));
+            set_smem(fwd_kernel<M, true>(), fwd_smem<M>(true));
+            set_smem(lti2_bwd_kernel<M, NWB, false>, smem_bytes<M>(false, NWB, 3));
+            set_smem(lti2_bwd_kernel<M, NWB, true>, smem_bytes<M>(true, NWB, 3));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ[0], fwd_kernel<M, false>(), NWF * 32,
+                                                          fwd_smem<M>(false));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ[1], fwd_kernel<M, true>(), NWF * 32,
+                                                          fwd_smem<M>(true));
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ[2], lti2_bwd_kernel<M, NWB, false>, NWB * 32,
-                                                          smem_bytes<M>(false, NWB));
+                                                          smem_bytes<M>(false, NWB, 3));
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ[3], lti2_bwd_kernel<M, NWB, true>, NWB * 32,
-                                                          smem_bytes<M>(true, NWB));
+                                                          smem_bytes<M>(true, NWB, 3));
             (void)cudaGetLastError();
             d.ready = true;
         }
@@ -73,12 +78,8 @@ struct Ops {
         if (s != IIR_OK) return s;
         const bool gt = c.ncoef > 1;
         return launch(K_LTI_FWD, c.st, [&] {
-            if (gt)
-                launch_pdl(lti2_fwd_kernel<M, NWF, true>, grid(d, 1, c.f.ntot, NWF), NWF * 32, smem_bytes<M>(true, NWF),
-                           c.st, c.f);
-            else
-                launch_pdl(lti2_fwd_kernel<M, NWF, false>, grid(d, 0, c.f.ntot, NWF), NWF * 32,
-                           smem_bytes<M>(false, NWF), c.st, c.f);
+            if (gt) launch_pdl(fwd_kernel<M, true>(), grid(d, 1, c.f.ntot, NWF), NWF * 32, fwd_smem<M>(true), c.st, c.f);
+            else launch_pdl(fwd_kernel<M, false>(), grid(d, 0, c.f.ntot, NWF), NWF * 32, fwd_smem<M>(false), c.st, c.f);
         });
     }
     static iir_status_t backward(const Call& c) {
@@ -86,11 +87,11 @@ struct Ops {
         const bool gt = c.ncoef > 1;
         return launch(K_LTI_BWD, c.st, [&] {
             if (gt)
-                launch_pdl(lti2_bwd_kernel<M, NWB, true>, grid(d, 3, c.g.ntot, NWB), NWB * 32, smem_bytes<M>(true, NWB),
+                launch_pdl(lti2_bwd_kernel<M, NWB, true>, grid(d, 3, c.g.ntot, NWB), NWB * 32, smem_bytes<M>(true, NWB, 3),
                            c.st, c.g);
             else
                 launch_pdl(lti2_bwd_kernel<M, NWB, false>, grid(d, 2, c.g.ntot, NWB), NWB * 32,
-                           smem_bytes<M>(false, NWB), c.st, c.g);
+                           smem_bytes<M>(false, NWB, 3), c.st, c.g);
         });
     }
 };

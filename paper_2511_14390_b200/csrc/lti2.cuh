@@ -1,46 +1,47 @@
 // lti2.cuh -- round-2 LTI engine for fp32 TDF-II filtering and its closed-form
 // backward (arXiv 2511.14390, Eqs.4-9; the BASELINE configs C2, C4, C5).
 //
-// Same method as lti.cuh (the chunked scan of Eq.10, with fp64
-// carries across tiles and a deterministic hierarchical look-back), re-laid out for
-// sm_100a as PERSISTENT WARP TILES:
+// Same method as lti.cuh (the chunked scan of Eq.10, with a
+// deterministic hierarchical look-back across tiles), re-laid out for sm_100a as
+// PERSISTENT WARP TILES:
 //   * a tile is 32 lane chunks of L samples of one sequence, owned by ONE warp (no
-//     block-level scan, no __syncthreads on the per-tile path); a CTA is NWP
-//     independent warps, the grid is one resident wave, and warps take tiles by an
-//     atomic ticket (tile t = time tile t / B of sequence t % B), so every tile a warp
-//     waits for was handed to a running warp;
+//     block-level scan, no __syncthreads on the per-tile path).  The grid is one
+//     resident wave; warp w of the grid takes tiles w, w + W, w + 2W, ... (W warps in the
+//     grid; tile t = time tile t / B of sequence t % B), so every tile a warp waits for
+//     belongs to a resident warp that reaches it first;
 //   * each lane's chunk arrives by one cp.async.bulk row copy (TMA engine, mbarrier
-//     completion) into a 16 B-padded shared row, double buffered: the next tile's
-//     load is in flight while the current tile looks back and emits;
+//     completion) into a 16 B-padded shared row;
 //   * the chunk aggregate (the zero-state end state, Eq.10's z) is the contraction
 //     w = sum_k K[k] x(k) with K[k] = A_f^(L-1-k) c (M FMA per sample, no serial
 //     chain) instead of a first run of the recursion;
-//   * the intra-warp carry scan runs in fp32 with paired FMAs (fma.rn.f32x2) and the
-//     prologue's powers A_f^(L 2^d); the cross-tile look-back in fp64 (lti.cuh);
-//   * forward emit: the TDF recursion re-run from the lane's exact carry-in (paired
-//     FMA form, lti.cuh Tdf2); y is written in place and leaves by bulk row stores;
+//   * the intra-warp carry scan runs with paired fp32 FMAs (fma.rn.f32x2) and the
+//     prologue's powers A_f^(L 2^d); the cross-tile look-back combines the predecessors'
+//     published aggregates in fp32 with per-lane power tables (lane l: A_f^(l 32^v TS));
+//   * tile pipeline per warp: tile t1's aggregate is computed and published BEFORE the
+//     warp waits on tile t0's look-back, and t0's input is parked in tensor memory
+//     (TMEM, 256 KB per SM, unused otherwise) between its aggregate and its emit, so a
+//     warp needs only one incoming shared buffer;
+//   * forward emit: the TDF recursion re-run from the lane's exact carry-in (paired FMA
+//     form, lti.cuh Tdf2) on x read back from TMEM; y leaves by bulk row stores;
 //   * backward: the adjoint state of TDF is the shift register d(n) = [g(n) ..
-//     g(n+M-1)] with g(n) = dy(n) - sum_k a_k g(n+k) (Eq.7 with A_f^T = A, C_f = e1),
-//     so after the carry pass A writes g over dy in shared memory and pass B (lanes
-//     interleaved over the tile, coalesced global x, y reads from L2) forms
-//     dx(n) = b0 dy(n) + sum_i c_i g(n+1+i) (Eq.8) and the coefficient sums of Eqs.6, 9.
-//     Substituting dy(n) = g(n) + sum_k a'_k g(n+k) (the recursion itself), pass B needs
-//     only g, x and y:  dx(n) = sum_{k=0..M} b'_k g(n+k)  (the adjoint of B(z)/A(z) is the
-//     reverse-time all-pole followed by the FIR b'), grad_b'_k = C_k = sum_n g(n+k) x(n)
-//     (k = 0..M; C_0 = Gd - sum_k a'_k Gx[k-1] of the state-space chain rule) and
-//     grad_a'_k = -D_k, D_k = sum_n g(n+k) y(n) (k = 1..M).
+//     g(n+M-1)] with g(n) = dy(n) - sum_k a'_k g(n+k) (Eq.7 with A_f^T = A, C_f = e1).
+//     Substituting dy(n) = g(n) + sum_k a'_k g(n+k) into Eq.8 and Eqs.6, 9 gives
+//       dx(n) = sum_{k=0..M} b'_k g(n+k)            (reverse-time all-pole, then FIR b'),
+//       grad_b'_k = C_k = sum_n g(n+k) x(n) (k = 0..M),   grad_a'_k = -D_k = -sum_n g(n+k) y(n),
+//     so one fused pass per lane (dy from TMEM, x and y by TMA rows) produces g, dx and the
+//     correlation sums with g(n..n+M) in registers.
 #pragma once
 #include "../../include/iirgrad.h"
 #include "lti.cuh"
 
 #ifndef IIRG_V2_NWF
-#define IIRG_V2_NWF 16
+#define IIRG_V2_NWF 12
 #endif
 #ifndef IIRG_V2_NWB
-#define IIRG_V2_NWB 16
+#define IIRG_V2_NWB 8
 #endif
 #ifndef IIRG_V2_L
-#define IIRG_V2_L 32
+#define IIRG_V2_L 64
 #endif
 
 namespace iirg {
@@ -52,20 +53,22 @@ template <int M> struct Cfg {
     static constexpr int MP = (M + 1) & ~1;             // order padded to a pair
     static constexpr int NPR = MP / 2;
     static constexpr int PITCH = L + 4;                 // floats per shared row (16 B pad)
-    static constexpr int BUF = 32 * PITCH + 16;         // 32 chunk rows + a 16-float halo (backward)
-    static constexpr int NBUF = 3;                      // buffers per warp (tile pipeline depth)
+    static constexpr int BUF = 32 * PITCH;              // 32 chunk rows
     static constexpr int r4(int n) { return (n + 3) / 4 * 4; }
-    // fp32 tables, one group per direction (forward: A_f = companion(a')^T; backward: A = A_f^T):
+    // fp32 tables, one group per direction (forward: X = A_f = companion(a')^T; backward:
+    // X = A = A_f^T):
     //   K [L][MP] | P [5][M][MP] (P[d][j][i] = X^(L 2^d)[i][j]) | b'[M+1] a'[M+1] c[M] |
-    //   Q [M][NPR][32] float2 (Q[j][ip][l] = (X^(l L)[2ip][j], X^(l L)[2ip+1][j]))
-    // [0, OQ) is staged in shared memory; Q (each lane reads its own matrix) is read through L1.
+    //   Q  [M][NPR][32] float2: Q[j][ip][l]    = (X^(l L)[2ip][j], X^(l L)[2ip+1][j])
+    //   PQ [LEVELS][M][NPR][32] float2: PQ[v][j][ip][k] = the same pairs of X^(k 32^v TS)
+    // [0, OQ) is staged in shared memory (broadcast reads); Q and PQ (each lane reads its
+    // own matrix) are read through L1.
     static constexpr int OK_ = 0, OP = r4(L * MP), OC = OP + r4(5 * M * MP), OQ = OC + r4(3 * M + 2);
+    static constexpr int OPQ = OQ + 32 * M * MP;
     static constexpr int STAGE = OQ;
-    static constexpr int DIR = OQ + 32 * M * MP;
+    static constexpr int DIR = OPQ + LEVELS * 32 * M * MP;
     static constexpr int SIZE32 = 2 * DIR;
-    // fp64 tables: look-back powers A_f^(k 32^l TS) [LEVELS][M*M][32], b'[M+1], a'[M+1], a0
-    static constexpr int M2 = M * M;
-    static constexpr int PQ = 0, COEF = LEVELS * 32 * M2, A0 = COEF + 2 * (M + 1);
+    // fp64: b'[M+1], a'[M+1], a0 (the chain rule of the gradient finalize)
+    static constexpr int COEF = 0, A0 = 2 * (M + 1);
     static constexpr int SIZE64 = (A0 + 1 + 31) / 32 * 32;
     static constexpr int NG = 2 * M + 1;                 // coefficient partial sums per tile
 };
@@ -115,137 +118,19 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
 __device__ __forceinline__ unsigned long long ld2(const float* p) {
     return *reinterpret_cast<const unsigned long long*>(p);
 }
-template <int M>
-__device__ __forceinline__ float comp(const unsigned long long (&S)[Cfg<M>::NPR], int j) {
+template <int NPR>
+__device__ __forceinline__ float comp(const unsigned long long (&S)[NPR], int j) {
     return (j & 1) ? hi2(S[j >> 1]) : lo2(S[j >> 1]);
 }
-
-// acc += (TR ? P^T : P) v, P = A_f^(k 32^l TS) from the fp64 look-back table (global, L1).
-template <int M, bool TR>
-__device__ __forceinline__ void mv_pq2(const double* __restrict__ t64, int l, int k, const double (&v)[M],
-                                       double (&acc)[M]) {
-    const double* P = t64 + Cfg<M>::PQ + l * 32 * M * M + k;
+template <int M, int NPR>
+__device__ __forceinline__ void pack_pairs(const float (&v)[M], unsigned long long (&o)[NPR]) {
 #pragma unroll
-    for (int i = 0; i < M; ++i) {
-        double s = acc[i];
-#pragma unroll
-        for (int j = 0; j < M; ++j) s = fma(__ldg(P + (TR ? j * M + i : i * M + j) * 32), v[j], s);
-        acc[i] = s;
-    }
+    for (int ip = 0; ip < NPR; ++ip) o[ip] = pk2(v[2 * ip], 2 * ip + 1 < M ? v[2 * ip + 1] : 0.f);
 }
-
-// Look-back payload publication: a value equal to the all-ones sentinel (a NaN with
-// the sign bit set, which a negation of the canonical NaN could produce) is published
-// as the canonical NaN, so a NaN input propagates instead of never becoming ready.
-template <int M>
-__device__ __forceinline__ void publish2(double* dst, const double (&v)[M], int lane) {
-    if (lane == 0) {
+template <int M, int NPR>
+__device__ __forceinline__ void unpack_pairs(const unsigned long long (&S)[NPR], float (&v)[M]) {
 #pragma unroll
-        for (int i = 0; i < M; ++i) {
-            double x = v[i];
-            if (is_sentinel(x)) x = __longlong_as_double(0x7ff8000000000000LL);
-            __stcg(dst + i, x);
-        }
-    }
-}
-
-// Cross-tile carry of one warp tile (the hierarchical base-32 look-back of lti.cuh
-// tile_carry, per warp), in two halves so that a tile's aggregate is published as soon
-// as it is known, before the warp waits on the look-back of an earlier tile.
-// Publication: tile jt's zero-carry aggregate G (tile 0 of a sequence folds in the
-// initial state: G += Q_0 X0) goes to its level-0 slot.
-template <int M, bool TR>
-__device__ __forceinline__ void warp_publish(const double* __restrict__ t64, int lane, int jt, int64_t seq,
-                                             const double (&X0)[M], double (&G)[M], const CarryWs& cw) {
-    if (jt == 0) mv_pq2<M, TR>(t64, 0, 1, X0, G);
-    publish2<M>(cw.agg[0] + (seq * cw.nblk[0] + jt) * M, G, lane);
-}
-// Closing publication: a tile whose lower base-32 digits are all 31 completes a block at
-// every such level; right after its own aggregate (not at its later look-back) it sums the
-// block's other 31 level-l aggregates, T_l = sum_{d<31} Q_l^(30-d) AGG^(l)_{32b+d}, and
-// publishes the block's level-(l+1) aggregate Q_l T_l + Own_l (Own_0 = G).  Publishing at
-// aggregate time keeps every level's aggregates as prompt as the tile aggregates.
-template <int M, bool TR>
-__device__ __forceinline__ void warp_close(const double* __restrict__ t64, int lane, int jt, int64_t seq,
-                                           const double (&G)[M], const CarryWs& cw) {
-    const int nl = cw.nlev;
-    if (nl < 2 || (jt & 31) != 31) return;
-    double Own[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) Own[i] = G[i];
-#pragma unroll 1
-    for (int l = 0; l + 1 < nl; ++l) {
-        if (((jt >> (5 * l)) & 31) != 31) break;
-        const int64_t blk = jt >> (5 * l);
-        double Tv[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) Tv[i] = 0.0;
-        if (lane < 31) {
-            double V[M];
-            const double* slot = cw.agg[l] + (seq * cw.nblk[l] + blk - 31 + lane) * M;
-            load_slot<M>(slot, V);
-            if (!slot_ready<M>(V)) wait_slot<M>(slot, V, cw.err);
-            mv_pq2<M, TR>(t64, l, 30 - lane, V, Tv);
-        }
-        warp_sum<M>(Tv);
-        mv_pq2<M, TR>(t64, l, 1, Tv, Own);                        // Own = Q_l T_l + Own
-        publish2<M>(cw.agg[l + 1] + (seq * cw.nblk[l + 1] + (jt >> (5 * (l + 1)))) * M, Own, lane);
-    }
-}
-
-// Look-back: returns in every lane the state X entering tile jt (scan order) of
-// sequence seq.  With base-32 digits d_l of jt, Q_l = A_f^(32^l TS):
-//   T_l = sum_{d < d_l} Q_l^(d_l - 1 - d) AGG^(l)_{(jt >> 5l) - d_l + d}     (lane d, one round trip)
-//   X   = T_0 + Q_0^d_0 (T_1 + Q_1^d_1 (T_2 + ...))
-// Each T_l is a fixed butterfly sum: bitwise deterministic.
-template <int M, bool TR>
-__device__ __forceinline__ void warp_lookback(const double* __restrict__ t64, int lane, int jt, int64_t seq,
-                                              const double (&X0)[M], const CarryWs& cw, double (*sT)[M],
-                                              double (&X)[M]) {
-    if (jt == 0) {
-#pragma unroll
-        for (int i = 0; i < M; ++i) X[i] = X0[i];
-        return;
-    }
-    const int nl = cw.nlev;
-#pragma unroll 1
-    for (int l = 0; l < nl; ++l) {
-        const int d = (jt >> (5 * l)) & 31;
-        const int64_t blk = jt >> (5 * l);
-        double Tv[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) Tv[i] = 0.0;
-        if (d > 0) {
-            if (lane < d) {
-                double V[M];
-                const double* slot = cw.agg[l] + (seq * cw.nblk[l] + blk - d + lane) * M;
-                load_slot<M>(slot, V);
-                if (!slot_ready<M>(V)) wait_slot<M>(slot, V, cw.err);
-                mv_pq2<M, TR>(t64, l, d - 1 - lane, V, Tv);
-            }
-            warp_sum<M>(Tv);
-        }
-        if (lane == 0) {
-#pragma unroll
-            for (int i = 0; i < M; ++i) sT[l][i] = Tv[i];
-        }
-    }
-    __syncwarp();
-    double R[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) R[i] = sT[nl - 1][i];
-#pragma unroll 1
-    for (int l = nl - 2; l >= 0; --l) {
-        double R2[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) R2[i] = sT[l][i];
-        mv_pq2<M, TR>(t64, l, (jt >> (5 * l)) & 31, R, R2);
-#pragma unroll
-        for (int i = 0; i < M; ++i) R[i] = R2[i];
-    }
-#pragma unroll
-    for (int i = 0; i < M; ++i) X[i] = R[i];
-    __syncwarp();                                    // sT is reused by the warp's next tile
+    for (int j = 0; j < M; ++j) v[j] = comp<NPR>(S, j);
 }
 
 // NPR consecutive float pairs from shared memory, 128-bit loads where aligned.
@@ -264,25 +149,243 @@ __device__ __forceinline__ void ld_pairs(const float* p, unsigned long long (&o)
     }
 }
 
-// Load the rows of one tile: lane r's row holds samples [p0 + rL, p0 + (r+1)L) of
-// `src` (one sequence, length T); samples outside [0, T) (or src == NULL) read as 0.
-// vec: bulk row copies on the TMA engine, completion counted on `bar`; else element
-// copies by the lanes and a plain arrive.
+// ---------------------------------------------------------------------------
+// Static persistent schedule: warp w of W takes tiles w, w + W, ...; (seq, j) of tile t =
+// (t % B, t / B) are advanced incrementally (no division per tile).
+struct Sched {
+    unsigned t; int64_t seq; int j;
+    unsigned W; int dj; int64_t ds, B;
+    __device__ __forceinline__ void init(unsigned t0, unsigned nw, int64_t b) {
+        W = nw; B = b;
+        t = t0; seq = (int64_t)(t0 % (unsigned long long)b); j = (int)(t0 / (unsigned long long)b);
+        dj = (int)(nw / (unsigned long long)b); ds = (int64_t)(nw % (unsigned long long)b);
+    }
+    __device__ __forceinline__ void next() {
+        t += W; seq += ds; j += dj;
+        if (seq >= B) { seq -= B; ++j; }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Cross-tile carry in fp32.  Look-back slots hold M floats (all-ones = not published;
+// 4-byte stores and loads are single-copy atomic, a reader re-polls until no element is
+// the sentinel).  A value equal to the sentinel (a NaN with the sign bit set) is
+// published as the canonical NaN, so a NaN input propagates instead of looking unpublished.
+__device__ __forceinline__ float ld_vol_f32(const float* p) {
+    float v;
+    asm volatile("ld.volatile.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ bool sent32(float v) { return __float_as_uint(v) == 0xffffffffu; }
+template <int M>
+__device__ __forceinline__ void slot_load(const float* src, float (&v)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) v[i] = ld_vol_f32(src + i);
+}
+template <int M>
+__device__ __forceinline__ bool slot_ok(const float (&v)[M]) {
+    bool r = true;
+#pragma unroll
+    for (int i = 0; i < M; ++i) r = r && !sent32(v[i]);
+    return r;
+}
+// A slot that is never published (a scheduling fault, e.g. CTAs that cannot all be
+// resident) does not hang or trap: after 2 s the waiter sets the workspace error word
+// (iir_check_workspace) and continues with NaN.
+template <int M>
+__device__ __forceinline__ void slot_wait(const float* src, float (&v)[M], unsigned* err) {
+    unsigned ns = 32;
+    unsigned long long t0 = 0;
+    for (;;) {
+        __nanosleep(ns);
+        slot_load<M>(src, v);
+        if (slot_ok<M>(v)) return;
+        if (ns < 256) ns *= 2;
+        else {
+            const unsigned long long now = gtimer();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 2000000000ull) {
+                if (err != nullptr) atomicOr(err, 1u);
+#pragma unroll
+                for (int i = 0; i < M; ++i) v[i] = __uint_as_float(0x7fc00000u);
+                return;
+            }
+        }
+    }
+}
+template <int M>
+__device__ __forceinline__ void slot_publish(float* dst, const float (&v)[M], int lane) {
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) __stcg(dst + i, sent32(v[i]) ? __uint_as_float(0x7fc00000u) : v[i]);
+    }
+}
+template <int M>
+__device__ __forceinline__ float* slot_ptr(const CarryWs& cw, int lev, int64_t seq, int64_t blk) {
+    return reinterpret_cast<float*>(cw.agg[lev]) + (seq * cw.nblk[lev] + blk) * M;
+}
+
+// acc += Y v with Y = matrix k of a pair table [j][ip][32] (k = lane: each lane its own
+// matrix, coalesced; k uniform: broadcast).
+template <int M>
+__device__ __forceinline__ void mvp(const float* __restrict__ Y, int k, const float (&v)[M],
+                                    unsigned long long (&acc)[Cfg<M>::NPR]) {
+    constexpr int NPR = Cfg<M>::NPR;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+        const unsigned long long Vj = pk2(v[j], v[j]);
+#pragma unroll
+        for (int ip = 0; ip < NPR; ++ip) {
+            const float2 q = __ldg(reinterpret_cast<const float2*>(Y) + (j * NPR + ip) * 32 + k);
+            acc[ip] = ffma2(pk2(q.x, q.y), Vj, acc[ip]);
+        }
+    }
+}
+// Sum over the warp by a fixed xor butterfly: every lane ends with bitwise the same sum
+// (each step adds the same two values in both partner lanes).
+template <int NPR>
+__device__ __forceinline__ void warp_sum2(unsigned long long (&a)[NPR]) {
+    const unsigned long long ONE = pk2(1.f, 1.f);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+        for (int ip = 0; ip < NPR; ++ip) {
+            const float lo = __shfl_xor_sync(0xffffffffu, lo2(a[ip]), o);
+            const float hi = __shfl_xor_sync(0xffffffffu, hi2(a[ip]), o);
+            a[ip] = ffma2(ONE, pk2(lo, hi), a[ip]);
+        }
+}
+
+// Publication of tile jt's zero-carry aggregate G (tile 0 of a sequence folds in the
+// initial state: G += Y_0^1 X0), then, for a tile whose lower base-32 digits are all 31,
+// the aggregates of the blocks it closes: T_v = sum_{l<31} Y_v^l AGG^(v)_{blk-1-l} over the
+// block's other 31 members and AGG^(v+1) = Y_v T_v + Own_v (Own_0 = G).  Publishing at
+// aggregate time keeps every level as prompt as the tile aggregates.
+template <int M>
+__device__ __forceinline__ void carry_publish(const float* __restrict__ PQ, int lane, int jt, int64_t seq,
+                                              const float (&X0)[M], float (&G)[M], const CarryWs& cw) {
+    constexpr int NPR = Cfg<M>::NPR, LV = 32 * M * Cfg<M>::MP;
+    if (jt == 0) {
+        unsigned long long G2[NPR];
+        pack_pairs<M, NPR>(G, G2);
+        mvp<M>(PQ, 1, X0, G2);
+        unpack_pairs<M, NPR>(G2, G);
+    }
+    slot_publish<M>(slot_ptr<M>(cw, 0, seq, jt), G, lane);
+    const int nl = cw.nlev;
+    if (nl < 2 || (jt & 31) != 31) return;
+    float Own[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) Own[i] = G[i];
+#pragma unroll 1
+    for (int v = 0; v + 1 < nl; ++v) {
+        if (((jt >> (5 * v)) & 31) != 31) break;
+        const int64_t blk = jt >> (5 * v);
+        float V[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) V[i] = 0.f;
+        if (lane < 31) {
+            const float* sp = slot_ptr<M>(cw, v, seq, blk - 1 - lane);
+            slot_load<M>(sp, V);
+            if (!slot_ok<M>(V)) slot_wait<M>(sp, V, cw.err);
+        }
+        __syncwarp();
+        unsigned long long T2[NPR];
+#pragma unroll
+        for (int ip = 0; ip < NPR; ++ip) T2[ip] = 0ull;
+        mvp<M>(PQ + v * LV, lane, V, T2);
+        warp_sum2<NPR>(T2);
+        float T[M];
+        unpack_pairs<M, NPR>(T2, T);
+        unsigned long long O2[NPR];
+        pack_pairs<M, NPR>(Own, O2);
+        mvp<M>(PQ + v * LV, 1, T, O2);                              // Own = Y_v T_v + Own
+        unpack_pairs<M, NPR>(O2, Own);
+        slot_publish<M>(slot_ptr<M>(cw, v + 1, seq, jt >> (5 * (v + 1))), Own, lane);
+    }
+}
+
+// Look-back: the state X entering tile jt (scan order) of sequence seq, in every lane.
+// With base-32 digits d_v of jt and Y_v = X^(32^v TS):
+//   T_v = sum_{l < d_v} Y_v^l AGG^(v)_{(jt >> 5v) - 1 - l}         (lane l, one round trip)
+//   X   = T_0 + Y_0^d_0 (T_1 + Y_1^d_1 (T_2 + ...))
+// Fixed combination order (per-lane products, a fixed butterfly): bitwise deterministic.
+template <int M>
+__device__ __forceinline__ void carry_lookback(const float* __restrict__ PQ, int lane, int jt, int64_t seq,
+                                               const float (&X0)[M], const CarryWs& cw, float (*sT)[M],
+                                               float (&X)[M]) {
+    constexpr int NPR = Cfg<M>::NPR, LV = 32 * M * Cfg<M>::MP;
+    if (jt == 0) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) X[i] = X0[i];
+        return;
+    }
+    const int nl = cw.nlev;
+#pragma unroll 1
+    for (int v = 0; v < nl; ++v) {
+        const int d = (jt >> (5 * v)) & 31;
+        const int64_t blk = jt >> (5 * v);
+        float V[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) V[i] = 0.f;
+        if (lane < d) {
+            const float* sp = slot_ptr<M>(cw, v, seq, blk - 1 - lane);
+            slot_load<M>(sp, V);
+            if (!slot_ok<M>(V)) slot_wait<M>(sp, V, cw.err);
+        }
+        __syncwarp();
+        unsigned long long T2[NPR];
+#pragma unroll
+        for (int ip = 0; ip < NPR; ++ip) T2[ip] = 0ull;
+        mvp<M>(PQ + v * LV, lane, V, T2);
+        warp_sum2<NPR>(T2);
+        if (lane == 0) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) sT[v][i] = comp<NPR>(T2, i);
+        }
+    }
+    __syncwarp();
+    float R[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) R[i] = sT[nl - 1][i];
+#pragma unroll 1
+    for (int v = nl - 2; v >= 0; --v) {
+        unsigned long long R2[NPR];
+        float Tv[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) Tv[i] = sT[v][i];
+        pack_pairs<M, NPR>(Tv, R2);
+        mvp<M>(PQ + v * LV, (jt >> (5 * v)) & 31, R, R2);
+        unpack_pairs<M, NPR>(R2, R);
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i) X[i] = R[i];
+    __syncwarp();                                                    // sT is reused by the warp's next tile
+}
+
+// ---------------------------------------------------------------------------
+// Load the rows of one tile: row r holds samples [p0 + rL, p0 + (r+1)L) of `src` (one
+// sequence, length T); samples outside [0, T) (or src == NULL) read as 0.  Lane l fills
+// row l (rowmap 0) or 31 - l (rowmap 1).  vec: bulk row copies on the TMA engine counted
+// on `bar`; `arm`: this call arms the barrier (arm_mult x the tile's bytes: several
+// streams may complete on one barrier).  Without vec: element copies by the lanes and
+// (arm) a plain arrive.
 template <int M>
 __device__ __forceinline__ void load_rows(float* buf, unsigned long long* bar, const float* src, int64_t p0,
-                                          int64_t T, bool vec, int lane, int rowmap) {
+                                          int64_t T, bool vec, int lane, int rowmap, bool arm = true,
+                                          unsigned arm_mult = 1) {
     using C = Cfg<M>;
     constexpr int L = C::L;
-    const int r = rowmap ? 31 - lane : lane;          // any bijection: each lane fills one row
+    const int r = rowmap ? 31 - lane : lane;
     const int64_t s = p0 + (int64_t)r * L;
     float* row = buf + r * C::PITCH;
     const int64_t lo = s > 0 ? s : 0, hi = (s + L < T) ? s + L : T;
     const bool any = src != nullptr && hi > lo;
     if (vec) {
-        if (lane == 0) {
+        if (arm && lane == 0) {
             const int64_t tlo = p0 > 0 ? p0 : 0, thi = (p0 + C::TS < T) ? p0 + C::TS : T;
             const unsigned bytes = (src != nullptr && thi > tlo) ? (unsigned)((thi - tlo) * 4) : 0u;
-            mbar_arrive_expect_tx(bar, bytes);
+            mbar_arrive_expect_tx(bar, bytes * arm_mult);
         }
         __syncwarp();
         if (any) bulk_g2s(row + (lo - s), src + lo, (unsigned)((hi - lo) * 4), bar);
@@ -298,26 +401,7 @@ __device__ __forceinline__ void load_rows(float* buf, unsigned long long* bar, c
             row[e] = (src != nullptr && n >= 0 && n < T) ? src[n] : 0.f;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar);
-    }
-}
-
-// w += sum_k K[k] v(k) over one chunk row (the K-form chunk aggregate).
-template <int M>
-__device__ __forceinline__ void chunk_aggregate(const float* row, const float* K, unsigned long long (&W)[Cfg<M>::NPR]) {
-    using C = Cfg<M>;
-#pragma unroll 4
-    for (int g = 0; g < C::L / 4; ++g) {
-        const float4 v = *reinterpret_cast<const float4*>(row + 4 * g);
-        const float xs[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            unsigned long long Kp[C::NPR];
-            ld_pairs<C::NPR>(K + (4 * g + e) * C::MP, Kp);
-            const unsigned long long X = pk2(xs[e], xs[e]);
-#pragma unroll
-            for (int ip = 0; ip < C::NPR; ++ip) W[ip] = ffma2(Kp[ip], X, W[ip]);
-        }
+        if (arm && lane == 0) mbar_arrive(bar);
     }
 }
 
@@ -325,7 +409,7 @@ __device__ __forceinline__ void chunk_aggregate(const float* row, const float* K
 // exclusive prefix E (lane 0: zero) and the tile aggregate G (lane 31's inclusive).
 template <int M>
 __device__ __forceinline__ void warp_scan32(const float* P0, int lane, unsigned long long (&S)[Cfg<M>::NPR],
-                                            float (&E)[M], double (&G)[M]) {
+                                            float (&E)[M], float (&G)[M]) {
     using C = Cfg<M>;
 #pragma unroll
     for (int d = 0; d < 5; ++d) {
@@ -333,7 +417,7 @@ __device__ __forceinline__ void warp_scan32(const float* P0, int lane, unsigned 
         float O[M];
 #pragma unroll
         for (int j = 0; j < M; ++j) {
-            const float v = __shfl_up_sync(0xffffffffu, comp<M>(S, j), off);
+            const float v = __shfl_up_sync(0xffffffffu, comp<C::NPR>(S, j), off);
             O[j] = lane >= off ? v : 0.f;
         }
         const float* P = P0 + d * M * C::MP;
@@ -348,33 +432,22 @@ __device__ __forceinline__ void warp_scan32(const float* P0, int lane, unsigned 
     }
 #pragma unroll
     for (int j = 0; j < M; ++j) {
-        const float v = comp<M>(S, j);
+        const float v = comp<C::NPR>(S, j);
         const float e = __shfl_up_sync(0xffffffffu, v, 1);
         E[j] = lane == 0 ? 0.f : e;
-        G[j] = (double)__shfl_sync(0xffffffffu, v, 31);
+        G[j] = __shfl_sync(0xffffffffu, v, 31);
     }
 }
 
-// State entering this lane's chunk: E + X^(lane L) X (fp32; Q from the tables).
+// State entering this lane's chunk: E + X^(lane L) Xc (Q from the tables, through L1).
 template <int M>
-__device__ __forceinline__ void lane_carry(const float* __restrict__ Q, int lane, const float (&E)[M], const double (&X)[M],
-                                           float (&v)[M]) {
+__device__ __forceinline__ void lane_carry(const float* __restrict__ Q, int lane, const float (&E)[M],
+                                           const float (&Xc)[M], float (&v)[M]) {
     using C = Cfg<M>;
     unsigned long long S[C::NPR];
-#pragma unroll
-    for (int ip = 0; ip < C::NPR; ++ip) S[ip] = pk2(E[2 * ip], 2 * ip + 1 < M ? E[2 * ip + 1] : 0.f);
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-        const float xj = (float)X[j];
-        const unsigned long long Xj = pk2(xj, xj);
-#pragma unroll
-        for (int ip = 0; ip < C::NPR; ++ip) {
-            const float2 q = __ldg(reinterpret_cast<const float2*>(Q) + (j * C::NPR + ip) * 32 + lane);
-            S[ip] = ffma2(pk2(q.x, q.y), Xj, S[ip]);
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < M; ++j) v[j] = comp<M>(S, j);
+    pack_pairs<M, C::NPR>(E, S);
+    mvp<M>(Q, lane, Xc, S);
+    unpack_pairs<M, C::NPR>(S, v);
 }
 
 template <int M>
@@ -384,131 +457,219 @@ __device__ __forceinline__ void load_coef32(const float* tab, float (&bc)[M + 1]
     for (int k = 0; k <= M; ++k) { bc[k] = tab[C::OC + k]; ac[k] = tab[C::OC + M + 1 + k]; }
 }
 
-__device__ __forceinline__ unsigned take_ticket(unsigned* ticket, int lane) {
-    unsigned t = 0;
-    if (lane == 0) t = atomicAdd(ticket, 1u);
-    return __shfl_sync(0xffffffffu, t, 0);
+// K-form chunk aggregate of 16 samples xs[0..15] at chunk positions k0 .. k0+15.
+template <int M>
+__device__ __forceinline__ void kform16(const float* K, int k0, const float (&xs)[16],
+                                        unsigned long long (&S)[Cfg<M>::NPR]) {
+    using C = Cfg<M>;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        unsigned long long Kp[C::NPR];
+        ld_pairs<C::NPR>(K + (k0 + e) * C::MP, Kp);
+        const unsigned long long X = pk2(xs[e], xs[e]);
+#pragma unroll
+        for (int ip = 0; ip < C::NPR; ++ip) S[ip] = ffma2(Kp[ip], X, S[ip]);
+    }
 }
 
 // ---------------------------------------------------------------------------
-// Forward (a2-a4).  Per warp, a three-deep tile pipeline: while tile t0 looks back
-// and emits, tile t1's aggregate is already published and tile t2 streams in, so a
-// warp never holds a handed-out tile whose aggregate waits behind its own look-back.
+// Tensor memory (TMEM) as a parking area (sm_100a).  Warp w may access TMEM lanes
+// 32 (w % 4) .. 32 (w % 4) + 31; with the 32x32b shape thread i of the warp reads / writes
+// its own lane, 16 consecutive 32-bit columns per instruction.
+__device__ __forceinline__ void tmem_alloc(unsigned* dst, unsigned ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(smem_u32(dst)), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(unsigned taddr, unsigned ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st16(unsigned taddr, const float (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};" ::"r"(taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+        "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+        "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+        "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
+        "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(unsigned taddr, float (&v)[16]) {
+    unsigned r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Forward (a2-a4).  Per warp: one incoming shared buffer (x by TMA), one outgoing buffer
+// (y, bulk row stores) and two TMEM slots.  Iteration for tile t0 (aggregate published,
+// x parked in TMEM): aggregate + publish t1 (data arrived an iteration ago) and park it,
+// issue t2's load, look back for t0, emit t0 from TMEM.
 template <int M, int NWP, bool GT>
 __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const FwdArgs p) {
     using C = Cfg<M>;
-    constexpr int L = C::L, TS = C::TS;
+    constexpr int L = C::L, TS = C::TS, NPR = C::NPR;
+    static_assert(L % 16 == 0 && NWP <= 16 && 2 * L * ((NWP + 3) / 4) <= 512, "TMEM slots");
     extern __shared__ __align__(128) float sm2[];
-    __shared__ __align__(8) unsigned long long s_bar[NWP][C::NBUF];
-    __shared__ double s_T[NWP][LEVELS][M];
+    __shared__ __align__(8) unsigned long long s_bar[NWP];
+    __shared__ float s_T[NWP][LEVELS][M];
+    __shared__ unsigned s_tmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* bA = sm2 + (GT ? 0 : C::STAGE) + warp * C::NBUF * C::BUF;
-    float* bB = bA + C::BUF;
-    float* bC = bB + C::BUF;
-    unsigned long long* rA = &s_bar[warp][0];
-    unsigned long long* rB = &s_bar[warp][1];
-    unsigned long long* rC = &s_bar[warp][2];
-    unsigned pA = 0, pB = 0, pC = 0;
-    if (lane == 0) { mbar_init(rA, 1); mbar_init(rB, 1); mbar_init(rC, 1); }
+    float* bX = sm2 + (GT ? 0 : C::STAGE) + warp * 2 * C::BUF;
+    float* bY = bX + C::BUF;
+    unsigned long long* bar = &s_bar[warp];
+    unsigned ph = 0;
+    if (lane == 0) mbar_init(bar, 1);
     mbar_fence_init();
     __syncwarp();
-    // The kernel before this one on the stream is always this call's prologue, which
-    // is launched WITHOUT programmatic serialization: everything enqueued before it
-    // (the caller's x, the previous call's use of the workspace) completed before it
-    // started.  So the workspace counters and the first x tiles are read before
-    // griddepcontrol.wait; only the prologue's tables are read after it.
+    if (warp == 0) tmem_alloc(&s_tmem, 512);
+    // The kernel before this one on the stream is always this call's prologue, launched
+    // WITHOUT programmatic serialization: everything enqueued before it (the caller's x,
+    // the previous call's use of the workspace) completed before it started.  So the
+    // workspace and the first x tile are read before griddepcontrol.wait; only the
+    // prologue's tables are read after it.
     CarryWs cw = p.cw;
     const unsigned ep = carry_bank(cw);
     rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
     const bool vec = p.vec != 0;
-    auto issue = [&](float* buf, unsigned long long* bar, unsigned t) {
-        load_rows<M>(buf, bar, p.x + (int64_t)(t % (unsigned long long)p.B) * p.T,
-                     (int64_t)(t / (unsigned long long)p.B) * TS, p.T, vec, lane, 0);
+    Sched s0, s1;
+    s0.init(blockIdx.x * NWP + warp, gridDim.x * NWP, p.B);
+    s1 = s0;
+    s1.next();
+    auto issue = [&](const Sched& s) {
+        load_rows<M>(bX, bar, p.x + s.seq * p.T, (int64_t)s.j * TS, p.T, vec, lane, 0);
     };
-    unsigned t0 = take_ticket(cw.ticket, lane);
-    unsigned t1 = take_ticket(cw.ticket, lane);
-    unsigned t2 = take_ticket(cw.ticket, lane);
-    if (t0 < p.ntot) issue(bA, rA, t0);
-    if (t1 < p.ntot) issue(bB, rB, t1);
-    pdl_wait();                                                  // the prologue's tables
+    if (s0.t < p.ntot) issue(s0);
+    pdl_wait();
     pdl_launch_dependents();
     if constexpr (!GT) {
         for (int i = threadIdx.x; i < C::STAGE / 4; i += blockDim.x) cp_async16_ca(sm2 + 4 * i, p.t32 + 4 * i);
         cp_async_commit();
         cp_async_wait<0>();
     }
+    tmem_fence_before();
     __syncthreads();
-    // a2 + a3 (intra-warp) of tile t in buf, then its publication: E, G for the look-back
-    auto aggregate = [&](float* buf, unsigned long long* bar, unsigned& ph, unsigned t, float (&E)[M]) {
-        const int64_t seq = (int64_t)(t % (unsigned long long)p.B);
-        const int jt = (int)(t / (unsigned long long)p.B);
-        const float* tab = GT ? p.t32 + seq * p.t32_stride : sm2;
-        double G[M];
-        V2_TRACE(p.trace, t, 0);
+    tmem_fence_after();
+    const unsigned tbase = s_tmem + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)((warp >> 2) * 2 * L);
+    auto aggregate = [&](const Sched& s, unsigned slot, float (&E)[M]) {
+        const float* tab = GT ? p.t32 + s.seq * p.t32_stride : sm2;
+        V2_TRACE(p.trace, s.t, 0);
         mbar_wait(bar, ph);
         ph ^= 1u;
-        V2_TRACE(p.trace, t, 1);
-        unsigned long long S[C::NPR];
+        V2_TRACE(p.trace, s.t, 1);
+        const float* row = bX + lane * C::PITCH;
+        unsigned long long S[NPR];
 #pragma unroll
-        for (int ip = 0; ip < C::NPR; ++ip) S[ip] = 0ull;
-        chunk_aggregate<M>(buf + lane * C::PITCH, tab + C::OK_, S);
+        for (int ip = 0; ip < NPR; ++ip) S[ip] = 0ull;
+#pragma unroll 1
+        for (int g = 0; g < L / 16; ++g) {
+            float xs[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 v = *reinterpret_cast<const float4*>(row + 16 * g + 4 * q);
+                xs[4 * q] = v.x; xs[4 * q + 1] = v.y; xs[4 * q + 2] = v.z; xs[4 * q + 3] = v.w;
+            }
+            tmem_st16(slot + 16 * g, xs);
+            kform16<M>(tab + C::OK_, 16 * g, xs, S);
+        }
+        float G[M];
         warp_scan32<M>(tab + C::OP, lane, S, E, G);
-        double X0[M];
+        float X0[M];
 #pragma unroll
-        for (int i = 0; i < M; ++i) X0[i] = (p.zi != nullptr && jt == 0) ? (double)p.zi[seq * M + i] : 0.0;
-        warp_publish<M, false>(p.t64 + seq * p.t64_stride, lane, jt, seq, X0, G, cw);
-        warp_close<M, false>(p.t64 + seq * p.t64_stride, lane, jt, seq, G, cw);
-        V2_TRACE(p.trace, t, 2);
+        for (int i = 0; i < M; ++i) X0[i] = 0.f;
+        if (s.j == 0 && p.zi != nullptr)
+#pragma unroll
+            for (int i = 0; i < M; ++i) X0[i] = p.zi[s.seq * M + i];
+        carry_publish<M>(p.t32 + s.seq * p.t32_stride + C::OPQ, lane, s.j, s.seq, X0, G, cw);
+        V2_TRACE(p.trace, s.t, 2);
     };
     float E0[M];
-    if (t0 < p.ntot) aggregate(bA, rA, pA, t0, E0);
-    while (t0 < p.ntot) {
-        unsigned t3 = 0;
-        if (lane == 0) t3 = atomicAdd(cw.ticket, 1u);             // three tiles ahead, in flight
+    unsigned sl = 0;                                             // TMEM slot of t0 (0 / 1)
+    if (s0.t < p.ntot) {
+        aggregate(s0, tbase, E0);
+        if (s1.t < p.ntot) { __syncwarp(); fence_proxy_async(); issue(s1); }
+    }
+    while (s0.t < p.ntot) {
+        Sched s2 = s1;
+        s2.next();
         float E1[M];
-        if (t1 < p.ntot) aggregate(bB, rB, pB, t1, E1);
-        if (t2 < p.ntot) {
-            bulk_wait_read0();                                   // this lane's store from bC has read it
-            issue(bC, rC, t2);
+        if (s1.t < p.ntot) {
+            aggregate(s1, tbase + (sl ^ 1u) * L, E1);
+            if (s2.t < p.ntot) { __syncwarp(); fence_proxy_async(); issue(s2); }
         }
-        const int64_t seq = (int64_t)(t0 % (unsigned long long)p.B);
-        const int jt = (int)(t0 / (unsigned long long)p.B);
+        const int64_t seq = s0.seq;
+        const int jt = s0.j;
         const int64_t p0 = (int64_t)jt * TS;
         const float* tab = GT ? p.t32 + seq * p.t32_stride : sm2;
-        float* row = bA + lane * C::PITCH;
-        // a3: cross-tile carry, then the state entering this lane's chunk
-        double X0[M], X[M];
+        const float* t32s = p.t32 + seq * p.t32_stride;
+        const unsigned slot = tbase + sl * L;
+        float X0[M], X[M];
 #pragma unroll
-        for (int i = 0; i < M; ++i) X0[i] = (p.zi != nullptr && jt == 0) ? (double)p.zi[seq * M + i] : 0.0;
-        V2_TRACE(p.trace, t0, 3);
-        warp_lookback<M, false>(p.t64 + seq * p.t64_stride, lane, jt, seq, X0, cw, s_T[warp], X);
-        V2_TRACE(p.trace, t0, 4);
+        for (int i = 0; i < M; ++i) X0[i] = 0.f;
+        if (jt == 0 && p.zi != nullptr)
+#pragma unroll
+            for (int i = 0; i < M; ++i) X0[i] = p.zi[seq * M + i];
+        V2_TRACE(p.trace, s0.t, 3);
+        carry_lookback<M>(t32s + C::OPQ, lane, jt, seq, X0, cw, s_T[warp], X);
+        V2_TRACE(p.trace, s0.t, 4);
         float vin[M];
-        lane_carry<M>(p.t32 + seq * p.t32_stride + C::OQ, lane, E0, X, vin);
+        lane_carry<M>(t32s + C::OQ, lane, E0, X, vin);
         float bc[M + 1], ac[M + 1];
         load_coef32<M>(tab, bc, ac);
-        // zf = v(T): the lane holding sample T-1 (when it is not its chunk's last)
+        tmem_wait_st();                                          // t0's parking (an iteration ago) is complete
+        // zf = v(T): the lane holding sample T-1 walks from its carry-in (warp-uniform branch)
         const int64_t ez = p.T - 1 - (p0 + (int64_t)lane * L);
-        if (p.zf != nullptr && ez >= 0 && ez < L - 1) {
+        const bool zwalk = p.zf != nullptr && ez >= 0 && ez < L - 1;
+        if (__any_sync(0xffffffffu, zwalk)) {
             float w2[M];
 #pragma unroll
             for (int i = 0; i < M; ++i) w2[i] = vin[i];
-            for (int n = 0; n <= (int)ez; ++n) { float du; fwd_step<float, M, 1>(w2, row[n], bc, ac, du); }
+#pragma unroll 1
+            for (int g = 0; g < L / 16; ++g) {
+                float xs[16];
+                tmem_ld16(slot + 16 * g, xs);
+                tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < M; ++i) p.zf[seq * M + i] = w2[i];
+                for (int e = 0; e < 16; ++e)
+                    if (zwalk && 16 * g + e <= ez) { float du; fwd_step<float, M, 1>(w2, xs[e], bc, ac, du); }
+            }
+            if (zwalk)
+#pragma unroll
+                for (int i = 0; i < M; ++i) p.zf[seq * M + i] = w2[i];
         }
-        // a4: re-run from the exact carry-in, y in place (paired FMAs)
+        // a4: re-run from the exact carry-in, x from TMEM, y into the outgoing buffer
+        bulk_wait_read0();                                       // the previous store from bY has read it
+        float* yr = bY + lane * C::PITCH;
         {
             Tdf2<M> c2;
             c2.init(bc, ac);
             unsigned long long VP[Tdf2<M>::NP];
             tdf2_pack<M>(vin, VP);
-#pragma unroll 4
-            for (int g = 0; g < L / 4; ++g) {
-                float4 xv = *reinterpret_cast<const float4*>(row + 4 * g);
-                tdf2_step<M>(VP, xv.x, xv.y, c2, xv.x, xv.y);
-                tdf2_step<M>(VP, xv.z, xv.w, c2, xv.z, xv.w);
-                *reinterpret_cast<float4*>(row + 4 * g) = xv;
+            float xs[16];
+            tmem_ld16(slot, xs);
+#pragma unroll 1
+            for (int g = 0; g < L / 16; ++g) {
+                tmem_wait_ld();
+                float ys[16];
+#pragma unroll
+                for (int e = 0; e < 16; e += 2) tdf2_step<M>(VP, xs[e], xs[e + 1], c2, ys[e], ys[e + 1]);
+                if (g + 1 < L / 16) tmem_ld16(slot + 16 * (g + 1), xs);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    *reinterpret_cast<float4*>(yr + 16 * g + 4 * q) =
+                        make_float4(ys[4 * q], ys[4 * q + 1], ys[4 * q + 2], ys[4 * q + 3]);
             }
             if (p.zf != nullptr && ez == L - 1) {
                 float v[M];
@@ -517,8 +678,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const FwdArgs p) 
                 for (int i = 0; i < M; ++i) p.zf[seq * M + i] = v[i];
             }
         }
-        V2_TRACE(p.trace, t0, 5);
-        // store this lane's row of y
+        V2_TRACE(p.trace, s0.t, 5);
         {
             const int64_t s = p0 + (int64_t)lane * L;
             const int64_t lo = s > 0 ? s : 0, hi = (s + L < p.T) ? s + L : p.T;
@@ -526,34 +686,34 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const FwdArgs p) 
             if (hi > lo) {
                 if (vec) {
                     fence_proxy_async();
-                    bulk_s2g(yrow + lo, row + (lo - s), (unsigned)((hi - lo) * 4));
+                    bulk_s2g(yrow + lo, yr + (lo - s), (unsigned)((hi - lo) * 4));
                     bulk_commit();
                 } else {
-                    for (int64_t n = lo; n < hi; ++n) yrow[n] = row[n - s];
+                    for (int64_t n = lo; n < hi; ++n) yrow[n] = yr[n - s];
                 }
             }
         }
-        V2_TRACE(p.trace, t0, 6);
-        if (p.trace != nullptr && lane == 0) p.trace[(size_t)t0 * 8 + 7] = blockIdx.x * NWP + warp;
-        // rotate the pipeline
-        t0 = t1; t1 = t2; t2 = __shfl_sync(0xffffffffu, t3, 0);
+        V2_TRACE(p.trace, s0.t, 6);
+        if (p.trace != nullptr && lane == 0) p.trace[(size_t)s0.t * 8 + 7] = blockIdx.x * NWP + warp;
+        s0 = s1;
+        s1 = s2;
 #pragma unroll
         for (int i = 0; i < M; ++i) E0[i] = E1[i];
-        float* tb_ = bA; bA = bB; bB = bC; bC = tb_;
-        unsigned long long* tr_ = rA; rA = rB; rB = rC; rC = tr_;
-        const unsigned tp_ = pA; pA = pB; pB = pC; pC = tp_;
+        sl ^= 1u;
     }
     bulk_wait0();
+    tmem_fence_before();
     cta_exit(cw, ep, gridDim.x);
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(s_tmem, 512);
 }
 
 // ---------------------------------------------------------------------------
-// Backward (a5-a8).  Tiles are aligned to the END of each sequence and taken last to
-// first; lane l owns chunk 31 - l of its tile (so the lane order is the scan order).
-template <int M>
-__device__ __forceinline__ int tidx(int e) {              // tile-local sample -> shared offset
-    return (e / Cfg<M>::L) * Cfg<M>::PITCH + (e % Cfg<M>::L);
-}
+// Backward (a5-a8).  Tiles are aligned to the END of each sequence and scanned last to
+// first; lane l owns chunk 31 - l of its tile (the lane order is the scan order).  Per
+// warp: shared buffers dy (incoming), x (-> dx in place, bulk stores) and y, and two TMEM
+// slots for the parked dy.  Iteration for tile t0: x, y of t0 go out by TMA, aggregate +
+// publish t1 (dy parked), issue dy of t2, look back for t0, then one fused pass per lane.
 
 // Fixed-order fp64 sum of `nrows` rows of NG values (row-major, stride NG): lane l sums
 // rows l, l+32, ... in increasing order, then a fixed xor butterfly; all lanes return all sums.
@@ -604,38 +764,28 @@ __device__ __forceinline__ void chain_rule2(const double (&G)[2 * M + 1], const 
     }
 }
 
-template <int M>
-__device__ __forceinline__ float4 ld_masked4(const float* row, int64_t pos, bool vec) {
-    if (row == nullptr || pos + 4 <= 0) return make_float4(0.f, 0.f, 0.f, 0.f);
-    if (vec && pos >= 0) return ldg_l2(reinterpret_cast<const float4*>(row + pos));
-    float4 r;
-    r.x = pos + 0 >= 0 ? row[pos + 0] : 0.f;
-    r.y = pos + 1 >= 0 ? row[pos + 1] : 0.f;
-    r.z = pos + 2 >= 0 ? row[pos + 2] : 0.f;
-    r.w = pos + 3 >= 0 ? row[pos + 3] : 0.f;
-    return r;
-}
-
 template <int M, int NWP, bool GT>
 __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) {
     using C = Cfg<M>;
-    constexpr int L = C::L, TS = C::TS, NG = C::NG;
+    constexpr int L = C::L, TS = C::TS, NG = C::NG, NPR = C::NPR;
+    static_assert(L % 16 == 0 && NWP <= 16 && 2 * L * ((NWP + 3) / 4) <= 512, "TMEM slots");
     extern __shared__ __align__(128) float sm2[];
-    __shared__ __align__(8) unsigned long long s_bar[NWP][C::NBUF];
-    __shared__ double s_T[NWP][LEVELS][M];
+    __shared__ __align__(8) unsigned long long s_bar[NWP][2];
+    __shared__ float s_T[NWP][LEVELS][M];
+    __shared__ unsigned s_tmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* bA = sm2 + (GT ? 0 : C::STAGE) + warp * C::NBUF * C::BUF;
-    float* bB = bA + C::BUF;
-    float* bC = bB + C::BUF;
-    unsigned long long* rA = &s_bar[warp][0];
-    unsigned long long* rB = &s_bar[warp][1];
-    unsigned long long* rC = &s_bar[warp][2];
-    unsigned pA = 0, pB = 0, pC = 0;
-    if (lane == 0) { mbar_init(rA, 1); mbar_init(rB, 1); mbar_init(rC, 1); }
+    float* bI = sm2 + (GT ? 0 : C::STAGE) + warp * 3 * C::BUF;    // dy (incoming)
+    float* bX = bI + C::BUF;                                      // x -> dx in place
+    float* bY = bX + C::BUF;                                      // y, then partial-sum scratch
+    unsigned long long* barI = &s_bar[warp][0];
+    unsigned long long* barXY = &s_bar[warp][1];
+    unsigned phI = 0, phXY = 0;
+    if (lane == 0) { mbar_init(barI, 1); mbar_init(barXY, 1); }
     mbar_fence_init();
     __syncwarp();
+    if (warp == 0) tmem_alloc(&s_tmem, 512);
     // grad_y may be written by the kernel right before this one (the caller's loss):
-    // nothing is read before griddepcontrol.wait.
+    // nothing the previous kernels wrote is read before griddepcontrol.wait.
     pdl_wait();
     pdl_launch_dependents();
     CarryWs cw = p.cw;
@@ -646,173 +796,217 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
         cp_async_commit();
     }
     rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
+    if constexpr (!GT) cp_async_wait<0>();
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const unsigned tbase = s_tmem + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)((warp >> 2) * 2 * L);
     const bool vec = p.vec != 0;
     const bool shared_set = p.ncoef == 1;
-    auto issue = [&](float* buf, unsigned long long* bar, unsigned t) {
-        const int64_t seq = (int64_t)(t % (unsigned long long)p.B);
-        const int64_t p0 = p.T - (int64_t)(t / (unsigned long long)p.B + 1) * TS;
-        const int64_t off = seq * p.T;
-        load_rows<M>(buf, bar, p.gy == nullptr ? nullptr : p.gy + off, p0, p.T, vec, lane, 1);
-        if (lane == 0 && vec) {                  // x, y are read by pass B: pull them into L2 now
-            const int64_t lo = p0 > 0 ? p0 : 0;
-            const unsigned bytes = (unsigned)((p0 + TS - lo) * 4);
-            prefetch_l2_bulk(p.x + off + lo, bytes);
-            prefetch_l2_bulk(p.y + off + lo, bytes);
-        }
+    Sched s0, s1;
+    s0.init(blockIdx.x * NWP + warp, gridDim.x * NWP, p.B);
+    s1 = s0;
+    s1.next();
+    auto p0_of = [&](const Sched& s) -> int64_t { return p.T - (int64_t)(s.j + 1) * TS; };
+    auto issue_dy = [&](const Sched& s) {
+        load_rows<M>(bI, barI, p.gy == nullptr ? nullptr : p.gy + s.seq * p.T, p0_of(s), p.T, vec, lane, 1);
     };
-    unsigned t0 = take_ticket(cw.ticket, lane);
-    unsigned t1 = take_ticket(cw.ticket, lane);
-    unsigned t2 = take_ticket(cw.ticket, lane);
-    if (t0 < p.ntot) issue(bA, rA, t0);
-    if (t1 < p.ntot) issue(bB, rB, t1);
-    if constexpr (!GT) cp_async_wait<0>();
-    __syncthreads();
-    // a5 + a6 (intra-warp) of tile t, then its publication (grad_zf folded into the last tile)
-    auto aggregate = [&](float* buf, unsigned long long* bar, unsigned& ph, unsigned t, float (&E)[M]) {
-        const int64_t seq = (int64_t)(t % (unsigned long long)p.B);
-        const int jr = (int)(t / (unsigned long long)p.B);
-        const float* tab = GT ? p.t32 + seq * p.t32_stride + C::DIR : sm2;
-        double G[M];
-        V2_TRACE(p.trace, t, 0);
-        mbar_wait(bar, ph);
-        ph ^= 1u;
-        V2_TRACE(p.trace, t, 1);
-        unsigned long long S[C::NPR];
+    auto issue_xy = [&](const Sched& s) {
+        const int64_t off = s.seq * p.T;
+        load_rows<M>(bX, barXY, p.x + off, p0_of(s), p.T, vec, lane, 1, true, 2);
+        load_rows<M>(bY, barXY, p.y + off, p0_of(s), p.T, vec, lane, 1, false);
+    };
+    // a5 + a6 (intra-warp) of tile t: dy rows -> TMEM slot, K-form aggregate, scan, publication
+    auto aggregate = [&](const Sched& s, unsigned slot, float (&E)[M]) {
+        const float* tab = GT ? p.t32 + s.seq * p.t32_stride + C::DIR : sm2;
+        V2_TRACE(p.trace, s.t, 0);
+        mbar_wait(barI, phI);
+        phI ^= 1u;
+        V2_TRACE(p.trace, s.t, 1);
+        const float* row = bI + (31 - lane) * C::PITCH;
+        unsigned long long S[NPR];
 #pragma unroll
-        for (int ip = 0; ip < C::NPR; ++ip) S[ip] = 0ull;
-        chunk_aggregate<M>(buf + (31 - lane) * C::PITCH, tab + C::OK_, S);
+        for (int ip = 0; ip < NPR; ++ip) S[ip] = 0ull;
+#pragma unroll 1
+        for (int g = 0; g < L / 16; ++g) {
+            float xs[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 v = *reinterpret_cast<const float4*>(row + 16 * g + 4 * q);
+                xs[4 * q] = v.x; xs[4 * q + 1] = v.y; xs[4 * q + 2] = v.z; xs[4 * q + 3] = v.w;
+            }
+            tmem_st16(slot + 16 * g, xs);
+            kform16<M>(tab + C::OK_, 16 * g, xs, S);
+        }
+        float G[M];
         warp_scan32<M>(tab + C::OP, lane, S, E, G);
-        double X0[M];
+        float X0[M];
 #pragma unroll
-        for (int i = 0; i < M; ++i) X0[i] = (p.gzf != nullptr && jr == 0) ? (double)p.gzf[seq * M + i] : 0.0;
-        warp_publish<M, true>(p.t64 + seq * p.t64_stride, lane, jr, seq, X0, G, cw);
-        warp_close<M, true>(p.t64 + seq * p.t64_stride, lane, jr, seq, G, cw);
-        V2_TRACE(p.trace, t, 2);
+        for (int i = 0; i < M; ++i) X0[i] = 0.f;
+        if (s.j == 0 && p.gzf != nullptr)
+#pragma unroll
+            for (int i = 0; i < M; ++i) X0[i] = p.gzf[s.seq * M + i];
+        carry_publish<M>(p.t32 + s.seq * p.t32_stride + C::DIR + C::OPQ, lane, s.j, s.seq, X0, G, cw);
+        V2_TRACE(p.trace, s.t, 2);
     };
     float E0[M];
-    if (t0 < p.ntot) aggregate(bA, rA, pA, t0, E0);
-    while (t0 < p.ntot) {
-        unsigned t3 = 0;
-        if (lane == 0) t3 = atomicAdd(cw.ticket, 1u);
-        float E1[M];
-        if (t1 < p.ntot) aggregate(bB, rB, pB, t1, E1);
-        if (t2 < p.ntot) {
-            fence_proxy_async();                                 // bC's generic reads / writes before the TMA writes
-            issue(bC, rC, t2);
-        }
-        const int64_t seq = (int64_t)(t0 % (unsigned long long)p.B);
-        const int jr = (int)(t0 / (unsigned long long)p.B);      // 0 = last tile in time
-        const int jt = p.ntiles - 1 - jr;
-        (void)jt;
-        const int64_t p0 = p.T - (int64_t)(jr + 1) * TS;          // may be < 0 (first tile in time)
-        const float* tab = GT ? p.t32 + seq * p.t32_stride + C::DIR : sm2;
-        const double* t64 = p.t64 + seq * p.t64_stride;
-        float* row = bA + (31 - lane) * C::PITCH;
-        // a6: cross-tile carry (transposed powers), seeded by grad_zf at the last tile
-        double X0[M], X[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) X0[i] = (p.gzf != nullptr && jr == 0) ? (double)p.gzf[seq * M + i] : 0.0;
-        V2_TRACE(p.trace, t0, 3);
-        warp_lookback<M, true>(t64, lane, jr, seq, X0, cw, s_T[warp], X);
-        V2_TRACE(p.trace, t0, 4);
-        float din[M];
-        lane_carry<M>(p.t32 + seq * p.t32_stride + C::DIR + C::OQ, lane, E0, X, din);     // [g(e) .. g(e+M-1)], e = this chunk's right end
-        float bc[M + 1], ac[M + 1];
-        load_coef32<M>(tab, bc, ac);
-        {
-            float hv = 0.f;
-#pragma unroll
-            for (int i = 0; i < M; ++i)
-                if (lane == i) hv = (float)X[i];
-            if (lane < 16) bA[32 * C::PITCH + lane] = hv;           // g(p0 + TS + i) = the tile's right carry
-        }
-        // a7 pass A: g(n) = dy(n) - sum_k a_k g(n+k), walking the chunk backwards; g over dy
-        {
-            float g[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) g[i] = din[i];
-#pragma unroll 4
-            for (int q = L / 4 - 1; q >= 0; --q) {
-                float4 v = *reinterpret_cast<const float4*>(row + 4 * q);
-                float vs[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                for (int e = 3; e >= 0; --e) {
-                    float acc = vs[e];
-#pragma unroll
-                    for (int k = M; k >= 2; --k) acc = fmaf(-ac[k], g[k - 1], acc);
-                    const float gn = fmaf(-ac[1], g[0], acc);
-#pragma unroll
-                    for (int k = M - 1; k >= 1; --k) g[k] = g[k - 1];
-                    g[0] = gn;
-                    vs[e] = gn;
-                }
-                *reinterpret_cast<float4*>(row + 4 * q) = make_float4(vs[0], vs[1], vs[2], vs[3]);
-            }
-        }
+    unsigned sl = 0;
+    if (s0.t < p.ntot) {
+        issue_dy(s0);
+        aggregate(s0, tbase, E0);
+        if (s1.t < p.ntot) { __syncwarp(); fence_proxy_async(); issue_dy(s1); }
+    }
+    while (s0.t < p.ntot) {
+        Sched s2 = s1;
+        s2.next();
+        bulk_wait_read0();                                       // this lane's dx store has read bX
         __syncwarp();
-        auto gptr = [&](int e) -> const float* { return bA + tidx<M>(e); };   // row 32: the halo
-        // grad_zi = d(0) = [g(0) .. g(M-1)] (Eq.9, App. A.3), read back from the tile
-        if (p.gzi != nullptr && p0 <= 0 && lane < M) p.gzi[seq * M + lane] = *gptr((int)(-p0) + lane);
-        // a7 pass B: dx(n) = sum_k b'_k g(n+k) and the correlation sums, lanes interleaved
-        float bk[M + 1];
+        fence_proxy_async();                                     // bX / bY generic accesses before the TMA writes
+        issue_xy(s0);
+        float E1[M];
+        if (s1.t < p.ntot) {
+            aggregate(s1, tbase + (sl ^ 1u) * L, E1);
+            if (s2.t < p.ntot) { __syncwarp(); fence_proxy_async(); issue_dy(s2); }
+        }
+        const int64_t seq = s0.seq;
+        const int jr = s0.j;                                     // 0 = last tile in time
+        const int64_t p0 = p0_of(s0);                            // may be < 0 (first tile in time)
+        const float* tab = GT ? p.t32 + seq * p.t32_stride + C::DIR : sm2;
+        const float* t32s = p.t32 + seq * p.t32_stride + C::DIR;
+        const double* t64 = p.t64 + seq * p.t64_stride;
+        const unsigned slot = tbase + sl * L;
+        const int c = 31 - lane;                                 // this lane's chunk (time order)
+        const int64_t s = p0 + (int64_t)c * L;
+        // a6: cross-tile carry (transposed powers), seeded by grad_zf at the last tile
+        float X0[M], X[M];
 #pragma unroll
-        for (int k = 0; k <= M; ++k) bk[k] = bc[k];
-        unsigned long long CD[M];                                // (C_k, D_k), k = 1..M
+        for (int i = 0; i < M; ++i) X0[i] = 0.f;
+        if (jr == 0 && p.gzf != nullptr)
+#pragma unroll
+            for (int i = 0; i < M; ++i) X0[i] = p.gzf[seq * M + i];
+        V2_TRACE(p.trace, s0.t, 3);
+        carry_lookback<M>(t32s + C::OPQ, lane, jr, seq, X0, cw, s_T[warp], X);
+        V2_TRACE(p.trace, s0.t, 4);
+        float din[M];
+        lane_carry<M>(t32s + C::OQ, lane, E0, X, din);           // [g(e) .. g(e+M-1)], e = this chunk's right end
+        float bk[M + 1], na[M + 1];
+        load_coef32<M>(tab, bk, na);
+#pragma unroll
+        for (int k = 0; k <= M; ++k) na[k] = -na[k];
+        mbar_wait(barXY, phXY);
+        phXY ^= 1u;
+        tmem_wait_st();
+        // grad_zi of a first tile that starts before n = 0: the lane whose chunk straddles
+        // n = 0 walks down to it (warp-uniform branch; dy from TMEM)
+        const bool zlane = p.gzi != nullptr && s < 0 && s + L > 0;
+        if (__any_sync(0xffffffffu, zlane)) {
+            float w2[M + 1];                                     // shifted once before each step
+#pragma unroll
+            for (int k = 0; k < M; ++k) w2[k] = din[k];
+            w2[M] = 0.f;
+#pragma unroll 1
+            for (int g = L / 16 - 1; g >= 0; --g) {
+                float ds[16];
+                tmem_ld16(slot + 16 * g, ds);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 15; e >= 0; --e) {
+                    if (zlane && s + 16 * g + e >= 0) {
+#pragma unroll
+                        for (int k = M; k >= 1; --k) w2[k] = w2[k - 1];
+                        float acc = ds[e];
+#pragma unroll
+                        for (int k = M; k >= 2; --k) acc = fmaf(na[k], w2[k], acc);
+                        w2[0] = fmaf(na[1], w2[1], acc);
+                    }
+                }
+            }
+            if (zlane)
+#pragma unroll
+                for (int i = 0; i < M; ++i) p.gzi[seq * M + i] = w2[i];
+        }
+        // a7: one fused pass per lane, backwards in time: g(n) (Eq.7), dx(n) = sum_k b'_k g(n+k)
+        // over dx in place of x, and the correlation sums C_k = sum g(n+k) x(n), D_k = sum g(n+k) y(n)
+        float w[M + 1];                                          // w[k] = g(n + k) after step n
+#pragma unroll
+        for (int k = 0; k < M; ++k) w[k] = din[k];               // (each step first shifts by one)
+        w[M] = 0.f;
+        unsigned long long CD[M];
 #pragma unroll
         for (int i = 0; i < M; ++i) CD[i] = 0ull;
         float C0 = 0.f;
-        const int64_t off = seq * p.T;
-        const float* xrow = p.x + off;
-        const float* yrow = p.y + off;
-        float* gxrow = p.gx == nullptr ? nullptr : p.gx + off;
-#pragma unroll 2
-        for (int k = 0; k < TS / 128; ++k) {
-            const int n0 = 4 * (lane + 32 * k);
-            const int64_t pos = p0 + n0;
-            const float4 xv = ld_masked4<M>(xrow, pos, vec);
-            const float4 yv = ld_masked4<M>(yrow, pos, vec);
-            float gw[12];
+        float* xr = bX + c * C::PITCH;
+        const float* yr = bY + c * C::PITCH;
+        {
+            float ds[16];
+            tmem_ld16(slot + 16 * (L / 16 - 1), ds);
+#pragma unroll 1
+            for (int g = L / 16 - 1; g >= 0; --g) {
+                tmem_wait_ld();
+                float dcur[16];
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                const float4 t = *reinterpret_cast<const float4*>(gptr(n0 + 4 * q));
-                gw[4 * q] = t.x; gw[4 * q + 1] = t.y; gw[4 * q + 2] = t.z; gw[4 * q + 3] = t.w;
-            }
-            const float xs[4] = {xv.x, xv.y, xv.z, xv.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w};
-            float dx[4];
+                for (int e = 0; e < 16; ++e) dcur[e] = ds[e];
+                if (g > 0) tmem_ld16(slot + 16 * (g - 1), ds);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                float d = bk[0] * gw[e];
+                for (int q = 3; q >= 0; --q) {
+                    const float4 xv = *reinterpret_cast<const float4*>(xr + 16 * g + 4 * q);
+                    const float4 yv = *reinterpret_cast<const float4*>(yr + 16 * g + 4 * q);
+                    const float xs[4] = {xv.x, xv.y, xv.z, xv.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w};
+                    float dxs[4];
 #pragma unroll
-                for (int k2 = 1; k2 <= M; ++k2) d = fmaf(bk[k2], gw[e + k2], d);
-                dx[e] = d;
-                C0 = fmaf(gw[e], xs[e], C0);
-                const unsigned long long XY = pk2(xs[e], ys[e]);
+                    for (int e = 3; e >= 0; --e) {
 #pragma unroll
-                for (int i = 0; i < M; ++i) CD[i] = ffma2(pk2(gw[e + 1 + i], gw[e + 1 + i]), XY, CD[i]);
-            }
-            if (gxrow != nullptr) {
-                if (vec && pos >= 0) stg_stream(reinterpret_cast<float4*>(gxrow + pos), make_float4(dx[0], dx[1], dx[2], dx[3]));
-                else
+                        for (int k = M; k >= 1; --k) w[k] = w[k - 1];
+                        float acc = dcur[4 * q + e];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if (pos + e >= 0) gxrow[pos + e] = dx[e];
+                        for (int k = M; k >= 2; --k) acc = fmaf(na[k], w[k], acc);
+                        w[0] = fmaf(na[1], w[1], acc);
+                        float d = bk[0] * w[0];
+#pragma unroll
+                        for (int k = 1; k <= M; ++k) d = fmaf(bk[k], w[k], d);
+                        dxs[e] = d;
+                        C0 = fmaf(w[0], xs[e], C0);
+                        const unsigned long long XY = pk2(xs[e], ys[e]);
+#pragma unroll
+                        for (int k = 1; k <= M; ++k) CD[k - 1] = ffma2(pk2(w[k], w[k]), XY, CD[k - 1]);
+                    }
+                    *reinterpret_cast<float4*>(xr + 16 * g + 4 * q) = make_float4(dxs[0], dxs[1], dxs[2], dxs[3]);
+                }
             }
         }
-        V2_TRACE(p.trace, t0, 5);
+        // grad_zi = d(0) = [g(0) .. g(M-1)] (Eq.9, App. A.3) when this chunk starts at n = 0
+        if (p.gzi != nullptr && s == 0)
+#pragma unroll
+            for (int i = 0; i < M; ++i) p.gzi[seq * M + i] = w[i];
+        V2_TRACE(p.trace, s0.t, 5);
+        // dx rows out
+        if (p.gx != nullptr) {
+            const int64_t lo = s > 0 ? s : 0, hi = (s + L < p.T) ? s + L : p.T;
+            float* gxrow = p.gx + seq * p.T;
+            if (hi > lo) {
+                if (vec) {
+                    fence_proxy_async();
+                    bulk_s2g(gxrow + lo, xr + (lo - s), (unsigned)((hi - lo) * 4));
+                    bulk_commit();
+                } else {
+                    for (int64_t n = lo; n < hi; ++n) gxrow[n] = xr[n - s];
+                }
+            }
+        }
         // a8: per-tile row of the coefficient partial sums (fixed order), group / set finalize
         if (p.want_coef) {
             __syncwarp();
-            float* scr = bA + lane * C::PITCH;                    // bA is free now: lane rows as scratch
+            float* scr = bY + lane * C::PITCH;                    // y has been consumed: lane rows as scratch
             scr[0] = C0;
 #pragma unroll
             for (int i = 0; i < M; ++i) { scr[1 + i] = lo2(CD[i]); scr[M + 1 + i] = hi2(CD[i]); }
             __syncwarp();
             double colsum = 0.0;
             if (lane < NG)
-                for (int r = 0; r < 32; ++r) colsum += (double)bA[r * C::PITCH + lane];
+                for (int r = 0; r < 32; ++r) colsum += (double)bY[r * C::PITCH + lane];
             const int64_t per_set = shared_set ? p.ntot : p.ntiles;
             const int64_t cset = shared_set ? 0 : seq;
-            const int64_t li = shared_set ? (int64_t)t0 : jr;
+            const int64_t li = shared_set ? (int64_t)s0.t : jr;
             double* part = p.partial + cset * per_set * NG;
             const bool flat = per_set <= FLAT_ROWS;
             const int64_t ngroups = (per_set + 31) >> 5;
@@ -855,18 +1049,20 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
                 }
             }
         }
-        V2_TRACE(p.trace, t0, 6);
-        if (p.trace != nullptr && lane == 0) p.trace[(size_t)t0 * 8 + 7] = blockIdx.x * NWP + warp;
-        // rotate the pipeline
-        t0 = t1; t1 = t2; t2 = __shfl_sync(0xffffffffu, t3, 0);
+        V2_TRACE(p.trace, s0.t, 6);
+        if (p.trace != nullptr && lane == 0) p.trace[(size_t)s0.t * 8 + 7] = blockIdx.x * NWP + warp;
+        s0 = s1;
+        s1 = s2;
 #pragma unroll
         for (int i = 0; i < M; ++i) E0[i] = E1[i];
+        sl ^= 1u;
         __syncwarp();
-        float* tb_ = bA; bA = bB; bB = bC; bC = tb_;
-        unsigned long long* tr_ = rA; rA = rB; rB = rC; rC = tr_;
-        const unsigned tp_ = pA; pA = pB; pB = pC; pC = tp_;
     }
+    bulk_wait0();
+    tmem_fence_before();
     cta_exit(cw, ep, gridDim.x);
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(s_tmem, 512);
 }
 
 // ---------------------------------------------------------------------------
@@ -975,21 +1171,25 @@ __global__ void __launch_bounds__(256) lti2_prep_kernel(const float* __restrict_
         o32[C::OK_ + w] = kf;
         o32[C::DIR + C::OK_ + w] = kb;
     }
-    // fp32 tables: P (scan powers) and Q (lane powers), forward (A_f) and backward (A_f^T)
+    // scan powers P[d][j][i] = X^(L 2^d)[i][j], forward X = A_f, backward X = A_f^T
     for (int w = tid; w < 5 * M * MP; w += 256) {
         const int d = w / (M * MP), j = (w / MP) % M, i = w % MP;
         const double* X = mat + (S::SL + (1 << d)) * M2;
         o32[C::OP + w] = i < M ? (float)X[i * M + j] : 0.f;
         o32[C::DIR + C::OP + w] = i < M ? (float)X[j * M + i] : 0.f;
     }
+    // pair tables [j][ip][32]: Q (lane powers X^(l L)) and PQ level v (X^(k 32^v TS))
+    auto pairs = [&](int off, const double* X, int j, int ip, int k) {
+        const int i0 = 2 * ip, i1 = 2 * ip + 1, w = (j * NPR + ip) * 32 + k;
+        o32[off + 2 * w] = (float)X[i0 * M + j];
+        o32[off + 2 * w + 1] = i1 < M ? (float)X[i1 * M + j] : 0.f;
+        o32[C::DIR + off + 2 * w] = (float)X[j * M + i0];
+        o32[C::DIR + off + 2 * w + 1] = i1 < M ? (float)X[j * M + i1] : 0.f;
+    };
     for (int w = tid; w < 32 * M * NPR; w += 256) {
-        const int l = w % 32, ip = (w / 32) % NPR, j = w / (32 * NPR);
-        const double* X = mat + (S::SL + l) * M2;
-        const int i0 = 2 * ip, i1 = 2 * ip + 1;
-        o32[C::OQ + 2 * w] = (float)X[i0 * M + j];
-        o32[C::OQ + 2 * w + 1] = i1 < M ? (float)X[i1 * M + j] : 0.f;
-        o32[C::DIR + C::OQ + 2 * w] = (float)X[j * M + i0];
-        o32[C::DIR + C::OQ + 2 * w + 1] = i1 < M ? (float)X[j * M + i1] : 0.f;
+        const int k = w % 32, ip = (w / 32) % NPR, j = w / (32 * NPR);
+        pairs(C::OQ, mat + (S::SL + k) * M2, j, ip, k);
+        for (int v = 0; v < nlev; ++v) pairs(C::OPQ + v * 32 * M * MP, mat + (S::SQ + v * 33 + k) * M2, j, ip, k);
     }
     if (tid <= M) {
         for (int g = 0; g < 2; ++g) {
@@ -1000,10 +1200,6 @@ __global__ void __launch_bounds__(256) lti2_prep_kernel(const float* __restrict_
         o64[C::COEF + tid] = bn[tid];
         o64[C::COEF + M + 1 + tid] = an[tid];
         if (tid == 0) o64[C::A0] = (double)aa[0];
-    }
-    for (int w = tid; w < nlev * 32 * M2; w += 256) {
-        const int l = w / (32 * M2), rr = w % (32 * M2), e = rr / 32, k = rr % 32;
-        o64[C::PQ + w] = mat[(S::SQ + l * 33 + k) * M2 + e];
     }
 }
 

@@ -3,7 +3,7 @@
 #   tools/prof_v2.sh TAG WORKLOAD [kernel-regex]
 TAG=${1:-p}; W=${2:-c5}; KRE=${3:-lti2_(fwd|bwd)}
 OUT=gpurun_out/$TAG; mkdir -p $OUT
-timeout 900 ncu --set full --import-source on --clock-control none -k "regex:$KRE" -s 2 -c 2 \
+IIRG_LIB=${IIRG_LIB:-} timeout 900 ncu --set full --import-source on --clock-control none -k "regex:$KRE" -s 2 -c 2 \
   -o $OUT/full python bench.py --workload $W --steps 2 --warmup 1 --no-graph --no-cpu-baseline > $OUT/ncu.log 2>&1
 echo "ncu rc=$?"
 python profiles/ncu_summary.py $OUT/full.ncu-rep $OUT/summary.txt > /dev/null 2>&1
