@@ -153,7 +153,9 @@ static Layout layout(const iir_desc_t* d) {
     while (L.nlev < MAX_LEVELS && (int64_t(1) << (5 * L.nlev)) < L.ntiles) ++L.nlev;
     for (int l = 0; l < MAX_LEVELS; ++l)
         L.nblk[l] = l < L.nlev ? (L.ntiles + (int64_t(1) << (5 * l)) - 1) >> (5 * l) : 0;
-    const int64_t per_set = d->coef_mode == IIR_COEF_SHARED ? L.ntot : L.ntiles;
+    // partial-sum rows per coefficient set: one per tile (the round-2 SHARED path: one per
+    // warp of the grid, at most ntot + 63)
+    const int64_t per_set = (d->coef_mode == IIR_COEF_SHARED ? L.ntot : L.ntiles) + (d->coef_mode == IIR_COEF_SHARED ? 64 : 0);
     const int64_t ng_set = (per_set + 31) / 32;
     L.ngroups = ng_set * L.ncoef;
     size_t o = 0;
@@ -166,7 +168,7 @@ static Layout layout(const iir_desc_t* d) {
     L.ws_bank = o - L.ws_sent;                           // two banks of look-back slots (epoch parity),
     o += 3 * L.ws_bank;                                  // for the forward and for the backward
     L.ws_sent_bytes = o - L.ws_sent;
-    L.ws_part = o; o += al256(L.ntot * NGP * 8);
+    L.ws_part = o; o += al256((L.ntot + 64) * NGP * 8);
     L.ws_part2 = o; o += al256(L.ngroups * NGP * 8);
     L.ws_car = o; o += al256(L.ntot * M * 8);
     L.ws_carb = o; o += al256(L.ntot * M * 8);

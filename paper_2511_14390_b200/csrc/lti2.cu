@@ -71,7 +71,7 @@ struct Ops {
     static iir_status_t forward(const Call& c) {
         const DevInfo& d = dev_info();
         iir_status_t s = launch(K_LTI_PREP, c.st, [&] {
-            lti2_prep_kernel<M><<<(unsigned)c.ncoef, 256, Prep2Slots<M>::bytes(), c.st>>>(
+            lti2_prep_kernel<M><<<dim3((unsigned)c.ncoef, 2 + c.nlev), PREP_NT, Prep2Slots<M>::bytes(), c.st>>>(
                 c.b, c.a, c.cstride, const_cast<float*>(c.f.t32), c.f.t32_stride, const_cast<double*>(c.f.t64),
                 c.f.t64_stride, c.nlev);
         });

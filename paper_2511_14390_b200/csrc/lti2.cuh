@@ -764,6 +764,75 @@ __device__ __forceinline__ void chain_rule2(const double (&G)[2 * M + 1], const 
     }
 }
 
+// One row of coefficient partial sums (lane k < NG holds value k) joins the fixed-order
+// reduction of its set: rows are reduced in groups of 32 by the group's last arrival, the
+// groups by the set's last group (flat when the set has at most FLAT_ROWS rows), then the
+// chain rule writes grad_b, grad_a.  Deterministic: every sum runs over row indices in a
+// fixed order, whatever the arrival order.
+template <int M>
+__device__ __forceinline__ void finalize_row(const BwdArgs& p, int64_t cset, int64_t per_set, int64_t li,
+                                             double colsum, int lane, const double* __restrict__ t64) {
+    constexpr int NG = Cfg<M>::NG;
+    double* part = p.partial + cset * per_set * NG;
+    const bool flat = per_set <= FLAT_ROWS;
+    const int64_t ngroups = (per_set + 31) >> 5;
+    const int64_t gi = li >> 5;
+    const int gsize = (int)((per_set - (gi << 5)) < 32 ? (per_set - (gi << 5)) : 32);
+    double* part2 = p.partial2 + cset * ngroups * NG;
+    if (lane < NG) __stcg(part + li * NG + lane, colsum);
+    __threadfence();
+    __syncwarp();
+    unsigned fin = 0;
+    if (lane == 0) {
+        if (flat) fin = (atomicAdd(p.scnt + cset, 1u) == (unsigned)per_set - 1u) ? 2u : 0u;
+        else fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
+    }
+    fin = __shfl_sync(0xffffffffu, fin, 0);
+    if (fin == 1u) {                                  // last row of its group: reduce the group
+        __threadfence();
+        double gs[NG];
+        warp_reduce_rows<NG>(part + (gi << 5) * NG, gsize, lane, gs);
+#pragma unroll
+        for (int k = 0; k < NG; ++k)
+            if (lane == k) __stcg(part2 + gi * NG + k, gs[k]);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+            p.gcnt[cset * ngroups + gi] = 0u;
+            fin = (atomicAdd(p.scnt + cset, 1u) == (unsigned)ngroups - 1u) ? 3u : 0u;
+        }
+        fin = __shfl_sync(0xffffffffu, fin, 0);
+    }
+    if (fin >= 2u) {                                  // last of the set: final sum + chain rule
+        __threadfence();
+        double gs[NG];
+        if (fin == 2u) warp_reduce_rows<NG>(part, per_set, lane, gs);
+        else warp_reduce_rows<NG>(part2, ngroups, lane, gs);
+        if (lane == 0) {
+            chain_rule2<M>(gs, t64, p.gb == nullptr ? nullptr : p.gb + cset * (M + 1),
+                           p.ga == nullptr ? nullptr : p.ga + cset * (M + 1));
+            p.scnt[cset] = 0u;
+        }
+    }
+}
+// The 32 lanes' partial sums (C_0, (C_k, D_k) pairs) -> fp64 column sums via lane rows of a
+// free shared buffer; lane k < NG returns sum k (fixed order over the lanes).
+template <int M>
+__device__ __forceinline__ double lane_colsum(float* scratch, int lane, float C0, const unsigned long long (&CD)[M]) {
+    using C = Cfg<M>;
+    __syncwarp();
+    float* scr = scratch + lane * C::PITCH;
+    scr[0] = C0;
+#pragma unroll
+    for (int i = 0; i < M; ++i) { scr[1 + i] = lo2(CD[i]); scr[M + 1 + i] = hi2(CD[i]); }
+    __syncwarp();
+    double colsum = 0.0;
+    if (lane < C::NG)
+        for (int r = 0; r < 32; ++r) colsum += (double)scratch[r * C::PITCH + lane];
+    __syncwarp();
+    return colsum;
+}
+
 template <int M, int NWP, bool GT>
 __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) {
     using C = Cfg<M>;
@@ -802,7 +871,6 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
     tmem_fence_after();
     const unsigned tbase = s_tmem + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)((warp >> 2) * 2 * L);
     const bool vec = p.vec != 0;
-    const bool shared_set = p.ncoef == 1;
     Sched s0, s1;
     s0.init(blockIdx.x * NWP + warp, gridDim.x * NWP, p.B);
     s1 = s0;
@@ -849,6 +917,12 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
         carry_publish<M>(p.t32 + s.seq * p.t32_stride + C::DIR + C::OPQ, lane, s.j, s.seq, X0, G, cw);
         V2_TRACE(p.trace, s.t, 2);
     };
+    // coefficient partial sums: SHARED accumulates over all of this warp's tiles (a fixed set
+    // in a fixed order under the static schedule) and flushes one row per warp at the end
+    unsigned long long CD[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) CD[i] = 0ull;
+    float C0 = 0.f;
     float E0[M];
     unsigned sl = 0;
     if (s0.t < p.ntot) {
@@ -931,10 +1005,11 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
 #pragma unroll
         for (int k = 0; k < M; ++k) w[k] = din[k];               // (each step first shifts by one)
         w[M] = 0.f;
-        unsigned long long CD[M];
+        if constexpr (GT) {                                     // PER_SEQ: one partial row per tile
 #pragma unroll
-        for (int i = 0; i < M; ++i) CD[i] = 0ull;
-        float C0 = 0.f;
+            for (int i = 0; i < M; ++i) CD[i] = 0ull;
+            C0 = 0.f;
+        }
         float* xr = bX + c * C::PITCH;
         const float* yr = bY + c * C::PITCH;
         {
@@ -993,60 +1068,11 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
                 }
             }
         }
-        // a8: per-tile row of the coefficient partial sums (fixed order), group / set finalize
-        if (p.want_coef) {
-            __syncwarp();
-            float* scr = bY + lane * C::PITCH;                    // y has been consumed: lane rows as scratch
-            scr[0] = C0;
-#pragma unroll
-            for (int i = 0; i < M; ++i) { scr[1 + i] = lo2(CD[i]); scr[M + 1 + i] = hi2(CD[i]); }
-            __syncwarp();
-            double colsum = 0.0;
-            if (lane < NG)
-                for (int r = 0; r < 32; ++r) colsum += (double)bY[r * C::PITCH + lane];
-            const int64_t per_set = shared_set ? p.ntot : p.ntiles;
-            const int64_t cset = shared_set ? 0 : seq;
-            const int64_t li = shared_set ? (int64_t)s0.t : jr;
-            double* part = p.partial + cset * per_set * NG;
-            const bool flat = per_set <= FLAT_ROWS;
-            const int64_t ngroups = (per_set + 31) >> 5;
-            const int64_t gi = li >> 5;
-            const int gsize = (int)((per_set - (gi << 5)) < 32 ? (per_set - (gi << 5)) : 32);
-            double* part2 = p.partial2 + cset * ngroups * NG;
-            if (lane < NG) __stcg(part + li * NG + lane, colsum);
-            __threadfence();
-            __syncwarp();
-            unsigned fin = 0;
-            if (lane == 0) {
-                if (flat) fin = (atomicAdd(p.scnt + cset, 1u) == (unsigned)per_set - 1u) ? 2u : 0u;
-                else fin = (atomicAdd(p.gcnt + cset * ngroups + gi, 1u) == (unsigned)gsize - 1u) ? 1u : 0u;
-            }
-            fin = __shfl_sync(0xffffffffu, fin, 0);
-            if (fin == 1u) {                                  // last tile of its group: reduce the group
-                __threadfence();
-                double gs[NG];
-                warp_reduce_rows<NG>(part + (gi << 5) * NG, gsize, lane, gs);
-#pragma unroll
-                for (int k = 0; k < NG; ++k)
-                    if (lane == k) __stcg(part2 + gi * NG + k, gs[k]);
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) {
-                    p.gcnt[cset * ngroups + gi] = 0u;
-                    fin = (atomicAdd(p.scnt + cset, 1u) == (unsigned)ngroups - 1u) ? 3u : 0u;
-                }
-                fin = __shfl_sync(0xffffffffu, fin, 0);
-            }
-            if (fin >= 2u) {                                  // last of the set: final sum + chain rule
-                __threadfence();
-                double gs[NG];
-                if (fin == 2u) warp_reduce_rows<NG>(part, per_set, lane, gs);
-                else warp_reduce_rows<NG>(part2, ngroups, lane, gs);
-                if (lane == 0) {
-                    chain_rule2<M>(gs, t64, p.gb == nullptr ? nullptr : p.gb + cset * (M + 1),
-                                   p.ga == nullptr ? nullptr : p.ga + cset * (M + 1));
-                    p.scnt[cset] = 0u;
-                }
+        // a8 (PER_SEQ): the tile's partial-sum row joins its sequence's fixed-order reduction
+        if constexpr (GT) {
+            if (p.want_coef) {
+                const double colsum = lane_colsum<M>(bY, lane, C0, CD);
+                finalize_row<M>(p, seq, p.ntiles, jr, colsum, lane, t64);
             }
         }
         V2_TRACE(p.trace, s0.t, 6);
@@ -1058,6 +1084,13 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
         sl ^= 1u;
         __syncwarp();
     }
+    // a8 (SHARED): one row per warp of the grid, indexed by the warp's global id
+    if constexpr (!GT) {
+        if (p.want_coef) {
+            const double colsum = lane_colsum<M>(bY, lane, C0, CD);
+            finalize_row<M>(p, 0, (int64_t)gridDim.x * NWP, (int64_t)blockIdx.x * NWP + warp, colsum, lane, p.t64);
+        }
+    }
     bulk_wait0();
     tmem_fence_before();
     cta_exit(cw, ep, gridDim.x);
@@ -1066,30 +1099,38 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
 }
 
 // ---------------------------------------------------------------------------
-// a1: prologue (one CTA per coefficient set, fp64): normalise by a0, A_f = companion(a')^T,
-// the chunk weights K, the scan powers, the lane powers and the look-back powers.  Every
-// table comes from powers built by batched doubling (about 6 + 5 + 5 nlev dependent
-// rounds of independent M x M products), so the prologue is a few microseconds.
+// a1: prologue (fp64), one small CTA per (coefficient set, role); the roles are
+// independent, so the prologue's latency is the longest role, not their sum:
+//   role 0: K weights by vector doubling (U[m] = A_f^m c, R[m] = e1^T A_f^m from the
+//           squarings A_f^(2^j)), the scan powers A_f^(L 2^d), the coefficients;
+//   role 1: the lane powers A_f^(l L), l = 0..32 (Q);
+//   role 2+v: the look-back powers A_f^(k 32^v TS), k = 0..31, of level v (PQ).
+// Each role builds its base power by repeated squaring of A_f, then doubles.
+constexpr int PREP_NT = 256;
 template <int M> struct Prep2Slots {
-    static constexpr int L = Cfg<M>::L;
-    static constexpr int SP = 0 /* L+1: A_f^m */, SL = SP + L + 1 /* 33: A_f^(l L) */, SQ = SL + 33 /* LEVELS x 33 */;
-    static constexpr int N = SQ + LEVELS * 33;
-    static constexpr size_t bytes() { return (size_t)N * M * M * sizeof(double); }
+    static constexpr int NSQ = 32;        // squarings A_f^(2^j), j < NSQ (enough for 32^3 TS)
+    static constexpr int SW = NSQ, SPOW = SW + 1, N = SPOW + 33;
+    static constexpr size_t bytes() { return (size_t)N * M * M * sizeof(double) + 2 * (size_t)Cfg<M>::L * M * sizeof(double); }
 };
 
 template <int M>
-__global__ void __launch_bounds__(256) lti2_prep_kernel(const float* __restrict__ b, const float* __restrict__ a,
-                                                       int64_t coef_stride, float* __restrict__ t32,
-                                                       int64_t t32_stride, double* __restrict__ t64,
-                                                       int64_t t64_stride, int nlev) {
+__global__ void __launch_bounds__(PREP_NT) lti2_prep_kernel(const float* __restrict__ b, const float* __restrict__ a,
+                                                           int64_t coef_stride, float* __restrict__ t32,
+                                                           int64_t t32_stride, double* __restrict__ t64,
+                                                           int64_t t64_stride, int nlev) {
     pdl_launch_dependents();
     using C = Cfg<M>;
     using S = Prep2Slots<M>;
     constexpr int L = C::L, M2 = M * M, MP = C::MP, NPR = C::NPR;
+    constexpr int LOG_L = L == 64 ? 6 : L == 32 ? 5 : L == 128 ? 7 : 0;
+    static_assert(LOG_L > 0, "chunk length must be 32, 64 or 128");
     extern __shared__ __align__(16) unsigned char prep2_raw[];
     double* mat = reinterpret_cast<double*>(prep2_raw);
+    double* U = mat + S::N * M2;                          // [L][M]: A_f^m c
+    double* R = U + L * M;                                // [L][M]: e1^T A_f^m
     __shared__ double bn[M + 1], an[M + 1], cv[M];
-    const int set = blockIdx.x, tid = threadIdx.x;
+    const int set = blockIdx.x, role = blockIdx.y, tid = threadIdx.x;
+    if (role >= 2 && role - 2 >= nlev) return;
     const float* bb = b + set * coef_stride;
     const float* aa = a + set * coef_stride;
     float* o32 = t32 + set * t32_stride;
@@ -1101,22 +1142,20 @@ __global__ void __launch_bounds__(256) lti2_prep_kernel(const float* __restrict_
     }
     __syncthreads();
     if (tid < M) cv[tid] = bn[tid + 1] - an[tid + 1] * bn[0];
-    for (int e = tid; e < M2; e += 256) {
+    for (int e = tid; e < M2; e += PREP_NT) {
         const int i = e / M, j = e % M;
-        mat[(S::SP + 1) * M2 + e] = (j == 0 ? -an[i + 1] : 0.0) + (j == i + 1 ? 1.0 : 0.0);   // A_f[i][j]
-        const double id = (i == j) ? 1.0 : 0.0;
-        mat[(S::SP + 0) * M2 + e] = id;
-        mat[(S::SL + 0) * M2 + e] = id;
-        for (int l = 0; l < LEVELS; ++l) mat[(S::SQ + l * 33) * M2 + e] = id;
+        mat[0 * M2 + e] = (j == 0 ? -an[i + 1] : 0.0) + (j == i + 1 ? 1.0 : 0.0);   // A_f[i][j] = squaring 0
+        mat[S::SPOW * M2 + e] = (i == j) ? 1.0 : 0.0;                                  // X^0
     }
     __syncthreads();
+    // batched products: for q < n: mat[dst(q)] = mat[lhs(q)] * mat[rhs(q)]
     auto mm_batch = [&](int n, auto dst, auto lhs, auto rhs) {
-        constexpr int R = (32 * M2 + 255) / 256;
-        double rr[R];
+        constexpr int RR = (16 * M2 + PREP_NT - 1) / PREP_NT;
+        double rr[RR];
 #pragma unroll
-        for (int s = 0; s < R; ++s) {
-            const int w = tid + s * 256;
-            rr[s] = 0.0;
+        for (int s2 = 0; s2 < RR; ++s2) {
+            const int w = tid + s2 * PREP_NT;
+            rr[s2] = 0.0;
             if (w < n * M2) {
                 const int q = w / M2, e = w % M2, i = e / M, j = e % M;
                 const double* A = mat + lhs(q) * M2;
@@ -1124,83 +1163,106 @@ __global__ void __launch_bounds__(256) lti2_prep_kernel(const float* __restrict_
                 double acc = 0.0;
 #pragma unroll
                 for (int k = 0; k < M; ++k) acc = fma(A[i * M + k], B[k * M + j], acc);
-                rr[s] = acc;
+                rr[s2] = acc;
             }
         }
         __syncthreads();
 #pragma unroll
-        for (int s = 0; s < R; ++s) {
-            const int w = tid + s * 256;
-            if (w < n * M2) mat[dst(w / M2) * M2 + (w % M2)] = rr[s];
+        for (int s2 = 0; s2 < RR; ++s2) {
+            const int w = tid + s2 * PREP_NT;
+            if (w < n * M2) mat[dst(w / M2) * M2 + (w % M2)] = rr[s2];
         }
         __syncthreads();
     };
-    // slot0 = X^0, slot0 + 1 = X^1 known: fill X^2 .. X^(2^rounds)
-    auto powers = [&](int slot0, int rounds) {
-        for (int st = 0; st < rounds; ++st) {
+    auto square_to = [&](int j1) {                      // squarings 1 .. j1 (A_f^(2^j))
+        for (int j = 1; j <= j1; ++j)
+            mm_batch(1, [&](int) { return j; }, [&](int) { return j - 1; }, [&](int) { return j - 1; });
+    };
+    // SPOW + k = X^k, k = 0..32, from X = squaring jx (SPOW + 1 set by the caller)
+    auto powers32 = [&]() {
+        for (int st = 0; st < 5; ++st) {
             const int h = 1 << st;
-            mm_batch(h, [&](int q) { return slot0 + h + 1 + q; }, [&](int) { return slot0 + h; },
-                     [&](int q) { return slot0 + 1 + q; });
+            mm_batch(h, [&](int q) { return S::SPOW + h + 1 + q; }, [&](int) { return S::SPOW + h; },
+                     [&](int q) { return S::SPOW + 1 + q; });
         }
     };
     auto copy = [&](int dst, int src) {
-        for (int e = tid; e < M2; e += 256) mat[dst * M2 + e] = mat[src * M2 + e];
+        for (int e = tid; e < M2; e += PREP_NT) mat[dst * M2 + e] = mat[src * M2 + e];
         __syncthreads();
     };
-    constexpr int LOG_L = L == 64 ? 6 : L == 32 ? 5 : L == 128 ? 7 : 0;
-    static_assert(LOG_L > 0, "chunk length must be 32, 64 or 128");
-    powers(S::SP, LOG_L);                                              // A_f^m, m = 0..L
-    copy(S::SL + 1, S::SP + L);
-    powers(S::SL, 5);                                                  // A_f^(l L), l = 0..32
-    copy(S::SQ + 1, S::SL + 32);                                       // A_f^TS
-    for (int l = 0; l < nlev; ++l) {
-        powers(S::SQ + l * 33, 5);                                     // A_f^(k 32^l TS), k = 0..32
-        if (l + 1 < LEVELS) copy(S::SQ + (l + 1) * 33 + 1, S::SQ + l * 33 + 32);
-    }
-    // chunk weights: KF[k] = A_f^(L-1-k) c (forward), KB[k] = (A_f^T)^k e1 = row 0 of A_f^k (backward)
-    for (int w = tid; w < L * MP; w += 256) {
-        const int k = w / MP, i = w % MP;
-        float kf = 0.f, kb = 0.f;
-        if (i < M) {
-            const double* X = mat + (S::SP + L - 1 - k) * M2;
-            double s = 0.0;
-            for (int j = 0; j < M; ++j) s = fma(X[i * M + j], cv[j], s);
-            kf = (float)s;
-            kb = (float)mat[(S::SP + k) * M2 + i];
+    // pair tables [j][ip][32] of X^k (k = 0..31), forward X and backward X^T
+    auto pair_table = [&](int off) {
+        for (int w = tid; w < 32 * M * NPR; w += PREP_NT) {
+            const int k = w % 32, ip = (w / 32) % NPR, j = w / (32 * NPR);
+            const double* X = mat + (S::SPOW + k) * M2;
+            const int i0 = 2 * ip, i1 = 2 * ip + 1;
+            o32[off + 2 * w] = (float)X[i0 * M + j];
+            o32[off + 2 * w + 1] = i1 < M ? (float)X[i1 * M + j] : 0.f;
+            o32[C::DIR + off + 2 * w] = (float)X[j * M + i0];
+            o32[C::DIR + off + 2 * w + 1] = i1 < M ? (float)X[j * M + i1] : 0.f;
         }
-        o32[C::OK_ + w] = kf;
-        o32[C::DIR + C::OK_ + w] = kb;
-    }
-    // scan powers P[d][j][i] = X^(L 2^d)[i][j], forward X = A_f, backward X = A_f^T
-    for (int w = tid; w < 5 * M * MP; w += 256) {
-        const int d = w / (M * MP), j = (w / MP) % M, i = w % MP;
-        const double* X = mat + (S::SL + (1 << d)) * M2;
-        o32[C::OP + w] = i < M ? (float)X[i * M + j] : 0.f;
-        o32[C::DIR + C::OP + w] = i < M ? (float)X[j * M + i] : 0.f;
-    }
-    // pair tables [j][ip][32]: Q (lane powers X^(l L)) and PQ level v (X^(k 32^v TS))
-    auto pairs = [&](int off, const double* X, int j, int ip, int k) {
-        const int i0 = 2 * ip, i1 = 2 * ip + 1, w = (j * NPR + ip) * 32 + k;
-        o32[off + 2 * w] = (float)X[i0 * M + j];
-        o32[off + 2 * w + 1] = i1 < M ? (float)X[i1 * M + j] : 0.f;
-        o32[C::DIR + off + 2 * w] = (float)X[j * M + i0];
-        o32[C::DIR + off + 2 * w + 1] = i1 < M ? (float)X[j * M + i1] : 0.f;
     };
-    for (int w = tid; w < 32 * M * NPR; w += 256) {
-        const int k = w % 32, ip = (w / 32) % NPR, j = w / (32 * NPR);
-        pairs(C::OQ, mat + (S::SL + k) * M2, j, ip, k);
-        for (int v = 0; v < nlev; ++v) pairs(C::OPQ + v * 32 * M * MP, mat + (S::SQ + v * 33 + k) * M2, j, ip, k);
-    }
-    if (tid <= M) {
-        for (int g = 0; g < 2; ++g) {
-            o32[g * C::DIR + C::OC + tid] = (float)bn[tid];
-            o32[g * C::DIR + C::OC + M + 1 + tid] = (float)an[tid];
-            if (tid < M) o32[g * C::DIR + C::OC + 2 * (M + 1) + tid] = (float)cv[tid];
+    if (role == 0) {
+        square_to(LOG_L + 4);                            // A_f^(2^j), j <= log2(L) + 4
+        // vector doubling: U[m] = A_f^m c, R[m] = e1^T A_f^m
+        if (tid < M) { U[tid] = cv[tid]; R[tid] = tid == 0 ? 1.0 : 0.0; }
+        __syncthreads();
+        for (int j = 0; j < LOG_L; ++j) {
+            const int h = 1 << j;
+            const double* X = mat + j * M2;              // A_f^h
+            double ru[(L / 2 * M + PREP_NT - 1) / PREP_NT], rr2[(L / 2 * M + PREP_NT - 1) / PREP_NT];
+#pragma unroll
+            for (int s2 = 0; s2 < (L / 2 * M + PREP_NT - 1) / PREP_NT; ++s2) {
+                const int w = tid + s2 * PREP_NT;
+                ru[s2] = rr2[s2] = 0.0;
+                if (w < h * M) {
+                    const int m = w / M, i = w % M;
+                    double su = 0.0, sr = 0.0;
+                    for (int k = 0; k < M; ++k) {
+                        su = fma(X[i * M + k], U[m * M + k], su);     // (A^h U[m])_i
+                        sr = fma(R[m * M + k], X[k * M + i], sr);     // (R[m] A^h)_i
+                    }
+                    ru[s2] = su;
+                    rr2[s2] = sr;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int s2 = 0; s2 < (L / 2 * M + PREP_NT - 1) / PREP_NT; ++s2) {
+                const int w = tid + s2 * PREP_NT;
+                if (w < h * M) { U[(w / M + h) * M + w % M] = ru[s2]; R[(w / M + h) * M + w % M] = rr2[s2]; }
+            }
+            __syncthreads();
         }
-        o64[C::COEF + tid] = bn[tid];
-        o64[C::COEF + M + 1 + tid] = an[tid];
-        if (tid == 0) o64[C::A0] = (double)aa[0];
+        for (int w = tid; w < L * MP; w += PREP_NT) {       // KF[k] = U[L-1-k], KB[k] = R[k]
+            const int k = w / MP, i = w % MP;
+            o32[C::OK_ + w] = i < M ? (float)U[(L - 1 - k) * M + i] : 0.f;
+            o32[C::DIR + C::OK_ + w] = i < M ? (float)R[k * M + i] : 0.f;
+        }
+        for (int w = tid; w < 5 * M * MP; w += PREP_NT) {   // P[d][j][i] = X^(L 2^d)[i][j]
+            const int d = w / (M * MP), j = (w / MP) % M, i = w % MP;
+            const double* X = mat + (LOG_L + d) * M2;
+            o32[C::OP + w] = i < M ? (float)X[i * M + j] : 0.f;
+            o32[C::DIR + C::OP + w] = i < M ? (float)X[j * M + i] : 0.f;
+        }
+        if (tid <= M) {
+            for (int g = 0; g < 2; ++g) {
+                o32[g * C::DIR + C::OC + tid] = (float)bn[tid];
+                o32[g * C::DIR + C::OC + M + 1 + tid] = (float)an[tid];
+                if (tid < M) o32[g * C::DIR + C::OC + 2 * (M + 1) + tid] = (float)cv[tid];
+            }
+            o64[C::COEF + tid] = bn[tid];
+            o64[C::COEF + M + 1 + tid] = an[tid];
+            if (tid == 0) o64[C::A0] = (double)aa[0];
+        }
+        return;
     }
+    // role 1: X = A_f^L;  role 2+v: X = A_f^(32^v TS) = A_f^(2^(LOG_L + 5 + 5 v))
+    const int jx = role == 1 ? LOG_L : LOG_L + 5 + 5 * (role - 2);
+    square_to(jx);
+    copy(S::SPOW + 1, jx);
+    powers32();
+    pair_table(role == 1 ? C::OQ : C::OPQ + (role - 2) * 32 * M * MP);
 }
 
 }  // namespace v2
