@@ -72,13 +72,9 @@ def algorithmic_bytes(w):
         return d
     # HBM bytes per kernel the method must move: fwd reads x, writes y (+u for DF);
     # bwd reads dy, x, y (TDF) or dy, u (DF) and writes dx: 24 B/sample in fp32
-    # three-phase schedule: lti_red_fwd reads x, lti_red_bwd reads dy (the emit
-    # kernels then re-read them, counted in their own bytes: from L2 when the
-    # working set fits); lti_cscan moves M fp64 per tile only
-    red = {"lti_red_fwd": s, "lti_red_bwd": s, "lti_cscan": 0}
     if w["form"] == "tdf":
-        return dict(red, lti_fwd=2 * s, lti_bwd=4 * s)
-    return dict(red, lti_fwd=3 * s, lti_bwd=3 * s)
+        return dict(lti_fwd=2 * s, lti_bwd=4 * s)
+    return dict(lti_fwd=3 * s, lti_bwd=3 * s)
 
 
 def step_min_bytes(w):
@@ -204,7 +200,10 @@ class Problem:
         self.gb = None if self.b is None else torch.empty_like(self.b)
         self.ga = None if w["coef"] == "per_sample" else torch.empty_like(self.a)
         # the workspace is cleared once; every completed call leaves it cleared
-        sched = {"auto": 0, "1p": B.IIR_FLAG_SINGLE_PASS, "3p": B.IIR_FLAG_THREE_PHASE}[w.get("scan", "auto")]
+        # engine: auto (by order), v1 (round-1 CTA tiles), v2 (round-2 persistent warp tiles);
+        # grad_y is resident before the step: the backward may read it while the forward drains
+        sched = {"auto": 0, "v1": B.IIR_FLAG_LEGACY_LTI, "v2": B.IIR_FLAG_ENGINE_V2}[w.get("engine", "auto")]
+        sched |= B.IIR_FLAG_GRAD_Y_EARLY
         if w.get("fir"):
             sched |= B.IIR_FLAG_PER_SAMPLE_B
         self.desc = B.make_desc(Bsz, T, M, w["form"], td, mode, flags=B.IIR_FLAG_WS_READY | sched)
@@ -543,10 +542,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--scan", default="auto", choices=["auto", "1p", "3p"],
-                    help="LTI scan schedule: auto (by tile count), single-pass or three-phase")
+    ap.add_argument("--engine", default="auto", choices=["auto", "v1", "v2"],
+                    help="fp32 TDF engine: auto (by order), v1 (round-1 CTA tiles), v2 (round-2 warp tiles)")
     args = ap.parse_args()
-    w = dict(WORKLOADS[args.workload], key=args.workload, scan=args.scan)
+    w = dict(WORKLOADS[args.workload], key=args.workload, engine=args.engine)
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: re-launch under torch.distributed.run (the driver's own launch line)
@@ -620,7 +619,7 @@ def main():
         "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic (seeded Gaussian signals, random stable filters)",
         "config": {"workload": w["desc"], "batch_per_gpu": w["batch"], "global_batch": w["batch"] * world,
                    "length": w["length"], "order": w["order"],
-                   "form": w["form"], "coef": w["coef"], "scan_schedule": w["scan"],
+                   "form": w["form"], "coef": w["coef"], "engine": w["engine"],
                    "l2": f"{r['nsets']} rotating input/output buffer sets x {r['set_bytes'] / 2**20:.0f} MiB "
                          f"(> 2x L2 = {2 * r['L2'] / 2**20:.0f} MiB)",
                    "timing": "CUDA graph of K steps" if r["graph"] else "eager launches",

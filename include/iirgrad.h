@@ -92,7 +92,7 @@ typedef void *iir_stream_t;  /* a cudaStream_t */
 typedef struct {
     int64_t batch;      /* B >= 1                                                  */
     int64_t length;     /* T >= 1 samples per sequence                             */
-    int32_t order;      /* M: 1..8 (SHARED / PER_SEQ); PER_SAMPLE: 1-8,10,12,16,20,24,28,31 */
+    int32_t order;      /* M: 1..8 (SHARED / PER_SEQ); PER_SAMPLE: 1..31                  */
     int32_t form;       /* iir_form_t                                              */
     int32_t dtype;      /* iir_dtype_t                                             */
     int32_t coef_mode;  /* iir_coef_mode_t                                         */
@@ -105,15 +105,12 @@ typedef enum {
      * it), so iir_forward / iir_backward skip their cudaMemsetAsync of it.  Without
      * this flag every call first clears the workspace's counters itself.           */
     IIR_FLAG_WS_READY = 1,
-    /* LTI scan schedule (default: SINGLE_PASS).
-     * SINGLE_PASS: one kernel per direction, carries by decoupled look-back across
-     * resident tiles.  THREE_PHASE: tile aggregates (streaming), a per-sequence
-     * fp64 carry scan, then emission from the precomputed carries (no inter-CTA
-     * waits, one more pass over the data; slower on the BASELINE shapes, see
-     * DESIGN.md).  Both give the same result up to fp64 rounding of the carries;
-     * the bare recurrence (IIR_SS) is always single-pass. */
+    /* Bit 1 is accepted and ignored (it named the single-pass LTI schedule, the only
+     * one).  Bit 2 named a three-phase schedule (tile aggregates, a separate carry scan,
+     * then emission) that lost on every measured shape; it was removed in ABI 2 and is
+     * rejected with IIR_EUNSUPPORTED. */
     IIR_FLAG_SINGLE_PASS = 2,
-    IIR_FLAG_THREE_PHASE = 4,
+    IIR_FLAG_THREE_PHASE_REMOVED = 4,
     /* IIR_COEF_PER_SAMPLE with a per-sample numerator: the general
      * time-varying DF-II filter u(n) = x(n) - sum_i a_i(n) u(n-i),
      * y(n) = sum_k b_k(n) u(n-k), both rows applied at output time n (R19);
@@ -121,10 +118,20 @@ typedef enum {
      * the internal signal history [u(-1)..u(-M)].  Without it, PER_SAMPLE is the
      * all-pole filter (b must be NULL). */
     IIR_FLAG_PER_SAMPLE_B = 8,
-    /* fp32 TDF-II with SHARED / PER_SEQ coefficients runs on the round-2 engine
-     * (persistent warp tiles) by default; this flag selects the
-     * round-1 engine (one CTA per tile) instead -- kept for A/B measurement. */
-    IIR_FLAG_LEGACY_LTI = 16
+    /* Engine of fp32 TDF-II with SHARED / PER_SEQ coefficients.
+     * Default: the round-2 engine (persistent warp tiles, TMEM parking, fused backward)
+     * from order 6 up, the round-1 engine (one CTA per tile) below, by measured speed.
+     * IIR_FLAG_LEGACY_LTI forces the round-1 engine, IIR_FLAG_ENGINE_V2 the round-2 one
+     * (both compute the same filter and gradients; they differ in rounding only). */
+    IIR_FLAG_LEGACY_LTI = 16,
+    IIR_FLAG_ENGINE_V2 = 32,
+    /* The caller asserts that grad_y and grad_zf of iir_backward were written before the
+     * matching iir_forward was enqueued (e.g. resident buffers, host copies), so the
+     * backward may read them while the forward is still draining (programmatic dependent
+     * launch).  Without it the backward reads nothing the previous kernel on the stream
+     * may have written before griddepcontrol.wait -- required when a kernel producing
+     * grad_y (a loss) runs between the two calls. */
+    IIR_FLAG_GRAD_Y_EARLY = 64
 } iir_flags_t;
 
 /* Bytes of the forward->backward tape / of the scratch workspace (0 on a bad desc). */

@@ -22,9 +22,11 @@ IIR_F32, IIR_F64 = 0, 1
 IIR_COEF_SHARED, IIR_COEF_PER_SEQ, IIR_COEF_PER_SAMPLE = 0, 1, 2
 IIR_FLAG_WS_READY = 1
 IIR_FLAG_SINGLE_PASS = 2
-IIR_FLAG_THREE_PHASE = 4
+IIR_FLAG_THREE_PHASE_REMOVED = 4
 IIR_FLAG_PER_SAMPLE_B = 8
 IIR_FLAG_LEGACY_LTI = 16
+IIR_FLAG_ENGINE_V2 = 32
+IIR_FLAG_GRAD_Y_EARLY = 64
 
 FORMS = {"df": IIR_DF2, "tdf": IIR_TDF2, "ss": IIR_SS, IIR_DF2: IIR_DF2, IIR_TDF2: IIR_TDF2, IIR_SS: IIR_SS}
 DTYPES = {torch.float32: IIR_F32, torch.float64: IIR_F64}

@@ -28,8 +28,7 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
 
 // ------------------------------------------------------- instrumentation ----
 static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_phi", "tv_chain", "tv_fwd",
-                                        "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd", "lti_red_fwd",
-                                        "lti_red_bwd", "lti_cscan", "state_carry", "tv_fir"};
+                                        "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd", "state_carry", "tv_fir"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;
@@ -96,12 +95,20 @@ iir_status_t rec_run(bool fwd, int dtype, int M, const Layout& L, const LtiFwdAr
                      cudaStream_t st);
 }  // namespace iirg
 
-// fp32 TDF-II with fixed coefficients runs on the round-2 engine (lti2.cuh) unless the
-// caller asks for a round-1 schedule.
-static bool use_v2(const iir_desc_t* d) {
+// Engine choice for fp32 TDF-II with fixed coefficients.  The round-2 engine (lti2.cuh:
+// persistent warp tiles, TMEM parking, fp32 carries, fused backward) is the default from
+// order 6 up; below it the round-1 engine (lti.cuh: one CTA per tile) is faster on the
+// measured shapes (B200: C5 M=8 205 vs 223 us/step, C4 M=4 190 vs
+// 175, C2 M=2 46 vs 32).  IIR_FLAG_ENGINE_V2 / IIR_FLAG_LEGACY_LTI force either one.
+static bool v2_capable(const iir_desc_t* d) {
     return d->form == IIR_TDF2 && d->dtype == IIR_F32 &&
            (d->coef_mode == IIR_COEF_SHARED || d->coef_mode == IIR_COEF_PER_SEQ) && d->order >= 1 && d->order <= 8 &&
-           !(d->flags & (IIR_FLAG_LEGACY_LTI | IIR_FLAG_THREE_PHASE));
+           !(d->flags & IIR_FLAG_LEGACY_LTI);
+}
+static bool use_v2(const iir_desc_t* d) {
+    if (!v2_capable(d)) return false;
+    if (d->flags & IIR_FLAG_ENGINE_V2) return true;
+    return d->order >= 6;
 }
 
 static int scan_tile_samples(const iir_desc_t* d) {
@@ -121,6 +128,8 @@ static iir_status_t check_desc(const iir_desc_t* d) {
             return fail(IIR_EUNSUPPORTED, "bare recurrence: A is SHARED or PER_SEQ");
         if (d->order < 1 || d->order > 4) return fail(IIR_EUNSUPPORTED, "bare recurrence: order must be 1..4");
     }
+    if (d->flags & IIR_FLAG_THREE_PHASE_REMOVED)
+        return fail(IIR_EUNSUPPORTED, "the three-phase LTI schedule was removed (it lost on every measured shape)");
     if ((d->flags & IIR_FLAG_PER_SAMPLE_B) && d->coef_mode != IIR_COEF_PER_SAMPLE)
         return fail(IIR_EINVAL, "IIR_FLAG_PER_SAMPLE_B needs IIR_COEF_PER_SAMPLE");
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) {
@@ -170,8 +179,6 @@ static Layout layout(const iir_desc_t* d) {
     L.ws_sent_bytes = o - L.ws_sent;
     L.ws_part = o; o += al256((L.ntot + 64) * NGP * 8);
     L.ws_part2 = o; o += al256(L.ngroups * NGP * 8);
-    L.ws_car = o; o += al256(L.ntot * M * 8);
-    L.ws_carb = o; o += al256(L.ntot * M * 8);
     L.ws_bytes = o;
     o = 0;
     L.v2 = use_v2(d);
@@ -317,7 +324,6 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     fa.tab = reinterpret_cast<const double*>(t + L.tp_tab);
     fa.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
     fa.cw = carry_ws(L, w, false);
-    fa.car = reinterpret_cast<double*>(w + L.ws_car);
     fa.B = d->batch; fa.Tlen = d->length; fa.ntiles = (int)L.ntiles; fa.vec = vec;
     fa.trace = g_trace;
     fa.span = g_trace == nullptr ? nullptr : g_trace + L.ntot * 16 + 2;   // [prep][fwd][bwd]
@@ -401,10 +407,10 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     ba.scnt = reinterpret_cast<unsigned*>(w + L.ws_scnt);
     ba.ncoef = L.ncoef;
     ba.want_coef = (grad_b != nullptr || grad_a != nullptr);
+    ba.gy_early = (d->flags & IIR_FLAG_GRAD_Y_EARLY) != 0;
     ba.tab = reinterpret_cast<const double*>(t + L.tp_tab);
     ba.tab_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : tab_size(d->order);
     ba.cw = carry_ws(L, w, true);
-    ba.car = reinterpret_cast<double*>(w + L.ws_carb);
     ba.B = d->batch; ba.Tlen = d->length; ba.ntiles = (int)L.ntiles; ba.vec = vec;
     ba.trace = g_trace;
     ba.span = g_trace == nullptr ? nullptr : g_trace + L.ntot * 16 + 4;

@@ -14,7 +14,7 @@ namespace iirg {
 iir_status_t fail(iir_status_t st, const std::string& msg);
 
 enum Kind { K_LTI_PREP = 0, K_LTI_FWD, K_LTI_BWD, K_TV_PHI, K_TV_CHAIN, K_TV_FWD, K_TV_BWD_AGG, K_TV_BWD, K_REC_FWD,
-            K_REC_BWD, K_LTI_RED_F, K_LTI_RED_B, K_LTI_CSCAN, K_STATE_CARRY, K_TV_FIR, K_NUM };
+            K_REC_BWD, K_STATE_CARRY, K_TV_FIR, K_NUM };
 
 // Launch bookkeeping: counts every kernel and (when profiling is on) brackets it
 // with CUDA events on its stream.
@@ -32,6 +32,20 @@ iir_status_t launch(int kind, cudaStream_t st, F&& f) {
 
 inline size_t al256(size_t n) { return (n + 255) / 256 * 256; }
 
+// Once-per-device setup (kernel attributes such as the max dynamic shared memory are
+// per device: a process driving several GPUs must set them on each).
+struct PerDevice {
+    std::mutex mu;
+    bool done[64] = {};
+    template <typename F>
+    void once(F&& f) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(mu);
+        if (!done[dev & 63]) { f(); done[dev & 63] = true; }
+    }
+};
+
 constexpr int MAX_LEVELS = 4;
 struct Layout {
     int64_t ntiles = 0, ntot = 0, ncoef = 0, ngroups = 0;
@@ -42,7 +56,6 @@ struct Layout {
     size_t ws_clear = 0;                                   // [0, ws_clear): counters, initialised to 0
     size_t ws_sent = 0, ws_sent_bytes = 0;                 // look-back slots, initialised to all-ones (NaN)
     size_t ws_agg[MAX_LEVELS] = {0, 0, 0, 0}, ws_part = 0, ws_part2 = 0, ws_bytes = 0;
-    size_t ws_car = 0, ws_carb = 0;                        // three-phase carries [B][ntiles][M] fp64 (fwd, bwd)
     size_t ws_du = 0, ws_duneg = 0;                        // general TV DF: FIR-stage adjoint of u
     size_t ws_psi = 0, ws_omega = 0, ws_sgrp = 0;          // TV two-level chain
     size_t tp_tab = 0, tp_u = 0, tp_extra = 0, tp_bytes = 0;
@@ -52,7 +65,7 @@ struct Layout {
 };
 
 // per-sample (time-varying all-pole) path, tv.cu
-constexpr int TV_MAX_M = 31;
+constexpr int TV_MAX_M = 31;   // per-sample orders 1..31 (the Phi kernel: one lane per basis state + the input)
 bool tv_supported(int M);
 Layout tv_layout(const iir_desc_t* d);
 iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* b, const void* a, const void* x,

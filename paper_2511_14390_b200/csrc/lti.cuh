@@ -442,7 +442,6 @@ struct LtiFwdArgs {
     const void* x; const void* zi; void* y; void* zf; void* u;    // u: DF tape signal
     const double* tab; int64_t tab_stride;                        // 0 for SHARED
     CarryWs cw;
-    double* car;                                                  // 3-phase: carry entering each tile [B][ntiles][M]
     int64_t B, Tlen; int ntiles; int vec;
     unsigned long long* trace;                                    // debug: per-tile phase times
     unsigned long long* span;                                     // debug: kernel span
@@ -451,12 +450,11 @@ struct LtiFwdArgs {
 struct LtiBwdArgs {
     const void* gy; const void* gzf; const void* x; const void* y; const void* u; const void* zi;
     const void* a; int64_t coef_stride;                           // bare recurrence (rec.cuh): A
-    void* gx; void* gzi; void* gb; void* ga; int want_coef;
+    void* gx; void* gzi; void* gb; void* ga; int want_coef; int gy_early;
     double* partial; double* partial2; unsigned* gcnt; unsigned* scnt;   // fused finalize
     int64_t ncoef;
     const double* tab; int64_t tab_stride;
     CarryWs cw;
-    double* car;                                                  // 3-phase: carry entering each tile [B][ntiles][M]
     int64_t B, Tlen; int ntiles; int vec;
     unsigned long long* trace;
     unsigned long long* span;
@@ -719,14 +717,6 @@ __device__ __forceinline__ void tile_carry(const double* st, const double* __res
     for (int i = 0; i < M; ++i) X[i] = R[i];
 }
 
-// Three-phase mode: the carry entering tile j (scan order) of sequence seq,
-// written by lti_cscan_kernel (every lane of the calling warp loads it).
-template <int M>
-__device__ __forceinline__ void load_carry(const double* __restrict__ car, int64_t idx, double (&X)[M]) {
-#pragma unroll
-    for (int i = 0; i < M; ++i) X[i] = __ldcg(car + idx * M + i);
-}
-
 // Scan order of this CTA's tile.  Tiles are scanned in CTA launch order: the
 // hardware dispatches the CTAs of a 1-D grid in increasing blockIdx, so every
 // tile a CTA waits for belongs to a CTA that is already resident (the single-
@@ -800,9 +790,7 @@ template <int M> constexpr int fwd_min_blocks() { return (M <= 2 ? IIRG_MINB2 : 
 template <int M> constexpr int bwd_min_blocks() { return (M <= 4 ? 4 : 3) * 128 / NT > 0 ? (M <= 4 ? 4 : 3) * 128 / NT : 1; }
 template <int M> constexpr int bwd_tdf_min_blocks() { return (M <= 2 ? IIRG_MINB2 : (M <= 4 ? 6 : 4)) * 128 / NT; }
 
-// PRE = true (three-phase mode): the carry entering the tile was computed by
-// lti_red_kernel + lti_cscan_kernel; the tile only emits (no look-back).
-template <typename T, int M, int FORM, bool PRE = false>
+template <typename T, int M, int FORM>
 __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const LtiFwdArgs p) {
     constexpr int L = Chunk<T, M>::L, TS = NT * L, W = Vec<T>::W;
     using V = typename Vec<T>::type;
@@ -815,10 +803,10 @@ __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const 
     __shared__ double s_agg[NW][M];
     __shared__ double s_xw[NW][M];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned tk = PRE ? blockIdx.x : tile_order(p.cw.ticket);
+    const unsigned tk = tile_order(p.cw.ticket);
     span_enter(p.span);
     CarryWs cw = p.cw;
-    const unsigned ep = PRE ? 0u : carry_bank(cw);
+    const unsigned ep = carry_bank(cw);
     const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
     const int jt = (int)(tk / (unsigned long long)p.B);
     const int64_t p0 = (int64_t)jt * TS;
@@ -835,7 +823,7 @@ __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const 
     const double* tb = p.tab + seq * p.tab_stride;
     stage_small_async<M>(st, tb);
     cp_async_commit();
-    if (!PRE) rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
+    rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
     T bc[M + 1], ac[M + 1];
     raw_coefs<T, M>(static_cast<const T*>(p.b) + seq * p.coef_stride,
                     static_cast<const T*>(p.a) + seq * p.coef_stride, bc, ac);
@@ -891,8 +879,7 @@ __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const 
 #pragma unroll
         for (int i = 0; i < M; ++i) X0[i] = (zi != nullptr && jt == 0) ? (double)zi[seq * M + i] : 0.0;
         IIRG_TRACE(p.trace, tk, 2);
-        if constexpr (PRE) load_carry<M>(p.car, seq * p.ntiles + jt, X);
-        else tile_carry<M, false>(st, tb, lane, jt, seq, X0, G, cw, X, p.trace, tk);
+        tile_carry<M, false>(st, tb, lane, jt, seq, X0, G, cw, X, p.trace, tk);
         IIRG_TRACE(p.trace, tk, 3);
         if (lane < NW) {                           // state entering warp `lane`
             double xw[M];
@@ -966,7 +953,7 @@ __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const 
         tile_store<T, TS>(urow, us, p0, p.Tlen, p.vec);
     }
     IIRG_TRACE(p.trace, tk, 5);
-    if (!PRE) cta_exit(cw, ep, gridDim.x);
+    cta_exit(cw, ep, gridDim.x);
     span_exit(p.span);
 }
 
@@ -1134,7 +1121,7 @@ __device__ __forceinline__ void bwd_finalize(const LtiBwdArgs& p, const CarryWs*
 // Backward: a5-a8.  Tiles are aligned to the END of each sequence and taken in
 // ticket order last to first; inside a tile thread t owns chunk NT-1-t, walked
 // backwards.  TDF: smem dy | x | y.  DF: smem dy | u (with HALO samples of history).
-template <typename T, int M, int FORM, bool PRE = false>
+template <typename T, int M, int FORM>
 __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const LtiBwdArgs p) {
     constexpr int L = Chunk<T, M>::L, TS = NT * L, W = Vec<T>::W;
     constexpr int NG = 2 * M + 1;                       // gradient partial sums
@@ -1151,10 +1138,10 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
     __shared__ double s_red[NW][NG];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned tk = PRE ? blockIdx.x : tile_order(p.cw.ticket);
+    const unsigned tk = tile_order(p.cw.ticket);
     span_enter(p.span);
     CarryWs cw = p.cw;
-    const unsigned ep = PRE ? 0u : carry_bank(cw);
+    const unsigned ep = carry_bank(cw);
     const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
     const int jr = (int)(tk / (unsigned long long)p.B);          // 0 = last tile in time
     const int jt = p.ntiles - 1 - jr;                            // time index of the tile
@@ -1177,8 +1164,7 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
         bwd_load_u<T, M, FORM>(p, seq, p0, s2);
     }
     cp_async_commit();
-    if (!PRE) rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
-    if (PRE) pdl_wait();                             // carries (lti_cscan_kernel) and, transitively, y / u
+    rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
     T bc[M + 1], ac[M + 1], cc[M];
     load_coefs<T, M>(tb, bc, ac, cc);
     cp_async_wait<2>();                              // dy
@@ -1222,8 +1208,7 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
 #pragma unroll
         for (int i = 0; i < M; ++i) X0[i] = (gzf != nullptr && jr == 0) ? (double)gzf[seq * M + i] : 0.0;
         IIRG_TRACE(p.trace, tk, 2);
-        if constexpr (PRE) { pdl_wait(); load_carry<M>(p.car, seq * p.ntiles + jr, X); }   // lti_cscan_kernel's carries
-        else tile_carry<M, true>(st, tb, lane, jr, seq, X0, G, cw, X, p.trace, tk);
+        tile_carry<M, true>(st, tb, lane, jr, seq, X0, G, cw, X, p.trace, tk);
         IIRG_TRACE(p.trace, tk, 3);
         if (lane < NW) {
             double xw[M];
@@ -1321,7 +1306,7 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
     // the look-back slots are no longer needed: count this CTA out first, so the
     // gradient finalize of the last CTAs is the kernel's only tail
     IIRG_TRACE(p.trace, tk, 10);
-    bwd_finalize<T, M, FORM>(p, PRE ? nullptr : &cw, ep, tk, seq, jt, tb, s_red);
+    bwd_finalize<T, M, FORM>(p, &cw, ep, tk, seq, jt, tb, s_red);
     IIRG_TRACE(p.trace, tk, 11);
     span_exit(p.span);
 }
@@ -1337,7 +1322,7 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
 // tile start) and storing dx straight to global memory.  The tile's shared
 // footprint drops from three tiles to one, so about twice as many tiles are in
 // flight.  g beyond the tile end comes from the carry: g(p0+TS+j) = X[j+1].
-template <typename T, int M, bool PRE = false>
+template <typename T, int M>
 __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kernel(const LtiBwdArgs p) {
     constexpr int L = Chunk<T, M>::L, TS = NT * L, W = Vec<T>::W;
     constexpr int NG = 2 * M + 1;
@@ -1353,10 +1338,10 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
     __shared__ T s_halo[8];                                     // g(p0 + TS + j), j < M - 1
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned tk = PRE ? blockIdx.x : tile_order(p.cw.ticket);
+    const unsigned tk = tile_order(p.cw.ticket);
     span_enter(p.span);
     CarryWs cw = p.cw;
-    const unsigned ep = PRE ? 0u : carry_bank(cw);
+    const unsigned ep = carry_bank(cw);
     const int64_t seq = (int64_t)(tk % (unsigned long long)p.B);
     const int jr = (int)(tk / (unsigned long long)p.B);          // 0 = last tile in time
     const int jt = p.ntiles - 1 - jr;
@@ -1368,6 +1353,10 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
     const T* yrow = static_cast<const T*>(p.y) + roff;
     IIRG_TRACE(p.trace, tk, 0);
 
+    // grad_y / grad_zf may be written by the kernel right before this one (the caller's
+    // loss): without IIR_FLAG_GRAD_Y_EARLY they are read only after griddepcontrol.wait.
+    // (The tables, x and the workspace were complete before this call's forward began.)
+    if (!p.gy_early) pdl_wait();
     if (p.gy != nullptr) tile_load_async<T, TS>(gs, gyrow, p0, p.Tlen, p.vec);
     else for (int e = tid; e < TS; e += NT) gs[pidx<T>(e)] = T(0);
     cp_async_commit();
@@ -1376,7 +1365,7 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
     if (tid == 0 && p.vec) prefetch_l2_bulk(xrow + pa, pbytes);
     stage_small_async<M>(st, tb);                    // tables live in the tape (written by the forward)
     cp_async_commit();
-    if (!PRE) rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
+    rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
     T bc[M + 1], ac[M + 1], cc[M];
     load_coefs<T, M>(tb, bc, ac, cc);
     cp_async_wait<0>();
@@ -1415,8 +1404,7 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
 #pragma unroll
         for (int i = 0; i < M; ++i) X0[i] = (gzf != nullptr && jr == 0) ? (double)gzf[seq * M + i] : 0.0;
         IIRG_TRACE(p.trace, tk, 2);
-        if constexpr (PRE) { pdl_wait(); load_carry<M>(p.car, seq * p.ntiles + jr, X); }   // lti_cscan_kernel's carries
-        else tile_carry<M, true>(st, tb, lane, jr, seq, X0, G, cw, X, p.trace, tk);
+        tile_carry<M, true>(st, tb, lane, jr, seq, X0, G, cw, X, p.trace, tk);
         IIRG_TRACE(p.trace, tk, 3);
         if (lane < NW) {
             double xw[M];
@@ -1543,294 +1531,10 @@ __global__ void __launch_bounds__(NT, bwd_tdf_min_blocks<M>()) lti_bwd_tdf_kerne
     __syncthreads();
     IIRG_TRACE(p.trace, tk, 5);
     IIRG_TRACE(p.trace, tk, 10);
-    bwd_finalize<T, M, 1>(p, PRE ? nullptr : &cw, ep, tk, seq, jt, tb, s_red);
+    bwd_finalize<T, M, 1>(p, &cw, ep, tk, seq, jt, tb, s_red);
     IIRG_TRACE(p.trace, tk, 11);
     span_exit(p.span);
 }
 
-
-// ---------------------------------------------------------------------------
-// Three-phase mode (multi-wave shapes: more tiles than resident CTAs).  The
-// single-pass look-back keeps every tile resident in shared memory while it
-// waits for its carry, so once the grid spans several waves the tile lifetime,
-// not HBM, bounds throughput.  Here no CTA ever waits on another:
-//   lti_red_kernel   reads a tile, runs the local pass (a2 / a5) and the warp /
-//                    block scans, and writes the tile aggregate (Eq.10's z of
-//                    the tile) -- a pure streaming pass;
-//   lti_cscan_kernel one CTA per sequence scans the aggregates in fp64 with the
-//                    constant transition Q = A_f^TS (a3 / a6) and writes the
-//                    carry entering every tile, in place;
-//   lti_fwd / lti_bwd kernels with PRE = true re-read the tile (an L2 hit when
-//                    the working set fits) and emit (a4 / a7 + a8) from the
-//                    precomputed carry.
-struct LtiRedArgs {
-    const void* src;                          // forward: x; backward: grad_y (NULL = zero)
-    const void* b; const void* a; int64_t coef_stride;
-    const double* tab; int64_t tab_stride;
-    double* car;                              // out: tile aggregates [B][ntiles][M], scan order
-    int64_t B, Tlen; int ntiles; int vec;
-    unsigned long long* span;                 // debug: kernel span
-};
-
-// Persistent and double-buffered: a CTA walks tiles blockIdx.x, +gridDim.x, ...
-// and has the next tile's load in flight while it computes the current one.
-template <typename T, int M> struct RedSmem {
-    static constexpr size_t tile_bytes = ((size_t)Smem<T, M>::PT * sizeof(T) + 15) / 16 * 16;
-    static constexpr size_t bytes() { return Smem<T, M>::tab_bytes + 2 * tile_bytes; }
-};
-
-template <typename T, int M, int FORM, bool BWD>
-__global__ void __launch_bounds__(NT) lti_red_kernel(const LtiRedArgs p) {
-    constexpr int L = Chunk<T, M>::L, TS = NT * L, W = Vec<T>::W;
-    using V = typename Vec<T>::type;
-    using SM = Smem<T, M>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double* st = reinterpret_cast<double*>(smem_raw);
-    T* buf[2] = {reinterpret_cast<T*>(smem_raw + SM::tab_bytes),
-                 reinterpret_cast<T*>(smem_raw + SM::tab_bytes + RedSmem<T, M>::tile_bytes)};
-    __shared__ double s_agg[NW][M];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t ntot = p.B * (int64_t)p.ntiles;
-    auto issue = [&](int64_t t, T* dst) {
-        const int64_t seq = t % p.B;
-        const int j = (int)(t / p.B);                                  // scan order
-        const int64_t p0 = BWD ? p.Tlen - (int64_t)(j + 1) * TS : (int64_t)j * TS;
-        if (p.src != nullptr) tile_load_async<T, TS>(dst, static_cast<const T*>(p.src) + seq * p.Tlen, p0, p.Tlen, p.vec);
-        else for (int e = tid; e < TS; e += NT) dst[pidx<T>(e)] = T(0);
-    };
-    span_enter(p.span);
-    int64_t t = blockIdx.x;
-    if (t < ntot) issue(t, buf[0]);
-    cp_async_commit();
-    if (!BWD) pdl_wait();                      // forward: the prologue's tables
-    pdl_launch_dependents();                   // the carry scan may become resident (it waits for this grid)
-    int64_t staged = -1;                       // coefficient set whose tables are in `st`
-    T bc[M + 1], ac[M + 1];
-    for (int it = 0; t < ntot; t += gridDim.x, ++it) {
-        T* xs = buf[it & 1];
-        const int64_t seq = t % p.B;
-        const int j = (int)(t / p.B);
-        if (t + gridDim.x < ntot) issue(t + gridDim.x, buf[(it + 1) & 1]);
-        cp_async_commit();
-        const int64_t cset = p.tab_stride != 0 ? seq : 0;
-        if (cset != staged) {                  // SHARED: once; PER_SEQ: when the set changes
-            __syncthreads();                   // warp 0 may still read the previous tables
-            const double* tb = p.tab + cset * p.tab_stride;
-            stage_small<M>(st, tb);
-            if constexpr (!BWD) {
-                raw_coefs<T, M>(static_cast<const T*>(p.b) + cset * p.coef_stride,
-                                static_cast<const T*>(p.a) + cset * p.coef_stride, bc, ac);
-            } else {
-                T cc[M];
-                load_coefs<T, M>(tb, bc, ac, cc);
-            }
-            staged = cset;
-        }
-        cp_async_wait<1>();                    // this tile (the next one stays in flight)
-        __syncthreads();
-        double S[M];
-        if constexpr (!BWD) {                  // a2: local forward pass from the zero state
-            const int s0 = tid * L;
-            T v[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) v[i] = T(0);
-#pragma unroll
-            for (int g = 0; g < L / W; ++g) {
-                const V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
-#pragma unroll
-                for (int e = 0; e < W; ++e) { T du; fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, du); }
-            }
-#pragma unroll
-            for (int i = 0; i < M; ++i) S[i] = (double)v[i];
-        } else {                               // a5: local adjoint pass, chunk NT-1-tid walked backwards
-            const int s0 = (NT - 1 - tid) * L;
-            T d[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) d[i] = T(0);
-#pragma unroll
-            for (int g = L / W - 1; g >= 0; --g) {
-                const V dv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
-#pragma unroll
-                for (int e = W - 1; e >= 0; --e) {
-                    if constexpr (FORM == 1) adj_tdf_step<T, M>(d, vget(dv, e), ac);
-                    else (void)adj_df_step<T, M>(d, vget(dv, e), bc, ac);
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < M; ++i) S[i] = (double)d[i];
-        }
-        warp_scan<M, BWD>(st, lane, S);
-        if (lane == 31) {
-#pragma unroll
-            for (int i = 0; i < M; ++i) s_agg[warp][i] = S[i];
-        }
-        __syncthreads();                       // also: every thread is done reading xs
-        if (warp == 0) {
-            double Jex[M], G[M];
-            block_scan<M, BWD>(st, lane, s_agg, Jex, G);
-            if (lane == 0) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) __stcg(p.car + (seq * p.ntiles + j) * M + i, G[i]);
-            }
-        }
-    }
-    cp_async_wait<0>();
-    // backward: the emit kernel reads the forward's y / u and reaches this grid
-    // only through the carry scan, so this grid completes after the forward
-    if (BWD) pdl_wait();
-    span_exit(p.span);
-}
-
-struct LtiScanArgs {
-    double* car;                              // in: tile aggregates; out: carry entering each tile (in place)
-    const void* x0;                           // initial state: zi (forward) / grad_zf (backward), (B, M); NULL = 0
-    const double* tab; int64_t tab_stride;
-    int64_t B; int ntiles;
-    unsigned long long* span;                 // debug: kernel span
-    unsigned long long* trace;                // debug: phase stamps of sequence 0
-};
-
-// a3 / a6 across tiles: X_0 = x0, X_{t+1} = Q X_t + G_t with Q = A_f^TS (or its
-// transpose), one CTA of CS_NT threads per sequence.  Thread r owns a run of
-// RUN (a power of two) consecutive tiles and folds them by Horner (thread 0
-// of a pass starts from the entering state); the runs are scanned over the
-// warp with Q^(RUN 2^d), the warp totals over the CTA with Q^(32 RUN 2^d),
-// and warps >= 1 fold their entering state into lane 0 and scan again, so only
-// powers Q^(2^k) are needed (the prologue's tables, staged in one round trip).
-// Every thread then walks its run writing X_t.  fp64, fixed order (bitwise
-// reproducible); passes of CS_NT RUN tiles chain through the pass carry.
-constexpr int CS_KP = 13;                                      // tables Q^(2^k), k < CS_KP
-template <int M> constexpr int cs_nt() { return M <= 4 ? 512 : 256; }   // register budget of the high orders
-template <typename T, int M, bool TR>
-__global__ void __launch_bounds__(cs_nt<M>()) lti_cscan_kernel(const LtiScanArgs p) {
-    using TB = Tab<M>;
-    constexpr int CS_NT = cs_nt<M>(), CS_NW = CS_NT / 32, CS_LOGW = CS_NW == 16 ? 4 : 3;
-    constexpr int M2 = M * M, RMAX = 16, RB = (32 / M) < 16 ? (32 / M) : 16;
-    __shared__ __align__(16) double s_P[CS_KP][M2];
-    __shared__ double s_w[CS_NW][M];
-    __shared__ double s_y[CS_NW + 1][M];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t seq = blockIdx.x;
-    const int64_t ntiles = p.ntiles;
-    span_enter(p.span);
-    unsigned long long* tr = (seq == 0) ? p.trace : nullptr;
-    IIRG_TRACE(tr, 0, 0);
-    int lrun = 0;
-    while ((1 << lrun) < RMAX && ((int64_t)CS_NT << lrun) < ntiles) ++lrun;
-    const int RUN = 1 << lrun;
-    // tables first (they come from the prologue, complete before the reduce kernel ran)
-    const double* PQ = p.tab + seq * p.tab_stride + TB::PQ;       // [l][i][j][k]: A_f^(k 32^l TS)
-    for (int w = tid; w < CS_KP * M2; w += CS_NT) {
-        const int k = w / M2, e = w % M2;
-        s_P[k][e] = ((int64_t)1 << k) < ntiles ? __ldg(PQ + ((k / 5) * M2 + e) * 32 + (1 << (k % 5))) : 0.0;
-    }
-    pdl_wait();                                // tile aggregates of the reduce kernel
-    pdl_launch_dependents();
-    IIRG_TRACE(tr, 0, 1);
-    if (tid < M) s_y[0][tid] = p.x0 != nullptr ? (double)static_cast<const T*>(p.x0)[seq * M + tid] : 0.0;
-    double* car = p.car + seq * ntiles * M;
-    __syncthreads();
-    IIRG_TRACE(tr, 0, 2);
-    for (int64_t base = 0; base < ntiles; base += (int64_t)CS_NT * RUN) {
-        const int64_t t0 = base + (int64_t)tid * RUN;
-        const int nt = (int)max((int64_t)0, min((int64_t)RUN, ntiles - t0));
-        const int64_t ntp = min((int64_t)CS_NT * RUN, ntiles - base);   // tiles in this pass
-        double R[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) R[i] = tid == 0 ? s_y[0][i] : 0.0;
-        for (int j0 = 0; j0 < nt; j0 += RB) {
-            double G[RB][M];
-#pragma unroll
-            for (int r = 0; r < RB; ++r)
-#pragma unroll
-                for (int i = 0; i < M; ++i) G[r][i] = (j0 + r < nt) ? car[(t0 + j0 + r) * M + i] : 0.0;
-#pragma unroll
-            for (int r = 0; r < RB; ++r) {
-                if (j0 + r < nt) {
-                    mv_acc_s<M, TR>(s_P[0], R, G[r]);                // R <- Q R + G
-#pragma unroll
-                    for (int i = 0; i < M; ++i) R[i] = G[r][i];
-                }
-            }
-        }
-        if (base == 0) IIRG_TRACE(tr, 0, 3);
-        // warp scan of the runs (inclusive); warp 0's already include the entering state
-        auto warp_ks = [&](double (&S)[M]) {
-#pragma unroll
-            for (int d = 0; d < 5; ++d) {
-                const int off = 1 << d;
-                double O[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) O[i] = shfl_up_d(S[i], off);
-                if (lane >= off && ((int64_t)RUN << d) < ntp) mv_acc_s<M, TR>(s_P[lrun + d], O, S);
-            }
-        };
-        double S[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) S[i] = R[i];
-        warp_ks(S);
-        if (lane == 31) {
-#pragma unroll
-            for (int i = 0; i < M; ++i) s_w[warp][i] = S[i];
-        }
-        __syncthreads();
-        if (warp == 0) {                       // warp totals -> state after each warp (lane w: after warp w)
-            double Wv[M];
-#pragma unroll
-            for (int i = 0; i < M; ++i) Wv[i] = lane < CS_NW ? s_w[lane][i] : 0.0;
-#pragma unroll
-            for (int d = 0; d < CS_LOGW; ++d) {
-                const int off = 1 << d;
-                double O[M];
-#pragma unroll
-                for (int i = 0; i < M; ++i) O[i] = shfl_up_d(Wv[i], off);
-                if (lane >= off && ((int64_t)32 * RUN << d) < ntp) mv_acc_s<M, TR>(s_P[lrun + 5 + d], O, Wv);
-            }
-            if (lane < CS_NW) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) s_y[lane + 1][i] = Wv[i];
-            }
-        }
-        __syncthreads();
-        if (base == 0) IIRG_TRACE(tr, 0, 4);
-        double Yw[M];
-#pragma unroll
-        for (int i = 0; i < M; ++i) Yw[i] = s_y[warp][i];
-        if (warp > 0 && (int64_t)warp * 32 * RUN < ntp) {   // fold the entering state into lane 0, scan again
-            if (lane == 0) mv_acc_s<M, TR>(s_P[lrun], Yw, R);
-#pragma unroll
-            for (int i = 0; i < M; ++i) S[i] = R[i];
-            warp_ks(S);
-        }
-        double X[M];                           // state entering this thread's run
-#pragma unroll
-        for (int i = 0; i < M; ++i) { X[i] = shfl_up_d(S[i], 1); if (lane == 0) X[i] = Yw[i]; }
-        if (nt > 0) {
-            for (int j0 = 0; j0 < nt; j0 += RB) {
-                double G[RB][M];
-#pragma unroll
-                for (int r = 0; r < RB; ++r)
-#pragma unroll
-                    for (int i = 0; i < M; ++i) G[r][i] = (j0 + r < nt) ? car[(t0 + j0 + r) * M + i] : 0.0;
-#pragma unroll
-                for (int r = 0; r < RB; ++r) {
-                    if (j0 + r < nt) {
-#pragma unroll
-                        for (int i = 0; i < M; ++i) car[(t0 + j0 + r) * M + i] = X[i];
-                        mv_acc_s<M, TR>(s_P[0], X, G[r]);            // X_{t+1} = Q X_t + G_t
-#pragma unroll
-                        for (int i = 0; i < M; ++i) X[i] = G[r][i];
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        if (base == 0) IIRG_TRACE(tr, 0, 5);
-        if (tid < M) s_y[0][tid] = s_y[CS_NW][tid];                  // pass carry (read only if a pass follows)
-        __syncthreads();
-    }
-    IIRG_TRACE(tr, 0, 6);
-    span_exit(p.span);
-}
 
 }  // namespace iirg

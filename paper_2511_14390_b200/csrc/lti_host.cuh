@@ -31,46 +31,22 @@ inline void launch_pdl(K kernel, unsigned grid, unsigned block, size_t smem, cud
 template <typename T, int M, int FORM>
 struct LtiOps {
     using SM = Smem<T, M>;
+    // the max-dynamic-smem attribute is per device: set once for every device that calls in
     static void attrs() {
-        static std::once_flag once;
-        std::call_once(once, [] {
-            set_smem(lti_prep_kernel<T, M, FORM>, PrepSlots<M>::bytes());
-            set_smem(lti_fwd_kernel<T, M, FORM>, SM::fwd(FORM));
-            set_smem(lti_fwd_kernel<T, M, FORM, true>, SM::fwd(FORM));
-            set_smem(lti_red_kernel<T, M, FORM, false>, RedSmem<T, M>::bytes());
-            set_smem(lti_red_kernel<T, M, FORM, true>, RedSmem<T, M>::bytes());
-            set_smem(lti_bwd_kernel<T, M, FORM>, SM::bwd(FORM));
-            set_smem(lti_bwd_kernel<T, M, FORM, true>, SM::bwd(FORM));
-            if constexpr (FORM == 1) {
-                set_smem(lti_bwd_tdf_kernel<T, M>, SM::bwd_tdf());
-                set_smem(lti_bwd_tdf_kernel<T, M, true>, SM::bwd_tdf());
-            }
-        });
+        static std::mutex mu;
+        static bool done[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(mu);
+        if (done[dev & 63]) return;
+        set_smem(lti_prep_kernel<T, M, FORM>, PrepSlots<M>::bytes());
+        set_smem(lti_fwd_kernel<T, M, FORM>, SM::fwd(FORM));
+        set_smem(lti_bwd_kernel<T, M, FORM>, SM::bwd(FORM));
+        if constexpr (FORM == 1) set_smem(lti_bwd_tdf_kernel<T, M>, SM::bwd_tdf());
+        done[dev & 63] = true;
     }
-    // Persistent grid of the reduce kernel: every resident slot, at most one CTA per tile.
-    static unsigned red_grid(int64_t ntot) {
-        static int64_t cap = 0;
-        static std::once_flag once;
-        std::call_once(once, [] {
-            int dev = 0, sms = 0, per = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, lti_red_kernel<T, M, FORM, false>, NT,
-                                                          RedSmem<T, M>::bytes());
-            cap = (int64_t)sms * (per > 0 ? per : 1);
-        });
-        return (unsigned)(ntot < cap ? ntot : cap);
-    }
-    // Schedule (iir_flags_t).  Default: single pass.  Measured on B200 (DESIGN.md
-    // §6), three-phase lost at every BASELINE shape: its extra pass over the data
-    // costs more issue slots than the look-back waits it removes (C2 44.6 vs 35.5,
-    // C4 181.6 vs 186.2, C5 252 vs 231 us/step), so it is opt-in only.
-    static bool three_phase(const iir_desc_t* d, const Layout&) {
-        if (d->flags & IIR_FLAG_SINGLE_PASS) return false;
-        return (d->flags & IIR_FLAG_THREE_PHASE) != 0;
-    }
-    // a1 prologue, then the scan (PDL throughout: each kernel's loads and local
-    // pass overlap its predecessor; it waits before reading the predecessor's output)
+    // a1 prologue, then the single-pass scan (PDL: each kernel's tile loads overlap its
+    // predecessor's tail; it waits before reading the predecessor's output)
     static iir_status_t forward(const iir_desc_t* d, const Layout& L, const void* b, const void* a,
                                 const LtiFwdArgs& fa, cudaStream_t st) {
         attrs();
@@ -81,47 +57,15 @@ struct LtiOps {
                 Tab<M>::SIZE, L.nlev, fa.span == nullptr ? nullptr : fa.span - 2);
         });
         if (s != IIR_OK) return s;
-        if (!three_phase(d, L))
-            return launch(K_LTI_FWD, st, [&] {
-                launch_pdl(lti_fwd_kernel<T, M, FORM>, (unsigned)L.ntot, NT, SM::fwd(FORM), st, fa);
-            });
-        unsigned long long* dbg = fa.span == nullptr ? nullptr : fa.span - 2;   // [prep][fwd][bwd] spans, then ours
-        const LtiRedArgs ra{fa.x, b, a, cstride, fa.tab, fa.tab_stride, fa.car, fa.B, fa.Tlen, fa.ntiles, fa.vec,
-                            dbg == nullptr ? nullptr : dbg + 8};
-        s = launch(K_LTI_RED_F, st, [&] {
-            launch_pdl(lti_red_kernel<T, M, FORM, false>, red_grid(L.ntot), NT, RedSmem<T, M>::bytes(), st, ra);
-        });
-        if (s != IIR_OK) return s;
-        const LtiScanArgs sa{fa.car, fa.zi, fa.tab, fa.tab_stride, fa.B, fa.ntiles,
-                             dbg == nullptr ? nullptr : dbg + 10, dbg == nullptr ? nullptr : dbg + 16};
-        s = launch(K_LTI_CSCAN, st, [&] { launch_pdl(lti_cscan_kernel<T, M, false>, (unsigned)fa.B, cs_nt<M>(), 0, st, sa); });
-        if (s != IIR_OK) return s;
         return launch(K_LTI_FWD, st, [&] {
-            launch_pdl(lti_fwd_kernel<T, M, FORM, true>, (unsigned)L.ntot, NT, SM::fwd(FORM), st, fa);
+            launch_pdl(lti_fwd_kernel<T, M, FORM>, (unsigned)L.ntot, NT, SM::fwd(FORM), st, fa);
         });
     }
-    static iir_status_t backward(const iir_desc_t* d, const Layout& L, const LtiBwdArgs& ba, cudaStream_t st) {
+    static iir_status_t backward(const iir_desc_t*, const Layout& L, const LtiBwdArgs& ba, cudaStream_t st) {
         attrs();
-        if (!three_phase(d, L))
-            return launch(K_LTI_BWD, st, [&] {
-                if constexpr (FORM == 1) launch_pdl(lti_bwd_tdf_kernel<T, M>, (unsigned)L.ntot, NT, SM::bwd_tdf(), st, ba);
-                else lti_bwd_kernel<T, M, FORM><<<(unsigned)L.ntot, NT, SM::bwd(FORM), st>>>(ba);
-            });
-        unsigned long long* dbg = ba.span == nullptr ? nullptr : ba.span - 4;
-        const LtiRedArgs ra{ba.gy, nullptr, nullptr, 0, ba.tab, ba.tab_stride, ba.car, ba.B, ba.Tlen, ba.ntiles, ba.vec,
-                            dbg == nullptr ? nullptr : dbg + 12};
-        iir_status_t s = launch(K_LTI_RED_B, st, [&] {
-            launch_pdl(lti_red_kernel<T, M, FORM, true>, red_grid(L.ntot), NT, RedSmem<T, M>::bytes(), st, ra);
-        });
-        if (s != IIR_OK) return s;
-        const LtiScanArgs sa{ba.car, ba.gzf, ba.tab, ba.tab_stride, ba.B, ba.ntiles,
-                             dbg == nullptr ? nullptr : dbg + 14, dbg == nullptr ? nullptr : dbg + 32};
-        s = launch(K_LTI_CSCAN, st, [&] { launch_pdl(lti_cscan_kernel<T, M, true>, (unsigned)ba.B, cs_nt<M>(), 0, st, sa); });
-        if (s != IIR_OK) return s;
         return launch(K_LTI_BWD, st, [&] {
-            if constexpr (FORM == 1)
-                launch_pdl(lti_bwd_tdf_kernel<T, M, true>, (unsigned)L.ntot, NT, SM::bwd_tdf(), st, ba);
-            else launch_pdl(lti_bwd_kernel<T, M, FORM, true>, (unsigned)L.ntot, NT, SM::bwd(FORM), st, ba);
+            if constexpr (FORM == 1) launch_pdl(lti_bwd_tdf_kernel<T, M>, (unsigned)L.ntot, NT, SM::bwd_tdf(), st, ba);
+            else lti_bwd_kernel<T, M, FORM><<<(unsigned)L.ntot, NT, SM::bwd(FORM), st>>>(ba);
         });
     }
 };

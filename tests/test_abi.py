@@ -91,3 +91,19 @@ def test_state_carry_rejects_bad_arguments_before_launch():
     d_ss = B.make_desc(2, 100, 2, "ss", B.IIR_F32, B.IIR_COEF_SHARED)
     assert L.iir_state_carry(ctypes.byref(d_ss), fake, fake, 2, 0, 10, 0, fake, None) == B.IIR_EUNSUPPORTED
     assert B.iir_launch_count() == n0
+
+
+def test_removed_three_phase_flag_rejected():
+    """The three-phase LTI schedule lost on every measured shape and was removed (ABI 2)."""
+    d = B.make_desc(2, 100, 2, "tdf", B.IIR_F32, B.IIR_COEF_SHARED, flags=B.IIR_FLAG_THREE_PHASE_REMOVED)
+    assert B.iir_tape_bytes(d) == 0
+    L = B.lib()
+    assert L.iir_forward(ctypes.byref(d), 8, 8, 8, None, 8, None, 8, 1 << 30, 8, 1 << 30, None) == B.IIR_EUNSUPPORTED
+
+
+def test_engine_flags_accepted_and_layouts_sized():
+    """fp32 TDF: both engines have a valid tape / workspace for every order."""
+    for M in range(1, 9):
+        for fl in (0, B.IIR_FLAG_LEGACY_LTI, B.IIR_FLAG_ENGINE_V2, B.IIR_FLAG_GRAD_Y_EARLY):
+            d = B.make_desc(3, 5000, M, "tdf", B.IIR_F32, B.IIR_COEF_SHARED, flags=fl)
+            assert B.iir_tape_bytes(d) > 0 and B.iir_workspace_bytes(d) > 0, (M, fl)

@@ -18,6 +18,8 @@ pytestmark = pytest.mark.gpu
 
 def _bufs(p, flags=0):
     td = torch.float32 if p["dtype"] == "f32" else torch.float64
+    if p["form"] == "tdf" and p["dtype"] == "f32":
+        flags |= B.IIR_FLAG_ENGINE_V2                  # the round-2 engine (the default only from order 6)
     x, b, a, zi, gy, gzf = (to_dev(p[k], td) for k in ("x", "b", "a", "zi", "gy", "gzf"))
     Bsz, T = x.shape
     M = b.shape[-1] - 1
@@ -150,7 +152,7 @@ def test_negative_control_flags_wrong_results():
     computed with a coefficient perturbed in its 4th significant digit, fails it."""
     p = inputs.lti_problem(8600, form="tdf", order=4, batch=4, length=3 * 2048, dtype="f32", angles="spread")
     o = run_lti_oracle(p)
-    g = run_lti_gpu(p)
+    g = run_lti_gpu(p, flags=B.IIR_FLAG_ENGINE_V2)
     errs, bad = compare(g, o, TOL["f32"])
     assert not bad, errs                                         # the real result passes
     for k in ("y", "gx", "gb", "ga", "gzi", "zf"):
@@ -161,7 +163,7 @@ def test_negative_control_flags_wrong_results():
         assert k in bad, f"a corrupted {k} passed the gate"
     q = dict(p, a=p["a"].copy())
     q["a"][1] *= 1.0 + 1e-3                                      # a wrong filter on the GPU side
-    gw = run_lti_gpu(q)
+    gw = run_lti_gpu(q, flags=B.IIR_FLAG_ENGINE_V2)
     _, bad = compare(gw, o, TOL["f32"])
     assert {"y", "gx"} <= set(bad), bad
 

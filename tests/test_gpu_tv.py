@@ -61,7 +61,7 @@ def test_config3_shape_lpc24_fp32():
     check(p, "f32")
 
 
-@pytest.mark.parametrize("M", [1, 2, 3, 4, 8, 12, 16, 24, 31])
+@pytest.mark.parametrize("M", [1, 2, 3, 4, 8, 9, 11, 12, 13, 16, 17, 18, 21, 24, 25, 27, 30, 31])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_orders(M, dtype):
     p = inputs.tv_allpole_problem(2100 + M, batch=3, length=5 * 512 + 37, order=M, dtype=dtype, hop=128)
@@ -79,9 +79,12 @@ def test_no_initial_conditions():
     check(p, "f32")
 
 
-def test_unsupported_order_rejected():
-    d = B.make_desc(1, 100, 9, "df", torch.float32, B.IIR_COEF_PER_SAMPLE)
-    assert B.iir_tape_bytes(d) == 0
+def test_every_order_up_to_31_supported_32_rejected():
+    """Every per-sample order 1..31 is compiled (the Phi kernel holds one lane per basis
+    state plus one for the input, so 31 is the largest); 32 is rejected before any launch."""
+    for M in range(1, 32):
+        assert B.iir_tape_bytes(B.make_desc(1, 100, M, "df", torch.float32, B.IIR_COEF_PER_SAMPLE)) > 0, M
+    assert B.iir_tape_bytes(B.make_desc(1, 100, 32, "df", torch.float32, B.IIR_COEF_PER_SAMPLE)) == 0
 
 
 def test_autograd_allpole_tv():

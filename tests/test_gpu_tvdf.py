@@ -54,7 +54,7 @@ def check(p, dtype, tol=None, want=("y", "zf", "gx", "gb", "ga", "gzi")):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-@pytest.mark.parametrize("M", [1, 2, 4, 8, 24])
+@pytest.mark.parametrize("M", [1, 2, 4, 8, 9, 15, 24, 31])
 def test_orders_dtypes(dtype, M):
     p = inputs.tv_df_problem(31000 + M, batch=3, length=3 * 512 + 37, order=M, dtype=dtype, hop=128)
     check(p, dtype)
