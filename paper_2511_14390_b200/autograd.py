@@ -209,10 +209,11 @@ def lfilter_tv(x, b, a, zi=None, return_zf=False):
 
 class LTIMatrixRecurrenceFunction(torch.autograd.Function):
     """v(1..N) = recurrence(A, v0, z): v(n+1) = A v(n) + z(n) (PAPER.md:296-343,
-    Listing 1), batched: z (B, N, M), v0 (B, M), A (M, M) shared or (B, M, M)."""
+    Listing 1), batched: z (B, N, M), v0 (B, M), A (M, M) shared or (B, M, M).
+    diag=True runs the paper's Diag-EXT variant (orders 1-2)."""
 
     @staticmethod
-    def forward(ctx, A, v0, z):
+    def forward(ctx, A, v0, z, diag=False):
         _require_cuda(A, v0, z)
         if z.dim() != 3 or A.dim() not in (2, 3):
             raise ValueError("matrix_recurrence: z must be (B, N, M), A (M, M) or (B, M, M)")
@@ -220,7 +221,7 @@ class LTIMatrixRecurrenceFunction(torch.autograd.Function):
         _check(z, [("A", A, [(M, M)] if A.dim() == 2 else [(Bsz, M, M)]), ("v0", v0, [(Bsz, M)])])
         A, v0, z = _c(A), _c(v0), _c(z)
         mode = B.IIR_COEF_SHARED if A.dim() == 2 else B.IIR_COEF_PER_SEQ
-        desc = B.make_desc(Bsz, N, M, "ss", z.dtype, mode)
+        desc = B.make_desc(Bsz, N, M, "ss", z.dtype, mode, flags=B.IIR_FLAG_DIAG if diag else 0)
         v = torch.empty_like(z)
         tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
         tape = torch.empty(tb, dtype=torch.uint8, device=z.device)
@@ -246,9 +247,11 @@ class LTIMatrixRecurrenceFunction(torch.autograd.Function):
         with torch.cuda.device(v.device):
             B.iir_backward(desc, gv, None, None, A, None, v, v0, tape, tape.numel(), gz, None, gA, gv0, ws, wb,
                            _stream(v))
-        return gA, gv0, gz
+        return gA, gv0, gz, None
 
 
-def matrix_recurrence(A, v0, z):
-    """Differentiable batched v(n+1) = A v(n) + z(n); returns v(1..N) (B, N, M)."""
-    return LTIMatrixRecurrenceFunction.apply(A, v0, z)
+def matrix_recurrence(A, v0, z, diag=False):
+    """Differentiable batched v(n+1) = A v(n) + z(n); returns v(1..N) (B, N, M).
+    diag=True: Diag-EXT (eigen-basis element-wise recursions, dense fallback for a
+    defective or ill-conditioned A), orders 1 and 2."""
+    return LTIMatrixRecurrenceFunction.apply(A, v0, z, diag)

@@ -28,7 +28,8 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
 
 // ------------------------------------------------------- instrumentation ----
 static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_phi", "tv_chain", "tv_fwd",
-                                        "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd", "state_carry", "tv_fir"};
+                                        "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd", "state_carry", "tv_fir",
+                                        "diag_prep", "diag_agg", "diag_scan", "diag_emit"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;
@@ -127,9 +128,13 @@ static iir_status_t check_desc(const iir_desc_t* d) {
         if (d->coef_mode != IIR_COEF_SHARED && d->coef_mode != IIR_COEF_PER_SEQ)
             return fail(IIR_EUNSUPPORTED, "bare recurrence: A is SHARED or PER_SEQ");
         if (d->order < 1 || d->order > 4) return fail(IIR_EUNSUPPORTED, "bare recurrence: order must be 1..4");
+        if ((d->flags & IIR_FLAG_DIAG) && d->order > 2)
+            return fail(IIR_EUNSUPPORTED, "Diag-EXT (IIR_FLAG_DIAG): order must be 1 or 2 (closed-form eigenbasis)");
     }
     if (d->flags & IIR_FLAG_THREE_PHASE_REMOVED)
         return fail(IIR_EUNSUPPORTED, "the three-phase LTI schedule was removed (it lost on every measured shape)");
+    if ((d->flags & IIR_FLAG_DIAG) && d->form != IIR_SS)
+        return fail(IIR_EINVAL, "IIR_FLAG_DIAG applies to the bare recurrence (form IIR_SS)");
     if ((d->flags & IIR_FLAG_PER_SAMPLE_B) && d->coef_mode != IIR_COEF_PER_SAMPLE)
         return fail(IIR_EINVAL, "IIR_FLAG_PER_SAMPLE_B needs IIR_COEF_PER_SAMPLE");
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) {
@@ -149,7 +154,26 @@ static iir_status_t check_desc(const iir_desc_t* d) {
     return IIR_OK;
 }
 
+static Layout diag_layout(const iir_desc_t* d) {
+    Layout L;
+    const int M = d->order;
+    L.ncoef = d->coef_mode == IIR_COEF_SHARED ? 1 : d->batch;
+    L.ntiles = (d->length + diag_chunk() - 1) / diag_chunk();        // chunks per sequence
+    L.ntot = L.ntiles * d->batch;
+    size_t o = 256;                                                  // (counters block unused; error word)
+    L.ws_err = 64;
+    L.ws_clear = 256;
+    L.ws_part = o; o += al256((size_t)L.ntot * 2 * M * 8);         // chunk aggregates (complex)
+    L.ws_part2 = o; o += al256((size_t)L.ntot * 2 * M * 8);        // carries entering each chunk
+    L.ws_psi = o; o += al256((size_t)L.ntot * M * M * 8);          // grad_A partial sums per chunk
+    L.ws_bytes = o;
+    L.tp_tab = 0;
+    L.tp_bytes = al256((size_t)L.ncoef * diag_tab_doubles(M) * 8);
+    return L;
+}
+
 static Layout layout(const iir_desc_t* d) {
+    if (d->form == IIR_SS && (d->flags & IIR_FLAG_DIAG)) return diag_layout(d);
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) return tv_layout(d);
     Layout L;
     const int M = d->order;
@@ -327,6 +351,10 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     fa.B = d->batch; fa.Tlen = d->length; fa.ntiles = (int)L.ntiles; fa.vec = vec;
     fa.trace = g_trace;
     fa.span = g_trace == nullptr ? nullptr : g_trace + L.ntot * 16 + 2;   // [prep][fwd][bwd]
+    if (d->form == IIR_SS && (d->flags & IIR_FLAG_DIAG))
+        return diag_run(true, d, a, x, zi, y, nullptr, nullptr, nullptr, nullptr, nullptr,
+                        reinterpret_cast<double*>(t + L.tp_tab), reinterpret_cast<double*>(w + L.ws_part),
+                        reinterpret_cast<double*>(w + L.ws_part2), reinterpret_cast<double*>(w + L.ws_psi), st);
     if (d->form == IIR_SS) {
         fa.coef_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : (int64_t)d->order * d->order;
         return rec_run(true, d->dtype, d->order, L, fa, LtiBwdArgs{}, st);
@@ -415,6 +443,11 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     ba.trace = g_trace;
     ba.span = g_trace == nullptr ? nullptr : g_trace + L.ntot * 16 + 4;
     (void)b;
+    if (d->form == IIR_SS && (d->flags & IIR_FLAG_DIAG))
+        return diag_run(false, d, a, nullptr, zi, nullptr, grad_y, y, grad_x, grad_a, grad_zi,
+                        reinterpret_cast<double*>(const_cast<char*>(t) + L.tp_tab),
+                        reinterpret_cast<double*>(w + L.ws_part), reinterpret_cast<double*>(w + L.ws_part2),
+                        reinterpret_cast<double*>(w + L.ws_psi), st);
     if (d->form == IIR_SS) {
         ba.a = a;
         ba.coef_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : (int64_t)d->order * d->order;

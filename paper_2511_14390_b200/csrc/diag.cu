@@ -1,0 +1,472 @@
+// diag.cu -- SURVEY 8(f) f3: the paper's Diag-EXT variant of the bare recurrence
+// (form IIR_SS with IIR_FLAG_DIAG; Eq.4 and Listing 1,
+// PAPER.md:60-63, 296-343), orders M = 1, 2 (the paper benchmarks M = 2).
+//
+//   A = V diag(lam) V^-1  ("decomposing A into diagonal and invertible matrices, reducing
+//   matrix multiplications to element-wise multiplications"):
+//   forward   w = V^-1 v,  w(n+1) = lam * w(n) + V^-1 z(n),  v(n+1) = Re V w(n+1)
+//   backward  h = V^T g,   h(n) = V^T gv(n) + lam * h(n+1),   g(n) = Re V^-T h(n)   (Listing 1's VJP)
+//             grad_z = g,  grad_v0 = A^T g(0),  grad_A = sum_n g(n) v(n)^T  (v(0) = v0)
+// Time parallelism: chunks of DG_C samples per thread, the chunk aggregates scanned per
+// sequence by one warp (Kogge-Stone over 32 chunks with the transition's powers, fp64), then
+// each chunk re-runs from its exact carry-in.  The eigen-decomposition is computed on device
+// (closed form for M <= 2, fp64) by a prologue that also estimates kappa(V) = ||V|| ||V^-1||:
+// a defective or ill-conditioned eigenbasis ("only applicable when A is diagonalisable",
+// PAPER.md:134) falls back, per coefficient set and without a host round trip, to the dense
+// transition (V = I, lam -> A), i.e. the plain recurrence run by the same kernels.
+#include <cuda_runtime.h>
+
+#include "host.h"
+#include "lti.cuh"
+
+namespace iirg {
+namespace dg {
+
+constexpr int DG_C = 256;          // samples per thread chunk
+constexpr int DG_NT = 128;         // threads per CTA of the chunk kernels
+
+template <typename T> struct cx { T r, i; };
+template <typename T> __device__ __forceinline__ cx<T> cmad(cx<T> a, cx<T> b, cx<T> c) {
+    return {fma(a.r, b.r, fma(-a.i, b.i, c.r)), fma(a.r, b.i, fma(a.i, b.r, c.i))};
+}
+
+// Per coefficient set (fp64, in the tape): flag (1 = diagonal basis, 0 = dense fallback),
+// lam[M], V[M][M], Vi[M][M] (complex), A[M][M] (real), and the transition powers used by the
+// carry scan: Pw[d] = X^(DG_C 2^d), d = 0..5, complex M x M (X = diag(lam) or A).
+template <int M> struct Tb {
+    static constexpr int FLAG = 0, LAM = 2, V = LAM + 2 * M, VI = V + 2 * M * M, A = VI + 2 * M * M;
+    static constexpr int PW = A + M * M, SIZE = (PW + 6 * 2 * M * M + 31) / 32 * 32;
+};
+
+// ---- prologue: closed-form eigen-decomposition, conditioning test, powers ------------------
+template <int M>
+__device__ void cmatmul(const double* X, const double* Y, double* Z) {   // complex M x M, interleaved re/im
+    double t[2 * M * M];
+    for (int i = 0; i < M; ++i)
+        for (int j = 0; j < M; ++j) {
+            double re = 0, im = 0;
+            for (int k = 0; k < M; ++k) {
+                const double ar = X[2 * (i * M + k)], ai = X[2 * (i * M + k) + 1];
+                const double br = Y[2 * (k * M + j)], bi = Y[2 * (k * M + j) + 1];
+                re += ar * br - ai * bi;
+                im += ar * bi + ai * br;
+            }
+            t[2 * (i * M + j)] = re;
+            t[2 * (i * M + j) + 1] = im;
+        }
+    for (int e = 0; e < 2 * M * M; ++e) Z[e] = t[e];
+}
+
+template <typename T, int M>
+__global__ void dg_prep_kernel(const T* __restrict__ a, int64_t stride, int64_t nsets, double* __restrict__ tab,
+                               double kmax) {
+    using TB = Tb<M>;
+    const int64_t set = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (set >= nsets) return;
+    const T* A = a + set * stride;
+    double* t = tab + set * TB::SIZE;
+    double Ar[M * M];
+    for (int e = 0; e < M * M; ++e) Ar[e] = (double)A[e];
+    double lr[M], li[M], Vr[M][M], Vim[M][M];
+    bool ok = true;
+    if (M == 1) {
+        lr[0] = Ar[0]; li[0] = 0; Vr[0][0] = 1; Vim[0][0] = 0;
+    } else {
+        const double a0 = Ar[0], b0 = Ar[1], c0 = Ar[2], d0 = Ar[3];
+        const double h = 0.5 * (a0 + d0), disc = 0.25 * (a0 - d0) * (a0 - d0) + b0 * c0;
+        const double s = sqrt(fabs(disc));
+        if (disc >= 0) { lr[0] = h + s; lr[1] = h - s; li[0] = li[1] = 0; }
+        else { lr[0] = lr[1] = h; li[0] = s; li[1] = -s; }
+        for (int k = 0; k < 2; ++k) {                  // eigenvector columns, unit 2-norm
+            double x0r, x0i, x1r, x1i;
+            if (b0 == 0 && c0 == 0) { x0r = k == 0; x1r = k == 1; x0i = x1i = 0; }
+            else if (fabs(b0) >= fabs(c0)) { x0r = b0; x0i = 0; x1r = lr[k] - a0; x1i = li[k]; }
+            else { x0r = lr[k] - d0; x0i = li[k]; x1r = c0; x1i = 0; }
+            const double nrm = sqrt(x0r * x0r + x0i * x0i + x1r * x1r + x1i * x1i);
+            ok = ok && nrm > 0;
+            const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
+            Vr[0][k] = x0r * inv; Vim[0][k] = x0i * inv; Vr[1][k] = x1r * inv; Vim[1][k] = x1i * inv;
+        }
+    }
+    // inverse (M <= 2) and kappa(V) ~ ||V||_F ||V^-1||_F
+    double Wr[M][M], Wi[M][M];
+    if (M == 1) { Wr[0][0] = 1; Wi[0][0] = 0; }
+    else {
+        const double dr = Vr[0][0] * Vr[1][1] - Vim[0][0] * Vim[1][1] - (Vr[0][1] * Vr[1][0] - Vim[0][1] * Vim[1][0]);
+        const double di = Vr[0][0] * Vim[1][1] + Vim[0][0] * Vr[1][1] - (Vr[0][1] * Vim[1][0] + Vim[0][1] * Vr[1][0]);
+        const double den = dr * dr + di * di;
+        ok = ok && den > 0;
+        const double ir = den > 0 ? dr / den : 0, ii = den > 0 ? -di / den : 0;   // 1 / det
+        auto mul = [&](double xr, double xi, double& orr, double& oi) { orr = xr * ir - xi * ii; oi = xr * ii + xi * ir; };
+        mul(Vr[1][1], Vim[1][1], Wr[0][0], Wi[0][0]);
+        mul(-Vr[0][1], -Vim[0][1], Wr[0][1], Wi[0][1]);
+        mul(-Vr[1][0], -Vim[1][0], Wr[1][0], Wi[1][0]);
+        mul(Vr[0][0], Vim[0][0], Wr[1][1], Wi[1][1]);
+    }
+    double nv = 0, nw = 0;
+    for (int i = 0; i < M; ++i)
+        for (int j = 0; j < M; ++j) {
+            nv += Vr[i][j] * Vr[i][j] + Vim[i][j] * Vim[i][j];
+            nw += Wr[i][j] * Wr[i][j] + Wi[i][j] * Wi[i][j];
+        }
+    const double kappa = sqrt(nv * nw);
+    ok = ok && kappa <= kmax && kappa == kappa;
+    // dense fallback: V = V^-1 = I and the transition is A itself
+    t[TB::FLAG] = ok ? 1.0 : 0.0;
+    for (int i = 0; i < M; ++i) {
+        t[TB::LAM + 2 * i] = ok ? lr[i] : 0.0;
+        t[TB::LAM + 2 * i + 1] = ok ? li[i] : 0.0;
+        for (int j = 0; j < M; ++j) {
+            t[TB::V + 2 * (i * M + j)] = ok ? Vr[i][j] : (i == j);
+            t[TB::V + 2 * (i * M + j) + 1] = ok ? Vim[i][j] : 0.0;
+            t[TB::VI + 2 * (i * M + j)] = ok ? Wr[i][j] : (i == j);
+            t[TB::VI + 2 * (i * M + j) + 1] = ok ? Wi[i][j] : 0.0;
+            t[TB::A + i * M + j] = Ar[i * M + j];
+        }
+    }
+    double X[2 * M * M];                               // the transition: diag(lam) or A
+    for (int i = 0; i < M; ++i)
+        for (int j = 0; j < M; ++j) {
+            X[2 * (i * M + j)] = ok ? (i == j ? lr[i] : 0.0) : Ar[i * M + j];
+            X[2 * (i * M + j) + 1] = ok ? (i == j ? li[i] : 0.0) : 0.0;
+        }
+    for (int q = 1; q < DG_C; q *= 2) cmatmul<M>(X, X, X);           // X^C
+    for (int d = 0; d < 6; ++d) {
+        for (int e = 0; e < 2 * M * M; ++e) t[TB::PW + d * 2 * M * M + e] = X[e];
+        cmatmul<M>(X, X, X);
+    }
+}
+
+// ---- chunk kernels ---------------------------------------------------------------------------
+struct Args {
+    const void* a; const void* z; const void* v0; void* v;          // forward
+    const void* gv; const void* vout; void* gz; void* gv0;          // backward
+    const double* tab; int64_t tab_stride, coef_stride;
+    double* agg; double* carry; double* gpart;                      // workspace
+    int64_t B, T; int nch; int ncoef;
+};
+
+template <typename T, int M>
+struct Par {                                                         // one set's parameters in T
+    bool diag;
+    cx<T> lam[M], V[M][M], Vi[M][M];
+    T A[M][M];
+    __device__ void load(const double* t) {
+        using TB = Tb<M>;
+        diag = t[TB::FLAG] != 0.0;
+        for (int i = 0; i < M; ++i) {
+            lam[i] = {(T)t[TB::LAM + 2 * i], (T)t[TB::LAM + 2 * i + 1]};
+            for (int j = 0; j < M; ++j) {
+                V[i][j] = {(T)t[TB::V + 2 * (i * M + j)], (T)t[TB::V + 2 * (i * M + j) + 1]};
+                Vi[i][j] = {(T)t[TB::VI + 2 * (i * M + j)], (T)t[TB::VI + 2 * (i * M + j) + 1]};
+                A[i][j] = (T)t[TB::A + i * M + j];
+            }
+        }
+    }
+};
+
+// one step of the state recursion in the working basis (BWD: the transposed operator)
+template <typename T, int M, bool BWD>
+__device__ __forceinline__ void dg_step(const Par<T, M>& P, cx<T> (&w)[M], const T (&in)[M]) {
+    cx<T> nw[M];
+    if (P.diag) {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            cx<T> acc = {T(0), T(0)};
+#pragma unroll
+            for (int j = 0; j < M; ++j) {                  // projection: V^-1 z (fwd) or V^T gv (bwd)
+                const cx<T> q = BWD ? P.V[j][i] : P.Vi[i][j];
+                acc.r = fma(q.r, in[j], acc.r);
+                acc.i = fma(q.i, in[j], acc.i);
+            }
+            nw[i] = cmad(P.lam[i], w[i], acc);            // element-wise
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            T acc = in[i];
+#pragma unroll
+            for (int j = 0; j < M; ++j) acc = fma(BWD ? P.A[j][i] : P.A[i][j], w[j].r, acc);
+            nw[i] = {acc, T(0)};
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i) w[i] = nw[i];
+}
+// back to the real state: Re V w (fwd) or Re V^-T h (bwd)
+template <typename T, int M, bool BWD>
+__device__ __forceinline__ void dg_out(const Par<T, M>& P, const cx<T> (&w)[M], T (&out)[M]) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+        if (P.diag) {
+            T s = T(0);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const cx<T> q = BWD ? P.Vi[i][k] : P.V[k][i];
+                s = fma(q.r, w[i].r, fma(-q.i, w[i].i, s));
+            }
+            out[k] = s;
+        } else {
+            out[k] = w[k].r;
+        }
+    }
+}
+
+template <typename T, int M>
+__device__ __forceinline__ void ld_vec(const T* p, int64_t idx, T (&v)[M]) {
+#pragma unroll
+    for (int j = 0; j < M; ++j) v[j] = p[idx * M + j];
+}
+
+// phase 1: chunk aggregates from the zero state (forward in time / backward in reverse time)
+template <typename T, int M, bool BWD>
+__global__ void __launch_bounds__(DG_NT) dg_agg_kernel(const Args p) {
+    const int64_t c = (int64_t)blockIdx.x * DG_NT + threadIdx.x;
+    if (c >= p.B * p.nch) return;
+    const int64_t seq = c / p.nch;
+    const int k = (int)(c - seq * p.nch);
+    Par<T, M> P;
+    P.load(p.tab + (p.ncoef > 1 ? seq : 0) * p.tab_stride);
+    // forward chunks start at 0 (the ragged chunk is the last); backward chunks, scanned last to
+    // first, end at T (the ragged chunk is the first in time): every scanned chunk but the final
+    // one spans exactly DG_C samples, the span of the scan's transition X^C
+    const int64_t n0 = BWD ? max((int64_t)0, p.T - (int64_t)(k + 1) * DG_C) : (int64_t)k * DG_C;
+    const int64_t n1 = BWD ? p.T - (int64_t)k * DG_C : min(n0 + DG_C, p.T);
+    const T* in = static_cast<const T*>(BWD ? p.gv : p.z) + seq * p.T * M;
+    cx<T> w[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) w[i] = {T(0), T(0)};
+    if (!BWD) {
+        for (int64_t n = n0; n < n1; ++n) { T zz[M]; ld_vec<T, M>(in, n, zz); dg_step<T, M, false>(P, w, zz); }
+    } else if (in != nullptr) {
+        for (int64_t n = n1 - 1; n >= n0; --n) { T gg[M]; ld_vec<T, M>(in, n, gg); dg_step<T, M, true>(P, w, gg); }
+    }
+    double* o = p.agg + c * 2 * M;
+#pragma unroll
+    for (int i = 0; i < M; ++i) { o[2 * i] = (double)w[i].r; o[2 * i + 1] = (double)w[i].i; }
+}
+
+// phase 2: one warp per sequence scans the chunk aggregates in fp64 (blocks of 32 chunks:
+// Kogge-Stone with X^(C 2^d), the block's carry-in folded into its first chunk) and writes
+// the state entering every chunk (forward: chunk order; backward: reverse chunk order)
+template <int M, bool BWD>
+__device__ __forceinline__ void cmv(const double* P, const double (&v)[2 * M], double (&acc)[2 * M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            const int e = BWD ? (j * M + i) : (i * M + j);     // the transposed operator for the adjoint
+            const double pr = P[2 * e], pi = P[2 * e + 1];
+            acc[2 * i] += pr * v[2 * j] - pi * v[2 * j + 1];
+            acc[2 * i + 1] += pr * v[2 * j + 1] + pi * v[2 * j];
+        }
+}
+
+template <typename T, int M, bool BWD>
+__global__ void __launch_bounds__(32) dg_scan_kernel(const Args p) {
+    using TB = Tb<M>;
+    const int64_t seq = blockIdx.x;
+    const int lane = threadIdx.x;
+    const double* t = p.tab + (p.ncoef > 1 ? seq : 0) * p.tab_stride;
+    const bool diag = t[TB::FLAG] != 0.0;
+    double X[2 * M];                                       // state entering the current block
+#pragma unroll
+    for (int i = 0; i < 2 * M; ++i) X[i] = 0.0;
+    if (!BWD && p.v0 != nullptr) {                         // forward: the projected initial state V^-1 v0
+        const T* v0 = static_cast<const T*>(p.v0) + seq * M;
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+                const double q0 = diag ? t[TB::VI + 2 * (i * M + j)] : (i == j), q1 = diag ? t[TB::VI + 2 * (i * M + j) + 1] : 0.0;
+                X[2 * i] += q0 * (double)v0[j];
+                X[2 * i + 1] += q1 * (double)v0[j];
+            }
+    }
+    for (int b0 = 0; b0 < p.nch; b0 += 32) {
+        const int c = b0 + lane;                                     // scan position
+        const int k = c;                                             // (backward chunk indices run from the end)
+        double S[2 * M];
+#pragma unroll
+        for (int i = 0; i < 2 * M; ++i) S[i] = c < p.nch ? p.agg[(seq * p.nch + k) * 2 * M + i] : 0.0;
+        if (lane == 0) cmv<M, BWD>(t + TB::PW, X, S);              // fold the block's carry-in
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+            double O[2 * M], acc[2 * M];
+#pragma unroll
+            for (int i = 0; i < 2 * M; ++i) { O[i] = __shfl_up_sync(0xffffffffu, S[i], 1 << d); acc[i] = 0.0; }
+            cmv<M, BWD>(t + TB::PW + d * 2 * M * M, O, acc);
+            if (lane >= (1 << d))
+#pragma unroll
+                for (int i = 0; i < 2 * M; ++i) S[i] += acc[i];
+        }
+        double E[2 * M];
+#pragma unroll
+        for (int i = 0; i < 2 * M; ++i) {
+            const double e = __shfl_up_sync(0xffffffffu, S[i], 1);
+            E[i] = lane == 0 ? X[i] : e;
+        }
+        if (c < p.nch)
+#pragma unroll
+            for (int i = 0; i < 2 * M; ++i) p.carry[(seq * p.nch + k) * 2 * M + i] = E[i];
+#pragma unroll
+        for (int i = 0; i < 2 * M; ++i) X[i] = __shfl_sync(0xffffffffu, S[i], 31);
+    }
+}
+
+// phase 3, forward: re-run every chunk from its carry-in, v(n+1) = Re V w(n+1)
+template <typename T, int M>
+__global__ void __launch_bounds__(DG_NT) dg_fwd_emit_kernel(const Args p) {
+    const int64_t c = (int64_t)blockIdx.x * DG_NT + threadIdx.x;
+    if (c >= p.B * p.nch) return;
+    const int64_t seq = c / p.nch;
+    const int k = (int)(c - seq * p.nch);
+    Par<T, M> P;
+    P.load(p.tab + (p.ncoef > 1 ? seq : 0) * p.tab_stride);
+    cx<T> w[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) w[i] = {(T)p.carry[c * 2 * M + 2 * i], (T)p.carry[c * 2 * M + 2 * i + 1]};
+    const int64_t n0 = (int64_t)k * DG_C, n1 = min(n0 + DG_C, p.T);
+    const T* z = static_cast<const T*>(p.z) + seq * p.T * M;
+    T* v = static_cast<T*>(p.v) + seq * p.T * M;
+    for (int64_t n = n0; n < n1; ++n) {
+        T zz[M], o[M];
+        ld_vec<T, M>(z, n, zz);
+        dg_step<T, M, false>(P, w, zz);
+        dg_out<T, M, false>(P, w, o);
+#pragma unroll
+        for (int j = 0; j < M; ++j) v[n * M + j] = o[j];
+    }
+}
+
+// phase 3, backward: h from the carry at the chunk's end, g(n) = Re V^-T h(n); grad_z = g;
+// per-chunk partial sums of grad_A = sum g(n) v(n)^T (fixed-order reduction later);
+// the chunk holding n = 0 writes grad_v0 = A^T g(0)
+template <typename T, int M>
+__global__ void __launch_bounds__(DG_NT) dg_bwd_emit_kernel(const Args p) {
+    const int64_t c = (int64_t)blockIdx.x * DG_NT + threadIdx.x;
+    if (c >= p.B * p.nch) return;
+    const int64_t seq = c / p.nch;
+    const int k = (int)(c - seq * p.nch);
+    Par<T, M> P;
+    P.load(p.tab + (p.ncoef > 1 ? seq : 0) * p.tab_stride);
+    cx<T> h[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) h[i] = {(T)p.carry[c * 2 * M + 2 * i], (T)p.carry[c * 2 * M + 2 * i + 1]};
+    const int64_t n0 = max((int64_t)0, p.T - (int64_t)(k + 1) * DG_C), n1 = p.T - (int64_t)k * DG_C;
+    const T* gv = static_cast<const T*>(p.gv);
+    const T* vo = static_cast<const T*>(p.vout) + seq * p.T * M;
+    const T* v0 = static_cast<const T*>(p.v0);
+    T* gz = static_cast<T*>(p.gz);
+    double gA[M][M];
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+        for (int j = 0; j < M; ++j) gA[i][j] = 0.0;
+    T g[M];
+    for (int64_t n = n1 - 1; n >= n0; --n) {
+        T gg[M];
+        if (gv != nullptr) ld_vec<T, M>(gv + seq * p.T * M, n, gg);
+        else
+#pragma unroll
+            for (int j = 0; j < M; ++j) gg[j] = T(0);
+        dg_step<T, M, true>(P, h, gg);
+        dg_out<T, M, true>(P, h, g);
+        if (gz != nullptr)
+#pragma unroll
+            for (int j = 0; j < M; ++j) gz[(seq * p.T + n) * M + j] = g[j];
+        T vp[M];                                           // v(n): v0 at n = 0, else the forward's v(n)
+#pragma unroll
+        for (int j = 0; j < M; ++j) vp[j] = n > 0 ? vo[(n - 1) * M + j] : (v0 != nullptr ? v0[seq * M + j] : T(0));
+#pragma unroll
+        for (int i = 0; i < M; ++i)
+#pragma unroll
+            for (int j = 0; j < M; ++j) gA[i][j] = fma((double)g[i], (double)vp[j], gA[i][j]);
+    }
+    if (n0 == 0 && p.gv0 != nullptr) {                     // g now holds g(0)
+        T* o = static_cast<T*>(p.gv0) + seq * M;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            T s = T(0);
+#pragma unroll
+            for (int j = 0; j < M; ++j) s = fma(P.A[j][i], g[j], s);
+            o[i] = s;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+        for (int j = 0; j < M; ++j) p.gpart[c * M * M + i * M + j] = gA[i][j];
+}
+
+// grad_A: fixed-order sum of the chunk partials (SHARED: every chunk; PER_SEQ: per sequence)
+template <typename T, int M>
+__global__ void __launch_bounds__(256) dg_reduce_kernel(const Args p, T* __restrict__ gA) {
+    __shared__ double red[256];
+    const int64_t set = blockIdx.x;
+    const int64_t r0 = p.ncoef > 1 ? set * p.nch : 0, nr = p.ncoef > 1 ? p.nch : p.B * p.nch;
+    for (int e = 0; e < M * M; ++e) {
+        double s = 0.0;
+        for (int64_t r = threadIdx.x; r < nr; r += 256) s += p.gpart[(r0 + r) * M * M + e];
+        red[threadIdx.x] = s;
+        __syncthreads();
+        for (int w = 128; w > 0; w >>= 1) {
+            if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) gA[set * M * M + e] = (T)red[0];
+        __syncthreads();
+    }
+}
+
+template <typename T, int M>
+static iir_status_t run(bool fwd, const iir_desc_t* d, Args& a, void* gA, cudaStream_t st) {
+    const unsigned nchunk = (unsigned)(a.B * a.nch), grid = (nchunk + DG_NT - 1) / DG_NT;
+    const double kmax = sizeof(T) == 4 ? 100.0 : 1e4;     // kappa(V) beyond which the dense fallback runs
+    iir_status_t s;
+    if (fwd) {
+        s = launch(K_DIAG_PREP, st, [&] {
+            dg_prep_kernel<T, M><<<(unsigned)((a.ncoef + 63) / 64), 64, 0, st>>>(static_cast<const T*>(a.a),
+                                                                                  a.coef_stride, a.ncoef,
+                                                                                  const_cast<double*>(a.tab), kmax);
+        });
+        if (s != IIR_OK) return s;
+        s = launch(K_DIAG_AGG, st, [&] { dg_agg_kernel<T, M, false><<<grid, DG_NT, 0, st>>>(a); });
+        if (s != IIR_OK) return s;
+        s = launch(K_DIAG_SCAN, st, [&] { dg_scan_kernel<T, M, false><<<(unsigned)a.B, 32, 0, st>>>(a); });
+        if (s != IIR_OK) return s;
+        return launch(K_DIAG_EMIT, st, [&] { dg_fwd_emit_kernel<T, M><<<grid, DG_NT, 0, st>>>(a); });
+    }
+    s = launch(K_DIAG_AGG, st, [&] { dg_agg_kernel<T, M, true><<<grid, DG_NT, 0, st>>>(a); });
+    if (s != IIR_OK) return s;
+    s = launch(K_DIAG_SCAN, st, [&] { dg_scan_kernel<T, M, true><<<(unsigned)a.B, 32, 0, st>>>(a); });
+    if (s != IIR_OK) return s;
+    s = launch(K_DIAG_EMIT, st, [&] { dg_bwd_emit_kernel<T, M><<<grid, DG_NT, 0, st>>>(a); });
+    if (s != IIR_OK || gA == nullptr) return s;
+    return launch(K_DIAG_EMIT, st, [&] {
+        dg_reduce_kernel<T, M><<<(unsigned)a.ncoef, 256, 0, st>>>(a, static_cast<T*>(gA));
+    });
+    (void)d;
+}
+
+}  // namespace dg
+
+size_t diag_tab_doubles(int M) { return M == 1 ? dg::Tb<1>::SIZE : dg::Tb<2>::SIZE; }
+int diag_chunk() { return dg::DG_C; }
+
+iir_status_t diag_run(bool fwd, const iir_desc_t* d, const void* A, const void* z, const void* v0, void* v,
+                      const void* gv, const void* vout, void* gz, void* gA, void* gv0, double* tab, double* agg,
+                      double* carry, double* gpart, cudaStream_t st) {
+    dg::Args a{};
+    a.a = A; a.z = z; a.v0 = v0; a.v = v; a.gv = gv; a.vout = vout; a.gz = gz; a.gv0 = gv0;
+    a.tab = tab; a.tab_stride = (int64_t)diag_tab_doubles(d->order);
+    a.coef_stride = d->coef_mode == IIR_COEF_SHARED ? 0 : (int64_t)d->order * d->order;
+    a.agg = agg; a.carry = carry; a.gpart = gpart;
+    a.B = d->batch; a.T = d->length; a.nch = (int)((d->length + dg::DG_C - 1) / dg::DG_C);
+    a.ncoef = d->coef_mode == IIR_COEF_SHARED ? 1 : (int)d->batch;
+    if (d->dtype == IIR_F64)
+        return d->order == 1 ? dg::run<double, 1>(fwd, d, a, gA, st) : dg::run<double, 2>(fwd, d, a, gA, st);
+    return d->order == 1 ? dg::run<float, 1>(fwd, d, a, gA, st) : dg::run<float, 2>(fwd, d, a, gA, st);
+}
+
+}  // namespace iirg

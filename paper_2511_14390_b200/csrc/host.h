@@ -14,7 +14,7 @@ namespace iirg {
 iir_status_t fail(iir_status_t st, const std::string& msg);
 
 enum Kind { K_LTI_PREP = 0, K_LTI_FWD, K_LTI_BWD, K_TV_PHI, K_TV_CHAIN, K_TV_FWD, K_TV_BWD_AGG, K_TV_BWD, K_REC_FWD,
-            K_REC_BWD, K_STATE_CARRY, K_TV_FIR, K_NUM };
+            K_REC_BWD, K_STATE_CARRY, K_TV_FIR, K_DIAG_PREP, K_DIAG_AGG, K_DIAG_SCAN, K_DIAG_EMIT, K_NUM };
 
 // Launch bookkeeping: counts every kernel and (when profiling is on) brackets it
 // with CUDA events on its stream.
@@ -63,6 +63,13 @@ struct Layout {
     size_t ws_err = 0;                                     // error word (look-back timeout)
     bool v2 = false;
 };
+
+// Diag-EXT bare recurrence (IIR_SS + IIR_FLAG_DIAG, M <= 2), diag.cu
+size_t diag_tab_doubles(int M);
+int diag_chunk();
+iir_status_t diag_run(bool fwd, const iir_desc_t* d, const void* A, const void* z, const void* v0, void* v,
+                      const void* gv, const void* vout, void* gz, void* gA, void* gv0, double* tab, double* agg,
+                      double* carry, double* gpart, cudaStream_t st);
 
 // per-sample (time-varying all-pole) path, tv.cu
 constexpr int TV_MAX_M = 31;   // per-sample orders 1..31 (the Phi kernel: one lane per basis state + the input)

@@ -58,9 +58,14 @@ struct TvArgs {
 template <typename T, int M, typename A = T>
 __global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs p) {
     static_assert(M + 1 <= 32, "one lane per basis state plus one for the input");
-    constexpr int TV_CH = tv_ch<T>();
+    // With A wider than T the staged chunk is converted ONCE into an A copy (each lane
+    // converts 1/32 of it) instead of every lane converting all M coefficients of every
+    // sample: the F2F conversions, not the FMAs, bounded the fp64-accumulating kernel.
+    constexpr bool CONV = sizeof(A) != sizeof(T);
+    constexpr int TV_CH = CONV ? 16 : tv_ch<T>();
     __shared__ __align__(16) T sa[TV_PHI_WARPS][2][TV_CH * M];
     __shared__ __align__(16) T sx[TV_PHI_WARPS][2][TV_CH];
+    __shared__ __align__(16) A sd[TV_PHI_WARPS][CONV ? TV_CH * M : 2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t seg = (int64_t)blockIdx.x * TV_PHI_WARPS + warp;
     if (seg >= p.B * p.nseg) return;
@@ -94,23 +99,32 @@ __global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs 
         cp_async_commit();
         cp_async_wait<1>();
         __syncwarp();
+        const A* cs;
+        if constexpr (CONV) {
+#pragma unroll
+            for (int e = lane; e < TV_CH * M; e += 32) sd[warp][e] = A(sa[warp][b][e]);
+            __syncwarp();
+            cs = sd[warp];
+        } else {
+            cs = reinterpret_cast<const A*>(sa[warp][b]);
+        }
         if (cnt == TV_CH) {
 #pragma unroll
             for (int s2 = 0; s2 < TV_CH; ++s2) {
                 A yn = (lane == M) ? A(sx[warp][b][s2]) : A(0);
-                T cf[M];
-                if constexpr ((M * sizeof(T)) % 16 == 0) {
+                A cf[M];
+                if constexpr ((M * sizeof(A)) % 16 == 0) {
 #pragma unroll
-                    for (int q = 0; q < M * (int)sizeof(T) / 16; ++q) {
-                        const uint4 t4 = reinterpret_cast<const uint4*>(&sa[warp][b][s2 * M])[q];
-                        memcpy(&cf[q * (16 / sizeof(T))], &t4, 16);
+                    for (int q = 0; q < M * (int)sizeof(A) / 16; ++q) {
+                        const uint4 t4 = reinterpret_cast<const uint4*>(cs + s2 * M)[q];
+                        memcpy(&cf[q * (16 / sizeof(A))], &t4, 16);
                     }
                 } else {
 #pragma unroll
-                    for (int i = 0; i < M; ++i) cf[i] = sa[warp][b][s2 * M + i];
+                    for (int i = 0; i < M; ++i) cf[i] = cs[s2 * M + i];
                 }
 #pragma unroll
-                for (int i = M - 1; i >= 0; --i) yn = fma(-A(cf[i]), v[i], yn);   // newest term last
+                for (int i = M - 1; i >= 0; --i) yn = fma(-cf[i], v[i], yn);
 #pragma unroll
                 for (int i = M - 1; i >= 1; --i) v[i] = v[i - 1];
                 v[0] = yn;
@@ -119,7 +133,7 @@ __global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs 
             for (int s2 = 0; s2 < cnt; ++s2) {
                 A yn = (lane == M) ? A(sx[warp][b][s2]) : A(0);
 #pragma unroll
-                for (int i = M - 1; i >= 0; --i) yn = fma(-A(sa[warp][b][s2 * M + i]), v[i], yn);
+                for (int i = M - 1; i >= 0; --i) yn = fma(-cs[s2 * M + i], v[i], yn);
 #pragma unroll
                 for (int i = M - 1; i >= 1; --i) v[i] = v[i - 1];
                 v[0] = yn;

@@ -14,13 +14,13 @@ from gpu_util import TOL, nrm_err, to_dev
 pytestmark = pytest.mark.gpu
 
 
-def run_gpu(p, want_v0_grad=True):
+def run_gpu(p, want_v0_grad=True, flags=0):
     td = torch.float32 if p["dtype"] == "f32" else torch.float64
     A, z, gv = to_dev(p["A"], td), to_dev(p["z"], td), to_dev(p["gv"], td)
     v0 = to_dev(p["v0"], td)
     Bsz, N, M = z.shape
     mode = B.IIR_COEF_SHARED if A.dim() == 2 else B.IIR_COEF_PER_SEQ
-    desc = B.make_desc(Bsz, N, M, "ss", td, mode)
+    desc = B.make_desc(Bsz, N, M, "ss", td, mode, flags=flags)
     tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
     tape = torch.empty(tb, dtype=torch.uint8, device="cuda")
     ws = torch.empty(wb, dtype=torch.uint8, device="cuda")
@@ -51,8 +51,8 @@ def run_oracle(p):
     return out
 
 
-def check(p):
-    g, o = run_gpu(p), run_oracle(p)
+def check(p, flags=0):
+    g, o = run_gpu(p, flags=flags), run_oracle(p)
     tol = TOL[p["dtype"]]
     for k in ("v", "gz", "gA", "gv0"):
         if g[k] is None:
