@@ -1,7 +1,7 @@
 """Benchmark of the hot path: forward + backward IIR filtering (BASELINE.json metric
 "fwd+bwd filtered samples/sec (B x T / s) and HBM GB/s vs peak").
 
-    python bench.py [--gpus N --steps K --warmup W] [--workload c5|c2|c1|c4|c3|f1|f2]
+    python bench.py [--gpus N --steps K --warmup W] [--workload c5|c2|c1|c4|c3|f1|f2|f3]
                     [--scaling weak|strong] [--impl ours|reference]
 
 Default workload: BASELINE.json's config 5 (order-8 TDF, shared coefficients,
@@ -52,12 +52,20 @@ WORKLOADS = {
                     "batch 32 x 2^18, fp32", fir=True, **inputs.CONFIGS["c3"]),
     "f1": dict(desc="SURVEY 8(f) f1: bare recurrence v(n+1) = A v(n) + z(n) of Listing 1, M = 2, batch 16 x 2^20, "
                     "fp32 (the paper's benchmarked operator at its longest N)", **dict(inputs.CONFIGS["f1"], batch=16)),
+    "f3": dict(desc="SURVEY 8(f) f3: Diag-EXT bare recurrence (eigen-basis element-wise complex scans), f1's shape: "
+                    "M = 2, batch 16 x 2^20, fp32", diag=True, **dict(inputs.CONFIGS["f1"], batch=16)),
 }
 
 
 def algorithmic_bytes(w):
     """Bytes per sample the method must move, per kernel."""
     s = 8 if w["dtype"] == "f64" else 4
+    if w["form"] == "ss" and w.get("diag"):
+        # diag_agg reads z (fwd) / gv (bwd); diag_fwd reads z, writes v; diag_bwd reads gv, v, writes gz;
+        # diag_prep / diag_scan / diag_red touch per-set and per-chunk data only
+        M = w["order"]
+        return {"diag_prep": 0, "diag_agg": M * s, "diag_scan": 0, "diag_fwd": 2 * M * s, "diag_bwd": 3 * M * s,
+                "diag_red": 0}
     if w["form"] == "ss":                       # rec_fwd reads z, writes v; rec_bwd reads gv, v, writes gz
         return {"rec_fwd": 2 * w["order"] * s, "rec_bwd": 3 * w["order"] * s}
     if w["coef"] == "per_sample":
@@ -206,6 +214,8 @@ class Problem:
         sched |= B.IIR_FLAG_GRAD_Y_EARLY
         if w.get("fir"):
             sched |= B.IIR_FLAG_PER_SAMPLE_B
+        if w.get("diag"):
+            sched |= B.IIR_FLAG_DIAG
         self.desc = B.make_desc(Bsz, T, M, w["form"], td, mode, flags=B.IIR_FLAG_WS_READY | sched)
         self.tb = B.iir_tape_bytes(self.desc)
         self.wb = B.iir_workspace_bytes(self.desc)
@@ -430,7 +440,15 @@ def cpu_baseline(w, budget_s=10.0):
     rng = np.random.default_rng(7)
     T = w["length"]
     nseq = min(w["batch"], 64)
-    if w["form"] == "ss":
+    what = "fp64 C oracle (dense state space)"
+    if w["form"] == "ss" and w.get("diag"):
+        from oracle import diag as odiag
+        T = min(T, 1 << 16)
+        nseq = 1
+        p = inputs.rec_problem(7, batch=nseq, length=T, order=w["order"], dtype=w["dtype"])
+        fn = lambda: odiag.diag_recurrence(p["A"], p["v0"][0], p["z"][0], p["gv"][0])
+        what = "numpy complex128 Diag-EXT oracle (oracle/diag.py)"
+    elif w["form"] == "ss":
         T = min(T, 1 << 20)
         nseq = 2
         p = inputs.rec_problem(7, batch=nseq, length=T, order=w["order"], dtype=w["dtype"])
@@ -464,8 +482,8 @@ def cpu_baseline(w, budget_s=10.0):
             break
     value = reps * nseq * T / el
     return dict(value=value, unit="samples/s", cores=cores, kind="oracle",
-                sample=f"{reps} x ({nseq} sequences x {T} samples) of the workload, fp64 C oracle "
-                       f"(dense state space), {cores} host threads, {el:.1f} s wall")
+                sample=f"{reps} x ({nseq} sequences x {T} samples) of the workload, {what}, "
+                       f"{cores} host threads, {el:.1f} s wall")
 
 
 # -------------------------------------------------------------- reference ---
@@ -477,7 +495,13 @@ def run_reference(args, w, rank, world):
     if rank != 0:
         return
     T = w["length"]
-    if w["form"] == "ss":
+    if w["form"] == "ss" and w.get("diag"):
+        from oracle import diag as odiag
+        T = min(T, 1 << 15)
+        nseq = 1
+        p = inputs.rec_problem(7, batch=nseq, length=T, order=w["order"], dtype=w["dtype"])
+        fn = lambda: odiag.diag_recurrence(p["A"], p["v0"][0], p["z"][0], p["gv"][0])
+    elif w["form"] == "ss":
         T = min(T, 1 << 19)
         nseq = 1
         p = inputs.rec_problem(7, batch=nseq, length=T, order=w["order"], dtype=w["dtype"])

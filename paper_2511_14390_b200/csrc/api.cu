@@ -29,7 +29,7 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
 // ------------------------------------------------------- instrumentation ----
 static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_phi", "tv_chain", "tv_fwd",
                                         "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd", "state_carry", "tv_fir",
-                                        "diag_prep", "diag_agg", "diag_scan", "diag_emit"};
+                                        "diag_prep", "diag_agg", "diag_scan", "diag_fwd", "diag_bwd", "diag_red"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;

@@ -435,15 +435,15 @@ static iir_status_t run(bool fwd, const iir_desc_t* d, Args& a, void* gA, cudaSt
         if (s != IIR_OK) return s;
         s = launch(K_DIAG_SCAN, st, [&] { dg_scan_kernel<T, M, false><<<(unsigned)a.B, 32, 0, st>>>(a); });
         if (s != IIR_OK) return s;
-        return launch(K_DIAG_EMIT, st, [&] { dg_fwd_emit_kernel<T, M><<<grid, DG_NT, 0, st>>>(a); });
+        return launch(K_DIAG_FWD, st, [&] { dg_fwd_emit_kernel<T, M><<<grid, DG_NT, 0, st>>>(a); });
     }
     s = launch(K_DIAG_AGG, st, [&] { dg_agg_kernel<T, M, true><<<grid, DG_NT, 0, st>>>(a); });
     if (s != IIR_OK) return s;
     s = launch(K_DIAG_SCAN, st, [&] { dg_scan_kernel<T, M, true><<<(unsigned)a.B, 32, 0, st>>>(a); });
     if (s != IIR_OK) return s;
-    s = launch(K_DIAG_EMIT, st, [&] { dg_bwd_emit_kernel<T, M><<<grid, DG_NT, 0, st>>>(a); });
+    s = launch(K_DIAG_BWD, st, [&] { dg_bwd_emit_kernel<T, M><<<grid, DG_NT, 0, st>>>(a); });
     if (s != IIR_OK || gA == nullptr) return s;
-    return launch(K_DIAG_EMIT, st, [&] {
+    return launch(K_DIAG_RED, st, [&] {
         dg_reduce_kernel<T, M><<<(unsigned)a.ncoef, 256, 0, st>>>(a, static_cast<T*>(gA));
     });
     (void)d;
