@@ -208,6 +208,12 @@ __device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
     else
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(s), "l"(gmem) : "memory");
 }
+// the mbarrier tracks this thread's prior cp.async copies: its pending count is raised by one
+// now and lowered when they have landed (no .noinc)
+__device__ __forceinline__ void cp_async_mbar_arrive(unsigned long long* bar) {
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];"
+                 :: "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }

@@ -221,8 +221,8 @@ __device__ __forceinline__ void slot_publish(float* dst, const float (&v)[M], in
     }
 }
 template <int M>
-__device__ __forceinline__ float* slot_ptr(const CarryWs& cw, int lev, int64_t seq, int64_t blk) {
-    return reinterpret_cast<float*>(cw.agg[lev]) + (seq * cw.nblk[lev] + blk) * M;
+__device__ __forceinline__ float* slot_ptr(const CarryWs& cw, int64_t boff, int lev, int64_t seq, int64_t blk) {
+    return reinterpret_cast<float*>(cw.agg[lev] + boff) + (seq * cw.nblk[lev] + blk) * M;
 }
 
 // acc += Y v with Y = matrix k of a pair table [j][ip][32] (k = lane: each lane its own
@@ -263,7 +263,8 @@ __device__ __forceinline__ void warp_sum2(unsigned long long (&a)[NPR]) {
 // aggregate time keeps every level as prompt as the tile aggregates.
 template <int M>
 __device__ __forceinline__ void carry_publish(const float* __restrict__ PQ, int lane, int jt, int64_t seq,
-                                              const float (&X0)[M], float (&G)[M], const CarryWs& cw) {
+                                              const float (&X0)[M], float (&G)[M], const CarryWs& cw,
+                                              int64_t boff) {
     constexpr int NPR = Cfg<M>::NPR, LV = 32 * M * Cfg<M>::MP;
     if (jt == 0) {
         unsigned long long G2[NPR];
@@ -271,7 +272,7 @@ __device__ __forceinline__ void carry_publish(const float* __restrict__ PQ, int 
         mvp<M>(PQ, 1, X0, G2);
         unpack_pairs<M, NPR>(G2, G);
     }
-    slot_publish<M>(slot_ptr<M>(cw, 0, seq, jt), G, lane);
+    slot_publish<M>(slot_ptr<M>(cw, boff, 0, seq, jt), G, lane);
     const int nl = cw.nlev;
     if (nl < 2 || (jt & 31) != 31) return;
     float Own[M];
@@ -285,7 +286,7 @@ __device__ __forceinline__ void carry_publish(const float* __restrict__ PQ, int 
 #pragma unroll
         for (int i = 0; i < M; ++i) V[i] = 0.f;
         if (lane < 31) {
-            const float* sp = slot_ptr<M>(cw, v, seq, blk - 1 - lane);
+            const float* sp = slot_ptr<M>(cw, boff, v, seq, blk - 1 - lane);
             slot_load<M>(sp, V);
             if (!slot_ok<M>(V)) slot_wait<M>(sp, V, cw.err);
         }
@@ -301,7 +302,7 @@ __device__ __forceinline__ void carry_publish(const float* __restrict__ PQ, int 
         pack_pairs<M, NPR>(Own, O2);
         mvp<M>(PQ + v * LV, 1, T, O2);                              // Own = Y_v T_v + Own
         unpack_pairs<M, NPR>(O2, Own);
-        slot_publish<M>(slot_ptr<M>(cw, v + 1, seq, jt >> (5 * (v + 1))), Own, lane);
+        slot_publish<M>(slot_ptr<M>(cw, boff, v + 1, seq, jt >> (5 * (v + 1))), Own, lane);
     }
 }
 
@@ -312,7 +313,8 @@ __device__ __forceinline__ void carry_publish(const float* __restrict__ PQ, int 
 // Fixed combination order (per-lane products, a fixed butterfly): bitwise deterministic.
 template <int M>
 __device__ __forceinline__ void carry_lookback(const float* __restrict__ PQ, int lane, int jt, int64_t seq,
-                                               const float (&X0)[M], const CarryWs& cw, float (*sT)[M],
+                                               const float (&X0)[M], const CarryWs& cw, int64_t boff,
+                                               float (*sT)[M],
                                                float (&X)[M]) {
     constexpr int NPR = Cfg<M>::NPR, LV = 32 * M * Cfg<M>::MP;
     if (jt == 0) {
@@ -329,7 +331,7 @@ __device__ __forceinline__ void carry_lookback(const float* __restrict__ PQ, int
 #pragma unroll
         for (int i = 0; i < M; ++i) V[i] = 0.f;
         if (lane < d) {
-            const float* sp = slot_ptr<M>(cw, v, seq, blk - 1 - lane);
+            const float* sp = slot_ptr<M>(cw, boff, v, seq, blk - 1 - lane);
             slot_load<M>(sp, V);
             if (!slot_ok<M>(V)) slot_wait<M>(sp, V, cw.err);
         }
@@ -363,45 +365,109 @@ __device__ __forceinline__ void carry_lookback(const float* __restrict__ PQ, int
     __syncwarp();                                                    // sT is reused by the warp's next tile
 }
 
+// Re-arm the bank the previous call used (cw unshifted; boff = this call's bank offset).
+__device__ __forceinline__ void rearm_other_bank2(const CarryWs& cw, int64_t boff, unsigned cta, unsigned nctas) {
+    double* other = cw.agg[0] + (boff != 0 ? 0 : cw.bank);
+    for (int64_t i = (int64_t)cta * blockDim.x + threadIdx.x; i < cw.bank; i += (int64_t)nctas * blockDim.x)
+        __stcg(other + i, sentinel());
+}
+
+template <int N, int I = 0, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (I < N) {
+        f(std::integral_constant<int, I>{});
+        static_for<N, I + 1>(f);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Load the rows of one tile: row r holds samples [p0 + rL, p0 + (r+1)L) of `src` (one
-// sequence, length T); samples outside [0, T) (or src == NULL) read as 0.  Lane l fills
-// row l (rowmap 0) or 31 - l (rowmap 1).  vec: bulk row copies on the TMA engine counted
-// on `bar`; `arm`: this call arms the barrier (arm_mult x the tile's bytes: several
-// streams may complete on one barrier).  Without vec: element copies by the lanes and
-// (arm) a plain arrive.
+// sequence, length T); samples outside [0, T) (or src == NULL) read as 0.
+// vec (rows 16 B aligned, T % 4 == 0): the warp copies the tile's 2048 samples as 512
+// coalesced 16-byte cp.async chunks (chunk c -> row c / (L/4), column 4 (c % (L/4)): each
+// warp instruction moves 512 contiguous bytes), zero-filling the chunks outside [0, T); the
+// copies complete on `bar` (every lane's cp.async.mbarrier.arrive; `arm`: lane 0's plain
+// arrive after the whole warp has issued, so with several streams on one barrier the
+// arming call comes LAST).  Without vec: element copies by the lanes (lane l fills row l,
+// or 31 - l for rowmap 1) and (arm) a plain arrive.
 template <int M>
 __device__ __forceinline__ void load_rows(float* buf, unsigned long long* bar, const float* src, int64_t p0,
-                                          int64_t T, bool vec, int lane, int rowmap, bool arm = true,
-                                          unsigned arm_mult = 1) {
+                                          int64_t T, bool vec, int lane, int rowmap, bool arm = true) {
     using C = Cfg<M>;
-    constexpr int L = C::L;
-    const int r = rowmap ? 31 - lane : lane;
-    const int64_t s = p0 + (int64_t)r * L;
-    float* row = buf + r * C::PITCH;
-    const int64_t lo = s > 0 ? s : 0, hi = (s + L < T) ? s + L : T;
-    const bool any = src != nullptr && hi > lo;
+    constexpr int L = C::L, CPR = L / 4;
+    static_assert(32 % CPR == 0, "whole rows per warp instruction");
     if (vec) {
-        if (arm && lane == 0) {
-            const int64_t tlo = p0 > 0 ? p0 : 0, thi = (p0 + C::TS < T) ? p0 + C::TS : T;
-            const unsigned bytes = (src != nullptr && thi > tlo) ? (unsigned)((thi - tlo) * 4) : 0u;
-            mbar_arrive_expect_tx(bar, bytes * arm_mult);
-        }
-        __syncwarp();
-        if (any) bulk_g2s(row + (lo - s), src + lo, (unsigned)((hi - lo) * 4), bar);
-        if (!any || lo > s || hi < s + L) {
-            for (int g = 0; g < L / 4; ++g) {
-                const int64_t e = s + 4 * g;
-                if (!any || e < lo || e >= hi) *reinterpret_cast<float4*>(row + 4 * g) = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (src != nullptr && p0 >= 0 && p0 + C::TS <= T) {        // interior tile: immediate offsets
+            const unsigned sb = smem_u32(buf + (lane / CPR) * C::PITCH + 4 * (lane % CPR));
+            const float* g = src + p0 + 4 * lane;
+            static_for<CPR>([&](auto ic) {
+                constexpr int i = decltype(ic)::value;
+                asm volatile("cp.async.cg.shared.global [%0+%2], [%1+%3], 16;"
+                             :: "r"(sb), "l"(g), "n"(i * (32 / CPR) * C::PITCH * 4), "n"(i * 512) : "memory");
+            });
+            cp_async_mbar_arrive(bar);
+        } else if (src != nullptr) {
+#pragma unroll 4
+            for (int i = 0; i < CPR; ++i) {
+                const int ci = 32 * i + lane;
+                const int64_t n = p0 + 4 * (int64_t)ci;
+                const bool in = n >= 0 && n < T;
+                cp_async16(buf + (ci / CPR) * C::PITCH + 4 * (ci % CPR), in ? src + n : src, in ? 16u : 0u);
+            }
+            cp_async_mbar_arrive(bar);
+        } else {
+#pragma unroll
+            for (int i = 0; i < CPR; ++i) {
+                const int ci = 32 * i + lane;
+                *reinterpret_cast<float4*>(buf + (ci / CPR) * C::PITCH + 4 * (ci % CPR)) = make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
+        __syncwarp();
+        if (arm && lane == 0) mbar_arrive(bar);
     } else {
+        const int r = rowmap ? 31 - lane : lane;
+        const int64_t s = p0 + (int64_t)r * L;
+        float* row = buf + r * C::PITCH;
         for (int e = 0; e < L; ++e) {
             const int64_t n = s + e;
             row[e] = (src != nullptr && n >= 0 && n < T) ? src[n] : 0.f;
         }
         __syncwarp();
         if (arm && lane == 0) mbar_arrive(bar);
+    }
+}
+
+// Store the rows of one tile (the inverse of load_rows; samples outside [0, T) dropped).
+// vec: coalesced 16-byte stores by the whole warp after a __syncwarp (every lane's row is
+// complete); otherwise lane l stores row l (rowmap 0) or 31 - l (rowmap 1).
+template <int M>
+__device__ __forceinline__ void store_rows(const float* buf, float* dst, int64_t p0, int64_t T, bool vec, int lane,
+                                           int rowmap) {
+    using C = Cfg<M>;
+    constexpr int L = C::L, CPR = L / 4;
+    static_assert(32 % CPR == 0, "whole rows per warp instruction");
+    if (vec && p0 >= 0 && p0 + C::TS <= T) {                    // interior tile
+        __syncwarp();
+        const float* sb = buf + (lane / CPR) * C::PITCH + 4 * (lane % CPR);
+        float* g = dst + p0 + 4 * lane;
+#pragma unroll
+        for (int i = 0; i < CPR; ++i)
+            *reinterpret_cast<float4*>(g + 128 * i) = *reinterpret_cast<const float4*>(sb + i * (32 / CPR) * C::PITCH);
+    } else if (vec) {
+        __syncwarp();
+#pragma unroll 4
+        for (int i = 0; i < CPR; ++i) {
+            const int ci = 32 * i + lane;
+            const int64_t n = p0 + 4 * (int64_t)ci;
+            const float4 v = *reinterpret_cast<const float4*>(buf + (ci / CPR) * C::PITCH + 4 * (ci % CPR));
+            if (n >= 0 && n < T) *reinterpret_cast<float4*>(dst + n) = v;
+        }
+    } else {
+        const int r = rowmap ? 31 - lane : lane;
+        const int64_t s = p0 + (int64_t)r * L;
+        const float* row = buf + r * C::PITCH;
+        const int64_t lo = s > 0 ? s : 0, hi = (s + L < T) ? s + L : T;
+        for (int64_t n = lo; n < hi; ++n) dst[n] = row[n - s];
     }
 }
 
@@ -518,7 +584,7 @@ __device__ __forceinline__ void tmem_ld16(unsigned taddr, float (&v)[16]) {
 // x parked in TMEM): aggregate + publish t1 (data arrived an iteration ago) and park it,
 // issue t2's load, look back for t0, emit t0 from TMEM.
 template <int M, int NWP, bool GT>
-__global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const FwdArgs p) {
+__global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const __grid_constant__ FwdArgs p) {
     using C = Cfg<M>;
     constexpr int L = C::L, TS = C::TS, NPR = C::NPR;
     static_assert(L % 16 == 0 && NWP <= 16 && 2 * L * ((NWP + 3) / 4) <= 512, "TMEM slots");
@@ -540,9 +606,10 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const FwdArgs p) 
     // the previous call's use of the workspace) completed before it started.  So the
     // workspace and the first x tile are read before griddepcontrol.wait; only the
     // prologue's tables are read after it.
-    CarryWs cw = p.cw;
-    const unsigned ep = carry_bank(cw);
-    rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
+    const CarryWs& cw = p.cw;                                  // grid constant: levels indexed from the param bank
+    const unsigned ep = __ldcg(cw.epoch);
+    const int64_t boff = (ep & 1u) ? cw.bank : 0;
+    rearm_other_bank2(cw, boff, blockIdx.x, gridDim.x);
     const bool vec = p.vec != 0;
     Sched s0, s1;
     s0.init(blockIdx.x * NWP + warp, gridDim.x * NWP, p.B);
@@ -592,14 +659,14 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const FwdArgs p) 
         if (s.j == 0 && p.zi != nullptr)
 #pragma unroll
             for (int i = 0; i < M; ++i) X0[i] = p.zi[s.seq * M + i];
-        carry_publish<M>(p.t32 + s.seq * p.t32_stride + C::OPQ, lane, s.j, s.seq, X0, G, cw);
+        carry_publish<M>(p.t32 + s.seq * p.t32_stride + C::OPQ, lane, s.j, s.seq, X0, G, cw, boff);
         V2_TRACE(p.trace, s.t, 2);
     };
     float E0[M];
     unsigned sl = 0;                                             // TMEM slot of t0 (0 / 1)
     if (s0.t < p.ntot) {
         aggregate(s0, tbase, E0);
-        if (s1.t < p.ntot) { __syncwarp(); fence_proxy_async(); issue(s1); }
+        if (s1.t < p.ntot) { __syncwarp(); issue(s1); }
     }
     while (s0.t < p.ntot) {
         Sched s2 = s1;
@@ -607,7 +674,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const FwdArgs p) 
         float E1[M];
         if (s1.t < p.ntot) {
             aggregate(s1, tbase + (sl ^ 1u) * L, E1);
-            if (s2.t < p.ntot) { __syncwarp(); fence_proxy_async(); issue(s2); }
+            if (s2.t < p.ntot) { __syncwarp(); issue(s2); }
         }
         const int64_t seq = s0.seq;
         const int jt = s0.j;
@@ -622,7 +689,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const FwdArgs p) 
 #pragma unroll
             for (int i = 0; i < M; ++i) X0[i] = p.zi[seq * M + i];
         V2_TRACE(p.trace, s0.t, 3);
-        carry_lookback<M>(t32s + C::OPQ, lane, jt, seq, X0, cw, s_T[warp], X);
+        carry_lookback<M>(t32s + C::OPQ, lane, jt, seq, X0, cw, boff, s_T[warp], X);
         V2_TRACE(p.trace, s0.t, 4);
         float vin[M];
         lane_carry<M>(t32s + C::OQ, lane, E0, X, vin);
@@ -650,7 +717,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const FwdArgs p) 
                 for (int i = 0; i < M; ++i) p.zf[seq * M + i] = w2[i];
         }
         // a4: re-run from the exact carry-in, x from TMEM, y into the outgoing buffer
-        bulk_wait_read0();                                       // the previous store from bY has read it
+        __syncwarp();                                            // the previous tile's stores have read bY
         float* yr = bY + lane * C::PITCH;
         {
             Tdf2<M> c2;
@@ -679,20 +746,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const FwdArgs p) 
             }
         }
         V2_TRACE(p.trace, s0.t, 5);
-        {
-            const int64_t s = p0 + (int64_t)lane * L;
-            const int64_t lo = s > 0 ? s : 0, hi = (s + L < p.T) ? s + L : p.T;
-            float* yrow = p.y + seq * p.T;
-            if (hi > lo) {
-                if (vec) {
-                    fence_proxy_async();
-                    bulk_s2g(yrow + lo, yr + (lo - s), (unsigned)((hi - lo) * 4));
-                    bulk_commit();
-                } else {
-                    for (int64_t n = lo; n < hi; ++n) yrow[n] = yr[n - s];
-                }
-            }
-        }
+        store_rows<M>(bY, p.y + seq * p.T, p0, p.T, vec, lane, 0);
         V2_TRACE(p.trace, s0.t, 6);
         if (p.trace != nullptr && lane == 0) p.trace[(size_t)s0.t * 8 + 7] = blockIdx.x * NWP + warp;
         s0 = s1;
@@ -701,7 +755,6 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const FwdArgs p) 
         for (int i = 0; i < M; ++i) E0[i] = E1[i];
         sl ^= 1u;
     }
-    bulk_wait0();
     tmem_fence_before();
     cta_exit(cw, ep, gridDim.x);
     tmem_fence_after();
@@ -834,7 +887,7 @@ __device__ __forceinline__ double lane_colsum(float* scratch, int lane, float C0
 }
 
 template <int M, int NWP, bool GT>
-__global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) {
+__global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_constant__ BwdArgs p) {
     using C = Cfg<M>;
     constexpr int L = C::L, TS = C::TS, NG = C::NG, NPR = C::NPR;
     static_assert(L % 16 == 0 && NWP <= 16 && 2 * L * ((NWP + 3) / 4) <= 512, "TMEM slots");
@@ -857,14 +910,15 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
     // nothing the previous kernels wrote is read before griddepcontrol.wait.
     pdl_wait();
     pdl_launch_dependents();
-    CarryWs cw = p.cw;
-    const unsigned ep = carry_bank(cw);
+    const CarryWs& cw = p.cw;                                  // grid constant: levels indexed from the param bank
+    const unsigned ep = __ldcg(cw.epoch);
+    const int64_t boff = (ep & 1u) ? cw.bank : 0;
     if constexpr (!GT) {
         const float* src = p.t32 + C::DIR;                       // backward table group
         for (int i = threadIdx.x; i < C::STAGE / 4; i += blockDim.x) cp_async16_ca(sm2 + 4 * i, src + 4 * i);
         cp_async_commit();
     }
-    rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
+    rearm_other_bank2(cw, boff, blockIdx.x, gridDim.x);
     if constexpr (!GT) cp_async_wait<0>();
     tmem_fence_before();
     __syncthreads();
@@ -881,8 +935,8 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
     };
     auto issue_xy = [&](const Sched& s) {
         const int64_t off = s.seq * p.T;
-        load_rows<M>(bX, barXY, p.x + off, p0_of(s), p.T, vec, lane, 1, true, 2);
         load_rows<M>(bY, barXY, p.y + off, p0_of(s), p.T, vec, lane, 1, false);
+        load_rows<M>(bX, barXY, p.x + off, p0_of(s), p.T, vec, lane, 1, true);     // arms last
     };
     // a5 + a6 (intra-warp) of tile t: dy rows -> TMEM slot, K-form aggregate, scan, publication
     auto aggregate = [&](const Sched& s, unsigned slot, float (&E)[M]) {
@@ -914,7 +968,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
         if (s.j == 0 && p.gzf != nullptr)
 #pragma unroll
             for (int i = 0; i < M; ++i) X0[i] = p.gzf[s.seq * M + i];
-        carry_publish<M>(p.t32 + s.seq * p.t32_stride + C::DIR + C::OPQ, lane, s.j, s.seq, X0, G, cw);
+        carry_publish<M>(p.t32 + s.seq * p.t32_stride + C::DIR + C::OPQ, lane, s.j, s.seq, X0, G, cw, boff);
         V2_TRACE(p.trace, s.t, 2);
     };
     // coefficient partial sums: SHARED accumulates over all of this warp's tiles (a fixed set
@@ -928,19 +982,17 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
     if (s0.t < p.ntot) {
         issue_dy(s0);
         aggregate(s0, tbase, E0);
-        if (s1.t < p.ntot) { __syncwarp(); fence_proxy_async(); issue_dy(s1); }
+        if (s1.t < p.ntot) { __syncwarp(); issue_dy(s1); }
     }
     while (s0.t < p.ntot) {
         Sched s2 = s1;
         s2.next();
-        bulk_wait_read0();                                       // this lane's dx store has read bX
-        __syncwarp();
-        fence_proxy_async();                                     // bX / bY generic accesses before the TMA writes
+        __syncwarp();                                            // the previous tile's dx stores have read bX
         issue_xy(s0);
         float E1[M];
         if (s1.t < p.ntot) {
             aggregate(s1, tbase + (sl ^ 1u) * L, E1);
-            if (s2.t < p.ntot) { __syncwarp(); fence_proxy_async(); issue_dy(s2); }
+            if (s2.t < p.ntot) { __syncwarp(); issue_dy(s2); }
         }
         const int64_t seq = s0.seq;
         const int jr = s0.j;                                     // 0 = last tile in time
@@ -959,7 +1011,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
 #pragma unroll
             for (int i = 0; i < M; ++i) X0[i] = p.gzf[seq * M + i];
         V2_TRACE(p.trace, s0.t, 3);
-        carry_lookback<M>(t32s + C::OPQ, lane, jr, seq, X0, cw, s_T[warp], X);
+        carry_lookback<M>(t32s + C::OPQ, lane, jr, seq, X0, cw, boff, s_T[warp], X);
         V2_TRACE(p.trace, s0.t, 4);
         float din[M];
         lane_carry<M>(t32s + C::OQ, lane, E0, X, din);           // [g(e) .. g(e+M-1)], e = this chunk's right end
@@ -1055,19 +1107,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
             for (int i = 0; i < M; ++i) p.gzi[seq * M + i] = w[i];
         V2_TRACE(p.trace, s0.t, 5);
         // dx rows out
-        if (p.gx != nullptr) {
-            const int64_t lo = s > 0 ? s : 0, hi = (s + L < p.T) ? s + L : p.T;
-            float* gxrow = p.gx + seq * p.T;
-            if (hi > lo) {
-                if (vec) {
-                    fence_proxy_async();
-                    bulk_s2g(gxrow + lo, xr + (lo - s), (unsigned)((hi - lo) * 4));
-                    bulk_commit();
-                } else {
-                    for (int64_t n = lo; n < hi; ++n) gxrow[n] = xr[n - s];
-                }
-            }
-        }
+        if (p.gx != nullptr) store_rows<M>(bX, p.gx + seq * p.T, p0, p.T, vec, lane, 1);
         // a8 (PER_SEQ): the tile's partial-sum row joins its sequence's fixed-order reduction
         if constexpr (GT) {
             if (p.want_coef) {
@@ -1091,7 +1131,6 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const BwdArgs p) 
             finalize_row<M>(p, 0, (int64_t)gridDim.x * NWP, (int64_t)blockIdx.x * NWP + warp, colsum, lane, p.t64);
         }
     }
-    bulk_wait0();
     tmem_fence_before();
     cta_exit(cw, ep, gridDim.x);
     tmem_fence_after();
