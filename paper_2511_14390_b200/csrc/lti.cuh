@@ -324,6 +324,18 @@ template <int M> struct Tdf2 {
         }
         b0 = bc[0]; b1 = bc[1]; na1 = -ac[1];
     }
+    // the same pairs from a table laid out [B2 | NA2 | B1 | NA1], stride jp pairs (lti2.cuh W)
+    __device__ __forceinline__ void init_pairs(const float* w, int jp, const float (&bc)[M + 1], const float (&ac)[M + 1]) {
+        const unsigned long long* wp = reinterpret_cast<const unsigned long long*>(w);
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+            B2[k] = wp[k];
+            NA2[k] = wp[jp + k];
+            B1[k] = wp[2 * jp + k];
+            NA1[k] = wp[3 * jp + k];
+        }
+        b0 = bc[0]; b1 = bc[1]; na1 = -ac[1];
+    }
 };
 template <int M>
 __device__ __forceinline__ void tdf2_pack(const float (&v)[M], unsigned long long (&V)[Tdf2<M>::NP]) {

@@ -100,8 +100,12 @@ iir_status_t run(bool fwd, int M, const Call& c) {
     switch (M) {
 #define IIRG_V2_CASE(m) \
         case m: return fwd ? Ops<m>::forward(c) : Ops<m>::backward(c);
+#ifdef IIRG_V2_ONLY                      // kernel experiments: one order only (tools/sass_loop.sh)
+        IIRG_V2_CASE(IIRG_V2_ONLY)
+#else
         IIRG_V2_CASE(1) IIRG_V2_CASE(2) IIRG_V2_CASE(3) IIRG_V2_CASE(4)
         IIRG_V2_CASE(5) IIRG_V2_CASE(6) IIRG_V2_CASE(7) IIRG_V2_CASE(8)
+#endif
 #undef IIRG_V2_CASE
     }
     return fail(IIR_EUNSUPPORTED, "order");

@@ -62,7 +62,12 @@ template <int M> struct Cfg {
     //   PQ [LEVELS][M][NPR][32] float2: PQ[v][j][ip][k] = the same pairs of X^(k 32^v TS)
     // [0, OQ) is staged in shared memory (broadcast reads); Q and PQ (each lane reads its
     // own matrix) are read through L1.
-    static constexpr int OK_ = 0, OP = r4(L * MP), OC = OP + r4(5 * M * MP), OQ = OC + r4(3 * M + 2);
+    // | W: coefficient pairs (JP of each, float2; na = -a', zero outside 0..M), read as pairs
+    //   so the hot loops never rebuild them: forward group, the Tdf2 pairs B2, NA2, B1, NA1;
+    //   backward group (a7): (na_2j+1, na_2j+2), (na_2j+2, na_2j+3), (b'_2j, b'_2j+1), (b'_2j-1, b'_2j)
+    static constexpr int JP = (M + 1) / 2 + 1;
+    static constexpr int OK_ = 0, OP = r4(L * MP), OC = OP + r4(5 * M * MP), OW = OC + r4(3 * M + 2);
+    static constexpr int OQ = OW + r4(8 * JP);
     static constexpr int OPQ = OQ + 32 * M * MP;
     static constexpr int STAGE = OQ;
     static constexpr int DIR = OPQ + LEVELS * 32 * M * MP;
@@ -428,6 +433,7 @@ __device__ __forceinline__ void load_rows(float* buf, unsigned long long* bar, c
         const int r = rowmap ? 31 - lane : lane;
         const int64_t s = p0 + (int64_t)r * L;
         float* row = buf + r * C::PITCH;
+#pragma unroll 1
         for (int e = 0; e < L; ++e) {
             const int64_t n = s + e;
             row[e] = (src != nullptr && n >= 0 && n < T) ? src[n] : 0.f;
@@ -467,6 +473,7 @@ __device__ __forceinline__ void store_rows(const float* buf, float* dst, int64_t
         const int64_t s = p0 + (int64_t)r * L;
         const float* row = buf + r * C::PITCH;
         const int64_t lo = s > 0 ? s : 0, hi = (s + L < T) ? s + L : T;
+#pragma unroll 1
         for (int64_t n = lo; n < hi; ++n) dst[n] = row[n - s];
     }
 }
@@ -721,7 +728,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const __grid_cons
         float* yr = bY + lane * C::PITCH;
         {
             Tdf2<M> c2;
-            c2.init(bc, ac);
+            c2.init_pairs(tab + C::OW, C::JP, bc, ac);
             unsigned long long VP[Tdf2<M>::NP];
             tdf2_pack<M>(vin, VP);
             float xs[16];
@@ -774,6 +781,7 @@ template <int NG>
 __device__ __forceinline__ void warp_reduce_rows(const double* src, int64_t nrows, int lane, double (&out)[NG]) {
 #pragma unroll
     for (int k = 0; k < NG; ++k) out[k] = 0.0;
+#pragma unroll 1
     for (int64_t r0 = lane; r0 < nrows; r0 += 64) {
         double v0[NG], v1[NG];
         const int64_t r1 = r0 + 32;
@@ -823,7 +831,7 @@ __device__ __forceinline__ void chain_rule2(const double (&G)[2 * M + 1], const 
 // chain rule writes grad_b, grad_a.  Deterministic: every sum runs over row indices in a
 // fixed order, whatever the arrival order.
 template <int M>
-__device__ __forceinline__ void finalize_row(const BwdArgs& p, int64_t cset, int64_t per_set, int64_t li,
+__device__ __noinline__ void finalize_row(const BwdArgs& p, int64_t cset, int64_t per_set, int64_t li,
                                              double colsum, int lane, const double* __restrict__ t64) {
     constexpr int NG = Cfg<M>::NG;
     double* part = p.partial + cset * per_set * NG;
@@ -871,13 +879,23 @@ __device__ __forceinline__ void finalize_row(const BwdArgs& p, int64_t cset, int
 // The 32 lanes' partial sums (C_0, (C_k, D_k) pairs) -> fp64 column sums via lane rows of a
 // free shared buffer; lane k < NG returns sum k (fixed order over the lanes).
 template <int M>
-__device__ __forceinline__ double lane_colsum(float* scratch, int lane, float C0, const unsigned long long (&CD)[M]) {
+__device__ __forceinline__ double lane_colsum(float* scratch, int lane, const unsigned long long (&CE)[(M + 1) / 2 + 1],
+                                              const unsigned long long (&CO)[(M + 1) / 2 + 1],
+                                              const unsigned long long (&DE)[(M + 1) / 2 + 1],
+                                              const unsigned long long (&DO)[(M + 1) / 2 + 1]) {
     using C = Cfg<M>;
     __syncwarp();
     float* scr = scratch + lane * C::PITCH;
-    scr[0] = C0;
+    auto ck = [&](const unsigned long long (&E)[(M + 1) / 2 + 1], const unsigned long long (&O)[(M + 1) / 2 + 1],
+                  int k) {
+        return (k & 1) ? lo2(O[(k + 1) / 2]) + hi2(O[(k - 1) / 2]) : lo2(E[k / 2]) + hi2(E[k / 2]);
+    };
+    scr[0] = ck(CE, CO, 0);
 #pragma unroll
-    for (int i = 0; i < M; ++i) { scr[1 + i] = lo2(CD[i]); scr[M + 1 + i] = hi2(CD[i]); }
+    for (int i = 0; i < M; ++i) {
+        scr[1 + i] = ck(CE, CO, 1 + i);
+        scr[M + 1 + i] = ck(DE, DO, 1 + i);
+    }
     __syncwarp();
     double colsum = 0.0;
     if (lane < C::NG)
@@ -973,10 +991,12 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
     };
     // coefficient partial sums: SHARED accumulates over all of this warp's tiles (a fixed set
     // in a fixed order under the static schedule) and flushes one row per warp at the end
-    unsigned long long CD[M];
+    // the correlation sums C_k = sum g(n+k) x(n), D_k = sum g(n+k) y(n) in paired partial
+    // sums (see a7): C_2j = CE_j.lo + CE_j.hi, C_2j+1 = CO_j+1.lo + CO_j.hi, D likewise
+    constexpr int JE = (M + 1) / 2 + 1;
+    unsigned long long CE[JE], CO[JE], DE[JE], DO[JE];
 #pragma unroll
-    for (int i = 0; i < M; ++i) CD[i] = 0ull;
-    float C0 = 0.f;
+    for (int j = 0; j < JE; ++j) CE[j] = CO[j] = DE[j] = DO[j] = 0ull;
     float E0[M];
     unsigned sl = 0;
     if (s0.t < p.ntot) {
@@ -1019,6 +1039,19 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
         load_coef32<M>(tab, bk, na);
 #pragma unroll
         for (int k = 0; k <= M; ++k) na[k] = -na[k];
+        // loop-invariant coefficient pairs of the a7 pass, loaded as pairs (table W)
+        unsigned long long NA1P[JE], NA0P[JE], B0P[JE], B1P[JE];
+        {
+            const unsigned long long* wp = reinterpret_cast<const unsigned long long*>(tab + C::OW);
+#pragma unroll
+            for (int j = 0; j < JE; ++j) {
+                NA1P[j] = wp[j];
+                NA0P[j] = wp[JE + j];
+                B0P[j] = wp[2 * JE + j];
+                B1P[j] = wp[3 * JE + j];
+            }
+        }
+        const float na1 = na[1];
         mbar_wait(barXY, phXY);
         phXY ^= 1u;
         tmem_wait_st();
@@ -1051,16 +1084,25 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
 #pragma unroll
                 for (int i = 0; i < M; ++i) p.gzi[seq * M + i] = w2[i];
         }
-        // a7: one fused pass per lane, backwards in time: g(n) (Eq.7), dx(n) = sum_k b'_k g(n+k)
-        // over dx in place of x, and the correlation sums C_k = sum g(n+k) x(n), D_k = sum g(n+k) y(n)
-        float w[M + 1];                                          // w[k] = g(n + k) after step n
-#pragma unroll
-        for (int k = 0; k < M; ++k) w[k] = din[k];               // (each step first shifts by one)
-        w[M] = 0.f;
+        // a7: one fused pass per lane, backwards in time, two samples (n, n+1) per step.  The g
+        // history is held as even-aligned pairs Ev[j] = (g(n+2j), g(n+2j+1)) only, and every
+        // product is a paired FMA on an aligned pair (coefficient pairs are loop-invariant,
+        // the (x, y) pairs are used as loaded or half-swapped):
+        //   g(n+1) = dy(n+1) + sum_j (na_2j+1, na_2j+2) . Eh[j],                      (Eq.7)
+        //   g(n)   = dy(n) + na_1 g(n+1) + sum_j (na_2j+2, na_2j+3) . Eh[j]  (Eh: before the step)
+        //   dx(n) = sum_j (b'_2j, b'_2j+1) . Ev[j],  dx(n+1) = sum_j (b'_2j-1, b'_2j) . Ev[j]  (Eq.8)
+        //   CE_j += Ev[j] * (x(n), x(n+1))  -> both halves C_2j;
+        //   CO_j += Ev[j] * (x(n+1), x(n))  -> halves C_2j-1 (sample n+1), C_2j+1 (sample n);
+        //   DE / DO likewise with y.
         if constexpr (GT) {                                     // PER_SEQ: one partial row per tile
 #pragma unroll
-            for (int i = 0; i < M; ++i) CD[i] = 0ull;
-            C0 = 0.f;
+            for (int j = 0; j < JE; ++j) CE[j] = CO[j] = DE[j] = DO[j] = 0ull;
+        }
+        unsigned long long Ev[JE];
+        {
+            auto dv = [&](int i) { return i < M ? din[i] : 0.f; };
+#pragma unroll
+            for (int j = 0; j < JE; ++j) Ev[j] = pk2(dv(2 * j), dv(2 * j + 1));
         }
         float* xr = bX + c * C::PITCH;
         const float* yr = bY + c * C::PITCH;
@@ -1078,24 +1120,36 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
                 for (int q = 3; q >= 0; --q) {
                     const float4 xv = *reinterpret_cast<const float4*>(xr + 16 * g + 4 * q);
                     const float4 yv = *reinterpret_cast<const float4*>(yr + 16 * g + 4 * q);
-                    const float xs[4] = {xv.x, xv.y, xv.z, xv.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w};
                     float dxs[4];
 #pragma unroll
-                    for (int e = 3; e >= 0; --e) {
+                    for (int h = 1; h >= 0; --h) {               // samples (n, n+1) = 4q + 2h + (0, 1)
+                        const float xa = h ? xv.z : xv.x, xb = h ? xv.w : xv.y;
+                        const float ya = h ? yv.z : yv.x, yb = h ? yv.w : yv.y;
+                        unsigned long long P1 = 0ull, P0 = 0ull;
 #pragma unroll
-                        for (int k = M; k >= 1; --k) w[k] = w[k - 1];
-                        float acc = dcur[4 * q + e];
+                        for (int j = JE - 1; j >= 0; --j) {      // the newest pair (j = 0) last
+                            if (2 * j + 1 <= M) P1 = ffma2(NA1P[j], Ev[j], P1);
+                            if (2 * j + 2 <= M) P0 = ffma2(NA0P[j], Ev[j], P0);
+                        }
+                        const float g1 = (dcur[4 * q + 2 * h + 1] + lo2(P1)) + hi2(P1);
+                        const float g0 = fmaf(na1, g1, (dcur[4 * q + 2 * h] + lo2(P0)) + hi2(P0));
 #pragma unroll
-                        for (int k = M; k >= 2; --k) acc = fmaf(na[k], w[k], acc);
-                        w[0] = fmaf(na[1], w[1], acc);
-                        float d = bk[0] * w[0];
+                        for (int j = JE - 1; j >= 1; --j) Ev[j] = Ev[j - 1];
+                        Ev[0] = pk2(g0, g1);
+                        const unsigned long long XP = pk2(xa, xb), XS = pk2(xb, xa);
+                        const unsigned long long YP = pk2(ya, yb), YS = pk2(yb, ya);
+                        unsigned long long A0 = 0ull, A1 = 0ull;
 #pragma unroll
-                        for (int k = 1; k <= M; ++k) d = fmaf(bk[k], w[k], d);
-                        dxs[e] = d;
-                        C0 = fmaf(w[0], xs[e], C0);
-                        const unsigned long long XY = pk2(xs[e], ys[e]);
-#pragma unroll
-                        for (int k = 1; k <= M; ++k) CD[k - 1] = ffma2(pk2(w[k], w[k]), XY, CD[k - 1]);
+                        for (int j = JE - 1; j >= 0; --j) {
+                            A0 = ffma2(B0P[j], Ev[j], A0);
+                            A1 = ffma2(B1P[j], Ev[j], A1);
+                            CE[j] = ffma2(Ev[j], XP, CE[j]);
+                            CO[j] = ffma2(Ev[j], XS, CO[j]);
+                            DE[j] = ffma2(Ev[j], YP, DE[j]);
+                            DO[j] = ffma2(Ev[j], YS, DO[j]);
+                        }
+                        dxs[2 * h] = lo2(A0) + hi2(A0);
+                        dxs[2 * h + 1] = lo2(A1) + hi2(A1);
                     }
                     *reinterpret_cast<float4*>(xr + 16 * g + 4 * q) = make_float4(dxs[0], dxs[1], dxs[2], dxs[3]);
                 }
@@ -1104,14 +1158,14 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
         // grad_zi = d(0) = [g(0) .. g(M-1)] (Eq.9, App. A.3) when this chunk starts at n = 0
         if (p.gzi != nullptr && s == 0)
 #pragma unroll
-            for (int i = 0; i < M; ++i) p.gzi[seq * M + i] = w[i];
+            for (int i = 0; i < M; ++i) p.gzi[seq * M + i] = (i & 1) ? hi2(Ev[i >> 1]) : lo2(Ev[i >> 1]);
         V2_TRACE(p.trace, s0.t, 5);
         // dx rows out
         if (p.gx != nullptr) store_rows<M>(bX, p.gx + seq * p.T, p0, p.T, vec, lane, 1);
         // a8 (PER_SEQ): the tile's partial-sum row joins its sequence's fixed-order reduction
         if constexpr (GT) {
             if (p.want_coef) {
-                const double colsum = lane_colsum<M>(bY, lane, C0, CD);
+                const double colsum = lane_colsum<M>(bY, lane, CE, CO, DE, DO);
                 finalize_row<M>(p, seq, p.ntiles, jr, colsum, lane, t64);
             }
         }
@@ -1127,7 +1181,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
     // a8 (SHARED): one row per warp of the grid, indexed by the warp's global id
     if constexpr (!GT) {
         if (p.want_coef) {
-            const double colsum = lane_colsum<M>(bY, lane, C0, CD);
+            const double colsum = lane_colsum<M>(bY, lane, CE, CO, DE, DO);
             finalize_row<M>(p, 0, (int64_t)gridDim.x * NWP, (int64_t)blockIdx.x * NWP + warp, colsum, lane, p.t64);
         }
     }
@@ -1293,6 +1347,21 @@ __global__ void __launch_bounds__(PREP_NT) lti2_prep_kernel(const float* __restr
             o64[C::COEF + tid] = bn[tid];
             o64[C::COEF + M + 1 + tid] = an[tid];
             if (tid == 0) o64[C::A0] = (double)aa[0];
+        }
+        for (int w = tid; w < 8 * C::JP; w += PREP_NT) {    // W (forward group): the Tdf2 pairs
+            const int arr = w / (2 * C::JP), j = (w / 2) % C::JP, h = w & 1;
+            const int k = (arr == 0 || arr == 1) ? 2 * j + 2 + h : 2 * j + 1 + h;
+            float v = 0.f;
+            if (j < (M + 1) / 2 && k <= M) v = (arr & 1) ? -(float)an[k] : (float)bn[k];
+            o32[C::OW + w] = v;
+        }
+        for (int w = tid; w < 8 * C::JP; w += PREP_NT) {    // W (backward group)
+            const int arr = w / (2 * C::JP), j = (w / 2) % C::JP, h = w & 1;
+            const int k = arr == 0 ? 2 * j + 1 + h : arr == 1 ? 2 * j + 2 + h : arr == 2 ? 2 * j + h : 2 * j - 1 + h;
+            float v = 0.f;
+            if (arr < 2) { if (k >= 1 && k <= M) v = -(float)an[k]; }
+            else if (k >= 0 && k <= M) v = (float)bn[k];
+            o32[C::DIR + C::OW + w] = v;
         }
         return;
     }
