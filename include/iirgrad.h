@@ -92,7 +92,7 @@ typedef void *iir_stream_t;  /* a cudaStream_t */
 typedef struct {
     int64_t batch;      /* B >= 1                                                  */
     int64_t length;     /* T >= 1 samples per sequence                             */
-    int32_t order;      /* M: 1..8 (SHARED / PER_SEQ); PER_SAMPLE: 1..31                  */
+    int32_t order;      /* M: 1..8 (SHARED / PER_SEQ); PER_SAMPLE: 1..32                  */
     int32_t form;       /* iir_form_t                                              */
     int32_t dtype;      /* iir_dtype_t                                             */
     int32_t coef_mode;  /* iir_coef_mode_t                                         */
@@ -139,7 +139,14 @@ typedef enum {
      * Same outputs and gradients as the dense path; where A is defective or its eigenbasis is
      * ill-conditioned (kappa(V) > 100 for fp32, 1e4 for fp64) the same kernels run the dense
      * transition instead (per coefficient set, no host round trip). */
-    IIR_FLAG_DIAG = 128
+    IIR_FLAG_DIAG = 128,
+    /* Round-2 engine only (fp32 TDF-II, orders 1..8): the split schedule -- per direction a
+     * carry kernel (chunk aggregates, scan, look-back; writes every lane chunk's carry-in to
+     * the workspace) and an emit kernel with no inter-tile waits -- instead of the fused
+     * single pass.  Same filter and gradients; x and grad_y are read twice. */
+    IIR_FLAG_SPLIT = 256,
+    /* Round-2 engine only: force the fused single pass (overrides the default choice). */
+    IIR_FLAG_FUSED = 512
 } iir_flags_t;
 
 /* Bytes of the forward->backward tape / of the scratch workspace (0 on a bad desc). */

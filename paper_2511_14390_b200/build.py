@@ -38,6 +38,17 @@ def _headers():
         glob.glob(os.path.join(INCLUDE, "*.h"))
 
 
+def _deps(obj, fallback):
+    """Headers an object depends on, from the nvcc -MD file of its last compile (all
+    headers when there is none)."""
+    try:
+        txt = open(obj + ".d").read().replace("\\\n", " ")
+    except OSError:
+        return fallback
+    deps = [d for d in txt.split(":", 1)[1].split() if d.startswith(CSRC) or d.startswith(INCLUDE)]
+    return [d for d in deps if os.path.exists(d)] or fallback
+
+
 def _stale(target, deps):
     if not os.path.exists(target):
         return True
@@ -55,12 +66,13 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     for s in srcs:
         o = os.path.join(BUILD, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
-        if force or _stale(o, [s] + hdrs):
+        if force or _stale(o, [s] + _deps(o, hdrs)):
             todo.append((s, o))
 
     def compile_one(so):
         s, o = so
-        cmd = [NVCC] + FLAGS + DEFS + (["-Xptxas", "-v"] if verbose else []) + ["-c", s, "-o", o + ".tmp"]
+        cmd = [NVCC] + FLAGS + DEFS + (["-Xptxas", "-v"] if verbose else []) + \
+            ["-MD", "-MF", o + ".d", "-c", s, "-o", o + ".tmp"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {s}:\n{r.stdout}\n{r.stderr}")

@@ -29,7 +29,8 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
 // ------------------------------------------------------- instrumentation ----
 static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_phi", "tv_chain", "tv_fwd",
                                         "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd", "state_carry", "tv_fir",
-                                        "diag_prep", "diag_agg", "diag_scan", "diag_fwd", "diag_bwd", "diag_red"};
+                                        "diag_prep", "diag_agg", "diag_scan", "diag_fwd", "diag_bwd", "diag_red",
+                                        "lti_fcarry", "lti_bcarry"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;
@@ -112,6 +113,13 @@ static bool use_v2(const iir_desc_t* d) {
     return d->order >= 6;
 }
 
+// Round-2 schedule: split carry / emit kernels or the fused single pass.
+static bool use_split(const iir_desc_t* d) {
+    if (d->flags & IIR_FLAG_SPLIT) return true;
+    if (d->flags & IIR_FLAG_FUSED) return false;
+    return false;
+}
+
 static int scan_tile_samples(const iir_desc_t* d) {
     if (use_v2(d)) return v2::tile_samples(d->order);
     return d->form == IIR_SS ? rec_tile_samples(d->dtype, d->order) : tile_samples(d->dtype, d->order);
@@ -139,7 +147,7 @@ static iir_status_t check_desc(const iir_desc_t* d) {
         return fail(IIR_EINVAL, "IIR_FLAG_PER_SAMPLE_B needs IIR_COEF_PER_SAMPLE");
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) {
         if (d->form != IIR_DF2) return fail(IIR_EUNSUPPORTED, "per-sample coefficients: only the DF form");
-        if (d->order < 1 || d->order > TV_MAX_M) return fail(IIR_EUNSUPPORTED, "per-sample order must be 1..31");
+        if (d->order < 1 || d->order > TV_MAX_M) return fail(IIR_EUNSUPPORTED, "per-sample order must be 1..32");
         if (!tv_supported(d->order)) return fail(IIR_EUNSUPPORTED, "per-sample order not compiled in");
         return IIR_OK;
     }
@@ -203,9 +211,10 @@ static Layout layout(const iir_desc_t* d) {
     L.ws_sent_bytes = o - L.ws_sent;
     L.ws_part = o; o += al256((L.ntot + 64) * NGP * 8);
     L.ws_part2 = o; o += al256(L.ngroups * NGP * 8);
+    L.v2 = use_v2(d);
+    if (L.v2) { L.ws_carr = o; o += al256((size_t)L.ntot * 32 * M * 4); }   // split schedule: lane carry-ins
     L.ws_bytes = o;
     o = 0;
-    L.v2 = use_v2(d);
     if (L.v2) {
         L.tp_t64 = o; o += al256((size_t)L.ncoef * v2::tab64_doubles(M) * 8);
         L.tp_t32 = o; o += al256((size_t)L.ncoef * v2::tab32_floats(M) * 4);
@@ -336,6 +345,8 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
         f.B = d->batch; f.T = d->length; f.ntiles = (int)L.ntiles; f.ntot = L.ntot;
         f.vec = (d->length % 4 == 0) && aligned16(x) && aligned16(y);
         f.trace = g_trace;
+        f.carr = reinterpret_cast<float*>(w + L.ws_carr);
+        c.split = use_split(d);
         return v2::run(true, d->order, c);
     }
 
@@ -419,6 +430,8 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
         g.B = d->batch; g.T = d->length; g.ntiles = (int)L.ntiles; g.ntot = L.ntot;
         g.vec = (d->length % 4 == 0) && aligned16(grad_y) && aligned16(x) && aligned16(y) && aligned16(grad_x);
         g.trace = g_trace;
+        g.carr = reinterpret_cast<float*>(w + L.ws_carr);
+        c.split = use_split(d);
         return v2::run(false, d->order, c);
     }
 

@@ -86,6 +86,7 @@ struct FwdArgs {
     CarryWs cw;
     int64_t B, T; int ntiles; int64_t ntot; int vec;
     unsigned long long* trace;                        // debug: 8 %globaltimer stamps per tile (NULL = off)
+    float* carr;                                      // split schedule: lane carry-ins [ntot][32][M]
 };
 struct BwdArgs {
     const float* gy; const float* gzf; const float* x; const float* y;
@@ -95,6 +96,7 @@ struct BwdArgs {
     double* partial; double* partial2; unsigned* gcnt; unsigned* scnt; int64_t ncoef;
     int64_t B, T; int ntiles; int64_t ntot; int vec;
     unsigned long long* trace;
+    float* carr;                                      // split schedule: lane carry-ins [ntot][32][M]
 };
 
 // Debug phase stamps (lane 0): [0] aggregate start, [1] data ready, [2] published, [3] look-back
@@ -104,6 +106,14 @@ struct BwdArgs {
         if ((tr) != nullptr && lane == 0) (tr)[(size_t)(t) * 8 + (k)] = gtimer();       \
     } while (0)
 
+// Debug CTA stamps (thread 0 of the CTA): [0] entry, [1] setup done, [2] tiles done,
+// [3] finalize done, stored after the tile stamps at (ntot + cta) * 8.
+#define V2_CTA_TRACE(tr, ntot, k)                                                       \
+    do {                                                                                \
+        if ((tr) != nullptr && threadIdx.x == 0)                                        \
+            (tr)[((size_t)(ntot) + blockIdx.x) * 8 + (k)] = gtimer();                   \
+    } while (0)
+
 // One call of the engine (host side): the launch arguments of both directions.
 struct Call {
     cudaStream_t st;
@@ -111,6 +121,7 @@ struct Call {
     int64_t ncoef; int nlev;
     FwdArgs f;
     BwdArgs g;
+    bool split;                                        // two kernels per direction (lti2s.cuh)
 };
 iir_status_t run(bool fwd, int M, const Call& c);   // lti2.cu
 int tile_samples(int M);
@@ -545,6 +556,70 @@ __device__ __forceinline__ void kform16(const float* K, int k0, const float (&xs
     }
 }
 
+// Chunk aggregates by the recursion itself, from the zero state (the default; IIRG_AGG_KFORM=1
+// selects the K-form above).  The K-form moves 8 broadcast table floats per sample and lane
+// through the shared-memory pipe (128 B/clk per SM): measured on C5 that pipe, not the FMAs,
+// bounded the aggregate (ncu: mio_throttle + short_scoreboard 34 % of stalls).  The
+// recursion keeps its 2M+1 coefficients in registers (loaded once per tile).
+#ifndef IIRG_AGG_KFORM
+#define IIRG_AGG_KFORM 0
+#endif
+// forward (a2): TDF-II over the lane's row, end state v(L) in scan-pair layout
+template <int M>
+__device__ __forceinline__ void agg_rec_fwd16(const Tdf2<M>& c2, const float (&xs)[16],
+                                              unsigned long long (&VP)[Tdf2<M>::NP]) {
+#pragma unroll
+    for (int e = 0; e < 16; e += 2) {
+        float y0, y1;
+        tdf2_step<M>(VP, xs[e], xs[e + 1], c2, y0, y1);
+    }
+}
+// backward (a5): the adjoint g(n) = dy(n) + sum_k na_k g(n+k) over 16 samples of the row,
+// newest last (n = k0 + 15 .. k0); Ev[j] = (g(n+2j), g(n+2j+1)) as in the a7 pass
+template <int M>
+__device__ __forceinline__ void agg_rec_bwd16(const float (&ds)[16], const unsigned long long (&NA1P)[(M + 1) / 2 + 1],
+                                              const unsigned long long (&NA0P)[(M + 1) / 2 + 1], float na1,
+                                              unsigned long long (&Ev)[(M + 1) / 2 + 1]) {
+    constexpr int JE = (M + 1) / 2 + 1;
+#pragma unroll
+    for (int e = 14; e >= 0; e -= 2) {
+        unsigned long long P1 = 0ull, P0 = 0ull;
+#pragma unroll
+        for (int j = JE - 1; j >= 0; --j) {
+            if (2 * j + 1 <= M) P1 = ffma2(NA1P[j], Ev[j], P1);
+            if (2 * j + 2 <= M) P0 = ffma2(NA0P[j], Ev[j], P0);
+        }
+        const float g1 = (ds[e + 1] + lo2(P1)) + hi2(P1);
+        const float g0 = fmaf(na1, g1, (ds[e] + lo2(P0)) + hi2(P0));
+#pragma unroll
+        for (int j = JE - 1; j >= 1; --j) Ev[j] = Ev[j - 1];
+        Ev[0] = pk2(g0, g1);
+    }
+}
+// the adjoint state [g(s) .. g(s+M-1)] in scan-pair layout (odd M: the pad slot zero)
+template <int M>
+__device__ __forceinline__ void ev_to_pairs(const unsigned long long (&Ev)[(M + 1) / 2 + 1],
+                                            unsigned long long (&S)[Cfg<M>::NPR]) {
+#pragma unroll
+    for (int ip = 0; ip < Cfg<M>::NPR; ++ip) S[ip] = (2 * ip + 1 < M) ? Ev[ip] : pk2(lo2(Ev[ip]), 0.f);
+}
+// the backward a7 coefficient pairs (table W of the backward group)
+template <int M>
+__device__ __forceinline__ void load_bwd_pairs(const float* tab, unsigned long long (&NA1P)[(M + 1) / 2 + 1],
+                                               unsigned long long (&NA0P)[(M + 1) / 2 + 1],
+                                               unsigned long long (&B0P)[(M + 1) / 2 + 1],
+                                               unsigned long long (&B1P)[(M + 1) / 2 + 1]) {
+    constexpr int JE = (M + 1) / 2 + 1;
+    const unsigned long long* wp = reinterpret_cast<const unsigned long long*>(tab + Cfg<M>::OW);
+#pragma unroll
+    for (int j = 0; j < JE; ++j) {
+        NA1P[j] = wp[j];
+        NA0P[j] = wp[JE + j];
+        B0P[j] = wp[2 * JE + j];
+        B1P[j] = wp[3 * JE + j];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Tensor memory (TMEM) as a parking area (sm_100a).  Warp w may access TMEM lanes
 // 32 (w % 4) .. 32 (w % 4) + 31; with the 32x32b shape thread i of the warp reads / writes
@@ -600,6 +675,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const __grid_cons
     __shared__ float s_T[NWP][LEVELS][M];
     __shared__ unsigned s_tmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    V2_CTA_TRACE(p.trace, p.ntot, 0);
     float* bX = sm2 + (GT ? 0 : C::STAGE) + warp * 2 * C::BUF;
     float* bY = bX + C::BUF;
     unsigned long long* bar = &s_bar[warp];
@@ -637,6 +713,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const __grid_cons
     __syncthreads();
     tmem_fence_after();
     const unsigned tbase = s_tmem + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)((warp >> 2) * 2 * L);
+    V2_CTA_TRACE(p.trace, p.ntot, 1);
     auto aggregate = [&](const Sched& s, unsigned slot, float (&E)[M]) {
         const float* tab = GT ? p.t32 + s.seq * p.t32_stride : sm2;
         V2_TRACE(p.trace, s.t, 0);
@@ -647,6 +724,12 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const __grid_cons
         unsigned long long S[NPR];
 #pragma unroll
         for (int ip = 0; ip < NPR; ++ip) S[ip] = 0ull;
+#if !IIRG_AGG_KFORM
+        float bc[M + 1], ac[M + 1];
+        load_coef32<M>(tab, bc, ac);
+        Tdf2<M> c2;
+        c2.init_pairs(tab + C::OW, C::JP, bc, ac);
+#endif
 #pragma unroll 1
         for (int g = 0; g < L / 16; ++g) {
             float xs[16];
@@ -656,7 +739,11 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const __grid_cons
                 xs[4 * q] = v.x; xs[4 * q + 1] = v.y; xs[4 * q + 2] = v.z; xs[4 * q + 3] = v.w;
             }
             tmem_st16(slot + 16 * g, xs);
+#if IIRG_AGG_KFORM
             kform16<M>(tab + C::OK_, 16 * g, xs, S);
+#else
+            agg_rec_fwd16<M>(c2, xs, S);
+#endif
         }
         float G[M];
         warp_scan32<M>(tab + C::OP, lane, S, E, G);
@@ -762,10 +849,12 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const __grid_cons
         for (int i = 0; i < M; ++i) E0[i] = E1[i];
         sl ^= 1u;
     }
+    V2_CTA_TRACE(p.trace, p.ntot, 2);
     tmem_fence_before();
     cta_exit(cw, ep, gridDim.x);
     tmem_fence_after();
     if (warp == 0) tmem_dealloc(s_tmem, 512);
+    V2_CTA_TRACE(p.trace, p.ntot, 3);
 }
 
 // ---------------------------------------------------------------------------
@@ -914,6 +1003,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
     __shared__ float s_T[NWP][LEVELS][M];
     __shared__ unsigned s_tmem;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    V2_CTA_TRACE(p.trace, p.ntot, 0);
     float* bI = sm2 + (GT ? 0 : C::STAGE) + warp * 3 * C::BUF;    // dy (incoming)
     float* bX = bI + C::BUF;                                      // x -> dx in place
     float* bY = bX + C::BUF;                                      // y, then partial-sum scratch
@@ -943,6 +1033,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
     tmem_fence_after();
     const unsigned tbase = s_tmem + ((unsigned)(32 * (warp & 3)) << 16) + (unsigned)((warp >> 2) * 2 * L);
     const bool vec = p.vec != 0;
+    V2_CTA_TRACE(p.trace, p.ntot, 1);
     Sched s0, s1;
     s0.init(blockIdx.x * NWP + warp, gridDim.x * NWP, p.B);
     s1 = s0;
@@ -967,6 +1058,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
         unsigned long long S[NPR];
 #pragma unroll
         for (int ip = 0; ip < NPR; ++ip) S[ip] = 0ull;
+#if IIRG_AGG_KFORM
 #pragma unroll 1
         for (int g = 0; g < L / 16; ++g) {
             float xs[16];
@@ -978,6 +1070,28 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
             tmem_st16(slot + 16 * g, xs);
             kform16<M>(tab + C::OK_, 16 * g, xs, S);
         }
+#else
+        {
+            constexpr int JE = (M + 1) / 2 + 1;
+            unsigned long long NA1P[JE], NA0P[JE], B0P[JE], B1P[JE], Ev[JE];
+            load_bwd_pairs<M>(tab, NA1P, NA0P, B0P, B1P);
+            const float na1 = -tab[C::OC + M + 2];
+#pragma unroll
+            for (int j = 0; j < JE; ++j) Ev[j] = 0ull;
+#pragma unroll 1
+            for (int g = L / 16 - 1; g >= 0; --g) {
+                float xs[16];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float4 v = *reinterpret_cast<const float4*>(row + 16 * g + 4 * q);
+                    xs[4 * q] = v.x; xs[4 * q + 1] = v.y; xs[4 * q + 2] = v.z; xs[4 * q + 3] = v.w;
+                }
+                tmem_st16(slot + 16 * g, xs);
+                agg_rec_bwd16<M>(xs, NA1P, NA0P, na1, Ev);
+            }
+            ev_to_pairs<M>(Ev, S);
+        }
+#endif
         float G[M];
         warp_scan32<M>(tab + C::OP, lane, S, E, G);
         float X0[M];
@@ -1178,6 +1292,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
         sl ^= 1u;
         __syncwarp();
     }
+    V2_CTA_TRACE(p.trace, p.ntot, 2);
     // a8 (SHARED): one row per warp of the grid, indexed by the warp's global id
     if constexpr (!GT) {
         if (p.want_coef) {
@@ -1189,6 +1304,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
     cta_exit(cw, ep, gridDim.x);
     tmem_fence_after();
     if (warp == 0) tmem_dealloc(s_tmem, 512);
+    V2_CTA_TRACE(p.trace, p.ntot, 3);
 }
 
 // ---------------------------------------------------------------------------

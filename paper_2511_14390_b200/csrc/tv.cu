@@ -1,6 +1,6 @@
 // tv.cu -- host side of the per-sample (time-varying) all-pole DF path
 // (IIR_COEF_PER_SAMPLE): layout and dispatch; the per-order kernels are
-// instantiated in tv_o1.cu .. tv_o4.cu (every order 1..31).
+// instantiated in tv_o1.cu .. tv_o4.cu (every order 1..32).
 #include <mutex>
 
 #include "host.h"
@@ -8,7 +8,7 @@
 
 namespace iirg {
 
-#define IIRG_TV_ORDERS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31)
+#define IIRG_TV_ORDERS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32)
 #define IIRG_EXTERN(m)                                                                                         \
     extern template iir_status_t tv_order<float, m>(int, const iir_desc_t*, const Layout&, TvArgs&,            \
                                                     const void*, const void*, const void*, const void*, void*, \
@@ -67,7 +67,7 @@ static iir_status_t tv_op(int op, const iir_desc_t* d, const Layout& L, TvArgs& 
         IIRG_TV_ORDERS(IIRG_CASE)
 #undef IIRG_CASE
     }
-    return fail(IIR_EUNSUPPORTED, "per-sample order must be 1..31");
+    return fail(IIR_EUNSUPPORTED, "per-sample order must be 1..32");
 }
 template <typename T>
 static iir_status_t fir_dispatch(bool fwd, const iir_desc_t* d, const void* b, const void* u, const void* zi,

@@ -57,7 +57,11 @@ struct TvArgs {
 // measured 2.7e-5 y error and 2e-4 grad_a error on config 3's 32 sequences).
 template <typename T, int M, typename A = T>
 __global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs p) {
-    static_assert(M + 1 <= 32, "one lane per basis state plus one for the input");
+    static_assert(M <= 32, "orders 1..32");
+    // Columns: lane l of column block cb carries column col = 32 cb + l (col < M: basis
+    // state e_col, col = M: the input response w).  Orders <= 31 need one block; order 32
+    // runs a second block for the input column (the segment's coefficients staged again).
+    constexpr int NCB = (M + 1 + 31) / 32;
     // With A wider than T the staged chunk is converted ONCE into an A copy (each lane
     // converts 1/32 of it) instead of every lane converting all M coefficients of every
     // sample: the F2F conversions, not the FMAs, bounded the fp64-accumulating kernel.
@@ -86,9 +90,13 @@ __global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs 
         }
         if (lane < TV_CH) sx[warp][b][lane] = (lane < cnt) ? xrow[c + lane] : T(0);
     };
+#pragma unroll 1
+    for (int cb = 0; cb < NCB; ++cb) {
+    const int col = 32 * cb + lane;
     A v[M];
 #pragma unroll
-    for (int i = 0; i < M; ++i) v[i] = (lane == i) ? A(1) : A(0);
+    for (int i = 0; i < M; ++i) v[i] = (col == i) ? A(1) : A(0);
+    __syncwarp();
     stage(n0, 0);
     cp_async_commit();
     int b = 0;
@@ -111,7 +119,7 @@ __global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs 
         if (cnt == TV_CH) {
 #pragma unroll
             for (int s2 = 0; s2 < TV_CH; ++s2) {
-                A yn = (lane == M) ? A(sx[warp][b][s2]) : A(0);
+                A yn = (col == M) ? A(sx[warp][b][s2]) : A(0);
                 A cf[M];
                 if constexpr ((M * sizeof(A)) % 16 == 0) {
 #pragma unroll
@@ -123,15 +131,24 @@ __global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs 
 #pragma unroll
                     for (int i = 0; i < M; ++i) cf[i] = cs[s2 * M + i];
                 }
+                if constexpr (sizeof(A) == 8 && M >= 8) {
+                    // fp64: four independent partial sums (terms i = 3 mod 4 ... 0 mod 4) cut the
+                    // dependent DFMA chain from M to M/4 + 2 (latency, not the FP64 pipe, bound it)
+                    A ps[4] = {yn, A(0), A(0), A(0)};
 #pragma unroll
-                for (int i = M - 1; i >= 0; --i) yn = fma(-cf[i], v[i], yn);
+                    for (int i = M - 1; i >= 0; --i) ps[i & 3] = fma(-cf[i], v[i], ps[i & 3]);
+                    yn = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+                } else {
+#pragma unroll
+                    for (int i = M - 1; i >= 0; --i) yn = fma(-cf[i], v[i], yn);
+                }
 #pragma unroll
                 for (int i = M - 1; i >= 1; --i) v[i] = v[i - 1];
                 v[0] = yn;
             }
         } else {                                   // ragged last chunk: exactly cnt samples
             for (int s2 = 0; s2 < cnt; ++s2) {
-                A yn = (lane == M) ? A(sx[warp][b][s2]) : A(0);
+                A yn = (col == M) ? A(sx[warp][b][s2]) : A(0);
 #pragma unroll
                 for (int i = M - 1; i >= 0; --i) yn = fma(-cs[s2 * M + i], v[i], yn);
 #pragma unroll
@@ -140,14 +157,15 @@ __global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs 
             }
         }
     }
-    if (lane < M) {
+    if (col < M) {
         T* ph = static_cast<T*>(p.phi) + seg * M * M;
 #pragma unroll
-        for (int i = 0; i < M; ++i) ph[i * M + lane] = (T)v[i];            // column `lane`
-    } else if (lane == M) {
+        for (int i = 0; i < M; ++i) ph[i * M + col] = (T)v[i];             // column `col`
+    } else if (col == M) {
 #pragma unroll
         for (int i = 0; i < M; ++i) p.w[seg * M + i] = (double)v[i];
     }
+    }                                                                    // column blocks
 }
 
 // ---------------------------------------------------------------------------

@@ -194,7 +194,11 @@ static iir_status_t tv_fwd_m(const Layout& L, TvArgs& a, cudaStream_t st) {
     const unsigned nseg_tot = (unsigned)L.ntot;
     iir_status_t s = launch(K_TV_PHI, st, [&] {
         // fp64 accumulation of the segment transitions for either data type (see tv_phi_kernel)
+#if IIRG_TV_PHI_F32
+        tv_phi_kernel<T, M, T><<<(nseg_tot + TV_PHI_WARPS - 1) / TV_PHI_WARPS, 32 * TV_PHI_WARPS, 0, st>>>(a);
+#else
         tv_phi_kernel<T, M, double><<<(nseg_tot + TV_PHI_WARPS - 1) / TV_PHI_WARPS, 32 * TV_PHI_WARPS, 0, st>>>(a);
+#endif
     });
     if (s != IIR_OK) return s;
     s = tv_chain2<T, M, false>(a, a.zi, st);

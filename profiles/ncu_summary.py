@@ -20,6 +20,15 @@ KEYS = [
     ("launch__grid_size", "grid", 1),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem_bank_conflicts", 1),
     ("smsp__inst_executed.sum", "warp_instructions", 1),
+    # pipe utilisation: FMA (fp32 incl. FFMA2), FP64, ALU, LSU, tensor
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "pipe_fma_pct", 1),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "pipe_fma_cycles_pct", 1),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "pipe_fp64_pct", 1),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "pipe_fp64_cycles_pct", 1),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "pipe_alu_pct", 1),
+    ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "pipe_lsu_pct", 1),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "pipe_tensor_pct", 1),
+    ("lts__t_sectors_srcunit_tex_op_read.sum", "l2_read_sectors", 1),
 ]
 
 

@@ -79,12 +79,22 @@ def test_no_initial_conditions():
     check(p, "f32")
 
 
-def test_every_order_up_to_31_supported_32_rejected():
-    """Every per-sample order 1..31 is compiled (the Phi kernel holds one lane per basis
-    state plus one for the input, so 31 is the largest); 32 is rejected before any launch."""
-    for M in range(1, 32):
+def test_every_order_up_to_32_supported_33_rejected():
+    """Every per-sample order 1..32 is compiled (orders up to 32 for the
+    per-sample path; the Phi kernel runs a second column block at 32); 33 is rejected
+    before any launch."""
+    for M in range(1, 33):
         assert B.iir_tape_bytes(B.make_desc(1, 100, M, "df", torch.float32, B.IIR_COEF_PER_SAMPLE)) > 0, M
-    assert B.iir_tape_bytes(B.make_desc(1, 100, 32, "df", torch.float32, B.IIR_COEF_PER_SAMPLE)) == 0
+    assert B.iir_tape_bytes(B.make_desc(1, 100, 33, "df", torch.float32, B.IIR_COEF_PER_SAMPLE)) == 0
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("M", [9, 18, 31, 32])
+def test_lpc_orders(M, dtype):
+    """LPC orders the round-1 build rejected (9, 18) and the two column-block edge (31, 32)
+    of the segment-transition kernel, several segments and a ragged tail."""
+    p = inputs.tv_allpole_problem(2500 + M, batch=3, length=3 * 512 + 77, order=M, dtype=dtype)
+    check(p, dtype)
 
 
 def test_autograd_allpole_tv():

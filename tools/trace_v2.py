@@ -14,9 +14,32 @@ import bench  # noqa: E402
 from paper_2511_14390_b200 import _binding as B  # noqa: E402
 
 
+def summarize_carry(name, tr, ntot):
+    """Carry-kernel stamps: [0] start [1] data [5] K-form done [6] scan done [2] published
+    [3] look-back start [4] carry known."""
+    t = tr[:ntot * 8].reshape(ntot, 8).astype(np.int64)
+    t = t[t[:, 0] > 0]
+    d = {"data wait": t[:, 1] - t[:, 0], "K-form": t[:, 5] - t[:, 1], "warp scan": t[:, 6] - t[:, 5],
+         "publish": t[:, 2] - t[:, 6], "until look-back": t[:, 3] - t[:, 2], "look-back+lane carry": t[:, 4] - t[:, 3]}
+    print(f"== {name}: {len(t)} tiles")
+    for k, v in d.items():
+        v = v / 1e3
+        print(f"   {k:22s} p10 {np.percentile(v, 10):7.2f}  p50 {np.percentile(v, 50):7.2f}  p90 {np.percentile(v, 90):7.2f}"
+              f"  mean {v.mean():7.2f} us")
+
+
 def summarize(name, tr, ntot):
     t = tr[:ntot * 8].reshape(ntot, 8).astype(np.int64)
-    t0 = t[:, 0].min()
+    c = tr[ntot * 8:].reshape(-1, 8).astype(np.int64)
+    c = c[c[:, 0] > 0]
+    t = t[t[:, 0] > 0]
+    t0 = min(t[:, 0].min(), c[:, 0].min()) if len(c) else t[:, 0].min()
+    if len(c):
+        cs = (c[:, :4] - t0) / 1e3
+        print(f"== {name}: {len(c)} CTAs: entry p50 {np.median(cs[:, 0]):.2f} max {cs[:, 0].max():.2f}; setup done p50 "
+              f"{np.median(cs[:, 1]):.2f} max {cs[:, 1].max():.2f}; tiles done p50 {np.median(cs[:, 2]):.2f} max "
+              f"{cs[:, 2].max():.2f}; exit p50 {np.median(cs[:, 3]):.2f} max {cs[:, 3].max():.2f} us")
+        ntot = len(t)
     st = (t[:, :7] - t0) / 1e3                     # us
     span = (t[:, 6].max() - t0) / 1e3
     d = {"data wait": st[:, 1] - st[:, 0], "aggregate": st[:, 2] - st[:, 1], "until look-back": st[:, 3] - st[:, 2],
@@ -36,14 +59,16 @@ def summarize(name, tr, ntot):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c5")
+    ap.add_argument("--engine", default="auto")
     a = ap.parse_args()
-    w = dict(bench.WORKLOADS[a.workload], key=a.workload)
+    w = dict(bench.WORKLOADS[a.workload], key=a.workload, engine=a.engine)
     prob = bench.Problem(w, 0, 1, 2)
     s = torch.cuda.Stream()
     ts = 32 * int(os.environ.get("IIRG_V2_L", "64"))
     ntot = w["batch"] * ((w["length"] + ts - 1) // ts)
-    buf = torch.zeros(ntot * 8 + 64, dtype=torch.int64, device="cuda")
-    buf2 = torch.zeros(ntot * 8 + 64, dtype=torch.int64, device="cuda")
+    half = (ntot + 4096) * 8                      # split schedule: carry kernels trace into the 2nd half
+    buf = torch.zeros(2 * half, dtype=torch.int64, device="cuda")
+    buf2 = torch.zeros(2 * half, dtype=torch.int64, device="cuda")
     for rep in range(3):
         with torch.cuda.stream(s):
             prob.step(0, s)
@@ -60,8 +85,14 @@ def main():
                            prob.tb, st["gx"], prob.gb, prob.ga, prob.gzi, prob.ws, prob.wb, s)
             B.iir_debug_trace(None)
         torch.cuda.synchronize()
-    summarize("forward", buf.cpu().numpy(), ntot)
-    summarize("backward", buf2.cpu().numpy(), ntot)
+    b1, b2 = buf.cpu().numpy(), buf2.cpu().numpy()
+    if b1[half:].any():
+        summarize("forward carry", b1[half:], ntot)
+        summarize_carry("forward carry phases", b1[half:], ntot)
+    summarize("forward", b1[:half], ntot)
+    if b2[half:].any():
+        summarize("backward carry", b2[half:], ntot)
+    summarize("backward", b2[:half], ntot)
 
 
 if __name__ == "__main__":
