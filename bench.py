@@ -81,8 +81,7 @@ def algorithmic_bytes(w):
     # HBM bytes per kernel the method must move: fwd reads x, writes y (+u for DF);
     # bwd reads dy, x, y (TDF) or dy, u (DF) and writes dx: 24 B/sample in fp32
     if w["form"] == "tdf":
-        # split schedule: lti_fcarry / lti_bcarry re-read x / dy (design overhead, counted)
-        return dict(lti_fwd=2 * s, lti_bwd=4 * s, lti_fcarry=s, lti_bcarry=s)
+        return dict(lti_fwd=2 * s, lti_bwd=4 * s)
     return dict(lti_fwd=3 * s, lti_bwd=3 * s)
 
 
@@ -211,8 +210,7 @@ class Problem:
         # the workspace is cleared once; every completed call leaves it cleared
         # engine: auto (by order), v1 (round-1 CTA tiles), v2 (round-2 persistent warp tiles);
         # grad_y is resident before the step: the backward may read it while the forward drains
-        sched = {"auto": 0, "v1": B.IIR_FLAG_LEGACY_LTI, "v2": B.IIR_FLAG_ENGINE_V2 | B.IIR_FLAG_FUSED,
-                 "v2s": B.IIR_FLAG_ENGINE_V2 | B.IIR_FLAG_SPLIT}[w.get("engine", "auto")]
+        sched = {"auto": 0, "v1": B.IIR_FLAG_LEGACY_LTI, "v2": B.IIR_FLAG_ENGINE_V2}[w.get("engine", "auto")]
         sched |= B.IIR_FLAG_GRAD_Y_EARLY
         if w.get("fir"):
             sched |= B.IIR_FLAG_PER_SAMPLE_B
@@ -568,9 +566,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--engine", default="auto", choices=["auto", "v1", "v2", "v2s"],
-                    help="fp32 TDF engine: auto (by order), v1 (round-1 CTA tiles), v2 (round-2 warp tiles, "
-                         "fused single pass), v2s (round-2, split carry / emit kernels)")
+    ap.add_argument("--engine", default="auto", choices=["auto", "v1", "v2"],
+                    help="fp32 TDF engine: auto (by order), v1 (round-1 CTA tiles), v2 (round-2 warp tiles)")
     args = ap.parse_args()
     w = dict(WORKLOADS[args.workload], key=args.workload, engine=args.engine)
 

@@ -120,7 +120,7 @@ typedef enum {
     IIR_FLAG_PER_SAMPLE_B = 8,
     /* Engine of fp32 TDF-II with SHARED / PER_SEQ coefficients.
      * Default: the round-2 engine (persistent warp tiles, TMEM parking, fused backward)
-     * from order 6 up, the round-1 engine (one CTA per tile) below, by measured speed.
+     * from order 4 up, the round-1 engine (one CTA per tile) below, by measured speed.
      * IIR_FLAG_LEGACY_LTI forces the round-1 engine, IIR_FLAG_ENGINE_V2 the round-2 one
      * (both compute the same filter and gradients; they differ in rounding only). */
     IIR_FLAG_LEGACY_LTI = 16,
@@ -139,14 +139,7 @@ typedef enum {
      * Same outputs and gradients as the dense path; where A is defective or its eigenbasis is
      * ill-conditioned (kappa(V) > 100 for fp32, 1e4 for fp64) the same kernels run the dense
      * transition instead (per coefficient set, no host round trip). */
-    IIR_FLAG_DIAG = 128,
-    /* Round-2 engine only (fp32 TDF-II, orders 1..8): the split schedule -- per direction a
-     * carry kernel (chunk aggregates, scan, look-back; writes every lane chunk's carry-in to
-     * the workspace) and an emit kernel with no inter-tile waits -- instead of the fused
-     * single pass.  Same filter and gradients; x and grad_y are read twice. */
-    IIR_FLAG_SPLIT = 256,
-    /* Round-2 engine only: force the fused single pass (overrides the default choice). */
-    IIR_FLAG_FUSED = 512
+    IIR_FLAG_DIAG = 128
 } iir_flags_t;
 
 /* Bytes of the forward->backward tape / of the scratch workspace (0 on a bad desc). */

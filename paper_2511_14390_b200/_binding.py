@@ -28,8 +28,6 @@ IIR_FLAG_LEGACY_LTI = 16
 IIR_FLAG_ENGINE_V2 = 32
 IIR_FLAG_GRAD_Y_EARLY = 64
 IIR_FLAG_DIAG = 128
-IIR_FLAG_SPLIT = 256
-IIR_FLAG_FUSED = 512
 
 FORMS = {"df": IIR_DF2, "tdf": IIR_TDF2, "ss": IIR_SS, IIR_DF2: IIR_DF2, IIR_TDF2: IIR_TDF2, IIR_SS: IIR_SS}
 DTYPES = {torch.float32: IIR_F32, torch.float64: IIR_F64}

@@ -29,8 +29,7 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
 // ------------------------------------------------------- instrumentation ----
 static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_phi", "tv_chain", "tv_fwd",
                                         "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd", "state_carry", "tv_fir",
-                                        "diag_prep", "diag_agg", "diag_scan", "diag_fwd", "diag_bwd", "diag_red",
-                                        "lti_fcarry", "lti_bcarry"};
+                                        "diag_prep", "diag_agg", "diag_scan", "diag_fwd", "diag_bwd", "diag_red"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;
@@ -99,9 +98,9 @@ iir_status_t rec_run(bool fwd, int dtype, int M, const Layout& L, const LtiFwdAr
 
 // Engine choice for fp32 TDF-II with fixed coefficients.  The round-2 engine (lti2.cuh:
 // persistent warp tiles, TMEM parking, fp32 carries, fused backward) is the default from
-// order 6 up; below it the round-1 engine (lti.cuh: one CTA per tile) is faster on the
-// measured shapes (B200: C5 M=8 205 vs 223 us/step, C4 M=4 190 vs
-// 175, C2 M=2 46 vs 32).  IIR_FLAG_ENGINE_V2 / IIR_FLAG_LEGACY_LTI force either one.
+// order 4 up; below it the round-1 engine (lti.cuh: one CTA per tile) is faster on the
+// measured shapes (B200, graph-timed us/step: C5 M=8 162 vs 216,
+// C4 M=4 168 vs 174, C2 M=2 42 vs 33).  IIR_FLAG_ENGINE_V2 / IIR_FLAG_LEGACY_LTI force either one.
 static bool v2_capable(const iir_desc_t* d) {
     return d->form == IIR_TDF2 && d->dtype == IIR_F32 &&
            (d->coef_mode == IIR_COEF_SHARED || d->coef_mode == IIR_COEF_PER_SEQ) && d->order >= 1 && d->order <= 8 &&
@@ -110,14 +109,7 @@ static bool v2_capable(const iir_desc_t* d) {
 static bool use_v2(const iir_desc_t* d) {
     if (!v2_capable(d)) return false;
     if (d->flags & IIR_FLAG_ENGINE_V2) return true;
-    return d->order >= 6;
-}
-
-// Round-2 schedule: split carry / emit kernels or the fused single pass.
-static bool use_split(const iir_desc_t* d) {
-    if (d->flags & IIR_FLAG_SPLIT) return true;
-    if (d->flags & IIR_FLAG_FUSED) return false;
-    return false;
+    return d->order >= 4;
 }
 
 static int scan_tile_samples(const iir_desc_t* d) {
@@ -212,7 +204,6 @@ static Layout layout(const iir_desc_t* d) {
     L.ws_part = o; o += al256((L.ntot + 64) * NGP * 8);
     L.ws_part2 = o; o += al256(L.ngroups * NGP * 8);
     L.v2 = use_v2(d);
-    if (L.v2) { L.ws_carr = o; o += al256((size_t)L.ntot * 32 * M * 4); }   // split schedule: lane carry-ins
     L.ws_bytes = o;
     o = 0;
     if (L.v2) {
@@ -345,8 +336,6 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
         f.B = d->batch; f.T = d->length; f.ntiles = (int)L.ntiles; f.ntot = L.ntot;
         f.vec = (d->length % 4 == 0) && aligned16(x) && aligned16(y);
         f.trace = g_trace;
-        f.carr = reinterpret_cast<float*>(w + L.ws_carr);
-        c.split = use_split(d);
         return v2::run(true, d->order, c);
     }
 
@@ -430,8 +419,6 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
         g.B = d->batch; g.T = d->length; g.ntiles = (int)L.ntiles; g.ntot = L.ntot;
         g.vec = (d->length % 4 == 0) && aligned16(grad_y) && aligned16(x) && aligned16(y) && aligned16(grad_x);
         g.trace = g_trace;
-        g.carr = reinterpret_cast<float*>(w + L.ws_carr);
-        c.split = use_split(d);
         return v2::run(false, d->order, c);
     }
 

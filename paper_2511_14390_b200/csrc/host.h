@@ -14,8 +14,7 @@ namespace iirg {
 iir_status_t fail(iir_status_t st, const std::string& msg);
 
 enum Kind { K_LTI_PREP = 0, K_LTI_FWD, K_LTI_BWD, K_TV_PHI, K_TV_CHAIN, K_TV_FWD, K_TV_BWD_AGG, K_TV_BWD, K_REC_FWD,
-            K_REC_BWD, K_STATE_CARRY, K_TV_FIR, K_DIAG_PREP, K_DIAG_AGG, K_DIAG_SCAN, K_DIAG_FWD, K_DIAG_BWD, K_DIAG_RED,
-            K_LTI_CARRY, K_LTI_BCARRY, K_NUM };
+            K_REC_BWD, K_STATE_CARRY, K_TV_FIR, K_DIAG_PREP, K_DIAG_AGG, K_DIAG_SCAN, K_DIAG_FWD, K_DIAG_BWD, K_DIAG_RED, K_NUM };
 
 // Launch bookkeeping: counts every kernel and (when profiling is on) brackets it
 // with CUDA events on its stream.
@@ -62,7 +61,6 @@ struct Layout {
     size_t tp_tab = 0, tp_u = 0, tp_extra = 0, tp_bytes = 0;
     size_t tp_t64 = 0, tp_t32 = 0;                         // v2 engine tables (lti2.cuh)
     size_t ws_err = 0;                                     // error word (look-back timeout)
-    size_t ws_carr = 0;                                    // round-2 split schedule: lane carry-ins
     bool v2 = false;
 };
 

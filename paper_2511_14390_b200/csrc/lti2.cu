@@ -7,7 +7,6 @@
 
 #include "host.h"
 #include "lti2.cuh"
-#include "lti2s.cuh"
 #include "lti_host.cuh"
 
 namespace iirg {
@@ -15,18 +14,6 @@ namespace v2 {
 
 constexpr int NWF = IIRG_V2_NWF;   // warps per CTA, forward
 constexpr int NWB = IIRG_V2_NWB;   // warps per CTA, backward
-#ifndef IIRG_S_NWC
-#define IIRG_S_NWC 12
-#endif
-#ifndef IIRG_S_NWEF
-#define IIRG_S_NWEF 12
-#endif
-#ifndef IIRG_S_NWEB
-#define IIRG_S_NWEB 8
-#endif
-constexpr int NWC = IIRG_S_NWC;    // split schedule: warps per CTA, carry kernels
-constexpr int NWEF = IIRG_S_NWEF;  //                 forward emit
-constexpr int NWEB = IIRG_S_NWEB;  //                 backward emit
 
 template <int M>
 constexpr size_t smem_bytes(bool gt, int nwp, int nbuf) {
@@ -44,7 +31,6 @@ struct DevInfo {
     bool ready = false;
     int sms = 0;
     int occ[4] = {0, 0, 0, 0};   // fwd shared, fwd global, bwd shared, bwd global
-    int socc[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // split: carry f/b, emit f, emit b  x  (shared, global)
 };
 
 template <int M>
@@ -71,79 +57,10 @@ struct Ops {
                                                           smem_bytes<M>(false, NWB, 3));
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ[3], lti2_bwd_kernel<M, NWB, true>, NWB * 32,
                                                           smem_bytes<M>(true, NWB, 3));
-            split_setup(d);
             (void)cudaGetLastError();
             d.ready = true;
         }
         return d;
-    }
-    // split schedule (lti2s.cuh): shared buffers per warp 2 (carry), 2 (forward emit), 3 (backward emit)
-    template <typename K>
-    static void attr_occ(K k, int nwp, size_t smem, int& occ) {
-        set_smem(k, smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, nwp * 32, smem);
-    }
-    static void split_setup(DevInfo& d) {
-        attr_occ(lti2s_carry_kernel<M, NWC, false, false>, NWC, smem_bytes<M>(false, NWC, CNBUF), d.socc[0]);
-        attr_occ(lti2s_carry_kernel<M, NWC, true, false>, NWC, smem_bytes<M>(true, NWC, CNBUF), d.socc[1]);
-        attr_occ(lti2s_carry_kernel<M, NWC, false, true>, NWC, smem_bytes<M>(false, NWC, CNBUF), d.socc[2]);
-        attr_occ(lti2s_carry_kernel<M, NWC, true, true>, NWC, smem_bytes<M>(true, NWC, CNBUF), d.socc[3]);
-        attr_occ(lti2s_emit_fwd_kernel<M, NWEF, false>, NWEF, smem_bytes<M>(false, NWEF, 2), d.socc[4]);
-        attr_occ(lti2s_emit_fwd_kernel<M, NWEF, true>, NWEF, smem_bytes<M>(true, NWEF, 2), d.socc[5]);
-        attr_occ(lti2s_emit_bwd_kernel<M, NWEB, false>, NWEB, smem_bytes<M>(false, NWEB, 3), d.socc[6]);
-        attr_occ(lti2s_emit_bwd_kernel<M, NWEB, true>, NWEB, smem_bytes<M>(true, NWEB, 3), d.socc[7]);
-    }
-    static unsigned sgrid(const DevInfo& d, int k, int64_t ntot, int nwp) {
-        const int64_t cap = (int64_t)d.sms * (d.socc[k] > 0 ? d.socc[k] : 1);
-        const int64_t need = (ntot + nwp - 1) / nwp;
-        return (unsigned)(need < cap ? need : cap);
-    }
-    static CarryArgs carry_args(const Call& c, bool bwd) {
-        CarryArgs a{};
-        if (!bwd) {
-            a.src = c.f.x; a.x0 = c.f.zi; a.t32 = c.f.t32; a.t32_stride = c.f.t32_stride; a.cw = c.f.cw;
-            a.B = c.f.B; a.T = c.f.T; a.ntiles = c.f.ntiles; a.ntot = c.f.ntot; a.vec = c.f.vec; a.carr = c.f.carr;
-            a.trace = c.f.trace == nullptr ? nullptr : c.f.trace + (c.f.ntot + 4096) * 8;   // 2nd half
-        } else {
-            a.src = c.g.gy; a.x0 = c.g.gzf; a.t32 = c.g.t32 + Cfg<M>::DIR; a.t32_stride = c.g.t32_stride; a.cw = c.g.cw;
-            a.B = c.g.B; a.T = c.g.T; a.ntiles = c.g.ntiles; a.ntot = c.g.ntot; a.vec = c.g.vec; a.carr = c.g.carr;
-            a.trace = c.g.trace == nullptr ? nullptr : c.g.trace + (c.g.ntot + 4096) * 8;
-        }
-        return a;
-    }
-    static iir_status_t split_forward(const Call& c, const DevInfo& d) {
-        const bool gt = c.ncoef > 1;
-        const CarryArgs a = carry_args(c, false);
-        iir_status_t s = launch(K_LTI_CARRY, c.st, [&] {
-            if (gt) launch_pdl(lti2s_carry_kernel<M, NWC, true, false>, sgrid(d, 1, a.ntot, NWC), NWC * 32,
-                               smem_bytes<M>(true, NWC, CNBUF), c.st, a);
-            else launch_pdl(lti2s_carry_kernel<M, NWC, false, false>, sgrid(d, 0, a.ntot, NWC), NWC * 32,
-                            smem_bytes<M>(false, NWC, CNBUF), c.st, a);
-        });
-        if (s != IIR_OK) return s;
-        return launch(K_LTI_FWD, c.st, [&] {
-            if (gt) launch_pdl(lti2s_emit_fwd_kernel<M, NWEF, true>, sgrid(d, 5, c.f.ntot, NWEF), NWEF * 32,
-                               smem_bytes<M>(true, NWEF, 2), c.st, c.f);
-            else launch_pdl(lti2s_emit_fwd_kernel<M, NWEF, false>, sgrid(d, 4, c.f.ntot, NWEF), NWEF * 32,
-                            smem_bytes<M>(false, NWEF, 2), c.st, c.f);
-        });
-    }
-    static iir_status_t split_backward(const Call& c, const DevInfo& d) {
-        const bool gt = c.ncoef > 1;
-        const CarryArgs a = carry_args(c, true);
-        iir_status_t s = launch(K_LTI_BCARRY, c.st, [&] {
-            if (gt) launch_pdl(lti2s_carry_kernel<M, NWC, true, true>, sgrid(d, 3, a.ntot, NWC), NWC * 32,
-                               smem_bytes<M>(true, NWC, CNBUF), c.st, a);
-            else launch_pdl(lti2s_carry_kernel<M, NWC, false, true>, sgrid(d, 2, a.ntot, NWC), NWC * 32,
-                            smem_bytes<M>(false, NWC, CNBUF), c.st, a);
-        });
-        if (s != IIR_OK) return s;
-        return launch(K_LTI_BWD, c.st, [&] {
-            if (gt) launch_pdl(lti2s_emit_bwd_kernel<M, NWEB, true>, sgrid(d, 7, c.g.ntot, NWEB), NWEB * 32,
-                               smem_bytes<M>(true, NWEB, 3), c.st, c.g);
-            else launch_pdl(lti2s_emit_bwd_kernel<M, NWEB, false>, sgrid(d, 6, c.g.ntot, NWEB), NWEB * 32,
-                            smem_bytes<M>(false, NWEB, 3), c.st, c.g);
-        });
     }
     // one resident wave, at most one warp per tile
     static unsigned grid(const DevInfo& d, int k, int64_t ntot, int nwp) {
@@ -159,7 +76,6 @@ struct Ops {
                 c.f.t64_stride, c.nlev);
         });
         if (s != IIR_OK) return s;
-        if (c.split) return split_forward(c, d);
         const bool gt = c.ncoef > 1;
         return launch(K_LTI_FWD, c.st, [&] {
             if (gt) launch_pdl(fwd_kernel<M, true>(), grid(d, 1, c.f.ntot, NWF), NWF * 32, fwd_smem<M>(true), c.st, c.f);
@@ -168,7 +84,6 @@ struct Ops {
     }
     static iir_status_t backward(const Call& c) {
         const DevInfo& d = dev_info();
-        if (c.split) return split_backward(c, d);
         const bool gt = c.ncoef > 1;
         return launch(K_LTI_BWD, c.st, [&] {
             if (gt)

@@ -86,7 +86,6 @@ struct FwdArgs {
     CarryWs cw;
     int64_t B, T; int ntiles; int64_t ntot; int vec;
     unsigned long long* trace;                        // debug: 8 %globaltimer stamps per tile (NULL = off)
-    float* carr;                                      // split schedule: lane carry-ins [ntot][32][M]
 };
 struct BwdArgs {
     const float* gy; const float* gzf; const float* x; const float* y;
@@ -96,7 +95,6 @@ struct BwdArgs {
     double* partial; double* partial2; unsigned* gcnt; unsigned* scnt; int64_t ncoef;
     int64_t B, T; int ntiles; int64_t ntot; int vec;
     unsigned long long* trace;
-    float* carr;                                      // split schedule: lane carry-ins [ntot][32][M]
 };
 
 // Debug phase stamps (lane 0): [0] aggregate start, [1] data ready, [2] published, [3] look-back
@@ -121,7 +119,6 @@ struct Call {
     int64_t ncoef; int nlev;
     FwdArgs f;
     BwdArgs g;
-    bool split;                                        // two kernels per direction (lti2s.cuh)
 };
 iir_status_t run(bool fwd, int M, const Call& c);   // lti2.cu
 int tile_samples(int M);

@@ -1,7 +1,6 @@
 """Both LTI engines for fp32 TDF-II against the fp64 oracle: the round-2 engine (lti2.cuh,
 IIR_FLAG_ENGINE_V2: persistent warp tiles, TMEM parking, fp32 carries, fused backward) and
-the round-1 engine (lti.cuh, IIR_FLAG_LEGACY_LTI), and the round-2 split schedule
-(lti2s.cuh, IIR_FLAG_SPLIT: carry kernel + emit kernel per direction), whichever the default dispatch picks for
+the round-1 engine (lti.cuh, IIR_FLAG_LEGACY_LTI), whichever the default dispatch picks for
 a shape.  Gate: 1e-4 of max|gpu - oracle| / rms(oracle) per output tensor."""
 import numpy as np
 import pytest
@@ -13,8 +12,7 @@ from gpu_util import TOL, compare, run_lti_gpu, run_lti_oracle
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = {"v2": B.IIR_FLAG_ENGINE_V2 | B.IIR_FLAG_FUSED, "v2s": B.IIR_FLAG_ENGINE_V2 | B.IIR_FLAG_SPLIT,
-           "v1": B.IIR_FLAG_LEGACY_LTI}
+ENGINES = {"v2": B.IIR_FLAG_ENGINE_V2, "v1": B.IIR_FLAG_LEGACY_LTI}
 TS2 = 2048                                            # round-2 tile: 32 lanes x 64 samples
 
 
@@ -26,7 +24,7 @@ def check(p, engine, seqs=None):
     return errs
 
 
-@pytest.mark.parametrize("engine", ["v2", "v2s", "v1"])
+@pytest.mark.parametrize("engine", ["v2", "v1"])
 @pytest.mark.parametrize("cfg", ["c2", "c4", "c5"])
 def test_baseline_configs(engine, cfg):
     c = dict(inputs.CONFIGS[cfg])
@@ -37,7 +35,7 @@ def test_baseline_configs(engine, cfg):
     check(p, engine)
 
 
-@pytest.mark.parametrize("engine", ["v2", "v2s", "v1"])
+@pytest.mark.parametrize("engine", ["v2", "v1"])
 @pytest.mark.parametrize("M", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_orders(engine, M):
     p = inputs.lti_problem(12000 + M, form="tdf", order=M, batch=3, length=3 * TS2 + 77, dtype="f32",
@@ -45,14 +43,14 @@ def test_orders(engine, M):
     check(p, engine)
 
 
-@pytest.mark.parametrize("engine", ["v2", "v2s", "v1"])
+@pytest.mark.parametrize("engine", ["v2", "v1"])
 @pytest.mark.parametrize("T", [1, 2, 3, 5, 8, 63, 64, 65, 2047, 2048, 2049, 4095, 4097, 6143, 10007])
 def test_edge_lengths(engine, T):
     p = inputs.lti_problem(13000 + T, form="tdf", order=3, batch=2, length=T, dtype="f32")
     check(p, engine)
 
 
-@pytest.mark.parametrize("engine", ["v2", "v2s", "v1"])
+@pytest.mark.parametrize("engine", ["v2", "v1"])
 @pytest.mark.parametrize("zi,gzf", [(False, False), (True, False), (False, True)])
 def test_initial_condition_paths(engine, zi, gzf):
     p = inputs.lti_problem(14000, form="tdf", order=8, batch=5, length=20000, dtype="f32", zi=zi, gzf=gzf,
@@ -60,7 +58,7 @@ def test_initial_condition_paths(engine, zi, gzf):
     check(p, engine)
 
 
-@pytest.mark.parametrize("engine", ["v2", "v2s", "v1"])
+@pytest.mark.parametrize("engine", ["v2", "v1"])
 @pytest.mark.parametrize("M", [2, 8])
 def test_per_sequence_coefficients(engine, M):
     p = inputs.lti_problem(15000 + M, form="tdf", order=M, batch=7, length=5 * TS2 + 5, dtype="f32",
@@ -68,7 +66,7 @@ def test_per_sequence_coefficients(engine, M):
     check(p, engine)
 
 
-@pytest.mark.parametrize("engine", ["v2", "v2s", "v1"])
+@pytest.mark.parametrize("engine", ["v2", "v1"])
 @pytest.mark.parametrize("a0", [1.7, -0.6])
 def test_unnormalised_a0(engine, a0):
     p = inputs.lti_problem(16000, form="tdf", order=6, batch=2, length=9000, dtype="f32", a0=a0, angles="spread",
@@ -76,7 +74,7 @@ def test_unnormalised_a0(engine, a0):
     check(p, engine)
 
 
-@pytest.mark.parametrize("engine", ["v2", "v2s"])
+@pytest.mark.parametrize("engine", ["v2"])
 @pytest.mark.parametrize("ntiles", [31, 32, 33, 63, 64, 65, 1023, 1024, 1025, 1057])
 def test_v2_lookback_levels(engine, ntiles):
     """Round-2 tile counts around the base-32 look-back levels (closing tiles publish
@@ -86,7 +84,7 @@ def test_v2_lookback_levels(engine, ntiles):
     check(p, engine)
 
 
-@pytest.mark.parametrize("engine", ["v2", "v2s"])
+@pytest.mark.parametrize("engine", ["v2"])
 def test_v2_bitwise_deterministic_per_seq(engine):
     p = inputs.lti_problem(18000, form="tdf", order=7, batch=9, length=7 * TS2 + 11, dtype="f32", coef="per_seq",
                            angles="spread")

@@ -14,20 +14,6 @@ import bench  # noqa: E402
 from paper_2511_14390_b200 import _binding as B  # noqa: E402
 
 
-def summarize_carry(name, tr, ntot):
-    """Carry-kernel stamps: [0] start [1] data [5] K-form done [6] scan done [2] published
-    [3] look-back start [4] carry known."""
-    t = tr[:ntot * 8].reshape(ntot, 8).astype(np.int64)
-    t = t[t[:, 0] > 0]
-    d = {"data wait": t[:, 1] - t[:, 0], "K-form": t[:, 5] - t[:, 1], "warp scan": t[:, 6] - t[:, 5],
-         "publish": t[:, 2] - t[:, 6], "until look-back": t[:, 3] - t[:, 2], "look-back+lane carry": t[:, 4] - t[:, 3]}
-    print(f"== {name}: {len(t)} tiles")
-    for k, v in d.items():
-        v = v / 1e3
-        print(f"   {k:22s} p10 {np.percentile(v, 10):7.2f}  p50 {np.percentile(v, 50):7.2f}  p90 {np.percentile(v, 90):7.2f}"
-              f"  mean {v.mean():7.2f} us")
-
-
 def summarize(name, tr, ntot):
     t = tr[:ntot * 8].reshape(ntot, 8).astype(np.int64)
     c = tr[ntot * 8:].reshape(-1, 8).astype(np.int64)
@@ -66,9 +52,9 @@ def main():
     s = torch.cuda.Stream()
     ts = 32 * int(os.environ.get("IIRG_V2_L", "64"))
     ntot = w["batch"] * ((w["length"] + ts - 1) // ts)
-    half = (ntot + 4096) * 8                      # split schedule: carry kernels trace into the 2nd half
-    buf = torch.zeros(2 * half, dtype=torch.int64, device="cuda")
-    buf2 = torch.zeros(2 * half, dtype=torch.int64, device="cuda")
+    half = (ntot + 4096) * 8                      # tile stamps, then CTA stamps
+    buf = torch.zeros(half, dtype=torch.int64, device="cuda")
+    buf2 = torch.zeros(half, dtype=torch.int64, device="cuda")
     for rep in range(3):
         with torch.cuda.stream(s):
             prob.step(0, s)
@@ -85,14 +71,8 @@ def main():
                            prob.tb, st["gx"], prob.gb, prob.ga, prob.gzi, prob.ws, prob.wb, s)
             B.iir_debug_trace(None)
         torch.cuda.synchronize()
-    b1, b2 = buf.cpu().numpy(), buf2.cpu().numpy()
-    if b1[half:].any():
-        summarize("forward carry", b1[half:], ntot)
-        summarize_carry("forward carry phases", b1[half:], ntot)
-    summarize("forward", b1[:half], ntot)
-    if b2[half:].any():
-        summarize("backward carry", b2[half:], ntot)
-    summarize("backward", b2[:half], ntot)
+    summarize("forward", buf.cpu().numpy(), ntot)
+    summarize("backward", buf2.cpu().numpy(), ntot)
 
 
 if __name__ == "__main__":
