@@ -55,8 +55,11 @@ struct TvArgs {
 // A: accumulation type (fp64 for fp32 data: the basis propagation over a segment
 // sees transient, non-normal growth of the time-varying product; fp32 accumulation
 // measured 2.7e-5 y error and 2e-4 grad_a error on config 3's 32 sequences).
+#ifndef IIRG_PHI_MINB
+#define IIRG_PHI_MINB 1
+#endif
 template <typename T, int M, typename A = T>
-__global__ void __launch_bounds__(32 * TV_PHI_WARPS) tv_phi_kernel(const TvArgs p) {
+__global__ void __launch_bounds__(32 * TV_PHI_WARPS, IIRG_PHI_MINB) tv_phi_kernel(const TvArgs p) {
     static_assert(M <= 32, "orders 1..32");
     // Columns: lane l of column block cb carries column col = 32 cb + l (col < M: basis
     // state e_col, col = M: the input response w).  Orders <= 31 need one block; order 32
