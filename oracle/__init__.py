@@ -64,6 +64,8 @@ def _load():
             lib.orc_tv_allpole.argtypes = [ctypes.c_int, ctypes.c_long] + [_dp] * 10
             lib.orc_tv_df.restype = ctypes.c_int
             lib.orc_tv_df.argtypes = [ctypes.c_int, ctypes.c_long] + [_dp] * 12
+            lib.orc_tv_tdf.restype = ctypes.c_int
+            lib.orc_tv_tdf.argtypes = [ctypes.c_int, ctypes.c_long] + [_dp] * 12
             lib.orc_recurrence.restype = ctypes.c_int
             lib.orc_recurrence.argtypes = [ctypes.c_int, ctypes.c_long] + [_dp] * 8
             _lib = lib
@@ -192,6 +194,39 @@ def tv_df(b, a, x, zi=None, gy=None, gzf=None, threads=None):
             _p(out["gzi"][i]))
         if rc != 0:
             raise ValueError(f"orc_tv_df failed rc={rc}")
+
+    nt = _nthreads(threads, B)
+    if nt == 1:
+        for i in range(B):
+            one(i)
+    else:
+        with ThreadPoolExecutor(nt) as ex:
+            list(ex.map(one, range(B)))
+    return out
+
+
+def tv_tdf(b, a, x, zi=None, gy=None, gzf=None, threads=None):
+    """Batched general time-varying TDF oracle (reading R20); b: (B, N, M+1), a: (B, N, M) monic."""
+    lib = _load()
+    x = _f64(x)
+    B, N = x.shape
+    a = _f64(a).reshape(B, N, -1)
+    M = a.shape[-1]
+    b = _f64(b).reshape(B, N, M + 1)
+    zi = None if zi is None else _f64(zi).reshape(B, M)
+    gy = None if gy is None else _f64(gy).reshape(B, N)
+    gzf = None if gzf is None else _f64(gzf).reshape(B, M)
+    out = dict(y=np.empty((B, N)), zf=np.empty((B, M)), gx=np.empty((B, N)),
+               gb=np.empty((B, N, M + 1)), ga=np.empty((B, N, M)), gzi=np.empty((B, M)))
+
+    def one(i):
+        rc = lib.orc_tv_tdf(
+            M, N, _p(b[i]), _p(a[i]), _p(x[i]), _p(None if zi is None else zi[i]),
+            _p(None if gy is None else gy[i]), _p(None if gzf is None else gzf[i]),
+            _p(out["y"][i]), _p(out["zf"][i]), _p(out["gx"][i]), _p(out["gb"][i]), _p(out["ga"][i]),
+            _p(out["gzi"][i]))
+        if rc != 0:
+            raise ValueError(f"orc_tv_tdf failed rc={rc}")
 
     nt = _nthreads(threads, B)
     if nt == 1:

@@ -38,6 +38,9 @@
  *   R11 its adjoint is Eq.7 with the time-varying A(n+1), C(n+1).
  *   R19 general time-varying DF (b(n) and a(n)): both rows apply at output
  *      time n; a(n) monic (orc_tv_df).
+ *   R20 general time-varying TDF: the TDF realisation of PAPER.md:67-68
+ *      ("replace A with its transpose and swap B and C") at every sample n,
+ *      with the coefficient rows of sample n (orc_tv_tdf).
  */
 #include <stdlib.h>
 #include <string.h>
@@ -377,6 +380,107 @@ int orc_tv_df(int M, long N, const double *b, const double *a, const double *x,
     }
 #undef BUILD_ACD
     free(v); free(dz); free(A); free(C);
+    return 0;
+}
+
+/*
+ * orc_tv_tdf: one sequence of the general time-varying TDF-II filter (SURVEY
+ * 8(f) f2, reading R20): the TDF realisation of PAPER.md:67-68 ("replacing A
+ * with its transpose and swapping B and C") built from the coefficient rows of
+ * sample n, i.e. the per-sample state space of Eqs.4-5 with
+ *   A_f(n) = companion(a(n))^T,  B_f(n) = c(n) = b(n)[1..M] - a(n) b_0(n),
+ *   C_f = e1,  D(n) = b_0(n);
+ *   v(n+1) = A_f(n) v(n) + B_f(n) x(n),   y(n) = C_f^T v(n) + D(n) x(n),
+ * v(0) = zi, zf = v(N) (the scipy lfilter TDF state when the rows are
+ * constant).  Backward: Eq.7 with A_f(n+1), C_f (R11 in transposed form),
+ * Eq.8 with B_f(n), D(n), A.3 with A_f(0); per sample dA_f(n) = dz(n) v(n)^T,
+ * dB_f(n) = dz(n) x(n), dD(n) = dy(n) x(n) (Eqs.6, 9 before the sum over n),
+ * mapped to (b(n), a(n)) as in the LTI TDF chain rule (A_f[k-1][0] = -a_k,
+ * c_{k-1} = b_k - a_k b_0):
+ *   gb_k(n) = dB_f(n)[k-1] (k >= 1),  gb_0(n) = dD(n) - sum_k a_k(n) dB_f(n)[k-1],
+ *   ga_k(n) = -dA_f(n)[k-1][0] - b_0(n) dB_f(n)[k-1].
+ * b: N x (M+1), a: N x M (monic), gb: N x (M+1), ga: N x M (row-major).
+ */
+int orc_tv_tdf(int M, long N, const double *b, const double *a, const double *x,
+               const double *zi, const double *gy, const double *gzf,
+               double *y, double *zf, double *gx, double *gb, double *ga, double *gzi)
+{
+    if (M < 1 || N < 1) return 1;
+    double *v = (double *)malloc((size_t)(N + 1) * M * sizeof(double));
+    double *dz = (double *)malloc((size_t)N * M * sizeof(double));
+    double *Af = (double *)malloc((size_t)M * M * sizeof(double));
+    double *Bf = (double *)malloc((size_t)M * sizeof(double));
+    if (!v || !dz || !Af || !Bf) return 2;
+    const int K = M + 1;
+
+    /* the TDF matrices of sample n: A_f = A^T with A = companion(a(n)), B_f = c(n) */
+#define BUILD_TDF(n)                                                       \
+    do {                                                                   \
+        double *A_ = (double *)calloc((size_t)M * M, sizeof(double));      \
+        for (int k = 1; k <= M; ++k) {                                     \
+            A_[IDX(0, k - 1, M)] = -a[(n) * M + (k - 1)];                  \
+            Bf[k - 1] = b[(n) * K + k] - a[(n) * M + (k - 1)] * b[(n) * K];\
+        }                                                                  \
+        for (int i = 1; i < M; ++i) A_[IDX(i, i - 1, M)] = 1.0;            \
+        for (int i = 0; i < M; ++i)                                        \
+            for (int j = 0; j < M; ++j) Af[IDX(i, j, M)] = A_[IDX(j, i, M)];\
+        free(A_);                                                          \
+    } while (0)
+
+    for (int i = 0; i < M; ++i) v[i] = zi ? zi[i] : 0.0;
+    for (long n = 0; n < N; ++n) {                  /* Eqs.4-5 with A_f(n), B_f(n), D(n) */
+        BUILD_TDF(n);
+        const double *vn = v + n * M;
+        double *vn1 = v + (n + 1) * M;
+        const double yn = vn[0] + b[n * K] * x[n];  /* C_f = e1 */
+        if (y) y[n] = yn;
+        for (int i = 0; i < M; ++i) {
+            double s = Bf[i] * x[n];
+            for (int j = 0; j < M; ++j) s += Af[IDX(i, j, M)] * vn[j];
+            vn1[i] = s;
+        }
+    }
+    if (zf) for (int i = 0; i < M; ++i) zf[i] = v[N * M + i];
+
+    for (int i = 0; i < M; ++i) dz[(N - 1) * M + i] = gzf ? gzf[i] : 0.0;   /* R4 */
+    for (long n = N - 2; n >= 0; --n) {             /* Eq.7: dz(n) = A_f(n+1)^T dz(n+1) + C_f dy(n+1) */
+        BUILD_TDF(n + 1);
+        const double *d1 = dz + (n + 1) * M;
+        const double dy1 = gy ? gy[n + 1] : 0.0;
+        for (int i = 0; i < M; ++i) {
+            double s = (i == 0 ? 1.0 : 0.0) * dy1;
+            for (int j = 0; j < M; ++j) s += Af[IDX(j, i, M)] * d1[j];
+            dz[n * M + i] = s;
+        }
+    }
+    for (long n = 0; n < N; ++n) {                  /* Eq.8 and the per-sample Eqs.6, 9 */
+        BUILD_TDF(n);
+        const double dyn = gy ? gy[n] : 0.0;
+        const double *dzn = dz + n * M;
+        double bfd = 0.0;
+        for (int i = 0; i < M; ++i) bfd += Bf[i] * dzn[i];
+        if (gx) gx[n] = bfd + b[n * K] * dyn;
+        double gb0 = dyn * x[n];                    /* dD(n) */
+        for (int k = 1; k <= M; ++k) {
+            const double dBk = dzn[k - 1] * x[n];   /* dB_f(n)[k-1] */
+            const double dAk0 = dzn[k - 1] * v[n * M + 0];   /* dA_f(n)[k-1][0] */
+            if (gb) gb[n * K + k] = dBk;
+            if (ga) ga[n * M + (k - 1)] = -dAk0 - b[n * K] * dBk;
+            gb0 -= a[n * M + (k - 1)] * dBk;
+        }
+        if (gb) gb[n * K] = gb0;
+    }
+    if (gzi) {                                      /* A.3 with A_f(0), C_f */
+        BUILD_TDF(0);
+        const double dy0 = gy ? gy[0] : 0.0;
+        for (int i = 0; i < M; ++i) {
+            double s = (i == 0 ? 1.0 : 0.0) * dy0;
+            for (int j = 0; j < M; ++j) s += Af[IDX(j, i, M)] * dz[j];
+            gzi[i] = s;
+        }
+    }
+#undef BUILD_TDF
+    free(v); free(dz); free(Af); free(Bf);
     return 0;
 }
 
