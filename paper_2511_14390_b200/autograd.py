@@ -156,19 +156,24 @@ def allpole_tv(x, a, zi=None, return_zf=False):
 
 
 class TVDFFunction(torch.autograd.Function):
-    """y, zf = general per-sample DF-II filter (R19):
-    u(n) = x(n) - sum_i a[.., n, i-1] u(n-i),  y(n) = sum_k b[.., n, k] u(n-k);  zi = [u(-1) .. u(-M)]."""
+    """y, zf = general per-sample filter.
+    form "df" (DESIGN.md R19): u(n) = x(n) - sum_i a[.., n, i-1] u(n-i),  y(n) = sum_k b[.., n, k] u(n-k);
+      zi = [u(-1) .. u(-M)].
+    form "tdf" (R20, the TDF realisation of PAPER.md:67-68 per sample):
+      y(n) = b_0(n) x(n) + v_1(n),  v_i(n+1) = v_{i+1}(n) + b_i(n) x(n) - a_i(n) y(n);  zi = v(0)."""
 
     @staticmethod
-    def forward(ctx, x, b, a, zi):
+    def forward(ctx, x, b, a, zi, form="df"):
         _require_cuda(x, b, a, zi)
         if x.dim() != 2 or a.dim() != 3:
             raise ValueError("lfilter_tv: x must be (B, T), b (B, T, M+1), a (B, T, M)")
+        if form not in ("df", "tdf"):
+            raise ValueError("lfilter_tv: form must be 'df' or 'tdf'")
         Bsz, T = x.shape
         M = a.shape[-1]
         _check(x, [("b", b, [(Bsz, T, M + 1)]), ("a", a, [(Bsz, T, M)]), ("zi", zi, [(Bsz, M)])])
         x, b, a, zi = _c(x), _c(b), _c(a), _c(zi)
-        desc = B.make_desc(Bsz, T, M, "df", x.dtype, B.IIR_COEF_PER_SAMPLE, flags=B.IIR_FLAG_PER_SAMPLE_B)
+        desc = B.make_desc(Bsz, T, M, form, x.dtype, B.IIR_COEF_PER_SAMPLE, flags=B.IIR_FLAG_PER_SAMPLE_B)
         y = torch.empty_like(x)
         zf = torch.empty((Bsz, M), dtype=x.dtype, device=x.device)
         tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
@@ -178,13 +183,16 @@ class TVDFFunction(torch.autograd.Function):
             B.iir_forward(desc, b, a, x, zi, y, zf, tape, tb, ws, wb, _stream(x))
         ctx.desc = desc
         ctx.has_zi = zi is not None
-        ctx.save_for_backward(b, a, zi if zi is not None else torch.empty(0, device=x.device), y, tape)
+        empty = torch.empty(0, device=x.device)
+        ctx.save_for_backward(b, a, zi if zi is not None else empty, y, tape, x if form == "tdf" else empty)
+        ctx.form = form
         return y, zf
 
     @staticmethod
     def backward(ctx, gy, gzf):
-        b, a, zi, y, tape = ctx.saved_tensors
+        b, a, zi, y, tape, x = ctx.saved_tensors
         zi = zi if ctx.has_zi else None
+        x = x if ctx.form == "tdf" else None
         desc = ctx.desc
         gx = torch.empty_like(y) if ctx.needs_input_grad[0] else None
         gb = torch.empty_like(b) if ctx.needs_input_grad[1] else None
@@ -195,15 +203,16 @@ class TVDFFunction(torch.autograd.Function):
         gy = None if gy is None else _c(gy.to(y.dtype))
         gzf = None if gzf is None else _c(gzf.to(y.dtype))
         with torch.cuda.device(y.device):
-            B.iir_backward(desc, gy, gzf, b, a, None, y, zi, tape, tape.numel(), gx, gb, ga, gzi, ws, wb,
+            B.iir_backward(desc, gy, gzf, b, a, x, y, zi, tape, tape.numel(), gx, gb, ga, gzi, ws, wb,
                            _stream(y))
-        return gx, gb, ga, gzi
+        return gx, gb, ga, gzi, None
 
 
-def lfilter_tv(x, b, a, zi=None, return_zf=False):
-    """Differentiable general per-sample DF filter: x (B, T), b (B, T, M+1), a (B, T, M)
-    (a[.., n, i-1] = a_i(n), monic), zi (B, M) = past internal signal u."""
-    y, zf = TVDFFunction.apply(x, b, a, zi)
+def lfilter_tv(x, b, a, zi=None, return_zf=False, form="df"):
+    """Differentiable general per-sample filter: x (B, T), b (B, T, M+1), a (B, T, M)
+    (a[.., n, i-1] = a_i(n), monic).  form "df": zi (B, M) = past internal signal u;
+    form "tdf": the per-sample TDF-II realisation, zi = v(0) (scipy's zi for constant rows)."""
+    y, zf = TVDFFunction.apply(x, b, a, zi, form)
     return (y, zf) if return_zf else y
 
 

@@ -29,7 +29,8 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
 // ------------------------------------------------------- instrumentation ----
 static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_phi", "tv_chain", "tv_fwd",
                                         "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd", "state_carry", "tv_fir",
-                                        "diag_prep", "diag_agg", "diag_scan", "diag_fwd", "diag_bwd", "diag_red"};
+                                        "diag_prep", "diag_agg", "diag_scan", "diag_fwd", "diag_bwd", "diag_red",
+                                        "tv_skew"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;
@@ -138,7 +139,10 @@ static iir_status_t check_desc(const iir_desc_t* d) {
     if ((d->flags & IIR_FLAG_PER_SAMPLE_B) && d->coef_mode != IIR_COEF_PER_SAMPLE)
         return fail(IIR_EINVAL, "IIR_FLAG_PER_SAMPLE_B needs IIR_COEF_PER_SAMPLE");
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) {
-        if (d->form != IIR_DF2) return fail(IIR_EUNSUPPORTED, "per-sample coefficients: only the DF form");
+        if (d->form != IIR_DF2 && d->form != IIR_TDF2)
+            return fail(IIR_EUNSUPPORTED, "per-sample coefficients: DF or TDF form");
+        if (d->form == IIR_TDF2 && !(d->flags & IIR_FLAG_PER_SAMPLE_B))
+            return fail(IIR_EUNSUPPORTED, "per-sample TDF: the general filter only (IIR_FLAG_PER_SAMPLE_B)");
         if (d->order < 1 || d->order > TV_MAX_M) return fail(IIR_EUNSUPPORTED, "per-sample order must be 1..32");
         if (!tv_supported(d->order)) return fail(IIR_EUNSUPPORTED, "per-sample order not compiled in");
         return IIR_OK;
@@ -382,6 +386,8 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
         return fail(IIR_EINVAL, "per-sample all-pole: grad_b must be NULL");
     if (d->coef_mode == IIR_COEF_PER_SAMPLE && (a == nullptr || y == nullptr))
         return fail(IIR_EINVAL, "per-sample backward needs the forward's a and y");
+    if (d->coef_mode == IIR_COEF_PER_SAMPLE && d->form == IIR_TDF2 && x == nullptr)
+        return fail(IIR_EINVAL, "per-sample TDF backward needs the forward's x");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     char* w = static_cast<char*>(ws);
     const char* t = static_cast<const char*>(tape);
@@ -394,7 +400,7 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     const bool vec = (rowlen % W == 0) && aligned16(grad_y) && aligned16(x) && aligned16(y) &&
                      aligned16(grad_x) && aligned16(t + L.tp_u);
     if (d->coef_mode == IIR_COEF_PER_SAMPLE)
-        return tv_backward(d, L, grad_y, grad_zf, b, a, y, zi, t, grad_x, grad_b, grad_a, grad_zi, w, vec, st);
+        return tv_backward(d, L, grad_y, grad_zf, b, a, y, zi, t, grad_x, grad_b, grad_a, grad_zi, w, vec, st, x);
     if (L.v2) {
         v2::Call c{};
         c.st = st;

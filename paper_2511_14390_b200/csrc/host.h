@@ -14,7 +14,8 @@ namespace iirg {
 iir_status_t fail(iir_status_t st, const std::string& msg);
 
 enum Kind { K_LTI_PREP = 0, K_LTI_FWD, K_LTI_BWD, K_TV_PHI, K_TV_CHAIN, K_TV_FWD, K_TV_BWD_AGG, K_TV_BWD, K_REC_FWD,
-            K_REC_BWD, K_STATE_CARRY, K_TV_FIR, K_DIAG_PREP, K_DIAG_AGG, K_DIAG_SCAN, K_DIAG_FWD, K_DIAG_BWD, K_DIAG_RED, K_NUM };
+            K_REC_BWD, K_STATE_CARRY, K_TV_FIR, K_DIAG_PREP, K_DIAG_AGG, K_DIAG_SCAN, K_DIAG_FWD, K_DIAG_BWD, K_DIAG_RED,
+            K_TV_SKEW, K_NUM };
 
 // Launch bookkeeping: counts every kernel and (when profiling is on) brackets it
 // with CUDA events on its stream.
@@ -57,6 +58,7 @@ struct Layout {
     size_t ws_sent = 0, ws_sent_bytes = 0;                 // look-back slots, initialised to all-ones (NaN)
     size_t ws_agg[MAX_LEVELS] = {0, 0, 0, 0}, ws_part = 0, ws_part2 = 0, ws_bytes = 0;
     size_t ws_du = 0, ws_duneg = 0;                        // general TV DF: FIR-stage adjoint of u
+    size_t ws_f = 0, ws_as = 0, ws_bs = 0, ws_gas = 0, ws_gbs = 0;   // general TV TDF (tvtdf.cuh)
     size_t ws_psi = 0, ws_omega = 0, ws_sgrp = 0;          // TV two-level chain
     size_t tp_tab = 0, tp_u = 0, tp_extra = 0, tp_bytes = 0;
     size_t tp_t64 = 0, tp_t32 = 0;                         // v2 engine tables (lti2.cuh)
@@ -79,6 +81,7 @@ iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* b, con
                         const void* zi, void* y, void* zf, char* tape, char* ws, bool vec, cudaStream_t st);
 iir_status_t tv_backward(const iir_desc_t* d, const Layout& L, const void* gy, const void* gzf, const void* b,
                          const void* a, const void* y, const void* zi, const char* tape, void* gx, void* gb,
-                         void* ga, void* gzi, char* ws, bool vec, cudaStream_t st);
+                         void* ga, void* gzi, char* ws, bool vec, cudaStream_t st,
+                         const void* x);
 
 }  // namespace iirg

@@ -5,6 +5,7 @@
 
 #include "host.h"
 #include "tv_impl.cuh"
+#include "tvtdf.cuh"
 
 namespace iirg {
 
@@ -50,10 +51,18 @@ Layout tv_layout(const iir_desc_t* d) {
     L.tp_tab = 0;
     L.tp_bytes = al256((size_t)L.ntot * M * M * ts);       // Phi_k per segment (reused by the backward)
     L.tp_u = L.tp_bytes;
-    if (d->flags & IIR_FLAG_PER_SAMPLE_B) {               // general DF: the all-pole output u (B, T)
-        L.tp_bytes += al256((size_t)d->batch * d->length * ts);
-        L.ws_du = o; o += al256((size_t)d->batch * d->length * ts);   // FIR-stage adjoint of u(0..T-1)
-        L.ws_duneg = o; o += al256((size_t)d->batch * M * ts);        //   ... and of u(-1..-M)
+    if (d->flags & IIR_FLAG_PER_SAMPLE_B) {
+        const size_t bt = (size_t)d->batch * d->length;
+        if (d->form == IIR_DF2) L.tp_bytes += al256(bt * ts);   // general DF: the all-pole output u (B, T)
+        L.ws_du = o; o += al256(bt * ts);                  // DF: FIR-stage adjoint of u(0..T-1); TDF: g = dL/df
+        L.ws_duneg = o; o += al256((size_t)d->batch * M * ts);   //   ... and of u(-1..-M)
+        if (d->form == IIR_TDF2) {                         // general TDF (tvtdf.cuh)
+            L.ws_f = o; o += al256(bt * ts);               // f (forward) / grad_y + zf tail (backward)
+            L.ws_as = o; o += al256(bt * M * ts);          // skewed rows a~, b~ and their gradients
+            L.ws_bs = o; o += al256(bt * (M + 1) * ts);
+            L.ws_gas = o; o += al256(bt * M * ts);
+            L.ws_gbs = o; o += al256(bt * (M + 1) * ts);
+        }
         L.ws_bytes = o;
     }
     return L;
@@ -88,9 +97,112 @@ static int tv_vec(const iir_desc_t* d, const void* a) {
     return (((size_t)d->order * ts) % 16 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15u) == 0);
 }
 
+// ---- general time-varying TDF (tvtdf.cuh, reading R20) -------------------------------
+static unsigned tdf_grid(int64_t n) {
+    const int64_t g = (n + tdf::NT - 1) / tdf::NT;
+    return (unsigned)(g < 148 * 16 ? (g > 0 ? g : 1) : 148 * 16);
+}
+static TvArgs tv_args(const iir_desc_t* d, const Layout& L, char* tape, char* ws) {
+    TvArgs ta{};
+    ta.phi = tape;
+    ta.w = reinterpret_cast<double*>(ws + L.ws_part);
+    ta.carry = reinterpret_cast<double*>(ws + L.ws_part2);
+    ta.B = d->batch; ta.T = d->length; ta.nseg = (int)L.ntiles;
+    ta.psi = reinterpret_cast<double*>(ws + L.ws_psi);
+    ta.omega = reinterpret_cast<double*>(ws + L.ws_omega);
+    ta.sgrp = reinterpret_cast<double*>(ws + L.ws_sgrp);
+    ta.ngrp = (int)L.ngroups;
+    return ta;
+}
+template <typename T>
+static iir_status_t tdf_forward(const iir_desc_t* d, const Layout& L, const void* b, const void* a, const void* x,
+                                const void* zi, void* y, void* zf, char* tape, char* ws, cudaStream_t st) {
+    const int64_t B = d->batch, N = d->length;
+    const int M = d->order;
+    T* as = reinterpret_cast<T*>(ws + L.ws_as);
+    T* bs = reinterpret_cast<T*>(ws + L.ws_bs);
+    T* f = reinterpret_cast<T*>(ws + L.ws_f);
+    iir_status_t s = launch(K_TV_SKEW, st, [&] {
+        tdf::skew_kernel<T><<<tdf_grid(B * N * (M + 1)), tdf::NT, 0, st>>>(static_cast<const T*>(a),
+            static_cast<const T*>(b), as, bs, B, N, M);
+    });
+    if (s != IIR_OK) return s;
+    // f(n) = sum_k b~_k(n) x(n-k) (zero history), + zi(n) for n < M
+    s = fir_dispatch<T>(true, d, bs, x, nullptr, nullptr, f, nullptr, nullptr, nullptr, st);
+    if (s != IIR_OK) return s;
+    if (zi != nullptr) {
+        s = launch(K_TV_SKEW, st, [&] {
+            tdf::zi_add_kernel<T><<<(unsigned)((B * M + 127) / 128), 128, 0, st>>>(f, static_cast<const T*>(zi), B, N, M);
+        });
+        if (s != IIR_OK) return s;
+    }
+    // y(n) = f(n) - sum_i a~_i(n) y(n-i), zero history
+    TvArgs ta = tv_args(d, L, tape, ws);
+    ta.a = as; ta.x = f; ta.zi = nullptr; ta.y = y; ta.zf = nullptr;
+    ta.vec = (((size_t)M * sizeof(T)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(as) & 15u) == 0);
+    s = tv_dispatch<T>(true, M, L, ta, st, d);
+    if (s != IIR_OK || zf == nullptr) return s;
+    return launch(K_TV_SKEW, st, [&] {
+        tdf::zf_kernel<T><<<(unsigned)((B * M + 127) / 128), 128, 0, st>>>(static_cast<const T*>(a),
+            static_cast<const T*>(b), static_cast<const T*>(x), static_cast<const T*>(y), static_cast<const T*>(zi),
+            static_cast<T*>(zf), B, N, M);
+    });
+}
+template <typename T>
+static iir_status_t tdf_backward(const iir_desc_t* d, const Layout& L, const void* gy, const void* gzf, const void* b,
+                                 const void* a, const void* x, const void* y, const char* tape, void* gx, void* gb,
+                                 void* ga, void* gzi, char* ws, cudaStream_t st) {
+    const int64_t B = d->batch, N = d->length;
+    const int M = d->order;
+    T* as = reinterpret_cast<T*>(ws + L.ws_as);
+    T* bs = reinterpret_cast<T*>(ws + L.ws_bs);
+    T* gas = reinterpret_cast<T*>(ws + L.ws_gas);
+    T* gbs = reinterpret_cast<T*>(ws + L.ws_gbs);
+    T* gye = reinterpret_cast<T*>(ws + L.ws_f);
+    T* g = reinterpret_cast<T*>(ws + L.ws_du);
+    T* duneg = reinterpret_cast<T*>(ws + L.ws_duneg);
+    iir_status_t s = launch(K_TV_SKEW, st, [&] {
+        tdf::skew_kernel<T><<<tdf_grid(B * N * (M + 1)), tdf::NT, 0, st>>>(static_cast<const T*>(a),
+            static_cast<const T*>(b), as, bs, B, N, M);
+    });
+    if (s != IIR_OK) return s;
+    s = launch(K_TV_SKEW, st, [&] {
+        tdf::gy_eff_kernel<T><<<tdf_grid(B * N), tdf::NT, 0, st>>>(static_cast<const T*>(gy),
+            static_cast<const T*>(gzf), static_cast<const T*>(a), gye, B, N, M);
+    });
+    if (s != IIR_OK) return s;
+    // all-pole adjoint on the skewed rows: g = dL/df, grad_a~
+    TvArgs ta = tv_args(d, L, const_cast<char*>(tape), ws);
+    ta.a = as; ta.zi = nullptr; ta.gy = gye; ta.gzf = nullptr; ta.yin = y;
+    ta.gx = g; ta.ga = gas; ta.gzi = nullptr;
+    ta.vec = (((size_t)M * sizeof(T)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(as) & 15u) == 0) &&
+             ((reinterpret_cast<uintptr_t>(gas) & 15u) == 0);
+    s = tv_dispatch<T>(false, M, L, ta, st, d);
+    if (s != IIR_OK) return s;
+    // FIR adjoint on the skewed rows: grad_x, grad_b~
+    s = fir_dispatch<T>(false, d, bs, x, nullptr, g, nullptr, gx != nullptr ? gx : static_cast<void*>(gye), duneg,
+                        gbs, st);
+    if (s != IIR_OK) return s;
+    if (ga != nullptr || gb != nullptr) {
+        s = launch(K_TV_SKEW, st, [&] {
+            tdf::unskew_kernel<T><<<tdf_grid(B * N * (M + 1)), tdf::NT, 0, st>>>(gas, gbs, static_cast<T*>(ga),
+                static_cast<T*>(gb), B, N, M);
+        });
+        if (s != IIR_OK) return s;
+    }
+    return launch(K_TV_SKEW, st, [&] {
+        tdf::tail_kernel<T><<<(unsigned)((B * M + 127) / 128), 128, 0, st>>>(static_cast<const T*>(gzf),
+            static_cast<const T*>(a), static_cast<const T*>(b), static_cast<const T*>(x), static_cast<const T*>(y), g,
+            static_cast<T*>(gx), static_cast<T*>(ga), static_cast<T*>(gb), static_cast<T*>(gzi), B, N, M);
+    });
+}
+
 iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* b, const void* a, const void* x,
                         const void* zi, void* y, void* zf, char* tape, char* ws, bool, cudaStream_t st) {
     const bool fir = (d->flags & IIR_FLAG_PER_SAMPLE_B) != 0;
+    if (d->form == IIR_TDF2)
+        return d->dtype == IIR_F64 ? tdf_forward<double>(d, L, b, a, x, zi, y, zf, tape, ws, st)
+                                   : tdf_forward<float>(d, L, b, a, x, zi, y, zf, tape, ws, st);
     void* u = fir ? static_cast<void*>(tape + L.tp_u) : y;   // general DF: the recursion's output is u
     TvArgs ta{};
     ta.a = a; ta.x = x; ta.zi = zi; ta.y = u; ta.zf = zf;
@@ -112,7 +224,10 @@ iir_status_t tv_forward(const iir_desc_t* d, const Layout& L, const void* b, con
 
 iir_status_t tv_backward(const iir_desc_t* d, const Layout& L, const void* gy, const void* gzf, const void* b,
                          const void* a, const void* y, const void* zi, const char* tape, void* gx, void* gb,
-                         void* ga, void* gzi, char* ws, bool, cudaStream_t st) {
+                         void* ga, void* gzi, char* ws, bool, cudaStream_t st, const void* x) {
+    if (d->form == IIR_TDF2)
+        return d->dtype == IIR_F64 ? tdf_backward<double>(d, L, gy, gzf, b, a, x, y, tape, gx, gb, ga, gzi, ws, st)
+                                   : tdf_backward<float>(d, L, gy, gzf, b, a, x, y, tape, gx, gb, ga, gzi, ws, st);
     const bool fir = (d->flags & IIR_FLAG_PER_SAMPLE_B) != 0;
     const void* u = fir ? static_cast<const void*>(tape + L.tp_u) : y;
     void* du = fir ? static_cast<void*>(ws + L.ws_du) : nullptr;

@@ -1,0 +1,131 @@
+// tvtdf.cuh -- general time-varying TDF-II filter (reading R20):
+// the TDF realisation of PAPER.md:67-68 at every sample,
+//     y(n) = b_0(n) x(n) + v_1(n),   v_i(n+1) = v_{i+1}(n) + b_i(n) x(n) - a_i(n) y(n).
+// Unrolled, y(n) = sum_k b_k(n-k) x(n-k) - sum_i a_i(n-i) y(n-i) + zi[n] (n < M): the
+// zeros-then-poles (DF-I) structure on SKEWED coefficient rows
+//     b~_k(n) = b_k(n - k),   a~_i(n) = a_i(n - i)      (zero before n = 0),
+// so the path reuses the per-sample kernels of the DF filter: the FIR stage (tv_fir, rows
+// b~, zero history) gives f, zi is added to f(0..M-1), and the all-pole recursion (rows a~,
+// zero history) gives y.  zf = v(N) is the tail sum
+//     zf_i = zi_{i+N} + sum_{d=0}^{min(N-1, M-i)} [b_{i+d}(m) x(m) - a_{i+d}(m) y(m)],  m = N-1-d.
+// Backward: the all-pole adjoint on rows a~ (input grad_y plus the zf tail terms) gives
+// g = dL/df and grad_a~; the FIR adjoint on rows b~ gives grad_x and grad_b~; the skew is
+// undone (grad_a_i(m) = grad_a~_i(m + i)) and the zf tail terms are added.
+#pragma once
+#include "common.cuh"
+
+namespace iirg {
+namespace tdf {
+
+constexpr int NT = 256;
+
+// a~ (B, N, M) and b~ (B, N, M+1) from a, b; one thread per (sequence, sample, k), k = 0..M
+template <typename T>
+__global__ void __launch_bounds__(NT) skew_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ as,
+                                                  T* __restrict__ bs, int64_t B, int64_t N, int M) {
+    const int64_t K = M + 1, tot = B * N * K;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / K;                      // (sequence, sample) row
+        const int k = (int)(e - r * K);
+        const int64_t n = r % N;
+        const bool in = n - k >= 0;
+        bs[e] = in ? b[(r - k) * K + k] : T(0);
+        if (k >= 1) as[r * M + k - 1] = in ? a[(r - k) * M + k - 1] : T(0);
+    }
+}
+
+// grad_a, grad_b from the gradients of the skewed rows: g_k(m) = g~_k(m + k) (zero past N)
+template <typename T>
+__global__ void __launch_bounds__(NT) unskew_kernel(const T* __restrict__ gas, const T* __restrict__ gbs,
+                                                    T* __restrict__ ga, T* __restrict__ gb, int64_t B, int64_t N,
+                                                    int M) {
+    const int64_t K = M + 1, tot = B * N * K;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / K;
+        const int k = (int)(e - r * K);
+        const int64_t m = r % N;
+        const bool in = m + k < N;
+        if (gb != nullptr) gb[e] = in ? gbs[(r + k) * K + k] : T(0);
+        if (k >= 1 && ga != nullptr) ga[r * M + k - 1] = in ? gas[(r + k) * M + k - 1] : T(0);
+    }
+}
+
+// f(n) += zi[n], n < min(M, N); one thread per (sequence, n)
+template <typename T>
+__global__ void zi_add_kernel(T* __restrict__ f, const T* __restrict__ zi, int64_t B, int64_t N, int M) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= B * M) return;
+    const int64_t s = e / M;
+    const int n = (int)(e - s * M);
+    if (n < N) f[s * N + n] = f[s * N + n] + zi[e];
+}
+
+// zf = v(N) by the tail sum (fp64 accumulation); one thread per (sequence, i)
+template <typename T>
+__global__ void zf_kernel(const T* __restrict__ a, const T* __restrict__ b, const T* __restrict__ x,
+                          const T* __restrict__ y, const T* __restrict__ zi, T* __restrict__ zf, int64_t B, int64_t N,
+                          int M) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= B * M) return;
+    const int64_t s = e / M;
+    const int i = (int)(e - s * M) + 1;               // 1-based state index
+    const int64_t K = M + 1;
+    double acc = (zi != nullptr && i + N <= M) ? (double)zi[s * M + i + N - 1] : 0.0;
+    for (int d = 0; d <= M - i && d < N; ++d) {
+        const int64_t m = N - 1 - d, r = s * N + m;
+        const int j = i + d;
+        acc += (double)b[r * K + j] * (double)x[r] - (double)a[r * M + j - 1] * (double)y[r];
+    }
+    zf[e] = (T)acc;
+}
+
+// gye(n) = gy(n) - sum_{i=1}^{M-d} a_{i+d}(n) gzf_i  (d = N-1-n; the zf tail's y terms);
+// one thread per (sequence, n)
+template <typename T>
+__global__ void __launch_bounds__(NT) gy_eff_kernel(const T* __restrict__ gy, const T* __restrict__ gzf,
+                                                    const T* __restrict__ a, T* __restrict__ gye, int64_t B, int64_t N,
+                                                    int M) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < B * N; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = r / N, n = r - s * N, d = N - 1 - n;
+        double v = gy != nullptr ? (double)gy[r] : 0.0;
+        if (gzf != nullptr && d < M)
+            for (int i = 1; i + d <= M; ++i) v -= (double)a[r * M + i + d - 1] * (double)gzf[s * M + i - 1];
+        gye[r] = (T)v;
+    }
+}
+
+// After the FIR adjoint and the unskew: the zf tail's x / coefficient terms and grad_zi.
+//   gx(m) += sum_{i} b_{i+d}(m) gzf_i,  gb_{i+d}(m) += gzf_i x(m),  ga_{i+d}(m) -= gzf_i y(m)  (m = N-1-d)
+//   gzi[k] = g(k) (k < N: zi adds into f(k))  +  gzf[k - N] (k >= N: zi_{k} reaches zf directly)
+// One thread per (sequence, k), k = 0..M-1 (k doubles as the tail offset d).
+template <typename T>
+__global__ void tail_kernel(const T* __restrict__ gzf, const T* __restrict__ a, const T* __restrict__ b,
+                            const T* __restrict__ x, const T* __restrict__ y, const T* __restrict__ g,
+                            T* __restrict__ gx, T* __restrict__ ga, T* __restrict__ gb, T* __restrict__ gzi,
+                            int64_t B, int64_t N, int M) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= B * M) return;
+    const int64_t s = e / M;
+    const int k = (int)(e - s * M);
+    const int64_t K = M + 1;
+    if (gzi != nullptr) {
+        double v = k < N ? (double)g[s * N + k] : 0.0;
+        if (gzf != nullptr && k >= N) v += (double)gzf[s * M + k - N];
+        gzi[e] = (T)v;
+    }
+    const int d = k;
+    if (gzf == nullptr || d >= N) return;
+    const int64_t m = N - 1 - d, r = s * N + m;
+    double dx = 0.0;
+    for (int i = 1; i + d <= M; ++i) {
+        const double gz = (double)gzf[s * M + i - 1];
+        const int j = i + d;
+        dx += (double)b[r * K + j] * gz;
+        if (gb != nullptr) gb[r * K + j] = (T)((double)gb[r * K + j] + gz * (double)x[r]);
+        if (ga != nullptr) ga[r * M + j - 1] = (T)((double)ga[r * M + j - 1] - gz * (double)y[r]);
+    }
+    if (gx != nullptr) gx[r] = (T)((double)gx[r] + dx);
+}
+
+}  // namespace tdf
+}  // namespace iirg
