@@ -50,6 +50,8 @@ WORKLOADS = {
                **inputs.CONFIGS["c3"]),
     "f2": dict(desc="SURVEY 8(f) f2: general time-varying DF (per-sample b and a), config-3 shape: order 24, "
                     "batch 32 x 2^18, fp32", fir=True, **inputs.CONFIGS["c3"]),
+    "f2t": dict(desc="SURVEY 8(f) f2: general time-varying TDF-II (per-sample b and a, DESIGN.md R20), config-3 "
+                     "shape: order 24, batch 32 x 2^18, fp32", fir=True, **dict(inputs.CONFIGS["c3"], form="tdf")),
     "f1": dict(desc="SURVEY 8(f) f1: bare recurrence v(n+1) = A v(n) + z(n) of Listing 1, M = 2, batch 16 x 2^20, "
                     "fp32 (the paper's benchmarked operator at its longest N)", **dict(inputs.CONFIGS["f1"], batch=16)),
     "f3": dict(desc="SURVEY 8(f) f3: Diag-EXT bare recurrence (eigen-basis element-wise complex scans), f1's shape: "
@@ -77,6 +79,8 @@ def algorithmic_bytes(w):
              "tv_bwd": (2 * M + 3) * s}
         if w.get("fir"):       # FIR stage, 3 launches per step: fwd b, u -> y; bwd b, dy, u -> du, grad_b; zi add
             d["tv_fir"] = ((M + 3) + (2 * M + 5)) * s / 3
+        if w.get("fir") and w["form"] == "tdf":   # TDF: skew / unskew of the (2M+1) rows (design overhead)
+            d["tv_skew"] = 2 * (2 * M + 1) * s
         return d
     # HBM bytes per kernel the method must move: fwd reads x, writes y (+u for DF);
     # bwd reads dy, x, y (TDF) or dy, u (DF) and writes dx: 24 B/sample in fp32

@@ -324,11 +324,21 @@ __device__ __forceinline__ void carry_publish(const float* __restrict__ PQ, int 
 //   T_v = sum_{l < d_v} Y_v^l AGG^(v)_{(jt >> 5v) - 1 - l}         (lane l, one round trip)
 //   X   = T_0 + Y_0^d_0 (T_1 + Y_1^d_1 (T_2 + ...))
 // Fixed combination order (per-lane products, a fixed butterfly): bitwise deterministic.
+// Level-0 slot of tile jt's look-back, loaded ahead of time (issued before the warp's next
+// aggregate so the L2 round trip overlaps it; re-polled in carry_lookback if it was not yet
+// published).  Lanes without a slot hold zeros.
+template <int M>
+__device__ __forceinline__ void lookback_prefetch(int lane, int jt, int64_t seq, const CarryWs& cw, int64_t boff,
+                                                  float (&V)[M]) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) V[i] = 0.f;
+    if (jt > 0 && lane < (jt & 31)) slot_load<M>(slot_ptr<M>(cw, boff, 0, seq, jt - 1 - lane), V);
+}
 template <int M>
 __device__ __forceinline__ void carry_lookback(const float* __restrict__ PQ, int lane, int jt, int64_t seq,
                                                const float (&X0)[M], const CarryWs& cw, int64_t boff,
                                                float (*sT)[M],
-                                               float (&X)[M]) {
+                                               float (&X)[M], const float (*V0pre)[M] = nullptr) {
     constexpr int NPR = Cfg<M>::NPR, LV = 32 * M * Cfg<M>::MP;
     if (jt == 0) {
 #pragma unroll
@@ -345,7 +355,12 @@ __device__ __forceinline__ void carry_lookback(const float* __restrict__ PQ, int
         for (int i = 0; i < M; ++i) V[i] = 0.f;
         if (lane < d) {
             const float* sp = slot_ptr<M>(cw, boff, v, seq, blk - 1 - lane);
-            slot_load<M>(sp, V);
+            if (v == 0 && V0pre != nullptr) {
+#pragma unroll
+                for (int i = 0; i < M; ++i) V[i] = (*V0pre)[i];
+            } else {
+                slot_load<M>(sp, V);
+            }
             if (!slot_ok<M>(V)) slot_wait<M>(sp, V, cw.err);
         }
         __syncwarp();
@@ -762,6 +777,8 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const __grid_cons
     while (s0.t < p.ntot) {
         Sched s2 = s1;
         s2.next();
+        float V0pre[M];                                          // t0's level-0 look-back slots, in flight
+        lookback_prefetch<M>(lane, s0.j, s0.seq, cw, boff, V0pre);   // across t1's aggregate
         float E1[M];
         if (s1.t < p.ntot) {
             aggregate(s1, tbase + (sl ^ 1u) * L, E1);
@@ -780,7 +797,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_fwd_kernel(const __grid_cons
 #pragma unroll
             for (int i = 0; i < M; ++i) X0[i] = p.zi[seq * M + i];
         V2_TRACE(p.trace, s0.t, 3);
-        carry_lookback<M>(t32s + C::OPQ, lane, jt, seq, X0, cw, boff, s_T[warp], X);
+        carry_lookback<M>(t32s + C::OPQ, lane, jt, seq, X0, cw, boff, s_T[warp], X, &V0pre);
         V2_TRACE(p.trace, s0.t, 4);
         float vin[M];
         lane_carry<M>(t32s + C::OQ, lane, E0, X, vin);
@@ -1120,6 +1137,8 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
         s2.next();
         __syncwarp();                                            // the previous tile's dx stores have read bX
         issue_xy(s0);
+        float V0pre[M];                                          // t0's level-0 look-back slots, in flight
+        lookback_prefetch<M>(lane, s0.j, s0.seq, cw, boff, V0pre);   // across t1's aggregate
         float E1[M];
         if (s1.t < p.ntot) {
             aggregate(s1, tbase + (sl ^ 1u) * L, E1);
@@ -1142,7 +1161,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
 #pragma unroll
             for (int i = 0; i < M; ++i) X0[i] = p.gzf[seq * M + i];
         V2_TRACE(p.trace, s0.t, 3);
-        carry_lookback<M>(t32s + C::OPQ, lane, jr, seq, X0, cw, boff, s_T[warp], X);
+        carry_lookback<M>(t32s + C::OPQ, lane, jr, seq, X0, cw, boff, s_T[warp], X, &V0pre);
         V2_TRACE(p.trace, s0.t, 4);
         float din[M];
         lane_carry<M>(t32s + C::OQ, lane, E0, X, din);           // [g(e) .. g(e+M-1)], e = this chunk's right end

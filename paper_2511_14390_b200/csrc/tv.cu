@@ -98,9 +98,19 @@ static int tv_vec(const iir_desc_t* d, const void* a) {
 }
 
 // ---- general time-varying TDF (tvtdf.cuh, reading R20) -------------------------------
-static unsigned tdf_grid(int64_t n) {
-    const int64_t g = (n + tdf::NT - 1) / tdf::NT;
-    return (unsigned)(g < 148 * 16 ? (g > 0 ? g : 1) : 148 * 16);
+// (row tiles, sequences) grid of the skew kernels, their shared memory (> 48 KB opt-in per device)
+template <typename T>
+static dim3 skew_grid(int64_t B, int64_t N) { return dim3((unsigned)((N + tdf::SR - 1) / tdf::SR), (unsigned)B); }
+template <typename T>
+static void skew_attrs(int M) {
+    static PerDevice attrs;
+    attrs.once([] {
+        cudaFuncSetAttribute(tdf::skew_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tdf::skew_smem<T>(TV_MAX_M));
+        cudaFuncSetAttribute(tdf::unskew_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tdf::skew_smem<T>(TV_MAX_M));
+    });
+    (void)M;
 }
 static TvArgs tv_args(const iir_desc_t* d, const Layout& L, char* tape, char* ws) {
     TvArgs ta{};
@@ -122,9 +132,10 @@ static iir_status_t tdf_forward(const iir_desc_t* d, const Layout& L, const void
     T* as = reinterpret_cast<T*>(ws + L.ws_as);
     T* bs = reinterpret_cast<T*>(ws + L.ws_bs);
     T* f = reinterpret_cast<T*>(ws + L.ws_f);
+    skew_attrs<T>(M);
     iir_status_t s = launch(K_TV_SKEW, st, [&] {
-        tdf::skew_kernel<T><<<tdf_grid(B * N * (M + 1)), tdf::NT, 0, st>>>(static_cast<const T*>(a),
-            static_cast<const T*>(b), as, bs, B, N, M);
+        tdf::skew_kernel<T><<<skew_grid<T>(B, N), tdf::NT, tdf::skew_smem<T>(M), st>>>(static_cast<const T*>(a),
+            static_cast<const T*>(b), as, bs, N, M);
     });
     if (s != IIR_OK) return s;
     // f(n) = sum_k b~_k(n) x(n-k) (zero history), + zi(n) for n < M
@@ -161,14 +172,15 @@ static iir_status_t tdf_backward(const iir_desc_t* d, const Layout& L, const voi
     T* gye = reinterpret_cast<T*>(ws + L.ws_f);
     T* g = reinterpret_cast<T*>(ws + L.ws_du);
     T* duneg = reinterpret_cast<T*>(ws + L.ws_duneg);
+    skew_attrs<T>(M);
     iir_status_t s = launch(K_TV_SKEW, st, [&] {
-        tdf::skew_kernel<T><<<tdf_grid(B * N * (M + 1)), tdf::NT, 0, st>>>(static_cast<const T*>(a),
-            static_cast<const T*>(b), as, bs, B, N, M);
+        tdf::skew_kernel<T><<<skew_grid<T>(B, N), tdf::NT, tdf::skew_smem<T>(M), st>>>(static_cast<const T*>(a),
+            static_cast<const T*>(b), as, bs, N, M);
     });
     if (s != IIR_OK) return s;
     s = launch(K_TV_SKEW, st, [&] {
-        tdf::gy_eff_kernel<T><<<tdf_grid(B * N), tdf::NT, 0, st>>>(static_cast<const T*>(gy),
-            static_cast<const T*>(gzf), static_cast<const T*>(a), gye, B, N, M);
+        tdf::gy_eff_kernel<T><<<dim3((unsigned)((N + tdf::NT - 1) / tdf::NT), (unsigned)B), tdf::NT, 0, st>>>(
+            static_cast<const T*>(gy), static_cast<const T*>(gzf), static_cast<const T*>(a), gye, N, M);
     });
     if (s != IIR_OK) return s;
     // all-pole adjoint on the skewed rows: g = dL/df, grad_a~
@@ -185,8 +197,8 @@ static iir_status_t tdf_backward(const iir_desc_t* d, const Layout& L, const voi
     if (s != IIR_OK) return s;
     if (ga != nullptr || gb != nullptr) {
         s = launch(K_TV_SKEW, st, [&] {
-            tdf::unskew_kernel<T><<<tdf_grid(B * N * (M + 1)), tdf::NT, 0, st>>>(gas, gbs, static_cast<T*>(ga),
-                static_cast<T*>(gb), B, N, M);
+            tdf::unskew_kernel<T><<<skew_grid<T>(B, N), tdf::NT, tdf::skew_smem<T>(M), st>>>(gas, gbs,
+                static_cast<T*>(ga), static_cast<T*>(gb), N, M);
         });
         if (s != IIR_OK) return s;
     }

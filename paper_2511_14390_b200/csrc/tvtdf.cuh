@@ -19,35 +19,76 @@ namespace tdf {
 
 constexpr int NT = 256;
 
-// a~ (B, N, M) and b~ (B, N, M+1) from a, b; one thread per (sequence, sample, k), k = 0..M
+constexpr int SR = 128;    // rows (samples) per block of the skew kernels
+
+// a~ (B, N, M) and b~ (B, N, M+1) from a, b.  Block (tile, sequence): rows [n0, n0 + SR) of
+// the output need input rows [n0 - M, n0 + SR); both are staged through shared memory so
+// every global access is a contiguous run of rows.
 template <typename T>
 __global__ void __launch_bounds__(NT) skew_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ as,
-                                                  T* __restrict__ bs, int64_t B, int64_t N, int M) {
-    const int64_t K = M + 1, tot = B * N * K;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e / K;                      // (sequence, sample) row
-        const int k = (int)(e - r * K);
-        const int64_t n = r % N;
-        const bool in = n - k >= 0;
-        bs[e] = in ? b[(r - k) * K + k] : T(0);
-        if (k >= 1) as[r * M + k - 1] = in ? a[(r - k) * M + k - 1] : T(0);
+                                                  T* __restrict__ bs, int64_t N, int M) {
+    extern __shared__ __align__(16) unsigned char skew_raw[];
+    T* sb = reinterpret_cast<T*>(skew_raw);                 // (SR + M) x K
+    T* sa = sb + (SR + M) * (M + 1);                         // (SR + M) x M
+    const int K = M + 1;
+    const int64_t s = blockIdx.y, n0 = (int64_t)blockIdx.x * SR;
+    const int64_t lo = n0 - M;                               // first staged input row
+    const int rows = (int)min((int64_t)SR + M, N - lo);
+    for (int e = threadIdx.x; e < (SR + M) * K; e += NT) {
+        const int r = e / K;
+        const int64_t n = lo + r;
+        sb[e] = (r < rows && n >= 0) ? b[(s * N + n) * K + (e - r * K)] : T(0);
+    }
+    for (int e = threadIdx.x; e < (SR + M) * M; e += NT) {
+        const int r = e / M;
+        const int64_t n = lo + r;
+        sa[e] = (r < rows && n >= 0) ? a[(s * N + n) * M + (e - r * M)] : T(0);
+    }
+    __syncthreads();
+    const int nout = (int)min((int64_t)SR, N - n0);
+    for (int e = threadIdx.x; e < nout * K; e += NT) {       // b~_k(n) = b_k(n - k)
+        const int r = e / K, k = e - r * K;
+        bs[(s * N + n0) * K + e] = sb[(r + M - k) * K + k];
+    }
+    for (int e = threadIdx.x; e < nout * M; e += NT) {       // a~_i(n) = a_i(n - i)
+        const int r = e / M, i = e - r * M + 1;
+        as[(s * N + n0) * M + e] = sa[(r + M - i) * M + i - 1];
     }
 }
+template <typename T>
+constexpr size_t skew_smem(int M) { return (size_t)(SR + M) * (2 * M + 1) * sizeof(T); }
 
-// grad_a, grad_b from the gradients of the skewed rows: g_k(m) = g~_k(m + k) (zero past N)
+// grad_a, grad_b from the gradients of the skewed rows: g_k(m) = g~_k(m + k) (zero past N);
+// block (tile, sequence) stages input rows [m0, m0 + SR + M)
 template <typename T>
 __global__ void __launch_bounds__(NT) unskew_kernel(const T* __restrict__ gas, const T* __restrict__ gbs,
-                                                    T* __restrict__ ga, T* __restrict__ gb, int64_t B, int64_t N,
-                                                    int M) {
-    const int64_t K = M + 1, tot = B * N * K;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e / K;
-        const int k = (int)(e - r * K);
-        const int64_t m = r % N;
-        const bool in = m + k < N;
-        if (gb != nullptr) gb[e] = in ? gbs[(r + k) * K + k] : T(0);
-        if (k >= 1 && ga != nullptr) ga[r * M + k - 1] = in ? gas[(r + k) * M + k - 1] : T(0);
+                                                    T* __restrict__ ga, T* __restrict__ gb, int64_t N, int M) {
+    extern __shared__ __align__(16) unsigned char skew_raw[];
+    T* sb = reinterpret_cast<T*>(skew_raw);
+    T* sa = sb + (SR + M) * (M + 1);
+    const int K = M + 1;
+    const int64_t s = blockIdx.y, m0 = (int64_t)blockIdx.x * SR;
+    const int rows = (int)min((int64_t)SR + M, N - m0);
+    for (int e = threadIdx.x; e < (SR + M) * K; e += NT) {
+        const int r = e / K;
+        sb[e] = r < rows ? gbs[(s * N + m0 + r) * K + (e - r * K)] : T(0);
     }
+    for (int e = threadIdx.x; e < (SR + M) * M; e += NT) {
+        const int r = e / M;
+        sa[e] = r < rows ? gas[(s * N + m0 + r) * M + (e - r * M)] : T(0);
+    }
+    __syncthreads();
+    const int nout = (int)min((int64_t)SR, N - m0);
+    if (gb != nullptr)
+        for (int e = threadIdx.x; e < nout * K; e += NT) {
+            const int r = e / K, k = e - r * K;
+            gb[(s * N + m0) * K + e] = sb[(r + k) * K + k];
+        }
+    if (ga != nullptr)
+        for (int e = threadIdx.x; e < nout * M; e += NT) {
+            const int r = e / M, i = e - r * M + 1;
+            ga[(s * N + m0) * M + e] = sa[(r + i) * M + i - 1];
+        }
 }
 
 // f(n) += zi[n], n < min(M, N); one thread per (sequence, n)
@@ -80,18 +121,17 @@ __global__ void zf_kernel(const T* __restrict__ a, const T* __restrict__ b, cons
 }
 
 // gye(n) = gy(n) - sum_{i=1}^{M-d} a_{i+d}(n) gzf_i  (d = N-1-n; the zf tail's y terms);
-// one thread per (sequence, n)
+// block (tile, sequence), one thread per n
 template <typename T>
 __global__ void __launch_bounds__(NT) gy_eff_kernel(const T* __restrict__ gy, const T* __restrict__ gzf,
-                                                    const T* __restrict__ a, T* __restrict__ gye, int64_t B, int64_t N,
-                                                    int M) {
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < B * N; r += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = r / N, n = r - s * N, d = N - 1 - n;
-        double v = gy != nullptr ? (double)gy[r] : 0.0;
-        if (gzf != nullptr && d < M)
-            for (int i = 1; i + d <= M; ++i) v -= (double)a[r * M + i + d - 1] * (double)gzf[s * M + i - 1];
-        gye[r] = (T)v;
-    }
+                                                    const T* __restrict__ a, T* __restrict__ gye, int64_t N, int M) {
+    const int64_t s = blockIdx.y, n = (int64_t)blockIdx.x * NT + threadIdx.x;
+    if (n >= N) return;
+    const int64_t r = s * N + n, d = N - 1 - n;
+    double v = gy != nullptr ? (double)gy[r] : 0.0;
+    if (gzf != nullptr && d < M)
+        for (int i = 1; i + d <= M; ++i) v -= (double)a[r * M + i + d - 1] * (double)gzf[s * M + i - 1];
+    gye[r] = (T)v;
 }
 
 // After the FIR adjoint and the unskew: the zf tail's x / coefficient terms and grad_zi.
