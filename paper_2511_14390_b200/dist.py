@@ -79,6 +79,28 @@ def sharded_step(compute: Callable, x: torch.Tensor, gy: torch.Tensor, b: torch.
     return ShardResult(y=y, zf=zf, gx=gx, gzi=gzi, gb=gb, ga=ga)
 
 
+_SHARD_BUFFERS = {}
+
+
+def _shard_buffers(Bsz, T, M, form, dtype, mode, device):
+    """Tape and workspace of one shard shape, allocated and cleared (iir_workspace_init) once
+    per (shape, device, stream); later calls pass IIR_FLAG_WS_READY (every completed call
+    leaves the workspace cleared), so a training loop allocates and memsets nothing per step."""
+    from . import _binding as B
+    stream = torch.cuda.current_stream(device)
+    key = (Bsz, T, M, form, dtype, mode, str(device), stream.cuda_stream)
+    hit = _SHARD_BUFFERS.get(key)
+    if hit is None:
+        desc0 = B.make_desc(Bsz, T, M, form, dtype, mode)
+        tb, wb = B.iir_tape_bytes(desc0), B.iir_workspace_bytes(desc0)
+        tape = torch.empty(tb, dtype=torch.uint8, device=device)
+        ws = torch.empty(wb, dtype=torch.uint8, device=device)
+        B.iir_workspace_init(desc0, ws, wb, stream)
+        desc = B.make_desc(Bsz, T, M, form, dtype, mode, flags=B.IIR_FLAG_WS_READY)
+        hit = _SHARD_BUFFERS[key] = (desc, tape, tb, ws, wb)
+    return hit
+
+
 def cuda_shard_compute(x, gy, b, a, zi, gzf, form):
     """Per-shard compute on the local GPU through the C ABI (no fallback)."""
     from . import _binding as B
@@ -91,10 +113,7 @@ def cuda_shard_compute(x, gy, b, a, zi, gzf, form):
     _check(x, [("gy", gy, [(Bsz, T)]), ("b", b, coef), ("a", a, coef), ("zi", zi, [(Bsz, M)]),
                ("gzf", gzf, [(Bsz, M)])])
     mode = B.IIR_COEF_SHARED if b.dim() == 1 else B.IIR_COEF_PER_SEQ
-    desc = B.make_desc(Bsz, T, M, form, x.dtype, mode)
-    tb, wb = B.iir_tape_bytes(desc), B.iir_workspace_bytes(desc)
-    tape = torch.empty(tb, dtype=torch.uint8, device=x.device)
-    ws = torch.empty(wb, dtype=torch.uint8, device=x.device)
+    desc, tape, tb, ws, wb = _shard_buffers(Bsz, T, M, form, x.dtype, mode, x.device)
     y = torch.empty_like(x)
     gx = torch.empty_like(x)
     zf = torch.empty((Bsz, M), dtype=x.dtype, device=x.device)
