@@ -14,13 +14,16 @@ import re
 import sys
 from collections import OrderedDict, defaultdict
 
-KIND = [(r"rec_fwd_kernel", "rec_fwd"), (r"rec_bwd_kernel", "rec_bwd"), (r"lti_prep_kernel", "lti_prep"),
-        (r"lti_red_kernel<[^>]*, *(\(bool\))?(0|false)>", "lti_red_fwd"),
-        (r"lti_red_kernel<[^>]*, *(\(bool\))?(1|true)>", "lti_red_bwd"), (r"lti_cscan_kernel", "lti_cscan"),
-        (r"state_carry_kernel", "state_carry"), (r"tv_fir_|tv_add_kernel", "tv_fir"), (r"lti_fwd_kernel", "lti_fwd"), (r"lti_bwd", "lti_bwd"),
-        (r"tv_phi2?_kernel", "tv_phi"), (r"tv_(group|groupchain|expand|chain)_kernel", "tv_chain"), (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?0>", "tv_fwd"),
+KIND = [(r"rec_fwd_kernel", "rec_fwd"), (r"rec_bwd_kernel", "rec_bwd"), (r"lti2?_prep_kernel", "lti_prep"),
+        (r"state_carry_kernel", "state_carry"), (r"tv_fir_|tv_add_kernel", "tv_fir"), (r"lti2?_fwd_kernel", "lti_fwd"),
+        (r"lti2?_bwd", "lti_bwd"),
+        (r"tv_phi2?_kernel", "tv_phi"), (r"tv_(group|groupchain|expand|chain)_kernel", "tv_chain"),
+        (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?0>", "tv_fwd"),
         (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?1>", "tv_bwd_agg"),
-        (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?2>", "tv_bwd")]
+        (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?2>", "tv_bwd"),
+        (r"(skew_kernel|unskew_kernel|zi_add_kernel|zf_kernel|gy_eff_kernel|tail_kernel)", "tv_skew"),
+        (r"dg_prep_kernel", "diag_prep"), (r"dg_agg_kernel", "diag_agg"), (r"dg_scan_kernel", "diag_scan"),
+        (r"dg_fwd_emit_kernel", "diag_fwd"), (r"dg_bwd_emit_kernel", "diag_bwd"), (r"dg_reduce_kernel", "diag_red")]
 
 
 def kind_of(name):
@@ -74,7 +77,7 @@ def main():
             a[2] += d.get("dram__bytes_read.sum", 0.0)
             a[3] += d.get("dram__bytes_write.sum", 0.0)
         traffic[w] = {k: (a[2] + a[3]) / a[0] for k, a in agg.items()}
-        fk = next(k for k in ("tv_fwd", "rec_fwd", "lti_fwd") if k in agg)
+        fk = next(k for k in ("tv_fwd", "rec_fwd", "lti_fwd", "diag_fwd") if k in agg)
         steps = agg[fk][0]
         tot = sum(a[1] for a in agg.values()) / steps
         lines.append(f"== {w}: {steps} steps, ncu cold-cache serialised replay; per launch and share of the step")
