@@ -56,6 +56,11 @@ WORKLOADS = {
                     "fp32 (the paper's benchmarked operator at its longest N)", **dict(inputs.CONFIGS["f1"], batch=16)),
     "f3": dict(desc="SURVEY 8(f) f3: Diag-EXT bare recurrence (eigen-basis element-wise complex scans), f1's shape: "
                     "M = 2, batch 16 x 2^20, fp32", diag=True, **dict(inputs.CONFIGS["f1"], batch=16)),
+    # PAPER.md:167 "we expect the gap [Diag-EXT vs EXT] to disappear as M increases": the same pair at M = 4
+    "f1m4": dict(desc="SURVEY 8(f) f1 at M = 4: dense bare recurrence, batch 16 x 2^20, fp32",
+                 **dict(inputs.CONFIGS["f1"], batch=16, order=4)),
+    "f3m4": dict(desc="SURVEY 8(f) f3 at M = 4: Diag-EXT bare recurrence, batch 16 x 2^20, fp32", diag=True,
+                 **dict(inputs.CONFIGS["f1"], batch=16, order=4)),
 }
 
 

@@ -132,9 +132,10 @@ typedef enum {
      * may have written before griddepcontrol.wait -- required when a kernel producing
      * grad_y (a loss) runs between the two calls. */
     IIR_FLAG_GRAD_Y_EARLY = 64,
-    /* Bare recurrence (form IIR_SS), orders 1 and 2: the paper's Diag-EXT variant (PAPER.md:
+    /* Bare recurrence (form IIR_SS), orders 1..4: the paper's Diag-EXT variant (PAPER.md:
      * 132-134, 145, 167).  A = V diag(lam) V^-1 is decomposed on device
-     * (closed form, fp64); the recursion and its VJP run element-wise in the eigenbasis
+     * (fp64: closed form for M <= 2; characteristic polynomial, Durand-Kerner roots and null
+     * vectors for M = 3, 4); the recursion and its VJP run element-wise in the eigenbasis
      * (complex first-order scans) with the eigen-space projection of the inputs and outputs.
      * Same outputs and gradients as the dense path; where A is defective or its eigenbasis is
      * ill-conditioned (kappa(V) > 100 for fp32, 1e4 for fp64) the same kernels run the dense

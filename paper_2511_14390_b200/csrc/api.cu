@@ -129,8 +129,8 @@ static iir_status_t check_desc(const iir_desc_t* d) {
         if (d->coef_mode != IIR_COEF_SHARED && d->coef_mode != IIR_COEF_PER_SEQ)
             return fail(IIR_EUNSUPPORTED, "bare recurrence: A is SHARED or PER_SEQ");
         if (d->order < 1 || d->order > 4) return fail(IIR_EUNSUPPORTED, "bare recurrence: order must be 1..4");
-        if ((d->flags & IIR_FLAG_DIAG) && d->order > 2)
-            return fail(IIR_EUNSUPPORTED, "Diag-EXT (IIR_FLAG_DIAG): order must be 1 or 2 (closed-form eigenbasis)");
+        if ((d->flags & IIR_FLAG_DIAG) && d->order > 4)
+            return fail(IIR_EUNSUPPORTED, "Diag-EXT (IIR_FLAG_DIAG): order must be 1..4");
     }
     if (d->flags & IIR_FLAG_THREE_PHASE_REMOVED)
         return fail(IIR_EUNSUPPORTED, "the three-phase LTI schedule was removed (it lost on every measured shape)");

@@ -1,6 +1,7 @@
 // diag.cu -- SURVEY 8(f) f3: the paper's Diag-EXT variant of the bare recurrence
 // (form IIR_SS with IIR_FLAG_DIAG; Eq.4 and Listing 1,
-// PAPER.md:60-63, 296-343), orders M = 1, 2 (the paper benchmarks M = 2).
+// PAPER.md:60-63, 296-343), orders M = 1..4 (the paper benchmarks M = 2; closed-form eigenbasis for
+// M <= 2, characteristic polynomial + Durand-Kerner roots + null vectors for M = 3, 4).
 //
 //   A = V diag(lam) V^-1  ("decomposing A into diagonal and invertible matrices, reducing
 //   matrix multiplications to element-wise multiplications"):
@@ -57,6 +58,151 @@ __device__ void cmatmul(const double* X, const double* Y, double* Z) {   // comp
     for (int e = 0; e < 2 * M * M; ++e) Z[e] = t[e];
 }
 
+// General eigen-decomposition for M = 3, 4 (fp64, one thread per coefficient set):
+//   characteristic polynomial by Faddeev-LeVerrier (M_k = A M_{k-1} + c_{M-k+1} I,
+//   c_{M-k} = -tr(A M_k) / k), roots by Durand-Kerner iterations polished with Newton steps,
+//   each eigenvector as the null vector of A - lam I by Gaussian elimination with complete
+//   pivoting (free variable = the last pivot), unit 2-norm; V^-1 by Gauss-Jordan with partial
+//   pivoting.  A defective or nearly defective A gives an ill-conditioned V: kappa(V) decides
+//   the dense fallback exactly as for the closed form.
+struct cd { double r, i; };
+__device__ __forceinline__ cd cd_add(cd a, cd b) { return {a.r + b.r, a.i + b.i}; }
+__device__ __forceinline__ cd cd_sub(cd a, cd b) { return {a.r - b.r, a.i - b.i}; }
+__device__ __forceinline__ cd cd_mul(cd a, cd b) { return {a.r * b.r - a.i * b.i, a.r * b.i + a.i * b.r}; }
+__device__ __forceinline__ double cd_abs2(cd a) { return a.r * a.r + a.i * a.i; }
+__device__ __forceinline__ cd cd_div(cd a, cd b) {
+    const double d = cd_abs2(b);
+    return {(a.r * b.r + a.i * b.i) / d, (a.i * b.r - a.r * b.i) / d};
+}
+
+template <int M>
+__device__ bool eig_general(const double (&Ar)[M * M], double (&lr)[M], double (&li)[M], double (&Vr)[M][M],
+                            double (&Vim)[M][M]) {
+    // characteristic polynomial p(x) = sum_k c[k] x^k, c[M] = 1
+    double c[M + 1], Mk[M * M], AM[M * M];
+    c[M] = 1.0;
+    for (int e = 0; e < M * M; ++e) Mk[e] = 0.0;
+    for (int k = 1; k <= M; ++k) {
+        for (int i = 0; i < M; ++i)                       // Mk = A Mk + c[M-k+1] I
+            for (int j = 0; j < M; ++j) {
+                double s = (i == j) ? c[M - k + 1] : 0.0;
+                for (int q = 0; q < M; ++q) s += Ar[i * M + q] * Mk[q * M + j];
+                AM[i * M + j] = s;
+            }
+        for (int e = 0; e < M * M; ++e) Mk[e] = AM[e];
+        double tr = 0.0;                                  // tr(A Mk)
+        for (int i = 0; i < M; ++i)
+            for (int q = 0; q < M; ++q) tr += Ar[i * M + q] * Mk[q * M + i];
+        c[M - k] = -tr / k;
+    }
+    auto peval = [&](cd x, cd& dp) {                      // p(x) and p'(x) by Horner
+        cd pv = {c[M], 0.0};
+        dp = {0.0, 0.0};
+        for (int k = M - 1; k >= 0; --k) {
+            dp = cd_add(cd_mul(dp, x), pv);
+            pv = cd_add(cd_mul(pv, x), cd{c[k], 0.0});
+        }
+        return pv;
+    };
+    double rad = 1.0;
+    for (int k = 0; k < M; ++k) rad = fmax(rad, 1.0 + fabs(c[k]));
+    cd z[M];
+    for (int k = 0; k < M; ++k) {                         // start on a circle, off the real axis
+        const double th = 0.4 + 6.283185307179586 * k / M;
+        z[k] = {0.5 * rad * cos(th), 0.5 * rad * sin(th)};
+    }
+    for (int it = 0; it < 500; ++it) {                    // Durand-Kerner
+        double mv = 0.0;
+        for (int k = 0; k < M; ++k) {
+            cd dp;
+            const cd pv = peval(z[k], dp);
+            cd den = {1.0, 0.0};
+            for (int j = 0; j < M; ++j)
+                if (j != k) den = cd_mul(den, cd_sub(z[k], z[j]));
+            if (cd_abs2(den) == 0.0) den = {1e-300, 0.0};
+            const cd dz = cd_div(pv, den);
+            z[k] = cd_sub(z[k], dz);
+            mv = fmax(mv, cd_abs2(dz) / fmax(cd_abs2(z[k]), 1e-300));
+        }
+        if (mv < 1e-30) break;
+    }
+    for (int k = 0; k < M; ++k)                           // Newton polish
+        for (int it = 0; it < 3; ++it) {
+            cd dp;
+            const cd pv = peval(z[k], dp);
+            if (cd_abs2(dp) > 0.0) z[k] = cd_sub(z[k], cd_div(pv, dp));
+        }
+    bool ok = true;
+    for (int k = 0; k < M; ++k) {
+        lr[k] = z[k].r;
+        li[k] = z[k].i;
+        // null vector of B = A - lam I: elimination with complete pivoting
+        cd Bm[M][M];
+        int col[M];
+        for (int i = 0; i < M; ++i) {
+            col[i] = i;
+            for (int j = 0; j < M; ++j) Bm[i][j] = {Ar[i * M + j] - (i == j ? z[k].r : 0.0), i == j ? -z[k].i : 0.0};
+        }
+        for (int q = 0; q < M - 1; ++q) {
+            int pi = q, pj = q;
+            double best = -1.0;
+            for (int i = q; i < M; ++i)
+                for (int j = q; j < M; ++j)
+                    if (cd_abs2(Bm[i][j]) > best) { best = cd_abs2(Bm[i][j]); pi = i; pj = j; }
+            for (int j = 0; j < M; ++j) { const cd t = Bm[q][j]; Bm[q][j] = Bm[pi][j]; Bm[pi][j] = t; }
+            for (int i = 0; i < M; ++i) { const cd t = Bm[i][q]; Bm[i][q] = Bm[i][pj]; Bm[i][pj] = t; }
+            { const int t = col[q]; col[q] = col[pj]; col[pj] = t; }
+            if (best <= 0.0) { ok = false; continue; }
+            for (int i = q + 1; i < M; ++i) {
+                const cd f = cd_div(Bm[i][q], Bm[q][q]);
+                for (int j = q; j < M; ++j) Bm[i][j] = cd_sub(Bm[i][j], cd_mul(f, Bm[q][j]));
+            }
+        }
+        cd y[M];
+        y[M - 1] = {1.0, 0.0};
+        for (int q = M - 2; q >= 0; --q) {
+            cd sacc = {0.0, 0.0};
+            for (int j = q + 1; j < M; ++j) sacc = cd_add(sacc, cd_mul(Bm[q][j], y[j]));
+            y[q] = cd_abs2(Bm[q][q]) > 0.0 ? cd_div(cd{-sacc.r, -sacc.i}, Bm[q][q]) : cd{0.0, 0.0};
+        }
+        double nrm = 0.0;
+        for (int j = 0; j < M; ++j) nrm += cd_abs2(y[j]);
+        nrm = sqrt(nrm);
+        ok = ok && nrm > 0.0 && nrm == nrm;
+        const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+        for (int j = 0; j < M; ++j) { Vr[col[j]][k] = y[j].r * inv; Vim[col[j]][k] = y[j].i * inv; }
+    }
+    return ok;
+}
+
+// V^-1 by Gauss-Jordan with partial pivoting (complex); false when singular
+template <int M>
+__device__ bool cinv(const double (&Vr)[M][M], const double (&Vim)[M][M], double (&Wr)[M][M], double (&Wi)[M][M]) {
+    cd a[M][2 * M];
+    for (int i = 0; i < M; ++i)
+        for (int j = 0; j < M; ++j) {
+            a[i][j] = {Vr[i][j], Vim[i][j]};
+            a[i][M + j] = {i == j ? 1.0 : 0.0, 0.0};
+        }
+    for (int q = 0; q < M; ++q) {
+        int pi = q;
+        for (int i = q + 1; i < M; ++i)
+            if (cd_abs2(a[i][q]) > cd_abs2(a[pi][q])) pi = i;
+        if (cd_abs2(a[pi][q]) == 0.0) return false;
+        for (int j = 0; j < 2 * M; ++j) { const cd t = a[q][j]; a[q][j] = a[pi][j]; a[pi][j] = t; }
+        const cd piv = a[q][q];
+        for (int j = 0; j < 2 * M; ++j) a[q][j] = cd_div(a[q][j], piv);
+        for (int i = 0; i < M; ++i) {
+            if (i == q) continue;
+            const cd f = a[i][q];
+            for (int j = 0; j < 2 * M; ++j) a[i][j] = cd_sub(a[i][j], cd_mul(f, a[q][j]));
+        }
+    }
+    for (int i = 0; i < M; ++i)
+        for (int j = 0; j < M; ++j) { Wr[i][j] = a[i][M + j].r; Wi[i][j] = a[i][M + j].i; }
+    return true;
+}
+
 template <typename T, int M>
 __global__ void dg_prep_kernel(const T* __restrict__ a, int64_t stride, int64_t nsets, double* __restrict__ tab,
                                double kmax) {
@@ -69,7 +215,9 @@ __global__ void dg_prep_kernel(const T* __restrict__ a, int64_t stride, int64_t 
     for (int e = 0; e < M * M; ++e) Ar[e] = (double)A[e];
     double lr[M], li[M], Vr[M][M], Vim[M][M];
     bool ok = true;
-    if (M == 1) {
+    if constexpr (M >= 3) {
+        ok = eig_general<M>(Ar, lr, li, Vr, Vim);
+    } else if (M == 1) {
         lr[0] = Ar[0]; li[0] = 0; Vr[0][0] = 1; Vim[0][0] = 0;
     } else {
         const double a0 = Ar[0], b0 = Ar[1], c0 = Ar[2], d0 = Ar[3];
@@ -90,7 +238,9 @@ __global__ void dg_prep_kernel(const T* __restrict__ a, int64_t stride, int64_t 
     }
     // inverse (M <= 2) and kappa(V) ~ ||V||_F ||V^-1||_F
     double Wr[M][M], Wi[M][M];
-    if (M == 1) { Wr[0][0] = 1; Wi[0][0] = 0; }
+    if constexpr (M >= 3) {
+        ok = ok && cinv<M>(Vr, Vim, Wr, Wi);
+    } else if (M == 1) { Wr[0][0] = 1; Wi[0][0] = 0; }
     else {
         const double dr = Vr[0][0] * Vr[1][1] - Vim[0][0] * Vim[1][1] - (Vr[0][1] * Vr[1][0] - Vim[0][1] * Vim[1][0]);
         const double di = Vr[0][0] * Vim[1][1] + Vim[0][0] * Vr[1][1] - (Vr[0][1] * Vim[1][0] + Vim[0][1] * Vr[1][0]);
@@ -451,7 +601,13 @@ static iir_status_t run(bool fwd, const iir_desc_t* d, Args& a, void* gA, cudaSt
 
 }  // namespace dg
 
-size_t diag_tab_doubles(int M) { return M == 1 ? dg::Tb<1>::SIZE : dg::Tb<2>::SIZE; }
+size_t diag_tab_doubles(int M) {
+    switch (M) {
+        case 1: return dg::Tb<1>::SIZE; case 2: return dg::Tb<2>::SIZE;
+        case 3: return dg::Tb<3>::SIZE; case 4: return dg::Tb<4>::SIZE;
+    }
+    return 0;
+}
 int diag_chunk() { return dg::DG_C; }
 
 iir_status_t diag_run(bool fwd, const iir_desc_t* d, const void* A, const void* z, const void* v0, void* v,
@@ -464,9 +620,17 @@ iir_status_t diag_run(bool fwd, const iir_desc_t* d, const void* A, const void* 
     a.agg = agg; a.carry = carry; a.gpart = gpart;
     a.B = d->batch; a.T = d->length; a.nch = (int)((d->length + dg::DG_C - 1) / dg::DG_C);
     a.ncoef = d->coef_mode == IIR_COEF_SHARED ? 1 : (int)d->batch;
-    if (d->dtype == IIR_F64)
-        return d->order == 1 ? dg::run<double, 1>(fwd, d, a, gA, st) : dg::run<double, 2>(fwd, d, a, gA, st);
-    return d->order == 1 ? dg::run<float, 1>(fwd, d, a, gA, st) : dg::run<float, 2>(fwd, d, a, gA, st);
+    switch (d->order * 2 + (d->dtype == IIR_F64 ? 1 : 0)) {
+        case 2: return dg::run<float, 1>(fwd, d, a, gA, st);
+        case 3: return dg::run<double, 1>(fwd, d, a, gA, st);
+        case 4: return dg::run<float, 2>(fwd, d, a, gA, st);
+        case 5: return dg::run<double, 2>(fwd, d, a, gA, st);
+        case 6: return dg::run<float, 3>(fwd, d, a, gA, st);
+        case 7: return dg::run<double, 3>(fwd, d, a, gA, st);
+        case 8: return dg::run<float, 4>(fwd, d, a, gA, st);
+        case 9: return dg::run<double, 4>(fwd, d, a, gA, st);
+    }
+    return fail(IIR_EUNSUPPORTED, "Diag-EXT: order must be 1..4");
 }
 
 }  // namespace iirg

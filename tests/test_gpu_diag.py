@@ -26,7 +26,7 @@ def _with_A(p, A):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-@pytest.mark.parametrize("M", [1, 2])
+@pytest.mark.parametrize("M", [1, 2, 3, 4])
 def test_orders_dtypes(dtype, M):
     check(inputs.rec_problem(9500 + M, batch=3, length=3 * 8192 + 77, order=M, dtype=dtype), flags=D)
 
@@ -99,10 +99,43 @@ def test_long_sequence():
     check(p, flags=D)
 
 
-def test_diag_rejects_order_3():
-    desc = B.make_desc(2, 100, 3, "ss", torch.float32, flags=D)
+def test_diag_rejects_order_5():
+    desc = B.make_desc(2, 100, 5, "ss", torch.float32, flags=D)
     assert B.iir_tape_bytes(desc) == 0                    # 0 = invalid descriptor (iirgrad.h)
-    assert b"order must be 1 or 2" in B.lib().iir_last_error()
+    assert b"order must be 1..4" in B.lib().iir_last_error()
+
+
+@pytest.mark.parametrize("A", [
+    [[0.5, 0.2, 0.0], [-0.3, 0.6, 0.1], [0.0, 0.2, -0.7]],          # complex pair + real
+    [[0.9, 0.0, 0.0], [0.1, -0.4, 0.0], [0.0, 0.3, 0.2]],           # triangular, real distinct
+    [[0.0, -0.6, 0.0, 0.0], [0.6, 0.0, 0.0, 0.0], [0.0, 0.0, 0.3, 0.8], [0.0, 0.0, -0.8, 0.3]],   # two pairs
+    [[0.7, 0.2, 0.1, 0.0], [0.0, 0.5, 0.3, 0.1], [0.1, 0.0, -0.6, 0.2], [0.2, 0.1, 0.0, 0.4]],    # dense
+])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_structured_matrices_order_3_4(A, dtype):
+    """The general eigen-decomposition (characteristic polynomial, Durand-Kerner roots,
+    null vectors) on structured 3x3 / 4x4 transitions."""
+    M = len(A)
+    p = _with_A(inputs.rec_problem(9810 + M, batch=2, length=6000, order=M, dtype=dtype), A)
+    assert odiag.diag_condition(p["A"]) < 100
+    check(p, flags=D)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_dense_fallback_order_4(dtype):
+    """A 4x4 transition with a Jordan block (defective): the dense fallback."""
+    A = [[0.9, 1.0, 0.0, 0.0], [0.0, 0.9, 0.0, 0.0], [0.0, 0.0, 0.5, 0.2], [0.0, 0.0, -0.2, 0.5]]
+    p = _with_A(inputs.rec_problem(9920, batch=2, length=7000, order=4, dtype=dtype), A)
+    check(p, flags=D)
+
+
+def test_matches_eigenbasis_oracle_order_4():
+    p = inputs.rec_problem(9955, batch=2, length=3000, order=4, dtype="f64")
+    g = run_gpu(p, flags=D)
+    for b in range(2):
+        o = odiag.diag_recurrence(p["A"], p["v0"][b], p["z"][b], p["gv"][b])
+        assert nrm_err(g["v"][b], o["v"]) <= 1e-10
+        assert nrm_err(g["gz"][b], o["gz"]) <= 1e-10
 
 
 def test_autograd_diag_matches_oracle():

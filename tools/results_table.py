@@ -17,8 +17,14 @@ def load(path):
     return None
 
 
+def traffic_table():
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "traffic.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
 def main():
     d = sys.argv[1]
+    tt = traffic_table()
     names = sys.argv[2:] or ORDER
     rows = ["| Workload | µs / step | samples/s | dominant kernel | its achieved GB/s (algorithmic) | roofline frac | "
             "DRAM bytes / launch (ncu) | e2e samples/s | oracle samples/s (cores) |",
@@ -33,7 +39,7 @@ def main():
         r = j["roofline"]
         cb = j.get("cpu_baseline") or {}
         e2e = (j.get("e2e") or {}).get("value")
-        tr = r.get("traffic")
+        tr = tt.get(w, {}).get(r.get("kernel")) or r.get("traffic")
         rows.append(f"| {w} ({j['config'].get('workload', '')[:40]}) | {j['ms_per_step'] * 1e3:.1f} | {j['value']:.3g} | "
                     f"`{r.get('kernel')}` | {r['achieved']:.0f} | {r['frac']:.3f} | "
                     f"{'%.3g' % tr if tr else 'n/a'} | {e2e:.3g} | "
