@@ -1316,8 +1316,10 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
             finalize_row<M>(p, 0, (int64_t)gridDim.x * NWP, (int64_t)blockIdx.x * NWP + warp, colsum, lane, p.t64);
         }
     }
+    V2_CTA_TRACE(p.trace, p.ntot, 4);
     tmem_fence_before();
     cta_exit(cw, ep, gridDim.x);
+    V2_CTA_TRACE(p.trace, p.ntot, 5);
     tmem_fence_after();
     if (warp == 0) tmem_dealloc(s_tmem, 512);
     V2_CTA_TRACE(p.trace, p.ntot, 3);

@@ -25,6 +25,12 @@ def summarize(name, tr, ntot):
         print(f"== {name}: {len(c)} CTAs: entry p50 {np.median(cs[:, 0]):.2f} max {cs[:, 0].max():.2f}; setup done p50 "
               f"{np.median(cs[:, 1]):.2f} max {cs[:, 1].max():.2f}; tiles done p50 {np.median(cs[:, 2]):.2f} max "
               f"{cs[:, 2].max():.2f}; exit p50 {np.median(cs[:, 3]):.2f} max {cs[:, 3].max():.2f} us")
+        if (c[:, 4] > 0).any():
+            c4 = (c[:, 4:6] - t0) / 1e3
+            i = int(np.argmax(cs[:, 3]))
+            print(f"   finalize done p50 {np.median(c4[:, 0]):.2f} max {c4[:, 0].max():.2f}; cta_exit done p50 "
+                  f"{np.median(c4[:, 1]):.2f} max {c4[:, 1].max():.2f}; last CTA {i}: tiles {cs[i, 2]:.2f} "
+                  f"finalize {c4[i, 0]:.2f} cta_exit {c4[i, 1]:.2f} exit {cs[i, 3]:.2f} us")
         ntot = len(t)
     st = (t[:, :7] - t0) / 1e3                     # us
     span = (t[:, 6].max() - t0) / 1e3
@@ -35,6 +41,10 @@ def summarize(name, tr, ntot):
     for k, v in d.items():
         print(f"   {k:16s} p10 {np.percentile(v, 10):7.2f}  p50 {np.percentile(v, 50):7.2f}  p90 {np.percentile(v, 90):7.2f}"
               f"  mean {v.mean():7.2f} us")
+    late = np.argsort(st[:, 6])[-8:]
+    for i in late:
+        print(f"   late tile (row {i}, warp {t[i, 7]}): start {st[i, 0]:.1f} data {st[i, 1]:.1f} pub {st[i, 2]:.1f} "
+              f"lb {st[i, 3]:.1f} carry {st[i, 4]:.1f} emit {st[i, 5]:.1f} stored {st[i, 6]:.1f}")
     w = t[:, 7]
     per = np.bincount(w.astype(np.int64))
     print(f"   tiles per warp: min {per[per > 0].min()} max {per.max()}")
