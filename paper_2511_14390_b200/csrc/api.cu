@@ -425,6 +425,7 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
         g.B = d->batch; g.T = d->length; g.ntiles = (int)L.ntiles; g.ntot = L.ntot;
         g.vec = (d->length % 4 == 0) && aligned16(grad_y) && aligned16(x) && aligned16(y) && aligned16(grad_x);
         g.trace = g_trace;
+        g.gy_early = (d->flags & IIR_FLAG_GRAD_Y_EARLY) != 0;
         return v2::run(false, d->order, c);
     }
 

@@ -95,6 +95,7 @@ struct BwdArgs {
     double* partial; double* partial2; unsigned* gcnt; unsigned* scnt; int64_t ncoef;
     int64_t B, T; int ntiles; int64_t ntot; int vec;
     unsigned long long* trace;
+    int gy_early;                                     // IIR_FLAG_GRAD_Y_EARLY: grad_y / grad_zf complete before the forward
 };
 
 // Debug phase stamps (lane 0): [0] aggregate start, [1] data ready, [2] published, [3] look-back
@@ -1028,9 +1029,15 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
     mbar_fence_init();
     __syncwarp();
     if (warp == 0) tmem_alloc(&s_tmem, 512);
-    // grad_y may be written by the kernel right before this one (the caller's loss):
-    // nothing the previous kernels wrote is read before griddepcontrol.wait.
-    pdl_wait();
+    // grad_y may be written by the kernel right before this one (the caller's loss): then
+    // nothing the previous kernels wrote is read before griddepcontrol.wait.  With
+    // IIR_FLAG_GRAD_Y_EARLY (grad_y, grad_zf written before the forward was enqueued) the
+    // first tile's dy load, aggregate and publication run while the forward drains: they read
+    // only grad_y, grad_zf, the prologue's tables (complete before the forward passed its own
+    // wait and released this grid) and this direction's workspace; the wait comes before the
+    // first read of y.
+    bool waited = false;
+    if (!p.gy_early) { pdl_wait(); waited = true; }
     pdl_launch_dependents();
     const CarryWs& cw = p.cw;                                  // grid constant: levels indexed from the param bank
     const unsigned ep = __ldcg(cw.epoch);
@@ -1136,6 +1143,7 @@ __global__ void __launch_bounds__(NWP * 32, 1) lti2_bwd_kernel(const __grid_cons
         Sched s2 = s1;
         s2.next();
         __syncwarp();                                            // the previous tile's dx stores have read bX
+        if (!waited) { pdl_wait(); waited = true; }             // y is the forward's output
         issue_xy(s0);
         float V0pre[M];                                          // t0's level-0 look-back slots, in flight
         lookback_prefetch<M>(lane, s0.j, s0.seq, cw, boff, V0pre);   // across t1's aggregate

@@ -92,3 +92,18 @@ def test_v2_bitwise_deterministic_per_seq(engine):
     g2 = run_lti_gpu(p, flags=ENGINES[engine])
     for k in g1:
         assert np.array_equal(g1[k], g2[k]), k
+
+
+@pytest.mark.parametrize("M,T", [(4, 3 * TS2 + 77), (8, 9 * TS2), (6, 1000), (8, 1 << 16)])
+def test_v2_grad_y_early(M, T):
+    """IIR_FLAG_GRAD_Y_EARLY (grad_y written before the forward): the round-2 backward loads dy,
+    aggregates and publishes its first tile before waiting for the forward; same results."""
+    p = inputs.lti_problem(19000 + M, form="tdf", order=M, batch=5, length=T, dtype="f32", angles="spread")
+    g = run_lti_gpu(p, flags=B.IIR_FLAG_ENGINE_V2 | B.IIR_FLAG_GRAD_Y_EARLY)
+    o = run_lti_oracle(p)
+    errs, bad = compare(g, o, TOL["f32"])
+    assert not bad, f"errors {errs}"
+    g2 = run_lti_gpu(p, flags=B.IIR_FLAG_ENGINE_V2)
+    for k in g:
+        if g[k] is not None:
+            assert np.array_equal(g[k], g2[k]), k                # bitwise the same as without the flag
