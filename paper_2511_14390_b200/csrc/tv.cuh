@@ -199,7 +199,10 @@ __device__ __forceinline__ void tv_load_phi(T* dst, const T* src, int lane, bool
 template <typename T, int M, bool BWD>
 __global__ void __launch_bounds__(32 * TV_GRP_WARPS) tv_group_kernel(const TvArgs p) {
     using PB = TvPhiBuf<T, M>;
+    constexpr bool CONV = sizeof(T) != sizeof(double);   // fp32 tape: convert each Phi once
+    constexpr int SDS = M + 1;                            // padded row stride of the fp64 copy
     __shared__ __align__(16) T sphi[TV_GRP_WARPS][2][PB::SLOT];
+    __shared__ __align__(16) double sdp[TV_GRP_WARPS][CONV ? M * SDS : 1];
     __shared__ double som[TV_GRP_WARPS][M];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t gid = (int64_t)blockIdx.x * TV_GRP_WARPS + warp;
@@ -225,21 +228,36 @@ __global__ void __launch_bounds__(32 * TV_GRP_WARPS) tv_group_kernel(const TvArg
         if (lane < M) som[warp][lane] = om;
         cp_async_wait<1>();
         __syncwarp();
-        const T* P = sphi[warp][b];
+        // the segment's transition converted to fp64 ONCE (each lane 1/32 of it; BWD: transposed)
+        // instead of one conversion per use by every lane (M^2 conversions per lane and segment)
+        if constexpr (CONV) {
+            const T* P = sphi[warp][b];
+            double* D = sdp[warp];
+            for (int e = lane; e < M * M; e += 32) {
+                const int r = e / M, c = e - r * M;
+                D[BWD ? c * SDS + r : r * SDS + c] = (double)P[e];
+            }
+        }
+        __syncwarp();
+        // element (i, l) of Phi (BWD: Phi^T)
+        auto el = [&](int i, int l) -> double {
+            if constexpr (CONV) return sdp[warp][i * SDS + l];
+            else { const T* P = sphi[warp][b]; return (double)(BWD ? P[l * M + i] : P[i * M + l]); }
+        };
         if (lane < M) {
             double nc[M];
 #pragma unroll
             for (int i = 0; i < M; ++i) {                // Psi <- Phi Psi  (BWD: Phi^T Psi)
                 double acc = 0.0;
 #pragma unroll
-                for (int l = 0; l < M; ++l) acc = fma((double)(BWD ? P[l * M + i] : P[i * M + l]), col[l], acc);
+                for (int l = 0; l < M; ++l) acc = fma(el(i, l), col[l], acc);
                 nc[i] = acc;
             }
 #pragma unroll
             for (int i = 0; i < M; ++i) col[i] = nc[i];
             double a = wk;                               // omega <- Phi omega + w_k
 #pragma unroll
-            for (int l = 0; l < M; ++l) a = fma((double)(BWD ? P[l * M + lane] : P[lane * M + l]), som[warp][l], a);
+            for (int l = 0; l < M; ++l) a = fma(el(lane, l), som[warp][l], a);
             om = a;
         }
         __syncwarp();
