@@ -58,10 +58,10 @@ Layout tv_layout(const iir_desc_t* d) {
         L.ws_duneg = o; o += al256((size_t)d->batch * M * ts);   //   ... and of u(-1..-M)
         if (d->form == IIR_TDF2) {                         // general TDF (tvtdf.cuh)
             L.ws_f = o; o += al256(bt * ts);               // f (forward) / grad_y + zf tail (backward)
-            L.ws_as = o; o += al256(bt * M * ts);          // skewed rows a~, b~ and their gradients
-            L.ws_bs = o; o += al256(bt * (M + 1) * ts);
-            L.ws_gas = o; o += al256(bt * M * ts);
+            L.ws_gas = o; o += al256(bt * M * ts);         // gradients of the skewed rows
             L.ws_gbs = o; o += al256(bt * (M + 1) * ts);
+            L.ws_as = L.tp_bytes; L.tp_bytes += al256(bt * M * ts);        // the skewed rows a~, b~ on the
+            L.ws_bs = L.tp_bytes; L.tp_bytes += al256(bt * (M + 1) * ts);  // tape (offsets into the tape)
         }
         L.ws_bytes = o;
     }
@@ -129,8 +129,8 @@ static iir_status_t tdf_forward(const iir_desc_t* d, const Layout& L, const void
                                 const void* zi, void* y, void* zf, char* tape, char* ws, cudaStream_t st) {
     const int64_t B = d->batch, N = d->length;
     const int M = d->order;
-    T* as = reinterpret_cast<T*>(ws + L.ws_as);
-    T* bs = reinterpret_cast<T*>(ws + L.ws_bs);
+    T* as = reinterpret_cast<T*>(tape + L.ws_as);                    // skewed rows: tape (reused backward)
+    T* bs = reinterpret_cast<T*>(tape + L.ws_bs);
     T* f = reinterpret_cast<T*>(ws + L.ws_f);
     skew_attrs<T>(M);
     iir_status_t s = launch(K_TV_SKEW, st, [&] {
@@ -165,20 +165,16 @@ static iir_status_t tdf_backward(const iir_desc_t* d, const Layout& L, const voi
                                  void* ga, void* gzi, char* ws, cudaStream_t st) {
     const int64_t B = d->batch, N = d->length;
     const int M = d->order;
-    T* as = reinterpret_cast<T*>(ws + L.ws_as);
-    T* bs = reinterpret_cast<T*>(ws + L.ws_bs);
+    const T* as = reinterpret_cast<const T*>(tape + L.ws_as);        // the forward's skewed rows (tape)
+    const T* bs = reinterpret_cast<const T*>(tape + L.ws_bs);
     T* gas = reinterpret_cast<T*>(ws + L.ws_gas);
     T* gbs = reinterpret_cast<T*>(ws + L.ws_gbs);
     T* gye = reinterpret_cast<T*>(ws + L.ws_f);
     T* g = reinterpret_cast<T*>(ws + L.ws_du);
     T* duneg = reinterpret_cast<T*>(ws + L.ws_duneg);
     skew_attrs<T>(M);
+    skew_attrs<T>(M);
     iir_status_t s = launch(K_TV_SKEW, st, [&] {
-        tdf::skew_kernel<T><<<skew_grid<T>(B, N), tdf::NT, tdf::skew_smem<T>(M), st>>>(static_cast<const T*>(a),
-            static_cast<const T*>(b), as, bs, N, M);
-    });
-    if (s != IIR_OK) return s;
-    s = launch(K_TV_SKEW, st, [&] {
         tdf::gy_eff_kernel<T><<<dim3((unsigned)((N + tdf::NT - 1) / tdf::NT), (unsigned)B), tdf::NT, 0, st>>>(
             static_cast<const T*>(gy), static_cast<const T*>(gzf), static_cast<const T*>(a), gye, N, M);
     });
