@@ -217,6 +217,18 @@ __global__ void dg_prep_kernel(const T* __restrict__ a, int64_t stride, int64_t 
     bool ok = true;
     if constexpr (M >= 3) {
         ok = eig_general<M>(Ar, lr, li, Vr, Vim);
+        // accept the iterative eigen-decomposition only if it reproduces A: max |A V - V Lambda|
+        // small against ||A|| (a repeated root converges to ~eps^(1/m) and its null vectors are
+        // not eigenvectors; the dense fallback is exact)
+        double an = 0.0, res = 0.0;
+        for (int e = 0; e < M * M; ++e) an += Ar[e] * Ar[e];
+        for (int i = 0; i < M; ++i)
+            for (int k = 0; k < M; ++k) {
+                double rr = -(Vr[i][k] * lr[k] - Vim[i][k] * li[k]), ri = -(Vr[i][k] * li[k] + Vim[i][k] * lr[k]);
+                for (int q = 0; q < M; ++q) { rr += Ar[i * M + q] * Vr[q][k]; ri += Ar[i * M + q] * Vim[q][k]; }
+                res = fmax(res, rr * rr + ri * ri);
+            }
+        ok = ok && sqrt(res) <= 1e-12 * (1.0 + sqrt(an));
     } else if (M == 1) {
         lr[0] = Ar[0]; li[0] = 0; Vr[0][0] = 1; Vim[0][0] = 0;
     } else {

@@ -151,3 +151,16 @@ def test_autograd_diag_matches_oracle():
     assert nrm_err(z.grad.cpu().numpy(), o["gz"]) <= 1e-10
     assert nrm_err(A.grad.cpu().numpy(), o["gA"]) <= 1e-10
     assert nrm_err(v0.grad.cpu().numpy(), o["gv0"]) <= 1e-10
+
+
+@pytest.mark.parametrize("A", [
+    [[0.0] * 3] * 3,                                                    # zero transition (triple eigenvalue 0)
+    [[0.7, 0.0, 0.0], [0.0, 0.7, 0.0], [0.0, 0.0, 0.7]],               # r I: repeated, diagonalisable
+    [[0.5, 1.0, 0.0], [0.0, 0.5, 1.0], [0.0, 0.0, 0.5]],               # one Jordan block of size 3
+])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_degenerate_order_3(A, dtype):
+    """Repeated eigenvalues at order 3 (the general eigen-decomposition's degenerate inputs):
+    whichever basis the prologue settles on (eigen or dense fallback), the result is exact."""
+    p = _with_A(inputs.rec_problem(9930, batch=2, length=2000, order=3, dtype=dtype), A)
+    check(p, flags=D)

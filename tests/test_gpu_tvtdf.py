@@ -120,3 +120,10 @@ def test_gradcheck_fp64_tiny():
     x, b, a, zi = mk(2, 19), mk(2, 19, 4), mk(2, 19, 3), mk(2, 3)
     f = lambda x, b, a, zi: lfilter_tv(x, b, a, zi=zi, return_zf=True, form="tdf")
     assert torch.autograd.gradcheck(f, (x, b, a, zi), eps=1e-6, atol=1e-8, rtol=1e-6)
+
+
+def test_gradients_without_grad_x_output():
+    """grad_x = NULL (the FIR adjoint then writes into scratch), grad_zf given: the other
+    gradients are unchanged."""
+    p = inputs.tv_df_problem(37300, batch=2, length=1300, order=5, dtype="f64")
+    check(p, "f64", want=("y", "zf", "gb", "ga", "gzi"))
