@@ -134,8 +134,8 @@ __global__ void __launch_bounds__(32 * TV_PHI_WARPS, IIRG_PHI_MINB) tv_phi_kerne
 #pragma unroll
                     for (int i = 0; i < M; ++i) cf[i] = cs[s2 * M + i];
                 }
-                if constexpr (sizeof(A) == 8 && M >= 8) {
-                    // fp64: four independent partial sums (terms i = 3 mod 4 ... 0 mod 4) cut the
+                if constexpr (M >= 8) {
+                    // four independent partial sums (terms i = 3 mod 4 ... 0 mod 4) cut the
                     // dependent DFMA chain from M to M/4 + 2 (latency, not the FP64 pipe, bound it)
                     A ps[4] = {yn, A(0), A(0), A(0)};
 #pragma unroll
@@ -395,7 +395,9 @@ __device__ __forceinline__ void load_row(const T* __restrict__ ar, T (&c)[M]) {
 // the coefficient bytes, and fp64 removes the O(TV_SEG) fp32 rounding growth of
 // a long feedback loop ("TV precision").
 constexpr int TV_SEQ_WARPS = 2;           // warps per CTA (x 32 segments)
-enum TvMode { TV_FWD_EMIT = 0, TV_BWD_AGG = 1, TV_BWD_EMIT = 2 };
+// TV_FWD_AGG: the forward recursion from the zero state over each segment, fp64, writing only
+// the segment's zero-state response w_k (no output): the input column of tv_phi in fp64.
+enum TvMode { TV_FWD_EMIT = 0, TV_BWD_AGG = 1, TV_BWD_EMIT = 2, TV_FWD_AGG = 3 };
 // Samples per staged chunk: the coefficient stream is latency-bound (one
 // thread per segment, few warps per SM), so the bytes in flight per lane are
 // what sets the bandwidth; the emit-backward also stages grad_a (its TMA
@@ -427,7 +429,8 @@ template <typename T, int M, int MODE>
 __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs p) {
     using R = double;
     using ST = TvStage<T, M, MODE>;
-    constexpr bool BWD = MODE != TV_FWD_EMIT;
+    constexpr bool BWD = MODE == TV_BWD_AGG || MODE == TV_BWD_EMIT;
+    constexpr bool FWD = !BWD;
     constexpr int C = ST::C;
     constexpr int NCH = TV_SEG / C;
     constexpr int RB = M * (int)sizeof(T);                  // bytes of one coefficient row
@@ -493,7 +496,7 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
     };
 #pragma unroll
     for (int i = 0; i < M; ++i) {
-        v[i] = (MODE == TV_BWD_AGG || !valid) ? 0.0 : p.carry[seg * M + i];
+        v[i] = (MODE == TV_BWD_AGG || MODE == TV_FWD_AGG || !valid) ? 0.0 : p.carry[seg * M + i];
         yw[i] = (MODE == TV_BWD_EMIT && valid) ? yat(n1 - 2 - i) : T(0);
     }
     // The per-sample scalar streams (x forward; dy and the y window backward) are
@@ -508,7 +511,7 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
             const int s2 = BWD ? C - 1 - u : u;
             const int64_t n = cs + s2;
             const bool in = valid && n >= n0 && n < n1;
-            if constexpr (MODE == TV_FWD_EMIT) ps[slot][u] = in ? __ldg(xrow + n) : T(0);
+            if constexpr (FWD) ps[slot][u] = in ? __ldg(xrow + n) : T(0);
             else ps[slot][u] = (in && gyrow != nullptr) ? __ldg(gyrow + n) : T(0);
             if constexpr (MODE == TV_BWD_EMIT) py[slot][u] = in ? yat(n - 1 - M) : T(0);
         }
@@ -549,7 +552,7 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
 #pragma unroll
                 for (int i = 0; i < M; ++i) cf[i] = my[s2 * M + i];
             }
-            if constexpr (MODE == TV_FWD_EMIT) {
+            if constexpr (FWD) {
                 if (in) {
                     // four independent partial sums of the older terms; only the
                     // newest term (a_1 y(n-1)) waits on the previous sample
@@ -561,7 +564,7 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
 #pragma unroll
                     for (int i = M - 1; i >= 1; --i) v[i] = v[i - 1];
                     v[0] = yn;
-                    youtrow[n] = (T)yn;
+                    if constexpr (MODE == TV_FWD_EMIT) youtrow[n] = (T)yn;
                 }
             } else {
                 if (in) {
@@ -608,7 +611,7 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
 #pragma unroll
             for (int i = 0; i < M; ++i) zf[i] = (T)v[i];
         }
-    } else if constexpr (MODE == TV_BWD_AGG) {
+    } else if constexpr (MODE == TV_BWD_AGG || MODE == TV_FWD_AGG) {
 #pragma unroll
         for (int i = 0; i < M; ++i) p.w[seg * M + i] = v[i];
     } else {
