@@ -404,8 +404,14 @@ enum TvMode { TV_FWD_EMIT = 0, TV_BWD_AGG = 1, TV_BWD_EMIT = 2, TV_FWD_AGG = 3 }
 // store beats per-lane row stores), so it keeps smaller chunks to stay at the
 // same occupancy.
 constexpr int TV_PF = 3;                  // chunks of scalar-stream prefetch in tv_seq_kernel (ring of 4)
+#ifndef IIRG_TV_CHF
+#define IIRG_TV_CHF 8                        // samples per staged coefficient chunk (forward / aggregate modes)
+#endif
+#ifndef IIRG_TV_CHB
+#define IIRG_TV_CHB 4                        // ... backward emit (three buffers)
+#endif
 template <typename T, int M, int MODE> constexpr int tv_chunk() {
-    return (MODE != TV_BWD_EMIT && M * (int)sizeof(T) <= 128) ? 8 : 4;
+    return (MODE != TV_BWD_EMIT && M * (int)sizeof(T) <= 128) ? IIRG_TV_CHF : IIRG_TV_CHB;
 }
 template <typename T, int M, int MODE>
 __device__ __forceinline__ int64_t chunk_start_of(int64_t n0, int c, bool bwd) {
