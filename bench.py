@@ -80,8 +80,9 @@ def algorithmic_bytes(w):
         # tv_bwd reads a, dy, y and writes dx, grad_a.  tv_chain moves only the
         # per-segment tape (M^2 per 512 samples): design overhead, no per-sample bytes.
         M = w["order"]
-        d = {"tv_phi": (M + 1) * s, "tv_chain": 0, "tv_fwd": (M + 2) * s, "tv_bwd_agg": (M + 1) * s,
-             "tv_bwd": (2 * M + 3) * s}
+        # tv_wagg: the fp64 re-run of the segments' zero-state responses (reads a, x; beside tv_phi)
+        d = {"tv_phi": (M + 1) * s, "tv_wagg": (M + 1) * s, "tv_chain": 0, "tv_fwd": (M + 2) * s,
+             "tv_bwd_agg": (M + 1) * s, "tv_bwd": (2 * M + 3) * s}
         if w.get("fir"):       # FIR stage, 3 launches per step: fwd b, u -> y; bwd b, dy, u -> du, grad_b; zi add
             d["tv_fir"] = ((M + 3) + (2 * M + 5)) * s / 3
         if w.get("fir") and w["form"] == "tdf":   # TDF: skew / unskew of the (2M+1) rows (design overhead)

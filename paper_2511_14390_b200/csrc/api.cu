@@ -24,13 +24,25 @@ iir_status_t fail(iir_status_t st, const std::string& msg) {
     g_err = msg;
     return st;
 }
+SideStream& side_stream() {
+    thread_local SideStream per_dev[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    SideStream& s = per_dev[dev & 63];
+    if (s.st == nullptr) {
+        cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming);
+    }
+    return s;
+}
 }  // namespace iirg
 
 // ------------------------------------------------------- instrumentation ----
 static const char* kKindNames[K_NUM] = {"lti_prep", "lti_fwd", "lti_bwd", "tv_phi", "tv_chain", "tv_fwd",
                                         "tv_bwd_agg", "tv_bwd", "rec_fwd", "rec_bwd", "state_carry", "tv_fir",
                                         "diag_prep", "diag_agg", "diag_scan", "diag_fwd", "diag_bwd", "diag_red",
-                                        "tv_skew"};
+                                        "tv_skew", "tv_wagg"};
 static std::atomic<int64_t> g_launches{0};
 struct ProfRec { int kind; cudaEvent_t e0, e1; };
 static std::mutex g_pmu;

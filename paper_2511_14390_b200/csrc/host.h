@@ -15,7 +15,7 @@ iir_status_t fail(iir_status_t st, const std::string& msg);
 
 enum Kind { K_LTI_PREP = 0, K_LTI_FWD, K_LTI_BWD, K_TV_PHI, K_TV_CHAIN, K_TV_FWD, K_TV_BWD_AGG, K_TV_BWD, K_REC_FWD,
             K_REC_BWD, K_STATE_CARRY, K_TV_FIR, K_DIAG_PREP, K_DIAG_AGG, K_DIAG_SCAN, K_DIAG_FWD, K_DIAG_BWD, K_DIAG_RED,
-            K_TV_SKEW, K_NUM };
+            K_TV_SKEW, K_TV_WAGG, K_NUM };
 
 // Launch bookkeeping: counts every kernel and (when profiling is on) brackets it
 // with CUDA events on its stream.
@@ -46,6 +46,15 @@ struct PerDevice {
         if (!done[dev & 63]) { f(); done[dev & 63] = true; }
     }
 };
+
+// A second stream per (host thread, device) for work of one call that is independent of the
+// caller stream's current work (fork: event on the caller stream -> side stream; join: event on
+// the side stream -> caller stream).  Works under stream capture (the events become graph edges).
+struct SideStream {
+    cudaStream_t st = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream& side_stream();
 
 constexpr int MAX_LEVELS = 4;
 struct Layout {

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(32 * TV_PHI_WARPS, IIRG_PHI_MINB) tv_phi_kerne
         T* ph = static_cast<T*>(p.phi) + seg * M * M;
 #pragma unroll
         for (int i = 0; i < M; ++i) ph[i * M + col] = (T)v[i];             // column `col`
-    } else if (col == M) {
+    } else if (col == M && p.w != nullptr) {                        // (NULL: w comes from TV_FWD_AGG)
 #pragma unroll
         for (int i = 0; i < M; ++i) p.w[seg * M + i] = (double)v[i];
     }

@@ -202,11 +202,21 @@ static iir_status_t tv_fwd_m(const Layout& L, TvArgs& a, cudaStream_t st) {
         // which carry the fp32-sequential error into the carries (R18), by an fp64 re-run of
         // the recursion (TV_FWD_AGG) that overwrites tv_phi's fp32 w.  The fp64 tv_phi was
         // bound by its fp64 coefficient broadcasts (twice the shared-memory traffic of fp32).
+        // The two are independent (both read a and x): the fp64 re-run (few, latency-bound warps)
+        // runs on a side stream beside the transitions (many warps, FMA / shared-memory bound).
+        SideStream& ss = side_stream();
+        if (cudaEventRecord(ss.fork, st) != cudaSuccess || cudaStreamWaitEvent(ss.st, ss.fork, 0) != cudaSuccess)
+            return fail(IIR_ECUDA, "side-stream fork failed");
+        s = launch(K_TV_WAGG, ss.st, [&] { tv_seq_launch<T, M, TV_FWD_AGG>(nseg_tot, a, ss.st); });
+        if (s != IIR_OK) return s;
+        if (cudaEventRecord(ss.join, ss.st) != cudaSuccess) return fail(IIR_ECUDA, "side-stream join failed");
+        TvArgs aphi = a;
+        aphi.w = nullptr;                                   // w is the side stream's
         s = launch(K_TV_PHI, st, [&] {
-            tv_phi_kernel<T, M, T><<<(nseg_tot + TV_PHI_WARPS - 1) / TV_PHI_WARPS, 32 * TV_PHI_WARPS, 0, st>>>(a);
+            tv_phi_kernel<T, M, T><<<(nseg_tot + TV_PHI_WARPS - 1) / TV_PHI_WARPS, 32 * TV_PHI_WARPS, 0, st>>>(aphi);
         });
         if (s != IIR_OK) return s;
-        s = launch(K_TV_PHI, st, [&] { tv_seq_launch<T, M, TV_FWD_AGG>(nseg_tot, a, st); });
+        if (cudaStreamWaitEvent(st, ss.join, 0) != cudaSuccess) return fail(IIR_ECUDA, "side-stream join failed");
     } else {
         s = launch(K_TV_PHI, st, [&] {
             tv_phi_kernel<T, M, double><<<(nseg_tot + TV_PHI_WARPS - 1) / TV_PHI_WARPS, 32 * TV_PHI_WARPS, 0, st>>>(a);

@@ -21,7 +21,7 @@ KIND = [(r"rec_fwd_kernel", "rec_fwd"), (r"rec_bwd_kernel", "rec_bwd"), (r"lti2?
         (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?0>", "tv_fwd"),
         (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?1>", "tv_bwd_agg"),
         (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?2>", "tv_bwd"),
-        (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?3>", "tv_phi"),   # TV_FWD_AGG: fp64 w re-run
+        (r"tv_seq_kernel<[^,]+, *(\(int\))?\d+, *(\(int\))?3>", "tv_wagg"),  # TV_FWD_AGG: fp64 w re-run
         (r"(skew_kernel|unskew_kernel|zi_add_kernel|zf_kernel|gy_eff_kernel|tail_kernel)", "tv_skew"),
         (r"dg_prep_kernel", "diag_prep"), (r"dg_agg_kernel", "diag_agg"), (r"dg_scan_kernel", "diag_scan"),
         (r"dg_fwd_emit_kernel", "diag_fwd"), (r"dg_bwd_emit_kernel", "diag_bwd"), (r"dg_reduce_kernel", "diag_red")]
