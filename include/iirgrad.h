@@ -111,12 +111,16 @@ typedef enum {
      * rejected with IIR_EUNSUPPORTED. */
     IIR_FLAG_SINGLE_PASS = 2,
     IIR_FLAG_THREE_PHASE_REMOVED = 4,
-    /* IIR_COEF_PER_SAMPLE with a per-sample numerator: the general
-     * time-varying DF-II filter u(n) = x(n) - sum_i a_i(n) u(n-i),
-     * y(n) = sum_k b_k(n) u(n-k), both rows applied at output time n (R19);
-     * b (B, T, M+1) and grad_b (B, T, M+1) are then required / returned; zi, zf are
-     * the internal signal history [u(-1)..u(-M)].  Without it, PER_SAMPLE is the
-     * all-pole filter (b must be NULL). */
+    /* IIR_COEF_PER_SAMPLE with a per-sample numerator; b (B, T, M+1) and
+     * grad_b (B, T, M+1) are then required / returned.
+     *   form IIR_DF2: the general time-varying DF-II filter u(n) = x(n) - sum_i a_i(n) u(n-i),
+     *     y(n) = sum_k b_k(n) u(n-k), both rows applied at output time n (R19);
+     *     zi, zf are the internal signal history [u(-1)..u(-M)].
+     *   form IIR_TDF2: the TDF-II realisation built from the rows of sample n (PAPER.md:67-68,
+     *     DESIGN.md R20): y(n) = b_0(n) x(n) + v_1(n), v_i(n+1) = v_{i+1}(n) + b_i(n) x(n)
+     *     - a_i(n) y(n); zi = v(0), zf = v(N) (scipy's zi for constant rows); iir_backward
+     *     needs the forward's x.
+     * Without the flag, PER_SAMPLE is the all-pole DF filter (form IIR_DF2, b must be NULL). */
     IIR_FLAG_PER_SAMPLE_B = 8,
     /* Engine of fp32 TDF-II with SHARED / PER_SEQ coefficients.
      * Default: the round-2 engine (persistent warp tiles, TMEM parking, fused backward)
