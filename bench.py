@@ -85,8 +85,8 @@ def algorithmic_bytes(w):
              "tv_bwd_agg": (M + 1) * s, "tv_bwd": (2 * M + 3) * s}
         if w.get("fir"):       # FIR stage, 3 launches per step: fwd b, u -> y; bwd b, dy, u -> du, grad_b; zi add
             d["tv_fir"] = ((M + 3) + (2 * M + 5)) * s / 3
-        if w.get("fir") and w["form"] == "tdf":   # TDF: skew / unskew of the (2M+1) rows (design overhead)
-            d["tv_skew"] = 2 * (2 * M + 1) * s
+        if w.get("fir") and w["form"] == "tdf":   # TDF: skew of a / unskew of grad_a~ (design overhead;
+            d["tv_skew"] = 4 * M * s             # b is read at skewed rows in place): read + write each
         return d
     # HBM bytes per kernel the method must move: fwd reads x, writes y (+u for DF);
     # bwd reads dy, x, y (TDF) or dy, u (DF) and writes dx: 24 B/sample in fp32

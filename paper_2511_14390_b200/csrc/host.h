@@ -67,7 +67,7 @@ struct Layout {
     size_t ws_sent = 0, ws_sent_bytes = 0;                 // look-back slots, initialised to all-ones (NaN)
     size_t ws_agg[MAX_LEVELS] = {0, 0, 0, 0}, ws_part = 0, ws_part2 = 0, ws_bytes = 0;
     size_t ws_du = 0, ws_duneg = 0;                        // general TV DF: FIR-stage adjoint of u
-    size_t ws_f = 0, ws_as = 0, ws_bs = 0, ws_gas = 0, ws_gbs = 0;   // general TV TDF (tvtdf.cuh)
+    size_t ws_f = 0, ws_as = 0, ws_gas = 0;   // general TV TDF (tvtdf.cuh)
     size_t ws_psi = 0, ws_omega = 0, ws_sgrp = 0;          // TV two-level chain
     size_t tp_tab = 0, tp_u = 0, tp_extra = 0, tp_bytes = 0;
     size_t tp_t64 = 0, tp_t32 = 0;                         // v2 engine tables (lti2.cuh)

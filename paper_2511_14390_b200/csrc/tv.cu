@@ -58,10 +58,9 @@ Layout tv_layout(const iir_desc_t* d) {
         L.ws_duneg = o; o += al256((size_t)d->batch * M * ts);   //   ... and of u(-1..-M)
         if (d->form == IIR_TDF2) {                         // general TDF (tvtdf.cuh)
             L.ws_f = o; o += al256(bt * ts);               // f (forward) / grad_y + zf tail (backward)
-            L.ws_gas = o; o += al256(bt * M * ts);         // gradients of the skewed rows
-            L.ws_gbs = o; o += al256(bt * (M + 1) * ts);
-            L.ws_as = L.tp_bytes; L.tp_bytes += al256(bt * M * ts);        // the skewed rows a~, b~ on the
-            L.ws_bs = L.tp_bytes; L.tp_bytes += al256(bt * (M + 1) * ts);  // tape (offsets into the tape)
+            L.ws_gas = o; o += al256(bt * M * ts);         // gradient of the skewed rows a~
+            L.ws_as = L.tp_bytes; L.tp_bytes += al256(bt * M * ts);        // the skewed rows a~ on the tape
+                                                                           // (offset into the tape)
         }
         L.ws_bytes = o;
     }
@@ -80,10 +79,11 @@ static iir_status_t tv_op(int op, const iir_desc_t* d, const Layout& L, TvArgs& 
 }
 template <typename T>
 static iir_status_t fir_dispatch(bool fwd, const iir_desc_t* d, const void* b, const void* u, const void* zi,
-                                 const void* gy, void* y, void* du, void* duneg, void* gb, cudaStream_t st) {
+                                 const void* gy, void* y, void* du, void* duneg, void* gb, cudaStream_t st,
+                                 bool skew = false) {
     static Layout none;
     TvArgs dummy{};
-    return tv_op<T>(fwd ? 2 : 3, d, none, dummy, b, u, zi, gy, y, du, duneg, gb, st);
+    return tv_op<T>(skew ? (fwd ? 4 : 5) : (fwd ? 2 : 3), d, none, dummy, b, u, zi, gy, y, du, duneg, gb, st);
 }
 template <typename T>
 static iir_status_t tv_dispatch(bool fwd, int, const Layout& L, TvArgs& a, cudaStream_t st, const iir_desc_t* d) {
@@ -130,16 +130,15 @@ static iir_status_t tdf_forward(const iir_desc_t* d, const Layout& L, const void
     const int64_t B = d->batch, N = d->length;
     const int M = d->order;
     T* as = reinterpret_cast<T*>(tape + L.ws_as);                    // skewed rows: tape (reused backward)
-    T* bs = reinterpret_cast<T*>(tape + L.ws_bs);
     T* f = reinterpret_cast<T*>(ws + L.ws_f);
     skew_attrs<T>(M);
     iir_status_t s = launch(K_TV_SKEW, st, [&] {
         tdf::skew_kernel<T><<<skew_grid<T>(B, N), tdf::NT, tdf::skew_smem<T>(M), st>>>(static_cast<const T*>(a),
-            static_cast<const T*>(b), as, bs, N, M);
+            as, N, M);
     });
     if (s != IIR_OK) return s;
-    // f(n) = sum_k b~_k(n) x(n-k) (zero history), + zi(n) for n < M
-    s = fir_dispatch<T>(true, d, bs, x, nullptr, nullptr, f, nullptr, nullptr, nullptr, st);
+    // f(n) = sum_k b~_k(n) x(n-k) (b read at skewed rows; zero history), + zi(n) for n < M
+    s = fir_dispatch<T>(true, d, b, x, nullptr, nullptr, f, nullptr, nullptr, nullptr, st, true);
     if (s != IIR_OK) return s;
     if (zi != nullptr) {
         s = launch(K_TV_SKEW, st, [&] {
@@ -166,13 +165,10 @@ static iir_status_t tdf_backward(const iir_desc_t* d, const Layout& L, const voi
     const int64_t B = d->batch, N = d->length;
     const int M = d->order;
     const T* as = reinterpret_cast<const T*>(tape + L.ws_as);        // the forward's skewed rows (tape)
-    const T* bs = reinterpret_cast<const T*>(tape + L.ws_bs);
     T* gas = reinterpret_cast<T*>(ws + L.ws_gas);
-    T* gbs = reinterpret_cast<T*>(ws + L.ws_gbs);
     T* gye = reinterpret_cast<T*>(ws + L.ws_f);
     T* g = reinterpret_cast<T*>(ws + L.ws_du);
     T* duneg = reinterpret_cast<T*>(ws + L.ws_duneg);
-    skew_attrs<T>(M);
     skew_attrs<T>(M);
     iir_status_t s = launch(K_TV_SKEW, st, [&] {
         tdf::gy_eff_kernel<T><<<dim3((unsigned)((N + tdf::NT - 1) / tdf::NT), (unsigned)B), tdf::NT, 0, st>>>(
@@ -187,14 +183,14 @@ static iir_status_t tdf_backward(const iir_desc_t* d, const Layout& L, const voi
              ((reinterpret_cast<uintptr_t>(gas) & 15u) == 0);
     s = tv_dispatch<T>(false, M, L, ta, st, d);
     if (s != IIR_OK) return s;
-    // FIR adjoint on the skewed rows: grad_x, grad_b~
-    s = fir_dispatch<T>(false, d, bs, x, nullptr, g, nullptr, gx != nullptr ? gx : static_cast<void*>(gye), duneg,
-                        gbs, st);
+    // FIR adjoint on the skewed rows (b read in place): grad_x, grad_b (unskewed)
+    s = fir_dispatch<T>(false, d, b, x, nullptr, g, nullptr, gx != nullptr ? gx : static_cast<void*>(gye), duneg,
+                        gb, st, true);
     if (s != IIR_OK) return s;
-    if (ga != nullptr || gb != nullptr) {
+    if (ga != nullptr) {
         s = launch(K_TV_SKEW, st, [&] {
-            tdf::unskew_kernel<T><<<skew_grid<T>(B, N), tdf::NT, tdf::skew_smem<T>(M), st>>>(gas, gbs,
-                static_cast<T*>(ga), static_cast<T*>(gb), N, M);
+            tdf::unskew_kernel<T><<<skew_grid<T>(B, N), tdf::NT, tdf::skew_smem<T>(M), st>>>(gas,
+                static_cast<T*>(ga), N, M);
         });
         if (s != IIR_OK) return s;
     }

@@ -29,7 +29,10 @@ constexpr int TV_PHI_WARPS = 4;      // warps (segments) per CTA of the Phi kern
 template <typename T> constexpr int tv_ch() { return sizeof(T) == 4 ? 32 : 16; }   // staged chunk (Phi kernel)
 constexpr int TV_U = 8;              // unroll of the sequential recursions
 
-constexpr int TV_GS = 16;            // segments per group of the two-level chain
+#ifndef IIRG_TV_GS
+#define IIRG_TV_GS 16
+#endif
+constexpr int TV_GS = IIRG_TV_GS;    // segments per group of the two-level chain
 constexpr int TV_GRP_WARPS = 2;      // warps (groups) per CTA of the group / expansion kernels
 
 struct TvArgs {

@@ -23,6 +23,11 @@ namespace iirg {
 // memory by coalesced loads (row stride padded to an odd count: the per-thread
 // row reads are conflict free); grad_b rows leave through shared memory by
 // coalesced stores.
+// skew != 0 (the general TDF filter, tvtdf.cuh, reading R20): the stage runs on the SKEWED
+// rows b~_k(n) = b_k(n - k) (zero before n = 0) without materialising them: the forward
+// stages b rows [n0 - M, n0 + FIR_TS) and reads b~_k(n) as row n - k; the adjoint uses
+// b~_k(m + k) = b_k(m) (rows of the tile only) and writes grad_b_k(m) = grad_b~_k(m + k)
+// = dy(m + k) u(m) directly (the unskewed gradient; u's history is zero: no du(-1..-M)).
 constexpr int FIR_TS = 256;
 template <int M> struct Fir {
     static constexpr int K = M + 1, RS = K | 1;
@@ -32,10 +37,11 @@ __device__ __forceinline__ void fir_stage_rows(T* sb, const T* __restrict__ b, i
                                                int nr) {
     constexpr int K = Fir<M>::K, RS = Fir<M>::RS, W = 16 / (int)sizeof(T);
     const int nv = (int)max((int64_t)0, min((int64_t)nr, Tlen - r0));   // rows inside the sequence
+    const int z = r0 < 0 ? (int)-r0 : 0;                                 // rows before n = 0 (skew: zero)
     const T* src = b + (seq * Tlen + r0) * K;
     // asynchronous copies (no register round trip: every load of the tile is in
     // flight at once); rows past the sequence end are zero-filled
-    if (RS == K && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {     // same layout: 16 B chunks
+    if (z == 0 && RS == K && (reinterpret_cast<uintptr_t>(src) & 15u) == 0) {     // same layout: 16 B chunks
         const int nvalid = nv * K;
         for (int e = threadIdx.x * W; e < nr * K; e += FIR_TS * W) {
             if (e + W <= nr * K) {
@@ -52,7 +58,7 @@ __device__ __forceinline__ void fir_stage_rows(T* sb, const T* __restrict__ b, i
     } else {
         for (int e = threadIdx.x; e < nr * K; e += FIR_TS) {
             const int r = e / K, k = e - r * K;
-            if (r < nv) cp_async_elem(sb + r * RS + k, src + e);
+            if (r >= z && r < nv) cp_async_elem(sb + r * RS + k, src + e);
             else sb[r * RS + k] = T(0);
         }
     }
@@ -65,7 +71,7 @@ __device__ __forceinline__ T u_at(const T* __restrict__ u, const T* __restrict__
     return zi != nullptr ? zi[seq * M + (-m - 1)] : T(0);
 }
 template <typename T, int M>
-constexpr size_t fir_fwd_smem() { return ((size_t)FIR_TS * Fir<M>::RS + FIR_TS + M) * sizeof(T); }
+constexpr size_t fir_fwd_smem() { return ((size_t)(FIR_TS + M) * Fir<M>::RS + FIR_TS + M) * sizeof(T); }
 template <typename T, int M>
 constexpr size_t fir_bwd_smem() {
     return ((size_t)(FIR_TS + M) * Fir<M>::RS + (size_t)FIR_TS * Fir<M>::K + 2 * (FIR_TS + M)) * sizeof(T);
@@ -74,21 +80,27 @@ constexpr size_t fir_bwd_smem() {
 template <typename T, int M>
 __global__ void __launch_bounds__(FIR_TS) tv_fir_fwd_kernel(const T* __restrict__ b, const T* __restrict__ u,
                                                             const T* __restrict__ zi, T* __restrict__ y,
-                                                            int64_t Tlen, int64_t ntile) {
+                                                            int64_t Tlen, int64_t ntile, int skew) {
     constexpr int RS = Fir<M>::RS;
     extern __shared__ __align__(16) unsigned char fir_raw[];
     T* sb = reinterpret_cast<T*>(fir_raw);
-    T* su = sb + FIR_TS * RS;                       // u(n0 - M .. n0 + FIR_TS - 1)
+    T* su = sb + (FIR_TS + M) * RS;                 // u(n0 - M .. n0 + FIR_TS - 1)
     const int64_t seq = blockIdx.x / ntile, n0 = (blockIdx.x - seq * ntile) * (int64_t)FIR_TS;
     const int t = threadIdx.x;
-    fir_stage_rows<T, M>(sb, b, seq, Tlen, n0, FIR_TS);
+    if (skew) fir_stage_rows<T, M>(sb, b, seq, Tlen, n0 - M, FIR_TS + M);   // rows n0 - M ..
+    else fir_stage_rows<T, M>(sb, b, seq, Tlen, n0, FIR_TS);
     for (int e = t; e < FIR_TS + M; e += FIR_TS) su[e] = u_at<T, M>(u, zi, seq, Tlen, n0 - M + e);
     cp_async_wait<0>();
     __syncthreads();
     if (n0 + t >= Tlen) return;
     double acc = 0.0;
+    if (skew) {                                     // b~_k(n) = b_k(n - k): staged row t + M - k
 #pragma unroll
-    for (int k = 0; k <= M; ++k) acc = fma((double)sb[t * RS + k], (double)su[M + t - k], acc);
+        for (int k = 0; k <= M; ++k) acc = fma((double)sb[(t + M - k) * RS + k], (double)su[M + t - k], acc);
+    } else {
+#pragma unroll
+        for (int k = 0; k <= M; ++k) acc = fma((double)sb[t * RS + k], (double)su[M + t - k], acc);
+    }
     y[seq * Tlen + n0 + t] = (T)acc;
 }
 
@@ -96,7 +108,8 @@ template <typename T, int M>
 __global__ void __launch_bounds__(FIR_TS) tv_fir_bwd_kernel(const T* __restrict__ b, const T* __restrict__ u,
                                                             const T* __restrict__ zi, const T* __restrict__ gy,
                                                             T* __restrict__ du, T* __restrict__ duneg,
-                                                            T* __restrict__ gb, int64_t Tlen, int64_t ntile) {
+                                                            T* __restrict__ gb, int64_t Tlen, int64_t ntile,
+                                                            int skew) {
     constexpr int K = Fir<M>::K, RS = Fir<M>::RS;
     extern __shared__ __align__(16) unsigned char fir_raw[];
     T* sb = reinterpret_cast<T*>(fir_raw);         // b rows n0 .. n0 + FIR_TS + M - 1
@@ -105,7 +118,7 @@ __global__ void __launch_bounds__(FIR_TS) tv_fir_bwd_kernel(const T* __restrict_
     T* su = sdy + FIR_TS + M;                      // u(n0 - M .. n0 + FIR_TS - 1)
     const int64_t seq = blockIdx.x / ntile, n0 = (blockIdx.x - seq * ntile) * (int64_t)FIR_TS;
     const int t = threadIdx.x;
-    fir_stage_rows<T, M>(sb, b, seq, Tlen, n0, FIR_TS + M);
+    fir_stage_rows<T, M>(sb, b, seq, Tlen, n0, skew ? FIR_TS : FIR_TS + M);
     for (int e = t; e < FIR_TS + M; e += FIR_TS) {
         const int64_t n = n0 + e;
         sdy[e] = (gy != nullptr && n < Tlen) ? gy[seq * Tlen + n] : T(0);
@@ -113,7 +126,17 @@ __global__ void __launch_bounds__(FIR_TS) tv_fir_bwd_kernel(const T* __restrict_
     }
     cp_async_wait<0>();
     __syncthreads();
-    if (n0 + t < Tlen) {                            // du(m) = sum_k b_k(m+k) dy(m+k)
+    if (skew) {
+        if (n0 + t < Tlen) {                        // du(m) = sum_k b~_k(m+k) dy(m+k) = sum_k b_k(m) dy(m+k)
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k <= M; ++k) acc = fma((double)sb[t * RS + k], (double)sdy[t + k], acc);
+            du[seq * Tlen + n0 + t] = (T)acc;
+            const double un = (double)su[M + t];    // grad_b_k(m) = grad_b~_k(m+k) = dy(m+k) u(m)
+#pragma unroll
+            for (int k = 0; k <= M; ++k) sg[t * K + k] = (T)((double)sdy[t + k] * un);
+        }
+    } else if (n0 + t < Tlen) {                     // du(m) = sum_k b_k(m+k) dy(m+k)
         double acc = 0.0;
 #pragma unroll
         for (int k = 0; k <= M; ++k) acc = fma((double)sb[(t + k) * RS + k], (double)sdy[t + k], acc);
@@ -122,7 +145,7 @@ __global__ void __launch_bounds__(FIR_TS) tv_fir_bwd_kernel(const T* __restrict_
 #pragma unroll
         for (int k = 0; k <= M; ++k) sg[t * K + k] = (T)(dyn * (double)su[M + t - k]);
     }
-    if (n0 == 0 && t < M) {                         // du(-1-t) (the zi entries): sum_{k > t} b_k(k-1-t) dy(k-1-t)
+    if (!skew && n0 == 0 && t < M) {               // du(-1-t) (the zi entries): sum_{k > t} b_k(k-1-t) dy(k-1-t)
         double acc = 0.0;
 #pragma unroll
         for (int k = 1; k <= M; ++k)
@@ -137,7 +160,7 @@ __global__ void __launch_bounds__(FIR_TS) tv_fir_bwd_kernel(const T* __restrict_
 }
 
 template <typename T, int M>
-static iir_status_t fir_run(bool fwd, const iir_desc_t* d, const void* b, const void* u, const void* zi,
+static iir_status_t fir_run(bool fwd, int skew, const iir_desc_t* d, const void* b, const void* u, const void* zi,
                             const void* gy, void* y, void* du, void* duneg, void* gb, cudaStream_t st) {
     const int64_t ntile = (d->length + FIR_TS - 1) / FIR_TS;
     const unsigned grid = (unsigned)(d->batch * ntile);
@@ -149,11 +172,11 @@ static iir_status_t fir_run(bool fwd, const iir_desc_t* d, const void* b, const 
     return launch(K_TV_FIR, st, [&] {
         if (fwd)
             tv_fir_fwd_kernel<T, M><<<grid, FIR_TS, fir_fwd_smem<T, M>(), st>>>(static_cast<const T*>(b),
-                static_cast<const T*>(u), static_cast<const T*>(zi), static_cast<T*>(y), d->length, ntile);
+                static_cast<const T*>(u), static_cast<const T*>(zi), static_cast<T*>(y), d->length, ntile, skew);
         else
             tv_fir_bwd_kernel<T, M><<<grid, FIR_TS, fir_bwd_smem<T, M>(), st>>>(static_cast<const T*>(b),
                 static_cast<const T*>(u), static_cast<const T*>(zi), static_cast<const T*>(gy), static_cast<T*>(du),
-                static_cast<T*>(duneg), static_cast<T*>(gb), d->length, ntile);
+                static_cast<T*>(duneg), static_cast<T*>(gb), d->length, ntile, skew);
     });
 }
 template <typename T>
@@ -246,8 +269,10 @@ iir_status_t tv_order(int op, const iir_desc_t* d, const Layout& L, TvArgs& a, c
     switch (op) {
         case 0: return tv_fwd_m<T, M>(L, a, st);
         case 1: return tv_bwd_m<T, M>(L, a, st);
-        case 2: return fir_run<T, M>(true, d, b, u, zi, gy, y, du, duneg, gb, st);
-        default: return fir_run<T, M>(false, d, b, u, zi, gy, y, du, duneg, gb, st);
+        case 2: return fir_run<T, M>(true, 0, d, b, u, zi, gy, y, du, duneg, gb, st);
+        case 3: return fir_run<T, M>(false, 0, d, b, u, zi, gy, y, du, duneg, gb, st);
+        case 4: return fir_run<T, M>(true, 1, d, b, u, zi, gy, y, du, duneg, gb, st);    // skewed rows (TDF)
+        default: return fir_run<T, M>(false, 1, d, b, u, zi, gy, y, du, duneg, gb, st);
     }
 }
 

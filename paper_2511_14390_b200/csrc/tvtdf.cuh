@@ -4,13 +4,14 @@
 // Unrolled, y(n) = sum_k b_k(n-k) x(n-k) - sum_i a_i(n-i) y(n-i) + zi[n] (n < M): the
 // zeros-then-poles (DF-I) structure on SKEWED coefficient rows
 //     b~_k(n) = b_k(n - k),   a~_i(n) = a_i(n - i)      (zero before n = 0),
-// so the path reuses the per-sample kernels of the DF filter: the FIR stage (tv_fir, rows
-// b~, zero history) gives f, zi is added to f(0..M-1), and the all-pole recursion (rows a~,
+// so the path reuses the per-sample kernels of the DF filter: the FIR stage (tv_fir on the
+// skewed rows b~, read in place from b; zero history) gives f, zi is added to f(0..M-1), and the all-pole recursion (rows a~,
 // zero history) gives y.  zf = v(N) is the tail sum
 //     zf_i = zi_{i+N} + sum_{d=0}^{min(N-1, M-i)} [b_{i+d}(m) x(m) - a_{i+d}(m) y(m)],  m = N-1-d.
 // Backward: the all-pole adjoint on rows a~ (input grad_y plus the zf tail terms) gives
-// g = dL/df and grad_a~; the FIR adjoint on rows b~ gives grad_x and grad_b~; the skew is
-// undone (grad_a_i(m) = grad_a~_i(m + i)) and the zf tail terms are added.
+// g = dL/df and grad_a~; the FIR adjoint on rows b~ gives grad_x and grad_b (= grad_b~ at the
+// skewed rows, written unskewed); the skew of a is undone (grad_a_i(m) = grad_a~_i(m + i)) and
+// the zf tail terms are added.
 #pragma once
 #include "common.cuh"
 
@@ -21,74 +22,73 @@ constexpr int NT = 256;
 
 constexpr int SR = 128;    // rows (samples) per block of the skew kernels
 
-// a~ (B, N, M) and b~ (B, N, M+1) from a, b.  Block (tile, sequence): rows [n0, n0 + SR) of
-// the output need input rows [n0 - M, n0 + SR); both are staged through shared memory so
-// every global access is a contiguous run of rows.
+// dst[q] = src[q] for q in [q_lo, q_hi), zero elsewhere, q in [0, cnt): a block's contiguous run of
+// rows staged into shared memory, four independent loads in flight per thread (the runs are read
+// once: streaming hint)
 template <typename T>
-__global__ void __launch_bounds__(NT) skew_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ as,
-                                                  T* __restrict__ bs, int64_t N, int M) {
-    extern __shared__ __align__(16) unsigned char skew_raw[];
-    T* sb = reinterpret_cast<T*>(skew_raw);                 // (SR + M) x K
-    T* sa = sb + (SR + M) * (M + 1);                         // (SR + M) x M
-    const int K = M + 1;
-    const int64_t s = blockIdx.y, n0 = (int64_t)blockIdx.x * SR;
-    const int64_t lo = n0 - M;                               // first staged input row
-    const int rows = (int)min((int64_t)SR + M, N - lo);
-    for (int e = threadIdx.x; e < (SR + M) * K; e += NT) {
-        const int r = e / K;
-        const int64_t n = lo + r;
-        sb[e] = (r < rows && n >= 0) ? b[(s * N + n) * K + (e - r * K)] : T(0);
+__device__ __forceinline__ void stage_rows(T* __restrict__ dst, const T* __restrict__ src, int64_t base, int cnt,
+                                           int q_lo, int q_hi) {
+    int q = threadIdx.x;
+    for (; q + 3 * NT < cnt; q += 4 * NT) {
+        T v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = q + u * NT;
+            v[u] = (e >= q_lo && e < q_hi) ? __ldcs(src + base + e) : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dst[q + u * NT] = v[u];
     }
-    for (int e = threadIdx.x; e < (SR + M) * M; e += NT) {
-        const int r = e / M;
-        const int64_t n = lo + r;
-        sa[e] = (r < rows && n >= 0) ? a[(s * N + n) * M + (e - r * M)] : T(0);
-    }
-    __syncthreads();
-    const int nout = (int)min((int64_t)SR, N - n0);
-    for (int e = threadIdx.x; e < nout * K; e += NT) {       // b~_k(n) = b_k(n - k)
-        const int r = e / K, k = e - r * K;
-        bs[(s * N + n0) * K + e] = sb[(r + M - k) * K + k];
-    }
-    for (int e = threadIdx.x; e < nout * M; e += NT) {       // a~_i(n) = a_i(n - i)
-        const int r = e / M, i = e - r * M + 1;
-        as[(s * N + n0) * M + e] = sa[(r + M - i) * M + i - 1];
+    for (; q < cnt; q += NT) dst[q] = (q >= q_lo && q < q_hi) ? __ldcs(src + base + q) : T(0);
+}
+
+// out[e] = s[e + off(c)], c = e mod W, for e in [0, cnt) (the column index c advanced
+// incrementally: no division in the loop)
+template <typename T, typename Off>
+__device__ __forceinline__ void emit_rows(T* __restrict__ out, const T* __restrict__ s, int cnt, int W, Off off) {
+    const int st = NT % W;
+    int c = threadIdx.x % W;
+    for (int e = threadIdx.x; e < cnt; e += NT) {
+        __stcs(out + e, s[e + off(c)]);
+        c += st;
+        if (c >= W) c -= W;
     }
 }
-template <typename T>
-constexpr size_t skew_smem(int M) { return (size_t)(SR + M) * (2 * M + 1) * sizeof(T); }
 
-// grad_a, grad_b from the gradients of the skewed rows: g_k(m) = g~_k(m + k) (zero past N);
+// a~ (B, N, M) from a.  Block (tile, sequence): rows [n0, n0 + SR) of the output need input
+// rows [n0 - M, n0 + SR); they are staged through shared memory so every global access is a
+// contiguous run of rows.  (b~ is never materialised: the FIR stage reads b at skewed rows,
+// tv_impl.cuh.)
+template <typename T>
+__global__ void __launch_bounds__(NT) skew_kernel(const T* __restrict__ a, T* __restrict__ as, int64_t N, int M) {
+    extern __shared__ __align__(16) unsigned char skew_raw[];
+    T* sa = reinterpret_cast<T*>(skew_raw);                 // (SR + M) x M
+    const int64_t s = blockIdx.y, n0 = (int64_t)blockIdx.x * SR;
+    const int64_t lo = n0 - M;                               // first staged input row
+    const int rows = (int)min((int64_t)SR + M, N - lo);      // staged rows inside the sequence
+    const int r0 = lo < 0 ? (int)-lo : 0;                    // staged rows before n = 0 (zero)
+    stage_rows(sa, a, (s * N + lo) * M, (SR + M) * M, r0 * M, rows * M);
+    __syncthreads();
+    const int nout = (int)min((int64_t)SR, N - n0);
+    // a~_i(n) = a_i(n - i), column c = i - 1: staged row r + M - i  ->  offset (M - 1 - c) M
+    emit_rows(as + (s * N + n0) * M, sa, nout * M, M, [=](int c) { return (M - 1 - c) * M; });
+}
+template <typename T>
+constexpr size_t skew_smem(int M) { return (size_t)(SR + M) * M * sizeof(T); }
+
+// grad_a from the gradient of the skewed rows: g_i(m) = g~_i(m + i) (zero past N);
 // block (tile, sequence) stages input rows [m0, m0 + SR + M)
 template <typename T>
-__global__ void __launch_bounds__(NT) unskew_kernel(const T* __restrict__ gas, const T* __restrict__ gbs,
-                                                    T* __restrict__ ga, T* __restrict__ gb, int64_t N, int M) {
+__global__ void __launch_bounds__(NT) unskew_kernel(const T* __restrict__ gas, T* __restrict__ ga, int64_t N, int M) {
     extern __shared__ __align__(16) unsigned char skew_raw[];
-    T* sb = reinterpret_cast<T*>(skew_raw);
-    T* sa = sb + (SR + M) * (M + 1);
-    const int K = M + 1;
+    T* sa = reinterpret_cast<T*>(skew_raw);
     const int64_t s = blockIdx.y, m0 = (int64_t)blockIdx.x * SR;
     const int rows = (int)min((int64_t)SR + M, N - m0);
-    for (int e = threadIdx.x; e < (SR + M) * K; e += NT) {
-        const int r = e / K;
-        sb[e] = r < rows ? gbs[(s * N + m0 + r) * K + (e - r * K)] : T(0);
-    }
-    for (int e = threadIdx.x; e < (SR + M) * M; e += NT) {
-        const int r = e / M;
-        sa[e] = r < rows ? gas[(s * N + m0 + r) * M + (e - r * M)] : T(0);
-    }
-    __syncthreads();
     const int nout = (int)min((int64_t)SR, N - m0);
-    if (gb != nullptr)
-        for (int e = threadIdx.x; e < nout * K; e += NT) {
-            const int r = e / K, k = e - r * K;
-            gb[(s * N + m0) * K + e] = sb[(r + k) * K + k];
-        }
-    if (ga != nullptr)
-        for (int e = threadIdx.x; e < nout * M; e += NT) {
-            const int r = e / M, i = e - r * M + 1;
-            ga[(s * N + m0) * M + e] = sa[(r + i) * M + i - 1];
-        }
+    stage_rows(sa, gas, (s * N + m0) * M, (SR + M) * M, 0, rows * M);
+    __syncthreads();
+    // column c = i - 1: staged row r + i  ->  offset (c + 1) M
+    emit_rows(ga + (s * N + m0) * M, sa, nout * M, M, [=](int c) { return (c + 1) * M; });
 }
 
 // f(n) += zi[n], n < min(M, N); one thread per (sequence, n)
