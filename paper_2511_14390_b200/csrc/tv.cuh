@@ -581,8 +581,16 @@ __global__ void __launch_bounds__(32 * TV_SEQ_WARPS) tv_seq_kernel(const TvArgs 
                     if constexpr (MODE == TV_BWD_EMIT) {
                         const T gT = (T)g;
                         if (gxrow) gxrow[n] = gT;
+                        if constexpr (sizeof(T) == 4 && M % 4 == 0) {   // 16 B stores (rows 16 B aligned)
 #pragma unroll
-                        for (int i = 0; i < M; ++i) myG[s2 * M + i] = -gT * yw[i];
+                            for (int q = 0; q < M / 4; ++q)
+                                reinterpret_cast<float4*>(myG + s2 * M)[q] =
+                                    make_float4(-gT * yw[4 * q], -gT * yw[4 * q + 1], -gT * yw[4 * q + 2],
+                                                -gT * yw[4 * q + 3]);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < M; ++i) myG[s2 * M + i] = -gT * yw[i];
+                        }
 #pragma unroll
                         for (int i = 0; i < M - 1; ++i) yw[i] = yw[i + 1];
                         yw[M - 1] = py[slot][u];
