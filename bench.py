@@ -57,6 +57,9 @@ WORKLOADS = {
     "f3": dict(desc="SURVEY 8(f) f3: Diag-EXT bare recurrence (eigen-basis element-wise complex scans), f1's shape: "
                     "M = 2, batch 16 x 2^20, fp32", diag=True, **dict(inputs.CONFIGS["f1"], batch=16)),
     # PAPER.md:167 "we expect the gap [Diag-EXT vs EXT] to disappear as M increases": the same pair at M = 4
+    # the DF-II form of config 5 (round-1 engine; u re-run in the backward from the tape's chunk states)
+    "c5df": dict(desc="config 5 per-GPU shard in DF-II form: order-8 DF shared coefficients, batch 256 x 2^16, fp32",
+                 **dict(inputs.CONFIGS["c5"], batch=256, form="df")),
     "f1m4": dict(desc="SURVEY 8(f) f1 at M = 4: dense bare recurrence, batch 16 x 2^20, fp32",
                  **dict(inputs.CONFIGS["f1"], batch=16, order=4)),
     "f3m4": dict(desc="SURVEY 8(f) f3 at M = 4: Diag-EXT bare recurrence, batch 16 x 2^20, fp32", diag=True,
@@ -88,16 +91,16 @@ def algorithmic_bytes(w):
         if w.get("fir") and w["form"] == "tdf":   # TDF: skew of a / unskew of grad_a~ (design overhead;
             d["tv_skew"] = 4 * M * s             # b is read at skewed rows in place): read + write each
         return d
-    # HBM bytes per kernel the method must move: fwd reads x, writes y (+u for DF);
-    # bwd reads dy, x, y (TDF) or dy, u (DF) and writes dx: 24 B/sample in fp32
+    # HBM bytes per kernel the method must move: fwd reads x, writes y; bwd reads dy, x, y (TDF:
+    # 24 B/sample in fp32) or dy, x (DF: u re-run from the tape's chunk states, 20 B/sample) and writes dx
     if w["form"] == "tdf":
         return dict(lti_fwd=2 * s, lti_bwd=4 * s)
-    return dict(lti_fwd=3 * s, lti_bwd=3 * s)
+    return dict(lti_fwd=2 * s, lti_bwd=3 * s)
 
 
 def step_min_bytes(w):
     """HBM bytes per sample any fwd+bwd implementation must move:
-    LTI TDF x, y, dy, dx (+x, y re-read by the backward); TV all-pole x, y, dy, dx,
+    LTI TDF x, y, dy, dx (+x, y re-read by the backward; DF +x only); TV all-pole x, y, dy, dx,
     a read by each direction and grad_a written: (3M + 5) elements."""
     s = 8 if w["dtype"] == "f64" else 4
     if w["form"] == "ss":
@@ -105,7 +108,7 @@ def step_min_bytes(w):
     if w["coef"] == "per_sample":
         # + per-sample b read by each direction and grad_b written (general DF)
         return (3 * w["order"] + 5 + (3 * (w["order"] + 1) if w.get("fir") else 0)) * s
-    return 6 * s
+    return (6 if w["form"] == "tdf" else 5) * s     # DF: x, y, dy, x, dx (u is not stored)
 
 
 def peaks():

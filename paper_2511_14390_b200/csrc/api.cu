@@ -119,6 +119,13 @@ static bool v2_capable(const iir_desc_t* d) {
            (d->coef_mode == IIR_COEF_SHARED || d->coef_mode == IIR_COEF_PER_SEQ) && d->order >= 1 && d->order <= 8 &&
            !(d->flags & IIR_FLAG_LEGACY_LTI);
 }
+// Chunk<T, M>::L of the round-1 engine (samples per thread chunk): the DF tape's state grid
+static int64_t df_chunk_len(const iir_desc_t* d) {
+    return (d->dtype == IIR_F64 ? 16 : 32) * (d->order >= IIRG_LONG_CHUNK_M ? 2 : 1);
+}
+static_assert(Chunk<float, 1>::L == 32 && Chunk<double, 1>::L == 16, "df_chunk_len");
+static_assert(Chunk<float, IIRG_LONG_CHUNK_M>::L == 64 && Chunk<double, IIRG_LONG_CHUNK_M>::L == 32, "df_chunk_len");
+
 static bool use_v2(const iir_desc_t* d) {
     if (!v2_capable(d)) return false;
     if (d->flags & IIR_FLAG_ENGINE_V2) return true;
@@ -231,8 +238,11 @@ static Layout layout(const iir_desc_t* d) {
         return L;
     }
     L.tp_tab = o; o += al256((size_t)L.ncoef * tab_size(M) * 8);
-    L.tp_u = o;
-    if (d->form == IIR_DF2) o += al256((size_t)d->batch * d->length * dsize(d->dtype));
+    L.tp_u = o;                                            // DF: the state entering every chunk
+    if (d->form == IIR_DF2) {                              // (B, ceil(T / L), M): M values per L samples
+        const int64_t Lc = df_chunk_len(d);
+        o += al256((size_t)d->batch * ((d->length + Lc - 1) / Lc) * d->order * dsize(d->dtype));
+    }
     L.tp_bytes = o;
     return L;
 }
@@ -331,7 +341,7 @@ iir_status_t iir_forward(const iir_desc_t* d, const void* b, const void* a, cons
     }
     const int W = d->dtype == IIR_F64 ? 2 : 4;
     const int64_t rowlen = d->length * (d->form == IIR_SS ? d->order : 1);
-    const bool vec = (rowlen % W == 0) && aligned16(x) && aligned16(y) && aligned16(t + L.tp_u);
+    const bool vec = (rowlen % W == 0) && aligned16(x) && aligned16(y);
     if (d->coef_mode == IIR_COEF_PER_SAMPLE) return tv_forward(d, L, b, a, x, zi, y, zf, t, w, vec, st);
     if (L.v2) {
         v2::Call c{};
@@ -389,6 +399,8 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     if (ws == nullptr || ws_bytes < L.ws_bytes) return fail(IIR_EWORKSPACE, "workspace missing or too small");
     if (d->coef_mode != IIR_COEF_PER_SAMPLE && d->form == IIR_TDF2 && (x == nullptr || y == nullptr))
         return fail(IIR_EINVAL, "TDF backward needs the forward's x and y");
+    if (d->coef_mode != IIR_COEF_PER_SAMPLE && d->form == IIR_DF2 && x == nullptr)
+        return fail(IIR_EINVAL, "DF backward needs the forward's x (u is re-run from the tape's chunk states)");
     if (d->form == IIR_SS && (a == nullptr || y == nullptr))
         return fail(IIR_EINVAL, "bare-recurrence backward needs A and the forward's v");
     if (d->form == IIR_SS && grad_b != nullptr) return fail(IIR_EINVAL, "bare recurrence: grad_b must be NULL");
@@ -410,7 +422,7 @@ iir_status_t iir_backward(const iir_desc_t* d, const void* grad_y, const void* g
     const int W = d->dtype == IIR_F64 ? 2 : 4;
     const int64_t rowlen = d->length * (d->form == IIR_SS ? d->order : 1);
     const bool vec = (rowlen % W == 0) && aligned16(grad_y) && aligned16(x) && aligned16(y) &&
-                     aligned16(grad_x) && aligned16(t + L.tp_u);
+                     aligned16(grad_x);
     if (d->coef_mode == IIR_COEF_PER_SAMPLE)
         return tv_backward(d, L, grad_y, grad_zf, b, a, y, zi, t, grad_x, grad_b, grad_a, grad_zi, w, vec, st, x);
     if (L.v2) {

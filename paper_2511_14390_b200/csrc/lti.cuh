@@ -451,7 +451,7 @@ struct CarryWs {
 
 struct LtiFwdArgs {
     const void* b; const void* a; int64_t coef_stride;           // raw coefficients (local pass)
-    const void* x; const void* zi; void* y; void* zf; void* u;    // u: DF tape signal
+    const void* x; const void* zi; void* y; void* zf; void* u;    // u: DF tape, chunk-entry states
     const double* tab; int64_t tab_stride;                        // 0 for SHARED
     CarryWs cw;
     int64_t B, Tlen; int ntiles; int vec;
@@ -781,7 +781,7 @@ struct Smem {
     static constexpr int PT = pidx<T>(TS);               // one padded tile
     static constexpr int PTH = pidx<T>(TS + HALO);       // padded tile with u history
     static constexpr size_t tab_bytes = ((size_t)Tab<M>::STAGE * 8 + 15) / 16 * 16;
-    static constexpr size_t fwd(int form) { return tab_bytes + (size_t)(PT + (form == 0 ? PT : 0)) * sizeof(T); }
+    static constexpr size_t fwd(int) { return tab_bytes + (size_t)PT * sizeof(T); }
     static constexpr size_t bwd_tdf() { return tab_bytes + (size_t)PT * sizeof(T); }
     static constexpr size_t bwd(int form) {
         return tab_bytes + (size_t)(PT + PTH + (form == 1 ? PT : 0)) * sizeof(T);
@@ -811,7 +811,6 @@ __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double* st = reinterpret_cast<double*>(smem_raw);
     T* xs = reinterpret_cast<T*>(smem_raw + SM::tab_bytes);     // x -> y in place
-    T* us = xs + SM::PT;                                          // DF: u tile
     __shared__ double s_agg[NW][M];
     __shared__ double s_xw[NW][M];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -913,6 +912,17 @@ __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const 
     T vin[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) { vin[i] = (T)E[i]; v[i] = vin[i]; }
+    if constexpr (FORM == 0) {
+        // DF: the tape keeps the state entering every chunk, [u(n-1) .. u(n-M)] at n = the
+        // chunk's first sample (M values per L samples), not the signal u itself: the
+        // backward re-runs the recursion from it (df_regen_u) -- the same fwd_step from the
+        // same T state, so the regenerated u is bit-identical to the one emitted here.
+        if (p0 + s0 < p.Tlen) {
+            T* ust = static_cast<T*>(p.u) + (seq * ((p.Tlen + L - 1) / L) + (p0 + s0) / L) * M;
+#pragma unroll
+            for (int i = 0; i < M; ++i) ust[i] = vin[i];
+        }
+    }
     // zf = v(T): the thread holding sample T-1 walks its chunk up to it (before
     // the emit pass overwrites x with y).
     if (p.zf != nullptr) {
@@ -927,7 +937,7 @@ __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const 
             for (int i = 0; i < M; ++i) zf[i] = w2[i];
         }
     }
-    // a4: re-run from the exact carry-in, emit y (and u for DF) in place.
+    // a4: re-run from the exact carry-in, emit y in place.
     if constexpr (use_tdf2<T, FORM>()) {
         Tdf2<M> c2;
         c2.init(bc, ac);
@@ -944,54 +954,92 @@ __global__ void __launch_bounds__(NT, fwd_min_blocks<M>()) lti_fwd_kernel(const 
 #pragma unroll
         for (int g = 0; g < L / W; ++g) {
             V xv = *reinterpret_cast<const V*>(xs + pidx<T>(s0 + g * W));
-            V uv;
 #pragma unroll
             for (int e = 0; e < W; ++e) {
                 T uu;
-                const T yy = fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, uu);
-                vset(xv, e, yy);
-                vset(uv, e, uu);
+                vset(xv, e, fwd_step<T, M, FORM>(v, vget(xv, e), bc, ac, uu));
             }
             *reinterpret_cast<V*>(xs + pidx<T>(s0 + g * W)) = xv;
-            if constexpr (FORM == 0) *reinterpret_cast<V*>(us + pidx<T>(s0 + g * W)) = uv;
         }
     }
     __syncthreads();
     IIRG_TRACE(p.trace, tk, 4);
     T* yrow = static_cast<T*>(p.y) + seq * p.Tlen;
     tile_store<T, TS>(yrow, xs, p0, p.Tlen, p.vec);
-    if constexpr (FORM == 0) {
-        T* urow = static_cast<T*>(p.u) + seq * p.Tlen;
-        tile_store<T, TS>(urow, us, p0, p.Tlen, p.vec);
-    }
     IIRG_TRACE(p.trace, tk, 5);
     cta_exit(cw, ep, gridDim.x);
     span_exit(p.span);
 }
 
-template <typename T, int M, int FORM>
-__device__ __forceinline__ void bwd_load_u(const LtiBwdArgs& p, int64_t seq, int64_t p0, T* s2) {
+// DF backward: x(p0 .. p0 + TS) -> s2[pidx(e + HALO)] (the slots of u, regenerated in place by
+// df_regen_u; samples before n = 0 are never read from x).
+template <typename T, int M>
+__device__ __forceinline__ void bwd_load_x_df(const LtiBwdArgs& p, int64_t seq, int64_t p0, T* s2) {
     constexpr int TS = NT * Chunk<T, M>::L, W = Vec<T>::W;
     using V = typename Vec<T>::type;
-    // u(p0 - HALO .. p0 + TS) -> s2[pidx(e + HALO)]; u(-k) = zi[k-1] (DF state).
-    const T* urow = static_cast<const T*>(p.u) + seq * p.Tlen;
-    const T* zi = static_cast<const T*>(p.zi);
-    for (int q = threadIdx.x; q < (TS + HALO) / W; q += NT) {
-        const int e = q * W - HALO;
+    const T* xrow = static_cast<const T*>(p.x) + seq * p.Tlen;
+    for (int q = threadIdx.x; q < TS / W; q += NT) {
+        const int e = q * W;
         const int64_t pos = p0 + e;
-        if (p.vec && pos >= 0 && pos + W <= p.Tlen) {
-            cp_async16(s2 + pidx<T>(e + HALO), urow + pos, 16u);
+        if (pos < 0 && pos + W <= 0) continue;
+        if (p.vec && pos >= 0) {
+            cp_async16(s2 + pidx<T>(e + HALO), xrow + pos, 16u);
         } else {
             V val;
 #pragma unroll
-            for (int r = 0; r < W; ++r) {
-                const int64_t pr = pos + r;
-                T s = T(0);
-                if (pr >= 0 && pr < p.Tlen) s = urow[pr];
-                else if (pr < 0 && pr >= -M && zi != nullptr) s = zi[seq * M + (-pr - 1)];
-                vset(val, r, s);
-            }
+            for (int r = 0; r < W; ++r) vset(val, r, pos + r >= 0 ? xrow[pos + r] : T(0));
             *reinterpret_cast<V*>(s2 + pidx<T>(e + HALO)) = val;
+        }
+    }
+}
+
+// DF backward: u(n) for this thread's chunk [p0 + s0, p0 + s0 + L) re-run from the chunk-entry
+// state the forward saved (Eqs.2-3: u = x - sum a_k u(n-k)), written over x in s2; u(-k) =
+// zi[k-1], zero beyond.  The tile's first chunk also writes the tile's u history u(n-1 .. n-M)
+// (the state itself).  A chunk that does not start on the forward's chunk grid (backward tiles
+// are aligned to the sequence end) first walks from the grid point before it on x read from
+// global memory (fewer than L samples; none when L divides T).
+template <typename T, int M>
+__device__ __forceinline__ void df_regen_u(const LtiBwdArgs& p, int64_t seq, int64_t p0, int s0, T* s2,
+                                           const T (&bc)[M + 1], const T (&ac)[M + 1]) {
+    constexpr int L = Chunk<T, M>::L, W = Vec<T>::W;
+    using V = typename Vec<T>::type;
+    const T* xrow = static_cast<const T*>(p.x) + seq * p.Tlen;
+    const T* zi = static_cast<const T*>(p.zi);
+    const int64_t ns = p0 + s0, hi = ns + L;                 // the chunk [ns, hi)
+    for (int64_t n = ns - (s0 == 0 ? HALO : 0); n < min(hi, (int64_t)0); ++n)
+        s2[pidx<T>((int)(n - p0) + HALO)] = (n >= -M && zi != nullptr) ? zi[seq * M + (-n - 1)] : T(0);
+    if (hi <= 0) return;
+    const int64_t first = max(ns, (int64_t)0);
+    const int64_t g = first / L * L;                         // forward chunk grid point <= first
+    const T* ust = static_cast<const T*>(p.u) + (seq * ((p.Tlen + L - 1) / L) + g / L) * M;
+    T v[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) v[i] = ust[i];
+    T uu;
+#pragma unroll 8
+    for (int64_t n = g; n < first; ++n) (void)fwd_step<T, M, 0>(v, __ldg(xrow + n), bc, ac, uu);
+    if (s0 == 0 && ns > 0) {                                 // the tile's history u(ns-1 .. ns-M)
+#pragma unroll
+        for (int k = 1; k <= M; ++k) s2[pidx<T>(HALO - k)] = v[k - 1];
+    }
+    if (first == ns) {                                       // the whole chunk, W-wide groups
+#pragma unroll
+        for (int q = 0; q < L / W; ++q) {
+            V* slot = reinterpret_cast<V*>(s2 + pidx<T>(s0 + HALO + q * W));
+            V xv = *slot;
+#pragma unroll
+            for (int e = 0; e < W; ++e) {
+                (void)fwd_step<T, M, 0>(v, vget(xv, e), bc, ac, uu);
+                vset(xv, e, uu);
+            }
+            *slot = xv;
+        }
+    } else {                                                 // the chunk holding n = 0 (first tile)
+        for (int64_t n = first; n < hi; ++n) {
+            T* slot = s2 + pidx<T>((int)(n - p0) + HALO);
+            (void)fwd_step<T, M, 0>(v, *slot, bc, ac, uu);
+            *slot = uu;
         }
     }
 }
@@ -1173,7 +1221,7 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
         tile_load_async<T, TS>(s2, static_cast<const T*>(p.x) + roff, p0, p.Tlen, p.vec);
         tile_load_async<T, TS>(s3, static_cast<const T*>(p.y) + roff, p0, p.Tlen, p.vec);
     } else {
-        bwd_load_u<T, M, FORM>(p, seq, p0, s2);
+        bwd_load_x_df<T, M>(p, seq, p0, s2);
     }
     cp_async_commit();
     rearm_other_bank(cw, ep, blockIdx.x, gridDim.x);
@@ -1199,7 +1247,7 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
     }
     IIRG_TRACE(p.trace, tk, 1);
     // a6: carries (transposed powers), tiles last -> first.
-    cp_async_wait<1>();                              // power tables
+    cp_async_wait<FORM == 0 ? 0 : 1>();              // power tables (DF: and x)
     __syncthreads();
     double S[M];
 #pragma unroll
@@ -1230,6 +1278,10 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
 #pragma unroll
             for (int i = 0; i < M; ++i) s_xw[lane][i] = xw[i];
         }
+    } else if constexpr (FORM == 0) {
+        // DF: while warp 0 looks back, the other warps re-run u over the tile (x -> u in place)
+        static_assert(NT > 32, "warps 1.. re-run u");
+        for (int c = tid - 32; c < NT; c += NT - 32) df_regen_u<T, M>(p, seq, p0, c * L, s2, bc, ac);
     }
     __syncthreads();
     {
@@ -1241,7 +1293,7 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
     T din[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) { din[i] = (T)E[i]; d[i] = din[i]; }
-    cp_async_wait<0>();                              // x, y / u
+    cp_async_wait<0>();                              // x, y (TDF)
     __syncthreads();
 
     // grad_zi = dz(-1) (Eq.9, A.3): the thread whose chunk holds n = 0 walks down
