@@ -1335,6 +1335,17 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
                 adj_tdf_step<T, M>(d, dy, ac);
             }
         } else {
+            // u(n - k), k = 0..M, of the group's W samples: one window of vector loads
+            // u(s0 + gW - MW .. s0 + gW + W - 1) (MW = M rounded up to W <= HALO)
+            constexpr int MW = (M + W - 1) / W * W;
+            static_assert(MW <= HALO, "u history window inside the halo");
+            T uw[MW + W];
+#pragma unroll
+            for (int q = 0; q < (MW + W) / W; ++q) {
+                const V t = *reinterpret_cast<const V*>(s2 + pidx<T>(s0 + g * W + HALO - MW + q * W));
+#pragma unroll
+                for (int r = 0; r < W; ++r) uw[q * W + r] = vget(t, r);
+            }
 #pragma unroll
             for (int e = W - 1; e >= 0; --e) {
                 const int n = s0 + g * W + e;                 // tile-local time index
@@ -1343,7 +1354,7 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
                 const T gmask = (!has_neg || p0 + n >= 0) ? dx : T(0);
 #pragma unroll
                 for (int k = 0; k <= M; ++k) {
-                    const T uk = s2[pidx<T>(n - k + HALO)];
+                    const T uk = uw[MW + e - k];
                     Gs[k] = fma(dy, uk, Gs[k]);                          // Gb[k] = sum dy u(n-k)
                     if (k >= 1) Gs[M + k] = fma(gmask, uk, Gs[M + k]);  // Ga[k] = sum dx u(n-k)
                 }
