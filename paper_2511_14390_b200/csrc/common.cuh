@@ -14,6 +14,9 @@ constexpr int NW = NT / 32;      // warps per CTA
 constexpr int LOG_NW = NW == 2 ? 1 : NW == 4 ? 2 : NW == 8 ? 3 : NW == 16 ? 4 : 5;
 
 constexpr int HALO = 8;          // u-history halo of the DF backward tile (>= M)
+#ifndef IIRG_DF_GU
+#define IIRG_DF_GU 2                 // unroll of the DF backward's per-chunk group loops (I-cache)
+#endif
 
 // Samples per thread chunk (L) by data type; a tile is NT * L samples.
 // High orders use twice the chunk length: the fp64 carry scans cost M^2 per

@@ -1023,8 +1023,9 @@ __device__ __forceinline__ void df_regen_u(const LtiBwdArgs& p, int64_t seq, int
 #pragma unroll
         for (int k = 1; k <= M; ++k) s2[pidx<T>(HALO - k)] = v[k - 1];
     }
+    constexpr int RU = IIRG_DF_GU;
     if (first == ns) {                                       // the whole chunk, W-wide groups
-#pragma unroll
+#pragma unroll RU
         for (int q = 0; q < L / W; ++q) {
             V* slot = reinterpret_cast<V*>(s2 + pidx<T>(s0 + HALO + q * W));
             V xv = *slot;
@@ -1232,11 +1233,14 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
 
     const int c = NT - 1 - tid;          // chunk index within the tile (time order)
     const int s0 = c * L;
+    // DF: the fully unrolled chunk loops overflow the instruction cache at M = 8 (ncu: 40 % of
+    // stalls "no_instructions"); the group loops are unrolled by IIRG_DF_GU only
+    constexpr int GU = FORM == 0 ? IIRG_DF_GU : L / W;
     // a5: local adjoint pass from the zero state, walking the chunk backwards.
     T d[M];
 #pragma unroll
     for (int i = 0; i < M; ++i) d[i] = T(0);
-#pragma unroll
+#pragma unroll GU
     for (int g = L / W - 1; g >= 0; --g) {
         const V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
 #pragma unroll
@@ -1316,7 +1320,7 @@ __global__ void __launch_bounds__(NT, bwd_min_blocks<M>()) lti_bwd_kernel(const 
 #pragma unroll
     for (int k = 0; k < NG; ++k) Gs[k] = T(0);
     const bool has_neg = (p0 + s0) < 0;                 // chunk reaches before n = 0
-#pragma unroll
+#pragma unroll GU
     for (int g = L / W - 1; g >= 0; --g) {
         V dv = *reinterpret_cast<const V*>(dys + pidx<T>(s0 + g * W));
         if constexpr (FORM == 1) {
