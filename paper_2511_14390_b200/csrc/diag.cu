@@ -445,19 +445,32 @@ __global__ void __launch_bounds__(32) dg_scan_kernel(const Args p) {
                 X[2 * i + 1] += q1 * (double)v0[j];
             }
     }
+    // the transition powers X^(C 2^d), d = 0..4, staged once in shared memory (read by broadcast
+    // in every block of the serial scan), and the next block's aggregates loaded one block
+    // ahead: the loop's only serial dependency is the carry X
+    constexpr int NPW = 5 * 2 * M * M;
+    __shared__ double spw[NPW];
+    for (int e = lane; e < NPW; e += 32) spw[e] = t[TB::PW + e];
+    __syncwarp();
+    double Sn[2 * M];
+#pragma unroll
+    for (int i = 0; i < 2 * M; ++i) Sn[i] = lane < p.nch ? p.agg[(seq * p.nch + lane) * 2 * M + i] : 0.0;
     for (int b0 = 0; b0 < p.nch; b0 += 32) {
         const int c = b0 + lane;                                     // scan position
         const int k = c;                                             // (backward chunk indices run from the end)
         double S[2 * M];
 #pragma unroll
-        for (int i = 0; i < 2 * M; ++i) S[i] = c < p.nch ? p.agg[(seq * p.nch + k) * 2 * M + i] : 0.0;
-        if (lane == 0) cmv<M, BWD>(t + TB::PW, X, S);              // fold the block's carry-in
+        for (int i = 0; i < 2 * M; ++i) S[i] = Sn[i];
+        const int cn = c + 32;
+#pragma unroll
+        for (int i = 0; i < 2 * M; ++i) Sn[i] = cn < p.nch ? p.agg[(seq * p.nch + cn) * 2 * M + i] : 0.0;
+        if (lane == 0) cmv<M, BWD>(spw, X, S);                     // fold the block's carry-in
 #pragma unroll
         for (int d = 0; d < 5; ++d) {
             double O[2 * M], acc[2 * M];
 #pragma unroll
             for (int i = 0; i < 2 * M; ++i) { O[i] = __shfl_up_sync(0xffffffffu, S[i], 1 << d); acc[i] = 0.0; }
-            cmv<M, BWD>(t + TB::PW + d * 2 * M * M, O, acc);
+            cmv<M, BWD>(spw + d * 2 * M * M, O, acc);
             if (lane >= (1 << d))
 #pragma unroll
                 for (int i = 0; i < 2 * M; ++i) S[i] += acc[i];
