@@ -577,21 +577,29 @@ __global__ void __launch_bounds__(DG_NT) dg_bwd_emit_kernel(const Args p) {
 // grad_A: fixed-order sum of the chunk partials (SHARED: every chunk; PER_SEQ: per sequence)
 template <typename T, int M>
 __global__ void __launch_bounds__(256) dg_reduce_kernel(const Args p, T* __restrict__ gA) {
+    // block (set, entry e of grad_A): every thread sums its fixed strided rows with four
+    // independent partial sums (loads in flight), then a fixed-order tree: deterministic
     __shared__ double red[256];
     const int64_t set = blockIdx.x;
+    const int e = blockIdx.y;
     const int64_t r0 = p.ncoef > 1 ? set * p.nch : 0, nr = p.ncoef > 1 ? p.nch : p.B * p.nch;
-    for (int e = 0; e < M * M; ++e) {
-        double s = 0.0;
-        for (int64_t r = threadIdx.x; r < nr; r += 256) s += p.gpart[(r0 + r) * M * M + e];
-        red[threadIdx.x] = s;
-        __syncthreads();
-        for (int w = 128; w > 0; w >>= 1) {
-            if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) gA[set * M * M + e] = (T)red[0];
+    const double* g = p.gpart + r0 * M * M + e;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t r = threadIdx.x;
+    for (; r + 3 * 256 < nr; r += 4 * 256) {
+        s0 += g[r * M * M];
+        s1 += g[(r + 256) * M * M];
+        s2 += g[(r + 512) * M * M];
+        s3 += g[(r + 768) * M * M];
+    }
+    for (; r < nr; r += 256) s0 += g[r * M * M];
+    red[threadIdx.x] = (s0 + s1) + (s2 + s3);
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
         __syncthreads();
     }
+    if (threadIdx.x == 0) gA[set * M * M + e] = (T)red[0];
 }
 
 template <typename T, int M>
@@ -619,7 +627,7 @@ static iir_status_t run(bool fwd, const iir_desc_t* d, Args& a, void* gA, cudaSt
     s = launch(K_DIAG_BWD, st, [&] { dg_bwd_emit_kernel<T, M><<<grid, DG_NT, 0, st>>>(a); });
     if (s != IIR_OK || gA == nullptr) return s;
     return launch(K_DIAG_RED, st, [&] {
-        dg_reduce_kernel<T, M><<<(unsigned)a.ncoef, 256, 0, st>>>(a, static_cast<T*>(gA));
+        dg_reduce_kernel<T, M><<<dim3((unsigned)a.ncoef, M * M), 256, 0, st>>>(a, static_cast<T*>(gA));
     });
     (void)d;
 }
