@@ -23,7 +23,10 @@
 namespace iirg {
 namespace dg {
 
-constexpr int DG_C = 256;          // samples per thread chunk
+#ifndef IIRG_DG_C
+#define IIRG_DG_C 256
+#endif
+constexpr int DG_C = IIRG_DG_C;    // samples per thread chunk
 constexpr int DG_NT = 128;         // threads per CTA of the chunk kernels
 
 template <typename T> struct cx { T r, i; };
