@@ -604,50 +604,162 @@ __global__ void __launch_bounds__(DG_NT) dg_fwd_emit_kernel(const Args p) {
 
 // phase 3, backward: h from the carry at the chunk's end, g(n) = Re V^-T h(n); grad_z = g;
 // per-chunk partial sums of grad_A = sum g(n) v(n)^T (fixed-order reduction later);
-// the chunk holding n = 0 writes grad_v0 = A^T g(0)
+// the chunk holding n = 0 writes grad_v0 = A^T g(0).  Staged like the forward emit, walking
+// back from the chunk's end: step s holds rows [b - S, b), b = n1 - s S, of gv and of the
+// forward's v (whose row n - 1 is v(n)); the first sample of a step pairs with the last row
+// of the next step (kept pending), the chunk's first sample with v(n0 - 1) or v0.
 template <typename T, int M>
 __global__ void __launch_bounds__(DG_NT) dg_bwd_emit_kernel(const Args p) {
-    const int64_t c = (int64_t)blockIdx.x * DG_NT + threadIdx.x;
-    if (c >= p.B * p.nch) return;
-    const int64_t seq = c / p.nch;
-    const int k = (int)(c - seq * p.nch);
-    Par<T, M> P;
-    P.load(p.tab + (p.ncoef > 1 ? seq : 0) * p.tab_stride);
-    cx<T> h[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) h[i] = {(T)p.carry[c * 2 * M + 2 * i], (T)p.carry[c * 2 * M + 2 * i + 1]};
-    const int64_t n0 = max((int64_t)0, p.T - (int64_t)(k + 1) * DG_C), n1 = p.T - (int64_t)k * DG_C;
+    constexpr int DG_S = dg_s<T, M>();
+    constexpr int ROW = DG_S * M, W = 16 / (int)sizeof(T), RS = ROW + W, PPC = ROW / W;
+    static_assert(ROW % W == 0, "whole 16 B pieces per chunk step");
+    // gv, v (double-buffered) and gz staging: 5 buffers
+    static_assert(5 * DG_NT * RS * (int)sizeof(T) <= 80 * 1024, "staged buffers");
+    extern __shared__ __align__(16) unsigned char dg_raw[];
+    T* sg = reinterpret_cast<T*>(dg_raw);                  // [2][DG_NT * RS] gv rows
+    T* sv = sg + 2 * DG_NT * RS;                           // [2][DG_NT * RS] forward v rows
+    T* so = sv + 2 * DG_NT * RS;                           // [DG_NT * RS] gz rows out
+    const int64_t ntot = p.B * p.nch, cbase = (int64_t)blockIdx.x * DG_NT;
+    const int64_t c = cbase + threadIdx.x;
+    const bool valid = c < ntot;
     const T* gv = static_cast<const T*>(p.gv);
-    const T* vo = static_cast<const T*>(p.vout) + seq * p.T * M;
+    const T* vo = static_cast<const T*>(p.vout);
     const T* v0 = static_cast<const T*>(p.v0);
     T* gz = static_cast<T*>(p.gz);
+    // rows of step `step` of chunk cc: [a, b) of its sequence, the valid part [max(a, n0), b)
+    auto span = [&](int64_t cc, int step, int64_t& rowbase, int& lo) {
+        const int64_t sq = cc / p.nch;
+        const int kk = (int)(cc - sq * p.nch);
+        const int64_t n0 = max((int64_t)0, p.T - (int64_t)(kk + 1) * DG_C), n1 = p.T - (int64_t)kk * DG_C;
+        const int64_t b = n1 - (int64_t)step * DG_S, a = b - DG_S;
+        rowbase = sq * p.T + a;                            // global row of buffer row 0
+        lo = (int)min((int64_t)DG_S, max((int64_t)0, n0 - a));   // buffer rows below lo are invalid
+        if (b <= n0) lo = DG_S;
+    };
+    auto stage_one = [&](const T* src, int step, T* dst) {
+        for (int q = threadIdx.x; q < DG_NT * PPC; q += DG_NT) {
+            const int lc = q / PPC, part = q - (q / PPC) * PPC;
+            const int64_t cc = cbase + lc;
+            T* d = dst + lc * RS + part * W;
+            int64_t rb = 0;
+            int lo = DG_S;
+            if (cc < ntot && src != nullptr) span(cc, step, rb, lo);
+            const int e0 = part * W;                       // first element of the piece
+            if (lo * M <= e0 && lo < DG_S) {
+                const T* g = src + rb * M + e0;
+                if ((reinterpret_cast<uintptr_t>(g) & 15u) == 0) { cp_async16(d, g, 16u); continue; }
+#pragma unroll
+                for (int r = 0; r < W; ++r) d[r] = g[r];
+            } else {
+#pragma unroll
+                for (int r = 0; r < W; ++r) d[r] = (lo < DG_S && e0 + r >= lo * M) ? src[rb * M + e0 + r] : T(0);
+            }
+        }
+    };
+    auto stage = [&](int step, int b) {
+        stage_one(gv, step, sg + b * DG_NT * RS);
+        stage_one(vo, step, sv + b * DG_NT * RS);
+        cp_async_commit();
+    };
+    Par<T, M> P;
+    cx<T> h[M];
+    int64_t n0 = 0, n1 = 0;
+    if (valid) {
+        const int64_t sq = c / p.nch;
+        const int kk = (int)(c - sq * p.nch);
+        n0 = max((int64_t)0, p.T - (int64_t)(kk + 1) * DG_C);
+        n1 = p.T - (int64_t)kk * DG_C;
+        P.load(p.tab + (p.ncoef > 1 ? sq : 0) * p.tab_stride);
+#pragma unroll
+        for (int i = 0; i < M; ++i) h[i] = {(T)p.carry[c * 2 * M + 2 * i], (T)p.carry[c * 2 * M + 2 * i + 1]};
+    }
     double gA[M][M];
 #pragma unroll
     for (int i = 0; i < M; ++i)
 #pragma unroll
         for (int j = 0; j < M; ++j) gA[i][j] = 0.0;
-    T g[M];
-    for (int64_t n = n1 - 1; n >= n0; --n) {
-        T gg[M];
-        if (gv != nullptr) ld_vec<T, M>(gv + seq * p.T * M, n, gg);
-        else
+    T g[M], gpend[M];
+    bool pending = false;
+    constexpr int NSTEP = DG_C / DG_S;
+    stage(0, 0);
+    for (int step = 0; step < NSTEP; ++step) {
+        const int b = step & 1;
+        if (step + 1 < NSTEP) { stage(step + 1, b ^ 1); cp_async_wait<1>(); }
+        else cp_async_wait<0>();
+        __syncthreads();                                   // this step's rows landed; so free
+        const int64_t bb = n1 - (int64_t)step * DG_S, aa = bb - DG_S;
+        const T* gr = sg + b * DG_NT * RS + threadIdx.x * RS;
+        const T* vr = sv + b * DG_NT * RS + threadIdx.x * RS;
+        T* orow = so + threadIdx.x * RS;
+        if (valid && bb > n0) {
+            if (pending) {                                 // v(aa_prev) = forward row aa_prev - 1 = this step's last row
 #pragma unroll
-            for (int j = 0; j < M; ++j) gg[j] = T(0);
-        dg_step<T, M, true>(P, h, gg);
-        dg_out<T, M, true>(P, h, g);
+                for (int i = 0; i < M; ++i)
+#pragma unroll
+                    for (int j = 0; j < M; ++j) gA[i][j] = fma((double)gpend[i], (double)vr[(DG_S - 1) * M + j], gA[i][j]);
+                pending = false;
+            }
+#pragma unroll
+            for (int u = DG_S - 1; u >= 0; --u) {
+                const int64_t n = aa + u;
+                if (n >= n0) {
+                    T gg[M];
+#pragma unroll
+                    for (int j = 0; j < M; ++j) gg[j] = gr[u * M + j];
+                    dg_step<T, M, true>(P, h, gg);
+                    dg_out<T, M, true>(P, h, g);
+#pragma unroll
+                    for (int j = 0; j < M; ++j) orow[u * M + j] = g[j];
+                    if (u > 0 && n - 1 >= n0) {            // v(n) = forward row n - 1, staged
+#pragma unroll
+                        for (int i = 0; i < M; ++i)
+#pragma unroll
+                            for (int j = 0; j < M; ++j) gA[i][j] = fma((double)g[i], (double)vr[(u - 1) * M + j], gA[i][j]);
+                    } else {
+                        pending = true;
+#pragma unroll
+                        for (int j = 0; j < M; ++j) gpend[j] = g[j];
+                    }
+                }
+            }
+        }
+        __syncthreads();                                   // so complete
         if (gz != nullptr)
+            for (int q = threadIdx.x; q < DG_NT * PPC; q += DG_NT) {   // cooperative store of the gz rows
+                const int lc = q / PPC, part = q - (q / PPC) * PPC;
+                const int64_t cc = cbase + lc;
+                if (cc >= ntot) continue;
+                int64_t rb;
+                int lo;
+                span(cc, step, rb, lo);
+                if (lo >= DG_S) continue;
+                const int e0 = part * W;
+                T* dst = gz + rb * M + e0;
+                const T* s2 = so + lc * RS + e0;
+                if (lo * M <= e0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+                    using V = typename Vec<T>::type;
+                    *reinterpret_cast<V*>(dst) = *reinterpret_cast<const V*>(s2);
+                } else {
 #pragma unroll
-            for (int j = 0; j < M; ++j) gz[(seq * p.T + n) * M + j] = g[j];
-        T vp[M];                                           // v(n): v0 at n = 0, else the forward's v(n)
+                    for (int r = 0; r < W; ++r)
+                        if (e0 + r >= lo * M) dst[r] = s2[r];
+                }
+            }
+    }
+    if (!valid) return;
+    if (pending) {                                         // the chunk's first sample n0: v(n0)
+        T vp[M];
+        const int64_t sq = c / p.nch;
 #pragma unroll
-        for (int j = 0; j < M; ++j) vp[j] = n > 0 ? vo[(n - 1) * M + j] : (v0 != nullptr ? v0[seq * M + j] : T(0));
+        for (int j = 0; j < M; ++j)
+            vp[j] = n0 > 0 ? vo[(sq * p.T + n0 - 1) * M + j] : (v0 != nullptr ? v0[sq * M + j] : T(0));
 #pragma unroll
         for (int i = 0; i < M; ++i)
 #pragma unroll
-            for (int j = 0; j < M; ++j) gA[i][j] = fma((double)g[i], (double)vp[j], gA[i][j]);
+            for (int j = 0; j < M; ++j) gA[i][j] = fma((double)gpend[i], (double)vp[j], gA[i][j]);
     }
     if (n0 == 0 && p.gv0 != nullptr) {                     // g now holds g(0)
-        T* o = static_cast<T*>(p.gv0) + seq * M;
+        T* o = static_cast<T*>(p.gv0) + (c / p.nch) * M;
 #pragma unroll
         for (int i = 0; i < M; ++i) {
             T s = T(0);
@@ -661,6 +773,8 @@ __global__ void __launch_bounds__(DG_NT) dg_bwd_emit_kernel(const Args p) {
 #pragma unroll
         for (int j = 0; j < M; ++j) p.gpart[c * M * M + i * M + j] = gA[i][j];
 }
+template <typename T, int M>
+constexpr size_t dg_bwd_smem() { return (size_t)5 * DG_NT * (dg_s<T, M>() * M + 16 / sizeof(T)) * sizeof(T); }
 
 // grad_A: fixed-order sum of the chunk partials (SHARED: every chunk; PER_SEQ: per sequence)
 template <typename T, int M>
@@ -712,7 +826,12 @@ static iir_status_t run(bool fwd, const iir_desc_t* d, Args& a, void* gA, cudaSt
     if (s != IIR_OK) return s;
     s = launch(K_DIAG_SCAN, st, [&] { dg_scan_kernel<T, M, true><<<(unsigned)a.B, 32, 0, st>>>(a); });
     if (s != IIR_OK) return s;
-    s = launch(K_DIAG_BWD, st, [&] { dg_bwd_emit_kernel<T, M><<<grid, DG_NT, 0, st>>>(a); });
+    static PerDevice attrs;
+    attrs.once([] {
+        cudaFuncSetAttribute(dg_bwd_emit_kernel<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dg_bwd_smem<T, M>());
+    });
+    s = launch(K_DIAG_BWD, st, [&] { dg_bwd_emit_kernel<T, M><<<grid, DG_NT, dg_bwd_smem<T, M>(), st>>>(a); });
     if (s != IIR_OK || gA == nullptr) return s;
     return launch(K_DIAG_RED, st, [&] {
         dg_reduce_kernel<T, M><<<dim3((unsigned)a.ncoef, M * M), 256, 0, st>>>(a, static_cast<T*>(gA));
