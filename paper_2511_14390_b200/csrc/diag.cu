@@ -383,33 +383,14 @@ __device__ __forceinline__ void ld_vec(const T* p, int64_t idx, T (&v)[M]) {
     for (int j = 0; j < M; ++j) v[j] = p[idx * M + j];
 }
 
-// phase 1: chunk aggregates from the zero state (forward in time / backward in reverse time)
+// phase 1: chunk aggregates from the zero state (forward in time / backward in reverse time).
+// Forward chunks start at 0 (the ragged chunk is the last); backward chunks, scanned last to
+// first, end at T (the ragged chunk is the first in time): every scanned chunk but the final
+// one spans exactly DG_C samples, the span of the scan's transition X^C.  The CTA's chunks
+// advance together DG_S samples per step with their input rows staged through shared memory
+// (cooperative 16 B copies, cp.async double buffer), as in the emit kernels below.
 template <typename T, int M, bool BWD>
-__global__ void __launch_bounds__(DG_NT) dg_agg_kernel(const Args p) {
-    const int64_t c = (int64_t)blockIdx.x * DG_NT + threadIdx.x;
-    if (c >= p.B * p.nch) return;
-    const int64_t seq = c / p.nch;
-    const int k = (int)(c - seq * p.nch);
-    Par<T, M> P;
-    P.load(p.tab + (p.ncoef > 1 ? seq : 0) * p.tab_stride);
-    // forward chunks start at 0 (the ragged chunk is the last); backward chunks, scanned last to
-    // first, end at T (the ragged chunk is the first in time): every scanned chunk but the final
-    // one spans exactly DG_C samples, the span of the scan's transition X^C
-    const int64_t n0 = BWD ? max((int64_t)0, p.T - (int64_t)(k + 1) * DG_C) : (int64_t)k * DG_C;
-    const int64_t n1 = BWD ? p.T - (int64_t)k * DG_C : min(n0 + DG_C, p.T);
-    const T* in = static_cast<const T*>(BWD ? p.gv : p.z) + seq * p.T * M;
-    cx<T> w[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i) w[i] = {T(0), T(0)};
-    if (!BWD) {
-        for (int64_t n = n0; n < n1; ++n) { T zz[M]; ld_vec<T, M>(in, n, zz); dg_step<T, M, false>(P, w, zz); }
-    } else if (in != nullptr) {
-        for (int64_t n = n1 - 1; n >= n0; --n) { T gg[M]; ld_vec<T, M>(in, n, gg); dg_step<T, M, true>(P, w, gg); }
-    }
-    double* o = p.agg + c * 2 * M;
-#pragma unroll
-    for (int i = 0; i < M; ++i) { o[2 * i] = (double)w[i].r; o[2 * i + 1] = (double)w[i].i; }
-}
+__global__ void __launch_bounds__(DG_NT) dg_agg_kernel(const Args p);
 
 // phase 2: one warp per sequence scans the chunk aggregates in fp64 (blocks of 32 chunks:
 // Kogge-Stone with X^(C 2^d), the block's carry-in folded into its first chunk) and writes
@@ -503,6 +484,86 @@ template <typename T, int M> constexpr bool dg_s_fits(int S) {
            3 * DG_NT * (S * M + 16 / (int)sizeof(T)) * (int)sizeof(T) <= 48 * 1024;
 }
 template <typename T, int M> constexpr int dg_s() { return dg_s_fits<T, M>(8) ? 8 : dg_s_fits<T, M>(4) ? 4 : 2; }
+template <typename T, int M, bool BWD>
+__global__ void __launch_bounds__(DG_NT) dg_agg_kernel(const Args p) {
+    constexpr int DG_S = dg_s<T, M>();
+    constexpr int ROW = DG_S * M, W = 16 / (int)sizeof(T), RS = ROW + W, PPC = ROW / W;
+    __shared__ __align__(16) T zs[2][DG_NT * RS];
+    const int64_t ntot = p.B * p.nch, cbase = (int64_t)blockIdx.x * DG_NT;
+    const int64_t c = cbase + threadIdx.x;
+    const bool valid = c < ntot;
+    const T* in = static_cast<const T*>(BWD ? p.gv : p.z);
+    // the chunk's sample range [n0, n1) and the first sample of step `step`'s rows
+    auto range = [&](int64_t cc, int64_t& n0, int64_t& n1) {
+        const int64_t sq = cc / p.nch;
+        const int kk = (int)(cc - sq * p.nch);
+        n0 = BWD ? max((int64_t)0, p.T - (int64_t)(kk + 1) * DG_C) : (int64_t)kk * DG_C;
+        n1 = BWD ? p.T - (int64_t)kk * DG_C : min(n0 + DG_C, p.T);
+        return sq;
+    };
+    auto stage = [&](int step, T* dst) {
+        for (int q = threadIdx.x; q < DG_NT * PPC; q += DG_NT) {
+            const int lc = q / PPC, part = q - (q / PPC) * PPC;
+            const int64_t cc = cbase + lc;
+            T* d = dst + lc * RS + part * W;
+            int64_t n0 = 0, n1 = 0, sq = 0;
+            if (cc < ntot && in != nullptr) sq = range(cc, n0, n1);
+            const int64_t a = BWD ? n1 - (int64_t)(step + 1) * DG_S : n0 + (int64_t)step * DG_S;   // buffer row 0
+            const int e0 = part * W;
+            // valid samples of the piece: n in [max(a, n0), min(a + S, n1))
+            const int64_t lo = max(a, n0), hi = min(a + DG_S, n1);
+            const int64_t elo = (lo - a) * M, ehi = (hi - a) * M;           // valid elements [elo, ehi)
+            const T* g = in + (sq * p.T + a) * M + e0;
+            if (cc < ntot && in != nullptr && e0 >= elo && e0 + W <= ehi &&
+                (reinterpret_cast<uintptr_t>(g) & 15u) == 0) {
+                cp_async16(d, g, 16u);
+            } else {
+#pragma unroll
+                for (int r = 0; r < W; ++r)
+                    d[r] = (cc < ntot && in != nullptr && e0 + r >= elo && e0 + r < ehi) ? g[r] : T(0);
+            }
+        }
+        cp_async_commit();
+    };
+    Par<T, M> P;
+    int64_t n0 = 0, n1 = 0;
+    if (valid) {
+        const int64_t sq = range(c, n0, n1);
+        P.load(p.tab + (p.ncoef > 1 ? sq : 0) * p.tab_stride);
+    }
+    cx<T> w[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) w[i] = {T(0), T(0)};
+    constexpr int NSTEP = DG_C / DG_S;
+    stage(0, zs[0]);
+    for (int step = 0; step < NSTEP; ++step) {
+        const int b = step & 1;
+        if (step + 1 < NSTEP) { stage(step + 1, zs[b ^ 1]); cp_async_wait<1>(); }
+        else cp_async_wait<0>();
+        __syncthreads();
+        if (valid && in != nullptr) {
+            const int64_t a = BWD ? n1 - (int64_t)(step + 1) * DG_S : n0 + (int64_t)step * DG_S;
+            const T* zr = zs[b] + threadIdx.x * RS;
+#pragma unroll
+            for (int uu = 0; uu < DG_S; ++uu) {
+                const int u = BWD ? DG_S - 1 - uu : uu;
+                const int64_t n = a + u;
+                if (n >= n0 && n < n1) {
+                    T zz[M];
+#pragma unroll
+                    for (int j = 0; j < M; ++j) zz[j] = zr[u * M + j];
+                    dg_step<T, M, BWD>(P, w, zz);
+                }
+            }
+        }
+        __syncthreads();                                   // zs[b] free for step + 2
+    }
+    if (!valid) return;
+    double* o = p.agg + c * 2 * M;
+#pragma unroll
+    for (int i = 0; i < M; ++i) { o[2 * i] = (double)w[i].r; o[2 * i + 1] = (double)w[i].i; }
+}
+
 template <typename T, int M>
 __device__ __forceinline__ int64_t dg_row0(const Args& p, int64_t cc, int step) {   // first element of a step
     const int64_t sq = cc / p.nch;
