@@ -36,10 +36,11 @@ template <typename T> __device__ __forceinline__ cx<T> cmad(cx<T> a, cx<T> b, cx
 
 // Per coefficient set (fp64, in the tape): flag (1 = diagonal basis, 0 = dense fallback),
 // lam[M], V[M][M], Vi[M][M] (complex), A[M][M] (real), and the transition powers used by the
-// carry scan: Pw[d] = X^(DG_C 2^d), d = 0..5, complex M x M (X = diag(lam) or A).
+// carry scan: Pw[d] = X^(DG_C 2^d), d = 0..6, complex M x M (X = diag(lam) or A).
 template <int M> struct Tb {
     static constexpr int FLAG = 0, LAM = 2, V = LAM + 2 * M, VI = V + 2 * M * M, A = VI + 2 * M * M;
-    static constexpr int PW = A + M * M, SIZE = (PW + 6 * 2 * M * M + 31) / 32 * 32;
+    static constexpr int NPW = 7;
+    static constexpr int PW = A + M * M, SIZE = (PW + NPW * 2 * M * M + 31) / 32 * 32;
 };
 
 // ---- prologue: closed-form eigen-decomposition, conditioning test, powers ------------------
@@ -296,7 +297,7 @@ __global__ void dg_prep_kernel(const T* __restrict__ a, int64_t stride, int64_t 
             X[2 * (i * M + j) + 1] = ok ? (i == j ? li[i] : 0.0) : 0.0;
         }
     for (int q = 1; q < DG_C; q *= 2) cmatmul<M>(X, X, X);           // X^C
-    for (int d = 0; d < 6; ++d) {
+    for (int d = 0; d < TB::NPW; ++d) {
         for (int e = 0; e < 2 * M * M; ++e) t[TB::PW + d * 2 * M * M + e] = X[e];
         cmatmul<M>(X, X, X);
     }
@@ -429,45 +430,79 @@ __global__ void __launch_bounds__(32) dg_scan_kernel(const Args p) {
                 X[2 * i + 1] += q1 * (double)v0[j];
             }
     }
-    // the transition powers X^(C 2^d), d = 0..4, staged once in shared memory (read by broadcast
-    // in every block of the serial scan), and the next block's aggregates loaded one block
-    // ahead: the loop's only serial dependency is the carry X
-    constexpr int NPW = 5 * 2 * M * M;
+    // Each lane owns DG_K consecutive chunks of a block of 32 DG_K: it folds them serially with
+    // X^C, the lanes' inclusive states are scanned with X^(DG_K C 2^d) (levels log2 DG_K + d of
+    // the table), and each lane then walks its chunks' entering states forward.  The powers are
+    // staged once in shared memory (read by broadcast) and the next block's aggregates are
+    // loaded one block ahead: the loop's only serial dependency is the carry X.
+    constexpr int DG_K = 4, LK = 2;                      // chunks per lane, log2
+    static_assert(LK + 4 < TB::NPW, "scan levels in the table");
+    constexpr int NPW = TB::NPW * 2 * M * M;
     __shared__ double spw[NPW];
     for (int e = lane; e < NPW; e += 32) spw[e] = t[TB::PW + e];
     __syncwarp();
-    double Sn[2 * M];
+    auto lvl = [&](int d) -> const double* { return spw + d * 2 * M * M; };
+    double An[DG_K][2 * M];
+    auto load = [&](int b0, double (&dst)[DG_K][2 * M]) {
 #pragma unroll
-    for (int i = 0; i < 2 * M; ++i) Sn[i] = lane < p.nch ? p.agg[(seq * p.nch + lane) * 2 * M + i] : 0.0;
-    for (int b0 = 0; b0 < p.nch; b0 += 32) {
-        const int c = b0 + lane;                                     // scan position
-        const int k = c;                                             // (backward chunk indices run from the end)
-        double S[2 * M];
+        for (int j = 0; j < DG_K; ++j) {
+            const int cc = b0 + lane * DG_K + j;
 #pragma unroll
-        for (int i = 0; i < 2 * M; ++i) S[i] = Sn[i];
-        const int cn = c + 32;
+            for (int i = 0; i < 2 * M; ++i) dst[j][i] = cc < p.nch ? p.agg[(seq * p.nch + cc) * 2 * M + i] : 0.0;
+        }
+    };
+    load(0, An);
+    for (int b0 = 0; b0 < p.nch; b0 += 32 * DG_K) {
+        double Ag[DG_K][2 * M];
 #pragma unroll
-        for (int i = 0; i < 2 * M; ++i) Sn[i] = cn < p.nch ? p.agg[(seq * p.nch + cn) * 2 * M + i] : 0.0;
-        if (lane == 0) cmv<M, BWD>(spw, X, S);                     // fold the block's carry-in
+        for (int j = 0; j < DG_K; ++j)
+#pragma unroll
+            for (int i = 0; i < 2 * M; ++i) Ag[j][i] = An[j][i];
+        load(b0 + 32 * DG_K, An);
+        double S[2 * M];                                   // the lane's inclusive aggregate (zero carry-in)
+#pragma unroll
+        for (int i = 0; i < 2 * M; ++i) S[i] = Ag[0][i];
+#pragma unroll
+        for (int j = 1; j < DG_K; ++j) {
+            double acc[2 * M];
+#pragma unroll
+            for (int i = 0; i < 2 * M; ++i) acc[i] = Ag[j][i];
+            cmv<M, BWD>(lvl(0), S, acc);
+#pragma unroll
+            for (int i = 0; i < 2 * M; ++i) S[i] = acc[i];
+        }
+        if (lane == 0) cmv<M, BWD>(lvl(LK), X, S);         // fold the block's carry-in
 #pragma unroll
         for (int d = 0; d < 5; ++d) {
             double O[2 * M], acc[2 * M];
 #pragma unroll
             for (int i = 0; i < 2 * M; ++i) { O[i] = __shfl_up_sync(0xffffffffu, S[i], 1 << d); acc[i] = 0.0; }
-            cmv<M, BWD>(spw + d * 2 * M * M, O, acc);
+            cmv<M, BWD>(lvl(LK + d), O, acc);
             if (lane >= (1 << d))
 #pragma unroll
                 for (int i = 0; i < 2 * M; ++i) S[i] += acc[i];
         }
-        double E[2 * M];
+        double E[2 * M];                                   // state entering the lane's first chunk
 #pragma unroll
         for (int i = 0; i < 2 * M; ++i) {
             const double e = __shfl_up_sync(0xffffffffu, S[i], 1);
             E[i] = lane == 0 ? X[i] : e;
         }
-        if (c < p.nch)
 #pragma unroll
-            for (int i = 0; i < 2 * M; ++i) p.carry[(seq * p.nch + k) * 2 * M + i] = E[i];
+        for (int j = 0; j < DG_K; ++j) {
+            const int cc = b0 + lane * DG_K + j;
+            if (cc < p.nch)
+#pragma unroll
+                for (int i = 0; i < 2 * M; ++i) p.carry[(seq * p.nch + cc) * 2 * M + i] = E[i];
+            if (j + 1 < DG_K) {
+                double acc[2 * M];
+#pragma unroll
+                for (int i = 0; i < 2 * M; ++i) acc[i] = Ag[j][i];
+                cmv<M, BWD>(lvl(0), E, acc);
+#pragma unroll
+                for (int i = 0; i < 2 * M; ++i) E[i] = acc[i];
+            }
+        }
 #pragma unroll
         for (int i = 0; i < 2 * M; ++i) X[i] = __shfl_sync(0xffffffffu, S[i], 31);
     }
